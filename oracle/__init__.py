@@ -1,0 +1,140 @@
+"""Python access to the fp64 CPU oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / ``--impl reference`` legs.  The product package
+(paper_2403_01596_b200) never imports this module.
+
+Every function here marshals numpy arrays into the C oracle; the arithmetic
+lives in oracle.c, which cites the paper passage each step follows.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["-O3", "-march=native", "-fopenmp", "-fPIC", "-shared", "-std=c11"]  # no -ffast-math
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c into oracle/liboracle.so (gcc, OpenMP, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.run(["gcc", *CFLAGS, _SRC, "-o", tmp, "-lm"], check=True)
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        i64, i32, f64 = C.c_int64, C.c_int, C.c_double
+        P = C.c_void_p
+        _lib.oracle_direct.argtypes = [i64, P, P, i64, P, i32, f64, i64, P, P, i32, P]
+        _lib.oracle_direct.restype = i32
+        _lib.oracle_bruteforce.argtypes = [i64, P, P, i64, P, i32, f64, P, P]
+        _lib.oracle_bruteforce.restype = i32
+        _lib.oracle_pair_potential.argtypes = [f64] * 6
+        _lib.oracle_pair_potential.restype = f64
+        _lib.oracle_morton.argtypes = [C.c_uint64, C.c_uint64, i32]
+        _lib.oracle_morton.restype = C.c_uint64
+        _lib.oracle_morton_decode.argtypes = [C.c_uint64, i32, P, P]
+        _lib.oracle_sort_points.argtypes = [i64, P, i32, P, P]
+        _lib.oracle_sort_points.restype = i32
+        _lib.oracle_neighbors.argtypes = [i32, P]
+        _lib.oracle_ct_level.argtypes = [i64, P, i64, P, i32, i32, i32]
+        _lib.oracle_ct_level.restype = i32
+        _lib.oracle_pair_count.argtypes = [i64, P, i64, P, i32]
+        _lib.oracle_pair_count.restype = i64
+        _lib.oracle_num_threads.restype = i32
+    return _lib
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def direct(src_xy, q, tgt_xy, level: int, eps: float = 1e-12, targets=None,
+           nthreads: int = 0) -> tuple[np.ndarray, int]:
+    """phi for all targets (or the index subset ``targets``) and the pair count."""
+    src_xy, q, tgt_xy = _f64(src_xy), _f64(q), _f64(tgt_xy)
+    sel = None if targets is None else np.ascontiguousarray(targets, dtype=np.int64)
+    n_out = len(tgt_xy) if sel is None else len(sel)
+    phi = np.empty(n_out, dtype=np.float64)
+    pairs = C.c_int64(0)
+    rc = lib().oracle_direct(len(src_xy), _ptr(src_xy), _ptr(q), len(tgt_xy), _ptr(tgt_xy),
+                             level, eps, 0 if sel is None else len(sel),
+                             None if sel is None else _ptr(sel), _ptr(phi), nthreads,
+                             C.byref(pairs))
+    if rc:
+        raise MemoryError("oracle_direct allocation failed")
+    return phi, pairs.value
+
+
+def bruteforce(src_xy, q, tgt_xy, level: int, eps: float = 1e-12) -> tuple[np.ndarray, int]:
+    src_xy, q, tgt_xy = _f64(src_xy), _f64(q), _f64(tgt_xy)
+    phi = np.empty(len(tgt_xy), dtype=np.float64)
+    pairs = C.c_int64(0)
+    lib().oracle_bruteforce(len(src_xy), _ptr(src_xy), _ptr(q), len(tgt_xy), _ptr(tgt_xy),
+                            level, eps, _ptr(phi), C.byref(pairs))
+    return phi, pairs.value
+
+
+def pair_potential(t, s, q: float, eps: float = 1e-12) -> float:
+    return lib().oracle_pair_potential(float(t[0]), float(t[1]), float(s[0]), float(s[1]),
+                                       float(q), eps)
+
+
+def morton(ix: int, iy: int, level: int) -> int:
+    return int(lib().oracle_morton(ix, iy, level))
+
+
+def morton_decode(code: int, level: int) -> tuple[int, int]:
+    x, y = C.c_uint64(0), C.c_uint64(0)
+    lib().oracle_morton_decode(code, level, C.byref(x), C.byref(y))
+    return x.value, y.value
+
+
+def sort_points(xy, level: int) -> tuple[np.ndarray, np.ndarray]:
+    """(perm[plan] = original index, box offsets[4^(L-1)+1]) in Morton order."""
+    xy = _f64(xy)
+    perm = np.empty(len(xy), dtype=np.int64)
+    off = np.empty((1 << (2 * (level - 1))) + 1, dtype=np.int64)
+    if lib().oracle_sort_points(len(xy), _ptr(xy), level, _ptr(perm), _ptr(off)):
+        raise MemoryError
+    return perm, off
+
+
+def neighbors(level: int) -> np.ndarray:
+    nb = np.empty((1 << (2 * (level - 1))) * 9, dtype=np.int64)
+    lib().oracle_neighbors(level, _ptr(nb))
+    return nb.reshape(-1, 9)
+
+
+def ct_level(src_xy, tgt_xy, ct: int = 15, l_start: int = 3, l_max: int = 16) -> int:
+    src_xy, tgt_xy = _f64(src_xy), _f64(tgt_xy)
+    return int(lib().oracle_ct_level(len(src_xy), _ptr(src_xy), len(tgt_xy), _ptr(tgt_xy),
+                                     ct, l_start, l_max))
+
+
+def pair_count(src_xy, tgt_xy, level: int) -> int:
+    src_xy, tgt_xy = _f64(src_xy), _f64(tgt_xy)
+    return int(lib().oracle_pair_count(len(src_xy), _ptr(src_xy), len(tgt_xy), _ptr(tgt_xy), level))
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())

@@ -1,0 +1,297 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct fp64 CPU oracle for the MLFMA
+ * near-field P2P operator of arXiv 2403.01596.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_2403_01596_b200/) never links, imports or calls it,
+ * and shares no code, header, table or helper with it.
+ *
+ * What it computes (§4.1, the CPU
+ * baseline: "for each target point in a box ... for each source point in the
+ * E_1 neighborhood, the potential function is executed once and its value is
+ * added"):
+ *
+ *   phi_t = sum_{s : |ix_s-ix_t|<=1 and |iy_s-iy_t|<=1 and r_ts >= eps}  q_s * ln(1/r_ts)
+ *
+ * with the leaf grid S = 2^(L-1) per side ("4^{L-1}" boxes,
+ * root = level 1), box(p) = (min(floor(x*S), S-1), min(floor(y*S), S-1))
+ * (half-open cells closed at the upper edge), the kernel
+ * G = q ln(1/r), 0 when r < eps ("electrical
+ * potential function on a two-dimensional PEC"), E1 = the 3x3 block of boxes
+ * clipped at the domain edge ("The number 9 above refers to the
+ * number of adjacent neighboring boxes").  ln(1/r) is evaluated as
+ * -0.5*log(r^2) with the C library log (<= 1 ulp).
+ *
+ * Pins: see tests/test_oracle_pins.py (closed-form lattice, SPEC worked
+ * values, brute force, reciprocity, linearity, permutation, pair-count closed
+ * form, SPEC geometry examples).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ---- geometry: PAPER.md §3.1 L67 ("division factor of 4"), SPEC.md L120 ---- */
+
+static int64_t grid_side(int L) { return (int64_t)1 << (L - 1); }
+
+static int64_t cell_of(double x, int64_t S)
+{
+    /* floor(x*S) is exact in fp64 because S is a power of two. */
+    int64_t c = (int64_t)floor(x * (double)S);
+    if (c > S - 1) c = S - 1; /* closed at x = 1 */
+    if (c < 0) c = 0;
+    return c;
+}
+
+/* Sources bucketed into an S x S array of lists, each list in original index
+ * order ("per-box insertion order").  Plain counting: count,
+ * prefix, fill.  Caller frees *start and *items. */
+static int bucket_sources(int64_t ns, const double *src_xy, int64_t S,
+                          int64_t **start_out, int64_t **items_out)
+{
+    int64_t cells = S * S;
+    int64_t *start = (int64_t *)calloc((size_t)(cells + 1), sizeof(int64_t));
+    int64_t *items = (int64_t *)malloc((size_t)(ns > 0 ? ns : 1) * sizeof(int64_t));
+    int64_t *fill = (int64_t *)malloc((size_t)(cells > 0 ? cells : 1) * sizeof(int64_t));
+    if (!start || !items || !fill) { free(start); free(items); free(fill); return -1; }
+    for (int64_t s = 0; s < ns; ++s) {
+        int64_t c = cell_of(src_xy[2 * s + 1], S) * S + cell_of(src_xy[2 * s], S);
+        start[c + 1] += 1;
+    }
+    for (int64_t c = 0; c < cells; ++c) start[c + 1] += start[c];
+    memcpy(fill, start, (size_t)cells * sizeof(int64_t));
+    for (int64_t s = 0; s < ns; ++s) {
+        int64_t c = cell_of(src_xy[2 * s + 1], S) * S + cell_of(src_xy[2 * s], S);
+        items[fill[c]++] = s;
+    }
+    free(fill);
+    *start_out = start;
+    *items_out = items;
+    return 0;
+}
+
+/* ---- C-2 step 3: the direct sum over the 3x3 neighbourhood ----------------
+ * For each selected target (all if sel == NULL): loop over the 3x3 block of
+ * cells around its cell (rows dy = -1..1, then columns dx = -1..1), over the
+ * sources of each cell in original index order; skip r^2 < eps^2; otherwise
+ * acc += q*log(r^2).  phi = -0.5*acc.  pairs_out (optional) receives the
+ * number of (t, s) pairs visited, guarded pairs included.
+ * Returns 0, or -1 on allocation failure. */
+int oracle_direct(int64_t ns, const double *src_xy, const double *q,
+                  int64_t nt, const double *tgt_xy, int L, double eps,
+                  int64_t nsel, const int64_t *sel, double *phi_out,
+                  int nthreads, int64_t *pairs_out)
+{
+    int64_t S = grid_side(L);
+    int64_t *start = NULL, *items = NULL;
+    if (bucket_sources(ns, src_xy, S, &start, &items)) return -1;
+    int64_t count = sel ? nsel : nt;
+    double eps2 = eps * eps;
+    int64_t pairs = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : pairs)
+    for (int64_t k = 0; k < count; ++k) {
+        int64_t t = sel ? sel[k] : k;
+        double xt = tgt_xy[2 * t], yt = tgt_xy[2 * t + 1];
+        int64_t ix = cell_of(xt, S), iy = cell_of(yt, S);
+        double acc = 0.0;
+        for (int64_t dy = -1; dy <= 1; ++dy) {
+            int64_t cy = iy + dy;
+            if (cy < 0 || cy >= S) continue;
+            for (int64_t dx = -1; dx <= 1; ++dx) {
+                int64_t cx = ix + dx;
+                if (cx < 0 || cx >= S) continue;
+                int64_t c = cy * S + cx;
+                for (int64_t j = start[c]; j < start[c + 1]; ++j) {
+                    int64_t s = items[j];
+                    double ddx = xt - src_xy[2 * s], ddy = yt - src_xy[2 * s + 1];
+                    double r2 = ddx * ddx + ddy * ddy;
+                    pairs += 1;
+                    if (r2 < eps2) continue; /* 0 when r < epsilon */
+                    acc += q[s] * log(r2);
+                }
+            }
+        }
+        phi_out[k] = -0.5 * acc;
+    }
+    free(start);
+    free(items);
+    if (pairs_out) *pairs_out = pairs;
+    return 0;
+}
+
+/* ---- C-2 step 4: brute force, no buckets -----------------------------------
+ * Every (t, s) pair, filtered by the 3x3 box-adjacency predicate. */
+int oracle_bruteforce(int64_t ns, const double *src_xy, const double *q,
+                      int64_t nt, const double *tgt_xy, int L, double eps,
+                      double *phi_out, int64_t *pairs_out)
+{
+    int64_t S = grid_side(L);
+    double eps2 = eps * eps;
+    int64_t pairs = 0;
+    for (int64_t t = 0; t < nt; ++t) {
+        int64_t ixt = cell_of(tgt_xy[2 * t], S), iyt = cell_of(tgt_xy[2 * t + 1], S);
+        double acc = 0.0;
+        for (int64_t s = 0; s < ns; ++s) {
+            int64_t ixs = cell_of(src_xy[2 * s], S), iys = cell_of(src_xy[2 * s + 1], S);
+            if (llabs(ixs - ixt) > 1 || llabs(iys - iyt) > 1) continue;
+            pairs += 1;
+            double ddx = tgt_xy[2 * t] - src_xy[2 * s];
+            double ddy = tgt_xy[2 * t + 1] - src_xy[2 * s + 1];
+            double r2 = ddx * ddx + ddy * ddy;
+            if (r2 < eps2) continue;
+            acc += q[s] * log(r2);
+        }
+        phi_out[t] = -0.5 * acc;
+    }
+    if (pairs_out) *pairs_out = pairs;
+    return 0;
+}
+
+/* ---- single pair: SPEC.md L150 pair_potential ------------------------------ */
+double oracle_pair_potential(double xt, double yt, double xs, double ys, double q, double eps)
+{
+    double ddx = xt - xs, ddy = yt - ys;
+    double r2 = ddx * ddx + ddy * ddy;
+    if (r2 < eps * eps) return 0.0;
+    return -0.5 * q * log(r2);
+}
+
+/* ---- C-2 step 5: plan-indexing oracle (bit-exact plan checks) --------------
+ * Morton code by a bit loop: bit b of ix goes to bit 2b, bit b of iy to bit
+ * 2b+1 ("x occupies even bit positions").  */
+uint64_t oracle_morton(uint64_t ix, uint64_t iy, int L)
+{
+    uint64_t code = 0;
+    for (int b = 0; b < L - 1; ++b) {
+        code |= ((ix >> b) & 1u) << (2 * b);
+        code |= ((iy >> b) & 1u) << (2 * b + 1);
+    }
+    return code;
+}
+
+void oracle_morton_decode(uint64_t code, int L, uint64_t *ix, uint64_t *iy)
+{
+    uint64_t x = 0, y = 0;
+    for (int b = 0; b < L - 1; ++b) {
+        x |= ((code >> (2 * b)) & 1u) << b;
+        y |= ((code >> (2 * b + 1)) & 1u) << b;
+    }
+    *ix = x;
+    *iy = y;
+}
+
+typedef struct { uint64_t code; int64_t idx; } keyed;
+
+static int cmp_keyed(const void *a, const void *b)
+{
+    const keyed *x = (const keyed *)a, *y = (const keyed *)b;
+    if (x->code != y->code) return x->code < y->code ? -1 : 1;
+    if (x->idx != y->idx) return x->idx < y->idx ? -1 : 1;
+    return 0;
+}
+
+/* Sort points by (Morton code, original index) -> perm[plan] = original index;
+ * off[B+1] = CSR box offsets over all B = 4^(L-1) boxes in Morton order. */
+int oracle_sort_points(int64_t n, const double *xy, int L, int64_t *perm, int64_t *off)
+{
+    int64_t S = grid_side(L), B = S * S;
+    keyed *k = (keyed *)malloc((size_t)(n > 0 ? n : 1) * sizeof(keyed));
+    if (!k) return -1;
+    for (int64_t i = 0; i < n; ++i) {
+        k[i].code = oracle_morton((uint64_t)cell_of(xy[2 * i], S), (uint64_t)cell_of(xy[2 * i + 1], S), L);
+        k[i].idx = i;
+    }
+    qsort(k, (size_t)n, sizeof(keyed), cmp_keyed);
+    for (int64_t b = 0; b <= B; ++b) off[b] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        perm[i] = k[i].idx;
+        off[k[i].code + 1] += 1;
+    }
+    for (int64_t b = 0; b < B; ++b) off[b + 1] += off[b];
+    free(k);
+    return 0;
+}
+
+/* E1 neighbour list of every box, ascending Morton, -1 padded to 9
+ * (SPEC.md L91-99 neighbors_e1). nb must hold 9*4^(L-1) entries. */
+void oracle_neighbors(int L, int64_t *nb)
+{
+    int64_t S = grid_side(L), B = S * S;
+    for (int64_t m = 0; m < B; ++m) {
+        uint64_t ix, iy;
+        oracle_morton_decode((uint64_t)m, L, &ix, &iy);
+        int64_t list[9];
+        int cnt = 0;
+        for (int64_t dy = -1; dy <= 1; ++dy)
+            for (int64_t dx = -1; dx <= 1; ++dx) {
+                int64_t cx = (int64_t)ix + dx, cy = (int64_t)iy + dy;
+                if (cx < 0 || cy < 0 || cx >= S || cy >= S) continue;
+                list[cnt++] = (int64_t)oracle_morton((uint64_t)cx, (uint64_t)cy, L);
+            }
+        for (int i = 1; i < cnt; ++i) /* insertion sort, ascending Morton */
+            for (int j = i; j > 0 && list[j - 1] > list[j]; --j) {
+                int64_t tmp = list[j]; list[j] = list[j - 1]; list[j - 1] = tmp;
+            }
+        for (int i = 0; i < 9; ++i) nb[9 * m + i] = i < cnt ? list[i] : -1;
+    }
+}
+
+/* ---- PAPER.md §3.1 L67-69 tree-construction loop ----------
+ * Start at l_start; while some leaf box holds more than ct sources or ct
+ * targets, L += 1.  Returns L, or -1 if l_max is exceeded. */
+int oracle_ct_level(int64_t ns, const double *src_xy, int64_t nt, const double *tgt_xy,
+                    int ct, int l_start, int l_max)
+{
+    for (int L = l_start; L <= l_max; ++L) {
+        int64_t S = grid_side(L), B = S * S;
+        int32_t *cs = (int32_t *)calloc((size_t)B, sizeof(int32_t));
+        int32_t *ctg = (int32_t *)calloc((size_t)B, sizeof(int32_t));
+        if (!cs || !ctg) { free(cs); free(ctg); return -2; }
+        int ok = 1;
+        for (int64_t i = 0; i < ns && ok; ++i)
+            if (++cs[cell_of(src_xy[2 * i + 1], S) * S + cell_of(src_xy[2 * i], S)] > ct) ok = 0;
+        for (int64_t i = 0; i < nt && ok; ++i)
+            if (++ctg[cell_of(tgt_xy[2 * i + 1], S) * S + cell_of(tgt_xy[2 * i], S)] > ct) ok = 0;
+        free(cs);
+        free(ctg);
+        if (ok) return L;
+    }
+    return -1;
+}
+
+/* Number of (t, s) pairs with box(s) in E1(box(t)) -- the pair-interaction
+ * count the metric divides by. */
+int64_t oracle_pair_count(int64_t ns, const double *src_xy, int64_t nt, const double *tgt_xy, int L)
+{
+    int64_t S = grid_side(L);
+    int64_t *start = NULL, *items = NULL;
+    if (bucket_sources(ns, src_xy, S, &start, &items)) return -1;
+    int64_t pairs = 0;
+    for (int64_t t = 0; t < nt; ++t) {
+        int64_t ix = cell_of(tgt_xy[2 * t], S), iy = cell_of(tgt_xy[2 * t + 1], S);
+        for (int64_t cy = iy - 1; cy <= iy + 1; ++cy)
+            for (int64_t cx = ix - 1; cx <= ix + 1; ++cx)
+                if (cx >= 0 && cy >= 0 && cx < S && cy < S)
+                    pairs += start[cy * S + cx + 1] - start[cy * S + cx];
+    }
+    free(start);
+    free(items);
+    return pairs;
+}
+
+int oracle_num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
