@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark of the MLFMA near-field P2P operator on B200 (BASELINE.json metric:
+P2P pair-interactions/s; roofline fraction).
+
+One *step* = one apply of the whole hot path (SURVEY.md §8(a) apply rows:
+[halo weight exchange] -> P2P kernel) over each config of the workload, with
+inputs resident in HBM.  Default workload = BASELINE.json configs[1], the
+density sweep: 1e6 points at 16, 32 and 64 points per box, non-redundant
+layout, fp32 (the headline), Morton plan order.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (strong scaling, NCCL halo exchange)
+
+Timing: W warm-up steps, then K steps timed with CUDA events on the apply
+stream, L2 flushed (256 MiB write) between steps, barrier + synchronize on
+both sides, max over ranks.  Clocks are sampled with NVML during the timed
+region.  The CPU baseline is the fp64 oracle (oracle/, test infrastructure)
+on a bounded sample of the same workload, rank 0 at N = 1 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2403_01596_b200 import workloads as W  # noqa: E402
+
+WORKLOADS = {
+    "density_1e6": ["d16_1e6", "d32_1e6", "d64_1e6"],           # configs[1] (headline)
+    "lowdensity_1e7": ["lowd025_1e7", "lowd1_1e7", "lowd2_1e7", "lowd4_1e7"],  # configs[2]
+    "surface_2e7": ["surf_2e7"],                                # configs[3]
+    "d32_7e7": ["d32_7e7"],                                     # configs[4]
+    "tiny": ["tiny"],                                           # configs[0]
+}
+METRIC = "P2P pair-interactions/s"
+MUFU_LG2_PER_CLK_PER_SM = 16       # SFU issue rate (checked by libp2p_peaks)
+SM_COUNT = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="density_1e6", choices=sorted(WORKLOADS))
+    ap.add_argument("--layout", default="nr", choices=["nr", "r"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--kind", default="iid", choices=["iid", "stratified"])
+    ap.add_argument("--no-extras", action="store_true", help="skip the R / fp64 detail lines")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras/baseline)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle)
+def cpu_baseline(cfg_names, kind, budget_s, seed_stream=0):
+    """The fp64 oracle as it stands, on a bounded sample of targets of each config."""
+    import oracle
+    nthreads = oracle.num_threads()
+    probs = [(W.CONFIGS[c], *W.make_problem(c, kind=kind)) for c in cfg_names]
+    # calibrate on 0.2% of the targets of the first config
+    c0, s0, t0, q0 = probs[0]
+    rng = np.random.default_rng(seed_stream)
+    cal = np.sort(rng.choice(len(t0), max(1, len(t0) // 500), replace=False))
+    tic = time.perf_counter()
+    _, pc = oracle.direct(s0, q0, t0, c0.level, targets=cal)
+    rate = pc / max(time.perf_counter() - tic, 1e-6)
+    pairs = 0
+    secs = 0.0
+    frac = 1.0
+    for cfg, s, t, q in probs:
+        per_cfg_pairs = budget_s / len(probs) * rate
+        full = cfg.density * 9 * len(t)
+        frac = min(1.0, per_cfg_pairs / full)
+        sel = np.sort(rng.choice(len(t), max(1, int(frac * len(t))), replace=False))
+        tic = time.perf_counter()
+        _, p = oracle.direct(s, q, t, cfg.level, targets=sel)
+        secs += time.perf_counter() - tic
+        pairs += p
+    return {"value": pairs / secs, "unit": "pair-interactions/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"{frac * 100:.2f}% of the targets of each of {','.join(cfg_names)} (seeded), "
+                      f"fp64 direct sum incl. bucketing, {pairs} pairs in {secs:.1f} s",
+            "pairs": pairs, "seconds": secs}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    names = WORKLOADS[args.workload]
+    per_step = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        cpu_baseline(names, args.kind, per_step / 4)
+    vals, pairs, secs = [], 0, 0.0
+    last = None
+    for k in range(args.steps):
+        last = cpu_baseline(names, args.kind, per_step, seed_stream=k + 1)
+        pairs += last["pairs"]
+        secs += last["seconds"]
+    v = pairs / secs
+    cfg = {"workload": args.workload, "configs": names, "layout": "oracle", "kind": args.kind}
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "pair-interactions/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64 plates, SURVEY.md §8(d))", "config": cfg,
+        "cpu_baseline": {"value": v, "unit": "pair-interactions/s", "cores": last["cores"], "kind": "oracle",
+                         "sample": last["sample"]},
+        "e2e": {"value": v, "unit": "pair-interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+# ---------------------------------------------------------------- GPU path
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2403_01596_b200 import p2p
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    names = WORKLOADS[args.workload]
+
+    # ---- plans (host build + upload; not timed)
+    jobs = []
+    for name in names:
+        cfg = W.CONFIGS[name]
+        src, tgt, q = W.make_problem(cfg, kind=args.kind)
+        pl = p2p.Plan(src, tgt, level=cfg.level, layout=args.layout, precision=args.precision, device=local,
+                      part_world=world, part_rank=rank)
+        info = pl.info
+        dt = pl.torch_dtype
+        job = {"name": name, "cfg": cfg, "plan": pl, "info": info, "q_user": q,
+               "out": torch.empty(max(1, info["n_tgt_local"]), dtype=dt, device=dev)}
+        if world == 1:
+            job["q"] = torch.as_tensor(q[pl.export("src_perm")], dtype=dt, device=dev)
+        else:
+            part = pl.export("partition").reshape(2, world + 1)
+            owned_user = _owned_user_indices(pl, src, part, rank)
+            job["q_owned"] = torch.as_tensor(q[owned_user], dtype=dt, device=dev)
+            hc = pl.export("halo_counts").reshape(2, world)
+            job["recv_splits"], job["send_splits"] = hc[0].tolist(), hc[1].tolist()
+            job["send"] = torch.empty(max(1, info["n_send"]), dtype=dt, device=dev)
+            job["halo"] = torch.empty(max(1, info["n_halo"]), dtype=dt, device=dev)
+        jobs.append(job)
+    pairs_step = sum(j["info"]["pairs_global"] for j in jobs)
+    pairs_local = sum(j["info"]["pairs"] for j in jobs)
+
+    def one_apply(j):
+        pl = j["plan"]
+        if world == 1:
+            p2p.p2p_apply(pl.handle, j["q"].data_ptr(), j["out"].data_ptr(), p2p.P2P_ORDER_PLAN, 0,
+                          stream.cuda_stream)
+        else:
+            if j["info"]["n_send"]:
+                pl.halo_pack(j["q_owned"], j["send"], stream.cuda_stream)
+            dist.all_to_all_single(j["halo"][: j["info"]["n_halo"]], j["send"][: j["info"]["n_send"]],
+                                   j["recv_splits"], j["send_splits"])
+            pl.apply_dist(j["q_owned"], j["halo"], j["out"], stream=stream.cuda_stream)
+
+    def step():
+        for j in jobs:
+            one_apply(j)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+
+    # ---- timed region: K steps, per-step events, L2 flush between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in jobs]
+           for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    barrier()
+    with sampler:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            for i, j in enumerate(jobs):
+                kev[k][i][0].record(stream)
+                one_apply(j)
+                kev[k][i][1].record(stream)
+            ev[k][1].record(stream)
+        barrier()
+    step_ms = np.array([a.elapsed_time(b) for a, b in ev])
+    kern_ms = np.array([[a.elapsed_time(b) for a, b in row] for row in kev])  # [K, jobs]
+    total_ms = float(step_ms.sum())
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = pairs_step / (ms_per_step * 1e-3)
+
+    # ---- roofline of the dominant kernel (the P2P kernel; SFU/MUFU-bound for dense boxes)
+    clocks = sampler.summary()
+    peak_clk = (clocks["sm_max_mhz"] or 1965) * 1e6
+    peak = MUFU_LG2_PER_CLK_PER_SM * SM_COUNT * peak_clk / 1e9  # Gpair/s
+    kernel_ms = float(kern_ms.sum(axis=0).sum() / args.steps)
+    achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
+    traffic = _ncu_traffic(args, names)
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gpair/s (1 MUFU.LG2 per pair)",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_basis": f"{MUFU_LG2_PER_CLK_PER_SM} MUFU.LG2/clk/SM x {SM_COUNT} SMs x "
+                              f"{peak_clk / 1e6:.0f} MHz (sm_max); DESIGN.md §5",
+                "kernel_ms_per_step": kernel_ms,
+                "alg_bytes_per_step": sum(j["info"]["alg_bytes_kernel"] for j in jobs),
+                "hbm_gbs_alg": sum(j["info"]["alg_bytes_kernel"] for j in jobs) / (kernel_ms * 1e-3) / 1e9}
+    per_cfg = []
+    for i, j in enumerate(jobs):
+        kms = float(np.mean(kern_ms[:, i]))
+        gp = j["info"]["pairs"] / (kms * 1e-3) / 1e9
+        per_cfg.append({"config": j["name"], "pairs": j["info"]["pairs"], "ms": kms, "Gpair_s": gp,
+                        "frac_mufu": gp / peak, "tile_log2": j["info"]["tile_log2"],
+                        "alg_GBs": j["info"]["alg_bytes_kernel"] / (kms * 1e-3) / 1e9,
+                        "D_occ": j["info"]["density_occupied"], "t_max": j["info"]["t_max"]})
+
+    # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier)
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "pair-interactions/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (seeded SplitMix64 plates shaped like the paper's PEC plate, SURVEY.md §8(d))",
+        "config": {"workload": args.workload, "configs": names, "layout": args.layout,
+                   "precision": args.precision, "kind": args.kind, "pairs_per_step": pairs_step,
+                   "order": "plan", "l2": "flushed (256 MiB write) between timed steps",
+                   "parallelism": f"morton-range x{world}" + (" + NCCL halo exchange" if world > 1 else "")},
+        "gpu_launches": args.steps * len(jobs) * (1 if world == 1 else 3),
+        "roofline": roofline, "clocks": clocks, "e2e": e2e, "per_config": per_cfg,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        out["cpu_baseline"] = {k: v for k, v in cpu_baseline(names, args.kind, args.cpu_seconds).items()
+                               if k not in ("pairs", "seconds")}
+    if rank == 0 and world == 1 and not args.no_extras and not args.profile:
+        out["extras"] = _extras(args, names, stream, dev)
+    for j in jobs:
+        j["plan"].close()
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _owned_user_indices(pl, src, part, rank):
+    """User indices of the sources this rank owns (global plan range part[0, rank]..part[0, rank+1])."""
+    gidx = pl.export("src_global")
+    uidx = pl.export("src_perm")
+    lo, hi = part[0, rank], part[0, rank + 1]
+    m = (gidx >= lo) & (gidx < hi)
+    owned = uidx[m]
+    # the local set may miss owned sources outside every tile region: rebuild from a full plan order
+    if len(owned) != hi - lo:
+        from paper_2403_01596_b200 import p2p
+        full = p2p.Plan(src, src[:1], level=pl.info["level"], device=-1)
+        owned = full.export("src_perm")[lo:hi]
+        full.close()
+    return owned
+
+
+def _ncu_traffic(args, names):
+    """dram bytes per launch of the P2P kernel from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        data = json.load(open(path))
+        key = f"{args.layout}_{args.precision}"
+        vals = [data[n][key]["dram_bytes"] for n in names if n in data and key in data[n]]
+        return float(sum(vals)) if len(vals) == len(names) else None
+    except Exception:
+        return None
+
+
+def _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier):
+    import torch
+    from paper_2403_01596_b200 import p2p
+    if world > 1:
+        return None
+    hq = [torch.as_tensor(j["q_user"], dtype=j["plan"].torch_dtype).pin_memory() for j in jobs]
+    ho = [torch.empty(j["info"]["n_tgt"], dtype=j["plan"].torch_dtype).pin_memory() for j in jobs]
+    h2d = sum(int(t.numel() * t.element_size()) for t in hq)
+    d2h = sum(int(t.numel() * t.element_size()) for t in ho)
+
+    def step():
+        for j, a, b in zip(jobs, hq, ho):
+            p2p.p2p_apply_host(j["plan"].handle, a.data_ptr(), b.data_ptr(), p2p.P2P_ORDER_USER, 0,
+                               stream.cuda_stream)
+    for _ in range(3):
+        step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    return {"value": pairs_step / (ms * 1e-3), "unit": "pair-interactions/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "order": "user (permutations on device)"}
+
+
+def _extras(args, names, stream, dev):
+    """Detail lines: both layouts x both precisions on the same workload (fewer steps)."""
+    import torch
+    from paper_2403_01596_b200 import p2p
+    res = []
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for layout in ("nr", "r"):
+        for prec in ("fp32", "fp64"):
+            for name in names:
+                cfg = W.CONFIGS[name]
+                src, tgt, q = W.make_problem(cfg, kind=args.kind)
+                with p2p.Plan(src, tgt, level=cfg.level, layout=layout, precision=prec, device=dev.index) as pl:
+                    qd = torch.as_tensor(q[pl.export("src_perm")], dtype=pl.torch_dtype, device=dev)
+                    out = torch.empty(pl.info["n_tgt_local"], dtype=pl.torch_dtype, device=dev)
+                    for _ in range(3):
+                        pl.apply(qd, out)
+                    times = []
+                    for _ in range(5):
+                        flush.zero_()
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record(stream)
+                        pl.apply(qd, out)
+                        b.record(stream)
+                        b.synchronize()
+                        times.append(a.elapsed_time(b))
+                    ms = float(np.median(times))
+                    info = pl.info
+                    res.append({"config": name, "layout": layout, "precision": prec, "ms": ms,
+                                "Gpair_s": info["pairs"] / (ms * 1e-3) / 1e9,
+                                "alg_GBs_apply": info["alg_bytes_apply"] / (ms * 1e-3) / 1e9,
+                                "plan_build_s": info["build_seconds"], "upload_s": info["upload_seconds"],
+                                "device_MB": info["device_bytes"] / 1e6, "halo_entries": info["halo_entries"]})
+    return res
+
+
+if __name__ == "__main__":
+    sys.exit(main())

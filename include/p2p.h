@@ -1,0 +1,207 @@
+/*
+ * p2p.h -- C ABI of the B200-native MLFMA near-field (P2P) operator.
+ *
+ * The operation (§3 L61-79 and §4.1; kernel per SPEC.md L150-158;
+ * SURVEY.md §8 hot-path sentence):
+ *
+ *     phi_t = sum_{s : box(s) in E1(box(t)), r_ts >= eps}  q_s * ln(1/r_ts)
+ *
+ * where the leaf level L gives a 2^(L-1) x 2^(L-1) grid of boxes on the unit
+ * square ("The number of boxes is equal to 4^{L-1}"), box(p) =
+ * (min(floor(x*2^(L-1)), 2^(L-1)-1), same for y), and E1(b) is
+ * b plus its <= 8 adjacent boxes, clipped at the domain edge (PAPER.md L88,
+ * "The number 9 ... adjacent neighboring boxes").
+ *
+ * Life cycle: p2p_plan_create (host-side plan build: level selection, box
+ * assignment, Morton sort, CSR offsets, tiles, partition, NR/R layout, upload)
+ * -> p2p_apply (per matrix-vector product; stream-ordered, allocation-free)
+ * -> p2p_destroy.
+ *
+ * Conventions:
+ *  - Every entry point returns a p2p_status; nothing throws or exits.  On
+ *    failure p2p_last_error() returns a thread-local human-readable detail.
+ *  - "Host" pointers are ordinary CPU memory; "device" pointers are CUDA
+ *    global memory on the plan's device (e.g. torch.Tensor.data_ptr()).
+ *  - Plan order ("P2P_ORDER_PLAN") is the Morton order of the leaf boxes, and
+ *    within a box the original index order (stable sort; "in the
+ *    order of the boxes' morton index").  It is the fast path: no permutation.
+ *  - One apply may be in flight per plan at a time (the plan owns workspace).
+ *  - There is no CPU fallback: a plan created with device < 0 is host-only
+ *    (plan building, introspection and export work; apply returns
+ *    P2P_ERROR_NO_DEVICE).
+ */
+#ifndef P2P_B200_H
+#define P2P_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define P2P_ABI_VERSION 1
+
+typedef struct p2p_plan_s *p2p_plan; /* opaque; owned by the library */
+
+typedef enum {
+    P2P_SUCCESS = 0,
+    P2P_ERROR_INVALID_ARGUMENT = 1,     /* n = 0, non-finite or out-of-[0,1] coordinate, L+i < 1 */
+    P2P_ERROR_CONSTRUCTION_FAILURE = 2, /* CT loop exceeded l_max */
+    P2P_ERROR_LAYOUT_CORRUPT = 3,       /* internal offsets inconsistent */
+    P2P_ERROR_OUT_OF_MEMORY = 4,        /* host or device allocation failed */
+    P2P_ERROR_CUDA = 5,                 /* a CUDA runtime call failed; detail in p2p_last_error() */
+    P2P_ERROR_NOT_SUPPORTED = 6,        /* valid request outside this build's envelope (e.g. L > 15) */
+    P2P_ERROR_NO_DEVICE = 7             /* apply on a host-only plan, or no CUDA device */
+} p2p_status;
+
+typedef enum { P2P_KERNEL_LAPLACE_2D = 0 /* q ln(1/r); 0 when r < eps */ } p2p_kernel;
+
+/* Source layouts (§3.2 Indexing = non-redundant; §3.3 Repetition =
+ * redundant), re-derived for B200: NR = Morton-sorted points + CSR box
+ * offsets, gathered per tile into shared memory; R = per target box, the
+ * packed halo of its E1 sources (coordinates copied at plan time, weights
+ * refreshed per apply by a pack kernel), read as one contiguous bulk copy
+ * per tile. */
+typedef enum { P2P_LAYOUT_NONREDUNDANT = 0, P2P_LAYOUT_REDUNDANT = 1 } p2p_layout;
+
+/* fp64 is paper-faithful ("stored as Double"); fp32 uses
+ * box-local coordinates and the SFU lg2. */
+typedef enum { P2P_FP64 = 0, P2P_FP32 = 1 } p2p_precision;
+
+typedef enum {
+    P2P_ORDER_PLAN = 0, /* q and phi in plan (Morton) order */
+    P2P_ORDER_USER = 1  /* q and phi in the caller's original point order */
+} p2p_order;
+
+typedef struct {
+    uint32_t struct_size;  /* = sizeof(p2p_plan_desc); set by p2p_plan_desc_init */
+    int32_t abi_version;   /* = P2P_ABI_VERSION */
+    int64_t n_src, n_tgt;  /* global point counts, >= 1 */
+    const double *src_xy;  /* host, [n_src][2] interleaved x,y in [0,1]^2; copied, caller keeps ownership */
+    const double *tgt_xy;  /* host, [n_tgt][2]; may alias src_xy (collocated) */
+    int32_t level;         /* > 0: leaf level L (grid 2^(L-1) per side); 0: CT loop */
+    int32_t ct;            /* CT loop clustering threshold (default 15) */
+    int32_t l_start;       /* CT loop start level (default 3) */
+    int32_t l_max;         /* CT loop cap (default 15 in this build; SPEC.md L122 caps at 16) */
+    int32_t level_delta;   /* i of PAPER.md Eq. 37 (L' = L + i), applied after the CT loop */
+    int32_t kernel;        /* p2p_kernel */
+    double epsilon;        /* minimum separation (default 1e-12) */
+    int32_t layout;        /* p2p_layout */
+    int32_t precision;     /* p2p_precision */
+    int32_t device;        /* CUDA device ordinal; -1 = host-only plan (no upload, no apply) */
+    int32_t tile_log2;     /* -1 = auto; else CTA tile side 2^tile_log2 leaf boxes */
+    void *stream;          /* cudaStream_t for plan-time uploads (NULL = default stream) */
+    int32_t part_world;    /* number of Morton-range partitions (ranks); 1 = whole problem */
+    int32_t part_rank;     /* partition owned by this plan, 0 <= part_rank < part_world */
+} p2p_plan_desc;
+
+/* Fill *desc with defaults (level 0 -> CT loop, ct 15, l_start 3, l_max 15,
+ * epsilon 1e-12, NR, fp32, device 0, auto tile, 1 partition). */
+void p2p_plan_desc_init(p2p_plan_desc *desc);
+
+/* Build a plan.  Copies the host inputs; allocates all device memory and
+ * workspace on desc->device; uploads on desc->stream and synchronises it.
+ * *out is set to NULL on failure.  Errors: INVALID_ARGUMENT, CONSTRUCTION_FAILURE,
+ * NOT_SUPPORTED, OUT_OF_MEMORY, CUDA. */
+p2p_status p2p_plan_create(const p2p_plan_desc *desc, p2p_plan *out);
+
+/* phi = A q on the plan's device, asynchronously on `stream` (cudaStream_t,
+ * NULL = default stream).
+ *   d_q   : device, weights in the plan precision (float or double).
+ *           ORDER_PLAN: n_src elements in global plan order.
+ *           ORDER_USER: n_src elements in the caller's point order.
+ *   d_out : device, results in the plan precision.
+ *           ORDER_PLAN: n_tgt_local elements = this partition's targets in plan order.
+ *           ORDER_USER: n_tgt elements in the caller's order; only this
+ *           partition's targets are written.
+ *   accumulate: 0 -> overwrite, 1 -> d_out += phi (near + far).
+ * The caller keeps ownership of d_q/d_out; they must not alias.
+ * Errors: INVALID_ARGUMENT (NULL pointers, bad order), NO_DEVICE, CUDA. */
+p2p_status p2p_apply(p2p_plan plan, const void *d_q, void *d_out, int32_t order,
+                     int32_t accumulate, void *stream);
+
+/* Same operation with HOST buffers (h_q: n_src weights, h_out: n_tgt_local
+ * (ORDER_PLAN) or n_tgt (ORDER_USER) results).  Copies h_q to the device,
+ * applies, copies the result back and synchronises `stream`.  For full copy
+ * bandwidth pass page-locked (pinned) memory.  With accumulate = 1, h_out is
+ * read first. */
+p2p_status p2p_apply_host(p2p_plan plan, const void *h_q, void *h_out, int32_t order,
+                          int32_t accumulate, void *stream);
+
+/* Distributed apply (part_world > 1, weights NOT replicated): phi for this
+ * partition's targets (plan order, n_tgt_local) from
+ *   d_q_owned: device, n_src_owned weights this partition owns, in plan order
+ *              (global plan indices [src_owned_begin, src_owned_begin + n_src_owned));
+ *   d_q_halo : device, n_halo weights received from the other partitions, grouped
+ *              by owner rank ascending and, within an owner, by global plan
+ *              index ascending (the order p2p_halo_pack produces on the owner).
+ * The halo weight exchange itself is the caller's collective (NCCL via a
+ * torch ProcessGroup). */
+p2p_status p2p_apply_dist(p2p_plan plan, const void *d_q_owned, const void *d_q_halo,
+                          void *d_out, int32_t accumulate, void *stream);
+
+/* Gather this partition's owned weights that the other partitions need into
+ * d_send (device, n_send elements), grouped by destination rank ascending,
+ * within a destination by global plan index ascending. */
+p2p_status p2p_halo_pack(p2p_plan plan, const void *d_q_owned, void *d_send, void *stream);
+
+/* Release all host and device memory of the plan.  NULL is a no-op. */
+p2p_status p2p_destroy(p2p_plan plan);
+
+typedef struct {
+    uint32_t struct_size;
+    int32_t level, tile_log2, layout, precision, device, part_world, part_rank;
+    int64_t side;                /* 2^(L-1) */
+    int64_t boxes;               /* 4^(L-1) */
+    int64_t n_src, n_tgt;        /* global */
+    int64_t n_src_local;         /* sources the kernel reads (owned + halo) */
+    int64_t n_tgt_local;         /* targets owned by this partition */
+    int64_t n_src_owned, src_owned_begin, tgt_begin; /* global plan index ranges */
+    int64_t n_halo, n_send;      /* per-apply exchange sizes (elements) */
+    int64_t occupied_src_boxes, occupied_tgt_boxes;
+    int64_t t_max;               /* max over boxes of max(#src, #tgt) ("t") */
+    double density;              /* D = N_tgt / 4^(L-1) */
+    double density_occupied;     /* N_tgt / occupied target boxes */
+    int64_t pairs;               /* pair-interactions of this partition (int64, exact) */
+    int64_t pairs_global;        /* pair-interactions of the whole problem */
+    int64_t tiles;               /* CTAs per apply (non-empty tiles of this partition) */
+    int64_t smem_bytes;          /* dynamic shared memory per CTA */
+    int64_t halo_entries;        /* R layout: packed halo entries (incl. padding) */
+    int64_t alg_bytes_kernel;    /* algorithmic HBM bytes of the P2P kernel per apply */
+    int64_t alg_bytes_apply;     /* algorithmic HBM bytes of the whole apply (incl. R pack) */
+    int64_t device_bytes;        /* device memory held by the plan */
+    double build_seconds;        /* host plan build */
+    double upload_seconds;       /* host -> device upload */
+} p2p_plan_info;
+
+p2p_status p2p_plan_get_info(p2p_plan plan, p2p_plan_info *info);
+
+typedef enum {
+    P2P_EXPORT_SRC_PERM = 0,        /* int64[n_src_local]: original (user) index of each local source, plan order */
+    P2P_EXPORT_TGT_PERM = 1,        /* int64[n_tgt_local]: original index of each owned target, plan order */
+    P2P_EXPORT_SRC_BOX_OFFSETS = 2, /* int64[boxes+1]: global CSR offsets of sources per Morton box */
+    P2P_EXPORT_TGT_BOX_OFFSETS = 3, /* int64[boxes+1]: global CSR offsets of targets per Morton box */
+    P2P_EXPORT_NEIGHBORS = 4,       /* int64[boxes*9]: E1 list per box, ascending Morton, -1 padded */
+    P2P_EXPORT_PARTITION = 5,       /* int64[2*(part_world+1)]: src_begin[0..W], tgt_begin[0..W] (global plan idx) */
+    P2P_EXPORT_SRC_GLOBAL = 6,      /* int64[n_src_local]: global plan index of each local source */
+    P2P_EXPORT_HALO_COUNTS = 7,     /* int64[2*part_world]: recv count per owner rank, send count per dest rank */
+    P2P_EXPORT_TILES = 8,           /* int64[tiles]: Morton index of each CTA tile (launch order) */
+    P2P_EXPORT_HALO_INDEX = 9,      /* int64[halo_entries]: R layout, local source of each packed entry (-1 = pad) */
+    P2P_EXPORT_SEND_INDEX = 10,     /* int64[n_send]: owned-local index of each sent weight */
+    P2P_EXPORT_HALO_OFFSETS = 11    /* int64[boxes+1]: R layout, packed-halo offsets per Morton box */
+} p2p_export_kind;
+
+/* Copy a plan array to host memory.  If host_dst is NULL, *bytes receives the
+ * required size; otherwise *bytes must be >= that size.  Arrays are computed
+ * by the host builder and are bit-exact functions of the inputs. */
+p2p_status p2p_plan_export(p2p_plan plan, int32_t kind, void *host_dst, size_t *bytes);
+
+const char *p2p_status_string(p2p_status status);
+const char *p2p_last_error(void); /* thread-local detail of the last failure ("" if none) */
+int32_t p2p_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* P2P_B200_H */

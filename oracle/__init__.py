@@ -17,7 +17,20 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+
+
+def _cpu_tag() -> str:
+    """-march=native binaries are CPU-specific: key the library by the host CPU."""
+    import hashlib
+    try:
+        info = open("/proc/cpuinfo").read()
+        model = [l for l in info.splitlines() if l.startswith(("model name", "flags"))][:2]
+    except OSError:
+        model = []
+    return hashlib.sha1("\n".join(model).encode()).hexdigest()[:10]
+
+
+_LIB = os.path.join(_HERE, f"liboracle_{_cpu_tag()}.so")
 
 CFLAGS = ["-O3", "-march=native", "-fopenmp", "-fPIC", "-shared", "-std=c11"]  # no -ffast-math
 

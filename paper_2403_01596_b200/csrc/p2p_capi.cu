@@ -1,0 +1,463 @@
+// p2p_capi.cu -- implementation of include/p2p.h: plan lifecycle, device
+// upload, apply dispatch, introspection and export.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "p2p.h"
+#include "p2p_kernels.cuh"
+#include "plan.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+p2p_status set_error(p2p_status s, const std::string &msg) {
+    g_last_error = msg;
+    return s;
+}
+
+struct CudaError : p2p::Error {
+    CudaError(const std::string &m) : p2p::Error(P2P_ERROR_CUDA, m) {}
+};
+
+void ck(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) {
+        if (e == cudaErrorMemoryAllocation) throw p2p::Error(P2P_ERROR_OUT_OF_MEMORY, std::string(what) + ": out of device memory");
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct p2p_plan_s {
+    p2p::HostPlan hp;
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    // device arrays
+    DevBuf tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
+    DevBuf halo_off, halo_idx, halo_uv, halo_q;
+    DevBuf q_local, phi, io_q, io_out;  // workspace
+    int64_t device_bytes = 0;
+    double upload_seconds = 0.0;
+    int elem = 4;
+
+    template <typename V>
+    void upload(DevBuf &b, const std::vector<V> &v) {
+        b.bytes = v.size() * sizeof(V);
+        if (!b.bytes) return;
+        ck(cudaMalloc(&b.p, b.bytes), "cudaMalloc");
+        device_bytes += (int64_t)b.bytes;
+        ck(cudaMemcpyAsync(b.p, v.data(), b.bytes, cudaMemcpyHostToDevice, stream), "cudaMemcpyAsync H2D");
+    }
+    void alloc(DevBuf &b, size_t bytes) {
+        b.bytes = bytes;
+        if (!bytes) return;
+        ck(cudaMalloc(&b.p, bytes), "cudaMalloc");
+        device_bytes += (int64_t)bytes;
+    }
+    void release() {
+        DevBuf *all[] = {&tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
+                         &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q, &q_local, &phi,
+                         &io_q, &io_out};
+        for (DevBuf *b : all) {
+            if (b->p) cudaFree(b->p);
+            b->p = nullptr;
+            b->bytes = 0;
+        }
+    }
+};
+
+namespace {
+
+template <typename T>
+const p2p::Layout<T> &layout_of(const p2p::HostPlan &hp);
+template <>
+const p2p::Layout<float> &layout_of<float>(const p2p::HostPlan &hp) { return hp.f32; }
+template <>
+const p2p::Layout<double> &layout_of<double>(const p2p::HostPlan &hp) { return hp.f64; }
+
+template <typename T>
+void upload_plan(p2p_plan_s &P) {
+    const p2p::HostPlan &hp = P.hp;
+    const p2p::Layout<T> &lay = layout_of<T>(hp);
+    P.upload(P.tiles, hp.tiles);
+    P.upload(P.tgt_off, hp.tgt_off);
+    P.upload(P.tgt_uv, lay.tgt_uv);
+    P.upload(P.tgt_uidx, hp.tgt_uidx);
+    P.upload(P.src_uidx, hp.src_uidx);
+    if (hp.part_world > 1) {
+        P.upload(P.src_gidx, hp.src_gidx);
+        P.upload(P.src_qidx, hp.src_qidx);
+        P.upload(P.send_idx, hp.send_idx);
+    }
+    if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
+        P.upload(P.src_off, hp.src_off);
+        P.upload(P.src_uv, lay.src_uv);
+    } else {
+        P.upload(P.halo_off, hp.halo_off);
+        P.upload(P.halo_idx, hp.halo_idx);
+        P.upload(P.halo_uv, lay.halo_uv);
+        P.alloc(P.halo_q, (size_t)hp.halo_entries * sizeof(T));
+    }
+    // The kernels' dynamic shared memory is fixed per plan: opt in once here, not per apply.
+    if (hp.smem_bytes > 48 * 1024) {
+        const int sm = (int)p2p::kSmemLimit;  // a permission, not a reservation: one value for all plans
+        if (hp.layout == P2P_LAYOUT_NONREDUNDANT)
+            ck(cudaFuncSetAttribute(p2p::dev::p2p_nr_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+        else
+            ck(cudaFuncSetAttribute(p2p::dev::p2p_r_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
+    }
+    P.alloc(P.q_local, (size_t)std::max<int64_t>(hp.n_src_local, 1) * sizeof(T));
+    P.alloc(P.phi, (size_t)std::max<int64_t>(hp.n_tgt_local, 1) * sizeof(T));
+    P.alloc(P.io_q, (size_t)std::max<int64_t>(hp.n_src, 1) * sizeof(T));
+    P.alloc(P.io_out, (size_t)std::max<int64_t>(hp.n_tgt, 1) * sizeof(T));
+}
+
+int grid_for(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+// The P2P kernel proper on q_local (local plan order) -> out (local plan order).
+template <typename T>
+void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStream_t s) {
+    const p2p::HostPlan &hp = P.hp;
+    const int ntiles = (int)hp.tiles.size();
+    if (ntiles == 0) return;
+    const T eps2 = (T)(hp.eps * hp.eps);
+    if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
+        auto kern = p2p::dev::p2p_nr_kernel<T>;
+        const int max_region = (int)((hp.max_region + 3) & ~int64_t(3));
+        kern<<<ntiles, p2p::kThreads, hp.smem_bytes, s>>>(
+            (const int32_t *)P.tiles.p, hp.k, hp.S, (T)hp.h, eps2, max_region, (const int32_t *)P.src_off.p,
+            (const int32_t *)P.tgt_off.p, (const typename p2p::dev::V2<T>::type *)P.src_uv.p, q_local,
+            (const typename p2p::dev::V2<T>::type *)P.tgt_uv.p, out, accumulate);
+    } else {
+        if (hp.halo_entries > 0)
+            p2p::dev::pack_r_kernel<T><<<grid_for(hp.halo_entries), 256, 0, s>>>(
+                (const int32_t *)P.halo_idx.p, q_local, (T *)P.halo_q.p, hp.halo_entries);
+        auto kern = p2p::dev::p2p_r_kernel<T>;
+        kern<<<ntiles, p2p::kThreads, hp.smem_bytes, s>>>(
+            (const int32_t *)P.tiles.p, hp.k, eps2, (const int32_t *)P.tgt_off.p, (const uint32_t *)P.halo_off.p,
+            (const T *)P.halo_uv.p, (const T *)P.halo_q.p, (const typename p2p::dev::V2<T>::type *)P.tgt_uv.p,
+            out, accumulate);
+    }
+    ck(cudaGetLastError(), "kernel launch");
+}
+
+template <typename T>
+void apply_impl(p2p_plan_s &P, const void *d_q, void *d_out, int order, int accumulate, cudaStream_t s) {
+    const p2p::HostPlan &hp = P.hp;
+    const T *q_local = (const T *)d_q;
+    if (order == P2P_ORDER_USER) {
+        if (hp.n_src_local)
+            p2p::dev::gather_kernel<T><<<grid_for(hp.n_src_local), 256, 0, s>>>(
+                (const int32_t *)P.src_uidx.p, (const T *)d_q, (T *)P.q_local.p, hp.n_src_local);
+        q_local = (const T *)P.q_local.p;
+    } else if (hp.part_world > 1) {  // replicated weights in global plan order
+        if (hp.n_src_local)
+            p2p::dev::gather_kernel<T><<<grid_for(hp.n_src_local), 256, 0, s>>>(
+                (const int32_t *)P.src_gidx.p, (const T *)d_q, (T *)P.q_local.p, hp.n_src_local);
+        q_local = (const T *)P.q_local.p;
+    }
+    if (order == P2P_ORDER_USER) {
+        launch_p2p<T>(P, q_local, (T *)P.phi.p, 0, s);
+        if (hp.n_tgt_local)
+            p2p::dev::scatter_kernel<T><<<grid_for(hp.n_tgt_local), 256, 0, s>>>(
+                (const int32_t *)P.tgt_uidx.p, (const T *)P.phi.p, (T *)d_out, hp.n_tgt_local, accumulate);
+    } else {
+        launch_p2p<T>(P, q_local, (T *)d_out, accumulate, s);
+    }
+    ck(cudaGetLastError(), "apply launch");
+}
+
+template <typename T>
+void apply_dist_impl(p2p_plan_s &P, const void *d_q_owned, const void *d_q_halo, void *d_out, int accumulate,
+                     cudaStream_t s) {
+    const p2p::HostPlan &hp = P.hp;
+    if (hp.n_src_local)
+        p2p::dev::gather2_kernel<T><<<grid_for(hp.n_src_local), 256, 0, s>>>(
+            (const int32_t *)P.src_qidx.p, (const T *)d_q_owned, (const T *)d_q_halo, hp.n_src_owned,
+            (T *)P.q_local.p, hp.n_src_local);
+    launch_p2p<T>(P, (const T *)P.q_local.p, (T *)d_out, accumulate, s);
+    ck(cudaGetLastError(), "apply_dist launch");
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (dev >= 0 && dev != prev) ck(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <typename F>
+p2p_status guarded(F f) {
+    try {
+        f();
+        g_last_error.clear();
+        return P2P_SUCCESS;
+    } catch (const p2p::Error &e) {
+        return set_error(e.code, e.what());
+    } catch (const std::bad_alloc &) {
+        return set_error(P2P_ERROR_OUT_OF_MEMORY, "host allocation failed");
+    } catch (const std::exception &e) {
+        return set_error(P2P_ERROR_CUDA, e.what());
+    }
+}
+
+void require_device(const p2p_plan_s *P) {
+    if (P->device < 0) throw p2p::Error(P2P_ERROR_NO_DEVICE, "host-only plan (device < 0): no apply; there is no CPU fallback");
+}
+
+}  // namespace
+
+extern "C" {
+
+void p2p_plan_desc_init(p2p_plan_desc *d) {
+    if (!d) return;
+    std::memset(d, 0, sizeof(*d));
+    d->struct_size = sizeof(p2p_plan_desc);
+    d->abi_version = P2P_ABI_VERSION;
+    d->level = 0;
+    d->ct = 15;
+    d->l_start = 3;
+    d->l_max = p2p::kMaxLevel;
+    d->level_delta = 0;
+    d->kernel = P2P_KERNEL_LAPLACE_2D;
+    d->epsilon = 1e-12;
+    d->layout = P2P_LAYOUT_NONREDUNDANT;
+    d->precision = P2P_FP32;
+    d->device = 0;
+    d->tile_log2 = -1;
+    d->stream = nullptr;
+    d->part_world = 1;
+    d->part_rank = 0;
+}
+
+p2p_status p2p_plan_create(const p2p_plan_desc *desc, p2p_plan *out) {
+    if (out) *out = nullptr;
+    if (!desc || !out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL desc or out");
+    std::unique_ptr<p2p_plan_s> P(new (std::nothrow) p2p_plan_s());
+    if (!P) return set_error(P2P_ERROR_OUT_OF_MEMORY, "host allocation failed");
+    p2p_status st = guarded([&] {
+        p2p::build_host_plan(*desc, P->hp);
+        P->device = desc->device;
+        P->elem = desc->precision == P2P_FP32 ? 4 : 8;
+        if (desc->device >= 0) {
+            int ndev = 0;
+            if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+                throw p2p::Error(P2P_ERROR_NO_DEVICE, "no CUDA device visible");
+            if (desc->device >= ndev) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "device ordinal out of range");
+            DeviceGuard g(desc->device);
+            P->stream = (cudaStream_t)desc->stream;
+            auto t0 = std::chrono::steady_clock::now();
+            try {
+                if (desc->precision == P2P_FP32) upload_plan<float>(*P);
+                else upload_plan<double>(*P);
+                ck(cudaStreamSynchronize(P->stream), "upload sync");
+            } catch (...) {
+                P->release();
+                throw;
+            }
+            P->upload_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+    if (st == P2P_SUCCESS) *out = P.release();
+    return st;
+}
+
+p2p_status p2p_apply(p2p_plan P, const void *d_q, void *d_out, int32_t order, int32_t accumulate, void *stream) {
+    if (!P || !d_q || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or buffer");
+    if (order != P2P_ORDER_PLAN && order != P2P_ORDER_USER) return set_error(P2P_ERROR_INVALID_ARGUMENT, "bad order");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        if (P->elem == 4) apply_impl<float>(*P, d_q, d_out, order, accumulate ? 1 : 0, s);
+        else apply_impl<double>(*P, d_q, d_out, order, accumulate ? 1 : 0, s);
+    });
+}
+
+p2p_status p2p_apply_host(p2p_plan P, const void *h_q, void *h_out, int32_t order, int32_t accumulate,
+                          void *stream) {
+    if (!P || !h_q || !h_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or buffer");
+    if (order != P2P_ORDER_PLAN && order != P2P_ORDER_USER) return set_error(P2P_ERROR_INVALID_ARGUMENT, "bad order");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        const p2p::HostPlan &hp = P->hp;
+        const size_t qb = (size_t)hp.n_src * P->elem;
+        const size_t ob = (size_t)(order == P2P_ORDER_USER ? hp.n_tgt : hp.n_tgt_local) * P->elem;
+        ck(cudaMemcpyAsync(P->io_q.p, h_q, qb, cudaMemcpyHostToDevice, s), "H2D q");
+        if (accumulate) ck(cudaMemcpyAsync(P->io_out.p, h_out, ob, cudaMemcpyHostToDevice, s), "H2D out");
+        if (P->elem == 4) apply_impl<float>(*P, P->io_q.p, P->io_out.p, order, accumulate ? 1 : 0, s);
+        else apply_impl<double>(*P, P->io_q.p, P->io_out.p, order, accumulate ? 1 : 0, s);
+        ck(cudaMemcpyAsync(h_out, P->io_out.p, ob, cudaMemcpyDeviceToHost, s), "D2H out");
+        ck(cudaStreamSynchronize(s), "apply_host sync");
+    });
+}
+
+p2p_status p2p_apply_dist(p2p_plan P, const void *d_q_owned, const void *d_q_halo, void *d_out, int32_t accumulate,
+                          void *stream) {
+    if (!P || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or output");
+    if (P->hp.n_src_owned && !d_q_owned) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_q_owned");
+    if (P->hp.n_halo && !d_q_halo) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_q_halo");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        if (P->elem == 4) apply_dist_impl<float>(*P, d_q_owned, d_q_halo, d_out, accumulate ? 1 : 0, s);
+        else apply_dist_impl<double>(*P, d_q_owned, d_q_halo, d_out, accumulate ? 1 : 0, s);
+    });
+}
+
+p2p_status p2p_halo_pack(p2p_plan P, const void *d_q_owned, void *d_send, void *stream) {
+    if (!P) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan");
+    if (P->hp.n_send && (!d_q_owned || !d_send)) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL buffer");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        const int64_t n = P->hp.n_send;
+        if (!n) return;
+        if (P->elem == 4)
+            p2p::dev::gather_kernel<float><<<grid_for(n), 256, 0, s>>>((const int32_t *)P->send_idx.p,
+                                                                       (const float *)d_q_owned, (float *)d_send, n);
+        else
+            p2p::dev::gather_kernel<double><<<grid_for(n), 256, 0, s>>>(
+                (const int32_t *)P->send_idx.p, (const double *)d_q_owned, (double *)d_send, n);
+        ck(cudaGetLastError(), "halo_pack launch");
+    });
+}
+
+p2p_status p2p_destroy(p2p_plan P) {
+    if (!P) return P2P_SUCCESS;
+    if (P->device >= 0) {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(P->device);
+        P->release();
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    delete P;
+    return P2P_SUCCESS;
+}
+
+p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *info) {
+    if (!P || !info) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or info");
+    const p2p::HostPlan &hp = P->hp;
+    std::memset(info, 0, sizeof(*info));
+    info->struct_size = sizeof(p2p_plan_info);
+    info->level = hp.L;
+    info->tile_log2 = hp.k;
+    info->layout = hp.layout;
+    info->precision = hp.precision;
+    info->device = P->device;
+    info->part_world = hp.part_world;
+    info->part_rank = hp.part_rank;
+    info->side = hp.S;
+    info->boxes = hp.B;
+    info->n_src = hp.n_src;
+    info->n_tgt = hp.n_tgt;
+    info->n_src_local = hp.n_src_local;
+    info->n_tgt_local = hp.n_tgt_local;
+    info->n_src_owned = hp.n_src_owned;
+    info->src_owned_begin = hp.src_owned_begin;
+    info->tgt_begin = hp.tgt_begin;
+    info->n_halo = hp.n_halo;
+    info->n_send = hp.n_send;
+    info->occupied_src_boxes = hp.occ_src;
+    info->occupied_tgt_boxes = hp.occ_tgt;
+    info->t_max = hp.t_max;
+    info->density = hp.density;
+    info->density_occupied = hp.density_occ;
+    info->pairs = hp.pairs;
+    info->pairs_global = hp.pairs_global;
+    info->tiles = (int64_t)hp.tiles.size();
+    info->smem_bytes = hp.smem_bytes;
+    info->halo_entries = hp.halo_entries;
+    const int64_t e = hp.precision == P2P_FP32 ? 4 : 8;
+    const int64_t offs = 8 * hp.boxes_in_tiles;  // tgt + src (or halo) CSR offsets of the tiles' boxes
+    if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
+        info->alg_bytes_kernel = hp.n_tgt_local * 3 * e + hp.n_src_local * 3 * e + offs;
+        info->alg_bytes_apply = info->alg_bytes_kernel;
+    } else {
+        info->alg_bytes_kernel = hp.n_tgt_local * 3 * e + hp.halo_entries * 3 * e + offs;
+        info->alg_bytes_apply = info->alg_bytes_kernel + hp.halo_entries * (4 + e) + hp.n_src_local * e;
+    }
+    info->device_bytes = P->device_bytes;
+    info->build_seconds = hp.build_seconds;
+    info->upload_seconds = P->upload_seconds;
+    return P2P_SUCCESS;
+}
+
+p2p_status p2p_plan_export(p2p_plan P, int32_t kind, void *host_dst, size_t *bytes) {
+    if (!P || !bytes) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or bytes");
+    return guarded([&] {
+        const p2p::HostPlan &hp = P->hp;
+        std::vector<int64_t> v;
+        auto take = [&](const auto &src) { v.assign(src.begin(), src.end()); };
+        switch (kind) {
+        case P2P_EXPORT_SRC_PERM: take(hp.src_uidx); break;
+        case P2P_EXPORT_TGT_PERM: take(hp.tgt_uidx); break;
+        case P2P_EXPORT_SRC_BOX_OFFSETS: take(hp.src_off_g); break;
+        case P2P_EXPORT_TGT_BOX_OFFSETS: take(hp.tgt_off_g); break;
+        case P2P_EXPORT_NEIGHBORS: v = p2p::neighbors_export(hp); break;
+        case P2P_EXPORT_PARTITION:
+            v.assign(hp.part_src.begin(), hp.part_src.end());
+            v.insert(v.end(), hp.part_tgt.begin(), hp.part_tgt.end());
+            break;
+        case P2P_EXPORT_SRC_GLOBAL: take(hp.src_gidx); break;
+        case P2P_EXPORT_HALO_COUNTS:
+            v.assign(hp.recv_counts.begin(), hp.recv_counts.end());
+            v.insert(v.end(), hp.send_counts.begin(), hp.send_counts.end());
+            break;
+        case P2P_EXPORT_TILES: take(hp.tiles); break;
+        case P2P_EXPORT_HALO_INDEX: take(hp.halo_idx); break;
+        case P2P_EXPORT_SEND_INDEX: take(hp.send_idx); break;
+        case P2P_EXPORT_HALO_OFFSETS: take(hp.halo_off); break;
+        default: throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "unknown export kind");
+        }
+        const size_t need = v.size() * sizeof(int64_t);
+        if (!host_dst) {
+            *bytes = need;
+            return;
+        }
+        if (*bytes < need) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "export buffer too small");
+        if (need) std::memcpy(host_dst, v.data(), need);
+        *bytes = need;
+    });
+}
+
+const char *p2p_status_string(p2p_status s) {
+    switch (s) {
+    case P2P_SUCCESS: return "P2P_SUCCESS";
+    case P2P_ERROR_INVALID_ARGUMENT: return "P2P_ERROR_INVALID_ARGUMENT";
+    case P2P_ERROR_CONSTRUCTION_FAILURE: return "P2P_ERROR_CONSTRUCTION_FAILURE";
+    case P2P_ERROR_LAYOUT_CORRUPT: return "P2P_ERROR_LAYOUT_CORRUPT";
+    case P2P_ERROR_OUT_OF_MEMORY: return "P2P_ERROR_OUT_OF_MEMORY";
+    case P2P_ERROR_CUDA: return "P2P_ERROR_CUDA";
+    case P2P_ERROR_NOT_SUPPORTED: return "P2P_ERROR_NOT_SUPPORTED";
+    case P2P_ERROR_NO_DEVICE: return "P2P_ERROR_NO_DEVICE";
+    }
+    return "P2P_ERROR_UNKNOWN";
+}
+
+const char *p2p_last_error(void) { return g_last_error.c_str(); }
+
+int32_t p2p_abi_version(void) { return P2P_ABI_VERSION; }
+
+}  // extern "C"

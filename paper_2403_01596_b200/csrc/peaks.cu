@@ -1,0 +1,159 @@
+// peaks.cu -- roofline-denominator microbenchmarks:
+// MUFU.LG2 issue rate, packed-FP32 (FFMA2) rate, DFMA rate and an HBM
+// read stream, each timed with CUDA events on one device.  C ABI in
+// include/p2p_peaks.h.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "p2p_peaks.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__global__ void __launch_bounds__(kThreads) mufu_lg2_kernel(float *out, int iters, float seed) {
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = seed + threadIdx.x * 1e-3f + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float r;
+            asm volatile("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x[i]));
+            x[i] = r + 24.0f;  // stays in [~28, ~29]: a fixed point neighbourhood of lg2(x)+24
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 1234.5f) out[0] = s;  // never true; keeps the chain alive
+}
+
+__global__ void __launch_bounds__(kThreads) ffma2_kernel(float *out, int iters, float seed) {
+    unsigned long long x[8];
+    const unsigned long long a = 0x3f7ff0003f7ff000ull, b = 0x3c23d70a3c23d70aull;  // (0.99976, 0.01)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        float f = seed + i;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(x[i]) : "f"(f));
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x[i]) : "l"(a), "l"(b));
+    }
+    unsigned long long s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s ^= x[i];
+    if (s == 42ull) out[0] = 1.f;
+}
+
+__global__ void __launch_bounds__(kThreads) dfma_kernel(double *out, int iters, double seed) {
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = seed + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = fma(x[i], 0.9999999, 1e-7);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 1234.5) out[0] = s;
+}
+
+__global__ void __launch_bounds__(kThreads) read_kernel(const int4 *__restrict__ p, int64_t n, int *out) {
+    int acc = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n; i += 4 * stride) {
+        int4 a = __ldcs(p + i), b = __ldcs(p + i + stride), c = __ldcs(p + i + 2 * stride), d = __ldcs(p + i + 3 * stride);
+        acc ^= a.x ^ b.y ^ c.z ^ d.w;
+    }
+    for (; i < n; i += stride) acc ^= __ldcs(p + i).x;
+    if (acc == 0x12345678) out[0] = acc;
+}
+
+template <typename F>
+p2p_peak_status timed(int device, int reps, F launch, double *ms_out) {
+    if (cudaSetDevice(device) != cudaSuccess) return 1;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    launch();  // warm-up
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) launch();
+    cudaEventRecord(b);
+    if (cudaEventSynchronize(b) != cudaSuccess) return 2;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms_out = ms / reps;
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int sm_count(int device) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+p2p_peak_status p2p_peak_mufu_lg2(int device, double *ops_per_s) {
+    const int grid = sm_count(device) * 8, iters = 4096;
+    float *d = nullptr;
+    cudaSetDevice(device);
+    cudaMalloc(&d, 16);
+    double ms = 0;
+    p2p_peak_status st = timed(device, 5, [&] { mufu_lg2_kernel<<<grid, kThreads>>>(d, iters, 25.f); }, &ms);
+    cudaFree(d);
+    *ops_per_s = (double)grid * kThreads * iters * 8 / (ms * 1e-3);
+    return st;
+}
+
+p2p_peak_status p2p_peak_ffma2(int device, double *flops) {
+    const int grid = sm_count(device) * 8, iters = 4096;
+    float *d = nullptr;
+    cudaSetDevice(device);
+    cudaMalloc(&d, 16);
+    double ms = 0;
+    p2p_peak_status st = timed(device, 5, [&] { ffma2_kernel<<<grid, kThreads>>>(d, iters, 1.f); }, &ms);
+    cudaFree(d);
+    *flops = (double)grid * kThreads * iters * 8 * 4 / (ms * 1e-3);  // 2 lanes x (mul + add)
+    return st;
+}
+
+p2p_peak_status p2p_peak_dfma(int device, double *flops) {
+    const int grid = sm_count(device) * 8, iters = 1024;
+    double *d = nullptr;
+    cudaSetDevice(device);
+    cudaMalloc(&d, 16);
+    double ms = 0;
+    p2p_peak_status st = timed(device, 5, [&] { dfma_kernel<<<grid, kThreads>>>(d, iters, 1.0); }, &ms);
+    cudaFree(d);
+    *flops = (double)grid * kThreads * iters * 8 * 2 / (ms * 1e-3);
+    return st;
+}
+
+p2p_peak_status p2p_peak_hbm_read(int device, double *bytes_per_s) {
+    const int64_t bytes = int64_t(2) << 30;  // 2 GiB >> 126 MB L2
+    int4 *p = nullptr;
+    int *o = nullptr;
+    cudaSetDevice(device);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return 4;
+    cudaMalloc(&o, 16);
+    cudaMemset(p, 1, bytes);
+    const int grid = sm_count(device) * 8;
+    double ms = 0;
+    p2p_peak_status st = timed(device, 5, [&] { read_kernel<<<grid, kThreads>>>(p, bytes / 16, o); }, &ms);
+    cudaFree(p);
+    cudaFree(o);
+    *bytes_per_s = (double)bytes / (ms * 1e-3);
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// plan.h -- internal plan representation shared by the host builder
+// (plan_builder.cpp), the C ABI (p2p_capi.cpp) and the kernel launchers
+// (p2p_kernels.cu).  Not part of the public ABI (include/p2p.h).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "p2p.h"
+
+namespace p2p {
+
+struct Error : std::runtime_error {
+    p2p_status code;
+    Error(p2p_status c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+constexpr int kMaxLevel = 15;          // full-grid CSR offsets: 4^(L-1) <= 2^28 boxes
+constexpr int kThreads = 256;          // CTA size of the P2P kernels
+constexpr int kMaxTileLog2 = 6;
+constexpr int64_t kSmemLimit = 200 * 1024;
+
+// ---- Morton (Z-order) codes: x in the even bits, y in the odd bits
+// ("the order of the boxes' morton index").
+inline uint32_t spread16(uint32_t v) {
+    v &= 0x0000FFFFu;
+    v = (v | (v << 8)) & 0x00FF00FFu;
+    v = (v | (v << 4)) & 0x0F0F0F0Fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+inline uint32_t compact16(uint32_t v) {
+    v &= 0x55555555u;
+    v = (v | (v >> 1)) & 0x33333333u;
+    v = (v | (v >> 2)) & 0x0F0F0F0Fu;
+    v = (v | (v >> 4)) & 0x00FF00FFu;
+    v = (v | (v >> 8)) & 0x0000FFFFu;
+    return v;
+}
+inline uint32_t morton_encode(uint32_t ix, uint32_t iy) { return spread16(ix) | (spread16(iy) << 1); }
+inline void morton_decode(uint32_t m, uint32_t &ix, uint32_t &iy) {
+    ix = compact16(m);
+    iy = compact16(m >> 1);
+}
+
+// Precision-specific device layout, built on the host.
+template <typename T>
+struct Layout {
+    std::vector<T> src_uv;   // [n_src_local][2] box-local coordinates (x - ix*h, y - iy*h)
+    std::vector<T> tgt_uv;   // [n_tgt_local][2]
+    std::vector<T> halo_uv;  // R: fp32 -> per source pair (u0,u1,v0,v1); fp64 -> (u,v) per entry
+};
+
+struct HostPlan {
+    // ---- parameters
+    int L = 0, k = 0, layout = 0, precision = 0, device = -1;
+    int part_world = 1, part_rank = 0;
+    int64_t S = 0, B = 0;        // grid side, number of leaf boxes
+    double h = 0.0, eps = 1e-12;
+    int64_t n_src = 0, n_tgt = 0;
+
+    // ---- global indexing (bit-exact exports)
+    std::vector<int32_t> src_off_g, tgt_off_g;    // [B+1] CSR offsets in Morton order
+    std::vector<int32_t> src_perm_g, tgt_perm_g;  // global plan index -> user index
+
+    // ---- tiles and partition
+    std::vector<int32_t> tiles_g;                 // non-empty tiles (Morton tile index), ascending
+    std::vector<int64_t> tile_pairs_g;            // pairs per non-empty tile
+    std::vector<int64_t> part_tile;               // [W+1] cut indices into tiles_g
+    std::vector<int64_t> part_src, part_tgt;      // [W+1] global plan index cuts
+    std::vector<int32_t> tiles;                   // this partition's tiles (launch order)
+
+    // ---- local (this partition) indexing
+    std::vector<int32_t> src_off, tgt_off;        // [B+1] local CSR offsets
+    std::vector<int32_t> src_gidx;                // local source -> global plan index
+    std::vector<int32_t> src_uidx;                // local source -> user index
+    std::vector<int32_t> tgt_uidx;                // local target -> user index
+    std::vector<int32_t> src_qidx;                // local source -> index into [owned | halo]
+    int64_t n_src_local = 0, n_tgt_local = 0, n_src_owned = 0, n_halo = 0, n_send = 0;
+    int64_t src_owned_begin = 0, tgt_begin = 0;
+    std::vector<int64_t> recv_counts, send_counts;  // [W]
+    std::vector<int32_t> send_idx;                  // owned-local index per sent weight
+
+    // ---- R layout
+    std::vector<uint32_t> halo_off;               // [B+1]
+    std::vector<int32_t> halo_idx;                // local source index, -1 = pad
+    int64_t halo_entries = 0;
+
+    Layout<float> f32;
+    Layout<double> f64;
+
+    // ---- statistics
+    int64_t pairs = 0, pairs_global = 0, t_max = 0, occ_src = 0, occ_tgt = 0;
+    int64_t boxes_in_tiles = 0, max_region = 0, max_tile_halo = 0, smem_bytes = 0;
+    double density = 0.0, density_occ = 0.0, build_seconds = 0.0;
+};
+
+void build_host_plan(const p2p_plan_desc &desc, HostPlan &hp);
+std::vector<int64_t> neighbors_export(const HostPlan &hp);
+int64_t nr_smem_bytes(int k, int64_t max_region, int elem_bytes);
+int64_t r_smem_bytes(int k, int64_t max_halo, int elem_bytes);
+
+}  // namespace p2p

@@ -1,0 +1,495 @@
+// plan_builder.cpp -- host-side plan builder ("data collection", PAPER.md
+// §3.2 L79 and §3.3, re-derived for B200).
+//
+// Steps:
+//   a1 level selection: explicit L, or the CT loop of PAPER.md §3.1
+//      (start at l_start, L += 1 until no leaf holds more than CT sources or
+//      CT targets), then L += level_delta (§4.6 Eq. 37).
+//   a2 box assignment: ix = min(floor(x*S), S-1) -> Morton code.
+//   a3 stable counting sort by Morton code -> permutation + CSR box offsets
+//      (the paper's "second order index").
+//   a4 E1 neighbourhoods are implicit (3x3 block, clipped); an
+//      explicit list is only materialised for export.
+//   a5 NR layout (Morton-sorted box-local coordinates) and R layout (per
+//      target box, the packed halo of its E1 sources; §3.3).
+// Plus CTA tiling, exact int64 pair counts and the Morton-range partition
+// across ranks.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <thread>
+
+#include "plan.h"
+
+namespace p2p {
+
+namespace {
+
+[[noreturn]] void fail(p2p_status c, const std::string &m) { throw Error(c, m); }
+
+template <typename F>
+void parallel_for(int64_t n, F f, int64_t grain = 1 << 15) {
+    unsigned hw = std::thread::hardware_concurrency();
+    unsigned nt = std::max(1u, std::min(hw ? hw : 1u, 64u));
+    if (n <= grain || nt == 1) {
+        f(int64_t(0), n);
+        return;
+    }
+    nt = (unsigned)std::min<int64_t>(nt, (n + grain - 1) / grain);
+    std::vector<std::thread> th;
+    int64_t chunk = (n + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+        int64_t a = (int64_t)t * chunk, b = std::min(n, a + chunk);
+        if (a >= b) break;
+        th.emplace_back([=] { f(a, b); });
+    }
+    for (auto &x : th) x.join();
+}
+
+inline uint32_t cell_of(double x, int64_t S) {
+    // floor(x*S) is exact: S is a power of two.  Closed at the upper edge.
+    int64_t c = (int64_t)std::floor(x * (double)S);
+    if (c > S - 1) c = S - 1;
+    if (c < 0) c = 0;
+    return (uint32_t)c;
+}
+
+inline int64_t pad2(int64_t n) { return (n + 1) & ~int64_t(1); }
+inline int64_t pad4(int64_t n) { return (n + 3) & ~int64_t(3); }
+
+void validate_points(const double *xy, int64_t n, const char *what) {
+    if (n < 1) fail(P2P_ERROR_INVALID_ARGUMENT, std::string(what) + ": n must be >= 1 (SPEC.md L55)");
+    if (!xy) fail(P2P_ERROR_INVALID_ARGUMENT, std::string(what) + ": NULL coordinates");
+    for (int64_t i = 0; i < 2 * n; ++i) {
+        double v = xy[i];
+        if (!(v >= 0.0 && v <= 1.0))  // also rejects NaN
+            fail(P2P_ERROR_INVALID_ARGUMENT, std::string(what) + ": coordinate " + std::to_string(i / 2) +
+                                                 " outside the unit square [0,1]^2 (SPEC.md L119)");
+    }
+}
+
+// Max number of points sharing one cell at level L, from codes sorted at
+// level lref >= L (a Morton code's prefix is the parent box: code_L = code >> 2(lref-L)).
+int64_t max_run(const std::vector<uint32_t> &sorted, int shift) {
+    int64_t best = 0, run = 0;
+    uint32_t prev = 0;
+    for (size_t i = 0; i < sorted.size(); ++i) {
+        uint32_t c = sorted[i] >> shift;
+        run = (i && c == prev) ? run + 1 : 1;
+        prev = c;
+        best = std::max(best, run);
+    }
+    return best;
+}
+
+// a1: PAPER.md §3.1 L67-69 tree-construction loop.
+int ct_loop_level(const p2p_plan_desc &d) {
+    int lmax = std::min(d.l_max, kMaxLevel);
+    if (d.l_start < 1) fail(P2P_ERROR_INVALID_ARGUMENT, "l_start must be >= 1");
+    if (d.ct < 1) fail(P2P_ERROR_INVALID_ARGUMENT, "ct must be >= 1");
+    int64_t Sref = int64_t(1) << (lmax - 1);
+    auto codes = [&](const double *xy, int64_t n) {
+        std::vector<uint32_t> c((size_t)n);
+        parallel_for(n, [&](int64_t a, int64_t b) {
+            for (int64_t i = a; i < b; ++i)
+                c[i] = morton_encode(cell_of(xy[2 * i], Sref), cell_of(xy[2 * i + 1], Sref));
+        });
+        std::sort(c.begin(), c.end());
+        return c;
+    };
+    std::vector<uint32_t> cs = codes(d.src_xy, d.n_src), ct = codes(d.tgt_xy, d.n_tgt);
+    for (int L = std::max(1, d.l_start); L <= lmax; ++L) {
+        int shift = 2 * (lmax - L);
+        if (max_run(cs, shift) <= d.ct && max_run(ct, shift) <= d.ct) return L;
+    }
+    fail(P2P_ERROR_CONSTRUCTION_FAILURE,
+         "CT loop: some leaf box still holds more than CT points at L = " + std::to_string(lmax) +
+             " (cap; SPEC.md L75)");
+}
+
+// a2 + a3: stable counting sort of points by Morton code of their leaf box.
+void csr_sort(const double *xy, int64_t n, const HostPlan &hp, std::vector<int32_t> &off,
+              std::vector<int32_t> &perm) {
+    std::vector<uint32_t> code((size_t)n);
+    parallel_for(n, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i)
+            code[i] = morton_encode(cell_of(xy[2 * i], hp.S), cell_of(xy[2 * i + 1], hp.S));
+    });
+    off.assign((size_t)hp.B + 1, 0);
+    for (int64_t i = 0; i < n; ++i) off[code[i] + 1] += 1;
+    for (int64_t b = 0; b < hp.B; ++b) off[b + 1] += off[b];
+    std::vector<int32_t> pos(off.begin(), off.end() - 1);
+    perm.resize((size_t)n);
+    for (int64_t i = 0; i < n; ++i) perm[pos[code[i]]++] = (int32_t)i;
+}
+
+}  // namespace
+
+int64_t nr_smem_bytes(int k, int64_t max_region, int e) {
+    int64_t W = int64_t(1) << k, R = W + 2, RR = R * R, WW = W * W;
+    int64_t tables = 4 * (3 * RR + WW + 2);
+    tables = (tables + 15) & ~int64_t(15);
+    return tables + pad4(max_region) * 3 * e;
+}
+
+int64_t r_smem_bytes(int k, int64_t max_halo, int e) {
+    int64_t W = int64_t(1) << k, WW = W * W;
+    int64_t tables = 8 * (WW + 1) + 16;  // toff, hoff, mbarrier
+    tables = (tables + 31) & ~int64_t(31);
+    return tables + max_halo * 3 * e;
+}
+
+void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (d.struct_size != sizeof(p2p_plan_desc)) fail(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
+    if (d.kernel != P2P_KERNEL_LAPLACE_2D) fail(P2P_ERROR_NOT_SUPPORTED, "only P2P_KERNEL_LAPLACE_2D");
+    if (d.layout != P2P_LAYOUT_NONREDUNDANT && d.layout != P2P_LAYOUT_REDUNDANT)
+        fail(P2P_ERROR_INVALID_ARGUMENT, "bad layout");
+    if (d.precision != P2P_FP32 && d.precision != P2P_FP64) fail(P2P_ERROR_INVALID_ARGUMENT, "bad precision");
+    if (!(d.epsilon > 0.0) || !std::isfinite(d.epsilon)) fail(P2P_ERROR_INVALID_ARGUMENT, "epsilon must be > 0");
+    if (d.part_world < 1 || d.part_rank < 0 || d.part_rank >= d.part_world)
+        fail(P2P_ERROR_INVALID_ARGUMENT, "bad part_world / part_rank");
+    validate_points(d.src_xy, d.n_src, "sources");
+    validate_points(d.tgt_xy, d.n_tgt, "targets");
+    if (d.n_src > INT32_MAX - 8 || d.n_tgt > INT32_MAX - 8)
+        fail(P2P_ERROR_NOT_SUPPORTED, "more than 2^31 points per set");
+
+    hp.layout = d.layout;
+    hp.precision = d.precision;
+    hp.device = d.device;
+    hp.eps = d.epsilon;
+    hp.part_world = d.part_world;
+    hp.part_rank = d.part_rank;
+    hp.n_src = d.n_src;
+    hp.n_tgt = d.n_tgt;
+
+    // ---- a1 level
+    int L = d.level > 0 ? d.level : ct_loop_level(d);
+    L += d.level_delta;
+    if (L < 1) fail(P2P_ERROR_INVALID_ARGUMENT, "L + level_delta < 1 (SPEC.md L85)");
+    if (L > kMaxLevel) fail(P2P_ERROR_NOT_SUPPORTED, "L > 15 (full-grid CSR offsets; see DESIGN.md)");
+    hp.L = L;
+    hp.S = int64_t(1) << (L - 1);
+    hp.B = hp.S * hp.S;
+    hp.h = 1.0 / (double)hp.S;
+
+    // ---- a2, a3
+    csr_sort(d.src_xy, d.n_src, hp, hp.src_off_g, hp.src_perm_g);
+    csr_sort(d.tgt_xy, d.n_tgt, hp, hp.tgt_off_g, hp.tgt_perm_g);
+    const int32_t *so = hp.src_off_g.data(), *to = hp.tgt_off_g.data();
+    auto ns = [&](int64_t b) -> int64_t { return so[b + 1] - so[b]; };
+    auto ntg = [&](int64_t b) -> int64_t { return to[b + 1] - to[b]; };
+
+    for (int64_t b = 0; b < hp.B; ++b) {
+        int64_t a = ns(b), t = ntg(b);
+        hp.occ_src += a > 0;
+        hp.occ_tgt += t > 0;
+        hp.t_max = std::max(hp.t_max, std::max(a, t));
+    }
+    hp.density = (double)hp.n_tgt / (double)hp.B;
+    hp.density_occ = hp.occ_tgt ? (double)hp.n_tgt / (double)hp.occ_tgt : 0.0;
+
+    // E1 source count of every target-occupied box (3x3, clipped).
+    std::vector<int32_t> n9((size_t)hp.B, 0);
+    const int64_t S = hp.S;
+    parallel_for(hp.B, [&](int64_t a, int64_t bnd) {
+        for (int64_t b = a; b < bnd; ++b) {
+            if (ntg(b) == 0) continue;
+            uint32_t ix, iy;
+            morton_decode((uint32_t)b, ix, iy);
+            int64_t c = 0;
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    int64_t x = (int64_t)ix + dx, y = (int64_t)iy + dy;
+                    if (x < 0 || y < 0 || x >= S || y >= S) continue;
+                    c += ns(morton_encode((uint32_t)x, (uint32_t)y));
+                }
+            n9[b] = (int32_t)c;
+        }
+    });
+
+    // ---- CTA tiles: Morton-aligned 2^k x 2^k blocks = contiguous Morton ranges.
+    const int e = d.precision == P2P_FP32 ? 4 : 8;
+    int kmax = std::min(L - 1, kMaxTileLog2);
+    int k;
+    if (d.tile_log2 >= 0) {
+        k = std::min(d.tile_log2, kmax);
+    } else {
+        double dd = std::max(hp.density_occ, 1e-3);
+        k = (int)std::lround(std::log(256.0 / dd) / std::log(4.0));
+        k = std::max(0, std::min(k, kmax));
+    }
+    for (;; --k) {
+        const int64_t W = int64_t(1) << k, WW = W * W, R = W + 2;
+        const int64_t ntile_all = hp.B / WW;
+        const int64_t side_t = S / W;
+        (void)side_t;
+        hp.tiles_g.clear();
+        for (int64_t t = 0; t < ntile_all; ++t)
+            if (to[(t + 1) * WW] > to[t * WW]) hp.tiles_g.push_back((int32_t)t);
+        const int64_t nt = (int64_t)hp.tiles_g.size();
+        hp.tile_pairs_g.assign((size_t)nt, 0);
+        std::vector<int64_t> region((size_t)nt, 0), halo((size_t)nt, 0);
+        parallel_for(nt, [&](int64_t a, int64_t bnd) {
+            for (int64_t i = a; i < bnd; ++i) {
+                int64_t t = hp.tiles_g[i];
+                int64_t pr = 0, hl = 0;
+                for (int64_t b = t * WW; b < (t + 1) * WW; ++b) {
+                    int64_t c = ntg(b);
+                    if (!c) continue;
+                    pr += c * (int64_t)n9[b];
+                    hl += pad2(n9[b]);
+                }
+                uint32_t tx, ty;
+                morton_decode((uint32_t)t, tx, ty);
+                int64_t X0 = (int64_t)tx * W - 1, Y0 = (int64_t)ty * W - 1, rg = 0;
+                for (int64_t ly = 0; ly < R; ++ly)
+                    for (int64_t lx = 0; lx < R; ++lx) {
+                        int64_t x = X0 + lx, y = Y0 + ly;
+                        if (x < 0 || y < 0 || x >= S || y >= S) continue;
+                        rg += pad2(ns(morton_encode((uint32_t)x, (uint32_t)y)));
+                    }
+                hp.tile_pairs_g[i] = pr;
+                region[i] = rg;
+                halo[i] = pad4(hl);
+            }
+        }, 256);
+        hp.max_region = region.empty() ? 0 : *std::max_element(region.begin(), region.end());
+        hp.max_tile_halo = halo.empty() ? 0 : *std::max_element(halo.begin(), halo.end());
+        int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? nr_smem_bytes(k, hp.max_region, e)
+                                                          : r_smem_bytes(k, hp.max_tile_halo, e);
+        hp.smem_bytes = smem;
+        if (smem <= kSmemLimit) break;
+        if (k == 0 || d.tile_log2 >= 0)
+            fail(P2P_ERROR_NOT_SUPPORTED,
+                 "a tile's near-field sources need " + std::to_string(smem) +
+                     " B of shared memory (> 200 KB); use a deeper level (CT loop) -- see DESIGN.md");
+    }
+    hp.k = k;
+    const int64_t W = int64_t(1) << k, WW = W * W, R = W + 2;
+    const int64_t ntiles = (int64_t)hp.tiles_g.size();
+    hp.pairs_global = 0;
+    for (int64_t p : hp.tile_pairs_g) hp.pairs_global += p;
+
+    // ---- partition: contiguous Morton ranges of tiles balanced by pair count.
+    const int P = d.part_world, r = d.part_rank;
+    {
+        std::vector<int64_t> prefix((size_t)ntiles + 1, 0);
+        for (int64_t i = 0; i < ntiles; ++i) prefix[i + 1] = prefix[i] + hp.tile_pairs_g[i];
+        hp.part_tile.assign((size_t)P + 1, 0);
+        hp.part_tile[P] = ntiles;
+        for (int q = 1; q < P; ++q) {
+            // first tile index j with prefix[j] * P >= q * total
+            int64_t lo = 0, hi = ntiles;
+            while (lo < hi) {
+                int64_t mid = (lo + hi) / 2;
+                if ((__int128)prefix[mid] * P >= (__int128)q * hp.pairs_global) hi = mid;
+                else lo = mid + 1;
+            }
+            hp.part_tile[q] = std::max<int64_t>(lo, hp.part_tile[q - 1]);
+        }
+        std::vector<int64_t> box_begin((size_t)P + 1);
+        for (int q = 0; q <= P; ++q) {
+            if (q == 0) box_begin[q] = 0;
+            else if (q == P || hp.part_tile[q] >= ntiles) box_begin[q] = hp.B;
+            else box_begin[q] = (int64_t)hp.tiles_g[hp.part_tile[q]] * WW;
+        }
+        hp.part_src.resize((size_t)P + 1);
+        hp.part_tgt.resize((size_t)P + 1);
+        for (int q = 0; q <= P; ++q) {
+            hp.part_src[q] = so[box_begin[q]];
+            hp.part_tgt[q] = to[box_begin[q]];
+        }
+        hp.tiles.assign(hp.tiles_g.begin() + hp.part_tile[r], hp.tiles_g.begin() + hp.part_tile[r + 1]);
+        hp.pairs = prefix[hp.part_tile[r + 1]] - prefix[hp.part_tile[r]];
+    }
+    hp.boxes_in_tiles = (int64_t)hp.tiles.size() * WW;
+
+    // Region boxes (tile + ring) of a tile, as Morton codes inside the grid.
+    auto region_boxes = [&](int64_t t, std::vector<uint32_t> &out) {
+        uint32_t tx, ty;
+        morton_decode((uint32_t)t, tx, ty);
+        int64_t X0 = (int64_t)tx * W - 1, Y0 = (int64_t)ty * W - 1;
+        for (int64_t ly = 0; ly < R; ++ly)
+            for (int64_t lx = 0; lx < R; ++lx) {
+                int64_t x = X0 + lx, y = Y0 + ly;
+                if (x < 0 || y < 0 || x >= S || y >= S) continue;
+                out.push_back(morton_encode((uint32_t)x, (uint32_t)y));
+            }
+    };
+
+    // ---- local source set: all sources (P = 1) or those in the regions of the owned tiles.
+    hp.src_owned_begin = hp.part_src[r];
+    hp.n_src_owned = hp.part_src[r + 1] - hp.part_src[r];
+    hp.tgt_begin = hp.part_tgt[r];
+    hp.n_tgt_local = hp.part_tgt[r + 1] - hp.part_tgt[r];
+    if (P == 1) {
+        hp.src_off = hp.src_off_g;
+        hp.n_src_local = hp.n_src;
+        hp.src_gidx.resize((size_t)hp.n_src);
+        std::iota(hp.src_gidx.begin(), hp.src_gidx.end(), 0);
+    } else {
+        std::vector<uint8_t> mark((size_t)hp.B, 0);
+        std::vector<uint32_t> boxes;
+        for (int32_t t : hp.tiles) {
+            boxes.clear();
+            region_boxes(t, boxes);
+            for (uint32_t m : boxes) mark[m] = 1;
+        }
+        hp.src_off.assign((size_t)hp.B + 1, 0);
+        hp.src_gidx.clear();
+        for (int64_t b = 0; b < hp.B; ++b) {
+            if (mark[b])
+                for (int32_t g = so[b]; g < so[b + 1]; ++g) hp.src_gidx.push_back(g);
+            hp.src_off[b + 1] = (int32_t)hp.src_gidx.size();
+        }
+        hp.n_src_local = (int64_t)hp.src_gidx.size();
+    }
+    hp.src_uidx.resize((size_t)hp.n_src_local);
+    for (int64_t i = 0; i < hp.n_src_local; ++i) hp.src_uidx[i] = hp.src_perm_g[hp.src_gidx[i]];
+
+    hp.tgt_off.resize((size_t)hp.B + 1);
+    for (int64_t b = 0; b <= hp.B; ++b)
+        hp.tgt_off[b] = (int32_t)std::min<int64_t>(std::max<int64_t>(to[b] - hp.tgt_begin, 0), hp.n_tgt_local);
+    hp.tgt_uidx.assign(hp.tgt_perm_g.begin() + hp.tgt_begin, hp.tgt_perm_g.begin() + hp.tgt_begin + hp.n_tgt_local);
+
+    // ---- halo bookkeeping for the per-apply weight exchange (P > 1).
+    hp.recv_counts.assign((size_t)P, 0);
+    hp.send_counts.assign((size_t)P, 0);
+    hp.src_qidx.resize((size_t)hp.n_src_local);
+    {
+        int64_t halo = 0;
+        for (int64_t i = 0; i < hp.n_src_local; ++i) {
+            int64_t g = hp.src_gidx[i];
+            if (g >= hp.part_src[r] && g < hp.part_src[r + 1]) {
+                hp.src_qidx[i] = (int32_t)(g - hp.part_src[r]);
+            } else {
+                int owner = (int)(std::upper_bound(hp.part_src.begin(), hp.part_src.end(), g) - hp.part_src.begin()) - 1;
+                // empty partitions share a begin index; the owner is the last rank starting at or before g
+                hp.recv_counts[owner] += 1;
+                hp.src_qidx[i] = (int32_t)(hp.n_src_owned + halo++);
+            }
+        }
+        hp.n_halo = halo;
+    }
+    if (P > 1) {
+        std::vector<uint32_t> boxes;
+        const int64_t bb_lo = hp.part_src[r], bb_hi = hp.part_src[r + 1];
+        for (int q = 0; q < P; ++q) {
+            if (q == r) continue;
+            boxes.clear();
+            for (int64_t i = hp.part_tile[q]; i < hp.part_tile[q + 1]; ++i) region_boxes(hp.tiles_g[i], boxes);
+            std::sort(boxes.begin(), boxes.end());
+            boxes.erase(std::unique(boxes.begin(), boxes.end()), boxes.end());
+            for (uint32_t m : boxes)
+                for (int32_t g = so[m]; g < so[m + 1]; ++g)
+                    if (g >= bb_lo && g < bb_hi) {
+                        hp.send_idx.push_back((int32_t)(g - bb_lo));
+                        hp.send_counts[q] += 1;
+                    }
+        }
+        hp.n_send = (int64_t)hp.send_idx.size();
+    }
+
+    // ---- a5 NR layout: box-local coordinates u = x - ix*h (exact in fp64 by Sterbenz).
+    auto fill_points = [&](auto &vec, const double *xy, const std::vector<int32_t> &uidx) {
+        int64_t n = (int64_t)uidx.size();
+        vec.resize((size_t)(2 * n));
+        parallel_for(n, [&](int64_t a, int64_t bnd) {
+            for (int64_t i = a; i < bnd; ++i) {
+                double x = xy[2 * (int64_t)uidx[i]], y = xy[2 * (int64_t)uidx[i] + 1];
+                vec[2 * i] = (typename std::decay_t<decltype(vec)>::value_type)(x - cell_of(x, S) * hp.h);
+                vec[2 * i + 1] = (typename std::decay_t<decltype(vec)>::value_type)(y - cell_of(y, S) * hp.h);
+            }
+        });
+    };
+    if (d.precision == P2P_FP32) {
+        fill_points(hp.f32.src_uv, d.src_xy, hp.src_uidx);
+        fill_points(hp.f32.tgt_uv, d.tgt_xy, hp.tgt_uidx);
+    } else {
+        fill_points(hp.f64.src_uv, d.src_xy, hp.src_uidx);
+        fill_points(hp.f64.tgt_uv, d.tgt_xy, hp.tgt_uidx);
+    }
+
+    // ---- a5 R layout: per target box, its E1 sources packed contiguously in
+    // the 3x3 row order (dy outer, dx inner), coordinates relative to the
+    // target box origin, each box padded to an even count, each tile to 4.
+    if (d.layout == P2P_LAYOUT_REDUNDANT) {
+        const int64_t nlt = (int64_t)hp.tiles.size();
+        std::vector<uint32_t> len((size_t)hp.B + 1, 0);
+        for (int64_t i = 0; i < nlt; ++i) {
+            int64_t t = hp.tiles[i], tot = 0;
+            for (int64_t b = t * WW; b < (t + 1) * WW; ++b)
+                if (ntg(b)) {
+                    len[b] = (uint32_t)pad2(n9[b]);
+                    tot += len[b];
+                }
+            len[(t + 1) * WW - 1] += (uint32_t)(pad4(tot) - tot);
+        }
+        hp.halo_off.assign((size_t)hp.B + 1, 0);
+        for (int64_t b = 0; b < hp.B; ++b) hp.halo_off[b + 1] = hp.halo_off[b] + len[b];
+        hp.halo_entries = hp.halo_off[hp.B];
+        if (hp.halo_entries > (int64_t)UINT32_MAX - 8) fail(P2P_ERROR_NOT_SUPPORTED, "R halo exceeds 2^32 entries");
+        hp.halo_idx.assign((size_t)hp.halo_entries, -1);
+        const double PADC = 1.0e4;
+        const bool f32 = d.precision == P2P_FP32;
+        if (f32) hp.f32.halo_uv.assign((size_t)hp.halo_entries * 2, (float)PADC);
+        else hp.f64.halo_uv.assign((size_t)hp.halo_entries * 2, PADC);
+        const double *sxy = d.src_xy;
+        parallel_for(nlt, [&](int64_t a, int64_t bnd) {
+            for (int64_t i = a; i < bnd; ++i) {
+                int64_t t = hp.tiles[i];
+                for (int64_t b = t * WW; b < (t + 1) * WW; ++b) {
+                    if (!ntg(b)) continue;
+                    uint32_t ix, iy;
+                    morton_decode((uint32_t)b, ix, iy);
+                    double ox = ix * hp.h, oy = iy * hp.h;
+                    int64_t ent = hp.halo_off[b];
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            int64_t x = (int64_t)ix + dx, y = (int64_t)iy + dy;
+                            if (x < 0 || y < 0 || x >= S || y >= S) continue;
+                            uint32_t m = morton_encode((uint32_t)x, (uint32_t)y);
+                            for (int32_t j = hp.src_off[m]; j < hp.src_off[m + 1]; ++j, ++ent) {
+                                int64_t u = hp.src_uidx[j];
+                                double rx = sxy[2 * u] - ox, ry = sxy[2 * u + 1] - oy;
+                                hp.halo_idx[ent] = j;
+                                if (f32) {  // (u0,u1,v0,v1) per source pair
+                                    int64_t p = ent >> 1, s = ent & 1;
+                                    hp.f32.halo_uv[4 * p + s] = (float)rx;
+                                    hp.f32.halo_uv[4 * p + 2 + s] = (float)ry;
+                                } else {
+                                    hp.f64.halo_uv[2 * ent] = rx;
+                                    hp.f64.halo_uv[2 * ent + 1] = ry;
+                                }
+                            }
+                        }
+                }
+            }
+        }, 64);
+    }
+    hp.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+std::vector<int64_t> neighbors_export(const HostPlan &hp) {
+    std::vector<int64_t> nb((size_t)hp.B * 9, -1);
+    for (int64_t b = 0; b < hp.B; ++b) {
+        uint32_t ix, iy;
+        morton_decode((uint32_t)b, ix, iy);
+        int64_t list[9];
+        int c = 0;
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                int64_t x = (int64_t)ix + dx, y = (int64_t)iy + dy;
+                if (x < 0 || y < 0 || x >= hp.S || y >= hp.S) continue;
+                list[c++] = morton_encode((uint32_t)x, (uint32_t)y);
+            }
+        std::sort(list, list + c);
+        std::copy(list, list + c, nb.begin() + 9 * b);
+    }
+    return nb;
+}
+
+}  // namespace p2p

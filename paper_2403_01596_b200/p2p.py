@@ -1,0 +1,296 @@
+"""Thin ctypes binding of the C ABI in include/p2p.h.
+
+Argument marshalling only: every step of plan building runs in the C++ host
+builder and every step of apply runs in the sm_100a kernels of
+libp2p_b200.so.  There is no CPU fallback: if the library is missing the
+import fails loudly, and applying a host-only plan raises P2PError.
+
+The function names mirror the C ABI (p2p_plan_create, p2p_apply, ...); the
+`Plan` class is a convenience wrapper that takes numpy points and torch
+device tensors.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libp2p_b200.so")
+
+P2P_SUCCESS = 0
+P2P_ERROR_INVALID_ARGUMENT = 1
+P2P_ERROR_CONSTRUCTION_FAILURE = 2
+P2P_ERROR_LAYOUT_CORRUPT = 3
+P2P_ERROR_OUT_OF_MEMORY = 4
+P2P_ERROR_CUDA = 5
+P2P_ERROR_NOT_SUPPORTED = 6
+P2P_ERROR_NO_DEVICE = 7
+
+P2P_KERNEL_LAPLACE_2D = 0
+P2P_LAYOUT_NONREDUNDANT = 0
+P2P_LAYOUT_REDUNDANT = 1
+P2P_FP64 = 0
+P2P_FP32 = 1
+P2P_ORDER_PLAN = 0
+P2P_ORDER_USER = 1
+
+EXPORT = {
+    "src_perm": 0, "tgt_perm": 1, "src_box_offsets": 2, "tgt_box_offsets": 3,
+    "neighbors": 4, "partition": 5, "src_global": 6, "halo_counts": 7, "tiles": 8,
+    "halo_index": 9, "send_index": 10, "halo_offsets": 11,
+}
+
+# Symbols declared in include/p2p.h (checked by tests/test_abi.py).
+ABI_SYMBOLS = (
+    "p2p_plan_desc_init", "p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_dist",
+    "p2p_halo_pack", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
+    "p2p_status_string", "p2p_last_error", "p2p_abi_version",
+)
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [
+        ("struct_size", C.c_uint32), ("abi_version", C.c_int32),
+        ("n_src", C.c_int64), ("n_tgt", C.c_int64),
+        ("src_xy", C.c_void_p), ("tgt_xy", C.c_void_p),
+        ("level", C.c_int32), ("ct", C.c_int32), ("l_start", C.c_int32), ("l_max", C.c_int32),
+        ("level_delta", C.c_int32), ("kernel", C.c_int32), ("epsilon", C.c_double),
+        ("layout", C.c_int32), ("precision", C.c_int32), ("device", C.c_int32),
+        ("tile_log2", C.c_int32), ("stream", C.c_void_p),
+        ("part_world", C.c_int32), ("part_rank", C.c_int32),
+    ]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("struct_size", C.c_uint32),
+        ("level", C.c_int32), ("tile_log2", C.c_int32), ("layout", C.c_int32), ("precision", C.c_int32),
+        ("device", C.c_int32), ("part_world", C.c_int32), ("part_rank", C.c_int32),
+        ("side", C.c_int64), ("boxes", C.c_int64), ("n_src", C.c_int64), ("n_tgt", C.c_int64),
+        ("n_src_local", C.c_int64), ("n_tgt_local", C.c_int64), ("n_src_owned", C.c_int64),
+        ("src_owned_begin", C.c_int64), ("tgt_begin", C.c_int64), ("n_halo", C.c_int64),
+        ("n_send", C.c_int64), ("occupied_src_boxes", C.c_int64), ("occupied_tgt_boxes", C.c_int64),
+        ("t_max", C.c_int64), ("density", C.c_double), ("density_occupied", C.c_double),
+        ("pairs", C.c_int64), ("pairs_global", C.c_int64), ("tiles", C.c_int64),
+        ("smem_bytes", C.c_int64), ("halo_entries", C.c_int64), ("alg_bytes_kernel", C.c_int64),
+        ("alg_bytes_apply", C.c_int64), ("device_bytes", C.c_int64), ("build_seconds", C.c_double),
+        ("upload_seconds", C.c_double),
+    ]
+
+
+class P2PError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        self.status = status
+        super().__init__(f"{where}: {_status_name(status)}: {detail}")
+
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """Load libp2p_b200.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    lib.p2p_plan_desc_init.argtypes = [C.POINTER(PlanDesc)]
+    lib.p2p_plan_desc_init.restype = None
+    lib.p2p_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(P)]
+    lib.p2p_apply.argtypes = [P, P, P, i32, i32, P]
+    lib.p2p_apply_host.argtypes = [P, P, P, i32, i32, P]
+    lib.p2p_apply_dist.argtypes = [P, P, P, P, i32, P]
+    lib.p2p_halo_pack.argtypes = [P, P, P, P]
+    lib.p2p_destroy.argtypes = [P]
+    lib.p2p_plan_get_info.argtypes = [P, C.POINTER(PlanInfo)]
+    lib.p2p_plan_export.argtypes = [P, i32, P, C.POINTER(C.c_size_t)]
+    lib.p2p_status_string.argtypes = [i32]
+    lib.p2p_status_string.restype = C.c_char_p
+    lib.p2p_last_error.restype = C.c_char_p
+    lib.p2p_abi_version.restype = i32
+    for name in ("p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_dist", "p2p_halo_pack",
+                 "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export"):
+        getattr(lib, name).restype = i32
+    _lib = lib
+    return lib
+
+
+def _status_name(s: int) -> str:
+    try:
+        return load_library().p2p_status_string(s).decode()
+    except Exception:
+        return str(s)
+
+
+def _check(status: int, where: str):
+    if status != P2P_SUCCESS:
+        raise P2PError(status, where, load_library().p2p_last_error().decode())
+
+
+# ------------------------------------------------------------- C-ABI mirror
+def p2p_plan_desc_init() -> PlanDesc:
+    d = PlanDesc()
+    load_library().p2p_plan_desc_init(C.byref(d))
+    return d
+
+
+def p2p_plan_create(desc: PlanDesc) -> C.c_void_p:
+    h = C.c_void_p()
+    _check(load_library().p2p_plan_create(C.byref(desc), C.byref(h)), "p2p_plan_create")
+    return h
+
+
+def p2p_apply(plan, d_q: int, d_out: int, order: int = P2P_ORDER_PLAN, accumulate: int = 0, stream: int = 0):
+    _check(load_library().p2p_apply(plan, d_q, d_out, order, accumulate, stream or None), "p2p_apply")
+
+
+def p2p_apply_host(plan, h_q: int, h_out: int, order: int = P2P_ORDER_PLAN, accumulate: int = 0, stream: int = 0):
+    _check(load_library().p2p_apply_host(plan, h_q, h_out, order, accumulate, stream or None), "p2p_apply_host")
+
+
+def p2p_apply_dist(plan, d_q_owned: int, d_q_halo: int, d_out: int, accumulate: int = 0, stream: int = 0):
+    _check(load_library().p2p_apply_dist(plan, d_q_owned or None, d_q_halo or None, d_out, accumulate,
+                                         stream or None), "p2p_apply_dist")
+
+
+def p2p_halo_pack(plan, d_q_owned: int, d_send: int, stream: int = 0):
+    _check(load_library().p2p_halo_pack(plan, d_q_owned or None, d_send or None, stream or None), "p2p_halo_pack")
+
+
+def p2p_destroy(plan):
+    _check(load_library().p2p_destroy(plan), "p2p_destroy")
+
+
+def p2p_plan_get_info(plan) -> dict:
+    info = PlanInfo()
+    _check(load_library().p2p_plan_get_info(plan, C.byref(info)), "p2p_plan_get_info")
+    return {name: getattr(info, name) for name, _ in PlanInfo._fields_ if name != "struct_size"}
+
+
+def p2p_plan_export(plan, kind) -> np.ndarray:
+    k = EXPORT[kind] if isinstance(kind, str) else int(kind)
+    nbytes = C.c_size_t(0)
+    lib = load_library()
+    _check(lib.p2p_plan_export(plan, k, None, C.byref(nbytes)), "p2p_plan_export")
+    out = np.empty(nbytes.value // 8, dtype=np.int64)
+    if out.size:
+        _check(lib.p2p_plan_export(plan, k, out.ctypes.data_as(C.c_void_p), C.byref(nbytes)), "p2p_plan_export")
+    return out
+
+
+# ------------------------------------------------------------- convenience
+class Plan:
+    """A P2P plan: ``Plan(src_xy, tgt_xy, level=...)`` then ``plan.apply(q, out)``.
+
+    src_xy / tgt_xy: numpy float64 [n, 2] in [0,1]^2 (copied by the library).
+    layout: "nr" (non-redundant) or "r" (redundant); precision: "fp32" or "fp64".
+    device: CUDA ordinal, or -1 for a host-only plan (build + export only).
+    """
+
+    def __init__(self, src_xy, tgt_xy=None, *, level: int = 0, ct: int = 15, l_start: int = 3,
+                 l_max: int = 15, level_delta: int = 0, epsilon: float = 1e-12, layout: str = "nr",
+                 precision: str = "fp32", device: int = 0, tile_log2: int = -1, stream: int = 0,
+                 part_world: int = 1, part_rank: int = 0):
+        self._src = np.ascontiguousarray(src_xy, dtype=np.float64)
+        self._tgt = self._src if tgt_xy is None else np.ascontiguousarray(tgt_xy, dtype=np.float64)
+        if self._src.ndim != 2 or self._src.shape[1] != 2 or self._tgt.ndim != 2 or self._tgt.shape[1] != 2:
+            raise ValueError("points must be [n, 2] arrays")
+        d = p2p_plan_desc_init()
+        d.n_src, d.n_tgt = len(self._src), len(self._tgt)
+        d.src_xy = self._src.ctypes.data
+        d.tgt_xy = self._tgt.ctypes.data
+        d.level, d.ct, d.l_start, d.l_max, d.level_delta = level, ct, l_start, l_max, level_delta
+        d.epsilon = epsilon
+        d.layout = {"nr": P2P_LAYOUT_NONREDUNDANT, "r": P2P_LAYOUT_REDUNDANT}[layout]
+        d.precision = {"fp32": P2P_FP32, "fp64": P2P_FP64}[precision]
+        d.device, d.tile_log2, d.stream = device, tile_log2, stream or None
+        d.part_world, d.part_rank = part_world, part_rank
+        self.layout, self.precision, self.device = layout, precision, device
+        self._h = p2p_plan_create(d)
+        self.info = p2p_plan_get_info(self._h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def torch_dtype(self):
+        import torch
+        return torch.float32 if self.precision == "fp32" else torch.float64
+
+    @property
+    def np_dtype(self):
+        return np.float32 if self.precision == "fp32" else np.float64
+
+    def export(self, kind) -> np.ndarray:
+        return p2p_plan_export(self._h, kind)
+
+    def _stream(self, stream):
+        if stream is not None:
+            return int(stream)
+        import torch
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _check_tensor(self, t, n, name):
+        import torch
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != self.torch_dtype or not t.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous CUDA {self.torch_dtype} tensor")
+        if t.numel() != n:
+            raise ValueError(f"{name} has {t.numel()} elements, expected {n}")
+
+    def apply(self, q, out=None, *, order: str = "plan", accumulate: bool = False, stream=None):
+        """phi = A q on the device (asynchronous on the current torch stream)."""
+        import torch
+        o = P2P_ORDER_USER if order == "user" else P2P_ORDER_PLAN
+        n_out = self.info["n_tgt"] if o == P2P_ORDER_USER else self.info["n_tgt_local"]
+        self._check_tensor(q, self.info["n_src"], "q")
+        if out is None:
+            out = torch.zeros(n_out, dtype=self.torch_dtype, device=q.device)
+        self._check_tensor(out, n_out, "out")
+        p2p_apply(self._h, q.data_ptr(), out.data_ptr(), o, int(accumulate), self._stream(stream))
+        return out
+
+    def apply_host(self, q: np.ndarray, out: np.ndarray | None = None, *, order: str = "plan",
+                   accumulate: bool = False, stream=None) -> np.ndarray:
+        """phi = A q from/to host buffers (H2D, apply, D2H, synchronise)."""
+        o = P2P_ORDER_USER if order == "user" else P2P_ORDER_PLAN
+        n_out = self.info["n_tgt"] if o == P2P_ORDER_USER else self.info["n_tgt_local"]
+        if q.dtype != self.np_dtype or q.size != self.info["n_src"] or not q.flags.c_contiguous:
+            raise TypeError("q: wrong dtype/size/layout")
+        if out is None:
+            out = np.zeros(n_out, dtype=self.np_dtype)
+        p2p_apply_host(self._h, q.ctypes.data, out.ctypes.data, o, int(accumulate), self._stream(stream))
+        return out
+
+    def apply_dist(self, q_owned, q_halo, out, *, accumulate: bool = False, stream=None):
+        self._check_tensor(out, self.info["n_tgt_local"], "out")
+        p2p_apply_dist(self._h, q_owned.data_ptr() if q_owned.numel() else 0,
+                       q_halo.data_ptr() if q_halo.numel() else 0, out.data_ptr(), int(accumulate),
+                       self._stream(stream))
+        return out
+
+    def halo_pack(self, q_owned, send, stream=None):
+        p2p_halo_pack(self._h, q_owned.data_ptr() if q_owned.numel() else 0,
+                      send.data_ptr() if send.numel() else 0, self._stream(stream))
+        return send
+
+    def close(self):
+        if getattr(self, "_h", None):
+            p2p_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -1,0 +1,144 @@
+"""Host plan builder vs the oracle's independent indexing (bit-exact), on
+host-only plans (device = -1): no GPU needed.
+
+SURVEY.md §8(c) C-2 step 5: the oracle computes Morton codes by a bit loop and
+sorts by (code, index) with qsort; the plan builder uses magic-number bit
+spreading and a counting sort.  Permutations, box offsets and neighbour lists
+must agree bit for bit."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2403_01596_b200 import p2p
+from paper_2403_01596_b200 import workloads as W
+
+
+def _plan(src, tgt, **kw):
+    kw.setdefault("device", -1)
+    return p2p.Plan(src, tgt, **kw)
+
+
+@pytest.mark.parametrize("cfg,kind,level", [
+    ("tiny", "iid", 4), ("tiny", "stratified", 4), ("tiny", "iid", 6), ("tiny", "iid", 1),
+])
+def test_indexing_bit_exact(cfg, kind, level):
+    src, tgt, _ = W.make_problem(cfg, kind=kind)
+    pl = _plan(src, tgt, level=level)
+    for xy, perm_kind, off_kind in ((src, "src_perm", "src_box_offsets"), (tgt, "tgt_perm", "tgt_box_offsets")):
+        perm, off = oracle.sort_points(xy, level)
+        np.testing.assert_array_equal(pl.export(perm_kind), perm)
+        np.testing.assert_array_equal(pl.export(off_kind), off)
+    np.testing.assert_array_equal(pl.export("neighbors").reshape(-1, 9), oracle.neighbors(level))
+
+
+def test_indexing_bit_exact_random_unit():
+    src, tgt, _ = W.uniform_unit(3000, 17)
+    for level in (2, 5, 7):
+        pl = _plan(src, tgt, level=level)
+        perm, off = oracle.sort_points(src, level)
+        np.testing.assert_array_equal(pl.export("src_perm"), perm)
+        np.testing.assert_array_equal(pl.export("src_box_offsets"), off)
+
+
+def test_duplicates_and_edges_bit_exact():
+    # points on cell edges, at x = 1, and exact duplicates exercise the boundary rule and stability
+    pts = np.array([[0.0, 0.0], [1.0, 1.0], [0.5, 0.5], [0.5, 0.5], [0.25, 1.0], [1.0, 0.0],
+                    [0.125, 0.375], [0.5, 0.5], [np.nextafter(0.5, 0), 0.5]])
+    for level in (1, 2, 3, 4):
+        pl = _plan(pts, pts, level=level)
+        perm, off = oracle.sort_points(pts, level)
+        np.testing.assert_array_equal(pl.export("src_perm"), perm)
+        np.testing.assert_array_equal(pl.export("tgt_box_offsets"), off)
+
+
+@pytest.mark.parametrize("seed,n", [(1, 1000), (2, 5000), (3, 20000)])
+def test_ct_loop_matches_oracle(seed, n):
+    src, tgt, _ = W.uniform_unit(n, seed)
+    for ct in (4, 15):
+        L = oracle.ct_level(src, tgt, ct, 3, 15)
+        assert _plan(src, tgt, ct=ct).info["level"] == L
+        assert _plan(src, tgt, ct=ct, level_delta=1).info["level"] == L + 1
+
+
+def test_spec_stats():
+    one = np.array([[0.3, 0.3]])
+    info = _plan(one, one, ct=15).info
+    assert info["level"] == 3 and info["boxes"] == 16
+    src, tgt, _ = W.uniform_unit(4096, 3)
+    info = _plan(src, tgt, level=6).info
+    assert info["density"] == 4.0
+    assert info["density"] * info["boxes"] == 4096
+
+
+@pytest.mark.parametrize("cfg,kind", [("tiny", "iid"), ("tiny", "stratified"), ("d64_1e6", None)])
+def test_pair_count(cfg, kind):
+    c = W.CONFIGS[cfg]
+    if kind is None:  # a smaller stratified plate at the d64 level
+        c = W.PlateConfig("s", 40, 23, c.level, 40 * 23 * 64, seed=5)
+        kind = "stratified"
+    src, tgt, _ = W.make_problem(c, kind=kind)
+    info = _plan(src, tgt, level=c.level).info
+    assert info["pairs"] == info["pairs_global"] == oracle.pair_count(src, tgt, c.level)
+    if kind == "stratified":
+        assert info["pairs"] == c.stratified_pairs()
+
+
+def _e1_sources(src, tgt_point, level):
+    S = 1 << (level - 1)
+    bs = np.minimum(np.floor(src * S), S - 1)
+    bt = np.minimum(np.floor(tgt_point * S), S - 1)
+    return set(np.nonzero((np.abs(bs[:, 0] - bt[0]) <= 1) & (np.abs(bs[:, 1] - bt[1]) <= 1))[0].tolist())
+
+
+def test_redundant_halo_interaction_set():
+    """the pairs implied by the R layout equal the brute-force E1 enumeration."""
+    src, tgt, _ = W.uniform_unit(1500, 23)
+    level = 5
+    pl = _plan(src, tgt, level=level, layout="r")
+    hidx = pl.export("halo_index")
+    hoff = pl.export("halo_offsets")
+    sperm = pl.export("src_perm")
+    tperm = pl.export("tgt_perm")
+    toff = pl.export("tgt_box_offsets")
+    for b in range(len(toff) - 1):
+        if toff[b + 1] == toff[b]:
+            continue
+        ent = hidx[hoff[b]:hoff[b + 1]]
+        got = set(sperm[ent[ent >= 0]].tolist())
+        assert len(got) == (ent >= 0).sum()  # no duplicates
+        assert len(ent) % 2 == 0
+        for t in tperm[toff[b]:toff[b + 1]]:
+            assert got == _e1_sources(src, tgt[t], level)
+    info = pl.info
+    assert info["halo_entries"] >= info["pairs"] / 1e9  # trivial sanity
+    assert info["halo_entries"] % 4 == 0
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_partition_covers_everything(world):
+    src, tgt, _ = W.make_problem("d16_1e6", n=40000)
+    level = 7
+    plans = [_plan(src, tgt, level=level, part_world=world, part_rank=r) for r in range(world)]
+    infos = [p.info for p in plans]
+    part = plans[0].export("partition").reshape(2, world + 1)
+    for p in plans[1:]:
+        np.testing.assert_array_equal(p.export("partition").reshape(2, world + 1), part)
+    assert part[0, 0] == 0 and part[0, -1] == len(src) and part[1, -1] == len(tgt)
+    assert sum(i["pairs"] for i in infos) == infos[0]["pairs_global"]
+    assert sum(i["n_tgt_local"] for i in infos) == len(tgt)
+    # balance: no rank above 1/world + one tile's worth of pairs
+    assert max(i["pairs"] for i in infos) <= infos[0]["pairs_global"] / world * 1.2
+    # owned targets concatenate to the global plan order
+    full = _plan(src, tgt, level=level)
+    np.testing.assert_array_equal(np.concatenate([p.export("tgt_perm") for p in plans]), full.export("tgt_perm"))
+    # halo bookkeeping: what r receives from q is what q sends to r
+    counts = [p.export("halo_counts").reshape(2, world) for p in plans]
+    for r in range(world):
+        for q in range(world):
+            assert counts[r][0, q] == counts[q][1, r]
+    # each rank's local sources cover the E1 sources of every owned target
+    for p in plans:
+        loc = set(p.export("src_perm").tolist())
+        tp = p.export("tgt_perm")
+        for t in tp[:: max(1, len(tp) // 50)]:
+            assert _e1_sources(src, tgt[t], level) <= loc
