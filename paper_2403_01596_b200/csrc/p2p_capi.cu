@@ -44,7 +44,8 @@ struct p2p_plan_s {
     // device arrays
     DevBuf tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
-    DevBuf q_local, phi, io_q, io_out;  // workspace
+    DevBuf q_local, phi, io_q, io_out, queue;  // workspace
+    int grid = 0;                                // persistent CTAs per launch
     int64_t device_bytes = 0;
     double upload_seconds = 0.0;
     int elem = 4;
@@ -66,7 +67,7 @@ struct p2p_plan_s {
     void release() {
         DevBuf *all[] = {&tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q, &q_local, &phi,
-                         &io_q, &io_out};
+                         &io_q, &io_out, &queue};
         for (DevBuf *b : all) {
             if (b->p) cudaFree(b->p);
             b->p = nullptr;
@@ -107,14 +108,17 @@ void upload_plan(p2p_plan_s &P) {
         P.upload(P.halo_uv, lay.halo_uv);
         P.alloc(P.halo_q, (size_t)hp.halo_entries * sizeof(T));
     }
-    // The kernels' dynamic shared memory is fixed per plan: opt in once here, not per apply.
-    if (hp.smem_bytes > 48 * 1024) {
-        const int sm = (int)p2p::kSmemLimit;  // a permission, not a reservation: one value for all plans
-        if (hp.layout == P2P_LAYOUT_NONREDUNDANT)
-            ck(cudaFuncSetAttribute(p2p::dev::p2p_nr_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-        else
-            ck(cudaFuncSetAttribute(p2p::dev::p2p_r_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm), "smem attr");
-    }
+    // Dynamic shared memory is fixed per plan: opt in once (a permission, not a
+    // reservation, so one value serves all plans), then size the persistent grid.
+    const void *kfn = hp.layout == P2P_LAYOUT_NONREDUNDANT ? (const void *)p2p::dev::p2p_nr_kernel<T>
+                                                           : (const void *)p2p::dev::p2p_r_kernel<T>;
+    ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2p::kSmemLimit), "smem attr");
+    int occ = 0, dev = 0, sms = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, p2p::kThreads, (size_t)hp.smem_bytes), "occupancy");
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+    P.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)hp.tiles.size(), (int64_t)std::max(occ, 1) * sms));
+    P.alloc(P.queue, 16);
     P.alloc(P.q_local, (size_t)std::max<int64_t>(hp.n_src_local, 1) * sizeof(T));
     P.alloc(P.phi, (size_t)std::max<int64_t>(hp.n_tgt_local, 1) * sizeof(T));
     P.alloc(P.io_q, (size_t)std::max<int64_t>(hp.n_src, 1) * sizeof(T));
@@ -132,23 +136,35 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
     const p2p::HostPlan &hp = P.hp;
     const int ntiles = (int)hp.tiles.size();
     if (ntiles == 0) return;
-    const T eps2 = (T)(hp.eps * hp.eps);
+    p2p::dev::P2PArgs<T> a{};
+    a.tiles = (const int32_t *)P.tiles.p;
+    a.ntiles = ntiles;
+    a.queue = (int *)P.queue.p;
+    a.k = hp.k;
+    a.S = hp.S;
+    a.h = (T)hp.h;
+    a.eps2 = (T)(hp.eps * hp.eps);
+    a.src_cap = (int)hp.src_cap;
+    a.tgt_cap = (int)hp.tgt_cap;
+    a.group_log2 = hp.group_log2;
+    a.tgt_off = (const int32_t *)P.tgt_off.p;
+    a.tgt_uv = (const typename p2p::dev::V2<T>::type *)P.tgt_uv.p;
+    a.out = out;
+    a.accumulate = accumulate;
+    ck(cudaMemsetAsync(P.queue.p, 0, sizeof(int), s), "queue reset");
     if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
-        auto kern = p2p::dev::p2p_nr_kernel<T>;
-        const int max_region = (int)((hp.max_region + 3) & ~int64_t(3));
-        kern<<<ntiles, p2p::kThreads, hp.smem_bytes, s>>>(
-            (const int32_t *)P.tiles.p, hp.k, hp.S, (T)hp.h, eps2, max_region, (const int32_t *)P.src_off.p,
-            (const int32_t *)P.tgt_off.p, (const typename p2p::dev::V2<T>::type *)P.src_uv.p, q_local,
-            (const typename p2p::dev::V2<T>::type *)P.tgt_uv.p, out, accumulate);
+        a.src_off = (const int32_t *)P.src_off.p;
+        a.src_uv = (const typename p2p::dev::V2<T>::type *)P.src_uv.p;
+        a.q = q_local;
+        p2p::dev::p2p_nr_kernel<T><<<P.grid, p2p::kThreads, hp.smem_bytes, s>>>(a);
     } else {
         if (hp.halo_entries > 0)
             p2p::dev::pack_r_kernel<T><<<grid_for(hp.halo_entries), 256, 0, s>>>(
                 (const int32_t *)P.halo_idx.p, q_local, (T *)P.halo_q.p, hp.halo_entries);
-        auto kern = p2p::dev::p2p_r_kernel<T>;
-        kern<<<ntiles, p2p::kThreads, hp.smem_bytes, s>>>(
-            (const int32_t *)P.tiles.p, hp.k, eps2, (const int32_t *)P.tgt_off.p, (const uint32_t *)P.halo_off.p,
-            (const T *)P.halo_uv.p, (const T *)P.halo_q.p, (const typename p2p::dev::V2<T>::type *)P.tgt_uv.p,
-            out, accumulate);
+        a.halo_off = (const uint32_t *)P.halo_off.p;
+        a.halo_uv = (const T *)P.halo_uv.p;
+        a.q = (const T *)P.halo_q.p;
+        p2p::dev::p2p_r_kernel<T><<<P.grid, p2p::kThreads, hp.smem_bytes, s>>>(a);
     }
     ck(cudaGetLastError(), "kernel launch");
 }

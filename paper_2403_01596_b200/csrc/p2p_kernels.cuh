@@ -2,14 +2,15 @@
 //
 //   phi_t = sum_{s : box(s) in E1(box(t)), r >= eps} q_s ln(1/r)
 //
-// One CTA per non-empty Morton-aligned tile of 2^k x 2^k leaf boxes.  The
-// tile's targets are one contiguous Morton range; each thread owns one target
-// (held in registers) and sweeps the sources of its 3x3 box neighbourhood
-// from shared memory.  The neighbourhood is walked as three row-runs (boxes
-// x-1..x+1 of rows y-1, y, y+1): in the NR kernel the tile's region (tile +
-// one-box ring) is staged in row-major box order, so each row-run is one
-// contiguous shared-memory span; in the R kernel the halo of each target box
-// is one contiguous span already (packed at plan time, §3.3).
+// Work unit: a non-empty Morton-aligned tile of 2^k x 2^k leaf boxes (one
+// contiguous Morton range of targets).  Persistent CTAs pull tiles from a
+// queue.  The sources a tile needs are staged in shared memory; targets are
+// held in registers and sweep contiguous shared-memory spans.  The 3x3
+// neighbourhood is walked as three row-runs (boxes x-1..x+1 of rows y-1, y,
+// y+1): the NR kernel stages the tile's region (tile + one-box ring) in
+// row-major box order so each row-run is one contiguous span; the R kernel's
+// halo of each target box is one contiguous span already (packed at plan
+// time, §3.3).
 //
 // fp32 pair evaluation: coordinates are relative to the CTA
 // region (NR) or the target box (R) in global units, so
@@ -22,6 +23,8 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+
+#include "plan.h"
 
 namespace p2p {
 namespace dev {
@@ -76,56 +79,6 @@ __device__ __forceinline__ float lg2_approx(float x) {
     float r;
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
-}
-
-// ---------------------------------------------------------------- block scan
-// In-place exclusive scan of a[0..n) (n <= ~64 per thread), returns the total.
-__device__ __forceinline__ int block_exclusive_scan(int *a, int n, int *warp_tot) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int per = (n + kThreads - 1) / kThreads;
-    const int lo = min(n, tid * per), hi = min(n, lo + per);
-    int s = 0;
-    for (int i = lo; i < hi; ++i) s += a[i];
-    int incl = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    if (lane == 31) warp_tot[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        int v = lane < kThreads / 32 ? warp_tot[lane] : 0;
-        int w = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int x = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += x;
-        }
-        if (lane < kThreads / 32) warp_tot[lane] = w - v;  // exclusive warp prefix
-        if (lane == kThreads / 32 - 1) warp_tot[32] = w;   // grand total
-    }
-    __syncthreads();
-    int run = warp_tot[wid] + incl - s;
-    for (int i = lo; i < hi; ++i) {
-        int v = a[i];
-        a[i] = run;
-        run += v;
-    }
-    int total = warp_tot[32];
-    __syncthreads();
-    return total;
-}
-
-// Last index j in [0, n) with a[j] <= x (a non-decreasing, a[0] <= x < a[n]).
-__device__ __forceinline__ int seg_search(const int *a, int n, int x) {
-    int lo = 0, hi = n;
-    while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
-        if (a[mid] <= x) lo = mid;
-        else hi = mid;
-    }
-    return lo;
 }
 
 // ---------------------------------------------------------------- pair loops
@@ -184,132 +137,195 @@ template <typename T> struct V2;
 template <> struct V2<float> { using type = float2; };
 template <> struct V2<double> { using type = double2; };
 
+// ---------------------------------------------------------------- launch arguments
+template <typename T>
+struct P2PArgs {
+    const int32_t *tiles;  // Morton tile indices in queue order (LPT or Morton, chosen by the plan)
+    int ntiles;
+    int *queue;            // dynamic tile counter, zeroed before each launch
+    int k;                 // tile side = 2^k leaf boxes
+    int64_t S;             // grid side 2^(L-1)
+    T h, eps2;
+    int src_cap;           // NR: max padded region sources of a tile; R: max packed-halo entries of a tile
+    int tgt_cap;           // max targets of a tile (multiple of 4)
+    int group_log2;        // NR source staging: 2^group_log2 lanes per region box
+    const int32_t *src_off, *tgt_off;  // [B+1] CSR offsets (local plan order)
+    const typename V2<T>::type *src_uv, *tgt_uv;  // box-local coordinates
+    const T *q;            // NR: q in local plan order; R: packed halo q (from pack_r)
+    const uint32_t *halo_off;  // R: [B+1] packed-halo offsets
+    const T *halo_uv;      // R: packed-halo coordinates relative to the target box origin
+    T *out;
+    int accumulate;
+};
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += x;
+    }
+    return v;
+}
+
+// Next tile from the dynamic queue (one atomic per CTA per tile).
+__device__ __forceinline__ int next_tile(int *queue, int *s_tile) {
+    if (threadIdx.x == 0) *s_tile = atomicAdd(queue, 1);
+    __syncthreads();
+    return *s_tile;
+}
+
 // ---------------------------------------------------------------- NR kernel
-// Shared memory: int sstart[RR+1], gstart[RR], cnt[RR], toff[WW+1], then the
-// staged region sources (fp32: float4 A[npair], float2 Q[npair];
-// fp64: double u[n], v[n], q[n]).  npair_max / n_max from the plan.
+// Persistent CTAs pull Morton-aligned 2^k x 2^k tiles from a queue.  Per tile:
+//  A1 all threads: region box table (source CSR segments of the (W+2)^2
+//     region, row-major) and the tile's target offsets;
+//  A2 warp 0: prefix of the even-padded box counts (warp shuffles) ->
+//     shared-memory start of every region box; warps 1..: targets of each
+//     tile box, rebased to the region origin, with their row-run base;
+//  B  2^g lanes per region box copy its sources into shared memory, rebased
+//     to the region origin (global units), padded to an even count;
+//  C  work items (target, row): each sweeps one contiguous row-run of 3 boxes;
+//  D  fixed-order sum of the 3 row partials (deterministic), write.
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-p2p_nr_kernel(const int32_t *__restrict__ tiles, int k, int64_t S, T h, T eps2, int max_region,
-              const int32_t *__restrict__ src_off, const int32_t *__restrict__ tgt_off,
-              const typename V2<T>::type *__restrict__ src_uv, const T *__restrict__ q,
-              const typename V2<T>::type *__restrict__ tgt_uv, T *__restrict__ out, int accumulate) {
+p2p_nr_kernel(const P2PArgs<T> a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ int warp_tot[33];
-    const int W = 1 << k, R = W + 2, RR = R * R, WW = W * W;
-    int *sstart = reinterpret_cast<int *>(smem);
-    int *gstart = sstart + RR + 1;
-    int *cnt = gstart + RR;
-    int *toff = cnt + RR;
-    const int tbytes = ((4 * (3 * RR + WW + 2)) + 15) & ~15;
-    unsigned char *data = smem + tbytes;
+    __shared__ int s_tile;
+    const int k = a.k, W = 1 << k, R = W + 2, RR = R * R, WW = W * W;
+    const NrCarve c = nr_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T));
+    int *sstart = reinterpret_cast<int *>(smem + c.sstart);
+    int *gstart = reinterpret_cast<int *>(smem + c.gstart);
+    int *cnt = reinterpret_cast<int *>(smem + c.cnt);
+    int *toff = reinterpret_cast<int *>(smem + c.toff);
+    int *tj0 = reinterpret_cast<int *>(smem + c.tj0);
+    T *tu = reinterpret_cast<T *>(smem + c.tu);
+    T *tv = reinterpret_cast<T *>(smem + c.tv);
+    T *part = reinterpret_cast<T *>(smem + c.part);
+    unsigned char *src = smem + c.src;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const T h = a.h;
 
-    const uint32_t tile = (uint32_t)tiles[blockIdx.x];
-    const uint32_t m0 = tile << (2 * k);
-    const int64_t X0 = (int64_t)compact16(tile) * W - 1, Y0 = (int64_t)compact16(tile >> 1) * W - 1;
-    const int tid = threadIdx.x;
+    for (int ti = next_tile(a.queue, &s_tile); ti < a.ntiles; ti = next_tile(a.queue, &s_tile)) {
+        const uint32_t tile = (uint32_t)a.tiles[ti];
+        const uint32_t m0 = tile << (2 * k);
+        const int64_t X0 = (int64_t)compact16(tile) * W - 1, Y0 = (int64_t)compact16(tile >> 1) * W - 1;
+        const int tb = a.tgt_off[m0];
 
-    // 1. region box table (row-major over the (W+2)^2 region) + tile target offsets
-    for (int j = tid; j < RR; j += kThreads) {
-        const int lx = j % R, ly = j / R;
-        const int64_t gx = X0 + lx, gy = Y0 + ly;
-        int a = 0, c = 0;
-        if (gx >= 0 && gy >= 0 && gx < S && gy < S) {
-            const uint32_t m = spread16((uint32_t)gx) | (spread16((uint32_t)gy) << 1);
-            a = src_off[m];
-            c = src_off[m + 1] - a;
-        }
-        gstart[j] = a;
-        cnt[j] = c;
-        sstart[j] = (c + 1) & ~1;  // each box padded to an even count
-    }
-    for (int i = tid; i <= WW; i += kThreads) toff[i] = tgt_off[m0 + i];
-    __syncthreads();
-    const int total = block_exclusive_scan(sstart, RR, warp_tot);
-    if (tid == 0) sstart[RR] = total;
-    __syncthreads();
-
-    // 2. stage the region's sources, rebased to the region origin (global units)
-    if constexpr (sizeof(T) == 4) {
-        float *Af = reinterpret_cast<float *>(data);
-        float *Qf = Af + 2 * max_region;
-        for (int i = tid; i < total; i += kThreads) {
-            const int j = seg_search(sstart, RR, i);
-            const int e = i - sstart[j];
-            float u = 1.0e4f, v = 1.0e4f, qq = 0.f;  // pad: far away, zero weight
-            if (e < cnt[j]) {
-                const int s = gstart[j] + e;
-                const float2 uv = src_uv[s];
-                u = uv.x + (float)(j % R) * h;
-                v = uv.y + (float)(j / R) * h;
-                qq = q[s];
+        // A1: tables
+        for (int j = tid; j < RR; j += kThreads) {
+            const int lx = j % R, ly = j / R;
+            const int64_t gx = X0 + lx, gy = Y0 + ly;
+            int st = 0, cn = 0;
+            if (gx >= 0 && gy >= 0 && gx < a.S && gy < a.S) {
+                const uint32_t m = spread16((uint32_t)gx) | (spread16((uint32_t)gy) << 1);
+                st = a.src_off[m];
+                cn = a.src_off[m + 1] - st;
             }
-            const int p = i >> 1, sl = i & 1;
-            Af[4 * p + sl] = u;
-            Af[4 * p + 2 + sl] = v;
-            Qf[i] = qq;
+            gstart[j] = st;
+            cnt[j] = cn;
         }
-    } else {
-        double *su = reinterpret_cast<double *>(data);
-        double *sv = su + max_region;
-        double *sq = sv + max_region;
-        for (int i = tid; i < total; i += kThreads) {
-            const int j = seg_search(sstart, RR, i);
-            const int e = i - sstart[j];
-            double u = 1.0e4, v = 1.0e4, qq = 0.0;
-            if (e < cnt[j]) {
-                const int s = gstart[j] + e;
-                const double2 uv = src_uv[s];
-                u = uv.x + (double)(j % R) * h;
-                v = uv.y + (double)(j / R) * h;
-                qq = q[s];
-            }
-            su[i] = u;
-            sv[i] = v;
-            sq[i] = qq;
-        }
-    }
-    __syncthreads();
+        for (int i = tid; i <= WW; i += kThreads) toff[i] = a.tgt_off[m0 + i] - tb;
+        __syncthreads();
 
-    // 3. one target per thread: three row-runs of its 3x3 neighbourhood
-    const int tb = toff[0], nt = toff[WW] - tb;
-    for (int it = tid; it < nt; it += kThreads) {
-        const int gi = tb + it;
-        const int bl = seg_search(toff, WW, gi);
-        const int bx = (int)compact16((uint32_t)bl), by = (int)compact16((uint32_t)bl >> 1);
-        const typename V2<T>::type uv = tgt_uv[gi];
-        const T ut = uv.x + (T)(bx + 1) * h, vt = uv.y + (T)(by + 1) * h;
-        T phi;
-        if constexpr (sizeof(T) == 4) {
-            const float4 *A = reinterpret_cast<const float4 *>(data);
-            const float2 *Q = reinterpret_cast<const float2 *>(reinterpret_cast<const float *>(data) + 2 * max_region);
-            float acc = 0.f;
-#pragma unroll 1
-            for (int row = 0; row < 3; ++row) {
-                const int j0 = (by + row) * R + bx;
-                acc += span_f32(A, Q, sstart[j0] >> 1, sstart[j0 + 3] >> 1, ut, vt);
+        // A2: warp 0 scans; the other warps stage targets box by box
+        if (wid == 0) {
+            int carry = 0;
+            for (int base = 0; base < RR; base += 32) {
+                const int j = base + lane;
+                const int pc = j < RR ? ((cnt[j] + 1) & ~1) : 0;
+                const int incl = warp_incl_scan(pc);
+                if (j < RR) sstart[j] = carry + incl - pc;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
             }
-            if (!isfinite(acc)) {  // a guarded pair (r < eps) is present: explicit guard
-                acc = 0.f;
-                for (int row = 0; row < 3; ++row) {
-                    const int j0 = (by + row) * R + bx;
-                    acc += span_f32_guarded(A, Q, sstart[j0] >> 1, sstart[j0 + 3] >> 1, ut, vt, eps2);
+            if (lane == 0) sstart[RR] = carry;
+        } else {
+            for (int bl = wid - 1; bl < WW; bl += kThreads / 32 - 1) {
+                const int t0 = toff[bl], t1 = toff[bl + 1];
+                if (t0 == t1) continue;
+                const int bx = (int)compact16((uint32_t)bl), by = (int)compact16((uint32_t)bl >> 1);
+                const T ox = (T)(bx + 1) * h, oy = (T)(by + 1) * h;
+                for (int t = t0 + lane; t < t1; t += 32) {
+                    const typename V2<T>::type uv = a.tgt_uv[tb + t];
+                    tu[t] = uv.x + ox;
+                    tv[t] = uv.y + oy;
+                    tj0[t] = by * R + bx;
                 }
             }
-            phi = (-0.5f * kLn2) * acc;
-        } else {
-            const double *su = reinterpret_cast<const double *>(data);
-            const double *sv = su + max_region;
-            const double *sq = sv + max_region;
-            double acc = 0.0;
-#pragma unroll 1
-            for (int row = 0; row < 3; ++row) {
-                const int j0 = (by + row) * R + bx;
-                acc += span_f64(su, sv, sq, sstart[j0], sstart[j0 + 3], ut, vt, eps2);
-            }
-            phi = -0.5 * acc;
         }
-        out[gi] = accumulate ? out[gi] + phi : phi;
+        __syncthreads();
+
+        // B: sources, 2^g lanes per region box
+        {
+            const int G = 1 << a.group_log2, gl = tid & (G - 1), ngrp = kThreads >> a.group_log2;
+            for (int j = tid >> a.group_log2; j < RR; j += ngrp) {
+                const int cn = cnt[j], s0 = sstart[j], g0 = gstart[j], pc = (cn + 1) & ~1;
+                const T ox = (T)(j % R) * h, oy = (T)(j / R) * h;
+                for (int e = gl; e < pc; e += G) {
+                    T u = (T)1.0e4, v = (T)1.0e4, qq = (T)0;  // pad: far away, zero weight
+                    if (e < cn) {
+                        const typename V2<T>::type uv = a.src_uv[g0 + e];
+                        u = uv.x + ox;
+                        v = uv.y + oy;
+                        qq = a.q[g0 + e];
+                    }
+                    const int i = s0 + e;
+                    if constexpr (sizeof(T) == 4) {
+                        float *Af = reinterpret_cast<float *>(src);
+                        float *Qf = Af + 2 * a.src_cap;
+                        const int p = i >> 1, sl = i & 1;
+                        Af[4 * p + sl] = u;
+                        Af[4 * p + 2 + sl] = v;
+                        Qf[i] = qq;
+                    } else {
+                        double *su = reinterpret_cast<double *>(src);
+                        su[i] = u;
+                        su[a.src_cap + i] = v;
+                        su[2 * a.src_cap + i] = qq;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+
+        // C: (target, row-run) work items
+        const int nt = toff[WW];
+        for (int it = tid; it < 3 * nt; it += kThreads) {
+            const int row = (it >= nt) + (it >= 2 * nt);
+            const int t = it - row * nt;
+            const int j0 = tj0[t] + row * R;
+            const int i0 = sstart[j0], i1 = sstart[j0 + 3];
+            if constexpr (sizeof(T) == 4) {
+                const float4 *A = reinterpret_cast<const float4 *>(src);
+                const float2 *Q = reinterpret_cast<const float2 *>(reinterpret_cast<const float *>(src) + 2 * a.src_cap);
+                part[it] = span_f32(A, Q, i0 >> 1, i1 >> 1, tu[t], tv[t]);
+            } else {
+                const double *su = reinterpret_cast<const double *>(src);
+                part[it] = span_f64(su, su + a.src_cap, su + 2 * a.src_cap, i0, i1, tu[t], tv[t], a.eps2);
+            }
+        }
+        __syncthreads();
+
+        // D: fixed-order reduction of the three row partials, write
+        for (int t = tid; t < nt; t += kThreads) {
+            T acc = part[t] + part[nt + t] + part[2 * nt + t];
+            T phi;
+            if constexpr (sizeof(T) == 4) {
+                if (!isfinite(acc)) {  // a pair closer than eps: redo this target with the explicit guard
+                    const float4 *A = reinterpret_cast<const float4 *>(src);
+                    const float2 *Q = reinterpret_cast<const float2 *>(reinterpret_cast<const float *>(src) + 2 * a.src_cap);
+                    acc = 0.f;
+                    for (int row = 0; row < 3; ++row) {
+                        const int j0 = tj0[t] + row * R;
+                        acc += span_f32_guarded(A, Q, sstart[j0] >> 1, sstart[j0 + 3] >> 1, tu[t], tv[t], a.eps2);
+                    }
+                }
+                phi = (-0.5f * kLn2) * acc;
+            } else {
+                phi = -0.5 * acc;
+            }
+            a.out[tb + t] = a.accumulate ? a.out[tb + t] + phi : phi;
+        }
+        // the next_tile() barrier orders this tile's shared-memory reads before the next tile's writes
     }
 }
 
@@ -318,84 +334,118 @@ __device__ __forceinline__ uint32_t smem_addr(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+// Persistent CTAs; per tile one TMA bulk copy (cp.async.bulk) per array brings
+// the tile's packed halo (contiguous in HBM, 16-B aligned) into shared memory
+// while the threads stage the tile's targets.  Work items (target, third of
+// its halo) balance the CTA; fixed-order reduction keeps results deterministic.
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-p2p_r_kernel(const int32_t *__restrict__ tiles, int k, T eps2, const int32_t *__restrict__ tgt_off,
-             const uint32_t *__restrict__ halo_off, const T *__restrict__ halo_uv,
-             const T *__restrict__ halo_q, const typename V2<T>::type *__restrict__ tgt_uv,
-             T *__restrict__ out, int accumulate) {
+p2p_r_kernel(const P2PArgs<T> a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int W = 1 << k, WW = W * W;
-    int *toff = reinterpret_cast<int *>(smem);
-    int *hoff = toff + WW + 1;
-    const int tbytes = (8 * (WW + 1) + 16 + 31) & ~31;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + tbytes - 16);
-    unsigned char *data = smem + tbytes;
-
-    const uint32_t tile = (uint32_t)tiles[blockIdx.x];
-    const uint32_t m0 = tile << (2 * k);
-    const uint32_t hb = halo_off[m0], he = halo_off[m0 + WW];
-    const uint32_t nent = he - hb;  // multiple of 4 (plan pads each tile)
-    const int tid = threadIdx.x;
-
-    // TMA bulk copy of the tile's packed halo (one contiguous span per array).
+    __shared__ int s_tile;
+    const int k = a.k, W = 1 << k, WW = W * W;
+    const RCarve c = r_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T));
+    int *toff = reinterpret_cast<int *>(smem + c.toff);
+    int *hoff = reinterpret_cast<int *>(smem + c.hoff);
+    int *tbx = reinterpret_cast<int *>(smem + c.tbx);
+    T *tu = reinterpret_cast<T *>(smem + c.tu);
+    T *tv = reinterpret_cast<T *>(smem + c.tv);
+    T *part = reinterpret_cast<T *>(smem + c.part);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + c.bar);
+    T *s_uv = reinterpret_cast<T *>(smem + c.src);
+    T *s_q = s_uv + 2 * (size_t)a.src_cap;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t bar = smem_addr(mbar);
-    T *s_uv = reinterpret_cast<T *>(data);
-    T *s_q = s_uv + 2 * (size_t)nent;
-    if (tid == 0 && nent > 0) {
-        const uint32_t b_uv = nent * 2 * sizeof(T), b_q = nent * sizeof(T);
+    if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(b_uv + b_q) : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_addr(s_uv)),
-            "l"(halo_uv + 2 * (size_t)hb), "r"(b_uv), "r"(bar)
-            : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_addr(s_q)),
-            "l"(halo_q + hb), "r"(b_q), "r"(bar)
-            : "memory");
     }
-    for (int i = tid; i <= WW; i += kThreads) {
-        toff[i] = tgt_off[m0 + i];
-        hoff[i] = (int)(halo_off[m0 + i] - hb);
-    }
-    __syncthreads();
-    if (nent > 0) {
+    uint32_t parity = 0;
+
+    for (int ti = next_tile(a.queue, &s_tile); ti < a.ntiles; ti = next_tile(a.queue, &s_tile)) {
+        const uint32_t m0 = (uint32_t)a.tiles[ti] << (2 * k);
+        const int tb = a.tgt_off[m0];
+        const uint32_t hb = a.halo_off[m0], nent = a.halo_off[m0 + WW] - hb;  // multiple of 4
+        if (tid == 0) {
+            const uint32_t b_uv = nent * 2 * (uint32_t)sizeof(T), b_q = nent * (uint32_t)sizeof(T);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(b_uv + b_q)
+                         : "memory");
+            if (nent) {
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_addr(s_uv)),
+                    "l"(a.halo_uv + 2 * (size_t)hb), "r"(b_uv), "r"(bar)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_addr(s_q)),
+                    "l"(a.q + hb), "r"(b_q), "r"(bar)
+                    : "memory");
+            }
+        }
+        for (int i = tid; i <= WW; i += kThreads) {
+            toff[i] = a.tgt_off[m0 + i] - tb;
+            hoff[i] = (int)(a.halo_off[m0 + i] - hb);
+        }
+        __syncthreads();
+        for (int bl = wid; bl < WW; bl += kThreads / 32) {
+            const int t0 = toff[bl], t1 = toff[bl + 1];
+            for (int t = t0 + lane; t < t1; t += 32) {
+                const typename V2<T>::type uv = a.tgt_uv[tb + t];
+                tu[t] = uv.x;
+                tv[t] = uv.y;
+                tbx[t] = bl;
+            }
+        }
         asm volatile(
             "{\n\t.reg .pred P;\n"
             "WAIT_%=:\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t"
-            "@!P bra WAIT_%=;\n}" ::"r"(bar)
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+            "@!P bra WAIT_%=;\n}" ::"r"(bar),
+            "r"(parity)
             : "memory");
-    }
+        parity ^= 1u;
+        __syncthreads();
 
-    const int tb = toff[0], nt = toff[WW] - tb;
-    for (int it = tid; it < nt; it += kThreads) {
-        const int gi = tb + it;
-        const int bl = seg_search(toff, WW, gi);
-        const int j0 = hoff[bl], j1 = hoff[bl + 1];
-        const typename V2<T>::type uv = tgt_uv[gi];
-        T phi;
-        if constexpr (sizeof(T) == 4) {
-            const float4 *A = reinterpret_cast<const float4 *>(s_uv);
-            const float2 *Q = reinterpret_cast<const float2 *>(s_q);
-            float acc = span_f32(A, Q, j0 >> 1, j1 >> 1, uv.x, uv.y);
-            if (!isfinite(acc)) acc = span_f32_guarded(A, Q, j0 >> 1, j1 >> 1, uv.x, uv.y, eps2);
-            phi = (-0.5f * kLn2) * acc;
-        } else {
-            const double *su = s_uv;
-            double acc = 0.0;
-            for (int j = j0; j < j1; ++j) {
-                const double du = uv.x - su[2 * j], dv = uv.y - su[2 * j + 1];
-                const double r2 = fma(dv, dv, du * du);
-                if (r2 >= eps2) acc = fma(s_q[j], log(r2), acc);
+        const int nt = toff[WW];
+        for (int it = tid; it < 3 * nt; it += kThreads) {
+            const int part3 = (it >= nt) + (it >= 2 * nt);
+            const int t = it - part3 * nt;
+            const int bl = tbx[t];
+            const int p0 = hoff[bl] >> 1, np = (hoff[bl + 1] >> 1) - p0;  // source pairs of this box's halo
+            const int q0 = p0 + (np * part3) / 3, q1 = p0 + (np * (part3 + 1)) / 3;
+            if constexpr (sizeof(T) == 4) {
+                part[it] = span_f32(reinterpret_cast<const float4 *>(s_uv), reinterpret_cast<const float2 *>(s_q), q0,
+                                    q1, tu[t], tv[t]);
+            } else {
+                const double *su = s_uv;
+                double acc = 0.0;
+                for (int j = 2 * q0; j < 2 * q1; ++j) {
+                    const double du = tu[t] - su[2 * j], dv = tv[t] - su[2 * j + 1];
+                    const double r2 = fma(dv, dv, du * du);
+                    if (r2 >= a.eps2) acc = fma(s_q[j], log(r2), acc);
+                }
+                part[it] = acc;
             }
-            phi = -0.5 * acc;
         }
-        out[gi] = accumulate ? out[gi] + phi : phi;
+        __syncthreads();
+        for (int t = tid; t < nt; t += kThreads) {
+            T acc = part[t] + part[nt + t] + part[2 * nt + t];
+            T phi;
+            if constexpr (sizeof(T) == 4) {
+                if (!isfinite(acc)) {
+                    const int bl = tbx[t];
+                    acc = span_f32_guarded(reinterpret_cast<const float4 *>(s_uv),
+                                           reinterpret_cast<const float2 *>(s_q), hoff[bl] >> 1, hoff[bl + 1] >> 1,
+                                           tu[t], tv[t], a.eps2);
+                }
+                phi = (-0.5f * kLn2) * acc;
+            } else {
+                phi = -0.5 * acc;
+            }
+            a.out[tb + t] = a.accumulate ? a.out[tb + t] + phi : phi;
+        }
     }
 }
 

@@ -10,7 +10,56 @@
 
 #include "p2p.h"
 
+#if defined(__CUDACC__)
+#define P2P_HD __host__ __device__
+#else
+#define P2P_HD
+#endif
+
 namespace p2p {
+
+// ---- shared-memory layouts of the P2P kernels (byte offsets), used by the
+// plan builder (sizing), the launcher and the kernels (carving).
+P2P_HD inline int align16(int x) { return (x + 15) & ~15; }
+
+struct NrCarve {
+    int sstart, gstart, cnt, toff, tj0, tu, tv, part, src, total;
+};
+// src_cap: max padded region sources of a tile (multiple of 4); tgt_cap: max targets (multiple of 4).
+P2P_HD inline NrCarve nr_carve(int k, int src_cap, int tgt_cap, int e) {
+    const int W = 1 << k, R = W + 2, RR = R * R, WW = W * W;
+    NrCarve c;
+    c.sstart = 0;
+    c.gstart = c.sstart + 4 * (RR + 1);
+    c.cnt = c.gstart + 4 * RR;
+    c.toff = c.cnt + 4 * RR;
+    c.tj0 = c.toff + 4 * (WW + 1);
+    c.tu = align16(c.tj0 + 4 * tgt_cap);
+    c.tv = align16(c.tu + e * tgt_cap);
+    c.part = align16(c.tv + e * tgt_cap);
+    c.src = align16(c.part + 3 * e * tgt_cap);
+    c.total = c.src + 3 * e * src_cap;
+    return c;
+}
+
+struct RCarve {
+    int toff, hoff, tbx, tu, tv, part, bar, src, total;
+};
+// src_cap: max packed-halo entries of a tile (multiple of 4).
+P2P_HD inline RCarve r_carve(int k, int src_cap, int tgt_cap, int e) {
+    const int W = 1 << k, WW = W * W;
+    RCarve c;
+    c.toff = 0;
+    c.hoff = c.toff + 4 * (WW + 1);
+    c.tbx = c.hoff + 4 * (WW + 1);
+    c.tu = align16(c.tbx + 4 * tgt_cap);
+    c.tv = align16(c.tu + e * tgt_cap);
+    c.part = align16(c.tv + e * tgt_cap);
+    c.bar = align16(c.part + 3 * e * tgt_cap);
+    c.src = align16(c.bar + 16);
+    c.total = c.src + 3 * e * src_cap;
+    return c;
+}
 
 struct Error : std::runtime_error {
     p2p_status code;
@@ -95,12 +144,13 @@ struct HostPlan {
     // ---- statistics
     int64_t pairs = 0, pairs_global = 0, t_max = 0, occ_src = 0, occ_tgt = 0;
     int64_t boxes_in_tiles = 0, max_region = 0, max_tile_halo = 0, smem_bytes = 0;
+    int64_t src_cap = 0, tgt_cap = 0;            // kernel smem capacities (multiples of 4)
+    int group_log2 = 0;                          // NR staging lanes per region box (log2)
+    bool lpt = false;                            // tiles queued by decreasing pairs (working set fits L2)
     double density = 0.0, density_occ = 0.0, build_seconds = 0.0;
 };
 
 void build_host_plan(const p2p_plan_desc &desc, HostPlan &hp);
 std::vector<int64_t> neighbors_export(const HostPlan &hp);
-int64_t nr_smem_bytes(int k, int64_t max_region, int elem_bytes);
-int64_t r_smem_bytes(int k, int64_t max_halo, int elem_bytes);
 
 }  // namespace p2p

@@ -127,20 +127,6 @@ void csr_sort(const double *xy, int64_t n, const HostPlan &hp, std::vector<int32
 
 }  // namespace
 
-int64_t nr_smem_bytes(int k, int64_t max_region, int e) {
-    int64_t W = int64_t(1) << k, R = W + 2, RR = R * R, WW = W * W;
-    int64_t tables = 4 * (3 * RR + WW + 2);
-    tables = (tables + 15) & ~int64_t(15);
-    return tables + pad4(max_region) * 3 * e;
-}
-
-int64_t r_smem_bytes(int k, int64_t max_halo, int e) {
-    int64_t W = int64_t(1) << k, WW = W * W;
-    int64_t tables = 8 * (WW + 1) + 16;  // toff, hoff, mbarrier
-    tables = (tables + 31) & ~int64_t(31);
-    return tables + max_halo * 3 * e;
-}
-
 void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     auto t0 = std::chrono::steady_clock::now();
     if (d.struct_size != sizeof(p2p_plan_desc)) fail(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
@@ -231,7 +217,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             if (to[(t + 1) * WW] > to[t * WW]) hp.tiles_g.push_back((int32_t)t);
         const int64_t nt = (int64_t)hp.tiles_g.size();
         hp.tile_pairs_g.assign((size_t)nt, 0);
-        std::vector<int64_t> region((size_t)nt, 0), halo((size_t)nt, 0);
+        std::vector<int64_t> region((size_t)nt, 0), halo((size_t)nt, 0), tcount((size_t)nt, 0);
         parallel_for(nt, [&](int64_t a, int64_t bnd) {
             for (int64_t i = a; i < bnd; ++i) {
                 int64_t t = hp.tiles_g[i];
@@ -252,14 +238,18 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                         rg += pad2(ns(morton_encode((uint32_t)x, (uint32_t)y)));
                     }
                 hp.tile_pairs_g[i] = pr;
+                tcount[i] = to[(t + 1) * WW] - to[t * WW];
                 region[i] = rg;
                 halo[i] = pad4(hl);
             }
         }, 256);
         hp.max_region = region.empty() ? 0 : *std::max_element(region.begin(), region.end());
         hp.max_tile_halo = halo.empty() ? 0 : *std::max_element(halo.begin(), halo.end());
-        int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? nr_smem_bytes(k, hp.max_region, e)
-                                                          : r_smem_bytes(k, hp.max_tile_halo, e);
+        hp.tgt_cap = pad4(tcount.empty() ? 0 : *std::max_element(tcount.begin(), tcount.end()));
+        hp.src_cap = d.layout == P2P_LAYOUT_NONREDUNDANT ? pad4(hp.max_region) : hp.max_tile_halo;
+        int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT
+                           ? (int64_t)nr_carve(k, (int)std::min<int64_t>(hp.src_cap, 1 << 24), (int)std::min<int64_t>(hp.tgt_cap, 1 << 24), e).total
+                           : (int64_t)r_carve(k, (int)std::min<int64_t>(hp.src_cap, 1 << 24), (int)std::min<int64_t>(hp.tgt_cap, 1 << 24), e).total;
         hp.smem_bytes = smem;
         if (smem <= kSmemLimit) break;
         if (k == 0 || d.tile_log2 >= 0)
@@ -268,6 +258,11 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                      " B of shared memory (> 200 KB); use a deeper level (CT loop) -- see DESIGN.md");
     }
     hp.k = k;
+    {   // NR staging: 2^g lanes per region box, g = ceil(log2(D_occ)) clamped to [1, 5]
+        int g = 1;
+        while (g < 5 && (double)(1 << g) < hp.density_occ) ++g;
+        hp.group_log2 = g;
+    }
     const int64_t W = int64_t(1) << k, WW = W * W, R = W + 2;
     const int64_t ntiles = (int64_t)hp.tiles_g.size();
     hp.pairs_global = 0;
@@ -469,6 +464,25 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                 }
             }
         }, 64);
+    }
+    // ---- queue order of this partition's tiles: when the working set fits
+    // comfortably in L2, longest tiles first (LPT) to shorten the tail; else
+    // Morton order, so concurrently running CTAs share their halo rings in L2.
+    {
+        const int64_t ws = (hp.n_src_local + hp.n_tgt_local) * 3 * (int64_t)e + 8 * hp.boxes_in_tiles +
+                           hp.halo_entries * 3 * (int64_t)e;
+        hp.lpt = ws < (int64_t)48 << 20;
+        if (hp.lpt) {
+            const int64_t base = hp.part_tile[r];
+            std::vector<int64_t> order(hp.tiles.size());
+            std::iota(order.begin(), order.end(), 0);
+            std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
+                return hp.tile_pairs_g[base + x] > hp.tile_pairs_g[base + y];
+            });
+            std::vector<int32_t> t2(hp.tiles.size());
+            for (size_t i = 0; i < order.size(); ++i) t2[i] = hp.tiles[order[i]];
+            hp.tiles.swap(t2);
+        }
     }
     hp.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
