@@ -52,13 +52,14 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="density_1e6", choices=sorted(WORKLOADS))
-    ap.add_argument("--layout", default="nr", choices=["nr", "r"])
+    ap.add_argument("--layout", default="nr", choices=["nr", "r", "tiled"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--kind", default="iid", choices=["iid", "stratified"])
     ap.add_argument("--no-extras", action="store_true", help="skip the R / fp64 detail lines")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras/baseline)")
+    ap.add_argument("--configs", default="", help="comma list of config names overriding --workload")
     return ap.parse_args()
 
 
@@ -192,7 +193,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    names = WORKLOADS[args.workload]
+    names = args.configs.split(",") if args.configs else WORKLOADS[args.workload]
 
     # ---- plans (host build + upload; not timed)
     jobs = []
@@ -386,7 +387,7 @@ def _extras(args, names, stream, dev):
     from paper_2403_01596_b200 import p2p
     res = []
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for layout in ("nr", "r"):
+    for layout in ("nr", "r", "tiled"):
         for prec in ("fp32", "fp64"):
             for name in names:
                 cfg = W.CONFIGS[name]

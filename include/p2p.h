@@ -58,12 +58,17 @@ typedef enum {
 typedef enum { P2P_KERNEL_LAPLACE_2D = 0 /* q ln(1/r); 0 when r < eps */ } p2p_kernel;
 
 /* Source layouts (§3.2 Indexing = non-redundant; §3.3 Repetition =
- * redundant), re-derived for B200: NR = Morton-sorted points + CSR box
- * offsets, gathered per tile into shared memory; R = per target box, the
- * packed halo of its E1 sources (coordinates copied at plan time, weights
- * refreshed per apply by a pack kernel), read as one contiguous bulk copy
- * per tile. */
-typedef enum { P2P_LAYOUT_NONREDUNDANT = 0, P2P_LAYOUT_REDUNDANT = 1 } p2p_layout;
+ * redundant), re-derived for B200:
+ *   NR    = Morton-sorted points + CSR box offsets, gathered per tile into
+ *           shared memory at run time (no copy of any point);
+ *   R     = per target box, the packed halo of its E1 sources (coordinates
+ *           copied at plan time, weights refreshed per apply by a pack
+ *           kernel), read as one contiguous TMA bulk copy per tile;
+ *   TILED = per CTA tile, its region (tile + one-box ring) packed at plan
+ *           time, rebased to the region origin: redundancy only on the ring,
+ *           ((W+2)/W)^2, streamed by one TMA bulk copy per tile; weights are
+ *           gathered in-kernel through a per-entry index. */
+typedef enum { P2P_LAYOUT_NONREDUNDANT = 0, P2P_LAYOUT_REDUNDANT = 1, P2P_LAYOUT_TILED = 2 } p2p_layout;
 
 /* fp64 is paper-faithful ("stored as Double"); fp32 uses
  * box-local coordinates and the SFU lg2. */
@@ -189,7 +194,9 @@ typedef enum {
     P2P_EXPORT_TILES = 8,           /* int64[tiles]: Morton index of each CTA tile (launch order) */
     P2P_EXPORT_HALO_INDEX = 9,      /* int64[halo_entries]: R layout, local source of each packed entry (-1 = pad) */
     P2P_EXPORT_SEND_INDEX = 10,     /* int64[n_send]: owned-local index of each sent weight */
-    P2P_EXPORT_HALO_OFFSETS = 11    /* int64[boxes+1]: R layout, packed-halo offsets per Morton box */
+    P2P_EXPORT_HALO_OFFSETS = 11,   /* int64[boxes+1]: R layout, packed-halo offsets per Morton box */
+    P2P_EXPORT_REGION_OFFSETS = 12, /* int64[tiles+1]: TILED layout, packed-region offsets per tile (Morton tile order) */
+    P2P_EXPORT_REGION_INDEX = 13    /* int64[entries]: TILED layout, local source of each packed entry (-1 = pad) */
 } p2p_export_kind;
 
 /* Copy a plan array to host memory.  If host_dst is NULL, *bytes receives the

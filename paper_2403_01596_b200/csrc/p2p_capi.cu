@@ -44,6 +44,7 @@ struct p2p_plan_s {
     // device arrays
     DevBuf tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
+    DevBuf tile_slot, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_ruv;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     int grid = 0;                                // persistent CTAs per launch
     int64_t device_bytes = 0;
@@ -66,7 +67,8 @@ struct p2p_plan_s {
     }
     void release() {
         DevBuf *all[] = {&tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
-                         &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q, &q_local, &phi,
+                         &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
+                         &tile_slot, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_ruv, &q_local, &phi,
                          &io_q, &io_out, &queue};
         for (DevBuf *b : all) {
             if (b->p) cudaFree(b->p);
@@ -102,6 +104,14 @@ void upload_plan(p2p_plan_s &P) {
     if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
         P.upload(P.src_off, hp.src_off);
         P.upload(P.src_uv, lay.src_uv);
+    } else if (hp.layout == P2P_LAYOUT_TILED) {
+        P.upload(P.tile_slot, hp.tile_slot);
+        P.upload(P.reg_off, hp.reg_off);
+        P.upload(P.reg_idx, hp.reg_idx);
+        P.upload(P.reg_uv, lay.reg_uv);
+        P.upload(P.reg_table, hp.reg_table);
+        P.upload(P.tgt_bl, hp.tgt_bl);
+        P.upload(P.tgt_ruv, lay.tgt_ruv);
     } else {
         P.upload(P.halo_off, hp.halo_off);
         P.upload(P.halo_idx, hp.halo_idx);
@@ -110,8 +120,13 @@ void upload_plan(p2p_plan_s &P) {
     }
     // Dynamic shared memory is fixed per plan: opt in once (a permission, not a
     // reservation, so one value serves all plans), then size the persistent grid.
-    const void *kfn = hp.layout == P2P_LAYOUT_NONREDUNDANT ? (const void *)p2p::dev::p2p_nr_kernel<T>
-                                                           : (const void *)p2p::dev::p2p_r_kernel<T>;
+    const bool two = hp.tpi == 2;
+    const void *kfn = hp.layout == P2P_LAYOUT_REDUNDANT ? (const void *)p2p::dev::p2p_r_kernel<T>
+                      : hp.layout == P2P_LAYOUT_TILED
+                          ? (two ? (const void *)p2p::dev::p2p_tiled_kernel<T, sizeof(T) == 4 ? 2 : 1>
+                                 : (const void *)p2p::dev::p2p_tiled_kernel<T, 1>)
+                          : (two ? (const void *)p2p::dev::p2p_nr_kernel<T, sizeof(T) == 4 ? 2 : 1>
+                                 : (const void *)p2p::dev::p2p_nr_kernel<T, 1>);
     ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2p::kSmemLimit), "smem attr");
     int occ = 0, dev = 0, sms = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, p2p::kThreads, (size_t)hp.smem_bytes), "occupancy");
@@ -156,7 +171,23 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.src_off = (const int32_t *)P.src_off.p;
         a.src_uv = (const typename p2p::dev::V2<T>::type *)P.src_uv.p;
         a.q = q_local;
-        p2p::dev::p2p_nr_kernel<T><<<P.grid, p2p::kThreads, hp.smem_bytes, s>>>(a);
+        if (hp.tpi == 2)
+            p2p::dev::p2p_nr_kernel<T, sizeof(T) == 4 ? 2 : 1><<<P.grid, p2p::kThreads, hp.smem_bytes, s>>>(a);
+        else
+            p2p::dev::p2p_nr_kernel<T, 1><<<P.grid, p2p::kThreads, hp.smem_bytes, s>>>(a);
+    } else if (hp.layout == P2P_LAYOUT_TILED) {
+        a.q = q_local;
+        a.tile_slot = (const int32_t *)P.tile_slot.p;
+        a.reg_off = (const uint32_t *)P.reg_off.p;
+        a.reg_idx = (const int32_t *)P.reg_idx.p;
+        a.reg_uv = (const T *)P.reg_uv.p;
+        a.reg_table = (const uint16_t *)P.reg_table.p;
+        a.tgt_bl = (const uint16_t *)P.tgt_bl.p;
+        a.tgt_ruv = (const typename p2p::dev::V2<T>::type *)P.tgt_ruv.p;
+        if (hp.tpi == 2)
+            p2p::dev::p2p_tiled_kernel<T, sizeof(T) == 4 ? 2 : 1><<<P.grid, p2p::kThreads, hp.smem_bytes, s>>>(a);
+        else
+            p2p::dev::p2p_tiled_kernel<T, 1><<<P.grid, p2p::kThreads, hp.smem_bytes, s>>>(a);
     } else {
         if (hp.halo_entries > 0)
             p2p::dev::pack_r_kernel<T><<<grid_for(hp.halo_entries), 256, 0, s>>>(
@@ -410,6 +441,13 @@ p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *info) {
     if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
         info->alg_bytes_kernel = hp.n_tgt_local * 3 * e + hp.n_src_local * 3 * e + offs;
         info->alg_bytes_apply = info->alg_bytes_kernel;
+    } else if (hp.layout == P2P_LAYOUT_TILED) {
+        // targets: region-relative coords + box byte pair + out + CSR offset; region: coords + index;
+        // tables; weights gathered once from plan order
+        info->alg_bytes_kernel = hp.n_tgt_local * (3 * e + 2) + 4 * hp.boxes_in_tiles +
+                                 hp.reg_entries * (2 * e + 4) + (int64_t)hp.reg_table.size() * 2 +
+                                 hp.n_src_local * e;
+        info->alg_bytes_apply = info->alg_bytes_kernel;
     } else {
         info->alg_bytes_kernel = hp.n_tgt_local * 3 * e + hp.halo_entries * 3 * e + offs;
         info->alg_bytes_apply = info->alg_bytes_kernel + hp.halo_entries * (4 + e) + hp.n_src_local * e;
@@ -445,6 +483,8 @@ p2p_status p2p_plan_export(p2p_plan P, int32_t kind, void *host_dst, size_t *byt
         case P2P_EXPORT_HALO_INDEX: take(hp.halo_idx); break;
         case P2P_EXPORT_SEND_INDEX: take(hp.send_idx); break;
         case P2P_EXPORT_HALO_OFFSETS: take(hp.halo_off); break;
+        case P2P_EXPORT_REGION_OFFSETS: take(hp.reg_off); break;
+        case P2P_EXPORT_REGION_INDEX: take(hp.reg_idx); break;
         default: throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "unknown export kind");
         }
         const size_t need = v.size() * sizeof(int64_t);

@@ -104,6 +104,36 @@ __device__ __forceinline__ float span_f32(const float4 *__restrict__ A, const fl
     return a0 + a1;
 }
 
+// Two targets sharing one span x two sources per step: 4 pairs per LDS.128 + LDS.64,
+// ~3 non-MUFU issue slots per pair (FADD2 x4, FMUL2 x2, FFMA2 x4 per 4 pairs).
+__device__ __forceinline__ void span2_f32(const float4 *__restrict__ A, const float2 *__restrict__ Q, int p0,
+                                          int p1, float ut0, float vt0, float ut1, float vt1, float &r0,
+                                          float &r1) {
+    const f2_t U0 = f2_pack(ut0, ut0), V0 = f2_pack(vt0, vt0);
+    const f2_t U1 = f2_pack(ut1, ut1), V1 = f2_pack(vt1, vt1);
+    f2_t a0 = 0ull, a1 = 0ull;
+#pragma unroll 4
+    for (int p = p0; p < p1; ++p) {
+        const float4 s = A[p];
+        const float2 q = Q[p];
+        const f2_t su = f2_pack(s.x, s.y), sv = f2_pack(s.z, s.w), qq = f2_pack(q.x, q.y);
+        const f2_t d0u = f2_sub(U0, su), d0v = f2_sub(V0, sv);
+        const f2_t d1u = f2_sub(U1, su), d1v = f2_sub(V1, sv);
+        const f2_t w0 = f2_fma(d0v, d0v, f2_mul(d0u, d0u));
+        const f2_t w1 = f2_fma(d1v, d1v, f2_mul(d1u, d1u));
+        float x0, x1, y0, y1;
+        f2_unpack(w0, x0, x1);
+        f2_unpack(w1, y0, y1);
+        a0 = f2_fma(qq, f2_pack(lg2_approx(x0), lg2_approx(x1)), a0);
+        a1 = f2_fma(qq, f2_pack(lg2_approx(y0), lg2_approx(y1)), a1);
+    }
+    float c0, c1;
+    f2_unpack(a0, c0, c1);
+    r0 = c0 + c1;
+    f2_unpack(a1, c0, c1);
+    r1 = c0 + c1;
+}
+
 // Explicitly guarded fp32 sweep (slow path for targets whose fast sum is not finite).
 __device__ __noinline__ float span_f32_guarded(const float4 *__restrict__ A, const float2 *__restrict__ Q,
                                                int p0, int p1, float ut, float vt, float eps2) {
@@ -154,6 +184,13 @@ struct P2PArgs {
     const T *q;            // NR: q in local plan order; R: packed halo q (from pack_r)
     const uint32_t *halo_off;  // R: [B+1] packed-halo offsets
     const T *halo_uv;      // R: packed-halo coordinates relative to the target box origin
+    const int32_t *tile_slot;   // TILED: launch order -> Morton slot of the per-tile arrays
+    const uint32_t *reg_off;    // TILED: [slots+1] packed-region offsets
+    const int32_t *reg_idx;     // TILED: local source index per packed entry (-1 = pad)
+    const T *reg_uv;            // TILED: region-relative coordinates (fp32: (u0,u1,v0,v1) per pair)
+    const uint16_t *reg_table;  // TILED: [slots][tstride] row-major box starts within the region
+    const uint16_t *tgt_bl;     // TILED: tile-local Morton box of each target
+    const typename V2<T>::type *tgt_ruv;  // TILED: target coordinates relative to the region origin
     T *out;
     int accumulate;
 };
@@ -180,24 +217,30 @@ __device__ __forceinline__ int next_tile(int *queue, int *s_tile) {
 //  A1 all threads: region box table (source CSR segments of the (W+2)^2
 //     region, row-major) and the tile's target offsets;
 //  A2 warp 0: prefix of the even-padded box counts (warp shuffles) ->
-//     shared-memory start of every region box; warps 1..: targets of each
-//     tile box, rebased to the region origin, with their row-run base;
+//     shared-memory start of every region box; warp 1 (TPI = 2): prefix of
+//     the per-box number of target pairs;
+//  A3 targets of each tile box, rebased to the region origin, grouped into
+//     work units of TPI targets of the same box (same row-runs);
 //  B  2^g lanes per region box copy its sources into shared memory, rebased
 //     to the region origin (global units), padded to an even count;
-//  C  work items (target, row): each sweeps one contiguous row-run of 3 boxes;
-//  D  fixed-order sum of the 3 row partials (deterministic), write.
-template <typename T>
+//  C  work items (unit, row): TPI targets sweep one contiguous row-run;
+//  D  fixed-order sum of the 3 row partials of each target (deterministic).
+template <typename T, int TPI>
 __global__ void __launch_bounds__(kThreads)
 p2p_nr_kernel(const P2PArgs<T> a) {
+    static_assert(TPI == 1 || (TPI == 2 && sizeof(T) == 4), "TPI = 2 is the fp32 path");
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ int s_tile;
+    __shared__ int s_tile, s_units;
     const int k = a.k, W = 1 << k, R = W + 2, RR = R * R, WW = W * W;
-    const NrCarve c = nr_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T));
+    const NrCarve c = nr_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI);
     int *sstart = reinterpret_cast<int *>(smem + c.sstart);
     int *gstart = reinterpret_cast<int *>(smem + c.gstart);
     int *cnt = reinterpret_cast<int *>(smem + c.cnt);
     int *toff = reinterpret_cast<int *>(smem + c.toff);
-    int *tj0 = reinterpret_cast<int *>(smem + c.tj0);
+    int *pstart = reinterpret_cast<int *>(smem + c.pstart);
+    int *uj0 = reinterpret_cast<int *>(smem + c.uj0);
+    int *ut = reinterpret_cast<int *>(smem + c.ut);
+    int *tslot = reinterpret_cast<int *>(smem + c.tslot);
     T *tu = reinterpret_cast<T *>(smem + c.tu);
     T *tv = reinterpret_cast<T *>(smem + c.tv);
     T *part = reinterpret_cast<T *>(smem + c.part);
@@ -227,7 +270,7 @@ p2p_nr_kernel(const P2PArgs<T> a) {
         for (int i = tid; i <= WW; i += kThreads) toff[i] = a.tgt_off[m0 + i] - tb;
         __syncthreads();
 
-        // A2: warp 0 scans; the other warps stage targets box by box
+        // A2: prefixes
         if (wid == 0) {
             int carry = 0;
             for (int base = 0; base < RR; base += 32) {
@@ -238,21 +281,42 @@ p2p_nr_kernel(const P2PArgs<T> a) {
                 carry += __shfl_sync(0xffffffffu, incl, 31);
             }
             if (lane == 0) sstart[RR] = carry;
-        } else {
-            for (int bl = wid - 1; bl < WW; bl += kThreads / 32 - 1) {
-                const int t0 = toff[bl], t1 = toff[bl + 1];
-                if (t0 == t1) continue;
-                const int bx = (int)compact16((uint32_t)bl), by = (int)compact16((uint32_t)bl >> 1);
-                const T ox = (T)(bx + 1) * h, oy = (T)(by + 1) * h;
-                for (int t = t0 + lane; t < t1; t += 32) {
-                    const typename V2<T>::type uv = a.tgt_uv[tb + t];
-                    tu[t] = uv.x + ox;
-                    tv[t] = uv.y + oy;
-                    tj0[t] = by * R + bx;
-                }
+        } else if (wid == 1) {
+            int carry = 0;
+            for (int base = 0; base < WW; base += 32) {
+                const int bl = base + lane;
+                const int n = bl < WW ? toff[bl + 1] - toff[bl] : 0;
+                const int np = TPI == 2 ? (n + 1) >> 1 : n;
+                const int incl = warp_incl_scan(np);
+                if (bl < WW) pstart[bl] = carry + incl - np;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
             }
+            if (lane == 0) s_units = carry;
         }
         __syncthreads();
+
+        // A3: targets -> units (flat over targets; box by binary search over the tile's offsets)
+        const int nt = toff[WW];
+        for (int t = tid; t < nt; t += kThreads) {
+            int lo = 0, hi = WW;  // last box bl with toff[bl] <= t
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (toff[mid] <= t) lo = mid;
+                else hi = mid;
+            }
+            const int bl = lo, t0 = toff[bl], t1 = toff[bl + 1];
+            const int bx = (int)compact16((uint32_t)bl), by = (int)compact16((uint32_t)bl >> 1);
+            const typename V2<T>::type uv = a.tgt_uv[tb + t];
+            tu[t] = uv.x + (T)(bx + 1) * h;
+            tv[t] = uv.y + (T)(by + 1) * h;
+            const int r = t - t0, u = pstart[bl] + r / TPI, sl = r % TPI;
+            ut[TPI * u + sl] = t;
+            tslot[t] = TPI * u + sl;
+            if (sl == 0) {
+                uj0[u] = by * R + bx;
+                if (TPI == 2 && t + 1 == t1) ut[TPI * u + 1] = t;  // odd box: duplicate, result unused
+            }
+        }
 
         // B: sources, 2^g lanes per region box
         {
@@ -287,35 +351,46 @@ p2p_nr_kernel(const P2PArgs<T> a) {
         }
         __syncthreads();
 
-        // C: (target, row-run) work items
-        const int nt = toff[WW];
-        for (int it = tid; it < 3 * nt; it += kThreads) {
-            const int row = (it >= nt) + (it >= 2 * nt);
-            const int t = it - row * nt;
-            const int j0 = tj0[t] + row * R;
+        // C: (unit, row-run) work items
+        const int nu = s_units;
+        for (int it = tid; it < 3 * nu; it += kThreads) {
+            const int row = (it >= nu) + (it >= 2 * nu);
+            const int u = it - row * nu;
+            const int j0 = uj0[u] + row * R;
             const int i0 = sstart[j0], i1 = sstart[j0 + 3];
+            T *pp = part + row * TPI * nu + TPI * u;
             if constexpr (sizeof(T) == 4) {
                 const float4 *A = reinterpret_cast<const float4 *>(src);
                 const float2 *Q = reinterpret_cast<const float2 *>(reinterpret_cast<const float *>(src) + 2 * a.src_cap);
-                part[it] = span_f32(A, Q, i0 >> 1, i1 >> 1, tu[t], tv[t]);
+                if constexpr (TPI == 2) {
+                    const int t0 = ut[2 * u], t1 = ut[2 * u + 1];
+                    span2_f32(A, Q, i0 >> 1, i1 >> 1, tu[t0], tv[t0], tu[t1], tv[t1], pp[0], pp[1]);
+                } else {
+                    const int t = ut[u];
+                    pp[0] = span_f32(A, Q, i0 >> 1, i1 >> 1, tu[t], tv[t]);
+                }
             } else {
+                const int t = ut[u];
                 const double *su = reinterpret_cast<const double *>(src);
-                part[it] = span_f64(su, su + a.src_cap, su + 2 * a.src_cap, i0, i1, tu[t], tv[t], a.eps2);
+                pp[0] = span_f64(su, su + a.src_cap, su + 2 * a.src_cap, i0, i1, tu[t], tv[t], a.eps2);
             }
         }
         __syncthreads();
 
         // D: fixed-order reduction of the three row partials, write
+        const int rs = TPI * nu;
         for (int t = tid; t < nt; t += kThreads) {
-            T acc = part[t] + part[nt + t] + part[2 * nt + t];
+            const int sl = tslot[t];
+            T acc = part[sl] + part[rs + sl] + part[2 * rs + sl];
             T phi;
             if constexpr (sizeof(T) == 4) {
                 if (!isfinite(acc)) {  // a pair closer than eps: redo this target with the explicit guard
                     const float4 *A = reinterpret_cast<const float4 *>(src);
                     const float2 *Q = reinterpret_cast<const float2 *>(reinterpret_cast<const float *>(src) + 2 * a.src_cap);
                     acc = 0.f;
+                    const int jb = uj0[sl / TPI];
                     for (int row = 0; row < 3; ++row) {
-                        const int j0 = tj0[t] + row * R;
+                        const int j0 = jb + row * R;
                         acc += span_f32_guarded(A, Q, sstart[j0] >> 1, sstart[j0 + 3] >> 1, tu[t], tv[t], a.eps2);
                     }
                 }
@@ -389,14 +464,17 @@ p2p_r_kernel(const P2PArgs<T> a) {
             hoff[i] = (int)(a.halo_off[m0 + i] - hb);
         }
         __syncthreads();
-        for (int bl = wid; bl < WW; bl += kThreads / 32) {
-            const int t0 = toff[bl], t1 = toff[bl + 1];
-            for (int t = t0 + lane; t < t1; t += 32) {
-                const typename V2<T>::type uv = a.tgt_uv[tb + t];
-                tu[t] = uv.x;
-                tv[t] = uv.y;
-                tbx[t] = bl;
+        for (int t = tid; t < toff[WW]; t += kThreads) {
+            int lo = 0, hi = WW;  // last box bl with toff[bl] <= t
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (toff[mid] <= t) lo = mid;
+                else hi = mid;
             }
+            const typename V2<T>::type uv = a.tgt_uv[tb + t];
+            tu[t] = uv.x;
+            tv[t] = uv.y;
+            tbx[t] = lo;
         }
         asm volatile(
             "{\n\t.reg .pred P;\n"
@@ -439,6 +517,171 @@ p2p_r_kernel(const P2PArgs<T> a) {
                     acc = span_f32_guarded(reinterpret_cast<const float4 *>(s_uv),
                                            reinterpret_cast<const float2 *>(s_q), hoff[bl] >> 1, hoff[bl + 1] >> 1,
                                            tu[t], tv[t], a.eps2);
+                }
+                phi = (-0.5f * kLn2) * acc;
+            } else {
+                phi = -0.5 * acc;
+            }
+            a.out[tb + t] = a.accumulate ? a.out[tb + t] + phi : phi;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- TILED kernel
+// The TILED layout packs each tile's region (tile + one-box ring) at plan time
+// in the staging order the NR kernel would build at run time.  Per tile: one
+// elected thread issues TMA bulk copies (cp.async.bulk, mbarrier completion)
+// of the region coordinates, its per-entry source index and the row-run
+// table, while the CTA loads the tile's targets; after the barrier the
+// weights are gathered through the index (q stays in plan order, L2-resident
+// for the density sweep); then the same (unit, row-run) items and
+// fixed-order reduction as the NR kernel.
+template <typename T, int TPI>
+__global__ void __launch_bounds__(kThreads)
+p2p_tiled_kernel(const P2PArgs<T> a) {
+    static_assert(TPI == 1 || (TPI == 2 && sizeof(T) == 4), "TPI = 2 is the fp32 path");
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ int s_tile, s_units;
+    const int k = a.k, W = 1 << k, R = W + 2, WW = W * W;
+    const TCarve c = tiled_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI);
+    uint16_t *table = reinterpret_cast<uint16_t *>(smem + c.table);
+    int *toff = reinterpret_cast<int *>(smem + c.toff);
+    int *pstart = reinterpret_cast<int *>(smem + c.pstart);
+    int *uj0 = reinterpret_cast<int *>(smem + c.uj0);
+    int *ut = reinterpret_cast<int *>(smem + c.ut);
+    int *tslot = reinterpret_cast<int *>(smem + c.tslot);
+    T *tu = reinterpret_cast<T *>(smem + c.tu);
+    T *tv = reinterpret_cast<T *>(smem + c.tv);
+    T *part = reinterpret_cast<T *>(smem + c.part);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + c.bar);
+    T *s_uv = reinterpret_cast<T *>(smem + c.src);
+    int32_t *s_idx = reinterpret_cast<int32_t *>(smem + c.q);
+    T *s_q = reinterpret_cast<T *>(smem + c.q + 4 * a.src_cap);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t bar = smem_addr(mbar);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    uint32_t parity = 0;
+
+    for (int ti = next_tile(a.queue, &s_tile); ti < a.ntiles; ti = next_tile(a.queue, &s_tile)) {
+        const uint32_t m0 = (uint32_t)a.tiles[ti] << (2 * k);
+        const int slot = a.tile_slot[ti];
+        const int tb = a.tgt_off[m0];
+        const uint32_t rb = a.reg_off[slot], nent = a.reg_off[slot + 1] - rb;  // multiple of 4
+        if (tid == 0) {
+            const uint32_t b_uv = nent * 2 * (uint32_t)sizeof(T), b_ix = nent * 4u, b_tab = (uint32_t)c.tstride * 2u;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                         "r"(b_uv + b_ix + b_tab)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(table)),
+                "l"(a.reg_table + (size_t)slot * c.tstride), "r"(b_tab), "r"(bar)
+                : "memory");
+            if (nent) {
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_addr(s_uv)),
+                    "l"(a.reg_uv + 2 * (size_t)rb), "r"(b_uv), "r"(bar)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_addr(s_idx)),
+                    "l"(a.reg_idx + rb), "r"(b_ix), "r"(bar)
+                    : "memory");
+            }
+        }
+        for (int i = tid; i <= WW; i += kThreads) toff[i] = a.tgt_off[m0 + i] - tb;
+        __syncthreads();
+        if (wid == 0) {  // units: TPI targets of one box
+            int carry = 0;
+            for (int base = 0; base < WW; base += 32) {
+                const int bl = base + lane;
+                const int n = bl < WW ? toff[bl + 1] - toff[bl] : 0;
+                const int np = TPI == 2 ? (n + 1) >> 1 : n;
+                const int incl = warp_incl_scan(np);
+                if (bl < WW) pstart[bl] = carry + incl - np;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (lane == 0) s_units = carry;
+        }
+        __syncthreads();
+        const int nt = toff[WW];
+        for (int t = tid; t < nt; t += kThreads) {
+            const int bl = a.tgt_bl[tb + t];
+            const typename V2<T>::type uv = a.tgt_ruv[tb + t];
+            tu[t] = uv.x;
+            tv[t] = uv.y;
+            const int r = t - toff[bl], u = pstart[bl] + r / TPI, sl = r % TPI;
+            ut[TPI * u + sl] = t;
+            tslot[t] = TPI * u + sl;
+            if (sl == 0) {
+                uj0[u] = (int)compact16((uint32_t)bl >> 1) * R + (int)compact16((uint32_t)bl);
+                if (TPI == 2 && t + 1 == toff[bl + 1]) ut[TPI * u + 1] = t;
+            }
+        }
+        asm volatile(
+            "{\n\t.reg .pred P;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+            "@!P bra WAIT_%=;\n}" ::"r"(bar),
+            "r"(parity)
+            : "memory");
+        parity ^= 1u;
+        for (int i = tid; i < (int)nent; i += kThreads) {  // weights through the per-entry index
+            const int32_t j = s_idx[i];
+            s_q[i] = j >= 0 ? a.q[j] : (T)0;
+        }
+        __syncthreads();
+
+        const int nu = s_units;
+        for (int it = tid; it < 3 * nu; it += kThreads) {
+            const int row = (it >= nu) + (it >= 2 * nu);
+            const int u = it - row * nu;
+            const int j0 = uj0[u] + row * R;
+            const int i0 = table[j0], i1 = table[j0 + 3];
+            T *pp = part + row * TPI * nu + TPI * u;
+            if constexpr (sizeof(T) == 4) {
+                const float4 *A = reinterpret_cast<const float4 *>(s_uv);
+                const float2 *Q = reinterpret_cast<const float2 *>(s_q);
+                if constexpr (TPI == 2) {
+                    const int t0 = ut[2 * u], t1 = ut[2 * u + 1];
+                    span2_f32(A, Q, i0 >> 1, i1 >> 1, tu[t0], tv[t0], tu[t1], tv[t1], pp[0], pp[1]);
+                } else {
+                    const int t = ut[u];
+                    pp[0] = span_f32(A, Q, i0 >> 1, i1 >> 1, tu[t], tv[t]);
+                }
+            } else {
+                const int t = ut[u];
+                double acc = 0.0;
+                for (int j = i0; j < i1; ++j) {
+                    const double du = tu[t] - s_uv[2 * j], dv = tv[t] - s_uv[2 * j + 1];
+                    const double r2 = fma(dv, dv, du * du);
+                    if (r2 >= a.eps2) acc = fma(s_q[j], log(r2), acc);
+                }
+                pp[0] = acc;
+            }
+        }
+        __syncthreads();
+
+        const int rs = TPI * nu;
+        for (int t = tid; t < nt; t += kThreads) {
+            const int sl = tslot[t];
+            T acc = part[sl] + part[rs + sl] + part[2 * rs + sl];
+            T phi;
+            if constexpr (sizeof(T) == 4) {
+                if (!isfinite(acc)) {
+                    const int jb = uj0[sl / TPI];
+                    acc = 0.f;
+                    for (int row = 0; row < 3; ++row) {
+                        const int j0 = jb + row * R;
+                        acc += span_f32_guarded(reinterpret_cast<const float4 *>(s_uv),
+                                                reinterpret_cast<const float2 *>(s_q), table[j0] >> 1,
+                                                table[j0 + 3] >> 1, tu[t], tv[t], a.eps2);
+                    }
                 }
                 phi = (-0.5f * kLn2) * acc;
             } else {

@@ -23,21 +23,31 @@ namespace p2p {
 P2P_HD inline int align16(int x) { return (x + 15) & ~15; }
 
 struct NrCarve {
-    int sstart, gstart, cnt, toff, tj0, tu, tv, part, src, total;
+    int sstart, gstart, cnt, toff, pstart, uj0, ut, tslot, tu, tv, part, src, total, ucap;
 };
-// src_cap: max padded region sources of a tile (multiple of 4); tgt_cap: max targets (multiple of 4).
-P2P_HD inline NrCarve nr_carve(int k, int src_cap, int tgt_cap, int e) {
+// NR layout.  src_cap: max padded region sources of a tile (multiple of 4);
+// tgt_cap: max targets of a tile (multiple of 4); tpi: targets per work unit
+// (1, or 2 = pairs of targets of the same box).
+P2P_HD inline int nr_unit_cap(int k, int tgt_cap, int tpi) {
+    const int WW = 1 << (2 * k);
+    return tpi == 2 ? (((tgt_cap + WW) / 2 + 4) & ~3) : tgt_cap;
+}
+P2P_HD inline NrCarve nr_carve(int k, int src_cap, int tgt_cap, int e, int tpi) {
     const int W = 1 << k, R = W + 2, RR = R * R, WW = W * W;
     NrCarve c;
+    c.ucap = nr_unit_cap(k, tgt_cap, tpi);
     c.sstart = 0;
     c.gstart = c.sstart + 4 * (RR + 1);
     c.cnt = c.gstart + 4 * RR;
     c.toff = c.cnt + 4 * RR;
-    c.tj0 = c.toff + 4 * (WW + 1);
-    c.tu = align16(c.tj0 + 4 * tgt_cap);
+    c.pstart = c.toff + 4 * (WW + 1);
+    c.uj0 = c.pstart + 4 * (WW + 1);
+    c.ut = c.uj0 + 4 * c.ucap;                      // unit -> its tpi targets
+    c.tslot = c.ut + 4 * tpi * c.ucap;              // target -> slot of its partials
+    c.tu = align16(c.tslot + 4 * tgt_cap);
     c.tv = align16(c.tu + e * tgt_cap);
     c.part = align16(c.tv + e * tgt_cap);
-    c.src = align16(c.part + 3 * e * tgt_cap);
+    c.src = align16(c.part + 3 * e * tpi * c.ucap);
     c.total = c.src + 3 * e * src_cap;
     return c;
 }
@@ -58,6 +68,35 @@ P2P_HD inline RCarve r_carve(int k, int src_cap, int tgt_cap, int e) {
     c.bar = align16(c.part + 3 * e * tgt_cap);
     c.src = align16(c.bar + 16);
     c.total = c.src + 3 * e * src_cap;
+    return c;
+}
+
+struct TCarve {
+    int table, toff, pstart, uj0, ut, tslot, tu, tv, part, bar, src, q, total, ucap, tstride;
+};
+// TILED layout.  src_cap: max packed-region entries of a tile (multiple of 4).
+P2P_HD inline int tiled_table_stride(int k) {
+    const int R = (1 << k) + 2;
+    return (R * R + 1 + 7) & ~7;  // uint16 entries, 16-B multiple for the bulk copy
+}
+P2P_HD inline TCarve tiled_carve(int k, int src_cap, int tgt_cap, int e, int tpi) {
+    const int WW = 1 << (2 * k);
+    TCarve c;
+    c.ucap = nr_unit_cap(k, tgt_cap, tpi);
+    c.tstride = tiled_table_stride(k);
+    c.table = 0;
+    c.toff = align16(c.table + 2 * c.tstride);
+    c.pstart = c.toff + 4 * (WW + 1);
+    c.uj0 = c.pstart + 4 * (WW + 1);
+    c.ut = c.uj0 + 4 * c.ucap;
+    c.tslot = c.ut + 4 * tpi * c.ucap;
+    c.tu = align16(c.tslot + 4 * tgt_cap);
+    c.tv = align16(c.tu + e * tgt_cap);
+    c.part = align16(c.tv + e * tgt_cap);
+    c.bar = align16(c.part + 3 * e * tpi * c.ucap);
+    c.src = align16(c.bar + 16);              // region coordinates (2 per entry) -- bulk copy dst
+    c.q = c.src + 2 * e * src_cap;            // region index (int32), then gathered weights
+    c.total = c.q + 4 * src_cap + e * src_cap;
     return c;
 }
 
@@ -101,6 +140,8 @@ struct Layout {
     std::vector<T> src_uv;   // [n_src_local][2] box-local coordinates (x - ix*h, y - iy*h)
     std::vector<T> tgt_uv;   // [n_tgt_local][2]
     std::vector<T> halo_uv;  // R: fp32 -> per source pair (u0,u1,v0,v1); fp64 -> (u,v) per entry
+    std::vector<T> reg_uv;   // TILED: region-relative, same pair packing as halo_uv
+    std::vector<T> tgt_ruv;  // TILED: [n_tgt_local][2] target coordinates relative to its tile's region origin
 };
 
 struct HostPlan {
@@ -138,6 +179,14 @@ struct HostPlan {
     std::vector<int32_t> halo_idx;                // local source index, -1 = pad
     int64_t halo_entries = 0;
 
+    // ---- TILED layout (per tile in Morton order = "slot")
+    std::vector<uint32_t> reg_off;                // [tiles+1] packed-region offsets
+    std::vector<int32_t> reg_idx;                 // local source index, -1 = pad
+    std::vector<uint16_t> reg_table;              // [tiles][tstride] region row-major box starts (relative)
+    std::vector<uint16_t> tgt_bl;                 // [n_tgt_local] tile-local Morton box index
+    std::vector<int32_t> tile_slot;               // launch order -> slot
+    int64_t reg_entries = 0;
+
     Layout<float> f32;
     Layout<double> f64;
 
@@ -146,6 +195,7 @@ struct HostPlan {
     int64_t boxes_in_tiles = 0, max_region = 0, max_tile_halo = 0, smem_bytes = 0;
     int64_t src_cap = 0, tgt_cap = 0;            // kernel smem capacities (multiples of 4)
     int group_log2 = 0;                          // NR staging lanes per region box (log2)
+    int tpi = 1;                                 // targets per work unit (2 for dense fp32 NR)
     bool lpt = false;                            // tiles queued by decreasing pairs (working set fits L2)
     double density = 0.0, density_occ = 0.0, build_seconds = 0.0;
 };

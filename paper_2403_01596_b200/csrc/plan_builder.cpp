@@ -131,7 +131,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     auto t0 = std::chrono::steady_clock::now();
     if (d.struct_size != sizeof(p2p_plan_desc)) fail(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
     if (d.kernel != P2P_KERNEL_LAPLACE_2D) fail(P2P_ERROR_NOT_SUPPORTED, "only P2P_KERNEL_LAPLACE_2D");
-    if (d.layout != P2P_LAYOUT_NONREDUNDANT && d.layout != P2P_LAYOUT_REDUNDANT)
+    if (d.layout != P2P_LAYOUT_NONREDUNDANT && d.layout != P2P_LAYOUT_REDUNDANT && d.layout != P2P_LAYOUT_TILED)
         fail(P2P_ERROR_INVALID_ARGUMENT, "bad layout");
     if (d.precision != P2P_FP32 && d.precision != P2P_FP64) fail(P2P_ERROR_INVALID_ARGUMENT, "bad precision");
     if (!(d.epsilon > 0.0) || !std::isfinite(d.epsilon)) fail(P2P_ERROR_INVALID_ARGUMENT, "epsilon must be > 0");
@@ -203,9 +203,20 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     if (d.tile_log2 >= 0) {
         k = std::min(d.tile_log2, kmax);
     } else {
-        double dd = std::max(hp.density_occ, 1e-3);
-        k = (int)std::lround(std::log(256.0 / dd) / std::log(4.0));
-        k = std::max(0, std::min(k, kmax));
+        // smallest k whose non-empty tiles hold >= ~256 targets on average (256 = CTA size)
+        k = kmax;
+        for (int kk = 0; kk <= kmax; ++kk) {
+            const int64_t WWk = int64_t(1) << (2 * kk);
+            int64_t ne = 0;
+            for (int64_t t = 0; t < hp.B / WWk; ++t) ne += to[(t + 1) * WWk] > to[t * WWk];
+            if ((double)hp.n_tgt / (double)std::max<int64_t>(ne, 1) >= 0.75 * kThreads) {
+                k = kk;
+                break;
+            }
+        }
+        // the R layout stages 9x the sources: keep its tile halo modest so >= 4 CTAs fit per SM
+        if (d.layout == P2P_LAYOUT_REDUNDANT)
+            while (k > 0 && 9.0 * hp.density_occ * (double)(int64_t(1) << (2 * k)) * 3 * e > 48.0 * 1024) --k;
     }
     for (;; --k) {
         const int64_t W = int64_t(1) << k, WW = W * W, R = W + 2;
@@ -246,10 +257,12 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         hp.max_region = region.empty() ? 0 : *std::max_element(region.begin(), region.end());
         hp.max_tile_halo = halo.empty() ? 0 : *std::max_element(halo.begin(), halo.end());
         hp.tgt_cap = pad4(tcount.empty() ? 0 : *std::max_element(tcount.begin(), tcount.end()));
-        hp.src_cap = d.layout == P2P_LAYOUT_NONREDUNDANT ? pad4(hp.max_region) : hp.max_tile_halo;
-        int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT
-                           ? (int64_t)nr_carve(k, (int)std::min<int64_t>(hp.src_cap, 1 << 24), (int)std::min<int64_t>(hp.tgt_cap, 1 << 24), e).total
-                           : (int64_t)r_carve(k, (int)std::min<int64_t>(hp.src_cap, 1 << 24), (int)std::min<int64_t>(hp.tgt_cap, 1 << 24), e).total;
+        hp.src_cap = d.layout == P2P_LAYOUT_REDUNDANT ? hp.max_tile_halo : pad4(hp.max_region);
+        hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= 4.0 && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT) ? 2 : 1;
+        const int sc = (int)std::min<int64_t>(hp.src_cap, 1 << 24), tc = (int)std::min<int64_t>(hp.tgt_cap, 1 << 24);
+        int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? (int64_t)nr_carve(k, sc, tc, e, hp.tpi).total
+                       : d.layout == P2P_LAYOUT_TILED      ? (int64_t)tiled_carve(k, sc, tc, e, hp.tpi).total
+                                                           : (int64_t)r_carve(k, sc, tc, e).total;
         hp.smem_bytes = smem;
         if (smem <= kSmemLimit) break;
         if (k == 0 || d.tile_log2 >= 0)
@@ -465,12 +478,102 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             }
         }, 64);
     }
+    // ---- TILED layout: per local tile (Morton order = slot), its region (tile +
+    // one-box ring) in row-major box order, each box padded to an even count,
+    // each tile to 4 entries; coordinates relative to the region origin
+    // ((tx*W - 1) h, (ty*W - 1) h), computed in fp64 and rounded once.
+    const int64_t nlt = (int64_t)hp.tiles.size();
+    hp.tile_slot.resize((size_t)nlt);
+    std::iota(hp.tile_slot.begin(), hp.tile_slot.end(), 0);
+    if (d.layout == P2P_LAYOUT_TILED) {
+        const int ts = tiled_table_stride(k);
+        hp.reg_off.assign((size_t)nlt + 1, 0);
+        hp.reg_table.assign((size_t)nlt * ts, 0);
+        for (int64_t i = 0; i < nlt; ++i) {  // sizes and tables
+            uint32_t tx, ty;
+            morton_decode((uint32_t)hp.tiles[i], tx, ty);
+            const int64_t X0 = (int64_t)tx * W - 1, Y0 = (int64_t)ty * W - 1;
+            int64_t run = 0;
+            for (int64_t j = 0; j < R * R; ++j) {
+                hp.reg_table[i * ts + j] = (uint16_t)run;
+                const int64_t x = X0 + j % R, y = Y0 + j / R;
+                if (x < 0 || y < 0 || x >= S || y >= S) continue;
+                const uint32_t m = morton_encode((uint32_t)x, (uint32_t)y);
+                run += pad2(hp.src_off[m + 1] - hp.src_off[m]);
+            }
+            if (run > 65535) fail(P2P_ERROR_NOT_SUPPORTED, "TILED region exceeds 65535 entries; use NR");
+            hp.reg_table[i * ts + R * R] = (uint16_t)run;
+            hp.reg_off[i + 1] = hp.reg_off[i] + (uint32_t)pad4(run);
+        }
+        hp.reg_entries = hp.reg_off[nlt];
+        hp.reg_idx.assign((size_t)hp.reg_entries, -1);
+        const double PADC = 1.0e4;
+        const bool f32 = d.precision == P2P_FP32;
+        if (f32) hp.f32.reg_uv.assign((size_t)hp.reg_entries * 2, (float)PADC);
+        else hp.f64.reg_uv.assign((size_t)hp.reg_entries * 2, PADC);
+        const double *sxy = d.src_xy;
+        parallel_for(nlt, [&](int64_t a, int64_t bnd) {
+            for (int64_t i = a; i < bnd; ++i) {
+                uint32_t tx, ty;
+                morton_decode((uint32_t)hp.tiles[i], tx, ty);
+                const int64_t X0 = (int64_t)tx * W - 1, Y0 = (int64_t)ty * W - 1;
+                const double ox = X0 * hp.h, oy = Y0 * hp.h;
+                for (int64_t j = 0; j < R * R; ++j) {
+                    const int64_t x = X0 + j % R, y = Y0 + j / R;
+                    if (x < 0 || y < 0 || x >= S || y >= S) continue;
+                    const uint32_t m = morton_encode((uint32_t)x, (uint32_t)y);
+                    int64_t ent = hp.reg_off[i] + hp.reg_table[i * ts + j];
+                    for (int32_t sj = hp.src_off[m]; sj < hp.src_off[m + 1]; ++sj, ++ent) {
+                        const int64_t u = hp.src_uidx[sj];
+                        const double rx = sxy[2 * u] - ox, ry = sxy[2 * u + 1] - oy;
+                        hp.reg_idx[ent] = sj;
+                        if (f32) {
+                            const int64_t p = ent >> 1, sl = ent & 1;
+                            hp.f32.reg_uv[4 * p + sl] = (float)rx;
+                            hp.f32.reg_uv[4 * p + 2 + sl] = (float)ry;
+                        } else {
+                            hp.f64.reg_uv[2 * ent] = rx;
+                            hp.f64.reg_uv[2 * ent + 1] = ry;
+                        }
+                    }
+                }
+            }
+        }, 64);
+        // targets: coordinates relative to their tile's region origin + tile-local box index
+        hp.tgt_bl.assign((size_t)hp.n_tgt_local, 0);
+        if (f32) hp.f32.tgt_ruv.assign((size_t)hp.n_tgt_local * 2, 0.f);
+        else hp.f64.tgt_ruv.assign((size_t)hp.n_tgt_local * 2, 0.0);
+        const double *txy = d.tgt_xy;
+        parallel_for(nlt, [&](int64_t a, int64_t bnd) {
+            for (int64_t i = a; i < bnd; ++i) {
+                const uint32_t t = (uint32_t)hp.tiles[i];
+                uint32_t tx, ty;
+                morton_decode(t, tx, ty);
+                const double ox = ((int64_t)tx * W - 1) * hp.h, oy = ((int64_t)ty * W - 1) * hp.h;
+                for (int64_t bl = 0; bl < WW; ++bl) {
+                    const int64_t b = (int64_t)t * WW + bl;
+                    for (int32_t g = hp.tgt_off[b]; g < hp.tgt_off[b + 1]; ++g) {
+                        const int64_t u = hp.tgt_uidx[g];
+                        hp.tgt_bl[g] = (uint16_t)bl;
+                        if (f32) {
+                            hp.f32.tgt_ruv[2 * g] = (float)(txy[2 * u] - ox);
+                            hp.f32.tgt_ruv[2 * g + 1] = (float)(txy[2 * u + 1] - oy);
+                        } else {
+                            hp.f64.tgt_ruv[2 * g] = txy[2 * u] - ox;
+                            hp.f64.tgt_ruv[2 * g + 1] = txy[2 * u + 1] - oy;
+                        }
+                    }
+                }
+            }
+        }, 64);
+    }
+
     // ---- queue order of this partition's tiles: when the working set fits
     // comfortably in L2, longest tiles first (LPT) to shorten the tail; else
     // Morton order, so concurrently running CTAs share their halo rings in L2.
     {
         const int64_t ws = (hp.n_src_local + hp.n_tgt_local) * 3 * (int64_t)e + 8 * hp.boxes_in_tiles +
-                           hp.halo_entries * 3 * (int64_t)e;
+                           (hp.halo_entries + hp.reg_entries) * 3 * (int64_t)e;
         hp.lpt = ws < (int64_t)48 << 20;
         if (hp.lpt) {
             const int64_t base = hp.part_tile[r];
@@ -479,9 +582,13 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
                 return hp.tile_pairs_g[base + x] > hp.tile_pairs_g[base + y];
             });
-            std::vector<int32_t> t2(hp.tiles.size());
-            for (size_t i = 0; i < order.size(); ++i) t2[i] = hp.tiles[order[i]];
+            std::vector<int32_t> t2(hp.tiles.size()), s2(hp.tiles.size());
+            for (size_t i = 0; i < order.size(); ++i) {
+                t2[i] = hp.tiles[order[i]];
+                s2[i] = hp.tile_slot[order[i]];
+            }
             hp.tiles.swap(t2);
+            hp.tile_slot.swap(s2);
         }
     }
     hp.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -31,6 +31,7 @@ P2P_ERROR_NO_DEVICE = 7
 P2P_KERNEL_LAPLACE_2D = 0
 P2P_LAYOUT_NONREDUNDANT = 0
 P2P_LAYOUT_REDUNDANT = 1
+P2P_LAYOUT_TILED = 2
 P2P_FP64 = 0
 P2P_FP32 = 1
 P2P_ORDER_PLAN = 0
@@ -39,7 +40,7 @@ P2P_ORDER_USER = 1
 EXPORT = {
     "src_perm": 0, "tgt_perm": 1, "src_box_offsets": 2, "tgt_box_offsets": 3,
     "neighbors": 4, "partition": 5, "src_global": 6, "halo_counts": 7, "tiles": 8,
-    "halo_index": 9, "send_index": 10, "halo_offsets": 11,
+    "halo_index": 9, "send_index": 10, "halo_offsets": 11, "region_offsets": 12, "region_index": 13,
 }
 
 # Symbols declared in include/p2p.h (checked by tests/test_abi.py).
@@ -187,7 +188,8 @@ class Plan:
     """A P2P plan: ``Plan(src_xy, tgt_xy, level=...)`` then ``plan.apply(q, out)``.
 
     src_xy / tgt_xy: numpy float64 [n, 2] in [0,1]^2 (copied by the library).
-    layout: "nr" (non-redundant) or "r" (redundant); precision: "fp32" or "fp64".
+    layout: "nr" (non-redundant), "r" (redundant per box) or "tiled" (redundant on
+    the tile ring only); precision: "fp32" or "fp64".
     device: CUDA ordinal, or -1 for a host-only plan (build + export only).
     """
 
@@ -205,7 +207,7 @@ class Plan:
         d.tgt_xy = self._tgt.ctypes.data
         d.level, d.ct, d.l_start, d.l_max, d.level_delta = level, ct, l_start, l_max, level_delta
         d.epsilon = epsilon
-        d.layout = {"nr": P2P_LAYOUT_NONREDUNDANT, "r": P2P_LAYOUT_REDUNDANT}[layout]
+        d.layout = {"nr": P2P_LAYOUT_NONREDUNDANT, "r": P2P_LAYOUT_REDUNDANT, "tiled": P2P_LAYOUT_TILED}[layout]
         d.precision = {"fp32": P2P_FP32, "fp64": P2P_FP64}[precision]
         d.device, d.tile_log2, d.stream = device, tile_log2, stream or None
         d.part_world, d.part_rank = part_world, part_rank

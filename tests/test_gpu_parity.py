@@ -17,7 +17,7 @@ torch = pytest.importorskip("torch")
 
 TOL = {"fp32": 1e-5, "fp64": 1e-12}
 TOL_EL = {"fp32": 2e-5, "fp64": 1e-12}
-COMBOS = [(lay, prec) for lay in ("nr", "r") for prec in ("fp32", "fp64")]
+COMBOS = [(lay, prec) for lay in ("nr", "r", "tiled") for prec in ("fp32", "fp64")]
 
 
 def rel_l2(a, b):
@@ -145,7 +145,7 @@ def test_deterministic(layout, prec):
     np.testing.assert_array_equal(a, b)
 
 
-@pytest.mark.parametrize("layout,prec", [("nr", "fp32"), ("r", "fp32"), ("nr", "fp64")])
+@pytest.mark.parametrize("layout,prec", [("nr", "fp32"), ("r", "fp32"), ("tiled", "fp32"), ("nr", "fp64")])
 @pytest.mark.parametrize("world", [2, 3])
 def test_partitions_bit_identical(layout, prec, world):
     """Results are bit-identical for any number of partitions:
@@ -182,7 +182,7 @@ FULL = ["d16_1e6", "d32_1e6", "d64_1e6", "lowd025_1e7", "lowd1_1e7", "lowd2_1e7"
 
 
 @pytest.mark.parametrize("cfg", FULL)
-@pytest.mark.parametrize("layout,prec", [("nr", "fp32"), ("r", "fp32"), ("nr", "fp64")])
+@pytest.mark.parametrize("layout,prec", [("nr", "fp32"), ("r", "fp32"), ("tiled", "fp32"), ("nr", "fp64"), ("tiled", "fp64")])
 def test_full_size_sampled(cfg, layout, prec):
     """BASELINE.json sizes, bench launch configuration; oracle on 3000 sampled targets."""
     c = W.CONFIGS[cfg]

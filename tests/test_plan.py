@@ -142,3 +142,29 @@ def test_partition_covers_everything(world):
         tp = p.export("tgt_perm")
         for t in tp[:: max(1, len(tp) // 50)]:
             assert _e1_sources(src, tgt[t], level) <= loc
+
+
+def test_tiled_region_interaction_set():
+    """TILED layout: the packed region of each tile holds exactly the sources of
+    the tile's boxes and their one-box ring (each once), so every target's E1
+    set is covered."""
+    src, tgt, _ = W.uniform_unit(2500, 29)
+    level = 6
+    for tile in (0, 1, 2):
+        pl = _plan(src, tgt, level=level, layout="tiled", tile_log2=tile)
+        roff = pl.export("region_offsets")
+        ridx = pl.export("region_index")
+        sperm = pl.export("src_perm")
+        tiles_launch = pl.export("tiles")
+        assert roff[-1] == len(ridx) and np.all(np.diff(roff) % 4 == 0)
+        S = 1 << (level - 1)
+        W_ = 1 << tile
+        for slot, t in enumerate(np.sort(tiles_launch)):  # slots are Morton tile order
+            ent = ridx[roff[slot]:roff[slot + 1]]
+            got = sperm[ent[ent >= 0]]
+            assert len(set(got.tolist())) == len(got)
+            tx, ty = oracle.morton_decode(int(t), level - tile)
+            x0, y0 = tx * W_ - 1, ty * W_ - 1
+            bs = np.minimum(np.floor(src * S), S - 1)
+            inside = (bs[:, 0] >= x0) & (bs[:, 0] <= x0 + W_ + 1) & (bs[:, 1] >= y0) & (bs[:, 1] <= y0 + W_ + 1)
+            assert set(got.tolist()) == set(np.nonzero(inside)[0].tolist())
