@@ -134,6 +134,13 @@ p2p_status p2p_apply(p2p_plan plan, const void *d_q, void *d_out, int32_t order,
 p2p_status p2p_apply_host(p2p_plan plan, const void *h_q, void *h_out, int32_t order,
                           int32_t accumulate, void *stream);
 
+/* Asynchronous variant of p2p_apply_host: enqueues the H2D copy, the apply and
+ * the D2H copy on `stream` and returns; h_q / h_out must stay valid (and, for
+ * overlap, be pinned) until the caller synchronises the stream.  Applies on
+ * different plans and streams overlap their copies with each other's kernels. */
+p2p_status p2p_apply_host_async(p2p_plan plan, const void *h_q, void *h_out, int32_t order,
+                                int32_t accumulate, void *stream);
+
 /* Distributed apply (part_world > 1, weights NOT replicated): phi for this
  * partition's targets (plan order, n_tgt_local) from
  *   d_q_owned: device, n_src_owned weights this partition owns, in plan order

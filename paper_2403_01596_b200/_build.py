@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps = [os.path.join(CSRC, f) for f in DEPS] + [os.path.join(INCLUDE, "p2p.h")]
     if force or stale(LIB, deps):
         _nvcc([os.path.join(CSRC, s) for s in SOURCES], LIB, "ptxas.log", verbose)
-    pdeps = [os.path.join(CSRC, "peaks.cu"), os.path.join(INCLUDE, "p2p_peaks.h")]
+    pdeps = [os.path.join(CSRC, "peaks.cu"), os.path.join(INCLUDE, "p2p_peaks.h"),
+             os.path.join(CSRC, "p2p_kernels.cuh")]
     if force or stale(PEAKS_LIB, pdeps):
         _nvcc([os.path.join(CSRC, "peaks.cu")], PEAKS_LIB, "ptxas_peaks.log", verbose)
     return LIB

@@ -44,7 +44,7 @@ struct p2p_plan_s {
     // device arrays
     DevBuf tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
-    DevBuf tile_slot, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_ruv;
+    DevBuf tile_slot, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     int grid = 0;                                // persistent CTAs per launch
     int64_t device_bytes = 0;
@@ -68,7 +68,8 @@ struct p2p_plan_s {
     void release() {
         DevBuf *all[] = {&tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
-                         &tile_slot, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_ruv, &q_local, &phi,
+                         &tile_slot, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_ruv,
+                         &tgt_pack_off, &tile_tgt_base, &q_local, &phi,
                          &io_q, &io_out, &queue};
         for (DevBuf *b : all) {
             if (b->p) cudaFree(b->p);
@@ -86,6 +87,25 @@ template <>
 const p2p::Layout<float> &layout_of<float>(const p2p::HostPlan &hp) { return hp.f32; }
 template <>
 const p2p::Layout<double> &layout_of<double>(const p2p::HostPlan &hp) { return hp.f64; }
+
+// TILED kernel instance for the plan's options (element type, targets per unit, CTA size, padding).
+template <typename T>
+const void *tiled_fn(int tpi, int nt, bool pad) {
+    using namespace p2p::dev;
+    if constexpr (sizeof(T) == 4) {
+        if (tpi == 2)
+            return nt == 128 ? (const void *)p2p_tiled_kernel<float, 2, 128, true>
+                             : (const void *)p2p_tiled_kernel<float, 2, 256, true>;
+        if (pad)
+            return nt == 128 ? (const void *)p2p_tiled_kernel<float, 1, 128, true>
+                             : (const void *)p2p_tiled_kernel<float, 1, 256, true>;
+        return nt == 128 ? (const void *)p2p_tiled_kernel<float, 1, 128, false>
+                         : (const void *)p2p_tiled_kernel<float, 1, 256, false>;
+    } else {
+        return nt == 128 ? (const void *)p2p_tiled_kernel<double, 1, 128, false>
+                         : (const void *)p2p_tiled_kernel<double, 1, 256, false>;
+    }
+}
 
 template <typename T>
 void upload_plan(p2p_plan_s &P) {
@@ -112,6 +132,8 @@ void upload_plan(p2p_plan_s &P) {
         P.upload(P.reg_table, hp.reg_table);
         P.upload(P.tgt_bl, hp.tgt_bl);
         P.upload(P.tgt_ruv, lay.tgt_ruv);
+        P.upload(P.tgt_pack_off, hp.tgt_pack_off);
+        P.upload(P.tile_tgt_base, hp.tile_tgt_base);
     } else {
         P.upload(P.halo_off, hp.halo_off);
         P.upload(P.halo_idx, hp.halo_idx);
@@ -123,13 +145,12 @@ void upload_plan(p2p_plan_s &P) {
     const bool two = hp.tpi == 2;
     const void *kfn = hp.layout == P2P_LAYOUT_REDUNDANT ? (const void *)p2p::dev::p2p_r_kernel<T>
                       : hp.layout == P2P_LAYOUT_TILED
-                          ? (two ? (const void *)p2p::dev::p2p_tiled_kernel<T, sizeof(T) == 4 ? 2 : 1>
-                                 : (const void *)p2p::dev::p2p_tiled_kernel<T, 1>)
+                          ? tiled_fn<T>(hp.tpi, hp.nt, hp.pad)
                           : (two ? (const void *)p2p::dev::p2p_nr_kernel<T, sizeof(T) == 4 ? 2 : 1>
                                  : (const void *)p2p::dev::p2p_nr_kernel<T, 1>);
     ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2p::kSmemLimit), "smem attr");
     int occ = 0, dev = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, p2p::kThreads, (size_t)hp.smem_bytes), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, hp.nt, (size_t)hp.smem_bytes), "occupancy");
     ck(cudaGetDevice(&dev), "cudaGetDevice");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
     P.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)hp.tiles.size(), (int64_t)std::max(occ, 1) * sms));
@@ -183,11 +204,15 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.reg_uv = (const T *)P.reg_uv.p;
         a.reg_table = (const uint16_t *)P.reg_table.p;
         a.tgt_bl = (const uint16_t *)P.tgt_bl.p;
-        a.tgt_ruv = (const typename p2p::dev::V2<T>::type *)P.tgt_ruv.p;
-        if (hp.tpi == 2)
-            p2p::dev::p2p_tiled_kernel<T, sizeof(T) == 4 ? 2 : 1><<<P.grid, p2p::kThreads, hp.smem_bytes, s>>>(a);
-        else
-            p2p::dev::p2p_tiled_kernel<T, 1><<<P.grid, p2p::kThreads, hp.smem_bytes, s>>>(a);
+        a.tgt_ruv = (const T *)P.tgt_ruv.p;
+        a.tgt_pack_off = (const uint32_t *)P.tgt_pack_off.p;
+        a.tile_tgt_base = (const int32_t *)P.tile_tgt_base.p;
+        a.ns = hp.ns;
+        a.nbuf = hp.nbuf;
+        void *args[] = {&a};
+        ck(cudaLaunchKernel(tiled_fn<T>(hp.tpi, hp.nt, hp.pad), dim3(P.grid), dim3(hp.nt), args,
+                            (size_t)hp.smem_bytes, s),
+           "tiled launch");
     } else {
         if (hp.halo_entries > 0)
             p2p::dev::pack_r_kernel<T><<<grid_for(hp.halo_entries), 256, 0, s>>>(
@@ -337,8 +362,8 @@ p2p_status p2p_apply(p2p_plan P, const void *d_q, void *d_out, int32_t order, in
     });
 }
 
-p2p_status p2p_apply_host(p2p_plan P, const void *h_q, void *h_out, int32_t order, int32_t accumulate,
-                          void *stream) {
+static p2p_status apply_host_common(p2p_plan P, const void *h_q, void *h_out, int32_t order, int32_t accumulate,
+                                    void *stream, bool sync) {
     if (!P || !h_q || !h_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or buffer");
     if (order != P2P_ORDER_PLAN && order != P2P_ORDER_USER) return set_error(P2P_ERROR_INVALID_ARGUMENT, "bad order");
     return guarded([&] {
@@ -353,8 +378,18 @@ p2p_status p2p_apply_host(p2p_plan P, const void *h_q, void *h_out, int32_t orde
         if (P->elem == 4) apply_impl<float>(*P, P->io_q.p, P->io_out.p, order, accumulate ? 1 : 0, s);
         else apply_impl<double>(*P, P->io_q.p, P->io_out.p, order, accumulate ? 1 : 0, s);
         ck(cudaMemcpyAsync(h_out, P->io_out.p, ob, cudaMemcpyDeviceToHost, s), "D2H out");
-        ck(cudaStreamSynchronize(s), "apply_host sync");
+        if (sync) ck(cudaStreamSynchronize(s), "apply_host sync");
     });
+}
+
+p2p_status p2p_apply_host(p2p_plan P, const void *h_q, void *h_out, int32_t order, int32_t accumulate,
+                          void *stream) {
+    return apply_host_common(P, h_q, h_out, order, accumulate, stream, true);
+}
+
+p2p_status p2p_apply_host_async(p2p_plan P, const void *h_q, void *h_out, int32_t order, int32_t accumulate,
+                                void *stream) {
+    return apply_host_common(P, h_q, h_out, order, accumulate, stream, false);
 }
 
 p2p_status p2p_apply_dist(p2p_plan P, const void *d_q_owned, const void *d_q_halo, void *d_out, int32_t accumulate,
@@ -444,9 +479,8 @@ p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *info) {
     } else if (hp.layout == P2P_LAYOUT_TILED) {
         // targets: region-relative coords + box byte pair + out + CSR offset; region: coords + index;
         // tables; weights gathered once from plan order
-        info->alg_bytes_kernel = hp.n_tgt_local * (3 * e + 2) + 4 * hp.boxes_in_tiles +
-                                 hp.reg_entries * (2 * e + 4) + (int64_t)hp.reg_table.size() * 2 +
-                                 hp.n_src_local * e;
+        info->alg_bytes_kernel = hp.n_tgt_local * (3 * e + 2) + hp.reg_entries * (2 * e + 4) +
+                                 (int64_t)hp.reg_table.size() * 2 + hp.n_src_local * e;
         info->alg_bytes_apply = info->alg_bytes_kernel;
     } else {
         info->alg_bytes_kernel = hp.n_tgt_local * 3 * e + hp.halo_entries * 3 * e + offs;

@@ -134,6 +134,42 @@ __device__ __forceinline__ void span2_f32(const float4 *__restrict__ A, const fl
     r1 = c0 + c1;
 }
 
+// Unpadded fp32 layout (sparse tiles): (u, v) per entry + q per entry, one
+// pair per step.  Returns sum q * lg2(r^2) (non-finite if some r^2 underflows).
+__device__ __forceinline__ float span1_f32(const float2 *__restrict__ UV, const float *__restrict__ Q, int j0, int j1,
+                                           float ut, float vt) {
+    float acc = 0.f;
+#pragma unroll 2
+    for (int j = j0; j < j1; ++j) {
+        const float2 s = UV[j];
+        const float du = ut - s.x, dv = vt - s.y;
+        acc = fmaf(Q[j], lg2_approx(fmaf(dv, dv, du * du)), acc);
+    }
+    return acc;
+}
+__device__ __noinline__ float span1_f32_guarded(const float2 *__restrict__ UV, const float *__restrict__ Q, int j0,
+                                                int j1, float ut, float vt, float eps2) {
+    float acc = 0.f;
+    for (int j = j0; j < j1; ++j) {
+        const float du = ut - UV[j].x, dv = vt - UV[j].y;
+        const float r2 = fmaf(dv, dv, du * du);
+        if (r2 >= eps2) acc = fmaf(Q[j], lg2_approx(r2), acc);
+    }
+    return acc;
+}
+// fp64, (u, v) per entry, explicit guard.
+__device__ __forceinline__ double span1_f64(const double2 *__restrict__ UV, const double *__restrict__ Q, int j0,
+                                            int j1, double ut, double vt, double eps2) {
+    double acc = 0.0;
+    for (int j = j0; j < j1; ++j) {
+        const double2 s = UV[j];
+        const double du = ut - s.x, dv = vt - s.y;
+        const double r2 = fma(dv, dv, du * du);
+        if (r2 >= eps2) acc = fma(Q[j], log(r2), acc);
+    }
+    return acc;
+}
+
 // Explicitly guarded fp32 sweep (slow path for targets whose fast sum is not finite).
 __device__ __noinline__ float span_f32_guarded(const float4 *__restrict__ A, const float2 *__restrict__ Q,
                                                int p0, int p1, float ut, float vt, float eps2) {
@@ -188,9 +224,13 @@ struct P2PArgs {
     const uint32_t *reg_off;    // TILED: [slots+1] packed-region offsets
     const int32_t *reg_idx;     // TILED: local source index per packed entry (-1 = pad)
     const T *reg_uv;            // TILED: region-relative coordinates (fp32: (u0,u1,v0,v1) per pair)
-    const uint16_t *reg_table;  // TILED: [slots][tstride] row-major box starts within the region
-    const uint16_t *tgt_bl;     // TILED: tile-local Morton box of each target
-    const typename V2<T>::type *tgt_ruv;  // TILED: target coordinates relative to the region origin
+    const uint16_t *reg_table;  // TILED: [slots][tstride] region box starts, then target box starts
+    const uint16_t *tgt_bl;     // TILED: packed targets' tile-local Morton box
+    const T *tgt_ruv;           // TILED: packed targets' coordinates relative to the region origin
+    const uint32_t *tgt_pack_off;   // TILED: [slots+1] packed-target offsets (multiples of 8)
+    const int32_t *tile_tgt_base;   // TILED: plan index of each tile's first target
+    int ns;                     // TILED: work items per target (1 = whole target, 3 = one per row-run)
+    int nbuf;                   // TILED: 2 = prefetch the next tile's record during this tile
     T *out;
     int accumulate;
 };
@@ -528,167 +568,266 @@ p2p_r_kernel(const P2PArgs<T> a) {
 }
 
 // ---------------------------------------------------------------- TILED kernel
-// The TILED layout packs each tile's region (tile + one-box ring) at plan time
-// in the staging order the NR kernel would build at run time.  Per tile: one
-// elected thread issues TMA bulk copies (cp.async.bulk, mbarrier completion)
-// of the region coordinates, its per-entry source index and the row-run
-// table, while the CTA loads the tile's targets; after the barrier the
-// weights are gathered through the index (q stays in plan order, L2-resident
-// for the density sweep); then the same (unit, row-run) items and
-// fixed-order reduction as the NR kernel.
-template <typename T, int TPI>
-__global__ void __launch_bounds__(kThreads)
+// The TILED layout packs, per tile, everything the CTA needs contiguously at
+// plan time: a table record (region box starts + target box starts), the
+// region's sources (tile + one-box ring, rebased to the region origin, in
+// row-run order) with a per-entry source index, and the tile's targets.  One
+// elected thread bulk-copies a tile's record with TMA (cp.async.bulk,
+// mbarrier completion), optionally one tile ahead (NBUF = 2).  Weights are
+// gathered through the per-entry index (q stays in plan order).
+//   PAD  (dense fp32): boxes padded to even counts, sources packed per pair,
+//        packed f32x2 loops; TPI = 2 targets per unit share each LDS.
+//   !PAD (sparse, fp64): no padding, one pair per step.
+//   NS = 3: work items (unit, row-run) + fixed-order reduction of the three
+//   partials; NS = 1: one item per unit sweeps its three row-runs in order.
+template <typename T, int TPI, int NT, bool PAD>
+__global__ void __launch_bounds__(NT)
 p2p_tiled_kernel(const P2PArgs<T> a) {
-    static_assert(TPI == 1 || (TPI == 2 && sizeof(T) == 4), "TPI = 2 is the fp32 path");
+    static_assert(!(TPI == 2) || (PAD && sizeof(T) == 4), "TPI = 2 is the padded fp32 path");
+    static_assert(!PAD || sizeof(T) == 4, "the padded layout is fp32");
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ int s_tile, s_units;
-    const int k = a.k, W = 1 << k, R = W + 2, WW = W * W;
-    const TCarve c = tiled_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI);
-    uint16_t *table = reinterpret_cast<uint16_t *>(smem + c.table);
-    int *toff = reinterpret_cast<int *>(smem + c.toff);
+    __shared__ int s_next, s_units, s_base_next;
+    const int k = a.k, W = 1 << k, R = W + 2, RR = R * R, WW = W * W, NS = a.ns;
+    const TCarve c = tiled_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI, NS, a.nbuf);
+    const bool db = a.nbuf == 2;
+    T *s_q = reinterpret_cast<T *>(smem + c.q);
     int *pstart = reinterpret_cast<int *>(smem + c.pstart);
     int *uj0 = reinterpret_cast<int *>(smem + c.uj0);
     int *ut = reinterpret_cast<int *>(smem + c.ut);
     int *tslot = reinterpret_cast<int *>(smem + c.tslot);
-    T *tu = reinterpret_cast<T *>(smem + c.tu);
-    T *tv = reinterpret_cast<T *>(smem + c.tv);
     T *part = reinterpret_cast<T *>(smem + c.part);
     uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + c.bar);
-    T *s_uv = reinterpret_cast<T *>(smem + c.src);
-    int32_t *s_idx = reinterpret_cast<int32_t *>(smem + c.q);
-    T *s_q = reinterpret_cast<T *>(smem + c.q + 4 * a.src_cap);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t bar = smem_addr(mbar);
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    uint32_t parity = 0;
 
-    for (int ti = next_tile(a.queue, &s_tile); ti < a.ntiles; ti = next_tile(a.queue, &s_tile)) {
-        const uint32_t m0 = (uint32_t)a.tiles[ti] << (2 * k);
+    auto issue = [&](int ti, int b) {  // one elected thread: arm buffer b and bulk-copy tile ti's record
         const int slot = a.tile_slot[ti];
-        const int tb = a.tgt_off[m0];
-        const uint32_t rb = a.reg_off[slot], nent = a.reg_off[slot + 1] - rb;  // multiple of 4
-        if (tid == 0) {
-            const uint32_t b_uv = nent * 2 * (uint32_t)sizeof(T), b_ix = nent * 4u, b_tab = (uint32_t)c.tstride * 2u;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                         "r"(b_uv + b_ix + b_tab)
-                         : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    smem_addr(table)),
-                "l"(a.reg_table + (size_t)slot * c.tstride), "r"(b_tab), "r"(bar)
-                : "memory");
-            if (nent) {
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        smem_addr(s_uv)),
-                    "l"(a.reg_uv + 2 * (size_t)rb), "r"(b_uv), "r"(bar)
-                    : "memory");
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        smem_addr(s_idx)),
-                    "l"(a.reg_idx + rb), "r"(b_ix), "r"(bar)
-                    : "memory");
+        unsigned char *buf = smem + c.buf0 + b * c.bufsz;
+        const uint32_t rb = a.reg_off[slot], nent = a.reg_off[slot + 1] - rb;
+        const uint32_t tb = a.tgt_pack_off[slot], ntp = a.tgt_pack_off[slot + 1] - tb;
+        const uint32_t b_tab = (uint32_t)c.tstride * 2u, b_uv = nent * 2 * (uint32_t)sizeof(T), b_ix = nent * 4u;
+        const uint32_t b_tuv = ntp * 2 * (uint32_t)sizeof(T), b_tbl = ntp * 2u;
+        const uint32_t bar = smem_addr(mbar + b);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(b_tab + b_uv + b_ix + b_tuv + b_tbl)
+                     : "memory");
+#define P2P_BULK(dst, src, bytes)                                                                        \
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" \
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(bar)                                   \
+                 : "memory")
+        P2P_BULK(buf + c.table, a.reg_table + (size_t)slot * c.tstride, b_tab);
+        if (nent) {
+            P2P_BULK(buf + c.uv, a.reg_uv + 2 * (size_t)rb, b_uv);
+            P2P_BULK(buf + c.idx, a.reg_idx + rb, b_ix);
+        }
+        if (ntp) {
+            P2P_BULK(buf + c.tuv, a.tgt_ruv + 2 * (size_t)tb, b_tuv);
+            P2P_BULK(buf + c.tbl, a.tgt_bl + tb, b_tbl);
+        }
+#undef P2P_BULK
+    };
+
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(mbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(mbar + 1)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const int t0 = atomicAdd(a.queue, 1);
+        s_next = t0;
+        if (t0 < a.ntiles) {
+            s_base_next = a.tile_tgt_base[a.tile_slot[t0]];
+            issue(t0, 0);
+        }
+    }
+    __syncthreads();
+    int cur = s_next, buf = 0, tb = s_base_next;
+    uint32_t parity = 0u;  // bit b = phase parity of buffer b's mbarrier
+
+    while (cur < a.ntiles) {
+        const unsigned char *B = smem + c.buf0 + buf * c.bufsz;
+        const uint16_t *table = reinterpret_cast<const uint16_t *>(B + c.table);
+        const uint16_t *ttab = table + RR + 1;  // target box starts of the tile
+        const T *s_uv = reinterpret_cast<const T *>(B + c.uv);
+        const int32_t *s_idx = reinterpret_cast<const int32_t *>(B + c.idx);
+        const T *tuv = reinterpret_cast<const T *>(B + c.tuv);
+        const uint16_t *tbl = reinterpret_cast<const uint16_t *>(B + c.tbl);
+        if (tid == 0) {  // next tile; with two buffers its record streams in while this tile computes
+            const int nx = atomicAdd(a.queue, 1);
+            s_next = nx;
+            if (nx < a.ntiles) {
+                s_base_next = a.tile_tgt_base[a.tile_slot[nx]];
+                if (db) issue(nx, buf ^ 1);
             }
         }
-        for (int i = tid; i <= WW; i += kThreads) toff[i] = a.tgt_off[m0 + i] - tb;
-        __syncthreads();
-        if (wid == 0) {  // units: TPI targets of one box
+        {
+            const uint32_t bar = smem_addr(mbar + buf);
+            asm volatile(
+                "{\n\t.reg .pred P;\n"
+                "WAIT_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+                "@!P bra WAIT_%=;\n}" ::"r"(bar),
+                "r"((parity >> buf) & 1u)
+                : "memory");
+            parity ^= 1u << buf;
+        }
+        const int nent = (int)table[RR];
+        const int nt = (int)ttab[WW];
+        if (TPI == 2 && wid == 0) {  // units of two targets of one box
             int carry = 0;
             for (int base = 0; base < WW; base += 32) {
                 const int bl = base + lane;
-                const int n = bl < WW ? toff[bl + 1] - toff[bl] : 0;
-                const int np = TPI == 2 ? (n + 1) >> 1 : n;
+                const int n = bl < WW ? (int)ttab[bl + 1] - (int)ttab[bl] : 0;
+                const int np = (n + 1) >> 1;
                 const int incl = warp_incl_scan(np);
                 if (bl < WW) pstart[bl] = carry + incl - np;
                 carry += __shfl_sync(0xffffffffu, incl, 31);
             }
             if (lane == 0) s_units = carry;
         }
-        __syncthreads();
-        const int nt = toff[WW];
-        for (int t = tid; t < nt; t += kThreads) {
-            const int bl = a.tgt_bl[tb + t];
-            const typename V2<T>::type uv = a.tgt_ruv[tb + t];
-            tu[t] = uv.x;
-            tv[t] = uv.y;
-            const int r = t - toff[bl], u = pstart[bl] + r / TPI, sl = r % TPI;
-            ut[TPI * u + sl] = t;
-            tslot[t] = TPI * u + sl;
-            if (sl == 0) {
-                uj0[u] = (int)compact16((uint32_t)bl >> 1) * R + (int)compact16((uint32_t)bl);
-                if (TPI == 2 && t + 1 == toff[bl + 1]) ut[TPI * u + 1] = t;
-            }
-        }
-        asm volatile(
-            "{\n\t.reg .pred P;\n"
-            "WAIT_%=:\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-            "@!P bra WAIT_%=;\n}" ::"r"(bar),
-            "r"(parity)
-            : "memory");
-        parity ^= 1u;
-        for (int i = tid; i < (int)nent; i += kThreads) {  // weights through the per-entry index
+        for (int i = tid; i < nent; i += NT) {  // weights through the per-entry index
             const int32_t j = s_idx[i];
             s_q[i] = j >= 0 ? a.q[j] : (T)0;
         }
         __syncthreads();
+        if (TPI == 2) {
+            for (int t = tid; t < nt; t += NT) {
+                const int bl = tbl[t];
+                const int r = t - (int)ttab[bl], u = pstart[bl] + (r >> 1), sl = r & 1;
+                ut[2 * u + sl] = t;
+                tslot[t] = 2 * u + sl;
+                if (sl == 0) {
+                    uj0[u] = (int)compact16((uint32_t)bl >> 1) * R + (int)compact16((uint32_t)bl);
+                    if (t + 1 == (int)ttab[bl + 1]) ut[2 * u + 1] = t;
+                }
+            }
+            __syncthreads();
+        }
+        const int nu = TPI == 2 ? s_units : nt;
 
-        const int nu = s_units;
-        for (int it = tid; it < 3 * nu; it += kThreads) {
-            const int row = (it >= nu) + (it >= 2 * nu);
-            const int u = it - row * nu;
-            const int j0 = uj0[u] + row * R;
-            const int i0 = table[j0], i1 = table[j0 + 3];
-            T *pp = part + row * TPI * nu + TPI * u;
-            if constexpr (sizeof(T) == 4) {
+        // one (unit, row) item: TPI partial sums over the row-run's sources
+        auto item = [&](int u, int row, T *res, int piece, int f) {
+            int t0, jb;
+            if (TPI == 2) {
+                t0 = ut[2 * u];
+                jb = uj0[u];
+            } else {
+                t0 = u;
+                const int bl = tbl[u];
+                jb = (int)compact16((uint32_t)bl >> 1) * R + (int)compact16((uint32_t)bl);
+            }
+            const int j0 = jb + row * R;
+            int i0 = table[j0], i1 = table[j0 + 3];
+            if (f > 1) {  // piece of the row-run (in source pairs when padded)
+                const int g = PAD ? 2 : 1, n = (i1 - i0) / g;
+                const int a0 = i0 + g * ((n * piece) / f), a1 = i0 + g * ((n * (piece + 1)) / f);
+                i0 = a0;
+                i1 = a1;
+            }
+            if constexpr (PAD) {
                 const float4 *A = reinterpret_cast<const float4 *>(s_uv);
                 const float2 *Q = reinterpret_cast<const float2 *>(s_q);
                 if constexpr (TPI == 2) {
-                    const int t0 = ut[2 * u], t1 = ut[2 * u + 1];
-                    span2_f32(A, Q, i0 >> 1, i1 >> 1, tu[t0], tv[t0], tu[t1], tv[t1], pp[0], pp[1]);
+                    const int t1 = ut[2 * u + 1];
+                    span2_f32(A, Q, i0 >> 1, i1 >> 1, tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t1], tuv[2 * t1 + 1],
+                              res[0], res[1]);
                 } else {
-                    const int t = ut[u];
-                    pp[0] = span_f32(A, Q, i0 >> 1, i1 >> 1, tu[t], tv[t]);
+                    res[0] = span_f32(A, Q, i0 >> 1, i1 >> 1, tuv[2 * t0], tuv[2 * t0 + 1]);
                 }
+            } else if constexpr (sizeof(T) == 4) {
+                res[0] = span1_f32(reinterpret_cast<const float2 *>(s_uv), reinterpret_cast<const float *>(s_q), i0,
+                                   i1, tuv[2 * t0], tuv[2 * t0 + 1]);
             } else {
-                const int t = ut[u];
-                double acc = 0.0;
-                for (int j = i0; j < i1; ++j) {
-                    const double du = tu[t] - s_uv[2 * j], dv = tv[t] - s_uv[2 * j + 1];
-                    const double r2 = fma(dv, dv, du * du);
-                    if (r2 >= a.eps2) acc = fma(s_q[j], log(r2), acc);
-                }
-                pp[0] = acc;
+                res[0] = span1_f64(reinterpret_cast<const double2 *>(s_uv), reinterpret_cast<const double *>(s_q), i0,
+                                   i1, tuv[2 * t0], tuv[2 * t0 + 1], a.eps2);
             }
-        }
-        __syncthreads();
-
-        const int rs = TPI * nu;
-        for (int t = tid; t < nt; t += kThreads) {
-            const int sl = tslot[t];
-            T acc = part[sl] + part[rs + sl] + part[2 * rs + sl];
-            T phi;
+        };
+        // final value of target t from its row-ordered sum (fp32: guarded redo if non-finite)
+        auto finish = [&](int t, T acc) {
             if constexpr (sizeof(T) == 4) {
                 if (!isfinite(acc)) {
-                    const int jb = uj0[sl / TPI];
+                    const int bl = tbl[t];
+                    const int jb = (int)compact16((uint32_t)bl >> 1) * R + (int)compact16((uint32_t)bl);
                     acc = 0.f;
                     for (int row = 0; row < 3; ++row) {
                         const int j0 = jb + row * R;
-                        acc += span_f32_guarded(reinterpret_cast<const float4 *>(s_uv),
-                                                reinterpret_cast<const float2 *>(s_q), table[j0] >> 1,
-                                                table[j0 + 3] >> 1, tu[t], tv[t], a.eps2);
+                        if constexpr (PAD)
+                            acc += span_f32_guarded(reinterpret_cast<const float4 *>(s_uv),
+                                                    reinterpret_cast<const float2 *>(s_q), table[j0] >> 1,
+                                                    table[j0 + 3] >> 1, tuv[2 * t], tuv[2 * t + 1], a.eps2);
+                        else
+                            acc += span1_f32_guarded(reinterpret_cast<const float2 *>(s_uv),
+                                                     reinterpret_cast<const float *>(s_q), table[j0], table[j0 + 3],
+                                                     tuv[2 * t], tuv[2 * t + 1], a.eps2);
                     }
                 }
-                phi = (-0.5f * kLn2) * acc;
+                acc = (-0.5f * kLn2) * acc;
             } else {
-                phi = -0.5 * acc;
+                acc = -0.5 * acc;
             }
-            a.out[tb + t] = a.accumulate ? a.out[tb + t] + phi : phi;
+            a.out[tb + t] = a.accumulate ? a.out[tb + t] + acc : acc;
+        };
+
+        if (NS == 1) {  // one item per unit, rows in order
+            for (int u = tid; u < nu; u += NT) {
+                T acc[TPI], r[TPI];
+#pragma unroll
+                for (int x = 0; x < TPI; ++x) acc[x] = (T)0;
+                for (int row = 0; row < 3; ++row) {
+                    item(u, row, r, 0, 1);
+#pragma unroll
+                    for (int x = 0; x < TPI; ++x) acc[x] += r[x];
+                }
+                if (TPI == 2) {
+                    const int t0 = ut[2 * u], t1 = ut[2 * u + 1];
+                    finish(t0, acc[0]);
+                    if (t1 != t0) finish(t1, acc[TPI - 1]);
+                } else {
+                    finish(u, acc[0]);
+                }
+            }
+        } else {
+            // (row, piece, unit) items: each row-run is split into f pieces, f chosen per
+            // tile so the item count lands just under a multiple of the CTA size (the
+            // last round of items is otherwise nearly empty); partials are then summed
+            // in (row, piece) order -- deterministic for a given plan.
+            int f = 1;
+            {
+                float best = 0.f;
+                for (int ff = 1; ff <= kMaxPieces; ++ff) {
+                    const int items = 3 * ff * nu, rounds = (items + NT - 1) / NT;
+                    const float eff = (float)items / (float)(rounds * NT) - 0.03f * (ff - 1);
+                    if (eff > best + 1e-6f) {
+                        best = eff;
+                        f = ff;
+                    }
+                }
+            }
+            const int nrp = 3 * f;
+            for (int it = tid; it < nrp * nu; it += NT) {
+                const int rp = it / nu, u = it - rp * nu;
+                const int row = rp / f, piece = rp - row * f;
+                T res[TPI];
+                if (f == 1) {
+                    item(u, row, res, 0, 1);
+                } else {
+                    item(u, row, res, piece, f);
+                }
+#pragma unroll
+                for (int x = 0; x < TPI; ++x) part[rp * TPI * nu + TPI * u + x] = res[x];
+            }
+            __syncthreads();
+            const int rs = TPI * nu;
+            for (int t = tid; t < nt; t += NT) {
+                const int sl = TPI == 2 ? tslot[t] : t;
+                T acc = part[sl];
+                for (int rp = 1; rp < nrp; ++rp) acc += part[rp * rs + sl];
+                finish(t, acc);
+            }
         }
+        __syncthreads();  // buffer `buf` and the work arrays are free; s_next / s_base_next visible
+        cur = s_next;
+        tb = s_base_next;
+        if (db) buf ^= 1;
+        else if (tid == 0 && cur < a.ntiles) issue(cur, 0);
     }
 }
 

@@ -6,6 +6,7 @@
 
 #include <cstdint>
 
+#include "p2p_kernels.cuh"
 #include "p2p_peaks.h"
 
 namespace {
@@ -74,6 +75,34 @@ __global__ void __launch_bounds__(kThreads) read_kernel(const int4 *__restrict__
     if (acc == 0x12345678) out[0] = acc;
 }
 
+// The P2P inner loops alone: every thread sweeps `nsrc` sources resident in
+// shared memory `iters` times (1 or 2 targets per thread).  Upper bound of the
+// pair rate the kernels can reach once staging and scheduling cost nothing.
+template <int TPI>
+__global__ void __launch_bounds__(kThreads) span_kernel(float *out, int iters, int nsrc) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    float4 *A = reinterpret_cast<float4 *>(sm);
+    float2 *Q = reinterpret_cast<float2 *>(sm + 8 * nsrc);
+    for (int p = threadIdx.x; p < nsrc / 2; p += blockDim.x) {
+        const float b = 0.001f * p;
+        A[p] = make_float4(0.1f + b, 0.2f + b, 0.3f - b, 0.4f - b);
+        Q[p] = make_float2(0.5f, -0.25f);
+    }
+    __syncthreads();
+    const float ut = 0.05f + 1e-4f * threadIdx.x, vt = 0.07f + 1e-4f * blockIdx.x;
+    float acc = 0.f;
+    for (int it = 0; it < iters; ++it) {
+        if (TPI == 2) {
+            float r0, r1;
+            p2p::dev::span2_f32(A, Q, 0, nsrc / 2, ut + it * 1e-7f, vt, ut, vt + 1e-3f, r0, r1);
+            acc += r0 + r1;
+        } else {
+            acc += p2p::dev::span_f32(A, Q, 0, nsrc / 2, ut + it * 1e-7f, vt);
+        }
+    }
+    if (acc == 1234.5f) out[0] = acc;
+}
+
 template <typename F>
 p2p_peak_status timed(int device, int reps, F launch, double *ms_out) {
     if (cudaSetDevice(device) != cudaSuccess) return 1;
@@ -136,6 +165,21 @@ p2p_peak_status p2p_peak_dfma(int device, double *flops) {
     p2p_peak_status st = timed(device, 5, [&] { dfma_kernel<<<grid, kThreads>>>(d, iters, 1.0); }, &ms);
     cudaFree(d);
     *flops = (double)grid * kThreads * iters * 8 * 2 / (ms * 1e-3);
+    return st;
+}
+
+p2p_peak_status p2p_peak_span(int device, int tpi, int nsrc, double *pairs_per_s) {
+    const int grid = sm_count(device) * 6, iters = 64;
+    float *d = nullptr;
+    cudaSetDevice(device);
+    cudaMalloc(&d, 16);
+    const size_t sm = (size_t)nsrc * 12;
+    double ms = 0;
+    p2p_peak_status st = tpi == 2
+        ? timed(device, 5, [&] { span_kernel<2><<<grid, kThreads, sm>>>(d, iters, nsrc); }, &ms)
+        : timed(device, 5, [&] { span_kernel<1><<<grid, kThreads, sm>>>(d, iters, nsrc); }, &ms);
+    cudaFree(d);
+    *pairs_per_s = (double)grid * kThreads * iters * nsrc * tpi / (ms * 1e-3);
     return st;
 }
 

@@ -71,32 +71,40 @@ P2P_HD inline RCarve r_carve(int k, int src_cap, int tgt_cap, int e) {
     return c;
 }
 
+constexpr int kMaxPieces = 3;  // TILED: a row-run split into at most 3 pieces
+
 struct TCarve {
-    int table, toff, pstart, uj0, ut, tslot, tu, tv, part, bar, src, q, total, ucap, tstride;
+    int buf0, bufsz;                      // double-buffered, bulk-copied part: 2 x bufsz bytes from buf0
+    int table, uv, idx, tuv, tbl;         // offsets inside one buffer
+    int q, pstart, uj0, ut, tslot, part, bar, total, ucap, tstride;
 };
-// TILED layout.  src_cap: max packed-region entries of a tile (multiple of 4).
+// TILED layout.  src_cap: max packed-region entries of a tile (multiple of 4);
+// tgt_cap: max packed targets of a tile (multiple of 8); tpi: targets per
+// unit; ns: work segments per target (3 row-runs, or 6 half row-runs).
 P2P_HD inline int tiled_table_stride(int k) {
-    const int R = (1 << k) + 2;
-    return (R * R + 1 + 7) & ~7;  // uint16 entries, 16-B multiple for the bulk copy
+    const int W = 1 << k, R = W + 2;
+    return (R * R + 1 + W * W + 1 + 7) & ~7;  // uint16: region box starts, then target box starts
 }
-P2P_HD inline TCarve tiled_carve(int k, int src_cap, int tgt_cap, int e, int tpi) {
+P2P_HD inline TCarve tiled_carve(int k, int src_cap, int tgt_cap, int e, int tpi, int ns, int nbuf) {
     const int WW = 1 << (2 * k);
     TCarve c;
     c.ucap = nr_unit_cap(k, tgt_cap, tpi);
     c.tstride = tiled_table_stride(k);
     c.table = 0;
-    c.toff = align16(c.table + 2 * c.tstride);
-    c.pstart = c.toff + 4 * (WW + 1);
+    c.uv = align16(2 * c.tstride);
+    c.idx = c.uv + 2 * e * src_cap;
+    c.tuv = align16(c.idx + 4 * src_cap);
+    c.tbl = c.tuv + 2 * e * tgt_cap;
+    c.bufsz = align16(c.tbl + 2 * tgt_cap);
+    c.buf0 = 0;
+    c.q = nbuf * c.bufsz;
+    c.pstart = align16(c.q + e * src_cap);
     c.uj0 = c.pstart + 4 * (WW + 1);
     c.ut = c.uj0 + 4 * c.ucap;
     c.tslot = c.ut + 4 * tpi * c.ucap;
-    c.tu = align16(c.tslot + 4 * tgt_cap);
-    c.tv = align16(c.tu + e * tgt_cap);
-    c.part = align16(c.tv + e * tgt_cap);
-    c.bar = align16(c.part + 3 * e * tpi * c.ucap);
-    c.src = align16(c.bar + 16);              // region coordinates (2 per entry) -- bulk copy dst
-    c.q = c.src + 2 * e * src_cap;            // region index (int32), then gathered weights
-    c.total = c.q + 4 * src_cap + e * src_cap;
+    c.part = align16(c.tslot + 4 * tgt_cap);
+    c.bar = align16(c.part + (ns == 1 ? 1 : 3 * kMaxPieces) * e * tpi * c.ucap);
+    c.total = c.bar + 16;
     return c;
 }
 
@@ -141,7 +149,7 @@ struct Layout {
     std::vector<T> tgt_uv;   // [n_tgt_local][2]
     std::vector<T> halo_uv;  // R: fp32 -> per source pair (u0,u1,v0,v1); fp64 -> (u,v) per entry
     std::vector<T> reg_uv;   // TILED: region-relative, same pair packing as halo_uv
-    std::vector<T> tgt_ruv;  // TILED: [n_tgt_local][2] target coordinates relative to its tile's region origin
+    std::vector<T> tgt_ruv;  // TILED: per-tile packed targets, coordinates relative to the region origin
 };
 
 struct HostPlan {
@@ -182,8 +190,14 @@ struct HostPlan {
     // ---- TILED layout (per tile in Morton order = "slot")
     std::vector<uint32_t> reg_off;                // [tiles+1] packed-region offsets
     std::vector<int32_t> reg_idx;                 // local source index, -1 = pad
-    std::vector<uint16_t> reg_table;              // [tiles][tstride] region row-major box starts (relative)
-    std::vector<uint16_t> tgt_bl;                 // [n_tgt_local] tile-local Morton box index
+    std::vector<uint16_t> reg_table;              // [tiles][tstride] region box starts, then target box starts
+    std::vector<uint16_t> tgt_bl;                 // per-tile packed targets: tile-local Morton box index
+    std::vector<uint32_t> tgt_pack_off;           // [tiles+1] packed-target offsets (multiples of 8)
+    std::vector<int32_t> tile_tgt_base;           // [tiles] plan index of each tile's first target
+    int ns = 3;                                   // TILED work segments per target
+    int nbuf = 1;                                 // TILED record buffers (2 = prefetch next tile)
+    bool pad = true;                              // TILED: boxes padded to even counts (packed f32x2 loops)
+    int nt = 256;                                 // threads per CTA (TILED: 128 or 256)
     std::vector<int32_t> tile_slot;               // launch order -> slot
     int64_t reg_entries = 0;
 

@@ -23,6 +23,8 @@
 
 #include "plan.h"
 
+#include <cstdlib>
+
 namespace p2p {
 
 namespace {
@@ -58,6 +60,7 @@ inline uint32_t cell_of(double x, int64_t S) {
 
 inline int64_t pad2(int64_t n) { return (n + 1) & ~int64_t(1); }
 inline int64_t pad4(int64_t n) { return (n + 3) & ~int64_t(3); }
+inline int64_t pad8(int64_t n) { return (n + 7) & ~int64_t(7); }
 
 void validate_points(const double *xy, int64_t n, const char *what) {
     if (n < 1) fail(P2P_ERROR_INVALID_ARGUMENT, std::string(what) + ": n must be >= 1 (SPEC.md L55)");
@@ -209,7 +212,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             const int64_t WWk = int64_t(1) << (2 * kk);
             int64_t ne = 0;
             for (int64_t t = 0; t < hp.B / WWk; ++t) ne += to[(t + 1) * WWk] > to[t * WWk];
-            if ((double)hp.n_tgt / (double)std::max<int64_t>(ne, 1) >= 0.75 * kThreads) {
+            if ((double)hp.n_tgt / (double)std::max<int64_t>(ne, 1) >= 0.75 * 256) {
                 k = kk;
                 break;
             }
@@ -256,12 +259,45 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         }, 256);
         hp.max_region = region.empty() ? 0 : *std::max_element(region.begin(), region.end());
         hp.max_tile_halo = halo.empty() ? 0 : *std::max_element(halo.begin(), halo.end());
-        hp.tgt_cap = pad4(tcount.empty() ? 0 : *std::max_element(tcount.begin(), tcount.end()));
+        hp.tgt_cap = pad8(tcount.empty() ? 0 : *std::max_element(tcount.begin(), tcount.end()));
         hp.src_cap = d.layout == P2P_LAYOUT_REDUNDANT ? hp.max_tile_halo : pad4(hp.max_region);
         hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= 4.0 && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT) ? 2 : 1;
+        // TILED defaults: dense fp32 -> padded pairs, 2 targets per unit, (unit, row) items;
+        // sparse or fp64 -> unpadded, one item per target; 128-thread CTAs.
+        hp.pad = d.layout == P2P_LAYOUT_TILED ? (hp.tpi == 2) : true;
+        hp.ns = hp.tpi == 2 ? 3 : 1;
+        hp.nbuf = 1;
+        hp.nt = d.layout == P2P_LAYOUT_TILED ? 128 : kThreads;
+        // tuning hooks (experiments only): P2P_TPI, P2P_NS, P2P_NBUF, P2P_PAD, P2P_NT
+        if (const char *v = std::getenv("P2P_TPI"))
+            if (d.precision == P2P_FP32 && d.layout != P2P_LAYOUT_REDUNDANT) hp.tpi = std::atoi(v) == 2 ? 2 : 1;
+        if (const char *v = std::getenv("P2P_PAD"))
+            if (d.layout == P2P_LAYOUT_TILED && d.precision == P2P_FP32) hp.pad = std::atoi(v) != 0;
+        if (hp.tpi == 2) hp.pad = true;
+        if (d.precision == P2P_FP64 && d.layout == P2P_LAYOUT_TILED) hp.pad = false;
+        if (const char *v = std::getenv("P2P_NS")) hp.ns = std::atoi(v) == 3 ? 3 : 1;
+        if (const char *v = std::getenv("P2P_NBUF")) hp.nbuf = std::atoi(v) == 2 ? 2 : 1;
+        if (const char *v = std::getenv("P2P_NT"))
+            if (d.layout == P2P_LAYOUT_TILED) hp.nt = std::atoi(v) == 256 ? 256 : 128;
+        if (d.layout == P2P_LAYOUT_TILED && !hp.pad) {  // unpadded region sizes
+            int64_t mx = 0;
+            for (int64_t i = 0; i < nt; ++i) {
+                uint32_t tx, ty;
+                morton_decode((uint32_t)hp.tiles_g[i], tx, ty);
+                int64_t X0 = (int64_t)tx * W - 1, Y0 = (int64_t)ty * W - 1, rg = 0;
+                for (int64_t ly = 0; ly < R; ++ly)
+                    for (int64_t lx = 0; lx < R; ++lx) {
+                        int64_t x = X0 + lx, y = Y0 + ly;
+                        if (x < 0 || y < 0 || x >= S || y >= S) continue;
+                        rg += ns(morton_encode((uint32_t)x, (uint32_t)y));
+                    }
+                mx = std::max(mx, rg);
+            }
+            hp.src_cap = pad4(mx);
+        }
         const int sc = (int)std::min<int64_t>(hp.src_cap, 1 << 24), tc = (int)std::min<int64_t>(hp.tgt_cap, 1 << 24);
         int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? (int64_t)nr_carve(k, sc, tc, e, hp.tpi).total
-                       : d.layout == P2P_LAYOUT_TILED      ? (int64_t)tiled_carve(k, sc, tc, e, hp.tpi).total
+                       : d.layout == P2P_LAYOUT_TILED      ? (int64_t)tiled_carve(k, sc, tc, e, hp.tpi, hp.ns, hp.nbuf).total
                                                            : (int64_t)r_carve(k, sc, tc, e).total;
         hp.smem_bytes = smem;
         if (smem <= kSmemLimit) break;
@@ -499,7 +535,8 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                 const int64_t x = X0 + j % R, y = Y0 + j / R;
                 if (x < 0 || y < 0 || x >= S || y >= S) continue;
                 const uint32_t m = morton_encode((uint32_t)x, (uint32_t)y);
-                run += pad2(hp.src_off[m + 1] - hp.src_off[m]);
+                const int64_t cnt = hp.src_off[m + 1] - hp.src_off[m];
+                run += hp.pad ? pad2(cnt) : cnt;
             }
             if (run > 65535) fail(P2P_ERROR_NOT_SUPPORTED, "TILED region exceeds 65535 entries; use NR");
             hp.reg_table[i * ts + R * R] = (uint16_t)run;
@@ -527,10 +564,13 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                         const int64_t u = hp.src_uidx[sj];
                         const double rx = sxy[2 * u] - ox, ry = sxy[2 * u + 1] - oy;
                         hp.reg_idx[ent] = sj;
-                        if (f32) {
+                        if (f32 && hp.pad) {  // (u0,u1,v0,v1) per source pair
                             const int64_t p = ent >> 1, sl = ent & 1;
                             hp.f32.reg_uv[4 * p + sl] = (float)rx;
                             hp.f32.reg_uv[4 * p + 2 + sl] = (float)ry;
+                        } else if (f32) {     // (u, v) per entry
+                            hp.f32.reg_uv[2 * ent] = (float)rx;
+                            hp.f32.reg_uv[2 * ent + 1] = (float)ry;
                         } else {
                             hp.f64.reg_uv[2 * ent] = rx;
                             hp.f64.reg_uv[2 * ent + 1] = ry;
@@ -539,10 +579,24 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                 }
             }
         }, 64);
-        // targets: coordinates relative to their tile's region origin + tile-local box index
-        hp.tgt_bl.assign((size_t)hp.n_tgt_local, 0);
-        if (f32) hp.f32.tgt_ruv.assign((size_t)hp.n_tgt_local * 2, 0.f);
-        else hp.f64.tgt_ruv.assign((size_t)hp.n_tgt_local * 2, 0.0);
+        // targets, packed per tile (8-entry aligned for the bulk copy): coordinates
+        // relative to the region origin + tile-local box index; target box starts
+        // go after the region box starts in the tile's table record
+        hp.tgt_pack_off.assign((size_t)nlt + 1, 0);
+        hp.tile_tgt_base.assign((size_t)nlt, 0);
+        for (int64_t i = 0; i < nlt; ++i) {
+            const int64_t m0 = (int64_t)hp.tiles[i] * WW;
+            const int64_t n = hp.tgt_off[m0 + WW] - hp.tgt_off[m0];
+            if (n > 65535) fail(P2P_ERROR_NOT_SUPPORTED, "TILED tile exceeds 65535 targets; use NR");
+            hp.tile_tgt_base[i] = hp.tgt_off[m0];
+            hp.tgt_pack_off[i + 1] = hp.tgt_pack_off[i] + (uint32_t)pad8(n);
+            for (int64_t bl = 0; bl <= WW; ++bl)
+                hp.reg_table[i * ts + R * R + 1 + bl] = (uint16_t)(hp.tgt_off[m0 + bl] - hp.tgt_off[m0]);
+        }
+        const int64_t np = hp.tgt_pack_off[nlt];
+        hp.tgt_bl.assign((size_t)np, 0);
+        if (f32) hp.f32.tgt_ruv.assign((size_t)np * 2, 0.f);
+        else hp.f64.tgt_ruv.assign((size_t)np * 2, 0.0);
         const double *txy = d.tgt_xy;
         parallel_for(nlt, [&](int64_t a, int64_t bnd) {
             for (int64_t i = a; i < bnd; ++i) {
@@ -550,17 +604,18 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                 uint32_t tx, ty;
                 morton_decode(t, tx, ty);
                 const double ox = ((int64_t)tx * W - 1) * hp.h, oy = ((int64_t)ty * W - 1) * hp.h;
+                const int64_t g0 = hp.tgt_off[(int64_t)t * WW];
                 for (int64_t bl = 0; bl < WW; ++bl) {
                     const int64_t b = (int64_t)t * WW + bl;
                     for (int32_t g = hp.tgt_off[b]; g < hp.tgt_off[b + 1]; ++g) {
-                        const int64_t u = hp.tgt_uidx[g];
-                        hp.tgt_bl[g] = (uint16_t)bl;
+                        const int64_t u = hp.tgt_uidx[g], j = hp.tgt_pack_off[i] + (g - g0);
+                        hp.tgt_bl[j] = (uint16_t)bl;
                         if (f32) {
-                            hp.f32.tgt_ruv[2 * g] = (float)(txy[2 * u] - ox);
-                            hp.f32.tgt_ruv[2 * g + 1] = (float)(txy[2 * u + 1] - oy);
+                            hp.f32.tgt_ruv[2 * j] = (float)(txy[2 * u] - ox);
+                            hp.f32.tgt_ruv[2 * j + 1] = (float)(txy[2 * u + 1] - oy);
                         } else {
-                            hp.f64.tgt_ruv[2 * g] = txy[2 * u] - ox;
-                            hp.f64.tgt_ruv[2 * g + 1] = txy[2 * u + 1] - oy;
+                            hp.f64.tgt_ruv[2 * j] = txy[2 * u] - ox;
+                            hp.f64.tgt_ruv[2 * j + 1] = txy[2 * u + 1] - oy;
                         }
                     }
                 }

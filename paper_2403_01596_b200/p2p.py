@@ -45,7 +45,8 @@ EXPORT = {
 
 # Symbols declared in include/p2p.h (checked by tests/test_abi.py).
 ABI_SYMBOLS = (
-    "p2p_plan_desc_init", "p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_dist",
+    "p2p_plan_desc_init", "p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async",
+    "p2p_apply_dist",
     "p2p_halo_pack", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
     "p2p_status_string", "p2p_last_error", "p2p_abi_version",
 )
@@ -104,6 +105,7 @@ def load_library() -> C.CDLL:
     lib.p2p_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(P)]
     lib.p2p_apply.argtypes = [P, P, P, i32, i32, P]
     lib.p2p_apply_host.argtypes = [P, P, P, i32, i32, P]
+    lib.p2p_apply_host_async.argtypes = [P, P, P, i32, i32, P]
     lib.p2p_apply_dist.argtypes = [P, P, P, P, i32, P]
     lib.p2p_halo_pack.argtypes = [P, P, P, P]
     lib.p2p_destroy.argtypes = [P]
@@ -113,7 +115,7 @@ def load_library() -> C.CDLL:
     lib.p2p_status_string.restype = C.c_char_p
     lib.p2p_last_error.restype = C.c_char_p
     lib.p2p_abi_version.restype = i32
-    for name in ("p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_dist", "p2p_halo_pack",
+    for name in ("p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async", "p2p_apply_dist", "p2p_halo_pack",
                  "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export"):
         getattr(lib, name).restype = i32
     _lib = lib
@@ -151,6 +153,12 @@ def p2p_apply(plan, d_q: int, d_out: int, order: int = P2P_ORDER_PLAN, accumulat
 
 def p2p_apply_host(plan, h_q: int, h_out: int, order: int = P2P_ORDER_PLAN, accumulate: int = 0, stream: int = 0):
     _check(load_library().p2p_apply_host(plan, h_q, h_out, order, accumulate, stream or None), "p2p_apply_host")
+
+
+def p2p_apply_host_async(plan, h_q: int, h_out: int, order: int = P2P_ORDER_PLAN, accumulate: int = 0,
+                         stream: int = 0):
+    _check(load_library().p2p_apply_host_async(plan, h_q, h_out, order, accumulate, stream or None),
+           "p2p_apply_host_async")
 
 
 def p2p_apply_dist(plan, d_q_owned: int, d_q_halo: int, d_out: int, accumulate: int = 0, stream: int = 0):

@@ -1,0 +1,4 @@
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "tiled" 2>&1 | tail -3
+timeout 1200 python tools/sweep.py --configs d16_1e6,d64_1e6 --layout tiled --tpi 1,2 --ns 1,3 --nbuf 1 --nt 128,256 --pad 1 --json gpurun_out/sweep2_dense.json
+timeout 1200 python tools/sweep.py --configs lowd1_1e7,lowd025_1e7 --layout tiled --tpi 1 --ns 1,3 --nbuf 1,2 --nt 128,256 --pad 0,1 --json gpurun_out/sweep2_sparse.json
