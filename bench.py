@@ -5,8 +5,9 @@ P2P pair-interactions/s; roofline fraction).
 One *step* = one apply of the whole hot path (SURVEY.md §8(a) apply rows:
 [halo weight exchange] -> P2P kernel) over each config of the workload, with
 inputs resident in HBM.  Default workload = BASELINE.json configs[1], the
-density sweep: 1e6 points at 16, 32 and 64 points per box, non-redundant
-layout, fp32 (the headline), Morton plan order.
+density sweep: 1e6 points at 16, 32 and 64 points per box, TILED layout
+(redundant only on the tile ring), fp32 (the headline), Morton plan order;
+the NR and R layouts and fp64 are reported under "extras".
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
   torchrun --nproc-per-node N bench.py --gpus N ...   (strong scaling, NCCL halo exchange)
@@ -52,7 +53,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="density_1e6", choices=sorted(WORKLOADS))
-    ap.add_argument("--layout", default="nr", choices=["nr", "r", "tiled"])
+    ap.add_argument("--layout", default="tiled", choices=["nr", "r", "tiled"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--kind", default="iid", choices=["iid", "stratified"])
     ap.add_argument("--no-extras", action="store_true", help="skip the R / fp64 detail lines")

@@ -20,8 +20,10 @@ p2p_peak_status p2p_peak_ffma2(int device, double *flops);
 /* fp64 FMA FLOP/s. */
 p2p_peak_status p2p_peak_dfma(int device, double *flops);
 /* The P2P fp32 inner loop alone (tpi = 1 or 2 targets per thread, nsrc
- * sources resident in shared memory): pair-interactions per second. */
-p2p_peak_status p2p_peak_span(int device, int tpi, int nsrc, double *pairs_per_s);
+ * sources resident in shared memory): pair-interactions per second.  The
+ * lanes of a warp form `groups` groups reading source pairs `gstride` apart
+ * (groups = 1: every lane reads the same source, a broadcast). */
+p2p_peak_status p2p_peak_span(int device, int tpi, int nsrc, int groups, int gstride, double *pairs_per_s);
 /* Streaming read of a 2 GiB buffer (bytes/s). */
 p2p_peak_status p2p_peak_hbm_read(int device, double *bytes_per_s);
 

@@ -47,6 +47,7 @@ struct p2p_plan_s {
     DevBuf tile_slot, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     int grid = 0;                                // persistent CTAs per launch
+    unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
     int64_t device_bytes = 0;
     double upload_seconds = 0.0;
     int elem = 4;
@@ -89,21 +90,43 @@ template <>
 const p2p::Layout<double> &layout_of<double>(const p2p::HostPlan &hp) { return hp.f64; }
 
 // TILED kernel instance for the plan's options (element type, targets per unit, CTA size, padding).
+template <typename T, int TPI, bool PAD>
+const void *tiled_fn_nt(int nt) {
+    using namespace p2p::dev;
+    switch (nt) {
+    case 32: return (const void *)p2p_tiled_kernel<T, TPI, 32, PAD>;
+    case 64: return (const void *)p2p_tiled_kernel<T, TPI, 64, PAD>;
+    case 128: return (const void *)p2p_tiled_kernel<T, TPI, 128, PAD>;
+    default: return (const void *)p2p_tiled_kernel<T, TPI, 256, PAD>;
+    }
+}
+
+// TILED kernel instance for the plan's options (element type, targets per unit, CTA size, padding).
 template <typename T>
 const void *tiled_fn(int tpi, int nt, bool pad) {
+    if constexpr (sizeof(T) == 4) {
+        if (tpi == 2) return tiled_fn_nt<float, 2, true>(nt);
+        return pad ? tiled_fn_nt<float, 1, true>(nt) : tiled_fn_nt<float, 1, false>(nt);
+    } else {
+        return tiled_fn_nt<double, 1, false>(nt);
+    }
+}
+
+template <typename T>
+const void *tiled_ws_fn(int tpi, int ncw, bool pad) {
     using namespace p2p::dev;
     if constexpr (sizeof(T) == 4) {
         if (tpi == 2)
-            return nt == 128 ? (const void *)p2p_tiled_kernel<float, 2, 128, true>
-                             : (const void *)p2p_tiled_kernel<float, 2, 256, true>;
+            return ncw == 8 ? (const void *)p2p_tiled_ws_kernel<float, 2, true, 8>
+                            : (const void *)p2p_tiled_ws_kernel<float, 2, true, 4>;
         if (pad)
-            return nt == 128 ? (const void *)p2p_tiled_kernel<float, 1, 128, true>
-                             : (const void *)p2p_tiled_kernel<float, 1, 256, true>;
-        return nt == 128 ? (const void *)p2p_tiled_kernel<float, 1, 128, false>
-                         : (const void *)p2p_tiled_kernel<float, 1, 256, false>;
+            return ncw == 8 ? (const void *)p2p_tiled_ws_kernel<float, 1, true, 8>
+                            : (const void *)p2p_tiled_ws_kernel<float, 1, true, 4>;
+        return ncw == 8 ? (const void *)p2p_tiled_ws_kernel<float, 1, false, 8>
+                        : (const void *)p2p_tiled_ws_kernel<float, 1, false, 4>;
     } else {
-        return nt == 128 ? (const void *)p2p_tiled_kernel<double, 1, 128, false>
-                         : (const void *)p2p_tiled_kernel<double, 1, 256, false>;
+        return ncw == 8 ? (const void *)p2p_tiled_ws_kernel<double, 1, false, 8>
+                        : (const void *)p2p_tiled_ws_kernel<double, 1, false, 4>;
     }
 }
 
@@ -145,16 +168,20 @@ void upload_plan(p2p_plan_s &P) {
     const bool two = hp.tpi == 2;
     const void *kfn = hp.layout == P2P_LAYOUT_REDUNDANT ? (const void *)p2p::dev::p2p_r_kernel<T>
                       : hp.layout == P2P_LAYOUT_TILED
-                          ? tiled_fn<T>(hp.tpi, hp.nt, hp.pad)
+                          ? (hp.ws ? tiled_ws_fn<T>(hp.tpi, hp.ncw, hp.pad) : tiled_fn<T>(hp.tpi, hp.nt, hp.pad))
                           : (two ? (const void *)p2p::dev::p2p_nr_kernel<T, sizeof(T) == 4 ? 2 : 1>
                                  : (const void *)p2p::dev::p2p_nr_kernel<T, 1>);
     ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2p::kSmemLimit), "smem attr");
     int occ = 0, dev = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, hp.nt, (size_t)hp.smem_bytes), "occupancy");
+    const int block = hp.layout == P2P_LAYOUT_TILED && hp.ws ? (hp.ncw + 1) * 32 : hp.nt;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, block, (size_t)hp.smem_bytes), "occupancy");
     ck(cudaGetDevice(&dev), "cudaGetDevice");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
     P.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)hp.tiles.size(), (int64_t)std::max(occ, 1) * sms));
     P.alloc(P.queue, 16);
+    ck(cudaMemsetAsync(P.queue.p, 0, 16, P.stream), "queue init");  // kernels reset it on exit
+    ck(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
+       "carveout");
     P.alloc(P.q_local, (size_t)std::max<int64_t>(hp.n_src_local, 1) * sizeof(T));
     P.alloc(P.phi, (size_t)std::max<int64_t>(hp.n_tgt_local, 1) * sizeof(T));
     P.alloc(P.io_q, (size_t)std::max<int64_t>(hp.n_src, 1) * sizeof(T));
@@ -187,7 +214,7 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
     a.tgt_uv = (const typename p2p::dev::V2<T>::type *)P.tgt_uv.p;
     a.out = out;
     a.accumulate = accumulate;
-    ck(cudaMemsetAsync(P.queue.p, 0, sizeof(int), s), "queue reset");
+    a.trace = P.trace;
     if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
         a.src_off = (const int32_t *)P.src_off.p;
         a.src_uv = (const typename p2p::dev::V2<T>::type *)P.src_uv.p;
@@ -210,9 +237,14 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.ns = hp.ns;
         a.nbuf = hp.nbuf;
         void *args[] = {&a};
-        ck(cudaLaunchKernel(tiled_fn<T>(hp.tpi, hp.nt, hp.pad), dim3(P.grid), dim3(hp.nt), args,
-                            (size_t)hp.smem_bytes, s),
-           "tiled launch");
+        if (hp.ws)
+            ck(cudaLaunchKernel(tiled_ws_fn<T>(hp.tpi, hp.ncw, hp.pad), dim3(P.grid), dim3((hp.ncw + 1) * 32),
+                                args, (size_t)hp.smem_bytes, s),
+               "tiled-ws launch");
+        else
+            ck(cudaLaunchKernel(tiled_fn<T>(hp.tpi, hp.nt, hp.pad), dim3(P.grid), dim3(hp.nt), args,
+                                (size_t)hp.smem_bytes, s),
+               "tiled launch");
     } else {
         if (hp.halo_entries > 0)
             p2p::dev::pack_r_kernel<T><<<grid_for(hp.halo_entries), 256, 0, s>>>(
@@ -549,5 +581,15 @@ const char *p2p_status_string(p2p_status s) {
 const char *p2p_last_error(void) { return g_last_error.c_str(); }
 
 int32_t p2p_abi_version(void) { return P2P_ABI_VERSION; }
+
+// Diagnostics only (not part of include/p2p.h): per-tile timeline of the TILED
+// kernel -- d_trace = device buffer of 8 x uint64 per tile (queue position):
+// {smid << 32 | cta, t_claim, t_data, t_units, -, t_end, units, entries}
+// in %globaltimer ns; NULL disables.
+p2p_status p2p_internal_set_trace(p2p_plan P, void *d_trace) {
+    if (!P) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan");
+    P->trace = (unsigned long long *)d_trace;
+    return P2P_SUCCESS;
+}
 
 }  // extern "C"

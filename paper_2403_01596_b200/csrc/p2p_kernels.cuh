@@ -106,13 +106,18 @@ __device__ __forceinline__ float span_f32(const float4 *__restrict__ A, const fl
 
 // Two targets sharing one span x two sources per step: 4 pairs per LDS.128 + LDS.64,
 // ~3 non-MUFU issue slots per pair (FADD2 x4, FMUL2 x2, FFMA2 x4 per 4 pairs).
+#ifndef P2P_SPAN2_UNROLL
+#define P2P_SPAN2_UNROLL 4
+#endif
+#define P2P_PRAGMA(x) _Pragma(#x)
+#define P2P_UNROLL(n) P2P_PRAGMA(unroll n)
 __device__ __forceinline__ void span2_f32(const float4 *__restrict__ A, const float2 *__restrict__ Q, int p0,
                                           int p1, float ut0, float vt0, float ut1, float vt1, float &r0,
                                           float &r1) {
     const f2_t U0 = f2_pack(ut0, ut0), V0 = f2_pack(vt0, vt0);
     const f2_t U1 = f2_pack(ut1, ut1), V1 = f2_pack(vt1, vt1);
     f2_t a0 = 0ull, a1 = 0ull;
-#pragma unroll 4
+    P2P_UNROLL(P2P_SPAN2_UNROLL)
     for (int p = p0; p < p1; ++p) {
         const float4 s = A[p];
         const float2 q = Q[p];
@@ -208,7 +213,7 @@ template <typename T>
 struct P2PArgs {
     const int32_t *tiles;  // Morton tile indices in queue order (LPT or Morton, chosen by the plan)
     int ntiles;
-    int *queue;            // dynamic tile counter, zeroed before each launch
+    int *queue;            // [0] dynamic tile counter, [1] exited CTAs; the last CTA out resets both
     int k;                 // tile side = 2^k leaf boxes
     int64_t S;             // grid side 2^(L-1)
     T h, eps2;
@@ -231,6 +236,7 @@ struct P2PArgs {
     const int32_t *tile_tgt_base;   // TILED: plan index of each tile's first target
     int ns;                     // TILED: work items per target (1 = whole target, 3 = one per row-run)
     int nbuf;                   // TILED: 2 = prefetch the next tile's record during this tile
+    unsigned long long *trace;  // optional per-tile timeline (diagnostics; nullptr = off)
     T *out;
     int accumulate;
 };
@@ -243,6 +249,49 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
         if (lane >= o) v += x;
     }
     return v;
+}
+
+// s_q[i] = q[s_idx[i]] (0 for pads) for i = first, first + stride, ... < n, with
+// up to 8 independent L2 loads in flight per thread.
+template <typename T>
+__device__ __forceinline__ void gather_weights(const int32_t *__restrict__ s_idx, const T *__restrict__ q,
+                                               T *__restrict__ s_q, int n, int first, int stride) {
+    for (int base = first; base < n; base += 8 * stride) {
+        T v[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+            const int i = base + x * stride;
+            const int32_t j = i < n ? s_idx[i] : -1;
+            v[x] = j >= 0 ? __ldg(q + j) : (T)0;
+        }
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+            const int i = base + x * stride;
+            if (i < n) s_q[i] = v[x];
+        }
+    }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
+// Called once per CTA by one thread after its last tile: the last CTA to leave
+// resets the queue for the next launch (no per-apply memset node).
+__device__ __forceinline__ void queue_exit(int *queue) {
+    __threadfence();
+    if (atomicAdd(queue + 1, 1) == (int)gridDim.x - 1) {
+        queue[0] = 0;
+        queue[1] = 0;
+        __threadfence();
+    }
 }
 
 // Next tile from the dynamic queue (one atomic per CTA per tile).
@@ -442,6 +491,7 @@ p2p_nr_kernel(const P2PArgs<T> a) {
         }
         // the next_tile() barrier orders this tile's shared-memory reads before the next tile's writes
     }
+    if (tid == 0) queue_exit(a.queue);
 }
 
 // ---------------------------------------------------------------- R kernel
@@ -565,6 +615,7 @@ p2p_r_kernel(const P2PArgs<T> a) {
             a.out[tb + t] = a.accumulate ? a.out[tb + t] + phi : phi;
         }
     }
+    if (tid == 0) queue_exit(a.queue);
 }
 
 // ---------------------------------------------------------------- TILED kernel
@@ -643,6 +694,11 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
     uint32_t parity = 0u;  // bit b = phase parity of buffer b's mbarrier
 
     while (cur < a.ntiles) {
+        unsigned long long *trc = (a.trace && tid == 0) ? a.trace + 8 * (size_t)cur : nullptr;
+        if (trc) {
+            trc[0] = (unsigned long long)smid() << 32 | blockIdx.x;
+            trc[1] = gtimer();
+        }
         const unsigned char *B = smem + c.buf0 + buf * c.bufsz;
         const uint16_t *table = reinterpret_cast<const uint16_t *>(B + c.table);
         const uint16_t *ttab = table + RR + 1;  // target box starts of the tile
@@ -669,6 +725,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                 : "memory");
             parity ^= 1u << buf;
         }
+        if (trc) trc[2] = gtimer();
         const int nent = (int)table[RR];
         const int nt = (int)ttab[WW];
         if (TPI == 2 && wid == 0) {  // units of two targets of one box
@@ -683,10 +740,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             }
             if (lane == 0) s_units = carry;
         }
-        for (int i = tid; i < nent; i += NT) {  // weights through the per-entry index
-            const int32_t j = s_idx[i];
-            s_q[i] = j >= 0 ? a.q[j] : (T)0;
-        }
+        gather_weights(s_idx, a.q, s_q, nent, tid, NT);  // weights through the per-entry index
         __syncthreads();
         if (TPI == 2) {
             for (int t = tid; t < nt; t += NT) {
@@ -702,6 +756,11 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             __syncthreads();
         }
         const int nu = TPI == 2 ? s_units : nt;
+        if (trc) {
+            trc[3] = gtimer();
+            trc[6] = nu;
+            trc[7] = (unsigned long long)nent;
+        }
 
         // one (unit, row) item: TPI partial sums over the row-run's sources
         auto item = [&](int u, int row, T *res, int piece, int f) {
@@ -784,50 +843,279 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                     finish(u, acc[0]);
                 }
             }
-        } else {
-            // (row, piece, unit) items: each row-run is split into f pieces, f chosen per
-            // tile so the item count lands just under a multiple of the CTA size (the
-            // last round of items is otherwise nearly empty); partials are then summed
-            // in (row, piece) order -- deterministic for a given plan.
-            int f = 1;
-            {
-                float best = 0.f;
-                for (int ff = 1; ff <= kMaxPieces; ++ff) {
-                    const int items = 3 * ff * nu, rounds = (items + NT - 1) / NT;
-                    const float eff = (float)items / (float)(rounds * NT) - 0.03f * (ff - 1);
-                    if (eff > best + 1e-6f) {
-                        best = eff;
-                        f = ff;
-                    }
-                }
-            }
-            const int nrp = 3 * f;
-            for (int it = tid; it < nrp * nu; it += NT) {
-                const int rp = it / nu, u = it - rp * nu;
-                const int row = rp / f, piece = rp - row * f;
+        } else {  // (unit, row) items, then the fixed-order reduction of the three partials
+            for (int it = tid; it < 3 * nu; it += NT) {
+                const int row = (it >= nu) + (it >= 2 * nu);
+                const int u = it - row * nu;
                 T res[TPI];
-                if (f == 1) {
-                    item(u, row, res, 0, 1);
-                } else {
-                    item(u, row, res, piece, f);
-                }
+                item(u, row, res, 0, 1);
 #pragma unroll
-                for (int x = 0; x < TPI; ++x) part[rp * TPI * nu + TPI * u + x] = res[x];
+                for (int x = 0; x < TPI; ++x) part[row * TPI * nu + TPI * u + x] = res[x];
             }
             __syncthreads();
             const int rs = TPI * nu;
             for (int t = tid; t < nt; t += NT) {
                 const int sl = TPI == 2 ? tslot[t] : t;
-                T acc = part[sl];
-                for (int rp = 1; rp < nrp; ++rp) acc += part[rp * rs + sl];
-                finish(t, acc);
+                finish(t, part[sl] + part[rs + sl] + part[2 * rs + sl]);
             }
         }
         __syncthreads();  // buffer `buf` and the work arrays are free; s_next / s_base_next visible
+        if (trc) trc[5] = gtimer();
         cur = s_next;
         tb = s_base_next;
         if (db) buf ^= 1;
         else if (tid == 0 && cur < a.ntiles) issue(cur, 0);
+    }
+    if (tid == 0) queue_exit(a.queue);
+}
+
+// ---------------------------------------------------------------- TILED-WS kernel
+// Warp-specialised persistent pipeline over the TILED layout (the canonical
+// Blackwell producer/consumer structure, with mbarriers instead of CTA-wide
+// barriers):
+//   producer warp (the last one): pulls tiles from the queue; per tile, into a
+//     free pipeline slot: TMA bulk copy of the tile record (full[s], tx-count),
+//     weight gather through the per-entry index, work-unit formation (TPI
+//     targets of one box), meta; then arrives on ready[s];
+//   consumer warps: wait ready[s], stream the slot's units (each unit sweeps
+//     its three row-runs in order and writes its targets' potentials), then
+//     arrive on empty[s] and move straight to the next slot.
+// No CTA-wide barrier in the steady state: consumers flow from tile to tile
+// while the producer stages ahead (nslot = 2 or 3 slots).
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+template <typename T, int TPI, bool PAD, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32)
+p2p_tiled_ws_kernel(const P2PArgs<T> a) {
+    static_assert(!(TPI == 2) || (PAD && sizeof(T) == 4), "TPI = 2 is the padded fp32 path");
+    static_assert(!PAD || sizeof(T) == 4, "the padded layout is fp32");
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int k = a.k, W = 1 << k, R = W + 2, RR = R * R, WW = W * W, NSLOT = a.nbuf;
+    const WsCarve c = ws_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI, NSLOT);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + c.bars);  // full[NSLOT], ready[NSLOT], empty[NSLOT]
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    auto full = [&](int s) { return smem_addr(bars + s); };
+    auto ready = [&](int s) { return smem_addr(bars + NSLOT + s); };
+    auto empty = [&](int s) { return smem_addr(bars + 2 * NSLOT + s); };
+    if (tid == 0) {
+        for (int s = 0; s < NSLOT; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full(s)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ready(s)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty(s)), "r"(NCW));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (wid == NCW) {  // ===================== producer warp
+        // slot of iteration j = j % NSLOT; the bulk copy of iteration j is issued at
+        // iteration j - (NSLOT - 1), so NSLOT - 1 copies stream ahead of the gather.
+        int it_end = 0x7fffffff;          // first iteration without a tile
+        int tiles_q[4] = {-1, -1, -1, -1};  // tile of each slot (NSLOT <= 4)
+        auto claim_and_issue = [&](int j) {  // claim the tile of iteration j, issue its copy
+            const int sj = j % NSLOT, usej = j / NSLOT;
+            int ti = 0;
+            if (lane == 0) ti = atomicAdd(a.queue, 1);
+            ti = __shfl_sync(0xffffffffu, ti, 0);
+            if (ti >= a.ntiles) {
+                it_end = min(it_end, j);
+                return;
+            }
+            if (usej > 0) mbar_wait(empty(sj), (usej - 1) & 1);
+            #pragma unroll
+            for (int x = 0; x < 4; ++x)
+                if (x == sj) tiles_q[x] = ti;
+            if (lane == 0) {
+                unsigned char *S = smem + c.slot0 + sj * c.slotsz;
+                const int slot = a.tile_slot[ti];
+                const uint32_t rb = a.reg_off[slot], nent = a.reg_off[slot + 1] - rb;
+                const uint32_t pb = a.tgt_pack_off[slot], ntp = a.tgt_pack_off[slot + 1] - pb;
+                const uint32_t b_tab = (uint32_t)c.tstride * 2u, b_uv = nent * 2 * (uint32_t)sizeof(T),
+                               b_ix = nent * 4u, b_tuv = ntp * 2 * (uint32_t)sizeof(T), b_tbl = ntp * 2u;
+                const uint32_t bar = full(sj);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                             "r"(b_tab + b_uv + b_ix + b_tuv + b_tbl)
+                             : "memory");
+#define P2P_BULK(dst, src, bytes)                                                                        \
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" \
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(bar)                                   \
+                 : "memory")
+                P2P_BULK(S + c.table, a.reg_table + (size_t)slot * c.tstride, b_tab);
+                if (nent) {
+                    P2P_BULK(S + c.uv, a.reg_uv + 2 * (size_t)rb, b_uv);
+                    P2P_BULK(S + c.idx, a.reg_idx + rb, b_ix);
+                }
+                if (ntp) {
+                    P2P_BULK(S + c.tuv, a.tgt_ruv + 2 * (size_t)pb, b_tuv);
+                    P2P_BULK(S + c.tbl, a.tgt_bl + pb, b_tbl);
+                }
+#undef P2P_BULK
+            }
+        };
+        for (int j = 0; j < NSLOT - 1; ++j) claim_and_issue(j);
+        for (int it = 0;; ++it) {
+            const int s = it % NSLOT, use = it / NSLOT;
+            unsigned char *S = smem + c.slot0 + s * c.slotsz;
+            int *meta = reinterpret_cast<int *>(S + c.meta);
+            if (it >= it_end) {  // end of stream: the slot's previous use must be released first
+                if (use > 0) mbar_wait(empty(s), (use - 1) & 1);
+                if (lane == 0) {
+                    meta[0] = -1;
+                    mbar_arrive(ready(s));
+                }
+                break;
+            }
+            int ti = -1;
+            #pragma unroll
+            for (int x = 0; x < 4; ++x)
+                if (x == s) ti = tiles_q[x];
+            const int slot = a.tile_slot[ti];
+            const int tb = a.tile_tgt_base[slot];
+            const uint32_t nent = a.reg_off[slot + 1] - a.reg_off[slot];
+            mbar_wait(full(s), use & 1);
+            const uint16_t *table = reinterpret_cast<const uint16_t *>(S + c.table);
+            const uint16_t *ttab = table + RR + 1;
+            gather_weights(reinterpret_cast<const int32_t *>(S + c.idx), a.q, reinterpret_cast<T *>(S + c.q),
+                           (int)nent, lane, 32);
+            const int nt = (int)ttab[WW];
+            int nu = nt;
+            if (TPI == 2) {  // units: pairs of targets of one box, in box order
+                int *ut = reinterpret_cast<int *>(S + c.ut);
+                int *uj0 = reinterpret_cast<int *>(S + c.uj0);
+                int carry = 0;
+                for (int base = 0; base < WW; base += 32) {
+                    const int bl = base + lane;
+                    const int n = bl < WW ? (int)ttab[bl + 1] - (int)ttab[bl] : 0;
+                    const int np = (n + 1) >> 1;
+                    const int incl = warp_incl_scan(np);
+                    const int u0 = carry + incl - np;
+                    if (bl < WW && n > 0) {
+                        const int j0 = (int)compact16((uint32_t)bl >> 1) * R + (int)compact16((uint32_t)bl);
+                        const int t0 = ttab[bl];
+                        for (int x = 0; x < np; ++x) {
+                            ut[2 * (u0 + x)] = t0 + 2 * x;
+                            ut[2 * (u0 + x) + 1] = min(t0 + 2 * x + 1, t0 + n - 1);
+                            uj0[u0 + x] = j0;
+                        }
+                    }
+                    carry += __shfl_sync(0xffffffffu, incl, 31);
+                }
+                nu = carry;
+            }
+            if (lane == 0) {
+                meta[0] = ti;
+                meta[1] = tb;
+                meta[2] = nu;
+                meta[3] = 0;  // next unit chunk to claim
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ready(s));  // release: slot s is ready
+            claim_and_issue(it + NSLOT - 1);       // keep NSLOT - 1 copies in flight
+        }
+        if (lane == 0) queue_exit(a.queue);
+        return;
+    }
+
+    // ===================== consumer warps
+    const int ctid = tid, NCT = NCW * 32;
+    for (int it = 0;; ++it) {
+        const int s = it % NSLOT, use = it / NSLOT;
+        unsigned char *S = smem + c.slot0 + s * c.slotsz;
+        mbar_wait(ready(s), use & 1);
+        int *meta = reinterpret_cast<int *>(S + c.meta);
+        if (meta[0] < 0) break;
+        mbar_wait(full(s), use & 1);  // (already complete) makes the bulk-copied bytes visible here too
+        const int tb = meta[1], nu = meta[2];
+        const uint16_t *table = reinterpret_cast<const uint16_t *>(S + c.table);
+        const T *s_uv = reinterpret_cast<const T *>(S + c.uv);
+        const T *tuv = reinterpret_cast<const T *>(S + c.tuv);
+        const uint16_t *tbl = reinterpret_cast<const uint16_t *>(S + c.tbl);
+        const T *s_q = reinterpret_cast<const T *>(S + c.q);
+        const int *ut = reinterpret_cast<const int *>(S + c.ut);
+        const int *uj0 = reinterpret_cast<const int *>(S + c.uj0);
+
+        for (;;) {  // claim chunks of 32 units until the slot is exhausted
+            int base = 0;
+            if (lane == 0) base = atomicAdd(meta + 3, 32);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base >= nu) break;
+            const int u = base + lane;
+            if (u >= nu) continue;
+            int t0, t1, jb;
+            if (TPI == 2) {
+                t0 = ut[2 * u];
+                t1 = ut[2 * u + 1];
+                jb = uj0[u];
+            } else {
+                t0 = t1 = u;
+                const int bl = tbl[u];
+                jb = (int)compact16((uint32_t)bl >> 1) * R + (int)compact16((uint32_t)bl);
+            }
+            T acc0 = (T)0, acc1 = (T)0;
+            for (int row = 0; row < 3; ++row) {
+                const int j0 = jb + row * R;
+                const int i0 = table[j0], i1 = table[j0 + 3];
+                if constexpr (PAD) {
+                    const float4 *A = reinterpret_cast<const float4 *>(s_uv);
+                    const float2 *Q = reinterpret_cast<const float2 *>(s_q);
+                    if constexpr (TPI == 2) {
+                        float r0, r1;
+                        span2_f32(A, Q, i0 >> 1, i1 >> 1, tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t1], tuv[2 * t1 + 1],
+                                  r0, r1);
+                        acc0 += r0;
+                        acc1 += r1;
+                    } else {
+                        acc0 += span_f32(A, Q, i0 >> 1, i1 >> 1, tuv[2 * t0], tuv[2 * t0 + 1]);
+                    }
+                } else if constexpr (sizeof(T) == 4) {
+                    acc0 += span1_f32(reinterpret_cast<const float2 *>(s_uv), reinterpret_cast<const float *>(s_q), i0,
+                                      i1, tuv[2 * t0], tuv[2 * t0 + 1]);
+                } else {
+                    acc0 += span1_f64(reinterpret_cast<const double2 *>(s_uv), reinterpret_cast<const double *>(s_q),
+                                      i0, i1, tuv[2 * t0], tuv[2 * t0 + 1], a.eps2);
+                }
+            }
+#pragma unroll
+            for (int x = 0; x < TPI; ++x) {
+                const int t = x == 0 ? t0 : t1;
+                if (x == 1 && t1 == t0) break;
+                T acc = x == 0 ? acc0 : acc1;
+                if constexpr (sizeof(T) == 4) {
+                    if (!isfinite(acc)) {  // a pair closer than eps: redo this target with the explicit guard
+                        acc = 0.f;
+                        for (int row = 0; row < 3; ++row) {
+                            const int j0 = jb + row * R;
+                            if constexpr (PAD)
+                                acc += span_f32_guarded(reinterpret_cast<const float4 *>(s_uv),
+                                                        reinterpret_cast<const float2 *>(s_q), table[j0] >> 1,
+                                                        table[j0 + 3] >> 1, tuv[2 * t], tuv[2 * t + 1], a.eps2);
+                            else
+                                acc += span1_f32_guarded(reinterpret_cast<const float2 *>(s_uv),
+                                                         reinterpret_cast<const float *>(s_q), table[j0],
+                                                         table[j0 + 3], tuv[2 * t], tuv[2 * t + 1], a.eps2);
+                        }
+                    }
+                    acc = (-0.5f * kLn2) * acc;
+                } else {
+                    acc = -0.5 * acc;
+                }
+                a.out[tb + t] = a.accumulate ? a.out[tb + t] + acc : acc;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty(s));  // this warp is done with slot s
     }
 }
 

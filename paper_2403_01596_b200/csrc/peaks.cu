@@ -79,25 +79,27 @@ __global__ void __launch_bounds__(kThreads) read_kernel(const int4 *__restrict__
 // shared memory `iters` times (1 or 2 targets per thread).  Upper bound of the
 // pair rate the kernels can reach once staging and scheduling cost nothing.
 template <int TPI>
-__global__ void __launch_bounds__(kThreads) span_kernel(float *out, int iters, int nsrc) {
+__global__ void __launch_bounds__(kThreads) span_kernel(float *out, int iters, int nsrc, int groups, int gstride) {
     extern __shared__ __align__(16) unsigned char sm[];
+    const int tot = nsrc / 2 + (groups - 1) * gstride;  // source pairs incl. the group offsets
     float4 *A = reinterpret_cast<float4 *>(sm);
-    float2 *Q = reinterpret_cast<float2 *>(sm + 8 * nsrc);
-    for (int p = threadIdx.x; p < nsrc / 2; p += blockDim.x) {
+    float2 *Q = reinterpret_cast<float2 *>(sm + 16 * tot);
+    for (int p = threadIdx.x; p < tot; p += blockDim.x) {
         const float b = 0.001f * p;
         A[p] = make_float4(0.1f + b, 0.2f + b, 0.3f - b, 0.4f - b);
         Q[p] = make_float2(0.5f, -0.25f);
     }
     __syncthreads();
     const float ut = 0.05f + 1e-4f * threadIdx.x, vt = 0.07f + 1e-4f * blockIdx.x;
+    const int off = ((threadIdx.x & 31) % groups) * gstride;  // lanes of different groups read different pairs
     float acc = 0.f;
     for (int it = 0; it < iters; ++it) {
         if (TPI == 2) {
             float r0, r1;
-            p2p::dev::span2_f32(A, Q, 0, nsrc / 2, ut + it * 1e-7f, vt, ut, vt + 1e-3f, r0, r1);
+            p2p::dev::span2_f32(A, Q, off, off + nsrc / 2, ut + it * 1e-7f, vt, ut, vt + 1e-3f, r0, r1);
             acc += r0 + r1;
         } else {
-            acc += p2p::dev::span_f32(A, Q, 0, nsrc / 2, ut + it * 1e-7f, vt);
+            acc += p2p::dev::span_f32(A, Q, off, off + nsrc / 2, ut + it * 1e-7f, vt);
         }
     }
     if (acc == 1234.5f) out[0] = acc;
@@ -168,16 +170,16 @@ p2p_peak_status p2p_peak_dfma(int device, double *flops) {
     return st;
 }
 
-p2p_peak_status p2p_peak_span(int device, int tpi, int nsrc, double *pairs_per_s) {
+p2p_peak_status p2p_peak_span(int device, int tpi, int nsrc, int groups, int gstride, double *pairs_per_s) {
     const int grid = sm_count(device) * 6, iters = 64;
     float *d = nullptr;
     cudaSetDevice(device);
     cudaMalloc(&d, 16);
-    const size_t sm = (size_t)nsrc * 12;
+    const size_t sm = (size_t)(nsrc / 2 + (groups - 1) * gstride) * 24;
     double ms = 0;
     p2p_peak_status st = tpi == 2
-        ? timed(device, 5, [&] { span_kernel<2><<<grid, kThreads, sm>>>(d, iters, nsrc); }, &ms)
-        : timed(device, 5, [&] { span_kernel<1><<<grid, kThreads, sm>>>(d, iters, nsrc); }, &ms);
+        ? timed(device, 5, [&] { span_kernel<2><<<grid, kThreads, sm>>>(d, iters, nsrc, groups, gstride); }, &ms)
+        : timed(device, 5, [&] { span_kernel<1><<<grid, kThreads, sm>>>(d, iters, nsrc, groups, gstride); }, &ms);
     cudaFree(d);
     *pairs_per_s = (double)grid * kThreads * iters * nsrc * tpi / (ms * 1e-3);
     return st;

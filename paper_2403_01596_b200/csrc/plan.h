@@ -71,8 +71,6 @@ P2P_HD inline RCarve r_carve(int k, int src_cap, int tgt_cap, int e) {
     return c;
 }
 
-constexpr int kMaxPieces = 3;  // TILED: a row-run split into at most 3 pieces
-
 struct TCarve {
     int buf0, bufsz;                      // double-buffered, bulk-copied part: 2 x bufsz bytes from buf0
     int table, uv, idx, tuv, tbl;         // offsets inside one buffer
@@ -103,8 +101,35 @@ P2P_HD inline TCarve tiled_carve(int k, int src_cap, int tgt_cap, int e, int tpi
     c.ut = c.uj0 + 4 * c.ucap;
     c.tslot = c.ut + 4 * tpi * c.ucap;
     c.part = align16(c.tslot + 4 * tgt_cap);
-    c.bar = align16(c.part + (ns == 1 ? 1 : 3 * kMaxPieces) * e * tpi * c.ucap);
+    c.bar = align16(c.part + (ns == 1 ? 1 : 3) * e * tpi * c.ucap);
     c.total = c.bar + 16;
+    return c;
+}
+
+// Warp-specialised TILED kernel: nslot pipeline slots, each = one tile record
+// (bulk-copied) + gathered weights + work units + meta; 3 mbarriers per slot.
+struct WsCarve {
+    int slot0, slotsz;                    // slot s at slot0 + s * slotsz
+    int table, uv, idx, tuv, tbl, q, ut, uj0, meta;  // offsets inside a slot
+    int bars, total, ucap, tstride;
+};
+P2P_HD inline WsCarve ws_carve(int k, int src_cap, int tgt_cap, int e, int tpi, int nslot) {
+    WsCarve c;
+    c.ucap = nr_unit_cap(k, tgt_cap, tpi);
+    c.tstride = tiled_table_stride(k);
+    c.table = 0;
+    c.uv = align16(2 * c.tstride);
+    c.idx = c.uv + 2 * e * src_cap;
+    c.tuv = align16(c.idx + 4 * src_cap);
+    c.tbl = c.tuv + 2 * e * tgt_cap;
+    c.q = align16(c.tbl + 2 * tgt_cap);
+    c.ut = align16(c.q + e * src_cap);
+    c.uj0 = c.ut + 4 * tpi * c.ucap;
+    c.meta = align16(c.uj0 + 4 * c.ucap);
+    c.slotsz = align16(c.meta + 16);
+    c.slot0 = 0;
+    c.bars = nslot * c.slotsz;
+    c.total = c.bars + 3 * 8 * nslot;
     return c;
 }
 
@@ -198,6 +223,8 @@ struct HostPlan {
     int nbuf = 1;                                 // TILED record buffers (2 = prefetch next tile)
     bool pad = true;                              // TILED: boxes padded to even counts (packed f32x2 loops)
     int nt = 256;                                 // threads per CTA (TILED: 128 or 256)
+    bool ws = true;                               // TILED: warp-specialised pipeline kernel
+    int ncw = 8;                                  // TILED-WS consumer warps per CTA
     std::vector<int32_t> tile_slot;               // launch order -> slot
     int64_t reg_entries = 0;
 

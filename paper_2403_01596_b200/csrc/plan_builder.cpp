@@ -212,7 +212,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             const int64_t WWk = int64_t(1) << (2 * kk);
             int64_t ne = 0;
             for (int64_t t = 0; t < hp.B / WWk; ++t) ne += to[(t + 1) * WWk] > to[t * WWk];
-            if ((double)hp.n_tgt / (double)std::max<int64_t>(ne, 1) >= 0.75 * 256) {
+            if ((double)hp.n_tgt / (double)std::max<int64_t>(ne, 1) >= 115.0) {  // measured best (tools/sweep.py)
                 k = kk;
                 break;
             }
@@ -278,7 +278,18 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         if (const char *v = std::getenv("P2P_NS")) hp.ns = std::atoi(v) == 3 ? 3 : 1;
         if (const char *v = std::getenv("P2P_NBUF")) hp.nbuf = std::atoi(v) == 2 ? 2 : 1;
         if (const char *v = std::getenv("P2P_NT"))
-            if (d.layout == P2P_LAYOUT_TILED) hp.nt = std::atoi(v) == 256 ? 256 : 128;
+            if (d.layout == P2P_LAYOUT_TILED) {
+                const int x = std::atoi(v);
+                hp.nt = x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : 256;
+            }
+        hp.ws = false;  // the warp-specialised variant measured slower; kept for experiments
+        if (const char *v = std::getenv("P2P_WS")) hp.ws = std::atoi(v) != 0;
+        hp.ncw = 8;
+        if (const char *v = std::getenv("P2P_NCW")) hp.ncw = std::atoi(v) == 4 ? 4 : 8;
+        if (d.layout == P2P_LAYOUT_TILED && hp.ws) {
+            hp.nbuf = 2;
+            if (const char *v = std::getenv("P2P_NBUF")) hp.nbuf = std::max(2, std::min(4, std::atoi(v)));
+        }
         if (d.layout == P2P_LAYOUT_TILED && !hp.pad) {  // unpadded region sizes
             int64_t mx = 0;
             for (int64_t i = 0; i < nt; ++i) {
@@ -297,7 +308,9 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         }
         const int sc = (int)std::min<int64_t>(hp.src_cap, 1 << 24), tc = (int)std::min<int64_t>(hp.tgt_cap, 1 << 24);
         int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? (int64_t)nr_carve(k, sc, tc, e, hp.tpi).total
-                       : d.layout == P2P_LAYOUT_TILED      ? (int64_t)tiled_carve(k, sc, tc, e, hp.tpi, hp.ns, hp.nbuf).total
+                       : d.layout == P2P_LAYOUT_TILED
+                           ? (hp.ws ? (int64_t)ws_carve(k, sc, tc, e, hp.tpi, hp.nbuf).total
+                                    : (int64_t)tiled_carve(k, sc, tc, e, hp.tpi, hp.ns, hp.nbuf).total)
                                                            : (int64_t)r_carve(k, sc, tc, e).total;
         hp.smem_bytes = smem;
         if (smem <= kSmemLimit) break;

@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libp2p_b200.so")
+LIB_PATH = os.environ.get("P2P_LIB") or os.path.join(_PKG, "lib", "libp2p_b200.so")  # P2P_LIB: experiments
 
 P2P_SUCCESS = 0
 P2P_ERROR_INVALID_ARGUMENT = 1

@@ -1,0 +1,5 @@
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "tiled" 2>&1 | tail -3
+timeout 1200 python tools/sweep.py --configs d16_1e6,d32_1e6,d64_1e6,lowd1_1e7,lowd025_1e7,lowd4_1e7 --layout tiled --tpi 1,2 --ns 1 --nbuf 2,3 --nt 128 --pad 1 --json gpurun_out/sweep4_ws.json
+P2P_NCW=4 timeout 1200 python tools/sweep.py --configs d16_1e6,d64_1e6,lowd1_1e7 --layout tiled --tpi 1,2 --ns 1 --nbuf 2 --nt 128 --pad 1
+timeout 1200 python tools/sweep.py --configs lowd1_1e7,lowd025_1e7 --layout tiled --tpi 1 --ns 1 --nbuf 2,3 --nt 128 --pad 0

@@ -1,0 +1,8 @@
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "tiled" 2>&1 | tail -3
+echo "== WS"
+timeout 1200 python tools/sweep.py --configs d16_1e6,d64_1e6 --layout tiled --tpi 1,2 --ns 1 --nbuf 2,3 --nt 128 --pad 1
+timeout 1200 python tools/sweep.py --configs lowd1_1e7,lowd025_1e7 --layout tiled --tpi 1 --ns 1 --nbuf 2,3,4 --nt 128 --pad 0
+echo "== non-WS"
+P2P_WS=0 timeout 1200 python tools/sweep.py --configs d16_1e6,d64_1e6 --layout tiled --tpi 2 --ns 3 --nbuf 1 --nt 128,256 --pad 1
+P2P_WS=0 timeout 1200 python tools/sweep.py --configs lowd1_1e7,lowd025_1e7 --layout tiled --tpi 1 --ns 1 --nbuf 1 --nt 128 --pad 0

@@ -1,0 +1,7 @@
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "tiled" 2>&1 | tail -2
+export P2P_WS=1
+for NCW in 8 4; do
+P2P_NCW=$NCW timeout 1200 python tools/sweep.py --configs d16_1e6,d32_1e6,d64_1e6 --layout tiled --tpi 2 --ns 1 --nbuf 2,3 --nt 128 --pad 1 --tile 1,2
+P2P_NCW=$NCW timeout 1200 python tools/sweep.py --configs lowd1_1e7,lowd025_1e7 --layout tiled --tpi 1 --ns 1 --nbuf 2,3 --nt 128 --pad 0
+done

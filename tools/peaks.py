@@ -11,9 +11,11 @@ for name in ("p2p_peak_mufu_lg2", "p2p_peak_ffma2", "p2p_peak_dfma", "p2p_peak_h
     f.argtypes = [C.c_int, C.POINTER(C.c_double)]
     v = C.c_double(0)
     out[name] = (f(0, C.byref(v)), v.value)
-lib.p2p_peak_span.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+lib.p2p_peak_span.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
 for tpi in (1, 2):
     for n in (48, 144, 576):
-        v = C.c_double(0)
-        out[f"span_tpi{tpi}_n{n}"] = (lib.p2p_peak_span(0, tpi, n, C.byref(v)), v.value)
+        for groups, gstride in ((1, 0), (2, 1), (4, 1), (4, 37), (8, 1), (8, 37), (32, 1)):
+            v = C.c_double(0)
+            out[f"span_tpi{tpi}_n{n}_g{groups}_s{gstride}"] = (lib.p2p_peak_span(0, tpi, n, groups, gstride, C.byref(v)),
+                                                               v.value / 4.653e12)
 print(json.dumps(out, indent=1))
