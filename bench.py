@@ -190,8 +190,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # More ranks than visible GPUs (a 1-GPU test box): ranks share devices and the
+    # halo exchange is staged through the host over gloo (test mode, flagged in the JSON).
+    shared = world > max(1, torch.cuda.device_count())
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
@@ -230,8 +237,14 @@ def main():
         else:
             if j["info"]["n_send"]:
                 pl.halo_pack(j["q_owned"], j["send"], stream.cuda_stream)
-            dist.all_to_all_single(j["halo"][: j["info"]["n_halo"]], j["send"][: j["info"]["n_send"]],
-                                   j["recv_splits"], j["send_splits"])
+            if shared:  # host-staged exchange (test mode)
+                recv = torch.empty(j["info"]["n_halo"], dtype=j["halo"].dtype)
+                dist.all_to_all_single(recv, j["send"][: j["info"]["n_send"]].cpu(), j["recv_splits"],
+                                       j["send_splits"])
+                j["halo"][: j["info"]["n_halo"]].copy_(recv)
+            else:
+                dist.all_to_all_single(j["halo"][: j["info"]["n_halo"]], j["send"][: j["info"]["n_send"]],
+                                       j["recv_splits"], j["send_splits"])
             pl.apply_dist(j["q_owned"], j["halo"], j["out"], stream=stream.cuda_stream)
 
     def step():
@@ -269,7 +282,7 @@ def main():
     kern_ms = np.array([[a.elapsed_time(b) for a, b in row] for row in kev])  # [K, jobs]
     total_ms = float(step_ms.sum())
     if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([total_ms], device="cpu" if shared else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -309,7 +322,9 @@ def main():
         "config": {"workload": args.workload, "configs": names, "layout": args.layout,
                    "precision": args.precision, "kind": args.kind, "pairs_per_step": pairs_step,
                    "order": "plan", "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": f"morton-range x{world}" + (" + NCCL halo exchange" if world > 1 else "")},
+                   "parallelism": f"morton-range x{world}" + (
+                       (" + host-staged gloo halo exchange, ranks sharing GPUs (TEST MODE)" if shared
+                        else " + NCCL halo exchange") if world > 1 else "")},
         "gpu_launches": args.steps * len(jobs) * (1 if world == 1 else 3),
         "roofline": roofline, "clocks": clocks, "e2e": e2e, "per_config": per_cfg,
     }

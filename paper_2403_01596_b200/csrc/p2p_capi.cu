@@ -44,7 +44,7 @@ struct p2p_plan_s {
     // device arrays
     DevBuf tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
-    DevBuf tile_slot, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_ruv, tgt_pack_off, tile_tgt_base;
+    DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     int grid = 0;                                // persistent CTAs per launch
     unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
@@ -69,7 +69,7 @@ struct p2p_plan_s {
     void release() {
         DevBuf *all[] = {&tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
-                         &tile_slot, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_ruv,
+                         &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi,
                          &io_q, &io_out, &queue};
         for (DevBuf *b : all) {
@@ -105,6 +105,7 @@ const void *tiled_fn_nt(int nt) {
 template <typename T>
 const void *tiled_fn(int tpi, int nt, bool pad) {
     if constexpr (sizeof(T) == 4) {
+        if (tpi == 4) return tiled_fn_nt<float, 4, true>(nt);
         if (tpi == 2) return tiled_fn_nt<float, 2, true>(nt);
         return pad ? tiled_fn_nt<float, 1, true>(nt) : tiled_fn_nt<float, 1, false>(nt);
     } else {
@@ -149,6 +150,7 @@ void upload_plan(p2p_plan_s &P) {
         P.upload(P.src_uv, lay.src_uv);
     } else if (hp.layout == P2P_LAYOUT_TILED) {
         P.upload(P.tile_slot, hp.tile_slot);
+        P.upload(P.tile_part, hp.tile_part);
         P.upload(P.reg_off, hp.reg_off);
         P.upload(P.reg_idx, hp.reg_idx);
         P.upload(P.reg_uv, lay.reg_uv);
@@ -226,6 +228,7 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
     } else if (hp.layout == P2P_LAYOUT_TILED) {
         a.q = q_local;
         a.tile_slot = (const int32_t *)P.tile_slot.p;
+        a.tile_part = (const int32_t *)P.tile_part.p;
         a.reg_off = (const uint32_t *)P.reg_off.p;
         a.reg_idx = (const int32_t *)P.reg_idx.p;
         a.reg_uv = (const T *)P.reg_uv.p;

@@ -175,6 +175,38 @@ __device__ __forceinline__ double span1_f64(const double2 *__restrict__ UV, cons
     return acc;
 }
 
+// Four targets sharing one span x two sources per step: 8 pairs per LDS.128 + LDS.64.
+__device__ __forceinline__ void span4_f32(const float4 *__restrict__ A, const float2 *__restrict__ Q, int p0,
+                                          int p1, const float *ut, const float *vt, float *r) {
+    f2_t U[4], V[4], acc[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+        U[x] = f2_pack(ut[x], ut[x]);
+        V[x] = f2_pack(vt[x], vt[x]);
+        acc[x] = 0ull;
+    }
+#pragma unroll 2
+    for (int p = p0; p < p1; ++p) {
+        const float4 s = A[p];
+        const float2 q = Q[p];
+        const f2_t su = f2_pack(s.x, s.y), sv = f2_pack(s.z, s.w), qq = f2_pack(q.x, q.y);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            const f2_t du = f2_sub(U[x], su), dv = f2_sub(V[x], sv);
+            const f2_t w = f2_fma(dv, dv, f2_mul(du, du));
+            float w0, w1;
+            f2_unpack(w, w0, w1);
+            acc[x] = f2_fma(qq, f2_pack(lg2_approx(w0), lg2_approx(w1)), acc[x]);
+        }
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+        float c0, c1;
+        f2_unpack(acc[x], c0, c1);
+        r[x] = c0 + c1;
+    }
+}
+
 // Explicitly guarded fp32 sweep (slow path for targets whose fast sum is not finite).
 __device__ __noinline__ float span_f32_guarded(const float4 *__restrict__ A, const float2 *__restrict__ Q,
                                                int p0, int p1, float ut, float vt, float eps2) {
@@ -226,6 +258,7 @@ struct P2PArgs {
     const uint32_t *halo_off;  // R: [B+1] packed-halo offsets
     const T *halo_uv;      // R: packed-halo coordinates relative to the target box origin
     const int32_t *tile_slot;   // TILED: launch order -> Morton slot of the per-tile arrays
+    const int32_t *tile_part;   // TILED: launch order -> part | nparts << 16 (unit range of the tile)
     const uint32_t *reg_off;    // TILED: [slots+1] packed-region offsets
     const int32_t *reg_idx;     // TILED: local source index per packed entry (-1 = pad)
     const T *reg_uv;            // TILED: region-relative coordinates (fp32: (u0,u1,v0,v1) per pair)
@@ -634,7 +667,7 @@ p2p_r_kernel(const P2PArgs<T> a) {
 template <typename T, int TPI, int NT, bool PAD>
 __global__ void __launch_bounds__(NT)
 p2p_tiled_kernel(const P2PArgs<T> a) {
-    static_assert(!(TPI == 2) || (PAD && sizeof(T) == 4), "TPI = 2 is the padded fp32 path");
+    static_assert(TPI == 1 || (PAD && sizeof(T) == 4), "TPI > 1 is the padded fp32 path");
     static_assert(!PAD || sizeof(T) == 4, "the padded layout is fp32");
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_next, s_units, s_base_next;
@@ -728,12 +761,12 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         if (trc) trc[2] = gtimer();
         const int nent = (int)table[RR];
         const int nt = (int)ttab[WW];
-        if (TPI == 2 && wid == 0) {  // units of two targets of one box
+        if (TPI > 1 && wid == 0) {  // units of TPI targets of one box
             int carry = 0;
             for (int base = 0; base < WW; base += 32) {
                 const int bl = base + lane;
                 const int n = bl < WW ? (int)ttab[bl + 1] - (int)ttab[bl] : 0;
-                const int np = (n + 1) >> 1;
+                const int np = (n + TPI - 1) / TPI;
                 const int incl = warp_incl_scan(np);
                 if (bl < WW) pstart[bl] = carry + incl - np;
                 carry += __shfl_sync(0xffffffffu, incl, 31);
@@ -742,20 +775,22 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         }
         gather_weights(s_idx, a.q, s_q, nent, tid, NT);  // weights through the per-entry index
         __syncthreads();
-        if (TPI == 2) {
+        if (TPI > 1) {
             for (int t = tid; t < nt; t += NT) {
                 const int bl = tbl[t];
-                const int r = t - (int)ttab[bl], u = pstart[bl] + (r >> 1), sl = r & 1;
-                ut[2 * u + sl] = t;
-                tslot[t] = 2 * u + sl;
-                if (sl == 0) {
-                    uj0[u] = (int)compact16((uint32_t)bl >> 1) * R + (int)compact16((uint32_t)bl);
-                    if (t + 1 == (int)ttab[bl + 1]) ut[2 * u + 1] = t;
-                }
+                const int r = t - (int)ttab[bl], u = pstart[bl] + r / TPI, sl = r % TPI;
+                ut[TPI * u + sl] = t;
+                tslot[t] = TPI * u + sl;
+                if (sl == 0) uj0[u] = (int)compact16((uint32_t)bl >> 1) * R + (int)compact16((uint32_t)bl);
+                if (t + 1 == (int)ttab[bl + 1])  // box's last target fills the unit's empty slots (duplicates)
+                    for (int x = sl + 1; x < TPI; ++x) ut[TPI * u + x] = t;
             }
             __syncthreads();
         }
-        const int nu = TPI == 2 ? s_units : nt;
+        const int nu = TPI > 1 ? s_units : nt;
+        const int pinfo = a.tile_part[cur], npart = pinfo >> 16, ipart = pinfo & 0xffff;
+        const int ub = (int)(((long long)nu * ipart) / npart), ue = (int)(((long long)nu * (ipart + 1)) / npart);
+        const int nr = ue - ub;
         if (trc) {
             trc[3] = gtimer();
             trc[6] = nu;
@@ -765,8 +800,8 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         // one (unit, row) item: TPI partial sums over the row-run's sources
         auto item = [&](int u, int row, T *res, int piece, int f) {
             int t0, jb;
-            if (TPI == 2) {
-                t0 = ut[2 * u];
+            if (TPI > 1) {
+                t0 = ut[TPI * u];
                 jb = uj0[u];
             } else {
                 t0 = u;
@@ -784,7 +819,16 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             if constexpr (PAD) {
                 const float4 *A = reinterpret_cast<const float4 *>(s_uv);
                 const float2 *Q = reinterpret_cast<const float2 *>(s_q);
-                if constexpr (TPI == 2) {
+                if constexpr (TPI == 4) {
+                    float xs[4], ys[4];
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const int tx = ut[4 * u + x];
+                        xs[x] = tuv[2 * tx];
+                        ys[x] = tuv[2 * tx + 1];
+                    }
+                    span4_f32(A, Q, i0 >> 1, i1 >> 1, xs, ys, res);
+                } else if constexpr (TPI == 2) {
                     const int t1 = ut[2 * u + 1];
                     span2_f32(A, Q, i0 >> 1, i1 >> 1, tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t1], tuv[2 * t1 + 1],
                               res[0], res[1]);
@@ -826,7 +870,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         };
 
         if (NS == 1) {  // one item per unit, rows in order
-            for (int u = tid; u < nu; u += NT) {
+            for (int u = ub + tid; u < ue; u += NT) {
                 T acc[TPI], r[TPI];
 #pragma unroll
                 for (int x = 0; x < TPI; ++x) acc[x] = (T)0;
@@ -835,18 +879,21 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
 #pragma unroll
                     for (int x = 0; x < TPI; ++x) acc[x] += r[x];
                 }
-                if (TPI == 2) {
-                    const int t0 = ut[2 * u], t1 = ut[2 * u + 1];
-                    finish(t0, acc[0]);
-                    if (t1 != t0) finish(t1, acc[TPI - 1]);
+                if (TPI > 1) {
+#pragma unroll
+                    for (int x = 0; x < TPI; ++x) {
+                        const int t = ut[TPI * u + x];
+                        if (x > 0 && t == ut[TPI * u + x - 1]) break;  // duplicates fill the box's last unit
+                        finish(t, acc[x]);
+                    }
                 } else {
                     finish(u, acc[0]);
                 }
             }
         } else {  // (unit, row) items, then the fixed-order reduction of the three partials
-            for (int it = tid; it < 3 * nu; it += NT) {
-                const int row = (it >= nu) + (it >= 2 * nu);
-                const int u = it - row * nu;
+            for (int it = tid; it < 3 * nr; it += NT) {
+                const int row = (it >= nr) + (it >= 2 * nr);
+                const int u = ub + it - row * nr;
                 T res[TPI];
                 item(u, row, res, 0, 1);
 #pragma unroll
@@ -854,9 +901,14 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             }
             __syncthreads();
             const int rs = TPI * nu;
-            for (int t = tid; t < nt; t += NT) {
-                const int sl = TPI == 2 ? tslot[t] : t;
-                finish(t, part[sl] + part[rs + sl] + part[2 * rs + sl]);
+            for (int u = ub + tid; u < ue; u += NT) {
+#pragma unroll
+                for (int x = 0; x < TPI; ++x) {
+                    const int t = TPI > 1 ? ut[TPI * u + x] : u;
+                    if (x > 0 && t == ut[TPI * u + x - 1]) break;  // duplicates fill the box's last unit
+                    const int sl = TPI * u + x;
+                    finish(t, part[sl] + part[rs + sl] + part[2 * rs + sl]);
+                }
             }
         }
         __syncthreads();  // buffer `buf` and the work arrays are free; s_next / s_base_next visible

@@ -30,7 +30,7 @@ struct NrCarve {
 // (1, or 2 = pairs of targets of the same box).
 P2P_HD inline int nr_unit_cap(int k, int tgt_cap, int tpi) {
     const int WW = 1 << (2 * k);
-    return tpi == 2 ? (((tgt_cap + WW) / 2 + 4) & ~3) : tgt_cap;
+    return tpi > 1 ? (((tgt_cap + (tpi - 1) * WW) / tpi + 4) & ~3) : tgt_cap;
 }
 P2P_HD inline NrCarve nr_carve(int k, int src_cap, int tgt_cap, int e, int tpi) {
     const int W = 1 << k, R = W + 2, RR = R * R, WW = W * W;
@@ -226,6 +226,7 @@ struct HostPlan {
     bool ws = true;                               // TILED: warp-specialised pipeline kernel
     int ncw = 8;                                  // TILED-WS consumer warps per CTA
     std::vector<int32_t> tile_slot;               // launch order -> slot
+    std::vector<int32_t> tile_part;               // launch order -> part | nparts << 16 (tail splitting)
     int64_t reg_entries = 0;
 
     Layout<float> f32;

@@ -261,19 +261,22 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         hp.max_tile_halo = halo.empty() ? 0 : *std::max_element(halo.begin(), halo.end());
         hp.tgt_cap = pad8(tcount.empty() ? 0 : *std::max_element(tcount.begin(), tcount.end()));
         hp.src_cap = d.layout == P2P_LAYOUT_REDUNDANT ? hp.max_tile_halo : pad4(hp.max_region);
-        hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= 4.0 && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT) ? 2 : 1;
+        hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= 8.0 && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT) ? 2 : 1;
         // TILED defaults: dense fp32 -> padded pairs, 2 targets per unit, (unit, row) items;
         // sparse or fp64 -> unpadded, one item per target; 128-thread CTAs.
         hp.pad = d.layout == P2P_LAYOUT_TILED ? (hp.tpi == 2) : true;
-        hp.ns = hp.tpi == 2 ? 3 : 1;
+        hp.ns = hp.tpi > 1 ? 3 : 1;
         hp.nbuf = 1;
         hp.nt = d.layout == P2P_LAYOUT_TILED ? 128 : kThreads;
         // tuning hooks (experiments only): P2P_TPI, P2P_NS, P2P_NBUF, P2P_PAD, P2P_NT
         if (const char *v = std::getenv("P2P_TPI"))
-            if (d.precision == P2P_FP32 && d.layout != P2P_LAYOUT_REDUNDANT) hp.tpi = std::atoi(v) == 2 ? 2 : 1;
+            if (d.precision == P2P_FP32 && d.layout != P2P_LAYOUT_REDUNDANT) {
+                const int x = std::atoi(v);
+                hp.tpi = x >= 4 && d.layout == P2P_LAYOUT_TILED ? 4 : x == 2 ? 2 : 1;
+            }
         if (const char *v = std::getenv("P2P_PAD"))
             if (d.layout == P2P_LAYOUT_TILED && d.precision == P2P_FP32) hp.pad = std::atoi(v) != 0;
-        if (hp.tpi == 2) hp.pad = true;
+        if (hp.tpi > 1) hp.pad = true;
         if (d.precision == P2P_FP64 && d.layout == P2P_LAYOUT_TILED) hp.pad = false;
         if (const char *v = std::getenv("P2P_NS")) hp.ns = std::atoi(v) == 3 ? 3 : 1;
         if (const char *v = std::getenv("P2P_NBUF")) hp.nbuf = std::atoi(v) == 2 ? 2 : 1;
@@ -657,6 +660,30 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             }
             hp.tiles.swap(t2);
             hp.tile_slot.swap(s2);
+        }
+    }
+    // ---- tail splitting (TILED): the last tiles of the queue are split into unit
+    // ranges so the final wave is fine-grained (each target is still computed
+    // whole by one thread: results do not depend on the split).
+    hp.tile_part.assign(hp.tiles.size(), 1 << 16);
+    if (d.layout == P2P_LAYOUT_TILED && !hp.ws) {
+        int64_t tail = 148 * 4, parts = 4;
+        if (const char *v = std::getenv("P2P_TAIL_TILES")) tail = std::atoll(v);
+        if (const char *v = std::getenv("P2P_TAIL_PARTS")) parts = std::max(1, std::min(16, std::atoi(v)));
+        tail = std::min<int64_t>(tail, (int64_t)hp.tiles.size() / 2);
+        if (parts > 1 && tail > 0) {
+            const size_t keep = hp.tiles.size() - (size_t)tail;
+            std::vector<int32_t> t2(hp.tiles.begin(), hp.tiles.begin() + keep),
+                s2(hp.tile_slot.begin(), hp.tile_slot.begin() + keep), p2(keep, 1 << 16);
+            for (size_t i = keep; i < hp.tiles.size(); ++i)
+                for (int64_t q = 0; q < parts; ++q) {
+                    t2.push_back(hp.tiles[i]);
+                    s2.push_back(hp.tile_slot[i]);
+                    p2.push_back((int32_t)(q | (parts << 16)));
+                }
+            hp.tiles.swap(t2);
+            hp.tile_slot.swap(s2);
+            hp.tile_part.swap(p2);
         }
     }
     hp.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

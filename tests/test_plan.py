@@ -159,7 +159,7 @@ def test_tiled_region_interaction_set():
         assert roff[-1] == len(ridx) and np.all(np.diff(roff) % 4 == 0)
         S = 1 << (level - 1)
         W_ = 1 << tile
-        for slot, t in enumerate(np.sort(tiles_launch)):  # slots are Morton tile order
+        for slot, t in enumerate(np.unique(tiles_launch)):  # slots are Morton tile order (tail tiles repeat)
             ent = ridx[roff[slot]:roff[slot + 1]]
             got = sperm[ent[ent >= 0]]
             assert len(set(got.tolist())) == len(got)
