@@ -205,47 +205,33 @@ def main():
     names = args.configs.split(",") if args.configs else WORKLOADS[args.workload]
 
     # ---- plans (host build + upload; not timed)
+    from paper_2403_01596_b200.dist import DistributedP2P
     jobs = []
     for name in names:
         cfg = W.CONFIGS[name]
         src, tgt, q = W.make_problem(cfg, kind=args.kind)
-        pl = p2p.Plan(src, tgt, level=cfg.level, layout=args.layout, precision=args.precision, device=local,
-                      part_world=world, part_rank=rank, tile_log2=args.tile)
-        info = pl.info
-        dt = pl.torch_dtype
-        job = {"name": name, "cfg": cfg, "plan": pl, "info": info, "q_user": q,
-               "out": torch.empty(max(1, info["n_tgt_local"]), dtype=dt, device=dev)}
+        kw = dict(level=cfg.level, layout=args.layout, precision=args.precision, tile_log2=args.tile)
         if world == 1:
-            job["q"] = torch.as_tensor(q[pl.export("src_perm")], dtype=dt, device=dev)
+            pl = p2p.Plan(src, tgt, device=local, **kw)
+            job = {"name": name, "cfg": cfg, "plan": pl, "info": pl.info, "q_user": q,
+                   "q": torch.as_tensor(q[pl.export("src_perm")], dtype=pl.torch_dtype, device=dev)}
         else:
-            part = pl.export("partition").reshape(2, world + 1)
-            owned_user = _owned_user_indices(pl, src, part, rank)
-            job["q_owned"] = torch.as_tensor(q[owned_user], dtype=dt, device=dev)
-            hc = pl.export("halo_counts").reshape(2, world)
-            job["recv_splits"], job["send_splits"] = hc[0].tolist(), hc[1].tolist()
-            job["send"] = torch.empty(max(1, info["n_send"]), dtype=dt, device=dev)
-            job["halo"] = torch.empty(max(1, info["n_halo"]), dtype=dt, device=dev)
+            dp = DistributedP2P(src, tgt, device=local, host_staged=shared, **kw)
+            pl = dp.plan
+            job = {"name": name, "cfg": cfg, "plan": pl, "dp": dp, "info": pl.info, "q_user": q,
+                   "q_owned": torch.as_tensor(q[_owned_user_indices(pl, src, dp.src_begin.reshape(1, -1), rank)],
+                                              dtype=pl.torch_dtype, device=dev)}
+        job["out"] = torch.empty(max(1, job["info"]["n_tgt_local"]), dtype=pl.torch_dtype, device=dev)
         jobs.append(job)
     pairs_step = sum(j["info"]["pairs_global"] for j in jobs)
     pairs_local = sum(j["info"]["pairs"] for j in jobs)
 
     def one_apply(j):
-        pl = j["plan"]
         if world == 1:
-            p2p.p2p_apply(pl.handle, j["q"].data_ptr(), j["out"].data_ptr(), p2p.P2P_ORDER_PLAN, 0,
+            p2p.p2p_apply(j["plan"].handle, j["q"].data_ptr(), j["out"].data_ptr(), p2p.P2P_ORDER_PLAN, 0,
                           stream.cuda_stream)
-        else:
-            if j["info"]["n_send"]:
-                pl.halo_pack(j["q_owned"], j["send"], stream.cuda_stream)
-            if shared:  # host-staged exchange (test mode)
-                recv = torch.empty(j["info"]["n_halo"], dtype=j["halo"].dtype)
-                dist.all_to_all_single(recv, j["send"][: j["info"]["n_send"]].cpu(), j["recv_splits"],
-                                       j["send_splits"])
-                j["halo"][: j["info"]["n_halo"]].copy_(recv)
-            else:
-                dist.all_to_all_single(j["halo"][: j["info"]["n_halo"]], j["send"][: j["info"]["n_send"]],
-                                       j["recv_splits"], j["send_splits"])
-            pl.apply_dist(j["q_owned"], j["halo"], j["out"], stream=stream.cuda_stream)
+        else:  # halo weight exchange (NCCL all-to-all) + distributed apply
+            j["dp"].apply(j["q_owned"], j["out"], stream=stream.cuda_stream)
 
     def step():
         for j in jobs:

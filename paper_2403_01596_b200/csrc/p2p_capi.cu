@@ -90,26 +90,27 @@ template <>
 const p2p::Layout<double> &layout_of<double>(const p2p::HostPlan &hp) { return hp.f64; }
 
 // TILED kernel instance for the plan's options (element type, targets per unit, CTA size, padding).
-template <typename T, int TPI, bool PAD>
+template <typename T, int TPI, bool PAD, int NS>
 const void *tiled_fn_nt(int nt) {
     using namespace p2p::dev;
     switch (nt) {
-    case 32: return (const void *)p2p_tiled_kernel<T, TPI, 32, PAD>;
-    case 64: return (const void *)p2p_tiled_kernel<T, TPI, 64, PAD>;
-    case 128: return (const void *)p2p_tiled_kernel<T, TPI, 128, PAD>;
-    default: return (const void *)p2p_tiled_kernel<T, TPI, 256, PAD>;
+    case 64: return (const void *)p2p_tiled_kernel<T, TPI, 64, PAD, NS>;
+    case 128: return (const void *)p2p_tiled_kernel<T, TPI, 128, PAD, NS>;
+    default: return (const void *)p2p_tiled_kernel<T, TPI, 256, PAD, NS>;
     }
 }
 
-// TILED kernel instance for the plan's options (element type, targets per unit, CTA size, padding).
+// TILED kernel instance for the plan's options (element type, targets per unit, CTA size, padding,
+// items per unit).  Instances: dense fp32 (2 targets/unit, padded, 3 row items), sparse fp32
+// (1 target/unit, unpadded or padded, whole-unit items), fp64 (unpadded, whole-unit items).
 template <typename T>
-const void *tiled_fn(int tpi, int nt, bool pad) {
+const void *tiled_fn(int tpi, int nt, bool pad, int ns) {
     if constexpr (sizeof(T) == 4) {
-        if (tpi == 4) return tiled_fn_nt<float, 4, true>(nt);
-        if (tpi == 2) return tiled_fn_nt<float, 2, true>(nt);
-        return pad ? tiled_fn_nt<float, 1, true>(nt) : tiled_fn_nt<float, 1, false>(nt);
+        if (tpi == 2) return ns == 3 ? tiled_fn_nt<float, 2, true, 3>(nt) : tiled_fn_nt<float, 2, true, 1>(nt);
+        if (pad) return ns == 3 ? tiled_fn_nt<float, 1, true, 3>(nt) : tiled_fn_nt<float, 1, true, 1>(nt);
+        return ns == 3 ? tiled_fn_nt<float, 1, false, 3>(nt) : tiled_fn_nt<float, 1, false, 1>(nt);
     } else {
-        return tiled_fn_nt<double, 1, false>(nt);
+        return ns == 3 ? tiled_fn_nt<double, 1, false, 3>(nt) : tiled_fn_nt<double, 1, false, 1>(nt);
     }
 }
 
@@ -170,7 +171,7 @@ void upload_plan(p2p_plan_s &P) {
     const bool two = hp.tpi == 2;
     const void *kfn = hp.layout == P2P_LAYOUT_REDUNDANT ? (const void *)p2p::dev::p2p_r_kernel<T>
                       : hp.layout == P2P_LAYOUT_TILED
-                          ? (hp.ws ? tiled_ws_fn<T>(hp.tpi, hp.ncw, hp.pad) : tiled_fn<T>(hp.tpi, hp.nt, hp.pad))
+                          ? (hp.ws ? tiled_ws_fn<T>(hp.tpi, hp.ncw, hp.pad) : tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns))
                           : (two ? (const void *)p2p::dev::p2p_nr_kernel<T, sizeof(T) == 4 ? 2 : 1>
                                  : (const void *)p2p::dev::p2p_nr_kernel<T, 1>);
     ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2p::kSmemLimit), "smem attr");
@@ -245,7 +246,7 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
                                 args, (size_t)hp.smem_bytes, s),
                "tiled-ws launch");
         else
-            ck(cudaLaunchKernel(tiled_fn<T>(hp.tpi, hp.nt, hp.pad), dim3(P.grid), dim3(hp.nt), args,
+            ck(cudaLaunchKernel(tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns), dim3(P.grid), dim3(hp.nt), args,
                                 (size_t)hp.smem_bytes, s),
                "tiled launch");
     } else {

@@ -96,12 +96,14 @@ P2P_HD inline TCarve tiled_carve(int k, int src_cap, int tgt_cap, int e, int tpi
     c.bufsz = align16(c.tbl + 2 * tgt_cap);
     c.buf0 = 0;
     c.q = nbuf * c.bufsz;
+    // unit tables only for TPI > 1 (TPI = 1: unit = target), partials only for NS = 3
+    const int uc = tpi > 1 ? c.ucap : 0, tc = tpi > 1 ? tgt_cap : 0;
     c.pstart = align16(c.q + e * src_cap);
-    c.uj0 = c.pstart + 4 * (WW + 1);
-    c.ut = c.uj0 + 4 * c.ucap;
-    c.tslot = c.ut + 4 * tpi * c.ucap;
-    c.part = align16(c.tslot + 4 * tgt_cap);
-    c.bar = align16(c.part + (ns == 1 ? 1 : 3) * e * tpi * c.ucap);
+    c.uj0 = c.pstart + 4 * (tpi > 1 ? WW + 1 : 0);
+    c.ut = c.uj0 + 4 * uc;
+    c.tslot = c.ut + 4 * tpi * uc;
+    c.part = align16(c.tslot + 4 * tc);
+    c.bar = align16(c.part + (ns == 1 ? 0 : 3) * e * tpi * c.ucap);
     c.total = c.bar + 16;
     return c;
 }
@@ -216,7 +218,7 @@ struct HostPlan {
     std::vector<uint32_t> reg_off;                // [tiles+1] packed-region offsets
     std::vector<int32_t> reg_idx;                 // local source index, -1 = pad
     std::vector<uint16_t> reg_table;              // [tiles][tstride] region box starts, then target box starts
-    std::vector<uint16_t> tgt_bl;                 // per-tile packed targets: tile-local Morton box index
+    std::vector<uint16_t> tgt_bl;                 // per-tile packed targets: row-run base j0 = by * R + bx
     std::vector<uint32_t> tgt_pack_off;           // [tiles+1] packed-target offsets (multiples of 8)
     std::vector<int32_t> tile_tgt_base;           // [tiles] plan index of each tile's first target
     int ns = 3;                                   // TILED work segments per target

@@ -267,7 +267,8 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         hp.pad = d.layout == P2P_LAYOUT_TILED ? (hp.tpi == 2) : true;
         hp.ns = hp.tpi > 1 ? 3 : 1;
         hp.nbuf = 1;
-        hp.nt = d.layout == P2P_LAYOUT_TILED ? 128 : kThreads;
+        // measured best (tools/gpu_ab*.sh): 128 threads for dense units, 64 for sparse targets
+        hp.nt = d.layout == P2P_LAYOUT_TILED ? (hp.tpi > 1 ? 128 : 64) : kThreads;
         // tuning hooks (experiments only): P2P_TPI, P2P_NS, P2P_NBUF, P2P_PAD, P2P_NT
         if (const char *v = std::getenv("P2P_TPI"))
             if (d.precision == P2P_FP32 && d.layout != P2P_LAYOUT_REDUNDANT) {
@@ -283,7 +284,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         if (const char *v = std::getenv("P2P_NT"))
             if (d.layout == P2P_LAYOUT_TILED) {
                 const int x = std::atoi(v);
-                hp.nt = x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : 256;
+                hp.nt = x <= 64 ? 64 : x <= 128 ? 128 : 256;
             }
         hp.ws = false;  // the warp-specialised variant measured slower; kept for experiments
         if (const char *v = std::getenv("P2P_WS")) hp.ws = std::atoi(v) != 0;
@@ -625,7 +626,9 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                     const int64_t b = (int64_t)t * WW + bl;
                     for (int32_t g = hp.tgt_off[b]; g < hp.tgt_off[b + 1]; ++g) {
                         const int64_t u = hp.tgt_uidx[g], j = hp.tgt_pack_off[i] + (g - g0);
-                        hp.tgt_bl[j] = (uint16_t)bl;
+                        uint32_t bx, by;  // tile-local box -> row-run base j0 = by * R + bx in the region
+                        morton_decode((uint32_t)bl, bx, by);
+                        hp.tgt_bl[j] = (uint16_t)(by * R + bx);
                         if (f32) {
                             hp.f32.tgt_ruv[2 * j] = (float)(txy[2 * u] - ox);
                             hp.f32.tgt_ruv[2 * j + 1] = (float)(txy[2 * u + 1] - oy);

@@ -1,0 +1,99 @@
+"""Multi-GPU P2P over Morton-range partitions.
+
+One process per GPU.  Every rank builds the plan for its partition from the
+global point set (deterministic synthetic generation makes that free), owns a
+contiguous Morton range of tiles -- its targets and the sources of its boxes
+-- and receives, per apply, the weights of the halo sources it needs from the
+other ranks.  The exchange is the caller's collective over a torch
+ProcessGroup (NCCL over NVLink/NVSwitch on a B200 node); packing the send
+buffer and assembling [owned | halo] weights run in the library's kernels.
+
+    dp = DistributedP2P(src, tgt, level=12, group=None)   # default process group
+    phi_local = dp.apply(q_owned)          # this rank's targets, plan order
+    phi_all = dp.gather(phi_local)         # allgatherv -> global plan order (every rank)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import p2p
+
+
+class DistributedP2P:
+    def __init__(self, src_xy, tgt_xy, *, group=None, device: int | None = None, host_staged: bool = False,
+                 **plan_kwargs):
+        import torch
+        import torch.distributed as dist
+        self.dist, self.torch = dist, torch
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = torch.cuda.current_device() if device is None else device
+        self.host_staged = host_staged  # gloo / test mode: exchange through host tensors
+        self.plan = p2p.Plan(src_xy, tgt_xy, device=self.device, part_world=self.world, part_rank=self.rank,
+                             **plan_kwargs)
+        info = self.plan.info
+        self.info = info
+        part = self.plan.export("partition").reshape(2, self.world + 1)
+        self.src_begin, self.tgt_begin = part[0], part[1]
+        hc = self.plan.export("halo_counts").reshape(2, self.world)
+        self.recv_splits, self.send_splits = hc[0].tolist(), hc[1].tolist()
+        dt = self.plan.torch_dtype
+        dev = torch.device("cuda", self.device)
+        self._send = torch.empty(max(1, info["n_send"]), dtype=dt, device=dev)
+        self._halo = torch.empty(max(1, info["n_halo"]), dtype=dt, device=dev)
+
+    @property
+    def n_src_owned(self) -> int:
+        return int(self.info["n_src_owned"])
+
+    @property
+    def n_tgt_local(self) -> int:
+        return int(self.info["n_tgt_local"])
+
+    def owned_source_range(self) -> tuple[int, int]:
+        """Global plan-order range of the sources this rank owns."""
+        return int(self.src_begin[self.rank]), int(self.src_begin[self.rank + 1])
+
+    def exchange(self, q_owned, stream=None):
+        """Halo weight exchange (a6): pack what the peers need, all-to-all, return the halo buffer."""
+        info = self.info
+        n_send, n_halo = int(info["n_send"]), int(info["n_halo"])
+        if n_send:
+            self.plan.halo_pack(q_owned, self._send, stream)
+        send, halo = self._send[:n_send], self._halo[:n_halo]
+        if self.host_staged:
+            recv = self.torch.empty(n_halo, dtype=halo.dtype)
+            self.dist.all_to_all_single(recv, send.cpu(), self.recv_splits, self.send_splits, group=self.group)
+            halo.copy_(recv)
+        else:
+            self.dist.all_to_all_single(halo, send, self.recv_splits, self.send_splits, group=self.group)
+        return self._halo
+
+    def apply(self, q_owned, out=None, *, accumulate: bool = False, stream=None):
+        """phi for this rank's targets (plan order) from its owned weights (plan order)."""
+        torch = self.torch
+        if out is None:
+            out = torch.empty(max(1, self.n_tgt_local), dtype=self.plan.torch_dtype,
+                              device=torch.device("cuda", self.device))
+        halo = self.exchange(q_owned, stream)
+        self.plan.apply_dist(q_owned, halo, out, accumulate=accumulate, stream=stream)
+        return out
+
+    def gather(self, phi_local):
+        """allgatherv (a11): every rank receives phi for all targets in global plan order."""
+        torch = self.torch
+        counts = np.diff(self.tgt_begin).astype(np.int64)
+        cmax = int(counts.max()) if len(counts) else 0
+        pad = torch.zeros(max(1, cmax), dtype=phi_local.dtype, device=phi_local.device)
+        pad[: self.n_tgt_local].copy_(phi_local[: self.n_tgt_local])
+        if self.host_staged:
+            parts = [torch.empty_like(pad, device="cpu") for _ in range(self.world)]
+            self.dist.all_gather(parts, pad.cpu(), group=self.group)
+        else:
+            parts = [torch.empty_like(pad) for _ in range(self.world)]
+            self.dist.all_gather(parts, pad, group=self.group)
+        return torch.cat([p[: int(c)].to(phi_local.device) for p, c in zip(parts, counts)])
+
+    def close(self):
+        self.plan.close()
