@@ -117,6 +117,17 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def _hbm_peak():
+    """HBM peak for the roofline: MEASURED_PEAKS.json (driver-written copy bandwidth), else the
+    B200_PROFILING.md fallback."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            v = float(json.load(f)["hbm_gbs"])
+        return v, f"MEASURED_PEAKS.json hbm_gbs ({v:.0f} GB/s, copy read+write)"
+    except Exception:
+        return 7000.0, "fallback 7.0 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
 # ---------------------------------------------------------------- CPU baseline (oracle)
 def cpu_baseline(cfg_names, kind, budget_s, seed_stream=0):
     """The fp64 oracle as it stands (never tuned), on a bounded, seeded sample of
@@ -274,28 +285,42 @@ def main():
     ms_per_step = total_ms / args.steps
     value = pairs_step / (ms_per_step * 1e-3)
 
-    # ---- roofline of the dominant kernel (the P2P kernel; SFU/MUFU-bound for dense boxes)
+    # ---- roofline of the dominant kernel (the P2P kernel).  Per config the floor is
+    # max(pairs / MUFU peak, algorithmic bytes / HBM peak); the workload is
+    # "alu"-bound (MUFU.LG2) when the MUFU floors dominate the sum, else "hbm"-bound.
     clocks = sampler.summary()
     peak_clk = (clocks["sm_max_mhz"] or 1965) * 1e6
-    peak = MUFU_LG2_PER_CLK_PER_SM * SM_COUNT * peak_clk / 1e9  # Gpair/s
+    peak_mufu = MUFU_LG2_PER_CLK_PER_SM * SM_COUNT * peak_clk / 1e9  # Gpair/s
+    peak_hbm, hbm_basis = _hbm_peak()
     kernel_ms = float(kern_ms.sum(axis=0).sum() / args.steps)
-    achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
+    alg_bytes = sum(j["info"]["alg_bytes_kernel"] for j in jobs)
+    t_mufu = sum(j["info"]["pairs"] / (peak_mufu * 1e9) for j in jobs)
+    t_hbm = sum(j["info"]["alg_bytes_kernel"] / (peak_hbm * 1e9) for j in jobs)
     traffic = _ncu_traffic(args, names)
-    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gpair/s (1 MUFU.LG2 per pair)",
-                "frac": achieved / peak, "traffic": traffic,
-                "peak_basis": f"{MUFU_LG2_PER_CLK_PER_SM} MUFU.LG2/clk/SM x {SM_COUNT} SMs x "
-                              f"{peak_clk / 1e6:.0f} MHz (sm_max); DESIGN.md §5",
-                "kernel_ms_per_step": kernel_ms,
-                "alg_bytes_per_step": sum(j["info"]["alg_bytes_kernel"] for j in jobs),
-                "hbm_gbs_alg": sum(j["info"]["alg_bytes_kernel"] for j in jobs) / (kernel_ms * 1e-3) / 1e9}
+    if t_mufu >= t_hbm:
+        achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak_mufu, "unit": "Gpair/s (1 MUFU.LG2 per pair)",
+                    "frac": achieved / peak_mufu, "traffic": traffic,
+                    "peak_basis": f"{MUFU_LG2_PER_CLK_PER_SM} MUFU.LG2/clk/SM x {SM_COUNT} SMs x "
+                                  f"{peak_clk / 1e6:.0f} MHz (sm_max); DESIGN.md §5"}
+    else:
+        achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s (algorithmic bytes)",
+                    "frac": achieved / peak_hbm, "traffic": traffic, "peak_basis": hbm_basis}
+    roofline.update({"kernel_ms_per_step": kernel_ms, "alg_bytes_per_step": alg_bytes,
+                     "hbm_gbs_alg": alg_bytes / (kernel_ms * 1e-3) / 1e9,
+                     "mufu_frac": pairs_local / (kernel_ms * 1e-3) / 1e9 / peak_mufu,
+                     "floor_frac": max(t_mufu, t_hbm) / (kernel_ms * 1e-3)})
     per_cfg = []
     for i, j in enumerate(jobs):
         kms = float(np.mean(kern_ms[:, i]))
         gp = j["info"]["pairs"] / (kms * 1e-3) / 1e9
+        ab = j["info"]["alg_bytes_kernel"] / (kms * 1e-3) / 1e9
         per_cfg.append({"config": j["name"], "pairs": j["info"]["pairs"], "ms": kms, "Gpair_s": gp,
-                        "frac_mufu": gp / peak, "tile_log2": j["info"]["tile_log2"],
-                        "alg_GBs": j["info"]["alg_bytes_kernel"] / (kms * 1e-3) / 1e9,
-                        "D_occ": j["info"]["density_occupied"], "t_max": j["info"]["t_max"]})
+                        "frac_mufu": gp / peak_mufu, "alg_GBs": ab, "frac_hbm": ab / peak_hbm,
+                        "layout_GBs": j["info"]["layout_bytes_apply"] / (kms * 1e-3) / 1e9,
+                        "tile_log2": j["info"]["tile_log2"], "D_occ": j["info"]["density_occupied"],
+                        "t_max": j["info"]["t_max"]})
 
     # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier)
@@ -426,7 +451,8 @@ def _extras(args, names, stream, dev):
                     info = pl.info
                     res.append({"config": name, "layout": layout, "precision": prec, "ms": ms,
                                 "Gpair_s": info["pairs"] / (ms * 1e-3) / 1e9,
-                                "alg_GBs_apply": info["alg_bytes_apply"] / (ms * 1e-3) / 1e9,
+                                "alg_GBs": info["alg_bytes_kernel"] / (ms * 1e-3) / 1e9,
+                                "layout_GBs": info["layout_bytes_apply"] / (ms * 1e-3) / 1e9,
                                 "plan_build_s": info["build_seconds"], "upload_s": info["upload_seconds"],
                                 "device_MB": info["device_bytes"] / 1e6, "halo_entries": info["halo_entries"]})
     return res

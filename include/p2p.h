@@ -180,8 +180,13 @@ typedef struct {
     int64_t tiles;               /* CTAs per apply (non-empty tiles of this partition) */
     int64_t smem_bytes;          /* dynamic shared memory per CTA */
     int64_t halo_entries;        /* R layout: packed halo entries (incl. padding) */
-    int64_t alg_bytes_kernel;    /* algorithmic HBM bytes of the P2P kernel per apply */
-    int64_t alg_bytes_apply;     /* algorithmic HBM bytes of the whole apply (incl. R pack) */
+    int64_t alg_bytes_kernel;    /* algorithmic HBM bytes per apply, independent of the layout:
+                                    each target's coordinates read + potential written, each source's
+                                    coordinates + weight read once, 8 B of CSR offsets per box of the
+                                    launched tiles */
+    int64_t layout_bytes_apply;  /* bytes the plan's layout moves per apply (model): NR = alg;
+                                    R = packed halo + pack_r; TILED = packed regions (+ring
+                                    redundancy), index, tables, packed targets, weight gather */
     int64_t device_bytes;        /* device memory held by the plan */
     double build_seconds;        /* host plan build */
     double upload_seconds;       /* host -> device upload */

@@ -44,7 +44,7 @@ struct p2p_plan_s {
     // device arrays
     DevBuf tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
-    DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_ruv, tgt_pack_off, tile_tgt_base;
+    DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_oix, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     int grid = 0;                                // persistent CTAs per launch
     unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
@@ -69,7 +69,7 @@ struct p2p_plan_s {
     void release() {
         DevBuf *all[] = {&tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
-                         &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_ruv,
+                         &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi,
                          &io_q, &io_out, &queue};
         for (DevBuf *b : all) {
@@ -157,6 +157,7 @@ void upload_plan(p2p_plan_s &P) {
         P.upload(P.reg_uv, lay.reg_uv);
         P.upload(P.reg_table, hp.reg_table);
         P.upload(P.tgt_bl, hp.tgt_bl);
+        P.upload(P.tgt_oix, hp.tgt_oix);
         P.upload(P.tgt_ruv, lay.tgt_ruv);
         P.upload(P.tgt_pack_off, hp.tgt_pack_off);
         P.upload(P.tile_tgt_base, hp.tile_tgt_base);
@@ -235,10 +236,12 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.reg_uv = (const T *)P.reg_uv.p;
         a.reg_table = (const uint16_t *)P.reg_table.p;
         a.tgt_bl = (const uint16_t *)P.tgt_bl.p;
+        a.tgt_oix = (const uint16_t *)P.tgt_oix.p;
         a.tgt_ruv = (const T *)P.tgt_ruv.p;
         a.tgt_pack_off = (const uint32_t *)P.tgt_pack_off.p;
         a.tile_tgt_base = (const int32_t *)P.tile_tgt_base.p;
         a.ns = hp.ns;
+        a.flat = hp.flat ? 1 : 0;
         a.nbuf = hp.nbuf;
         void *args[] = {&a};
         if (hp.ws)
@@ -508,19 +511,19 @@ p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *info) {
     info->smem_bytes = hp.smem_bytes;
     info->halo_entries = hp.halo_entries;
     const int64_t e = hp.precision == P2P_FP32 ? 4 : 8;
-    const int64_t offs = 8 * hp.boxes_in_tiles;  // tgt + src (or halo) CSR offsets of the tiles' boxes
+    const int64_t offs = 8 * hp.boxes_in_tiles;  // tgt + src CSR offsets of the tiles' boxes
+    info->alg_bytes_kernel = hp.n_tgt_local * 3 * e + hp.n_src_local * 3 * e + offs;
     if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
-        info->alg_bytes_kernel = hp.n_tgt_local * 3 * e + hp.n_src_local * 3 * e + offs;
-        info->alg_bytes_apply = info->alg_bytes_kernel;
+        info->layout_bytes_apply = info->alg_bytes_kernel;
     } else if (hp.layout == P2P_LAYOUT_TILED) {
-        // targets: region-relative coords + box byte pair + out + CSR offset; region: coords + index;
-        // tables; weights gathered once from plan order
-        info->alg_bytes_kernel = hp.n_tgt_local * (3 * e + 2) + hp.reg_entries * (2 * e + 4) +
-                                 (int64_t)hp.reg_table.size() * 2 + hp.n_src_local * e;
-        info->alg_bytes_apply = info->alg_bytes_kernel;
+        // targets: region-relative coords + row-run base (+ output index) + out; region: coords +
+        // index; tables; weights gathered once from plan order
+        info->layout_bytes_apply = hp.n_tgt_local * (3 * e + 2 + (hp.lean ? 2 : 0)) +
+                                   hp.reg_entries * (2 * e + 4) + (int64_t)hp.reg_table.size() * 2 +
+                                   hp.n_src_local * e;
     } else {
-        info->alg_bytes_kernel = hp.n_tgt_local * 3 * e + hp.halo_entries * 3 * e + offs;
-        info->alg_bytes_apply = info->alg_bytes_kernel + hp.halo_entries * (4 + e) + hp.n_src_local * e;
+        info->layout_bytes_apply = hp.n_tgt_local * 3 * e + hp.halo_entries * 3 * e + offs +
+                                   hp.halo_entries * (4 + e) + hp.n_src_local * e;
     }
     info->device_bytes = P->device_bytes;
     info->build_seconds = hp.build_seconds;

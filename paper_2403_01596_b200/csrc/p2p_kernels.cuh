@@ -175,6 +175,43 @@ __device__ __forceinline__ double span1_f64(const double2 *__restrict__ UV, cons
     return acc;
 }
 
+// The three row-runs [s_r, e_r) of a target as ONE index sequence v = s0 .. s0+n-1
+// mapped to j = v + (v >= b1 ? d1 : 0) + (v >= b2 ? d2 : 0): lanes whose targets
+// have equal totals (tsort plans) stay converged across row boundaries.  One
+// accumulator, sources in row order (a fixed order per target).
+struct Runs3 {
+    int v0, n, b1, d1, b2, d2;
+    __device__ __forceinline__ Runs3(int s0, int e0, int s1, int e1, int s2, int e2)
+        : v0(s0), n((e0 - s0) + (e1 - s1) + (e2 - s2)), b1(e0), d1(s1 - e0), b2(e0 + (e1 - s1)), d2(s2 - e1) {}
+    __device__ __forceinline__ int at(int v) const { return v + (v >= b1 ? d1 : 0) + (v >= b2 ? d2 : 0); }
+};
+__device__ __forceinline__ float span3_f32(const float2 *__restrict__ UV, const float *__restrict__ Q, const Runs3 &r,
+                                           float ut, float vt) {
+    float acc = 0.f;
+    const int v1 = r.v0 + r.n;
+#pragma unroll 2
+    for (int v = r.v0; v < v1; ++v) {
+        const int j = r.at(v);
+        const float2 s = UV[j];
+        const float du = ut - s.x, dv = vt - s.y;
+        acc = fmaf(Q[j], lg2_approx(fmaf(dv, dv, du * du)), acc);
+    }
+    return acc;
+}
+__device__ __forceinline__ double span3_f64(const double2 *__restrict__ UV, const double *__restrict__ Q,
+                                            const Runs3 &r, double ut, double vt, double eps2) {
+    double acc = 0.0;
+    const int v1 = r.v0 + r.n;
+    for (int v = r.v0; v < v1; ++v) {
+        const int j = r.at(v);
+        const double2 s = UV[j];
+        const double du = ut - s.x, dv = vt - s.y;
+        const double r2 = fma(dv, dv, du * du);
+        if (r2 >= eps2) acc = fma(Q[j], log(r2), acc);
+    }
+    return acc;
+}
+
 // Four targets sharing one span x two sources per step: 8 pairs per LDS.128 + LDS.64.
 __device__ __forceinline__ void span4_f32(const float4 *__restrict__ A, const float2 *__restrict__ Q, int p0,
                                           int p1, const float *ut, const float *vt, float *r) {
@@ -264,10 +301,12 @@ struct P2PArgs {
     const T *reg_uv;            // TILED: region-relative coordinates (fp32: (u0,u1,v0,v1) per pair)
     const uint16_t *reg_table;  // TILED: [slots][tstride] region box starts, then target box starts
     const uint16_t *tgt_bl;     // TILED: packed targets' row-run base j0 = by*R + bx in the region
+    const uint16_t *tgt_oix;    // TILED lean path: packed target -> tile-local output index (tsort plans)
     const T *tgt_ruv;           // TILED: packed targets' coordinates relative to the region origin
     const uint32_t *tgt_pack_off;   // TILED: [slots+1] packed-target offsets (multiples of 8)
     const int32_t *tile_tgt_base;   // TILED: plan index of each tile's first target
     int ns;                     // TILED: work items per target (1 = whole target, 3 = one per row-run)
+    int flat;                   // TILED lean path: sweep the three row-runs as one sequence
     int nbuf;                   // TILED: 2 = prefetch the next tile's record during this tile
     unsigned long long *trace;  // optional per-tile timeline (diagnostics; nullptr = off)
     T *out;
@@ -672,6 +711,8 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_next, s_units, s_base_next;
     constexpr int NS = NS_;  // work items per unit: 1 (whole unit) or 3 (one per row-run)
+    // lean sparse path (tsort plans): one thread per target, targets sorted by n9, flattened row-runs
+    constexpr bool LEAN = NS == 1 && TPI == 1 && !PAD;
     const int k = a.k, W = 1 << k, R = W + 2, RR = R * R, WW = W * W;
     const unsigned rinv = ((1u << 20) + (unsigned)R - 1) / (unsigned)R;
     const TCarve c = tiled_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI, NS, a.nbuf);
@@ -692,10 +733,11 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         const uint32_t tb = a.tgt_pack_off[slot], ntp = a.tgt_pack_off[slot + 1] - tb;
         const uint32_t b_tab = (uint32_t)c.tstride * 2u, b_uv = nent * 2 * (uint32_t)sizeof(T), b_ix = nent * 4u;
         const uint32_t b_tuv = ntp * 2 * (uint32_t)sizeof(T), b_tbl = ntp * 2u;
+        const uint32_t b_oix = LEAN ? ntp * 2u : 0u;
         const uint32_t bar = smem_addr(mbar + b);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "r"(b_tab + b_uv + b_ix + b_tuv + b_tbl)
+                     "r"(b_tab + b_uv + b_ix + b_tuv + b_tbl + b_oix)
                      : "memory");
 #define P2P_BULK(dst, src, bytes)                                                                        \
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" \
@@ -709,6 +751,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         if (ntp) {
             P2P_BULK(buf + c.tuv, a.tgt_ruv + 2 * (size_t)tb, b_tuv);
             P2P_BULK(buf + c.tbl, a.tgt_bl + tb, b_tbl);
+            if (LEAN) P2P_BULK(buf + c.oix, a.tgt_oix + tb, b_oix);
         }
 #undef P2P_BULK
     };
@@ -741,6 +784,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         const int32_t *s_idx = reinterpret_cast<const int32_t *>(B + c.idx);
         const T *tuv = reinterpret_cast<const T *>(B + c.tuv);
         const uint16_t *tbl = reinterpret_cast<const uint16_t *>(B + c.tbl);
+        const uint16_t *oix = reinterpret_cast<const uint16_t *>(B + c.oix);
         if (tid == 0) {  // next tile; with two buffers its record streams in while this tile computes
             const int nx = atomicAdd(a.queue, 1);
             s_next = nx;
@@ -762,7 +806,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         }
         if (trc) trc[2] = gtimer();
         const int nent = (int)table[RR];
-        const int nt = (int)ttab[WW];
+        const int nt = TPI == 1 && NS == 1 ? (int)ttab[0] : (int)ttab[WW];  // short table: the target count
         if (TPI > 1 && wid == 0) {  // units of TPI targets of one box
             int carry = 0;
             for (int base = 0; base < WW; base += 32) {
@@ -793,7 +837,11 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         }
         const int nu = TPI > 1 ? s_units : nt;
         const int pinfo = a.tile_part[cur], npart = pinfo >> 16, ipart = pinfo & 0xffff;
-        const int ub = (int)(((long long)nu * ipart) / npart), ue = (int)(((long long)nu * (ipart + 1)) / npart);
+        int ub = 0, ue = nu;
+        if (npart > 1) {  // tail tile split into npart unit ranges (nu * npart < 2^31)
+            ub = (nu * ipart) / npart;
+            ue = (nu * (ipart + 1)) / npart;
+        }
         const int nr = ue - ub;
         if (trc) {
             trc[3] = gtimer();
@@ -846,8 +894,9 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                                    i1, tuv[2 * t0], tuv[2 * t0 + 1], a.eps2);
             }
         };
-        // final value of target t from its row-ordered sum (fp32: guarded redo if non-finite)
-        auto finish = [&](int t, T acc) {
+        // final value of target t (written to tile-local output o) from its row-ordered
+        // sum (fp32: guarded redo if non-finite)
+        auto finish = [&](int t, int o, T acc) {
             if constexpr (sizeof(T) == 4) {
                 if (!isfinite(acc)) {
                     const int jb = tbl[t];
@@ -868,10 +917,39 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             } else {
                 acc = -0.5 * acc;
             }
-            a.out[tb + t] = a.accumulate ? a.out[tb + t] + acc : acc;
+            a.out[tb + o] = a.accumulate ? a.out[tb + o] + acc : acc;
         };
 
-        if constexpr (NS == 1 && TPI == 1) {  // lean path: one thread per target, its three row-runs in order
+        if constexpr (LEAN) {  // one thread per target (sorted by n9), its three row-runs as one sequence
+            for (int t = ub + tid; t < ue; t += NT) {
+                const int jb = tbl[t];
+                const T ux = tuv[2 * t], uy = tuv[2 * t + 1];
+                T acc = (T)0;
+                if (a.flat) {
+                    const Runs3 runs(table[jb], table[jb + 3], table[jb + R], table[jb + R + 3], table[jb + 2 * R],
+                                     table[jb + 2 * R + 3]);
+                    if constexpr (sizeof(T) == 4)
+                        acc = span3_f32(reinterpret_cast<const float2 *>(s_uv), reinterpret_cast<const float *>(s_q),
+                                        runs, ux, uy);
+                    else
+                        acc = span3_f64(reinterpret_cast<const double2 *>(s_uv),
+                                        reinterpret_cast<const double *>(s_q), runs, ux, uy, a.eps2);
+                } else {
+#pragma unroll
+                    for (int row = 0; row < 3; ++row) {
+                        const int j0 = jb + row * R;
+                        if constexpr (sizeof(T) == 4)
+                            acc += span1_f32(reinterpret_cast<const float2 *>(s_uv),
+                                             reinterpret_cast<const float *>(s_q), table[j0], table[j0 + 3], ux, uy);
+                        else
+                            acc += span1_f64(reinterpret_cast<const double2 *>(s_uv),
+                                             reinterpret_cast<const double *>(s_q), table[j0], table[j0 + 3], ux, uy,
+                                             a.eps2);
+                    }
+                }
+                finish(t, oix[t], acc);
+            }
+        } else if constexpr (NS == 1 && TPI == 1) {  // padded rows, one thread per target
             for (int t = ub + tid; t < ue; t += NT) {
                 const int jb = tbl[t];
                 const T ux = tuv[2 * t], uy = tuv[2 * t + 1];
@@ -879,18 +957,10 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
 #pragma unroll
                 for (int row = 0; row < 3; ++row) {
                     const int j0 = jb + row * R;
-                    const int i0 = table[j0], i1 = table[j0 + 3];
-                    if constexpr (PAD)
-                        acc += span_f32(reinterpret_cast<const float4 *>(s_uv), reinterpret_cast<const float2 *>(s_q),
-                                        i0 >> 1, i1 >> 1, ux, uy);
-                    else if constexpr (sizeof(T) == 4)
-                        acc += span1_f32(reinterpret_cast<const float2 *>(s_uv), reinterpret_cast<const float *>(s_q),
-                                         i0, i1, ux, uy);
-                    else
-                        acc += span1_f64(reinterpret_cast<const double2 *>(s_uv),
-                                         reinterpret_cast<const double *>(s_q), i0, i1, ux, uy, a.eps2);
+                    acc += span_f32(reinterpret_cast<const float4 *>(s_uv), reinterpret_cast<const float2 *>(s_q),
+                                    table[j0] >> 1, table[j0 + 3] >> 1, ux, uy);
                 }
-                finish(t, acc);
+                finish(t, t, acc);
             }
         } else if constexpr (NS == 1) {  // one item per unit, rows in order
             for (int u = ub + tid; u < ue; u += NT) {
@@ -907,10 +977,10 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                     for (int x = 0; x < TPI; ++x) {
                         const int t = ut[TPI * u + x];
                         if (x > 0 && t == ut[TPI * u + x - 1]) break;  // duplicates fill the box's last unit
-                        finish(t, acc[x]);
+                        finish(t, t, acc[x]);
                     }
                 } else {
-                    finish(u, acc[0]);
+                    finish(u, u, acc[0]);
                 }
             }
         } else {  // (unit, row) items, then the fixed-order reduction of the three partials
@@ -930,7 +1000,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                     const int t = TPI > 1 ? ut[TPI * u + x] : u;
                     if (x > 0 && t == ut[TPI * u + x - 1]) break;  // duplicates fill the box's last unit
                     const int sl = TPI * u + x;
-                    finish(t, part[sl] + part[rs + sl] + part[2 * rs + sl]);
+                    finish(t, t, part[sl] + part[rs + sl] + part[2 * rs + sl]);
                 }
             }
         }

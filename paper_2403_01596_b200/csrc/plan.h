@@ -73,27 +73,30 @@ P2P_HD inline RCarve r_carve(int k, int src_cap, int tgt_cap, int e) {
 
 struct TCarve {
     int buf0, bufsz;                      // double-buffered, bulk-copied part: 2 x bufsz bytes from buf0
-    int table, uv, idx, tuv, tbl;         // offsets inside one buffer
+    int table, uv, idx, tuv, tbl, oix;    // offsets inside one buffer
     int q, pstart, uj0, ut, tslot, part, bar, total, ucap, tstride;
 };
 // TILED layout.  src_cap: max packed-region entries of a tile (multiple of 4);
 // tgt_cap: max packed targets of a tile (multiple of 8); tpi: targets per
 // unit; ns: work segments per target (3 row-runs, or 6 half row-runs).
-P2P_HD inline int tiled_table_stride(int k) {
+P2P_HD inline int tiled_table_stride(int k, bool lean) {
     const int W = 1 << k, R = W + 2;
-    return (R * R + 1 + W * W + 1 + 7) & ~7;  // uint16: region box starts, then target box starts
+    // uint16: region box starts, then target box starts (units of TPI > 1 / NS = 3 plans)
+    // or, for one-item-per-target plans, just the tile's target count
+    return lean ? (R * R + 2 + 7) & ~7 : (R * R + 1 + W * W + 1 + 7) & ~7;
 }
 P2P_HD inline TCarve tiled_carve(int k, int src_cap, int tgt_cap, int e, int tpi, int ns, int nbuf) {
     const int WW = 1 << (2 * k);
     TCarve c;
     c.ucap = nr_unit_cap(k, tgt_cap, tpi);
-    c.tstride = tiled_table_stride(k);
+    c.tstride = tiled_table_stride(k, tpi == 1 && ns == 1);
     c.table = 0;
     c.uv = align16(2 * c.tstride);
     c.idx = c.uv + 2 * e * src_cap;
     c.tuv = align16(c.idx + 4 * src_cap);
     c.tbl = c.tuv + 2 * e * tgt_cap;
-    c.bufsz = align16(c.tbl + 2 * tgt_cap);
+    c.oix = c.tbl + 2 * tgt_cap;
+    c.bufsz = align16(c.oix + (tpi == 1 && ns == 1 ? 2 * tgt_cap : 0));
     c.buf0 = 0;
     c.q = nbuf * c.bufsz;
     // unit tables only for TPI > 1 (TPI = 1: unit = target), partials only for NS = 3
@@ -118,7 +121,7 @@ struct WsCarve {
 P2P_HD inline WsCarve ws_carve(int k, int src_cap, int tgt_cap, int e, int tpi, int nslot) {
     WsCarve c;
     c.ucap = nr_unit_cap(k, tgt_cap, tpi);
-    c.tstride = tiled_table_stride(k);
+    c.tstride = tiled_table_stride(k, false);
     c.table = 0;
     c.uv = align16(2 * c.tstride);
     c.idx = c.uv + 2 * e * src_cap;
@@ -219,12 +222,16 @@ struct HostPlan {
     std::vector<int32_t> reg_idx;                 // local source index, -1 = pad
     std::vector<uint16_t> reg_table;              // [tiles][tstride] region box starts, then target box starts
     std::vector<uint16_t> tgt_bl;                 // per-tile packed targets: row-run base j0 = by * R + bx
+    std::vector<uint16_t> tgt_oix;                // lean: packed target -> tile-local output index
     std::vector<uint32_t> tgt_pack_off;           // [tiles+1] packed-target offsets (multiples of 8)
     std::vector<int32_t> tile_tgt_base;           // [tiles] plan index of each tile's first target
     int ns = 3;                                   // TILED work segments per target
     int nbuf = 1;                                 // TILED record buffers (2 = prefetch next tile)
     bool pad = true;                              // TILED: boxes padded to even counts (packed f32x2 loops)
     int nt = 256;                                 // threads per CTA (TILED: 128 or 256)
+    bool lean = false;                            // TILED lean kernel path (tpi 1, ns 1, unpadded): reads tgt_oix
+    bool tsort = false;                           // lean path: targets sorted by n9 within the tile
+    bool flat = false;                            // lean path: row-runs swept as one sequence (sparse)
     bool ws = true;                               // TILED: warp-specialised pipeline kernel
     int ncw = 8;                                  // TILED-WS consumer warps per CTA
     std::vector<int32_t> tile_slot;               // launch order -> slot

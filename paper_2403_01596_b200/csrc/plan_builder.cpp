@@ -267,8 +267,8 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         hp.pad = d.layout == P2P_LAYOUT_TILED ? (hp.tpi == 2) : true;
         hp.ns = hp.tpi > 1 ? 3 : 1;
         hp.nbuf = 1;
-        // measured best (tools/gpu_ab*.sh): 128 threads for dense units, 64 for sparse targets
-        hp.nt = d.layout == P2P_LAYOUT_TILED ? (hp.tpi > 1 ? 128 : 64) : kThreads;
+        // measured best (tools/gpu_ab*.sh): 128 threads for dense units and fp64, 64 for sparse fp32
+        hp.nt = d.layout == P2P_LAYOUT_TILED ? (hp.tpi > 1 || d.precision == P2P_FP64 ? 128 : 64) : kThreads;
         // tuning hooks (experiments only): P2P_TPI, P2P_NS, P2P_NBUF, P2P_PAD, P2P_NT
         if (const char *v = std::getenv("P2P_TPI"))
             if (d.precision == P2P_FP32 && d.layout != P2P_LAYOUT_REDUNDANT) {
@@ -294,6 +294,16 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             hp.nbuf = 2;
             if (const char *v = std::getenv("P2P_NBUF")) hp.nbuf = std::max(2, std::min(4, std::atoi(v)));
         }
+        // lean sparse path: targets of a tile sorted by neighbourhood size (n9), so the
+        // lanes of a warp sweep near-equal pair counts (P2P_TSORT=0 disables)
+        hp.lean = d.layout == P2P_LAYOUT_TILED && !hp.ws && hp.tpi == 1 && hp.ns == 1 && !hp.pad;
+        hp.tsort = hp.lean;
+        if (const char *v = std::getenv("P2P_TSORT")) hp.tsort = hp.lean && std::atoi(v) != 0;
+        // flattened row-runs pay below ~3 sources per box (more index work per pair,
+        // fewer idle lanes) and always in fp64 (the log dwarfs the index work); above,
+        // row loops (P2P_FLAT overrides)
+        hp.flat = hp.lean && (hp.density_occ < 3.0 || d.precision == P2P_FP64);
+        if (const char *v = std::getenv("P2P_FLAT")) hp.flat = hp.lean && std::atoi(v) != 0;
         if (d.layout == P2P_LAYOUT_TILED && !hp.pad) {  // unpadded region sizes
             int64_t mx = 0;
             for (int64_t i = 0; i < nt; ++i) {
@@ -539,7 +549,8 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     hp.tile_slot.resize((size_t)nlt);
     std::iota(hp.tile_slot.begin(), hp.tile_slot.end(), 0);
     if (d.layout == P2P_LAYOUT_TILED) {
-        const int ts = tiled_table_stride(k);
+        const bool short_table = !hp.ws && hp.tpi == 1 && hp.ns == 1;
+        const int ts = tiled_table_stride(k, short_table);
         hp.reg_off.assign((size_t)nlt + 1, 0);
         hp.reg_table.assign((size_t)nlt * ts, 0);
         for (int64_t i = 0; i < nlt; ++i) {  // sizes and tables
@@ -607,35 +618,52 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             if (n > 65535) fail(P2P_ERROR_NOT_SUPPORTED, "TILED tile exceeds 65535 targets; use NR");
             hp.tile_tgt_base[i] = hp.tgt_off[m0];
             hp.tgt_pack_off[i + 1] = hp.tgt_pack_off[i] + (uint32_t)pad8(n);
-            for (int64_t bl = 0; bl <= WW; ++bl)
-                hp.reg_table[i * ts + R * R + 1 + bl] = (uint16_t)(hp.tgt_off[m0 + bl] - hp.tgt_off[m0]);
+            if (short_table)
+                hp.reg_table[i * ts + R * R + 1] = (uint16_t)n;
+            else
+                for (int64_t bl = 0; bl <= WW; ++bl)
+                    hp.reg_table[i * ts + R * R + 1 + bl] = (uint16_t)(hp.tgt_off[m0 + bl] - hp.tgt_off[m0]);
         }
         const int64_t np = hp.tgt_pack_off[nlt];
         hp.tgt_bl.assign((size_t)np, 0);
+        if (hp.lean) hp.tgt_oix.assign((size_t)np, 0);
         if (f32) hp.f32.tgt_ruv.assign((size_t)np * 2, 0.f);
         else hp.f64.tgt_ruv.assign((size_t)np * 2, 0.0);
         const double *txy = d.tgt_xy;
         parallel_for(nlt, [&](int64_t a, int64_t bnd) {
+            std::vector<int32_t> order, key;
             for (int64_t i = a; i < bnd; ++i) {
                 const uint32_t t = (uint32_t)hp.tiles[i];
                 uint32_t tx, ty;
                 morton_decode(t, tx, ty);
                 const double ox = ((int64_t)tx * W - 1) * hp.h, oy = ((int64_t)ty * W - 1) * hp.h;
-                const int64_t g0 = hp.tgt_off[(int64_t)t * WW];
-                for (int64_t bl = 0; bl < WW; ++bl) {
-                    const int64_t b = (int64_t)t * WW + bl;
-                    for (int32_t g = hp.tgt_off[b]; g < hp.tgt_off[b + 1]; ++g) {
-                        const int64_t u = hp.tgt_uidx[g], j = hp.tgt_pack_off[i] + (g - g0);
-                        uint32_t bx, by;  // tile-local box -> row-run base j0 = by * R + bx in the region
-                        morton_decode((uint32_t)bl, bx, by);
-                        hp.tgt_bl[j] = (uint16_t)(by * R + bx);
-                        if (f32) {
-                            hp.f32.tgt_ruv[2 * j] = (float)(txy[2 * u] - ox);
-                            hp.f32.tgt_ruv[2 * j + 1] = (float)(txy[2 * u + 1] - oy);
-                        } else {
-                            hp.f64.tgt_ruv[2 * j] = txy[2 * u] - ox;
-                            hp.f64.tgt_ruv[2 * j + 1] = txy[2 * u + 1] - oy;
-                        }
+                const int64_t m0 = (int64_t)t * WW, g0 = hp.tgt_off[m0], n = hp.tgt_off[m0 + WW] - g0;
+                // packed position of the tile's k-th target (plan order): identity, or
+                // stable order of descending n9 of the target's box
+                order.resize((size_t)n);
+                std::iota(order.begin(), order.end(), 0);
+                if (hp.tsort) {
+                    key.resize((size_t)n);
+                    for (int64_t bl = 0; bl < WW; ++bl)
+                        for (int32_t g = hp.tgt_off[m0 + bl]; g < hp.tgt_off[m0 + bl + 1]; ++g)
+                            key[(size_t)(g - g0)] = n9[(size_t)(m0 + bl)];
+                    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return key[x] > key[y]; });
+                }
+                for (int64_t kk = 0; kk < n; ++kk) {
+                    const int64_t g = g0 + order[(size_t)kk], j = hp.tgt_pack_off[i] + kk, u = hp.tgt_uidx[g];
+                    // tile-local box -> row-run base j0 = by * R + bx in the region
+                    const uint32_t bl = (uint32_t)(std::upper_bound(hp.tgt_off.begin() + m0, hp.tgt_off.begin() + m0 + WW + 1,
+                                                                    (int32_t)g) - (hp.tgt_off.begin() + m0) - 1);
+                    uint32_t bx, by;
+                    morton_decode(bl, bx, by);
+                    hp.tgt_bl[j] = (uint16_t)(by * R + bx);
+                    if (hp.lean) hp.tgt_oix[j] = (uint16_t)(g - g0);
+                    if (f32) {
+                        hp.f32.tgt_ruv[2 * j] = (float)(txy[2 * u] - ox);
+                        hp.f32.tgt_ruv[2 * j + 1] = (float)(txy[2 * u + 1] - oy);
+                    } else {
+                        hp.f64.tgt_ruv[2 * j] = txy[2 * u] - ox;
+                        hp.f64.tgt_ruv[2 * j + 1] = txy[2 * u + 1] - oy;
                     }
                 }
             }

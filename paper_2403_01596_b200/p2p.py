@@ -77,7 +77,7 @@ class PlanInfo(C.Structure):
         ("t_max", C.c_int64), ("density", C.c_double), ("density_occupied", C.c_double),
         ("pairs", C.c_int64), ("pairs_global", C.c_int64), ("tiles", C.c_int64),
         ("smem_bytes", C.c_int64), ("halo_entries", C.c_int64), ("alg_bytes_kernel", C.c_int64),
-        ("alg_bytes_apply", C.c_int64), ("device_bytes", C.c_int64), ("build_seconds", C.c_double),
+        ("layout_bytes_apply", C.c_int64), ("device_bytes", C.c_int64), ("build_seconds", C.c_double),
         ("upload_seconds", C.c_double),
     ]
 

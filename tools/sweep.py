@@ -71,10 +71,10 @@ def main():
             i = pl.info
             row = dict(config=name, tpi=tpi, ns=ns, nbuf=nbuf, nt=nt, pad=pad, tile=i["tile_log2"], smem=i["smem_bytes"],
                        us=ms * 1e3, gpair=i["pairs"] / ms / 1e6, frac=i["pairs"] / (ms * 1e-3) / peak,
-                       alg_gbs=i["alg_bytes_apply"] / ms / 1e6)
+                       alg_gbs=i["alg_bytes_kernel"] / ms / 1e6, lay_gbs=i["layout_bytes_apply"] / ms / 1e6)
             rows.append(row)
             print(f"{name:12s} tpi {tpi} ns {ns} nbuf {nbuf} nt {nt} pad {pad} k {i['tile_log2']} smem {i['smem_bytes']:6d} "
-                  f"{ms * 1e3:8.1f} us {row['gpair']:8.1f} Gpair/s mufu {row['frac']:.3f} alg {row['alg_gbs']:6.0f} GB/s",
+                  f"{ms * 1e3:8.1f} us {row['gpair']:8.1f} Gpair/s mufu {row['frac']:.3f} alg {row['alg_gbs']:6.0f} layout {row['lay_gbs']:6.0f} GB/s",
                   flush=True)
             pl.close()
     if args.json:
