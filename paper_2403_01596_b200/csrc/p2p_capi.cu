@@ -44,7 +44,7 @@ struct p2p_plan_s {
     // device arrays
     DevBuf tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
-    DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_oix, tgt_ruv, tgt_pack_off, tile_tgt_base;
+    DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     int grid = 0;                                // persistent CTAs per launch
     unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
@@ -69,7 +69,7 @@ struct p2p_plan_s {
     void release() {
         DevBuf *all[] = {&tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
-                         &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &tgt_ruv,
+                         &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi,
                          &io_q, &io_out, &queue};
         for (DevBuf *b : all) {
@@ -93,6 +93,8 @@ const p2p::Layout<double> &layout_of<double>(const p2p::HostPlan &hp) { return h
 template <typename T, int TPI, bool PAD, int NS>
 const void *tiled_fn_nt(int nt) {
     using namespace p2p::dev;
+    if constexpr (TPI == 1 && !PAD && NS == 1)  // lean path: one-warp CTAs as well
+        if (nt == 32) return (const void *)p2p_tiled_kernel<T, TPI, 32, PAD, NS>;
     switch (nt) {
     case 64: return (const void *)p2p_tiled_kernel<T, TPI, 64, PAD, NS>;
     case 128: return (const void *)p2p_tiled_kernel<T, TPI, 128, PAD, NS>;
@@ -100,9 +102,9 @@ const void *tiled_fn_nt(int nt) {
     }
 }
 
-// TILED kernel instance for the plan's options (element type, targets per unit, CTA size, padding,
-// items per unit).  Instances: dense fp32 (2 targets/unit, padded, 3 row items), sparse fp32
-// (1 target/unit, unpadded or padded, whole-unit items), fp64 (unpadded, whole-unit items).
+// TILED kernel instance for the plan's options (element type, slots per unit, CTA size, padding,
+// items per unit).  Defaults: dense fp32 (2 slots/unit, padded, 3 row items), sparse fp32 and
+// fp64 (1 slot/unit, unpadded, whole-unit items = the lean path); the rest are tuning variants.
 template <typename T>
 const void *tiled_fn(int tpi, int nt, bool pad, int ns) {
     if constexpr (sizeof(T) == 4) {
@@ -111,24 +113,6 @@ const void *tiled_fn(int tpi, int nt, bool pad, int ns) {
         return ns == 3 ? tiled_fn_nt<float, 1, false, 3>(nt) : tiled_fn_nt<float, 1, false, 1>(nt);
     } else {
         return ns == 3 ? tiled_fn_nt<double, 1, false, 3>(nt) : tiled_fn_nt<double, 1, false, 1>(nt);
-    }
-}
-
-template <typename T>
-const void *tiled_ws_fn(int tpi, int ncw, bool pad) {
-    using namespace p2p::dev;
-    if constexpr (sizeof(T) == 4) {
-        if (tpi == 2)
-            return ncw == 8 ? (const void *)p2p_tiled_ws_kernel<float, 2, true, 8>
-                            : (const void *)p2p_tiled_ws_kernel<float, 2, true, 4>;
-        if (pad)
-            return ncw == 8 ? (const void *)p2p_tiled_ws_kernel<float, 1, true, 8>
-                            : (const void *)p2p_tiled_ws_kernel<float, 1, true, 4>;
-        return ncw == 8 ? (const void *)p2p_tiled_ws_kernel<float, 1, false, 8>
-                        : (const void *)p2p_tiled_ws_kernel<float, 1, false, 4>;
-    } else {
-        return ncw == 8 ? (const void *)p2p_tiled_ws_kernel<double, 1, false, 8>
-                        : (const void *)p2p_tiled_ws_kernel<double, 1, false, 4>;
     }
 }
 
@@ -158,6 +142,8 @@ void upload_plan(p2p_plan_s &P) {
         P.upload(P.reg_table, hp.reg_table);
         P.upload(P.tgt_bl, hp.tgt_bl);
         P.upload(P.tgt_oix, hp.tgt_oix);
+        P.upload(P.item_off, hp.item_off);
+        P.upload(P.items, hp.items);
         P.upload(P.tgt_ruv, lay.tgt_ruv);
         P.upload(P.tgt_pack_off, hp.tgt_pack_off);
         P.upload(P.tile_tgt_base, hp.tile_tgt_base);
@@ -172,12 +158,12 @@ void upload_plan(p2p_plan_s &P) {
     const bool two = hp.tpi == 2;
     const void *kfn = hp.layout == P2P_LAYOUT_REDUNDANT ? (const void *)p2p::dev::p2p_r_kernel<T>
                       : hp.layout == P2P_LAYOUT_TILED
-                          ? (hp.ws ? tiled_ws_fn<T>(hp.tpi, hp.ncw, hp.pad) : tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns))
+                          ? tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns)
                           : (two ? (const void *)p2p::dev::p2p_nr_kernel<T, sizeof(T) == 4 ? 2 : 1>
                                  : (const void *)p2p::dev::p2p_nr_kernel<T, 1>);
     ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2p::kSmemLimit), "smem attr");
     int occ = 0, dev = 0, sms = 0;
-    const int block = hp.layout == P2P_LAYOUT_TILED && hp.ws ? (hp.ncw + 1) * 32 : hp.nt;
+    const int block = hp.nt;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, block, (size_t)hp.smem_bytes), "occupancy");
     ck(cudaGetDevice(&dev), "cudaGetDevice");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
@@ -237,6 +223,8 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.reg_table = (const uint16_t *)P.reg_table.p;
         a.tgt_bl = (const uint16_t *)P.tgt_bl.p;
         a.tgt_oix = (const uint16_t *)P.tgt_oix.p;
+        a.item_off = (const uint32_t *)P.item_off.p;
+        a.items = (const uint16_t *)P.items.p;
         a.tgt_ruv = (const T *)P.tgt_ruv.p;
         a.tgt_pack_off = (const uint32_t *)P.tgt_pack_off.p;
         a.tile_tgt_base = (const int32_t *)P.tile_tgt_base.p;
@@ -244,14 +232,9 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.flat = hp.flat ? 1 : 0;
         a.nbuf = hp.nbuf;
         void *args[] = {&a};
-        if (hp.ws)
-            ck(cudaLaunchKernel(tiled_ws_fn<T>(hp.tpi, hp.ncw, hp.pad), dim3(P.grid), dim3((hp.ncw + 1) * 32),
-                                args, (size_t)hp.smem_bytes, s),
-               "tiled-ws launch");
-        else
-            ck(cudaLaunchKernel(tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns), dim3(P.grid), dim3(hp.nt), args,
-                                (size_t)hp.smem_bytes, s),
-               "tiled launch");
+        ck(cudaLaunchKernel(tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns), dim3(P.grid), dim3(hp.nt), args,
+                            (size_t)hp.smem_bytes, s),
+           "tiled launch");
     } else {
         if (hp.halo_entries > 0)
             p2p::dev::pack_r_kernel<T><<<grid_for(hp.halo_entries), 256, 0, s>>>(

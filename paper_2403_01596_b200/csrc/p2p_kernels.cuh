@@ -212,37 +212,6 @@ __device__ __forceinline__ double span3_f64(const double2 *__restrict__ UV, cons
     return acc;
 }
 
-// Four targets sharing one span x two sources per step: 8 pairs per LDS.128 + LDS.64.
-__device__ __forceinline__ void span4_f32(const float4 *__restrict__ A, const float2 *__restrict__ Q, int p0,
-                                          int p1, const float *ut, const float *vt, float *r) {
-    f2_t U[4], V[4], acc[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-        U[x] = f2_pack(ut[x], ut[x]);
-        V[x] = f2_pack(vt[x], vt[x]);
-        acc[x] = 0ull;
-    }
-#pragma unroll 2
-    for (int p = p0; p < p1; ++p) {
-        const float4 s = A[p];
-        const float2 q = Q[p];
-        const f2_t su = f2_pack(s.x, s.y), sv = f2_pack(s.z, s.w), qq = f2_pack(q.x, q.y);
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-            const f2_t du = f2_sub(U[x], su), dv = f2_sub(V[x], sv);
-            const f2_t w = f2_fma(dv, dv, f2_mul(du, du));
-            float w0, w1;
-            f2_unpack(w, w0, w1);
-            acc[x] = f2_fma(qq, f2_pack(lg2_approx(w0), lg2_approx(w1)), acc[x]);
-        }
-    }
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-        float c0, c1;
-        f2_unpack(acc[x], c0, c1);
-        r[x] = c0 + c1;
-    }
-}
 
 // Explicitly guarded fp32 sweep (slow path for targets whose fast sum is not finite).
 __device__ __noinline__ float span_f32_guarded(const float4 *__restrict__ A, const float2 *__restrict__ Q,
@@ -301,7 +270,9 @@ struct P2PArgs {
     const T *reg_uv;            // TILED: region-relative coordinates (fp32: (u0,u1,v0,v1) per pair)
     const uint16_t *reg_table;  // TILED: [slots][tstride] region box starts, then target box starts
     const uint16_t *tgt_bl;     // TILED: packed targets' row-run base j0 = by*R + bx in the region
-    const uint16_t *tgt_oix;    // TILED lean path: packed target -> tile-local output index (tsort plans)
+    const uint16_t *tgt_oix;    // TILED: per target slot, tile-local output index (0xFFFF: duplicate slot)
+    const uint32_t *item_off;   // TILED NS = 3: [slots+1] item-list offsets
+    const uint16_t *items;      // TILED NS = 3: unit << 2 | row, length-sorted per part
     const T *tgt_ruv;           // TILED: packed targets' coordinates relative to the region origin
     const uint32_t *tgt_pack_off;   // TILED: [slots+1] packed-target offsets (multiples of 8)
     const int32_t *tile_tgt_base;   // TILED: plan index of each tile's first target
@@ -692,52 +663,51 @@ p2p_r_kernel(const P2PArgs<T> a) {
 
 // ---------------------------------------------------------------- TILED kernel
 // The TILED layout packs, per tile, everything the CTA needs contiguously at
-// plan time: a table record (region box starts + target box starts), the
-// region's sources (tile + one-box ring, rebased to the region origin, in
-// row-run order) with a per-entry source index, and the tile's targets.  One
-// elected thread bulk-copies a tile's record with TMA (cp.async.bulk,
-// mbarrier completion), optionally one tile ahead (NBUF = 2).  Weights are
-// gathered through the per-entry index (q stays in plan order).
+// plan time: a table record (region box starts + slot count), the region's
+// sources (tile + one-box ring, rebased to the region origin, in row-run order)
+// with a per-entry source index, the tile's target slots (coordinates, row-run
+// base, output index) and, for NS = 3, the item list.  One elected thread
+// bulk-copies a tile's record with TMA (cp.async.bulk, mbarrier completion),
+// optionally one tile ahead (NBUF = 2).  Weights are gathered through the
+// per-entry index (q stays in plan order).
 //   PAD  (dense fp32): boxes padded to even counts, sources packed per pair,
-//        packed f32x2 loops; TPI = 2 targets per unit share each LDS.
+//        packed f32x2 loops; TPI = 2 slots per unit share each LDS.
 //   !PAD (sparse, fp64): no padding, one pair per step.
-//   NS = 3: work items (unit, row-run) + fixed-order reduction of the three
-//   partials; NS = 1: one item per unit sweeps its three row-runs in order.
-template <typename T, int TPI, int NT, bool PAD, int NS_>
+//   NS = 3: items (unit, row-run) in the plan's length-sorted order, then the
+//   fixed-order reduction of the three partials; NS = 1: one item per unit
+//   sweeps its three row-runs in order (LEAN: TPI = 1 unpadded, boxes ordered
+//   by n9, the three runs optionally flattened into one sequence).
+// Every target's sum has a fixed order independent of the launch, the tile
+// split and the partition: results are bit-reproducible.
+template <typename T, int TPI, int NT, bool PAD, int NS>
 __global__ void __launch_bounds__(NT)
 p2p_tiled_kernel(const P2PArgs<T> a) {
-    static_assert(TPI == 1 || (PAD && sizeof(T) == 4), "TPI > 1 is the padded fp32 path");
+    static_assert(TPI == 1 || (TPI == 2 && PAD && sizeof(T) == 4), "TPI = 2 is the padded fp32 path");
     static_assert(!PAD || sizeof(T) == 4, "the padded layout is fp32");
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ int s_next, s_units, s_base_next;
-    constexpr int NS = NS_;  // work items per unit: 1 (whole unit) or 3 (one per row-run)
-    // lean sparse path (tsort plans): one thread per target, targets sorted by n9, flattened row-runs
+    static_assert(NS == 1 || NS == 3, "one item per unit, or one per row-run");
     constexpr bool LEAN = NS == 1 && TPI == 1 && !PAD;
-    const int k = a.k, W = 1 << k, R = W + 2, RR = R * R, WW = W * W;
-    const unsigned rinv = ((1u << 20) + (unsigned)R - 1) / (unsigned)R;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ int s_next, s_base_next;
+    const int k = a.k, W = 1 << k, R = W + 2, RR = R * R;
     const TCarve c = tiled_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI, NS, a.nbuf);
     const bool db = a.nbuf == 2;
     T *s_q = reinterpret_cast<T *>(smem + c.q);
-    int *pstart = reinterpret_cast<int *>(smem + c.pstart);
-    int *uj0 = reinterpret_cast<int *>(smem + c.uj0);
-    int *ut = reinterpret_cast<int *>(smem + c.ut);
-    int *tslot = reinterpret_cast<int *>(smem + c.tslot);
     T *part = reinterpret_cast<T *>(smem + c.part);
     uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + c.bar);
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int tid = threadIdx.x;
 
     auto issue = [&](int ti, int b) {  // one elected thread: arm buffer b and bulk-copy tile ti's record
         const int slot = a.tile_slot[ti];
         unsigned char *buf = smem + c.buf0 + b * c.bufsz;
         const uint32_t rb = a.reg_off[slot], nent = a.reg_off[slot + 1] - rb;
         const uint32_t tb = a.tgt_pack_off[slot], ntp = a.tgt_pack_off[slot + 1] - tb;
+        const uint32_t ib = NS == 3 ? a.item_off[slot] : 0u, nit = NS == 3 ? a.item_off[slot + 1] - ib : 0u;
         const uint32_t b_tab = (uint32_t)c.tstride * 2u, b_uv = nent * 2 * (uint32_t)sizeof(T), b_ix = nent * 4u;
-        const uint32_t b_tuv = ntp * 2 * (uint32_t)sizeof(T), b_tbl = ntp * 2u;
-        const uint32_t b_oix = LEAN ? ntp * 2u : 0u;
+        const uint32_t b_tuv = ntp * 2 * (uint32_t)sizeof(T), b_t16 = ntp * 2u, b_it = nit * 2u;
         const uint32_t bar = smem_addr(mbar + b);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "r"(b_tab + b_uv + b_ix + b_tuv + b_tbl + b_oix)
+                     "r"(b_tab + b_uv + b_ix + b_tuv + 2 * b_t16 + b_it)
                      : "memory");
 #define P2P_BULK(dst, src, bytes)                                                                        \
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" \
@@ -750,9 +720,10 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         }
         if (ntp) {
             P2P_BULK(buf + c.tuv, a.tgt_ruv + 2 * (size_t)tb, b_tuv);
-            P2P_BULK(buf + c.tbl, a.tgt_bl + tb, b_tbl);
-            if (LEAN) P2P_BULK(buf + c.oix, a.tgt_oix + tb, b_oix);
+            P2P_BULK(buf + c.tbl, a.tgt_bl + tb, b_t16);
+            P2P_BULK(buf + c.oix, a.tgt_oix + tb, b_t16);
         }
+        if (nit) P2P_BULK(buf + c.items, a.items + ib, b_it);
 #undef P2P_BULK
     };
 
@@ -779,12 +750,12 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         }
         const unsigned char *B = smem + c.buf0 + buf * c.bufsz;
         const uint16_t *table = reinterpret_cast<const uint16_t *>(B + c.table);
-        const uint16_t *ttab = table + RR + 1;  // target box starts of the tile
         const T *s_uv = reinterpret_cast<const T *>(B + c.uv);
         const int32_t *s_idx = reinterpret_cast<const int32_t *>(B + c.idx);
         const T *tuv = reinterpret_cast<const T *>(B + c.tuv);
         const uint16_t *tbl = reinterpret_cast<const uint16_t *>(B + c.tbl);
         const uint16_t *oix = reinterpret_cast<const uint16_t *>(B + c.oix);
+        const uint16_t *items = reinterpret_cast<const uint16_t *>(B + c.items);
         if (tid == 0) {  // next tile; with two buffers its record streams in while this tile computes
             const int nx = atomicAdd(a.queue, 1);
             s_next = nx;
@@ -805,87 +776,33 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             parity ^= 1u << buf;
         }
         if (trc) trc[2] = gtimer();
-        const int nent = (int)table[RR];
-        const int nt = TPI == 1 && NS == 1 ? (int)ttab[0] : (int)ttab[WW];  // short table: the target count
-        if (TPI > 1 && wid == 0) {  // units of TPI targets of one box
-            int carry = 0;
-            for (int base = 0; base < WW; base += 32) {
-                const int bl = base + lane;
-                const int n = bl < WW ? (int)ttab[bl + 1] - (int)ttab[bl] : 0;
-                const int np = (n + TPI - 1) / TPI;
-                const int incl = warp_incl_scan(np);
-                if (bl < WW) pstart[bl] = carry + incl - np;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            if (lane == 0) s_units = carry;
-        }
+        const int nent = (int)table[RR], nslot = (int)table[RR + 1], nu = nslot / TPI;
         gather_weights(s_idx, a.q, s_q, nent, tid, NT);  // weights through the per-entry index
         __syncthreads();
-        if (TPI > 1) {
-            for (int t = tid; t < nt; t += NT) {
-                // j0 / R by multiply-shift: exact for R <= 66, j0 < 4356 (error < 0.004 < 1/R)
-                const int j0t = tbl[t], by = (int)(((unsigned)j0t * rinv) >> 20), bx = j0t - by * R;
-                const int bl = (int)(spread16((uint32_t)bx) | (spread16((uint32_t)by) << 1));
-                const int r = t - (int)ttab[bl], u = pstart[bl] + r / TPI, sl = r % TPI;
-                ut[TPI * u + sl] = t;
-                tslot[t] = TPI * u + sl;
-                if (sl == 0) uj0[u] = j0t;
-                if (t + 1 == (int)ttab[bl + 1])  // box's last target fills the unit's empty slots (duplicates)
-                    for (int x = sl + 1; x < TPI; ++x) ut[TPI * u + x] = t;
-            }
-            __syncthreads();
-        }
-        const int nu = TPI > 1 ? s_units : nt;
         const int pinfo = a.tile_part[cur], npart = pinfo >> 16, ipart = pinfo & 0xffff;
         int ub = 0, ue = nu;
         if (npart > 1) {  // tail tile split into npart unit ranges (nu * npart < 2^31)
             ub = (nu * ipart) / npart;
             ue = (nu * (ipart + 1)) / npart;
         }
-        const int nr = ue - ub;
         if (trc) {
             trc[3] = gtimer();
             trc[6] = nu;
             trc[7] = (unsigned long long)nent;
         }
 
-        // one (unit, row) item: TPI partial sums over the row-run's sources
-        auto item = [&](int u, int row, T *res, int piece, int f) {
-            int t0, jb;
-            if (TPI > 1) {
-                t0 = ut[TPI * u];
-                jb = uj0[u];
-            } else {
-                t0 = u;
-                jb = tbl[u];
-            }
-            const int j0 = jb + row * R;
-            int i0 = table[j0], i1 = table[j0 + 3];
-            if (f > 1) {  // piece of the row-run (in source pairs when padded)
-                const int g = PAD ? 2 : 1, n = (i1 - i0) / g;
-                const int a0 = i0 + g * ((n * piece) / f), a1 = i0 + g * ((n * (piece + 1)) / f);
-                i0 = a0;
-                i1 = a1;
-            }
+        // TPI partial sums of unit u over its row-run `row`
+        auto unit_row = [&](int u, int row, T *res) {
+            const int t0 = TPI * u, j0 = tbl[t0] + row * R;
+            const int i0 = table[j0], i1 = table[j0 + 3];
             if constexpr (PAD) {
                 const float4 *A = reinterpret_cast<const float4 *>(s_uv);
                 const float2 *Q = reinterpret_cast<const float2 *>(s_q);
-                if constexpr (TPI == 4) {
-                    float xs[4], ys[4];
-#pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        const int tx = ut[4 * u + x];
-                        xs[x] = tuv[2 * tx];
-                        ys[x] = tuv[2 * tx + 1];
-                    }
-                    span4_f32(A, Q, i0 >> 1, i1 >> 1, xs, ys, res);
-                } else if constexpr (TPI == 2) {
-                    const int t1 = ut[2 * u + 1];
-                    span2_f32(A, Q, i0 >> 1, i1 >> 1, tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t1], tuv[2 * t1 + 1],
+                if constexpr (TPI == 2)
+                    span2_f32(A, Q, i0 >> 1, i1 >> 1, tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t0 + 2], tuv[2 * t0 + 3],
                               res[0], res[1]);
-                } else {
+                else
                     res[0] = span_f32(A, Q, i0 >> 1, i1 >> 1, tuv[2 * t0], tuv[2 * t0 + 1]);
-                }
             } else if constexpr (sizeof(T) == 4) {
                 res[0] = span1_f32(reinterpret_cast<const float2 *>(s_uv), reinterpret_cast<const float *>(s_q), i0,
                                    i1, tuv[2 * t0], tuv[2 * t0 + 1]);
@@ -894,9 +811,11 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                                    i1, tuv[2 * t0], tuv[2 * t0 + 1], a.eps2);
             }
         };
-        // final value of target t (written to tile-local output o) from its row-ordered
-        // sum (fp32: guarded redo if non-finite)
-        auto finish = [&](int t, int o, T acc) {
+        // final value of slot t from its row-ordered sum (fp32: guarded redo if non-finite),
+        // written to the slot's tile-local output index (duplicate slots write nothing)
+        auto finish = [&](int t, T acc) {
+            const int o = oix[t];
+            if (TPI > 1 && o == 0xFFFF) return;
             if constexpr (sizeof(T) == 4) {
                 if (!isfinite(acc)) {
                     const int jb = tbl[t];
@@ -920,7 +839,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             a.out[tb + o] = a.accumulate ? a.out[tb + o] + acc : acc;
         };
 
-        if constexpr (LEAN) {  // one thread per target (sorted by n9), its three row-runs as one sequence
+        if constexpr (LEAN) {  // one thread per target (boxes by n9): three row-runs, flattened or in turn
             for (int t = ub + tid; t < ue; t += NT) {
                 const int jb = tbl[t];
                 const T ux = tuv[2 * t], uy = tuv[2 * t + 1];
@@ -947,20 +866,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                                              a.eps2);
                     }
                 }
-                finish(t, oix[t], acc);
-            }
-        } else if constexpr (NS == 1 && TPI == 1) {  // padded rows, one thread per target
-            for (int t = ub + tid; t < ue; t += NT) {
-                const int jb = tbl[t];
-                const T ux = tuv[2 * t], uy = tuv[2 * t + 1];
-                T acc = (T)0;
-#pragma unroll
-                for (int row = 0; row < 3; ++row) {
-                    const int j0 = jb + row * R;
-                    acc += span_f32(reinterpret_cast<const float4 *>(s_uv), reinterpret_cast<const float2 *>(s_q),
-                                    table[j0] >> 1, table[j0 + 3] >> 1, ux, uy);
-                }
-                finish(t, t, acc);
+                finish(t, acc);
             }
         } else if constexpr (NS == 1) {  // one item per unit, rows in order
             for (int u = ub + tid; u < ue; u += NT) {
@@ -968,39 +874,27 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
 #pragma unroll
                 for (int x = 0; x < TPI; ++x) acc[x] = (T)0;
                 for (int row = 0; row < 3; ++row) {
-                    item(u, row, r, 0, 1);
+                    unit_row(u, row, r);
 #pragma unroll
                     for (int x = 0; x < TPI; ++x) acc[x] += r[x];
                 }
-                if (TPI > 1) {
 #pragma unroll
-                    for (int x = 0; x < TPI; ++x) {
-                        const int t = ut[TPI * u + x];
-                        if (x > 0 && t == ut[TPI * u + x - 1]) break;  // duplicates fill the box's last unit
-                        finish(t, t, acc[x]);
-                    }
-                } else {
-                    finish(u, u, acc[0]);
-                }
+                for (int x = 0; x < TPI; ++x) finish(TPI * u + x, acc[x]);
             }
-        } else {  // (unit, row) items, then the fixed-order reduction of the three partials
-            for (int it = tid; it < 3 * nr; it += NT) {
-                const int row = (it >= nr) + (it >= 2 * nr);
-                const int u = ub + it - row * nr;
+        } else {  // (unit, row) items in the plan's order, then the fixed-order reduction of the partials
+            for (int it = 3 * ub + tid; it < 3 * ue; it += NT) {
+                const int w = items[it], u = w >> 2, row = w & 3;
                 T res[TPI];
-                item(u, row, res, 0, 1);
+                unit_row(u, row, res);
 #pragma unroll
-                for (int x = 0; x < TPI; ++x) part[row * TPI * nu + TPI * u + x] = res[x];
+                for (int x = 0; x < TPI; ++x) part[row * nslot + TPI * u + x] = res[x];
             }
             __syncthreads();
-            const int rs = TPI * nu;
             for (int u = ub + tid; u < ue; u += NT) {
 #pragma unroll
                 for (int x = 0; x < TPI; ++x) {
-                    const int t = TPI > 1 ? ut[TPI * u + x] : u;
-                    if (x > 0 && t == ut[TPI * u + x - 1]) break;  // duplicates fill the box's last unit
                     const int sl = TPI * u + x;
-                    finish(t, t, part[sl] + part[rs + sl] + part[2 * rs + sl]);
+                    finish(sl, part[sl] + part[nslot + sl] + part[2 * nslot + sl]);
                 }
             }
         }
@@ -1012,255 +906,6 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         else if (tid == 0 && cur < a.ntiles) issue(cur, 0);
     }
     if (tid == 0) queue_exit(a.queue);
-}
-
-// ---------------------------------------------------------------- TILED-WS kernel
-// Warp-specialised persistent pipeline over the TILED layout (the canonical
-// Blackwell producer/consumer structure, with mbarriers instead of CTA-wide
-// barriers):
-//   producer warp (the last one): pulls tiles from the queue; per tile, into a
-//     free pipeline slot: TMA bulk copy of the tile record (full[s], tx-count),
-//     weight gather through the per-entry index, work-unit formation (TPI
-//     targets of one box), meta; then arrives on ready[s];
-//   consumer warps: wait ready[s], stream the slot's units (each unit sweeps
-//     its three row-runs in order and writes its targets' potentials), then
-//     arrive on empty[s] and move straight to the next slot.
-// No CTA-wide barrier in the steady state: consumers flow from tile to tile
-// while the producer stages ahead (nslot = 2 or 3 slots).
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-        "@!P bra WAIT_%=;\n}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-
-template <typename T, int TPI, bool PAD, int NCW>
-__global__ void __launch_bounds__((NCW + 1) * 32)
-p2p_tiled_ws_kernel(const P2PArgs<T> a) {
-    static_assert(!(TPI == 2) || (PAD && sizeof(T) == 4), "TPI = 2 is the padded fp32 path");
-    static_assert(!PAD || sizeof(T) == 4, "the padded layout is fp32");
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int k = a.k, W = 1 << k, R = W + 2, RR = R * R, WW = W * W, NSLOT = a.nbuf;
-    const WsCarve c = ws_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI, NSLOT);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + c.bars);  // full[NSLOT], ready[NSLOT], empty[NSLOT]
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    auto full = [&](int s) { return smem_addr(bars + s); };
-    auto ready = [&](int s) { return smem_addr(bars + NSLOT + s); };
-    auto empty = [&](int s) { return smem_addr(bars + 2 * NSLOT + s); };
-    if (tid == 0) {
-        for (int s = 0; s < NSLOT; ++s) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full(s)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ready(s)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty(s)), "r"(NCW));
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    if (wid == NCW) {  // ===================== producer warp
-        // slot of iteration j = j % NSLOT; the bulk copy of iteration j is issued at
-        // iteration j - (NSLOT - 1), so NSLOT - 1 copies stream ahead of the gather.
-        int it_end = 0x7fffffff;          // first iteration without a tile
-        int tiles_q[4] = {-1, -1, -1, -1};  // tile of each slot (NSLOT <= 4)
-        auto claim_and_issue = [&](int j) {  // claim the tile of iteration j, issue its copy
-            const int sj = j % NSLOT, usej = j / NSLOT;
-            int ti = 0;
-            if (lane == 0) ti = atomicAdd(a.queue, 1);
-            ti = __shfl_sync(0xffffffffu, ti, 0);
-            if (ti >= a.ntiles) {
-                it_end = min(it_end, j);
-                return;
-            }
-            if (usej > 0) mbar_wait(empty(sj), (usej - 1) & 1);
-            #pragma unroll
-            for (int x = 0; x < 4; ++x)
-                if (x == sj) tiles_q[x] = ti;
-            if (lane == 0) {
-                unsigned char *S = smem + c.slot0 + sj * c.slotsz;
-                const int slot = a.tile_slot[ti];
-                const uint32_t rb = a.reg_off[slot], nent = a.reg_off[slot + 1] - rb;
-                const uint32_t pb = a.tgt_pack_off[slot], ntp = a.tgt_pack_off[slot + 1] - pb;
-                const uint32_t b_tab = (uint32_t)c.tstride * 2u, b_uv = nent * 2 * (uint32_t)sizeof(T),
-                               b_ix = nent * 4u, b_tuv = ntp * 2 * (uint32_t)sizeof(T), b_tbl = ntp * 2u;
-                const uint32_t bar = full(sj);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                             "r"(b_tab + b_uv + b_ix + b_tuv + b_tbl)
-                             : "memory");
-#define P2P_BULK(dst, src, bytes)                                                                        \
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" \
-                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(bar)                                   \
-                 : "memory")
-                P2P_BULK(S + c.table, a.reg_table + (size_t)slot * c.tstride, b_tab);
-                if (nent) {
-                    P2P_BULK(S + c.uv, a.reg_uv + 2 * (size_t)rb, b_uv);
-                    P2P_BULK(S + c.idx, a.reg_idx + rb, b_ix);
-                }
-                if (ntp) {
-                    P2P_BULK(S + c.tuv, a.tgt_ruv + 2 * (size_t)pb, b_tuv);
-                    P2P_BULK(S + c.tbl, a.tgt_bl + pb, b_tbl);
-                }
-#undef P2P_BULK
-            }
-        };
-        for (int j = 0; j < NSLOT - 1; ++j) claim_and_issue(j);
-        for (int it = 0;; ++it) {
-            const int s = it % NSLOT, use = it / NSLOT;
-            unsigned char *S = smem + c.slot0 + s * c.slotsz;
-            int *meta = reinterpret_cast<int *>(S + c.meta);
-            if (it >= it_end) {  // end of stream: the slot's previous use must be released first
-                if (use > 0) mbar_wait(empty(s), (use - 1) & 1);
-                if (lane == 0) {
-                    meta[0] = -1;
-                    mbar_arrive(ready(s));
-                }
-                break;
-            }
-            int ti = -1;
-            #pragma unroll
-            for (int x = 0; x < 4; ++x)
-                if (x == s) ti = tiles_q[x];
-            const int slot = a.tile_slot[ti];
-            const int tb = a.tile_tgt_base[slot];
-            const uint32_t nent = a.reg_off[slot + 1] - a.reg_off[slot];
-            mbar_wait(full(s), use & 1);
-            const uint16_t *table = reinterpret_cast<const uint16_t *>(S + c.table);
-            const uint16_t *ttab = table + RR + 1;
-            gather_weights(reinterpret_cast<const int32_t *>(S + c.idx), a.q, reinterpret_cast<T *>(S + c.q),
-                           (int)nent, lane, 32);
-            const int nt = (int)ttab[WW];
-            int nu = nt;
-            if (TPI == 2) {  // units: pairs of targets of one box, in box order
-                int *ut = reinterpret_cast<int *>(S + c.ut);
-                int *uj0 = reinterpret_cast<int *>(S + c.uj0);
-                int carry = 0;
-                for (int base = 0; base < WW; base += 32) {
-                    const int bl = base + lane;
-                    const int n = bl < WW ? (int)ttab[bl + 1] - (int)ttab[bl] : 0;
-                    const int np = (n + 1) >> 1;
-                    const int incl = warp_incl_scan(np);
-                    const int u0 = carry + incl - np;
-                    if (bl < WW && n > 0) {
-                        const int j0 = (int)compact16((uint32_t)bl >> 1) * R + (int)compact16((uint32_t)bl);
-                        const int t0 = ttab[bl];
-                        for (int x = 0; x < np; ++x) {
-                            ut[2 * (u0 + x)] = t0 + 2 * x;
-                            ut[2 * (u0 + x) + 1] = min(t0 + 2 * x + 1, t0 + n - 1);
-                            uj0[u0 + x] = j0;
-                        }
-                    }
-                    carry += __shfl_sync(0xffffffffu, incl, 31);
-                }
-                nu = carry;
-            }
-            if (lane == 0) {
-                meta[0] = ti;
-                meta[1] = tb;
-                meta[2] = nu;
-                meta[3] = 0;  // next unit chunk to claim
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(ready(s));  // release: slot s is ready
-            claim_and_issue(it + NSLOT - 1);       // keep NSLOT - 1 copies in flight
-        }
-        if (lane == 0) queue_exit(a.queue);
-        return;
-    }
-
-    // ===================== consumer warps
-    const int ctid = tid, NCT = NCW * 32;
-    for (int it = 0;; ++it) {
-        const int s = it % NSLOT, use = it / NSLOT;
-        unsigned char *S = smem + c.slot0 + s * c.slotsz;
-        mbar_wait(ready(s), use & 1);
-        int *meta = reinterpret_cast<int *>(S + c.meta);
-        if (meta[0] < 0) break;
-        mbar_wait(full(s), use & 1);  // (already complete) makes the bulk-copied bytes visible here too
-        const int tb = meta[1], nu = meta[2];
-        const uint16_t *table = reinterpret_cast<const uint16_t *>(S + c.table);
-        const T *s_uv = reinterpret_cast<const T *>(S + c.uv);
-        const T *tuv = reinterpret_cast<const T *>(S + c.tuv);
-        const uint16_t *tbl = reinterpret_cast<const uint16_t *>(S + c.tbl);
-        const T *s_q = reinterpret_cast<const T *>(S + c.q);
-        const int *ut = reinterpret_cast<const int *>(S + c.ut);
-        const int *uj0 = reinterpret_cast<const int *>(S + c.uj0);
-
-        for (;;) {  // claim chunks of 32 units until the slot is exhausted
-            int base = 0;
-            if (lane == 0) base = atomicAdd(meta + 3, 32);
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (base >= nu) break;
-            const int u = base + lane;
-            if (u >= nu) continue;
-            int t0, t1, jb;
-            if (TPI == 2) {
-                t0 = ut[2 * u];
-                t1 = ut[2 * u + 1];
-                jb = uj0[u];
-            } else {
-                t0 = t1 = u;
-                jb = tbl[u];
-            }
-            T acc0 = (T)0, acc1 = (T)0;
-            for (int row = 0; row < 3; ++row) {
-                const int j0 = jb + row * R;
-                const int i0 = table[j0], i1 = table[j0 + 3];
-                if constexpr (PAD) {
-                    const float4 *A = reinterpret_cast<const float4 *>(s_uv);
-                    const float2 *Q = reinterpret_cast<const float2 *>(s_q);
-                    if constexpr (TPI == 2) {
-                        float r0, r1;
-                        span2_f32(A, Q, i0 >> 1, i1 >> 1, tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t1], tuv[2 * t1 + 1],
-                                  r0, r1);
-                        acc0 += r0;
-                        acc1 += r1;
-                    } else {
-                        acc0 += span_f32(A, Q, i0 >> 1, i1 >> 1, tuv[2 * t0], tuv[2 * t0 + 1]);
-                    }
-                } else if constexpr (sizeof(T) == 4) {
-                    acc0 += span1_f32(reinterpret_cast<const float2 *>(s_uv), reinterpret_cast<const float *>(s_q), i0,
-                                      i1, tuv[2 * t0], tuv[2 * t0 + 1]);
-                } else {
-                    acc0 += span1_f64(reinterpret_cast<const double2 *>(s_uv), reinterpret_cast<const double *>(s_q),
-                                      i0, i1, tuv[2 * t0], tuv[2 * t0 + 1], a.eps2);
-                }
-            }
-#pragma unroll
-            for (int x = 0; x < TPI; ++x) {
-                const int t = x == 0 ? t0 : t1;
-                if (x == 1 && t1 == t0) break;
-                T acc = x == 0 ? acc0 : acc1;
-                if constexpr (sizeof(T) == 4) {
-                    if (!isfinite(acc)) {  // a pair closer than eps: redo this target with the explicit guard
-                        acc = 0.f;
-                        for (int row = 0; row < 3; ++row) {
-                            const int j0 = jb + row * R;
-                            if constexpr (PAD)
-                                acc += span_f32_guarded(reinterpret_cast<const float4 *>(s_uv),
-                                                        reinterpret_cast<const float2 *>(s_q), table[j0] >> 1,
-                                                        table[j0 + 3] >> 1, tuv[2 * t], tuv[2 * t + 1], a.eps2);
-                            else
-                                acc += span1_f32_guarded(reinterpret_cast<const float2 *>(s_uv),
-                                                         reinterpret_cast<const float *>(s_q), table[j0],
-                                                         table[j0 + 3], tuv[2 * t], tuv[2 * t + 1], a.eps2);
-                        }
-                    }
-                    acc = (-0.5f * kLn2) * acc;
-                } else {
-                    acc = -0.5 * acc;
-                }
-                a.out[tb + t] = a.accumulate ? a.out[tb + t] + acc : acc;
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty(s));  // this warp is done with slot s
-    }
 }
 
 // ---------------------------------------------------------------- data movement

@@ -72,69 +72,39 @@ P2P_HD inline RCarve r_carve(int k, int src_cap, int tgt_cap, int e) {
 }
 
 struct TCarve {
-    int buf0, bufsz;                      // double-buffered, bulk-copied part: 2 x bufsz bytes from buf0
-    int table, uv, idx, tuv, tbl, oix;    // offsets inside one buffer
-    int q, pstart, uj0, ut, tslot, part, bar, total, ucap, tstride;
+    int buf0, bufsz;                            // NBUF bulk-copied buffers of bufsz bytes from buf0
+    int table, uv, idx, tuv, tbl, oix, items;   // offsets inside one buffer
+    int q, part, bar, total, tstride, icap;
 };
-// TILED layout.  src_cap: max packed-region entries of a tile (multiple of 4);
-// tgt_cap: max packed targets of a tile (multiple of 8); tpi: targets per
-// unit; ns: work segments per target (3 row-runs, or 6 half row-runs).
-P2P_HD inline int tiled_table_stride(int k, bool lean) {
+// TILED layout.  Per tile record: table (region box starts + slot count), region
+// entries (coordinates, source index), target slots (coordinates, row-run base,
+// output index) and, for NS = 3 plans, the item list.  src_cap: max region
+// entries of a tile (multiple of 4); slot_cap: max target slots of a tile
+// (multiple of 8); tpi: slots per unit; ns: items per unit (1, or 3 row-runs).
+P2P_HD inline int tiled_table_stride(int k) {
     const int W = 1 << k, R = W + 2;
-    // uint16: region box starts, then target box starts (units of TPI > 1 / NS = 3 plans)
-    // or, for one-item-per-target plans, just the tile's target count
-    return lean ? (R * R + 2 + 7) & ~7 : (R * R + 1 + W * W + 1 + 7) & ~7;
+    return (R * R + 2 + 7) & ~7;  // uint16: region box starts [R*R + 1], then the tile's slot count
 }
-P2P_HD inline TCarve tiled_carve(int k, int src_cap, int tgt_cap, int e, int tpi, int ns, int nbuf) {
-    const int WW = 1 << (2 * k);
+P2P_HD inline int tiled_item_cap(int slot_cap, int tpi, int ns) {
+    return ns == 3 ? (3 * (slot_cap / tpi) + 7) & ~7 : 0;
+}
+P2P_HD inline TCarve tiled_carve(int k, int src_cap, int slot_cap, int e, int tpi, int ns, int nbuf) {
     TCarve c;
-    c.ucap = nr_unit_cap(k, tgt_cap, tpi);
-    c.tstride = tiled_table_stride(k, tpi == 1 && ns == 1);
+    c.tstride = tiled_table_stride(k);
+    c.icap = tiled_item_cap(slot_cap, tpi, ns);
     c.table = 0;
     c.uv = align16(2 * c.tstride);
     c.idx = c.uv + 2 * e * src_cap;
     c.tuv = align16(c.idx + 4 * src_cap);
-    c.tbl = c.tuv + 2 * e * tgt_cap;
-    c.oix = c.tbl + 2 * tgt_cap;
-    c.bufsz = align16(c.oix + (tpi == 1 && ns == 1 ? 2 * tgt_cap : 0));
+    c.tbl = c.tuv + 2 * e * slot_cap;
+    c.oix = c.tbl + 2 * slot_cap;
+    c.items = c.oix + 2 * slot_cap;
+    c.bufsz = align16(c.items + 2 * c.icap);
     c.buf0 = 0;
     c.q = nbuf * c.bufsz;
-    // unit tables only for TPI > 1 (TPI = 1: unit = target), partials only for NS = 3
-    const int uc = tpi > 1 ? c.ucap : 0, tc = tpi > 1 ? tgt_cap : 0;
-    c.pstart = align16(c.q + e * src_cap);
-    c.uj0 = c.pstart + 4 * (tpi > 1 ? WW + 1 : 0);
-    c.ut = c.uj0 + 4 * uc;
-    c.tslot = c.ut + 4 * tpi * uc;
-    c.part = align16(c.tslot + 4 * tc);
-    c.bar = align16(c.part + (ns == 1 ? 0 : 3) * e * tpi * c.ucap);
+    c.part = align16(c.q + e * src_cap);  // NS = 3: three partial sums per slot
+    c.bar = align16(c.part + (ns == 3 ? 3 * e * slot_cap : 0));
     c.total = c.bar + 16;
-    return c;
-}
-
-// Warp-specialised TILED kernel: nslot pipeline slots, each = one tile record
-// (bulk-copied) + gathered weights + work units + meta; 3 mbarriers per slot.
-struct WsCarve {
-    int slot0, slotsz;                    // slot s at slot0 + s * slotsz
-    int table, uv, idx, tuv, tbl, q, ut, uj0, meta;  // offsets inside a slot
-    int bars, total, ucap, tstride;
-};
-P2P_HD inline WsCarve ws_carve(int k, int src_cap, int tgt_cap, int e, int tpi, int nslot) {
-    WsCarve c;
-    c.ucap = nr_unit_cap(k, tgt_cap, tpi);
-    c.tstride = tiled_table_stride(k, false);
-    c.table = 0;
-    c.uv = align16(2 * c.tstride);
-    c.idx = c.uv + 2 * e * src_cap;
-    c.tuv = align16(c.idx + 4 * src_cap);
-    c.tbl = c.tuv + 2 * e * tgt_cap;
-    c.q = align16(c.tbl + 2 * tgt_cap);
-    c.ut = align16(c.q + e * src_cap);
-    c.uj0 = c.ut + 4 * tpi * c.ucap;
-    c.meta = align16(c.uj0 + 4 * c.ucap);
-    c.slotsz = align16(c.meta + 16);
-    c.slot0 = 0;
-    c.bars = nslot * c.slotsz;
-    c.total = c.bars + 3 * 8 * nslot;
     return c;
 }
 
@@ -220,20 +190,20 @@ struct HostPlan {
     // ---- TILED layout (per tile in Morton order = "slot")
     std::vector<uint32_t> reg_off;                // [tiles+1] packed-region offsets
     std::vector<int32_t> reg_idx;                 // local source index, -1 = pad
-    std::vector<uint16_t> reg_table;              // [tiles][tstride] region box starts, then target box starts
-    std::vector<uint16_t> tgt_bl;                 // per-tile packed targets: row-run base j0 = by * R + bx
-    std::vector<uint16_t> tgt_oix;                // lean: packed target -> tile-local output index
-    std::vector<uint32_t> tgt_pack_off;           // [tiles+1] packed-target offsets (multiples of 8)
+    std::vector<uint16_t> reg_table;              // [tiles][tstride] region box starts, then the slot count
+    std::vector<uint16_t> tgt_bl;                 // per target slot: row-run base j0 = by * R + bx
+    std::vector<uint16_t> tgt_oix;                // per target slot: tile-local output index (0xFFFF: duplicate)
+    std::vector<uint32_t> tgt_pack_off;           // [tiles+1] target-slot offsets (multiples of 8)
+    std::vector<uint32_t> item_off;               // NS = 3: [tiles+1] item-list offsets (multiples of 8)
+    std::vector<uint16_t> items;                  // NS = 3: unit << 2 | row, sorted by row-run length per part
     std::vector<int32_t> tile_tgt_base;           // [tiles] plan index of each tile's first target
     int ns = 3;                                   // TILED work segments per target
     int nbuf = 1;                                 // TILED record buffers (2 = prefetch next tile)
     bool pad = true;                              // TILED: boxes padded to even counts (packed f32x2 loops)
     int nt = 256;                                 // threads per CTA (TILED: 128 or 256)
-    bool lean = false;                            // TILED lean kernel path (tpi 1, ns 1, unpadded): reads tgt_oix
-    bool tsort = false;                           // lean path: targets sorted by n9 within the tile
+    bool lean = false;                            // TILED lean kernel path (tpi 1, ns 1, unpadded)
+    bool tsort = false;                           // ns 1: target boxes of a tile ordered by n9 (descending)
     bool flat = false;                            // lean path: row-runs swept as one sequence (sparse)
-    bool ws = true;                               // TILED: warp-specialised pipeline kernel
-    int ncw = 8;                                  // TILED-WS consumer warps per CTA
     std::vector<int32_t> tile_slot;               // launch order -> slot
     std::vector<int32_t> tile_part;               // launch order -> part | nparts << 16 (tail splitting)
     int64_t reg_entries = 0;

@@ -231,14 +231,15 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             if (to[(t + 1) * WW] > to[t * WW]) hp.tiles_g.push_back((int32_t)t);
         const int64_t nt = (int64_t)hp.tiles_g.size();
         hp.tile_pairs_g.assign((size_t)nt, 0);
-        std::vector<int64_t> region((size_t)nt, 0), halo((size_t)nt, 0), tcount((size_t)nt, 0);
+        std::vector<int64_t> region((size_t)nt, 0), halo((size_t)nt, 0), tcount((size_t)nt, 0), tcount2((size_t)nt, 0);
         parallel_for(nt, [&](int64_t a, int64_t bnd) {
             for (int64_t i = a; i < bnd; ++i) {
                 int64_t t = hp.tiles_g[i];
-                int64_t pr = 0, hl = 0;
+                int64_t pr = 0, hl = 0, sl2 = 0;
                 for (int64_t b = t * WW; b < (t + 1) * WW; ++b) {
                     int64_t c = ntg(b);
                     if (!c) continue;
+                    sl2 += c + (c & 1);  // target slots of 2-target units (odd boxes: one duplicate)
                     pr += c * (int64_t)n9[b];
                     hl += pad2(n9[b]);
                 }
@@ -253,13 +254,13 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                     }
                 hp.tile_pairs_g[i] = pr;
                 tcount[i] = to[(t + 1) * WW] - to[t * WW];
+                tcount2[i] = sl2;
                 region[i] = rg;
                 halo[i] = pad4(hl);
             }
         }, 256);
         hp.max_region = region.empty() ? 0 : *std::max_element(region.begin(), region.end());
         hp.max_tile_halo = halo.empty() ? 0 : *std::max_element(halo.begin(), halo.end());
-        hp.tgt_cap = pad8(tcount.empty() ? 0 : *std::max_element(tcount.begin(), tcount.end()));
         hp.src_cap = d.layout == P2P_LAYOUT_REDUNDANT ? hp.max_tile_halo : pad4(hp.max_region);
         hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= 8.0 && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT) ? 2 : 1;
         // TILED defaults: dense fp32 -> padded pairs, 2 targets per unit, (unit, row) items;
@@ -273,7 +274,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         if (const char *v = std::getenv("P2P_TPI"))
             if (d.precision == P2P_FP32 && d.layout != P2P_LAYOUT_REDUNDANT) {
                 const int x = std::atoi(v);
-                hp.tpi = x >= 4 && d.layout == P2P_LAYOUT_TILED ? 4 : x == 2 ? 2 : 1;
+                hp.tpi = x == 2 ? 2 : 1;
             }
         if (const char *v = std::getenv("P2P_PAD"))
             if (d.layout == P2P_LAYOUT_TILED && d.precision == P2P_FP32) hp.pad = std::atoi(v) != 0;
@@ -284,26 +285,27 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         if (const char *v = std::getenv("P2P_NT"))
             if (d.layout == P2P_LAYOUT_TILED) {
                 const int x = std::atoi(v);
-                hp.nt = x <= 64 ? 64 : x <= 128 ? 128 : 256;
+                hp.nt = x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : 256;
             }
-        hp.ws = false;  // the warp-specialised variant measured slower; kept for experiments
-        if (const char *v = std::getenv("P2P_WS")) hp.ws = std::atoi(v) != 0;
-        hp.ncw = 8;
-        if (const char *v = std::getenv("P2P_NCW")) hp.ncw = std::atoi(v) == 4 ? 4 : 8;
-        if (d.layout == P2P_LAYOUT_TILED && hp.ws) {
-            hp.nbuf = 2;
-            if (const char *v = std::getenv("P2P_NBUF")) hp.nbuf = std::max(2, std::min(4, std::atoi(v)));
-        }
         // lean sparse path: targets of a tile sorted by neighbourhood size (n9), so the
         // lanes of a warp sweep near-equal pair counts (P2P_TSORT=0 disables)
-        hp.lean = d.layout == P2P_LAYOUT_TILED && !hp.ws && hp.tpi == 1 && hp.ns == 1 && !hp.pad;
+        hp.lean = d.layout == P2P_LAYOUT_TILED && hp.tpi == 1 && hp.ns == 1 && !hp.pad;
         hp.tsort = hp.lean;
-        if (const char *v = std::getenv("P2P_TSORT")) hp.tsort = hp.lean && std::atoi(v) != 0;
+        if (hp.nt == 32 && !hp.lean) hp.nt = 64;  // one-warp CTAs: lean instances only
+        // lean fp32: ~4 targets per thread measured best (tools/gpu_prof5.sh): one-warp CTAs for small tiles
+        if (hp.lean && d.precision == P2P_FP32 && !std::getenv("P2P_NT") &&
+            (double)hp.n_tgt / (double)std::max<size_t>(hp.tiles_g.size(), 1) < 192.0)
+            hp.nt = 32;
+        if (const char *v = std::getenv("P2P_TSORT")) hp.tsort = hp.ns == 1 && std::atoi(v) != 0;
         // flattened row-runs pay below ~3 sources per box (more index work per pair,
         // fewer idle lanes) and always in fp64 (the log dwarfs the index work); above,
         // row loops (P2P_FLAT overrides)
         hp.flat = hp.lean && (hp.density_occ < 3.0 || d.precision == P2P_FP64);
         if (const char *v = std::getenv("P2P_FLAT")) hp.flat = hp.lean && std::atoi(v) != 0;
+        {
+            const auto &tc = d.layout == P2P_LAYOUT_TILED && hp.tpi == 2 ? tcount2 : tcount;
+            hp.tgt_cap = pad8(tc.empty() ? 0 : *std::max_element(tc.begin(), tc.end()));
+        }
         if (d.layout == P2P_LAYOUT_TILED && !hp.pad) {  // unpadded region sizes
             int64_t mx = 0;
             for (int64_t i = 0; i < nt; ++i) {
@@ -323,8 +325,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         const int sc = (int)std::min<int64_t>(hp.src_cap, 1 << 24), tc = (int)std::min<int64_t>(hp.tgt_cap, 1 << 24);
         int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? (int64_t)nr_carve(k, sc, tc, e, hp.tpi).total
                        : d.layout == P2P_LAYOUT_TILED
-                           ? (hp.ws ? (int64_t)ws_carve(k, sc, tc, e, hp.tpi, hp.nbuf).total
-                                    : (int64_t)tiled_carve(k, sc, tc, e, hp.tpi, hp.ns, hp.nbuf).total)
+                           ? (int64_t)tiled_carve(k, sc, tc, e, hp.tpi, hp.ns, hp.nbuf).total
                                                            : (int64_t)r_carve(k, sc, tc, e).total;
         hp.smem_bytes = smem;
         if (smem <= kSmemLimit) break;
@@ -549,8 +550,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     hp.tile_slot.resize((size_t)nlt);
     std::iota(hp.tile_slot.begin(), hp.tile_slot.end(), 0);
     if (d.layout == P2P_LAYOUT_TILED) {
-        const bool short_table = !hp.ws && hp.tpi == 1 && hp.ns == 1;
-        const int ts = tiled_table_stride(k, short_table);
+        const int ts = tiled_table_stride(k);
         hp.reg_off.assign((size_t)nlt + 1, 0);
         hp.reg_table.assign((size_t)nlt * ts, 0);
         for (int64_t i = 0; i < nlt; ++i) {  // sizes and tables
@@ -607,63 +607,65 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                 }
             }
         }, 64);
-        // targets, packed per tile (8-entry aligned for the bulk copy): coordinates
-        // relative to the region origin + tile-local box index; target box starts
-        // go after the region box starts in the tile's table record
+        // target slots, packed per tile (8-entry aligned for the bulk copy): the
+        // tile's target boxes in Morton order (NS = 1 plans: by descending n9, so
+        // the lanes of a warp sweep near-equal pair counts), each box's targets in
+        // plan order; TPI = 2: units = consecutive slot pairs of one box, odd boxes
+        // end with a duplicate slot (output index 0xFFFF).  Per slot: coordinates
+        // relative to the region origin, row-run base j0 = by*R + bx, output index.
+        const int tpi = hp.tpi;
+        auto box_slots = [&](int64_t b) {
+            const int64_t c = hp.tgt_off[b + 1] - hp.tgt_off[b];
+            return tpi == 2 ? c + (c & 1) : c;
+        };
         hp.tgt_pack_off.assign((size_t)nlt + 1, 0);
         hp.tile_tgt_base.assign((size_t)nlt, 0);
         for (int64_t i = 0; i < nlt; ++i) {
             const int64_t m0 = (int64_t)hp.tiles[i] * WW;
-            const int64_t n = hp.tgt_off[m0 + WW] - hp.tgt_off[m0];
-            if (n > 65535) fail(P2P_ERROR_NOT_SUPPORTED, "TILED tile exceeds 65535 targets; use NR");
+            int64_t n = 0;
+            for (int64_t bl = 0; bl < WW; ++bl) n += box_slots(m0 + bl);
+            if (n > (hp.ns == 3 ? 16383 * tpi : 65534))
+                fail(P2P_ERROR_NOT_SUPPORTED, "TILED tile exceeds its target-slot limit; use a deeper level or NR");
             hp.tile_tgt_base[i] = hp.tgt_off[m0];
             hp.tgt_pack_off[i + 1] = hp.tgt_pack_off[i] + (uint32_t)pad8(n);
-            if (short_table)
-                hp.reg_table[i * ts + R * R + 1] = (uint16_t)n;
-            else
-                for (int64_t bl = 0; bl <= WW; ++bl)
-                    hp.reg_table[i * ts + R * R + 1 + bl] = (uint16_t)(hp.tgt_off[m0 + bl] - hp.tgt_off[m0]);
+            hp.reg_table[i * ts + R * R + 1] = (uint16_t)n;
         }
         const int64_t np = hp.tgt_pack_off[nlt];
         hp.tgt_bl.assign((size_t)np, 0);
-        if (hp.lean) hp.tgt_oix.assign((size_t)np, 0);
+        hp.tgt_oix.assign((size_t)np, 0xFFFF);
         if (f32) hp.f32.tgt_ruv.assign((size_t)np * 2, 0.f);
         else hp.f64.tgt_ruv.assign((size_t)np * 2, 0.0);
         const double *txy = d.tgt_xy;
         parallel_for(nlt, [&](int64_t a, int64_t bnd) {
-            std::vector<int32_t> order, key;
+            std::vector<int32_t> order;
             for (int64_t i = a; i < bnd; ++i) {
                 const uint32_t t = (uint32_t)hp.tiles[i];
                 uint32_t tx, ty;
                 morton_decode(t, tx, ty);
                 const double ox = ((int64_t)tx * W - 1) * hp.h, oy = ((int64_t)ty * W - 1) * hp.h;
-                const int64_t m0 = (int64_t)t * WW, g0 = hp.tgt_off[m0], n = hp.tgt_off[m0 + WW] - g0;
-                // packed position of the tile's k-th target (plan order): identity, or
-                // stable order of descending n9 of the target's box
-                order.resize((size_t)n);
+                const int64_t m0 = (int64_t)t * WW, g0 = hp.tgt_off[m0];
+                order.resize((size_t)WW);
                 std::iota(order.begin(), order.end(), 0);
-                if (hp.tsort) {
-                    key.resize((size_t)n);
-                    for (int64_t bl = 0; bl < WW; ++bl)
-                        for (int32_t g = hp.tgt_off[m0 + bl]; g < hp.tgt_off[m0 + bl + 1]; ++g)
-                            key[(size_t)(g - g0)] = n9[(size_t)(m0 + bl)];
-                    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return key[x] > key[y]; });
-                }
-                for (int64_t kk = 0; kk < n; ++kk) {
-                    const int64_t g = g0 + order[(size_t)kk], j = hp.tgt_pack_off[i] + kk, u = hp.tgt_uidx[g];
-                    // tile-local box -> row-run base j0 = by * R + bx in the region
-                    const uint32_t bl = (uint32_t)(std::upper_bound(hp.tgt_off.begin() + m0, hp.tgt_off.begin() + m0 + WW + 1,
-                                                                    (int32_t)g) - (hp.tgt_off.begin() + m0) - 1);
+                if (hp.tsort)
+                    std::stable_sort(order.begin(), order.end(),
+                                     [&](int32_t x, int32_t y) { return n9[(size_t)(m0 + x)] > n9[(size_t)(m0 + y)]; });
+                int64_t j = hp.tgt_pack_off[i];
+                for (int32_t bl : order) {
+                    const int64_t b = m0 + bl, ns_b = box_slots(b);
                     uint32_t bx, by;
-                    morton_decode(bl, bx, by);
-                    hp.tgt_bl[j] = (uint16_t)(by * R + bx);
-                    if (hp.lean) hp.tgt_oix[j] = (uint16_t)(g - g0);
-                    if (f32) {
-                        hp.f32.tgt_ruv[2 * j] = (float)(txy[2 * u] - ox);
-                        hp.f32.tgt_ruv[2 * j + 1] = (float)(txy[2 * u + 1] - oy);
-                    } else {
-                        hp.f64.tgt_ruv[2 * j] = txy[2 * u] - ox;
-                        hp.f64.tgt_ruv[2 * j + 1] = txy[2 * u + 1] - oy;
+                    morton_decode((uint32_t)bl, bx, by);
+                    for (int64_t x = 0; x < ns_b; ++x, ++j) {
+                        const int64_t g = std::min<int64_t>(hp.tgt_off[b] + x, hp.tgt_off[b + 1] - 1);
+                        const int64_t u = hp.tgt_uidx[g];
+                        hp.tgt_bl[j] = (uint16_t)(by * R + bx);
+                        if (hp.tgt_off[b] + x < hp.tgt_off[b + 1]) hp.tgt_oix[j] = (uint16_t)(g - g0);
+                        if (f32) {
+                            hp.f32.tgt_ruv[2 * j] = (float)(txy[2 * u] - ox);
+                            hp.f32.tgt_ruv[2 * j + 1] = (float)(txy[2 * u + 1] - oy);
+                        } else {
+                            hp.f64.tgt_ruv[2 * j] = txy[2 * u] - ox;
+                            hp.f64.tgt_ruv[2 * j + 1] = txy[2 * u + 1] - oy;
+                        }
                     }
                 }
             }
@@ -697,7 +699,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     // ranges so the final wave is fine-grained (each target is still computed
     // whole by one thread: results do not depend on the split).
     hp.tile_part.assign(hp.tiles.size(), 1 << 16);
-    if (d.layout == P2P_LAYOUT_TILED && !hp.ws) {
+    if (d.layout == P2P_LAYOUT_TILED) {
         int64_t tail = 148 * 4, parts = 4;
         if (const char *v = std::getenv("P2P_TAIL_TILES")) tail = std::atoll(v);
         if (const char *v = std::getenv("P2P_TAIL_PARTS")) parts = std::max(1, std::min(16, std::atoi(v)));
@@ -716,6 +718,39 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             hp.tile_slot.swap(s2);
             hp.tile_part.swap(p2);
         }
+    }
+    // ---- NS = 3 item lists (TILED): per tile, the (unit, row-run) items of each
+    // part's unit range [nu*ip/np, nu*(ip+1)/np) sorted by row-run length
+    // (descending, stable), so the lanes of a warp sweep near-equal runs.
+    if (d.layout == P2P_LAYOUT_TILED && hp.ns == 3) {
+        const int ts = tiled_table_stride(k), tpi = hp.tpi;
+        std::vector<int32_t> nparts((size_t)nlt, 1);
+        for (size_t li = 0; li < hp.tile_slot.size(); ++li) nparts[hp.tile_slot[li]] = hp.tile_part[li] >> 16;
+        hp.item_off.assign((size_t)nlt + 1, 0);
+        for (int64_t i = 0; i < nlt; ++i)
+            hp.item_off[i + 1] = hp.item_off[i] + (uint32_t)pad8(3 * (hp.reg_table[i * ts + R * R + 1] / tpi));
+        hp.items.assign(hp.item_off[nlt], 0);
+        parallel_for(nlt, [&](int64_t a, int64_t bnd) {
+            std::vector<int32_t> len, ord;
+            for (int64_t i = a; i < bnd; ++i) {
+                const uint16_t *tab = &hp.reg_table[i * ts];
+                const int64_t nu = tab[R * R + 1] / tpi, tb = hp.tgt_pack_off[i], np_ = nparts[i];
+                len.assign((size_t)(3 * nu), 0);
+                for (int64_t u = 0; u < nu; ++u)
+                    for (int row = 0; row < 3; ++row) {
+                        const int64_t j0 = hp.tgt_bl[tb + tpi * u] + row * R;
+                        len[3 * u + row] = tab[j0 + 3] - tab[j0];
+                    }
+                for (int64_t ip = 0; ip < np_; ++ip) {
+                    const int64_t ub = nu * ip / np_, ue = nu * (ip + 1) / np_;
+                    ord.resize((size_t)(3 * (ue - ub)));
+                    std::iota(ord.begin(), ord.end(), (int32_t)(3 * ub));
+                    std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return len[x] > len[y]; });
+                    for (size_t q = 0; q < ord.size(); ++q)
+                        hp.items[hp.item_off[i] + 3 * ub + q] = (uint16_t)((ord[q] / 3) << 2 | (ord[q] % 3));
+                }
+            }
+        }, 64);
     }
     hp.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
