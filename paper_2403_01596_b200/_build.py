@@ -39,10 +39,10 @@ def stale(lib: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _nvcc(sources: list[str], out: str, log: str, verbose: bool):
+def _nvcc(sources: list[str], out: str, log: str, verbose: bool, extra: tuple[str, ...] = ()):
     os.makedirs(LIBDIR, exist_ok=True)
     tmp = out + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, *sources, "-o", tmp, "-lpthread"]
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, *sources, "-o", tmp, "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
@@ -65,5 +65,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """A/B experiments: the operator library built with extra -D defines as lib/libp2p_b200_<name>.so
+    (load it with P2P_LIB=<path>)."""
+    out = os.path.join(LIBDIR, f"libp2p_b200_{name}.so")
+    _nvcc([os.path.join(CSRC, s) for s in SOURCES], out, f"ptxas_v_{name}.log", False,
+          tuple("-D" + d for d in defines))
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+    if len(sys.argv) > 2 and sys.argv[1] == "variant":  # python _build.py variant NAME DEF=1 ...
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        print(build(force=True, verbose=True))

@@ -679,8 +679,11 @@ p2p_r_kernel(const P2PArgs<T> a) {
 //   by n9, the three runs optionally flattened into one sequence).
 // Every target's sum has a fixed order independent of the launch, the tile
 // split and the partition: results are bit-reproducible.
+#ifndef P2P_DENSE_MINB
+#define P2P_DENSE_MINB 0  // > 0: register cap via min resident CTAs for the TPI = 2 instances (experiments)
+#endif
 template <typename T, int TPI, int NT, bool PAD, int NS>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, (TPI == 2 && P2P_DENSE_MINB > 0) ? P2P_DENSE_MINB : 0)
 p2p_tiled_kernel(const P2PArgs<T> a) {
     static_assert(TPI == 1 || (TPI == 2 && PAD && sizeof(T) == 4), "TPI = 2 is the padded fp32 path");
     static_assert(!PAD || sizeof(T) == 4, "the padded layout is fp32");
