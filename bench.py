@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--layout", default="tiled", choices=["nr", "r", "tiled"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--kind", default="iid", choices=["iid", "stratified"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = each config's plate widened N x (same points per box, N x the "
+                         "points, per-GPU work fixed), Morton-range sharded with the halo exchange; "
+                         "strong = the same global problem split N ways")
     ap.add_argument("--no-extras", action="store_true", help="skip the R / fp64 detail lines")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
@@ -218,9 +222,11 @@ def main():
     # ---- plans (host build + upload; not timed)
     from paper_2403_01596_b200.dist import DistributedP2P
     jobs = []
+    weak = world > 1 and args.scaling == "weak"
     for name in names:
-        cfg = W.CONFIGS[name]
+        cfg = W.widened(W.CONFIGS[name], world) if weak else W.CONFIGS[name]
         src, tgt, q = W.make_problem(cfg, kind=args.kind)
+        name = cfg.name
         kw = dict(level=cfg.level, layout=args.layout, precision=args.precision, tile_log2=args.tile)
         if world == 1:
             pl = p2p.Plan(src, tgt, device=local, **kw)
@@ -296,7 +302,7 @@ def main():
     alg_bytes = sum(j["info"]["alg_bytes_kernel"] for j in jobs)
     t_mufu = sum(j["info"]["pairs"] / (peak_mufu * 1e9) for j in jobs)
     t_hbm = sum(j["info"]["alg_bytes_kernel"] / (peak_hbm * 1e9) for j in jobs)
-    traffic = _ncu_traffic(args, names)
+    traffic = _ncu_traffic(args, [j["name"] for j in jobs]) if world == 1 else None
     if t_mufu >= t_hbm:
         achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak_mufu, "unit": "Gpair/s (1 MUFU.LG2 per pair)",
@@ -328,9 +334,10 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "pair-interactions/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (seeded SplitMix64 plates shaped like the paper's PEC plate, SURVEY.md §8(d))",
-        "config": {"workload": args.workload, "configs": names, "layout": args.layout,
+        "config": {"workload": args.workload + (f" x{world} (plates widened, weak scaling)" if weak else ""),
+                   "configs": [j["cfg"].name for j in jobs], "layout": args.layout,
                    "precision": args.precision, "kind": args.kind, "pairs_per_step": pairs_step,
                    "order": "plan", "l2": "flushed (256 MiB write) between timed steps",
                    "parallelism": f"morton-range x{world}" + (
@@ -369,6 +376,44 @@ def _owned_user_indices(pl, src, part, rank):
     return owned
 
 
+def _e2e_dist(args, jobs, stream, pairs_step, barrier):
+    """N > 1: each rank's public-API step from host memory: H2D of its owned weights (pinned),
+    halo exchange + distributed apply (DistributedP2P.apply), D2H of its potentials; time = max
+    over ranks."""
+    import torch
+    import torch.distributed as dist
+    hq = [j["q_owned"].cpu().pin_memory() for j in jobs]
+    ho = [torch.empty_like(j["out"], device="cpu").pin_memory() for j in jobs]
+    dq = [torch.empty_like(j["q_owned"]) for j in jobs]
+    h2d = sum(int(t.numel() * t.element_size()) for t in hq)
+    d2h = sum(int(t.numel() * t.element_size()) for t in ho)
+
+    def step():
+        for j, a, d, b in zip(jobs, hq, dq, ho):
+            d.copy_(a, non_blocking=True)
+            j["dp"].apply(d, j["out"], stream=stream.cuda_stream)
+            b.copy_(j["out"], non_blocking=True)
+
+    for _ in range(3):
+        step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": pairs_step / (ms * 1e-3), "unit": "pair-interactions/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "path": "per rank: pinned H2D of owned weights, DistributedP2P.apply (halo exchange + "
+                    "p2p_apply_dist), D2H of local potentials; max over ranks"}
+
+
 def _ncu_traffic(args, names):
     """dram bytes per launch of the P2P kernel from the committed ncu --set full summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -389,7 +434,7 @@ def _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier):
     import torch
     from paper_2403_01596_b200 import p2p
     if world > 1:
-        return None
+        return _e2e_dist(args, jobs, stream, pairs_step, barrier)
     hq = [torch.as_tensor(j["q_user"], dtype=j["plan"].torch_dtype).pin_memory() for j in jobs]
     ho = [torch.empty(j["info"]["n_tgt"], dtype=j["plan"].torch_dtype).pin_memory() for j in jobs]
     h2d = sum(int(t.numel() * t.element_size()) for t in hq)

@@ -91,6 +91,26 @@ CONFIGS: dict[str, PlateConfig] = {
 }
 
 
+MAX_LEVEL = 15  # the plan builder's level cap (R16)
+
+
+def widened(cfg: PlateConfig, factor: int) -> PlateConfig:
+    """The plate ``factor`` times longer (same points per box, ``factor`` x the points):
+    the weak-scaling problem for ``factor`` GPUs.  The leaf level rises only if the
+    wider plate no longer fits the grid (boxes stay boxes: D is unchanged)."""
+    if factor == 1:
+        return cfg
+    sx, sy = cfg.sx, cfg.sy
+    if sx <= sy:
+        sx *= factor
+    else:
+        sy *= factor
+    level = max(cfg.level, int(np.ceil(np.log2(max(sx, sy)))) + 1)
+    if level > MAX_LEVEL:
+        raise ValueError(f"{cfg.name} x{factor}: a {sx}x{sy} plate needs level {level} > {MAX_LEVEL}")
+    return PlateConfig(f"{cfg.name}_x{factor}", sx, sy, level, cfg.n * factor, cfg.seed)
+
+
 def _below(limit: float, x: np.ndarray) -> np.ndarray:
     """Clamp x strictly below ``limit`` (guards against round-up at the plate edge)."""
     return np.minimum(x, np.nextafter(limit, 0.0))
