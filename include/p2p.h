@@ -190,8 +190,16 @@ typedef struct {
     int64_t device_bytes;        /* device memory held by the plan */
     double build_seconds;        /* host plan build */
     double upload_seconds;       /* host -> device upload */
+    int32_t cta_threads;         /* threads per CTA of the P2P kernel */
+    int32_t slots_per_unit;      /* TILED: target slots per work unit (2: dense fp32 pairs of one box) */
+    int32_t items_per_unit;      /* TILED: 3 = one item per row-run (sorted item list), 1 = whole unit */
+    int32_t flags;               /* TILED: bit 0 n9-ordered boxes, bit 1 flattened row-runs */
 } p2p_plan_info;
 
+/* Plan statistics.  Versioning: a caller compiled against an older (smaller)
+ * p2p_plan_info sets info->struct_size = sizeof(its struct) and receives that
+ * prefix only; struct_size = 0 (or >= the current size) means the current
+ * layout.  On return struct_size holds the number of bytes written. */
 p2p_status p2p_plan_get_info(p2p_plan plan, p2p_plan_info *info);
 
 typedef enum {
@@ -208,7 +216,15 @@ typedef enum {
     P2P_EXPORT_SEND_INDEX = 10,     /* int64[n_send]: owned-local index of each sent weight */
     P2P_EXPORT_HALO_OFFSETS = 11,   /* int64[boxes+1]: R layout, packed-halo offsets per Morton box */
     P2P_EXPORT_REGION_OFFSETS = 12, /* int64[tiles+1]: TILED layout, packed-region offsets per tile (Morton tile order) */
-    P2P_EXPORT_REGION_INDEX = 13    /* int64[entries]: TILED layout, local source of each packed entry (-1 = pad) */
+    P2P_EXPORT_REGION_INDEX = 13,   /* int64[entries]: TILED layout, local source of each packed entry (-1 = pad) */
+    P2P_EXPORT_REGION_TABLE = 14,   /* int64[tiles*stride]: TILED, per tile its region box starts then its slot count */
+    P2P_EXPORT_SLOT_OFFSETS = 15,   /* int64[tiles+1]: TILED, target-slot offsets per tile (Morton tile order) */
+    P2P_EXPORT_SLOT_BASE = 16,      /* int64[slots]: TILED, row-run base j0 = by*(W+2) + bx of each slot */
+    P2P_EXPORT_SLOT_OUTPUT = 17,    /* int64[slots]: TILED, tile-local output index of each slot (-1 = duplicate) */
+    P2P_EXPORT_ITEM_OFFSETS = 18,   /* int64[tiles+1]: TILED NS = 3 plans, item-list offsets per tile */
+    P2P_EXPORT_ITEMS = 19,          /* int64[items]: TILED NS = 3 plans, unit << 2 | row in kernel order */
+    P2P_EXPORT_LAUNCH = 20          /* int64[2*launches]: TILED, Morton-order slot of each queue entry, then its
+                                       part | nparts << 16 */
 } p2p_export_kind;
 
 /* Copy a plan array to host memory.  If host_dst is NULL, *bytes receives the

@@ -2,6 +2,7 @@
 // upload, apply dispatch, introspection and export.
 #include <algorithm>
 #include <chrono>
+#include <cstddef>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -460,11 +461,17 @@ p2p_status p2p_destroy(p2p_plan P) {
     return P2P_SUCCESS;
 }
 
-p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *info) {
-    if (!P || !info) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or info");
+p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *out) {
+    if (!P || !out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or info");
+    const uint32_t want = out->struct_size;
+    if (want && want < offsetof(p2p_plan_info, level))
+        return set_error(P2P_ERROR_INVALID_ARGUMENT, "p2p_plan_info.struct_size too small");
+    const size_t n = want && want < sizeof(p2p_plan_info) ? want : sizeof(p2p_plan_info);
     const p2p::HostPlan &hp = P->hp;
+    p2p_plan_info full;
+    p2p_plan_info *info = &full;
     std::memset(info, 0, sizeof(*info));
-    info->struct_size = sizeof(p2p_plan_info);
+    info->struct_size = (uint32_t)n;
     info->level = hp.L;
     info->tile_log2 = hp.k;
     info->layout = hp.layout;
@@ -511,6 +518,11 @@ p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *info) {
     info->device_bytes = P->device_bytes;
     info->build_seconds = hp.build_seconds;
     info->upload_seconds = P->upload_seconds;
+    info->cta_threads = hp.layout == P2P_LAYOUT_TILED ? hp.nt : p2p::kThreads;
+    info->slots_per_unit = hp.tpi;
+    info->items_per_unit = hp.layout == P2P_LAYOUT_TILED ? hp.ns : 3;
+    info->flags = (hp.tsort ? 1 : 0) | (hp.flat ? 2 : 0);
+    std::memcpy(out, info, n);
     return P2P_SUCCESS;
 }
 
@@ -541,6 +553,19 @@ p2p_status p2p_plan_export(p2p_plan P, int32_t kind, void *host_dst, size_t *byt
         case P2P_EXPORT_HALO_OFFSETS: take(hp.halo_off); break;
         case P2P_EXPORT_REGION_OFFSETS: take(hp.reg_off); break;
         case P2P_EXPORT_REGION_INDEX: take(hp.reg_idx); break;
+        case P2P_EXPORT_REGION_TABLE: take(hp.reg_table); break;
+        case P2P_EXPORT_SLOT_OFFSETS: take(hp.tgt_pack_off); break;
+        case P2P_EXPORT_SLOT_BASE: take(hp.tgt_bl); break;
+        case P2P_EXPORT_SLOT_OUTPUT:
+            take(hp.tgt_oix);
+            for (int64_t &x : v) x = x == 0xFFFF ? -1 : x;
+            break;
+        case P2P_EXPORT_ITEM_OFFSETS: take(hp.item_off); break;
+        case P2P_EXPORT_ITEMS: take(hp.items); break;
+        case P2P_EXPORT_LAUNCH:
+            take(hp.tile_slot);
+            v.insert(v.end(), hp.tile_part.begin(), hp.tile_part.end());
+            break;
         default: throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "unknown export kind");
         }
         const size_t need = v.size() * sizeof(int64_t);

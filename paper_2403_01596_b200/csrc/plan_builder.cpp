@@ -128,6 +128,49 @@ void csr_sort(const double *xy, int64_t n, const HostPlan &hp, std::vector<int32
     for (int64_t i = 0; i < n; ++i) perm[pos[code[i]]++] = (int32_t)i;
 }
 
+// Item layout for the kernel's mapping (position p -> round p / nt, warp (p % nt) / 32,
+// lane p % 32) from items sorted by descending length: 32-item batches (sorted, so the
+// lanes of a batch sweep near-equal runs) are dealt to warps longest-processing-time
+// first, so every warp of the CTA reaches the tile's barrier at about the same time.
+// The partial batch (if any) takes the one partial slot, which the mapping gives to
+// the last position's warp.
+void balance_batches(const std::vector<int32_t> &ord, const std::vector<int32_t> &len, int nt,
+                     std::vector<int32_t> &lay) {
+    const int64_t n = (int64_t)ord.size(), nw = nt / 32;
+    lay.assign(ord.begin(), ord.end());
+    if (n <= 32 || nw <= 1) return;
+    const int64_t nb = (n + 31) / 32;  // batches; the last one may be partial
+    // slots: position blocks of 32 in kernel order; slot s covers positions [32 s, 32 s + 32)
+    std::vector<int64_t> load((size_t)nw, 0);
+    std::vector<std::vector<int64_t>> slots((size_t)nw);
+    for (int64_t sl = 0; sl < nb; ++sl) slots[(size_t)((sl * 32 % nt) / 32)].push_back(sl);
+    std::vector<int64_t> free_full((size_t)nw, 0);
+    const bool partial = n % 32 != 0;
+    for (int64_t w = 0; w < nw; ++w)
+        for (int64_t sl : slots[(size_t)w]) free_full[(size_t)w] += !(partial && sl == nb - 1);
+    std::vector<int64_t> slot_of_batch((size_t)nb, -1);
+    if (partial) {  // the partial batch (the shortest items) fills the partial slot
+        const int64_t w = ((nb - 1) * 32 % nt) / 32;
+        slot_of_batch[(size_t)(nb - 1)] = nb - 1;
+        load[(size_t)w] += len[(size_t)ord[(size_t)((nb - 1) * 32)]];
+    }
+    std::vector<size_t> next((size_t)nw, 0);
+    for (int64_t b = 0; b < nb - (partial ? 1 : 0); ++b) {  // batch b: items [32 b, 32 b + 32), longest first
+        int64_t best = -1;
+        for (int64_t w = 0; w < nw; ++w)
+            if (free_full[(size_t)w] > 0 && (best < 0 || load[(size_t)w] < load[(size_t)best])) best = w;
+        // the batch's duration ~ its longest item (lanes run in lockstep)
+        load[(size_t)best] += len[(size_t)ord[(size_t)(32 * b)]];
+        --free_full[(size_t)best];
+        while (partial && slots[(size_t)best][next[(size_t)best]] == nb - 1) ++next[(size_t)best];
+        slot_of_batch[(size_t)b] = slots[(size_t)best][next[(size_t)best]++];
+    }
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t sl = slot_of_batch[(size_t)b];
+        for (int64_t x = 0; x < 32 && 32 * b + x < n; ++x) lay[(size_t)(32 * sl + x)] = ord[(size_t)(32 * b + x)];
+    }
+}
+
 }  // namespace
 
 void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
@@ -730,8 +773,11 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         for (int64_t i = 0; i < nlt; ++i)
             hp.item_off[i + 1] = hp.item_off[i] + (uint32_t)pad8(3 * (hp.reg_table[i * ts + R * R + 1] / tpi));
         hp.items.assign(hp.item_off[nlt], 0);
+        const int nt = hp.nt;
+        bool balance = true;  // P2P_BALANCE=0: items in plain length order (A/B)
+        if (const char *v = std::getenv("P2P_BALANCE")) balance = std::atoi(v) != 0;
         parallel_for(nlt, [&](int64_t a, int64_t bnd) {
-            std::vector<int32_t> len, ord;
+            std::vector<int32_t> len, ord, lay;
             for (int64_t i = a; i < bnd; ++i) {
                 const uint16_t *tab = &hp.reg_table[i * ts];
                 const int64_t nu = tab[R * R + 1] / tpi, tb = hp.tgt_pack_off[i], np_ = nparts[i];
@@ -746,8 +792,10 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                     ord.resize((size_t)(3 * (ue - ub)));
                     std::iota(ord.begin(), ord.end(), (int32_t)(3 * ub));
                     std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return len[x] > len[y]; });
-                    for (size_t q = 0; q < ord.size(); ++q)
-                        hp.items[hp.item_off[i] + 3 * ub + q] = (uint16_t)((ord[q] / 3) << 2 | (ord[q] % 3));
+                    if (balance) balance_batches(ord, len, nt, lay);
+                    else lay = ord;
+                    for (size_t q = 0; q < lay.size(); ++q)
+                        hp.items[hp.item_off[i] + 3 * ub + q] = (uint16_t)((lay[q] / 3) << 2 | (lay[q] % 3));
                 }
             }
         }, 64);

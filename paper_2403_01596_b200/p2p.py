@@ -41,6 +41,8 @@ EXPORT = {
     "src_perm": 0, "tgt_perm": 1, "src_box_offsets": 2, "tgt_box_offsets": 3,
     "neighbors": 4, "partition": 5, "src_global": 6, "halo_counts": 7, "tiles": 8,
     "halo_index": 9, "send_index": 10, "halo_offsets": 11, "region_offsets": 12, "region_index": 13,
+    "region_table": 14, "slot_offsets": 15, "slot_base": 16, "slot_output": 17, "item_offsets": 18,
+    "items": 19, "launch": 20,
 }
 
 # Symbols declared in include/p2p.h (checked by tests/test_abi.py).
@@ -78,7 +80,8 @@ class PlanInfo(C.Structure):
         ("pairs", C.c_int64), ("pairs_global", C.c_int64), ("tiles", C.c_int64),
         ("smem_bytes", C.c_int64), ("halo_entries", C.c_int64), ("alg_bytes_kernel", C.c_int64),
         ("layout_bytes_apply", C.c_int64), ("device_bytes", C.c_int64), ("build_seconds", C.c_double),
-        ("upload_seconds", C.c_double),
+        ("upload_seconds", C.c_double), ("cta_threads", C.c_int32), ("slots_per_unit", C.c_int32),
+        ("items_per_unit", C.c_int32), ("flags", C.c_int32),
     ]
 
 

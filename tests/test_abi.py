@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 from paper_2403_01596_b200 import p2p
+from paper_2403_01596_b200 import workloads as W
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -77,3 +78,19 @@ def test_host_only_plan_refuses_apply():
 
 def test_destroy_null_is_noop():
     p2p.p2p_destroy(None)
+
+
+def test_plan_info_struct_size_prefix():
+    """A caller with an older, smaller p2p_plan_info gets only its prefix (include/p2p.h)."""
+    src, tgt, _ = W.make_problem("tiny")
+    with p2p.Plan(src, tgt, level=4, device=-1) as h:
+        lib = p2p.load_library()
+        cut = p2p.PlanInfo.cta_threads.offset
+        buf = (C.c_uint8 * C.sizeof(p2p.PlanInfo))(*([0xAB] * C.sizeof(p2p.PlanInfo)))
+        info = p2p.PlanInfo.from_buffer(buf)
+        info.struct_size = cut
+        assert lib.p2p_plan_get_info(h.handle, C.byref(info)) == 0
+        assert info.struct_size == cut and info.level == 4
+        assert bytes(buf[cut:]) == bytes([0xAB] * (C.sizeof(p2p.PlanInfo) - cut))
+        info.struct_size = 2  # smaller than the struct_size field itself: rejected
+        assert lib.p2p_plan_get_info(h.handle, C.byref(info)) == p2p.P2P_ERROR_INVALID_ARGUMENT

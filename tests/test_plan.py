@@ -168,3 +168,65 @@ def test_tiled_region_interaction_set():
             bs = np.minimum(np.floor(src * S), S - 1)
             inside = (bs[:, 0] >= x0) & (bs[:, 0] <= x0 + W_ + 1) & (bs[:, 1] >= y0) & (bs[:, 1] <= y0 + W_ + 1)
             assert set(got.tolist()) == set(np.nonzero(inside)[0].tolist())
+
+
+def _tiled_layout_checks(pl, level, nt):
+    """Invariants of the TILED target slots and item lists (plan builder, host only)."""
+    k = pl.info["tile_log2"]
+    W_, WW = 1 << k, 1 << (2 * k)
+    R, RR = W_ + 2, (W_ + 2) ** 2
+    stride = (RR + 2 + 7) & ~7
+    tiles = np.unique(pl.export("tiles"))  # Morton slot order
+    soff, sbase, sout = pl.export("slot_offsets"), pl.export("slot_base"), pl.export("slot_output")
+    table = pl.export("region_table").reshape(len(tiles), stride)
+    toff = pl.export("tgt_box_offsets")
+    ioff, items = pl.export("item_offsets"), pl.export("items")
+    launch = pl.export("launch").reshape(2, -1)
+    nparts = {int(s): int(p) >> 16 for s, p in zip(launch[0], launch[1])}
+    assert np.all(soff % 8 == 0)
+    tpi = pl.info["slots_per_unit"]
+    assert (len(items) > 0) == (pl.info["items_per_unit"] == 3)
+    for i, t in enumerate(tiles):
+        nslot = int(table[i, RR + 1])
+        assert soff[i] + nslot <= soff[i + 1]
+        o, b = sout[soff[i]:soff[i] + nslot], sbase[soff[i]:soff[i] + nslot]
+        g0, n = toff[t * WW], toff[(t + 1) * WW] - toff[t * WW]
+        real = o[o >= 0]
+        assert np.array_equal(np.sort(real), np.arange(n))           # every target exactly once
+        for x, j0 in zip(o, b):                                          # row-run base = the target's box
+            if x < 0:
+                continue
+            box = np.searchsorted(toff, g0 + x, side="right") - 1
+            bx, by = oracle.morton_decode(int(box - t * WW), k + 1)  # level k + 1: k bits per axis
+            assert j0 == by * R + bx
+        if tpi == 2:                                                     # units: 2 slots of one box
+            assert nslot % 2 == 0 and np.all(b[0::2] == b[1::2]) and np.all(o[0::2] >= 0)
+        else:
+            assert np.all(o >= 0)
+        if len(items) == 0:
+            continue
+        nu = nslot // tpi
+        it = items[ioff[i]:ioff[i] + 3 * nu]
+        np_ = nparts[i]
+        for ip in range(np_):
+            ub, ue = nu * ip // np_, nu * (ip + 1) // np_
+            part = it[3 * ub:3 * ue]
+            assert sorted(part.tolist()) == sorted(u << 2 | r for u in range(ub, ue) for r in range(3))
+            # balanced batches: every warp's summed batch maxima within one batch of the others
+            j0 = b[tpi * (part >> 2)] + (part & 3) * R
+            ln = table[i, j0 + 3].astype(np.int64) - table[i, j0]
+            loads = np.zeros(nt // 32, dtype=np.int64)
+            for s in range(0, len(part), 32):
+                loads[(s % nt) // 32] += ln[s:s + 32].max()
+            if len(part) > nt:
+                assert loads.max() - loads.min() <= ln.max()
+
+
+@pytest.mark.parametrize("level,precision", [(4, "fp32"), (5, "fp32"), (6, "fp32"), (4, "fp64"), (6, "fp64")])
+def test_tiled_slots_and_items(level, precision):
+    src, tgt, _ = W.make_problem(W.widened(W.CONFIGS["tiny"], 4))
+    level += 1  # the widened tiny plate needs one more level
+    for tile in (-1, 0, 1, 2):
+        pl = _plan(src, tgt, level=level, layout="tiled", precision=precision, tile_log2=tile)
+        _tiled_layout_checks(pl, level, pl.info["cta_threads"])
+        pl.close()
