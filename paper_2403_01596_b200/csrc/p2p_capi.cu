@@ -45,7 +45,7 @@ struct p2p_plan_s {
     // device arrays
     DevBuf tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
-    DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, tgt_ruv, tgt_pack_off, tile_tgt_base;
+    DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, log_tab, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     int grid = 0;                                // persistent CTAs per launch
     unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
@@ -70,7 +70,7 @@ struct p2p_plan_s {
     void release() {
         DevBuf *all[] = {&tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
-                         &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &tgt_ruv,
+                         &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi,
                          &io_q, &io_out, &queue};
         for (DevBuf *b : all) {
@@ -126,6 +126,7 @@ void upload_plan(p2p_plan_s &P) {
     P.upload(P.tgt_uv, lay.tgt_uv);
     P.upload(P.tgt_uidx, hp.tgt_uidx);
     P.upload(P.src_uidx, hp.src_uidx);
+    P.upload(P.log_tab, hp.log_tab);  // fp64 plans
     if (hp.part_world > 1) {
         P.upload(P.src_gidx, hp.src_gidx);
         P.upload(P.src_qidx, hp.src_qidx);
@@ -198,6 +199,7 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
     a.S = hp.S;
     a.h = (T)hp.h;
     a.eps2 = (T)(hp.eps * hp.eps);
+    a.log_tab = (const double2 *)P.log_tab.p;
     a.src_cap = (int)hp.src_cap;
     a.tgt_cap = (int)hp.tgt_cap;
     a.group_log2 = hp.group_log2;

@@ -162,15 +162,36 @@ __device__ __noinline__ float span1_f32_guarded(const float2 *__restrict__ UV, c
     }
     return acc;
 }
+// fp64 log, table-driven (libdevice's log is ~30 DP ops; this is ~11): x = m 2^e, m in [1, 2);
+// k = top 7 mantissa bits; LT[k] = (c_inv, -log c_inv) with c_inv ~ 1 / (1 + (k + 1/2)/128) (host,
+// plan_builder.cpp); t = m c_inv - 1 (one fma, |t| < 2^-8); log1p(t) to degree 6 (truncation
+// < 2e-18); log x = e ln2 + (-log c_inv) + log1p(t).  x must be a positive normal double.
+constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
+__device__ __forceinline__ double log_tab(double x, const double2 *__restrict__ LT) {
+    const long long b = __double_as_longlong(x);
+    const int e = (int)(b >> 52) - 1023;
+    const double2 c = LT[(int)(b >> 45) & 127];
+    const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+    const double t = fma(m, c.x, -1.0);
+    double q = fma(t, -1.0 / 6.0, 0.2);
+    q = fma(t, q, -0.25);
+    q = fma(t, q, 1.0 / 3.0);
+    q = fma(t, q, -0.5);
+    const double p = fma(t * t, q, t);
+    const double de = (double)e;
+    return fma(de, kLn2Hi, c.y) + fma(de, kLn2Lo, p);
+}
+
 // fp64, (u, v) per entry, explicit guard.
 __device__ __forceinline__ double span1_f64(const double2 *__restrict__ UV, const double *__restrict__ Q, int j0,
-                                            int j1, double ut, double vt, double eps2) {
+                                            int j1, double ut, double vt, double eps2,
+                                            const double2 *__restrict__ LT) {
     double acc = 0.0;
     for (int j = j0; j < j1; ++j) {
         const double2 s = UV[j];
         const double du = ut - s.x, dv = vt - s.y;
         const double r2 = fma(dv, dv, du * du);
-        if (r2 >= eps2) acc = fma(Q[j], log(r2), acc);
+        if (r2 >= eps2) acc = fma(Q[j], log_tab(r2, LT), acc);
     }
     return acc;
 }
@@ -199,7 +220,8 @@ __device__ __forceinline__ float span3_f32(const float2 *__restrict__ UV, const 
     return acc;
 }
 __device__ __forceinline__ double span3_f64(const double2 *__restrict__ UV, const double *__restrict__ Q,
-                                            const Runs3 &r, double ut, double vt, double eps2) {
+                                            const Runs3 &r, double ut, double vt, double eps2,
+                                            const double2 *__restrict__ LT) {
     double acc = 0.0;
     const int v1 = r.v0 + r.n;
     for (int v = r.v0; v < v1; ++v) {
@@ -207,7 +229,7 @@ __device__ __forceinline__ double span3_f64(const double2 *__restrict__ UV, cons
         const double2 s = UV[j];
         const double du = ut - s.x, dv = vt - s.y;
         const double r2 = fma(dv, dv, du * du);
-        if (r2 >= eps2) acc = fma(Q[j], log(r2), acc);
+        if (r2 >= eps2) acc = fma(Q[j], log_tab(r2, LT), acc);
     }
     return acc;
 }
@@ -231,13 +253,13 @@ __device__ __noinline__ float span_f32_guarded(const float4 *__restrict__ A, con
 // fp64: SoA u, v, q; returns sum q * log(r^2) over non-guarded pairs.
 __device__ __forceinline__ double span_f64(const double *__restrict__ su, const double *__restrict__ sv,
                                            const double *__restrict__ sq, int j0, int j1, double ut,
-                                           double vt, double eps2) {
+                                           double vt, double eps2, const double2 *__restrict__ LT) {
     double acc = 0.0;
 #pragma unroll 2
     for (int j = j0; j < j1; ++j) {
         const double du = ut - su[j], dv = vt - sv[j];
         const double r2 = fma(dv, dv, du * du);
-        if (r2 >= eps2) acc = fma(sq[j], log(r2), acc);
+        if (r2 >= eps2) acc = fma(sq[j], log_tab(r2, LT), acc);
     }
     return acc;
 }
@@ -273,6 +295,7 @@ struct P2PArgs {
     const uint16_t *tgt_oix;    // TILED: per target slot, tile-local output index (0xFFFF: duplicate slot)
     const uint32_t *item_off;   // TILED NS = 3: [slots+1] item-list offsets
     const uint16_t *items;      // TILED NS = 3: unit << 2 | row, length-sorted per part
+    const double2 *log_tab;     // fp64 TILED: kLogTab x (c_inv, -log c_inv) for log_tab()
     const T *tgt_ruv;           // TILED: packed targets' coordinates relative to the region origin
     const uint32_t *tgt_pack_off;   // TILED: [slots+1] packed-target offsets (multiples of 8)
     const int32_t *tile_tgt_base;   // TILED: plan index of each tile's first target
@@ -365,6 +388,9 @@ p2p_nr_kernel(const P2PArgs<T> a) {
     __shared__ int s_tile, s_units;
     const int k = a.k, W = 1 << k, R = W + 2, RR = R * R, WW = W * W;
     const NrCarve c = nr_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI);
+    double2 *s_lt = reinterpret_cast<double2 *>(smem + c.ltab);
+    if constexpr (sizeof(T) == 8)  // visible after next_tile()'s barrier
+        for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_lt[i] = a.log_tab[i];
     int *sstart = reinterpret_cast<int *>(smem + c.sstart);
     int *gstart = reinterpret_cast<int *>(smem + c.gstart);
     int *cnt = reinterpret_cast<int *>(smem + c.cnt);
@@ -504,7 +530,7 @@ p2p_nr_kernel(const P2PArgs<T> a) {
             } else {
                 const int t = ut[u];
                 const double *su = reinterpret_cast<const double *>(src);
-                pp[0] = span_f64(su, su + a.src_cap, su + 2 * a.src_cap, i0, i1, tu[t], tv[t], a.eps2);
+                pp[0] = span_f64(su, su + a.src_cap, su + 2 * a.src_cap, i0, i1, tu[t], tv[t], a.eps2, s_lt);
             }
         }
         __syncthreads();
@@ -553,6 +579,9 @@ p2p_r_kernel(const P2PArgs<T> a) {
     __shared__ int s_tile;
     const int k = a.k, W = 1 << k, WW = W * W;
     const RCarve c = r_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T));
+    double2 *s_lt = reinterpret_cast<double2 *>(smem + c.ltab);
+    if constexpr (sizeof(T) == 8)  // visible after the first tile's barrier
+        for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) s_lt[i] = a.log_tab[i];
     int *toff = reinterpret_cast<int *>(smem + c.toff);
     int *hoff = reinterpret_cast<int *>(smem + c.hoff);
     int *tbx = reinterpret_cast<int *>(smem + c.tbx);
@@ -635,7 +664,7 @@ p2p_r_kernel(const P2PArgs<T> a) {
                 for (int j = 2 * q0; j < 2 * q1; ++j) {
                     const double du = tu[t] - su[2 * j], dv = tv[t] - su[2 * j + 1];
                     const double r2 = fma(dv, dv, du * du);
-                    if (r2 >= a.eps2) acc = fma(s_q[j], log(r2), acc);
+                    if (r2 >= a.eps2) acc = fma(s_q[j], log_tab(r2, s_lt), acc);
                 }
                 part[it] = acc;
             }
@@ -696,8 +725,11 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
     const bool db = a.nbuf == 2;
     T *s_q = reinterpret_cast<T *>(smem + c.q);
     T *part = reinterpret_cast<T *>(smem + c.part);
+    double2 *s_lt = reinterpret_cast<double2 *>(smem + c.ltab);
     uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + c.bar);
     const int tid = threadIdx.x;
+    if constexpr (sizeof(T) == 8)
+        for (int i = tid; i < kLogTab; i += NT) s_lt[i] = a.log_tab[i];
 
     auto issue = [&](int ti, int b) {  // one elected thread: arm buffer b and bulk-copy tile ti's record
         const int slot = a.tile_slot[ti];
@@ -811,7 +843,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                                    i1, tuv[2 * t0], tuv[2 * t0 + 1]);
             } else {
                 res[0] = span1_f64(reinterpret_cast<const double2 *>(s_uv), reinterpret_cast<const double *>(s_q), i0,
-                                   i1, tuv[2 * t0], tuv[2 * t0 + 1], a.eps2);
+                                   i1, tuv[2 * t0], tuv[2 * t0 + 1], a.eps2, s_lt);
             }
         };
         // final value of slot t from its row-ordered sum (fp32: guarded redo if non-finite),
@@ -855,7 +887,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                                         runs, ux, uy);
                     else
                         acc = span3_f64(reinterpret_cast<const double2 *>(s_uv),
-                                        reinterpret_cast<const double *>(s_q), runs, ux, uy, a.eps2);
+                                        reinterpret_cast<const double *>(s_q), runs, ux, uy, a.eps2, s_lt);
                 } else {
 #pragma unroll
                     for (int row = 0; row < 3; ++row) {
@@ -866,7 +898,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                         else
                             acc += span1_f64(reinterpret_cast<const double2 *>(s_uv),
                                              reinterpret_cast<const double *>(s_q), table[j0], table[j0 + 3], ux, uy,
-                                             a.eps2);
+                                             a.eps2, s_lt);
                     }
                 }
                 finish(t, acc);

@@ -21,9 +21,10 @@ namespace p2p {
 // ---- shared-memory layouts of the P2P kernels (byte offsets), used by the
 // plan builder (sizing), the launcher and the kernels (carving).
 P2P_HD inline int align16(int x) { return (x + 15) & ~15; }
+constexpr int kLogTab = 128;  // fp64 log: table of (1/c_k rounded, -log of it), c_k = 1 + (k + 1/2) / 128
 
 struct NrCarve {
-    int sstart, gstart, cnt, toff, pstart, uj0, ut, tslot, tu, tv, part, src, total, ucap;
+    int sstart, gstart, cnt, toff, pstart, uj0, ut, tslot, tu, tv, part, src, ltab, total, ucap;
 };
 // NR layout.  src_cap: max padded region sources of a tile (multiple of 4);
 // tgt_cap: max targets of a tile (multiple of 4); tpi: targets per work unit
@@ -48,12 +49,13 @@ P2P_HD inline NrCarve nr_carve(int k, int src_cap, int tgt_cap, int e, int tpi) 
     c.tv = align16(c.tu + e * tgt_cap);
     c.part = align16(c.tv + e * tgt_cap);
     c.src = align16(c.part + 3 * e * tpi * c.ucap);
-    c.total = c.src + 3 * e * src_cap;
+    c.ltab = align16(c.src + 3 * e * src_cap);  // fp64: the log table
+    c.total = c.ltab + (e == 8 ? 16 * kLogTab : 0);
     return c;
 }
 
 struct RCarve {
-    int toff, hoff, tbx, tu, tv, part, bar, src, total;
+    int toff, hoff, tbx, tu, tv, part, bar, src, ltab, total;
 };
 // src_cap: max packed-halo entries of a tile (multiple of 4).
 P2P_HD inline RCarve r_carve(int k, int src_cap, int tgt_cap, int e) {
@@ -67,14 +69,15 @@ P2P_HD inline RCarve r_carve(int k, int src_cap, int tgt_cap, int e) {
     c.part = align16(c.tv + e * tgt_cap);
     c.bar = align16(c.part + 3 * e * tgt_cap);
     c.src = align16(c.bar + 16);
-    c.total = c.src + 3 * e * src_cap;
+    c.ltab = align16(c.src + 3 * e * src_cap);  // fp64: the log table
+    c.total = c.ltab + (e == 8 ? 16 * kLogTab : 0);
     return c;
 }
 
 struct TCarve {
     int buf0, bufsz;                            // NBUF bulk-copied buffers of bufsz bytes from buf0
     int table, uv, idx, tuv, tbl, oix, items;   // offsets inside one buffer
-    int q, part, bar, total, tstride, icap;
+    int q, part, ltab, bar, total, tstride, icap;
 };
 // TILED layout.  Per tile record: table (region box starts + slot count), region
 // entries (coordinates, source index), target slots (coordinates, row-run base,
@@ -103,7 +106,8 @@ P2P_HD inline TCarve tiled_carve(int k, int src_cap, int slot_cap, int e, int tp
     c.buf0 = 0;
     c.q = nbuf * c.bufsz;
     c.part = align16(c.q + e * src_cap);  // NS = 3: three partial sums per slot
-    c.bar = align16(c.part + (ns == 3 ? 3 * e * slot_cap : 0));
+    c.ltab = align16(c.part + (ns == 3 ? 3 * e * slot_cap : 0));  // fp64: the log table (kLogTab entries)
+    c.bar = align16(c.ltab + (e == 8 ? 16 * kLogTab : 0));
     c.total = c.bar + 16;
     return c;
 }
@@ -204,6 +208,7 @@ struct HostPlan {
     bool lean = false;                            // TILED lean kernel path (tpi 1, ns 1, unpadded)
     bool tsort = false;                           // ns 1: target boxes of a tile ordered by n9 (descending)
     bool flat = false;                            // lean path: row-runs swept as one sequence (sparse)
+    std::vector<double> log_tab;                  // fp64: kLogTab x (c_inv, -log c_inv) for the table-driven log
     std::vector<int32_t> tile_slot;               // launch order -> slot
     std::vector<int32_t> tile_part;               // launch order -> part | nparts << 16 (tail splitting)
     int64_t reg_entries = 0;

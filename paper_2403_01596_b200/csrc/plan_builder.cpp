@@ -309,10 +309,14 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         // TILED defaults: dense fp32 -> padded pairs, 2 targets per unit, (unit, row) items;
         // sparse or fp64 -> unpadded, one item per target; 128-thread CTAs.
         hp.pad = d.layout == P2P_LAYOUT_TILED ? (hp.tpi == 2) : true;
-        hp.ns = hp.tpi > 1 ? 3 : 1;
+        // fp64 dense boxes: (target, row-run) items too (sorted), 256-thread CTAs (tools/gpu_ab11.sh)
+        const bool dense64 = d.precision == P2P_FP64 && hp.density_occ >= 8.0;
+        hp.ns = hp.tpi > 1 || dense64 ? 3 : 1;
         hp.nbuf = 1;
-        // measured best (tools/gpu_ab*.sh): 128 threads for dense units and fp64, 64 for sparse fp32
-        hp.nt = d.layout == P2P_LAYOUT_TILED ? (hp.tpi > 1 || d.precision == P2P_FP64 ? 128 : 64) : kThreads;
+        // measured best (tools/gpu_ab*.sh): 128 threads for dense fp32 units and sparse fp64,
+        // 256 for dense fp64, 64 (or 32, below) for sparse fp32
+        hp.nt = d.layout == P2P_LAYOUT_TILED
+                    ? (dense64 ? 256 : hp.tpi > 1 || d.precision == P2P_FP64 ? 128 : 64) : kThreads;
         // tuning hooks (experiments only): P2P_TPI, P2P_NS, P2P_NBUF, P2P_PAD, P2P_NT
         if (const char *v = std::getenv("P2P_TPI"))
             if (d.precision == P2P_FP32 && d.layout != P2P_LAYOUT_REDUNDANT) {
@@ -760,6 +764,18 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             hp.tiles.swap(t2);
             hp.tile_slot.swap(s2);
             hp.tile_part.swap(p2);
+        }
+    }
+    // ---- fp64 log table: log x = e ln2 + L_k + log1p(t), t = m c_inv_k - 1, |t| < 2^-8, with
+    // c_inv_k = 1 / (1 + (k + 1/2) / 128) rounded to double and L_k = -log(c_inv_k) from the
+    // 64-bit-mantissa long double log (the kernel's `log_tab`)
+    if (d.precision == P2P_FP64) {
+        hp.log_tab.resize(2 * kLogTab);
+        for (int kk = 0; kk < kLogTab; ++kk) {
+            const double c = 1.0 + (kk + 0.5) / kLogTab;
+            const double cinv = 1.0 / c;
+            hp.log_tab[2 * kk] = cinv;
+            hp.log_tab[2 * kk + 1] = (double)(-logl((long double)cinv));
         }
     }
     // ---- NS = 3 item lists (TILED): per tile, the (unit, row-run) items of each
