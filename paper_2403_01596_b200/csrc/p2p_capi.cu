@@ -45,7 +45,7 @@ struct p2p_plan_s {
     // device arrays
     DevBuf tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
-    DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, log_tab, tgt_ruv, tgt_pack_off, tile_tgt_base;
+    DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uidx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, log_tab, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     int grid = 0;                                // persistent CTAs per launch
     unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
@@ -70,7 +70,7 @@ struct p2p_plan_s {
     void release() {
         DevBuf *all[] = {&tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
-                         &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
+                         &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uidx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi,
                          &io_q, &io_out, &queue};
         for (DevBuf *b : all) {
@@ -140,6 +140,7 @@ void upload_plan(p2p_plan_s &P) {
         P.upload(P.tile_part, hp.tile_part);
         P.upload(P.reg_off, hp.reg_off);
         P.upload(P.reg_idx, hp.reg_idx);
+        P.upload(P.reg_uidx, hp.reg_uidx);
         P.upload(P.reg_uv, lay.reg_uv);
         P.upload(P.reg_table, hp.reg_table);
         P.upload(P.tgt_bl, hp.tgt_bl);
@@ -187,7 +188,7 @@ int grid_for(int64_t n) {
 
 // The P2P kernel proper on q_local (local plan order) -> out (local plan order).
 template <typename T>
-void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStream_t s) {
+void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStream_t s, bool user = false) {
     const p2p::HostPlan &hp = P.hp;
     const int ntiles = (int)hp.tiles.size();
     if (ntiles == 0) return;
@@ -221,7 +222,10 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.tile_slot = (const int32_t *)P.tile_slot.p;
         a.tile_part = (const int32_t *)P.tile_part.p;
         a.reg_off = (const uint32_t *)P.reg_off.p;
-        a.reg_idx = (const int32_t *)P.reg_idx.p;
+        // ORDER_USER (TILED): weights gathered through the entries' user indices and results written
+        // through the targets' user indices, inside the kernel (no permutation kernels)
+        a.reg_idx = (const int32_t *)(user ? P.reg_uidx.p : P.reg_idx.p);
+        a.out_idx = user ? (const int32_t *)P.tgt_uidx.p : nullptr;
         a.reg_uv = (const T *)P.reg_uv.p;
         a.reg_table = (const uint16_t *)P.reg_table.p;
         a.tgt_bl = (const uint16_t *)P.tgt_bl.p;
@@ -254,6 +258,11 @@ template <typename T>
 void apply_impl(p2p_plan_s &P, const void *d_q, void *d_out, int order, int accumulate, cudaStream_t s) {
     const p2p::HostPlan &hp = P.hp;
     const T *q_local = (const T *)d_q;
+    if (order == P2P_ORDER_USER && hp.layout == P2P_LAYOUT_TILED) {  // permutations fused into the kernel
+        launch_p2p<T>(P, (const T *)d_q, (T *)d_out, accumulate, s, true);
+        ck(cudaGetLastError(), "apply launch");
+        return;
+    }
     if (order == P2P_ORDER_USER) {
         if (hp.n_src_local)
             p2p::dev::gather_kernel<T><<<grid_for(hp.n_src_local), 256, 0, s>>>(

@@ -295,7 +295,8 @@ struct P2PArgs {
     const uint16_t *tgt_oix;    // TILED: per target slot, tile-local output index (0xFFFF: duplicate slot)
     const uint32_t *item_off;   // TILED NS = 3: [slots+1] item-list offsets
     const uint16_t *items;      // TILED NS = 3: unit << 2 | row, length-sorted per part
-    const double2 *log_tab;     // fp64 TILED: kLogTab x (c_inv, -log c_inv) for log_tab()
+    const double2 *log_tab;     // fp64: kLogTab x (c_inv, -log c_inv) for log_tab()
+    const int32_t *out_idx;     // TILED: output position of each local target (ORDER_USER), or nullptr
     const T *tgt_ruv;           // TILED: packed targets' coordinates relative to the region origin
     const uint32_t *tgt_pack_off;   // TILED: [slots+1] packed-target offsets (multiples of 8)
     const int32_t *tile_tgt_base;   // TILED: plan index of each tile's first target
@@ -871,7 +872,8 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             } else {
                 acc = -0.5 * acc;
             }
-            a.out[tb + o] = a.accumulate ? a.out[tb + o] + acc : acc;
+            const int oi = a.out_idx ? a.out_idx[tb + o] : tb + o;
+            a.out[oi] = a.accumulate ? a.out[oi] + acc : acc;
         };
 
         if constexpr (LEAN) {  // one thread per target (boxes by n9): three row-runs, flattened or in turn

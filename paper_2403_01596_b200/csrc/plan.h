@@ -194,6 +194,7 @@ struct HostPlan {
     // ---- TILED layout (per tile in Morton order = "slot")
     std::vector<uint32_t> reg_off;                // [tiles+1] packed-region offsets
     std::vector<int32_t> reg_idx;                 // local source index, -1 = pad
+    std::vector<int32_t> reg_uidx;                // user (original) source index, -1 = pad: ORDER_USER applies
     std::vector<uint16_t> reg_table;              // [tiles][tstride] region box starts, then the slot count
     std::vector<uint16_t> tgt_bl;                 // per target slot: row-run base j0 = by * R + bx
     std::vector<uint16_t> tgt_oix;                // per target slot: tile-local output index (0xFFFF: duplicate)

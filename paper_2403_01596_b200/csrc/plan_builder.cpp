@@ -619,6 +619,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         }
         hp.reg_entries = hp.reg_off[nlt];
         hp.reg_idx.assign((size_t)hp.reg_entries, -1);
+        hp.reg_uidx.assign((size_t)hp.reg_entries, -1);
         const double PADC = 1.0e4;
         const bool f32 = d.precision == P2P_FP32;
         if (f32) hp.f32.reg_uv.assign((size_t)hp.reg_entries * 2, (float)PADC);
@@ -639,6 +640,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                         const int64_t u = hp.src_uidx[sj];
                         const double rx = sxy[2 * u] - ox, ry = sxy[2 * u + 1] - oy;
                         hp.reg_idx[ent] = sj;
+                        hp.reg_uidx[ent] = (int32_t)u;
                         if (f32 && hp.pad) {  // (u0,u1,v0,v1) per source pair
                             const int64_t p = ent >> 1, sl = ent & 1;
                             hp.f32.reg_uv[4 * p + sl] = (float)rx;
