@@ -723,11 +723,13 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
 
     // ---- queue order of this partition's tiles: when the working set fits
     // comfortably in L2, longest tiles first (LPT) to shorten the tail; else
-    // Morton order, so concurrently running CTAs share their halo rings in L2.
+    // Morton order, so concurrently running CTAs share their halo rings in L2
+    // (and the tail is split instead, below).
     {
         const int64_t ws = (hp.n_src_local + hp.n_tgt_local) * 3 * (int64_t)e + 8 * hp.boxes_in_tiles +
                            (hp.halo_entries + hp.reg_entries) * 3 * (int64_t)e;
-        hp.lpt = ws < (int64_t)48 << 20;
+        hp.lpt = ws < (int64_t)100 << 20;  // L2 = 126 MB; measured (tools/gpu_ab12.sh)
+        if (const char *v = std::getenv("P2P_LPT")) hp.lpt = std::atoi(v) != 0;  // tuning hook
         if (hp.lpt) {
             const int64_t base = hp.part_tile[r];
             std::vector<int64_t> order(hp.tiles.size());
@@ -749,7 +751,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     // whole by one thread: results do not depend on the split).
     hp.tile_part.assign(hp.tiles.size(), 1 << 16);
     if (d.layout == P2P_LAYOUT_TILED) {
-        int64_t tail = 148 * 4, parts = 4;
+        int64_t tail = hp.lpt ? 0 : 148 * 4, parts = 4;  // LPT already ends on the short tiles
         if (const char *v = std::getenv("P2P_TAIL_TILES")) tail = std::atoll(v);
         if (const char *v = std::getenv("P2P_TAIL_PARTS")) parts = std::max(1, std::min(16, std::atoi(v)));
         tail = std::min<int64_t>(tail, (int64_t)hp.tiles.size() / 2);

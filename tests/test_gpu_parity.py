@@ -191,3 +191,21 @@ def test_full_size_sampled(cfg, layout, prec):
         rng = np.random.default_rng(0)
         sample = np.sort(rng.choice(len(tgt), 3000, replace=False))
         check(pl, src, tgt, q, c.level, targets_plan=sample)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("level", [5, 7])
+def test_tail_split_bit_identical(prec, level, monkeypatch):
+    """Tail tiles split into unit ranges (forced: the plan's default splits only Morton-ordered
+    queues) give bit-identical results to the unsplit plan, and match the oracle."""
+    src, tgt, q = W.make_problem(W.widened(W.CONFIGS["tiny"], 4))
+    with p2p.Plan(src, tgt, level=level, layout="tiled", precision=prec) as pl:
+        base = gpu_apply(pl, q)
+    for tiles, parts in ((4, 3), (1000, 5)):
+        monkeypatch.setenv("P2P_TAIL_TILES", str(tiles))
+        monkeypatch.setenv("P2P_TAIL_PARTS", str(parts))
+        with p2p.Plan(src, tgt, level=level, layout="tiled", precision=prec) as pl:
+            launch = pl.export("launch").reshape(2, -1)
+            assert np.any((launch[1] >> 16) == parts)
+            assert np.array_equal(gpu_apply(pl, q), base)
+            check(pl, src, tgt, q, level)

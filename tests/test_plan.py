@@ -222,8 +222,12 @@ def _tiled_layout_checks(pl, level, nt):
                 assert loads.max() - loads.min() <= ln.max()
 
 
+@pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("level,precision", [(4, "fp32"), (5, "fp32"), (6, "fp32"), (4, "fp64"), (6, "fp64")])
-def test_tiled_slots_and_items(level, precision):
+def test_tiled_slots_and_items(level, precision, split, monkeypatch):
+    if split:  # force tail splitting (the default splits only Morton-ordered queues)
+        monkeypatch.setenv("P2P_TAIL_TILES", "1000")
+        monkeypatch.setenv("P2P_TAIL_PARTS", "3")
     src, tgt, _ = W.make_problem(W.widened(W.CONFIGS["tiny"], 4))
     level += 1  # the widened tiny plate needs one more level
     for tile in (-1, 0, 1, 2):

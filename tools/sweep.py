@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--tile", default="-1")
     ap.add_argument("--nt", default="128")
     ap.add_argument("--pad", default="1")
+    ap.add_argument("--lpt", default="", help="P2P_LPT values (comma list; empty = plan default)")
+    ap.add_argument("--tail", default="", help="tail splitting as TILES:PARTS (comma list; empty = default)")
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--json", default="")
     args = ap.parse_args()
@@ -41,9 +43,15 @@ def main():
     for name in args.configs.split(","):
         cfg = W.CONFIGS[name]
         src, tgt, q = W.make_problem(cfg)
-        for tpi, ns, nbuf, tile, nt, pad in itertools.product(args.tpi.split(","), args.ns.split(","),
-                                                              args.nbuf.split(","), args.tile.split(","),
-                                                              args.nt.split(","), args.pad.split(",")):
+        for tpi, ns, nbuf, tile, nt, pad, lpt, tail in itertools.product(
+                args.tpi.split(","), args.ns.split(","), args.nbuf.split(","), args.tile.split(","),
+                args.nt.split(","), args.pad.split(","), args.lpt.split(","), args.tail.split(",")):
+            for key, val in (("P2P_LPT", lpt), ("P2P_TAIL_TILES", tail.split(":")[0] if tail else ""),
+                             ("P2P_TAIL_PARTS", tail.split(":")[1] if tail else "")):
+                if val:
+                    os.environ[key] = val
+                else:
+                    os.environ.pop(key, None)
             if tpi == "2" and pad == "0":
                 continue
             os.environ["P2P_TPI"], os.environ["P2P_NS"], os.environ["P2P_NBUF"] = tpi, ns, nbuf
@@ -69,11 +77,13 @@ def main():
                 ts.append(a.elapsed_time(b))
             ms = float(np.median(ts))
             i = pl.info
-            row = dict(config=name, tpi=tpi, ns=ns, nbuf=nbuf, nt=nt, pad=pad, tile=i["tile_log2"], smem=i["smem_bytes"],
+            row = dict(config=name, tpi=tpi, ns=ns, nbuf=nbuf, nt=nt, pad=pad, lpt=lpt, tail=tail,
+                       tile=i["tile_log2"], smem=i["smem_bytes"],
                        us=ms * 1e3, gpair=i["pairs"] / ms / 1e6, frac=i["pairs"] / (ms * 1e-3) / peak,
                        alg_gbs=i["alg_bytes_kernel"] / ms / 1e6, lay_gbs=i["layout_bytes_apply"] / ms / 1e6)
             rows.append(row)
-            print(f"{name:12s} tpi {tpi} ns {ns} nbuf {nbuf} nt {nt} pad {pad} k {i['tile_log2']} smem {i['smem_bytes']:6d} "
+            print(f"{name:12s} tpi {tpi} ns {ns} nbuf {nbuf} nt {nt} pad {pad} lpt {lpt or '-'} tail {tail or '-'} "
+                  f"k {i['tile_log2']} smem {i['smem_bytes']:6d} "
                   f"{ms * 1e3:8.1f} us {row['gpair']:8.1f} Gpair/s mufu {row['frac']:.3f} alg {row['alg_gbs']:6.0f} layout {row['lay_gbs']:6.0f} GB/s",
                   flush=True)
             pl.close()
