@@ -720,7 +720,9 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
     static_assert(NS == 1 || NS == 3, "one item per unit, or one per row-run");
     constexpr bool LEAN = NS == 1 && TPI == 1 && !PAD;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ int s_next, s_base_next;
+    // next tile + its first target, double-buffered by iteration parity: thread 0 writes slot
+    // (it + 1) & 1 during iteration it while the others may still read slot it & 1
+    __shared__ int s_next[2], s_base_next[2];
     const int k = a.k, W = 1 << k, R = W + 2, RR = R * R;
     const TCarve c = tiled_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI, NS, a.nbuf);
     const bool db = a.nbuf == 2;
@@ -768,14 +770,14 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(mbar + 1)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const int t0 = atomicAdd(a.queue, 1);
-        s_next = t0;
+        s_next[0] = t0;
         if (t0 < a.ntiles) {
-            s_base_next = a.tile_tgt_base[a.tile_slot[t0]];
+            s_base_next[0] = a.tile_tgt_base[a.tile_slot[t0]];
             issue(t0, 0);
         }
     }
     __syncthreads();
-    int cur = s_next, buf = 0, tb = s_base_next;
+    int cur = s_next[0], buf = 0, tb = s_base_next[0], it = 0;
     uint32_t parity = 0u;  // bit b = phase parity of buffer b's mbarrier
 
     while (cur < a.ntiles) {
@@ -794,9 +796,9 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         const uint16_t *items = reinterpret_cast<const uint16_t *>(B + c.items);
         if (tid == 0) {  // next tile; with two buffers its record streams in while this tile computes
             const int nx = atomicAdd(a.queue, 1);
-            s_next = nx;
+            s_next[(it + 1) & 1] = nx;
             if (nx < a.ntiles) {
-                s_base_next = a.tile_tgt_base[a.tile_slot[nx]];
+                s_base_next[(it + 1) & 1] = a.tile_tgt_base[a.tile_slot[nx]];
                 if (db) issue(nx, buf ^ 1);
             }
         }
@@ -937,8 +939,9 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         }
         __syncthreads();  // buffer `buf` and the work arrays are free; s_next / s_base_next visible
         if (trc) trc[5] = gtimer();
-        cur = s_next;
-        tb = s_base_next;
+        ++it;
+        cur = s_next[it & 1];
+        tb = s_base_next[it & 1];
         if (db) buf ^= 1;
         else if (tid == 0 && cur < a.ntiles) issue(cur, 0);
     }

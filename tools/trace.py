@@ -14,6 +14,7 @@ from paper_2403_01596_b200 import workloads as W  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="d16_1e6")
 ap.add_argument("--layout", default="tiled")
+ap.add_argument("--flush", action="store_true", help="flush L2 (256 MiB write) right before the traced apply")
 args = ap.parse_args()
 lib = p2p.load_library()
 lib.p2p_internal_set_trace.argtypes = [C.c_void_p, C.c_void_p]
@@ -29,6 +30,8 @@ for name in args.configs.split(","):
         pl.apply(qd, out)
     lib.p2p_internal_set_trace(pl.handle, C.c_void_p(tr.data_ptr()))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if args.flush:
+        torch.empty(256 << 20, dtype=torch.uint8, device="cuda").zero_()
     e0.record()
     pl.apply(qd, out)
     e1.record()
@@ -53,6 +56,9 @@ for name in args.configs.split(","):
         busy.append(end[m].max() - claim[m].min())
     busy = np.array(busy)
     print(f"  per-SM active span us: min {busy.min():.1f} mean {busy.mean():.1f} max {busy.max():.1f}")
+    first = np.argsort(claim)[:min(len(claim), 1332)]
+    print(f"  first wave: wait-data mean {np.mean((data - claim)[first]):.2f} us, max {np.max((data - claim)[first]):.2f}; "
+          f"later tiles {np.mean(np.delete(data - claim, first)):.2f} us")
     # concurrency: average number of tiles in flight per SM
     conc = dur.sum() / (len(np.unique(sm)) * end.max())
     print(f"  mean tiles in flight per SM {conc:.2f}; pairs {pl.info['pairs']}, "
