@@ -70,13 +70,30 @@ class DistributedP2P:
             self.dist.all_to_all_single(halo, send, self.recv_splits, self.send_splits, group=self.group)
         return self._halo
 
-    def apply(self, q_owned, out=None, *, accumulate: bool = False, stream=None):
-        """phi for this rank's targets (plan order) from its owned weights (plan order)."""
+    def exchange_async(self, q_owned, comm_stream):
+        """Start the halo exchange on ``comm_stream`` (a torch.cuda.Stream) and return an event
+        the compute stream can wait on: independent problems overlap one's exchange with
+        another's kernel (bench.py's step)."""
+        torch = self.torch
+        with torch.cuda.stream(comm_stream):
+            self.exchange(q_owned, comm_stream.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(comm_stream)
+        return ev
+
+    def apply(self, q_owned, out=None, *, accumulate: bool = False, stream=None, halo_ready=None):
+        """phi for this rank's targets (plan order) from its owned weights (plan order).
+        ``halo_ready``: an event from exchange_async (the exchange is then not repeated)."""
         torch = self.torch
         if out is None:
             out = torch.empty(max(1, self.n_tgt_local), dtype=self.plan.torch_dtype,
                               device=torch.device("cuda", self.device))
-        halo = self.exchange(q_owned, stream)
+        if halo_ready is None:
+            halo = self.exchange(q_owned, stream)
+        else:
+            halo = self._halo
+            cur = torch.cuda.current_stream(self.device) if stream is None else torch.cuda.ExternalStream(stream)
+            cur.wait_event(halo_ready)
         self.plan.apply_dist(q_owned, halo, out, accumulate=accumulate, stream=stream)
         return out
 
