@@ -153,6 +153,19 @@ p2p_status p2p_apply_host_async(p2p_plan plan, const void *h_q, void *h_out, int
 p2p_status p2p_apply_dist(p2p_plan plan, const void *d_q_owned, const void *d_q_halo,
                           void *d_out, int32_t accumulate, void *stream);
 
+/* p2p_apply_dist in two phases, to overlap the halo exchange with work that does
+ * not need it (issue both on the same stream, interior first):
+ *   p2p_apply_dist_interior: stages d_q_owned and runs the TILED tiles whose
+ *     regions hold owned sources only (p2p_plan_info.interior_launches queue
+ *     entries; every tile when part_world = 1; none for NR / R);
+ *   p2p_apply_dist_boundary: stages d_q_halo and runs the remaining tiles.
+ * The caller's exchange of d_q_halo may be in flight during the interior phase;
+ * d_q_owned must stay valid until the boundary phase is enqueued. */
+p2p_status p2p_apply_dist_interior(p2p_plan plan, const void *d_q_owned, void *d_out, int32_t accumulate,
+                                   void *stream);
+p2p_status p2p_apply_dist_boundary(p2p_plan plan, const void *d_q_halo, void *d_out, int32_t accumulate,
+                                   void *stream);
+
 /* Gather this partition's owned weights that the other partitions need into
  * d_send (device, n_send elements), grouped by destination rank ascending,
  * within a destination by global plan index ascending. */
@@ -194,6 +207,8 @@ typedef struct {
     int32_t slots_per_unit;      /* TILED: target slots per work unit (2: dense fp32 pairs of one box) */
     int32_t items_per_unit;      /* TILED: 3 = one item per row-run (sorted item list), 1 = whole unit */
     int32_t flags;               /* TILED: bit 0 n9-ordered boxes, bit 1 flattened row-runs */
+    int64_t interior_launches;   /* TILED: queue entries run by p2p_apply_dist_interior */
+    int64_t launches;            /* queue entries of a full apply (tiles, tail tiles split) */
 } p2p_plan_info;
 
 /* Plan statistics.  Versioning: a caller compiled against an older (smaller)

@@ -43,11 +43,12 @@ struct p2p_plan_s {
     int device = -1;
     cudaStream_t stream = nullptr;
     // device arrays
-    DevBuf tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
+    DevBuf halo_lidx, tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
     DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uidx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, log_tab, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     int grid = 0;                                // persistent CTAs per launch
+    int64_t occ_sms = 1;                         // resident CTAs per SM x SMs (grid cap of a launch)
     unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
     int64_t device_bytes = 0;
     double upload_seconds = 0.0;
@@ -68,7 +69,7 @@ struct p2p_plan_s {
         device_bytes += (int64_t)bytes;
     }
     void release() {
-        DevBuf *all[] = {&tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
+        DevBuf *all[] = {&halo_lidx, &tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
                          &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uidx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi,
@@ -130,6 +131,7 @@ void upload_plan(p2p_plan_s &P) {
     if (hp.part_world > 1) {
         P.upload(P.src_gidx, hp.src_gidx);
         P.upload(P.src_qidx, hp.src_qidx);
+        P.upload(P.halo_lidx, hp.halo_lidx);
         P.upload(P.send_idx, hp.send_idx);
     }
     if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
@@ -170,7 +172,8 @@ void upload_plan(p2p_plan_s &P) {
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, block, (size_t)hp.smem_bytes), "occupancy");
     ck(cudaGetDevice(&dev), "cudaGetDevice");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
-    P.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)hp.tiles.size(), (int64_t)std::max(occ, 1) * sms));
+    P.occ_sms = (int64_t)std::max(occ, 1) * sms;
+    P.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)hp.tiles.size(), P.occ_sms));
     P.alloc(P.queue, 16);
     ck(cudaMemsetAsync(P.queue.p, 0, 16, P.stream), "queue init");  // kernels reset it on exit
     ck(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
@@ -188,10 +191,16 @@ int grid_for(int64_t n) {
 
 // The P2P kernel proper on q_local (local plan order) -> out (local plan order).
 template <typename T>
-void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStream_t s, bool user = false) {
+void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStream_t s, bool user = false,
+                int64_t e0 = 0, int64_t e1 = -1) {
     const p2p::HostPlan &hp = P.hp;
-    const int ntiles = (int)hp.tiles.size();
-    if (ntiles == 0) return;
+    // TILED: launch entries [e0, e1) of the queue (interior / boundary phases); NR, R: all tiles
+    if (e1 < 0 || hp.layout != P2P_LAYOUT_TILED) {
+        e0 = 0;
+        e1 = (int64_t)hp.tiles.size();
+    }
+    const int ntiles = (int)(e1 - e0);
+    if (ntiles <= 0) return;
     p2p::dev::P2PArgs<T> a{};
     a.tiles = (const int32_t *)P.tiles.p;
     a.ntiles = ntiles;
@@ -219,8 +228,9 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
             p2p::dev::p2p_nr_kernel<T, 1><<<P.grid, p2p::kThreads, hp.smem_bytes, s>>>(a);
     } else if (hp.layout == P2P_LAYOUT_TILED) {
         a.q = q_local;
-        a.tile_slot = (const int32_t *)P.tile_slot.p;
-        a.tile_part = (const int32_t *)P.tile_part.p;
+        a.tile_slot = (const int32_t *)P.tile_slot.p + e0;
+        a.tile_part = (const int32_t *)P.tile_part.p + e0;
+        a.trace = P.trace ? P.trace + 8 * e0 : nullptr;
         a.reg_off = (const uint32_t *)P.reg_off.p;
         // ORDER_USER (TILED): weights gathered through the entries' user indices and results written
         // through the targets' user indices, inside the kernel (no permutation kernels)
@@ -239,7 +249,8 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.flat = hp.flat ? 1 : 0;
         a.nbuf = hp.nbuf;
         void *args[] = {&a};
-        ck(cudaLaunchKernel(tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns), dim3(P.grid), dim3(hp.nt), args,
+        const int grid = (int)std::min<int64_t>(ntiles, P.occ_sms);
+        ck(cudaLaunchKernel(tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns), dim3(grid), dim3(hp.nt), args,
                             (size_t)hp.smem_bytes, s),
            "tiled launch");
     } else {
@@ -285,16 +296,34 @@ void apply_impl(p2p_plan_s &P, const void *d_q, void *d_out, int order, int accu
     ck(cudaGetLastError(), "apply launch");
 }
 
+// Distributed apply in two phases on one stream: the interior phase needs
+// only the owned weights (copied into the local set's owned range) and runs the TILED tiles
+// whose regions hold owned sources only; the boundary phase scatters the received halo
+// weights into the local set and runs the remaining tiles (NR, R: everything).
 template <typename T>
-void apply_dist_impl(p2p_plan_s &P, const void *d_q_owned, const void *d_q_halo, void *d_out, int accumulate,
-                     cudaStream_t s) {
+void apply_dist_interior_impl(p2p_plan_s &P, const void *d_q_owned, void *d_out, int accumulate, cudaStream_t s) {
     const p2p::HostPlan &hp = P.hp;
-    if (hp.n_src_local)
-        p2p::dev::gather2_kernel<T><<<grid_for(hp.n_src_local), 256, 0, s>>>(
-            (const int32_t *)P.src_qidx.p, (const T *)d_q_owned, (const T *)d_q_halo, hp.n_src_owned,
-            (T *)P.q_local.p, hp.n_src_local);
-    launch_p2p<T>(P, (const T *)P.q_local.p, (T *)d_out, accumulate, s);
-    ck(cudaGetLastError(), "apply_dist launch");
+    if (hp.n_src_owned)
+        ck(cudaMemcpyAsync((T *)P.q_local.p + hp.owned_local_begin, d_q_owned, (size_t)hp.n_src_owned * sizeof(T),
+                           cudaMemcpyDeviceToDevice, s),
+           "owned weights");
+    if (hp.layout == P2P_LAYOUT_TILED)
+        launch_p2p<T>(P, (const T *)P.q_local.p, (T *)d_out, accumulate, s, false, 0, hp.n_interior);
+    ck(cudaGetLastError(), "apply_dist interior launch");
+}
+
+template <typename T>
+void apply_dist_boundary_impl(p2p_plan_s &P, const void *d_q_halo, void *d_out, int accumulate, cudaStream_t s) {
+    const p2p::HostPlan &hp = P.hp;
+    if (hp.n_halo)
+        p2p::dev::scatter_kernel<T><<<grid_for(hp.n_halo), 256, 0, s>>>(
+            (const int32_t *)P.halo_lidx.p, (const T *)d_q_halo, (T *)P.q_local.p, hp.n_halo, 0);
+    if (hp.layout == P2P_LAYOUT_TILED)
+        launch_p2p<T>(P, (const T *)P.q_local.p, (T *)d_out, accumulate, s, false, hp.n_interior,
+                      (int64_t)hp.tiles.size());
+    else
+        launch_p2p<T>(P, (const T *)P.q_local.p, (T *)d_out, accumulate, s);
+    ck(cudaGetLastError(), "apply_dist boundary launch");
 }
 
 struct DeviceGuard {
@@ -428,15 +457,33 @@ p2p_status p2p_apply_host_async(p2p_plan P, const void *h_q, void *h_out, int32_
 
 p2p_status p2p_apply_dist(p2p_plan P, const void *d_q_owned, const void *d_q_halo, void *d_out, int32_t accumulate,
                           void *stream) {
+    p2p_status st = p2p_apply_dist_interior(P, d_q_owned, d_out, accumulate, stream);
+    return st == P2P_SUCCESS ? p2p_apply_dist_boundary(P, d_q_halo, d_out, accumulate, stream) : st;
+}
+
+p2p_status p2p_apply_dist_interior(p2p_plan P, const void *d_q_owned, void *d_out, int32_t accumulate,
+                                   void *stream) {
     if (!P || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or output");
     if (P->hp.n_src_owned && !d_q_owned) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_q_owned");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        if (P->elem == 4) apply_dist_interior_impl<float>(*P, d_q_owned, d_out, accumulate ? 1 : 0, s);
+        else apply_dist_interior_impl<double>(*P, d_q_owned, d_out, accumulate ? 1 : 0, s);
+    });
+}
+
+p2p_status p2p_apply_dist_boundary(p2p_plan P, const void *d_q_halo, void *d_out, int32_t accumulate,
+                                   void *stream) {
+    if (!P || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or output");
     if (P->hp.n_halo && !d_q_halo) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_q_halo");
     return guarded([&] {
         require_device(P);
         DeviceGuard g(P->device);
         cudaStream_t s = (cudaStream_t)stream;
-        if (P->elem == 4) apply_dist_impl<float>(*P, d_q_owned, d_q_halo, d_out, accumulate ? 1 : 0, s);
-        else apply_dist_impl<double>(*P, d_q_owned, d_q_halo, d_out, accumulate ? 1 : 0, s);
+        if (P->elem == 4) apply_dist_boundary_impl<float>(*P, d_q_halo, d_out, accumulate ? 1 : 0, s);
+        else apply_dist_boundary_impl<double>(*P, d_q_halo, d_out, accumulate ? 1 : 0, s);
     });
 }
 
@@ -533,6 +580,8 @@ p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *out) {
     info->slots_per_unit = hp.tpi;
     info->items_per_unit = hp.layout == P2P_LAYOUT_TILED ? hp.ns : 3;
     info->flags = (hp.tsort ? 1 : 0) | (hp.flat ? 2 : 0);
+    info->interior_launches = hp.layout == P2P_LAYOUT_TILED ? hp.n_interior : 0;
+    info->launches = (int64_t)hp.tiles.size();
     std::memcpy(out, info, n);
     return P2P_SUCCESS;
 }

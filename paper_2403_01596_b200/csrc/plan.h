@@ -181,6 +181,9 @@ struct HostPlan {
     std::vector<int32_t> src_uidx;                // local source -> user index
     std::vector<int32_t> tgt_uidx;                // local target -> user index
     std::vector<int32_t> src_qidx;                // local source -> index into [owned | halo]
+    std::vector<int32_t> halo_lidx;               // local index of each halo source, in halo-slot order
+    int64_t owned_local_begin = 0;                // owned sources = local indices [begin, begin + n_src_owned)
+    int64_t n_interior = 0;                       // TILED: launch entries [0, n_interior) read owned sources only
     int64_t n_src_local = 0, n_tgt_local = 0, n_src_owned = 0, n_halo = 0, n_send = 0;
     int64_t src_owned_begin = 0, tgt_begin = 0;
     std::vector<int64_t> recv_counts, send_counts;  // [W]

@@ -480,11 +480,15 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     hp.src_qidx.resize((size_t)hp.n_src_local);
     {
         int64_t halo = 0;
+        hp.halo_lidx.clear();
+        hp.owned_local_begin = std::lower_bound(hp.src_gidx.begin(), hp.src_gidx.end(), (int32_t)hp.part_src[r]) -
+                               hp.src_gidx.begin();  // local order = global order: owned is contiguous
         for (int64_t i = 0; i < hp.n_src_local; ++i) {
             int64_t g = hp.src_gidx[i];
             if (g >= hp.part_src[r] && g < hp.part_src[r + 1]) {
                 hp.src_qidx[i] = (int32_t)(g - hp.part_src[r]);
             } else {
+                hp.halo_lidx.push_back((int32_t)i);
                 int owner = (int)(std::upper_bound(hp.part_src.begin(), hp.part_src.end(), g) - hp.part_src.begin()) - 1;
                 // empty partitions share a begin index; the owner is the last rank starting at or before g
                 hp.recv_counts[owner] += 1;
@@ -746,6 +750,35 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             hp.tile_slot.swap(s2);
         }
     }
+    // ---- interior tiles first (TILED, P > 1): tiles whose regions hold owned sources only can
+    // run before the halo weights arrive (p2p_apply_dist_interior), overlapping the exchange;
+    // the boundary tiles follow (p2p_apply_dist_boundary).  Relative order kept in each class.
+    hp.n_interior = (int64_t)hp.tiles.size();
+    if (d.layout == P2P_LAYOUT_TILED && P > 1) {
+        const int64_t lo = hp.owned_local_begin, hi = hp.owned_local_begin + hp.n_src_owned;
+        std::vector<uint8_t> interior(hp.tiles.size(), 1);
+        for (size_t li = 0; li < hp.tiles.size(); ++li) {
+            const int32_t slot = hp.tile_slot[li];
+            for (uint32_t e = hp.reg_off[slot]; e < hp.reg_off[slot + 1]; ++e) {
+                const int32_t x = hp.reg_idx[e];
+                if (x >= 0 && (x < lo || x >= hi)) {
+                    interior[li] = 0;
+                    break;
+                }
+            }
+        }
+        std::vector<size_t> ord(hp.tiles.size());
+        std::iota(ord.begin(), ord.end(), 0);
+        std::stable_partition(ord.begin(), ord.end(), [&](size_t x) { return interior[x] != 0; });
+        std::vector<int32_t> t2(ord.size()), s2(ord.size());
+        for (size_t i = 0; i < ord.size(); ++i) {
+            t2[i] = hp.tiles[ord[i]];
+            s2[i] = hp.tile_slot[ord[i]];
+        }
+        hp.tiles.swap(t2);
+        hp.tile_slot.swap(s2);
+        hp.n_interior = std::count(interior.begin(), interior.end(), (uint8_t)1);
+    }
     // ---- tail splitting (TILED): the last tiles of the queue are split into unit
     // ranges so the final wave is fine-grained (each target is still computed
     // whole by one thread: results do not depend on the split).
@@ -768,6 +801,8 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             hp.tiles.swap(t2);
             hp.tile_slot.swap(s2);
             hp.tile_part.swap(p2);
+            // interior tiles that fell in the split tail become `parts` launch entries each
+            if (hp.n_interior > (int64_t)keep) hp.n_interior = (int64_t)keep + (hp.n_interior - (int64_t)keep) * parts;
         }
     }
     // ---- fp64 log table: log x = e ln2 + L_k + log1p(t), t = m c_inv_k - 1, |t| < 2^-8, with

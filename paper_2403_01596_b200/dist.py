@@ -70,11 +70,14 @@ class DistributedP2P:
             self.dist.all_to_all_single(halo, send, self.recv_splits, self.send_splits, group=self.group)
         return self._halo
 
-    def exchange_async(self, q_owned, comm_stream):
+    def exchange_async(self, q_owned, comm_stream, after=None):
         """Start the halo exchange on ``comm_stream`` (a torch.cuda.Stream) and return an event
         the compute stream can wait on: independent problems overlap one's exchange with
-        another's kernel (bench.py's step)."""
+        another's kernel (bench.py's step).  ``after``: a stream whose queued work (the previous
+        apply still reading the halo buffer) the exchange must follow."""
         torch = self.torch
+        if after is not None:
+            comm_stream.wait_stream(after)
         with torch.cuda.stream(comm_stream):
             self.exchange(q_owned, comm_stream.cuda_stream)
             ev = torch.cuda.Event()
@@ -83,19 +86,29 @@ class DistributedP2P:
 
     def apply(self, q_owned, out=None, *, accumulate: bool = False, stream=None, halo_ready=None):
         """phi for this rank's targets (plan order) from its owned weights (plan order).
-        ``halo_ready``: an event from exchange_async (the exchange is then not repeated)."""
+        ``halo_ready``: an event from exchange_async (the exchange is then not repeated); the
+        interior tiles run before waiting on it, so the exchange overlaps them."""
         torch = self.torch
         if out is None:
             out = torch.empty(max(1, self.n_tgt_local), dtype=self.plan.torch_dtype,
                               device=torch.device("cuda", self.device))
         if halo_ready is None:
             halo = self.exchange(q_owned, stream)
-        else:
-            halo = self._halo
-            cur = torch.cuda.current_stream(self.device) if stream is None else torch.cuda.ExternalStream(stream)
-            cur.wait_event(halo_ready)
-        self.plan.apply_dist(q_owned, halo, out, accumulate=accumulate, stream=stream)
+            self.plan.apply_dist(q_owned, halo, out, accumulate=accumulate, stream=stream)
+            return out
+        self.plan.apply_dist_interior(q_owned, out, accumulate=accumulate, stream=stream)
+        cur = torch.cuda.current_stream(self.device) if stream is None else torch.cuda.ExternalStream(stream)
+        cur.wait_event(halo_ready)
+        self.plan.apply_dist_boundary(self._halo, out, accumulate=accumulate, stream=stream)
         return out
+
+    def apply_overlapped(self, q_owned, comm_stream, out=None, *, accumulate: bool = False, stream=None):
+        """One problem with its exchange overlapped: exchange on ``comm_stream`` while the
+        interior tiles run on ``stream``; the boundary tiles wait for the halo."""
+        torch = self.torch
+        cur = torch.cuda.current_stream(self.device) if stream is None else torch.cuda.ExternalStream(stream)
+        ev = self.exchange_async(q_owned, comm_stream, after=cur)
+        return self.apply(q_owned, out, accumulate=accumulate, stream=stream, halo_ready=ev)
 
     def gather(self, phi_local):
         """allgatherv (a11): every rank receives phi for all targets in global plan order."""

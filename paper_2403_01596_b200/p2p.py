@@ -48,7 +48,7 @@ EXPORT = {
 # Symbols declared in include/p2p.h (checked by tests/test_abi.py).
 ABI_SYMBOLS = (
     "p2p_plan_desc_init", "p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async",
-    "p2p_apply_dist",
+    "p2p_apply_dist", "p2p_apply_dist_interior", "p2p_apply_dist_boundary",
     "p2p_halo_pack", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
     "p2p_status_string", "p2p_last_error", "p2p_abi_version",
 )
@@ -81,7 +81,8 @@ class PlanInfo(C.Structure):
         ("smem_bytes", C.c_int64), ("halo_entries", C.c_int64), ("alg_bytes_kernel", C.c_int64),
         ("layout_bytes_apply", C.c_int64), ("device_bytes", C.c_int64), ("build_seconds", C.c_double),
         ("upload_seconds", C.c_double), ("cta_threads", C.c_int32), ("slots_per_unit", C.c_int32),
-        ("items_per_unit", C.c_int32), ("flags", C.c_int32),
+        ("items_per_unit", C.c_int32), ("flags", C.c_int32), ("interior_launches", C.c_int64),
+        ("launches", C.c_int64),
     ]
 
 
@@ -110,6 +111,8 @@ def load_library() -> C.CDLL:
     lib.p2p_apply_host.argtypes = [P, P, P, i32, i32, P]
     lib.p2p_apply_host_async.argtypes = [P, P, P, i32, i32, P]
     lib.p2p_apply_dist.argtypes = [P, P, P, P, i32, P]
+    lib.p2p_apply_dist_interior.argtypes = [P, P, P, i32, P]
+    lib.p2p_apply_dist_boundary.argtypes = [P, P, P, i32, P]
     lib.p2p_halo_pack.argtypes = [P, P, P, P]
     lib.p2p_destroy.argtypes = [P]
     lib.p2p_plan_get_info.argtypes = [P, C.POINTER(PlanInfo)]
@@ -118,7 +121,8 @@ def load_library() -> C.CDLL:
     lib.p2p_status_string.restype = C.c_char_p
     lib.p2p_last_error.restype = C.c_char_p
     lib.p2p_abi_version.restype = i32
-    for name in ("p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async", "p2p_apply_dist", "p2p_halo_pack",
+    for name in ("p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async", "p2p_apply_dist", "p2p_apply_dist_interior",
+                 "p2p_apply_dist_boundary", "p2p_halo_pack",
                  "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export"):
         getattr(lib, name).restype = i32
     _lib = lib
@@ -162,6 +166,16 @@ def p2p_apply_host_async(plan, h_q: int, h_out: int, order: int = P2P_ORDER_PLAN
                          stream: int = 0):
     _check(load_library().p2p_apply_host_async(plan, h_q, h_out, order, accumulate, stream or None),
            "p2p_apply_host_async")
+
+
+def p2p_apply_dist_interior(plan, d_q_owned: int, d_out: int, accumulate: int = 0, stream: int = 0):
+    _check(load_library().p2p_apply_dist_interior(plan, d_q_owned or None, d_out, accumulate, stream or None),
+           "p2p_apply_dist_interior")
+
+
+def p2p_apply_dist_boundary(plan, d_q_halo: int, d_out: int, accumulate: int = 0, stream: int = 0):
+    _check(load_library().p2p_apply_dist_boundary(plan, d_q_halo or None, d_out, accumulate, stream or None),
+           "p2p_apply_dist_boundary")
 
 
 def p2p_apply_dist(plan, d_q_owned: int, d_q_halo: int, d_out: int, accumulate: int = 0, stream: int = 0):
@@ -284,6 +298,18 @@ class Plan:
         p2p_apply_dist(self._h, q_owned.data_ptr() if q_owned.numel() else 0,
                        q_halo.data_ptr() if q_halo.numel() else 0, out.data_ptr(), int(accumulate),
                        self._stream(stream))
+        return out
+
+    def apply_dist_interior(self, q_owned, out, *, accumulate: bool = False, stream=None):
+        self._check_tensor(out, self.info["n_tgt_local"], "out")
+        p2p_apply_dist_interior(self._h, q_owned.data_ptr() if q_owned.numel() else 0, out.data_ptr(),
+                                int(accumulate), self._stream(stream))
+        return out
+
+    def apply_dist_boundary(self, q_halo, out, *, accumulate: bool = False, stream=None):
+        self._check_tensor(out, self.info["n_tgt_local"], "out")
+        p2p_apply_dist_boundary(self._h, q_halo.data_ptr() if q_halo.numel() else 0, out.data_ptr(),
+                                int(accumulate), self._stream(stream))
         return out
 
     def halo_pack(self, q_owned, send, stream=None):

@@ -234,3 +234,26 @@ def test_tiled_slots_and_items(level, precision, split, monkeypatch):
         pl = _plan(src, tgt, level=level, layout="tiled", precision=precision, tile_log2=tile)
         _tiled_layout_checks(pl, level, pl.info["cta_threads"])
         pl.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("level", [5, 7])
+def test_interior_launches_read_owned_sources_only(world, level):
+    """Distributed TILED plans put interior tiles first: their regions hold owned sources only
+    (they run before the halo arrives); every boundary tile reads at least one halo source."""
+    src, tgt, _ = W.make_problem(W.widened(W.CONFIGS["tiny"], 4))
+    for r in range(world):
+        pl = _plan(src, tgt, level=level, layout="tiled", part_world=world, part_rank=r)
+        info = pl.info
+        launch = pl.export("launch").reshape(2, -1)
+        roff, ridx = pl.export("region_offsets"), pl.export("region_index")
+        sg = pl.export("src_global")
+        lo, hi = info["src_owned_begin"], info["src_owned_begin"] + info["n_src_owned"]
+        n_int = info["interior_launches"]
+        assert 0 <= n_int <= info["launches"] == launch.shape[1]
+        for e, slot in enumerate(launch[0]):
+            ent = ridx[roff[slot]:roff[slot + 1]]
+            g = sg[ent[ent >= 0]]
+            owned = np.all((g >= lo) & (g < hi))
+            assert owned == (e < n_int), (r, e, n_int)
+        pl.close()
