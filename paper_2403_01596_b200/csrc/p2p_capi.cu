@@ -43,7 +43,7 @@ struct p2p_plan_s {
     int device = -1;
     cudaStream_t stream = nullptr;
     // device arrays
-    DevBuf halo_lidx, tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, src_qidx, send_idx;
+    DevBuf halo_lidx, tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
     DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uidx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, log_tab, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
@@ -70,7 +70,7 @@ struct p2p_plan_s {
     }
     void release() {
         DevBuf *all[] = {&halo_lidx, &tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
-                         &src_qidx, &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
+                         &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
                          &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uidx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi,
                          &io_q, &io_out, &queue};
@@ -130,7 +130,6 @@ void upload_plan(p2p_plan_s &P) {
     P.upload(P.log_tab, hp.log_tab);  // fp64 plans
     if (hp.part_world > 1) {
         P.upload(P.src_gidx, hp.src_gidx);
-        P.upload(P.src_qidx, hp.src_qidx);
         P.upload(P.halo_lidx, hp.halo_lidx);
         P.upload(P.send_idx, hp.send_idx);
     }

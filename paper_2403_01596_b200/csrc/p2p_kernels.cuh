@@ -968,15 +968,6 @@ __global__ void gather_kernel(const int32_t *__restrict__ idx, const T *__restri
 }
 
 // dst[i] = i2 < n_owned ? owned[i2] : halo[i2 - n_owned], i2 = qidx[i]  (distributed import)
-template <typename T>
-__global__ void gather2_kernel(const int32_t *__restrict__ qidx, const T *__restrict__ owned,
-                               const T *__restrict__ halo, int64_t n_owned, T *__restrict__ dst, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = qidx[i];
-        dst[i] = j < n_owned ? owned[j] : halo[j - n_owned];
-    }
-}
-
 // out[idx[i]] (+)= phi[i]  (ORDER_USER export)
 template <typename T>
 __global__ void scatter_kernel(const int32_t *__restrict__ idx, const T *__restrict__ phi, T *__restrict__ out,
