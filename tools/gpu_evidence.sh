@@ -5,7 +5,7 @@ TAG=${TAG:-r01}
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -7
 timeout 1800 python -m pytest tests -q -m gpu 2>&1 | tail -4
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; tail -2 gpurun_out/${TAG}_bench.err
-timeout 900 python bench.py --workload lowdensity_1e7 --no-extras --steps 10 > gpurun_out/${TAG}_bench_lowd.json 2> gpurun_out/${TAG}_bench_lowd.err
+timeout 1500 python bench.py --workload lowdensity_1e7 --steps 10 > gpurun_out/${TAG}_bench_lowd.json 2> gpurun_out/${TAG}_bench_lowd.err
 timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > /dev/null 2>&1
