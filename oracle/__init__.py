@@ -68,6 +68,12 @@ def lib():
         _lib.oracle_ct_level.argtypes = [i64, P, i64, P, i32, i32, i32]
         _lib.oracle_ct_level.restype = i32
         _lib.oracle_pair_count.argtypes = [i64, P, i64, P, i32]
+        _lib.oracle_indexing_bytes.argtypes = [i64, i32, i64]
+        _lib.oracle_indexing_bytes.restype = i64
+        _lib.oracle_repetition_bytes.argtypes = [i64, i64]
+        _lib.oracle_repetition_bytes.restype = i64
+        _lib.oracle_box_tmax.argtypes = [i64, P, i64, P, i32]
+        _lib.oracle_box_tmax.restype = i64
         _lib.oracle_pair_count.restype = i64
         _lib.oracle_num_threads.restype = i32
     return _lib
@@ -147,6 +153,22 @@ def ct_level(src_xy, tgt_xy, ct: int = 15, l_start: int = 3, l_max: int = 16) ->
 def pair_count(src_xy, tgt_xy, level: int) -> int:
     src_xy, tgt_xy = _f64(src_xy), _f64(tgt_xy)
     return int(lib().oracle_pair_count(len(src_xy), _ptr(src_xy), len(tgt_xy), _ptr(tgt_xy), level))
+
+
+def indexing_bytes(n: int, level: int, t: int) -> int:
+    """PAPER.md Eq. 3 (L96): 40N + 4^L (2 + 10t) bytes."""
+    return int(lib().oracle_indexing_bytes(n, level, t))
+
+
+def repetition_bytes(n: int, ct: int) -> int:
+    """PAPER.md Eq. 8 (L126): 8N(3 + 27 CT) bytes."""
+    return int(lib().oracle_repetition_bytes(n, ct))
+
+
+def box_tmax(src_xy, tgt_xy, level: int) -> int:
+    """t of Eqs. 3-5: max over leaf boxes of max(#sources, #targets)."""
+    s, t = _f64(src_xy), _f64(tgt_xy)
+    return int(lib().oracle_box_tmax(len(s), _ptr(s), len(t), _ptr(t), level))
 
 
 def num_threads() -> int:

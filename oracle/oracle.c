@@ -295,3 +295,46 @@ int oracle_num_threads(void)
     return 1;
 #endif
 }
+
+/* ---- the paper's layout byte accounting ----------
+ * Eq. 3 (§3.2): Memory_indexing = 5N Double + 4^(L-1)(2 + t + 9t)
+ * Integer = 40N + 4^L (2 + 10t) bytes (Double = 8 B, Integer = 4 B, L97).
+ * Eq. 8 (§3.3): Memory_Repetition = N(3 + 27 CT) Double
+ * = 8N(3 + 27 CT) bytes.  t = the maximum number of points in a leaf box
+ * ("maximum points in the boxes after applying CT"). */
+int64_t oracle_indexing_bytes(int64_t n, int L, int64_t t)
+{
+    int64_t four_L = 1;
+    for (int i = 0; i < L; ++i) four_L *= 4;
+    return 40 * n + four_L * (2 + 10 * t);
+}
+
+int64_t oracle_repetition_bytes(int64_t n, int64_t ct)
+{
+    return 8 * n * (3 + 27 * ct);
+}
+
+/* t of Eq. 3-5: max over leaf boxes of max(#sources, #targets) in the box. */
+int64_t oracle_box_tmax(int64_t ns, const double *src_xy, int64_t nt, const double *tgt_xy, int L)
+{
+    const int64_t S = grid_side(L);
+    int64_t *cs = calloc((size_t)(S * S), sizeof(int64_t));
+    int64_t *ctg = calloc((size_t)(S * S), sizeof(int64_t));
+    int64_t t = 0;
+    if (!cs || !ctg) {
+        free(cs);
+        free(ctg);
+        return -1;
+    }
+    for (int64_t i = 0; i < ns; ++i)
+        cs[cell_of(src_xy[2 * i + 1], S) * S + cell_of(src_xy[2 * i], S)] += 1;
+    for (int64_t i = 0; i < nt; ++i)
+        ctg[cell_of(tgt_xy[2 * i + 1], S) * S + cell_of(tgt_xy[2 * i], S)] += 1;
+    for (int64_t b = 0; b < S * S; ++b) {
+        if (cs[b] > t) t = cs[b];
+        if (ctg[b] > t) t = ctg[b];
+    }
+    free(cs);
+    free(ctg);
+    return t;
+}

@@ -256,3 +256,36 @@ def test_spec_ct_loop():
     for p in (src, tgt):
         cells = np.minimum(np.floor(p * S), S - 1).astype(int)
         assert np.bincount(cells[:, 1] * S + cells[:, 0]).max() <= 15
+
+
+def test_paper_layout_bytes_golden():
+    """Eq. 3 / Eq. 8 byte accounting against the worked values SPEC.md gives (tests/golden)."""
+    import json
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_layout_bytes.json")))
+    for e in g["indexing"]:
+        assert oracle.indexing_bytes(e["N"], e["L"], e["t"]) == e["bytes"], e["cite"]
+    for e in g["repetition"]:
+        assert oracle.repetition_bytes(e["N"], e["CT"]) == e["bytes"], e["cite"]
+
+
+def test_paper_layout_bytes_structure():
+    """Eq. 3: 5 doubles per point + (2 + t + 9t) 4-byte integers per box; Eq. 8: 3 + 27 CT doubles
+    per target -- each term moved by exactly its unit when one variable changes."""
+    for n, L, t in [(10, 2, 3), (1000, 5, 15), (7, 4, 0)]:
+        assert oracle.indexing_bytes(n + 1, L, t) - oracle.indexing_bytes(n, L, t) == 5 * 8
+        assert oracle.indexing_bytes(n, L, t + 1) - oracle.indexing_bytes(n, L, t) == 4 ** (L - 1) * 10 * 4
+        assert oracle.indexing_bytes(n, L + 1, t) - oracle.indexing_bytes(n, L, t) == 3 * 4 ** L * (2 + 10 * t)
+    for n, ct in [(5, 1), (100, 15), (3, 64)]:
+        assert oracle.repetition_bytes(n + 1, ct) - oracle.repetition_bytes(n, ct) == 8 * (3 + 27 * ct)
+        assert oracle.repetition_bytes(n, ct + 1) - oracle.repetition_bytes(n, ct) == 8 * n * 27
+
+
+def test_box_tmax_brute():
+    """t = max box occupancy, against a numpy count on the same half-open cells."""
+    src, tgt, _ = W.make_problem("tiny")
+    for L in (1, 3, 4, 6):
+        S = 1 << (L - 1)
+        cell = lambda p: np.minimum(np.floor(p * S), S - 1).astype(int)
+        cs = np.bincount(cell(src[:, 1]) * S + cell(src[:, 0]), minlength=S * S)
+        ct = np.bincount(cell(tgt[:, 1]) * S + cell(tgt[:, 0]), minlength=S * S)
+        assert oracle.box_tmax(src, tgt, L) == max(cs.max(), ct.max())
