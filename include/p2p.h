@@ -68,7 +68,25 @@ typedef enum { P2P_KERNEL_LAPLACE_2D = 0 /* q ln(1/r); 0 when r < eps (SPEC.md L
  *           time, rebased to the region origin: redundancy only on the ring,
  *           ((W+2)/W)^2, streamed by one TMA bulk copy per tile; weights are
  *           gathered in-kernel through a per-entry index. */
-typedef enum { P2P_LAYOUT_NONREDUNDANT = 0, P2P_LAYOUT_REDUNDANT = 1, P2P_LAYOUT_TILED = 2 } p2p_layout;
+typedef enum {
+    P2P_LAYOUT_NONREDUNDANT = 0,
+    P2P_LAYOUT_REDUNDANT = 1,
+    P2P_LAYOUT_TILED = 2,
+    /* The paper's own layouts and kernels, reproduced as written (fp64,
+     * one partition, weights/potentials in either order, no accumulate with P2P_ORDER_PLAN):
+     *   PAPER_INDEXING (§3.2): the seven arrays -- source and target coordinates and
+     *     source weights in the caller's order, per-box target index lists and per-box E1
+     *     source index lists (boxes in Morton order) with their offsets; one GPU thread per box
+     *     loops its targets x neighbour sources through the indices (global memory only, as in
+     *     the paper: "none of ... Shared Memory ... were employed", L61).  Eq. 3 bytes.
+     *   PAPER_REPETITION (§3.3): one fixed-stride record of 3 + 27*C doubles per target
+     *     (caller's order) = [x_t, y_t, count (integer in the low 4 bytes of its slot), then
+     *     (x_s, y_s, q_s) per E1 source]; C = max(ct, t) (ct of the descriptor, t the largest box
+     *     occupancy); one GPU thread per target; each apply first writes q into the records
+     *     (the paper's per-execution collection of potentials).  Eq. 8 bytes (with C = ct). */
+    P2P_LAYOUT_PAPER_INDEXING = 3,
+    P2P_LAYOUT_PAPER_REPETITION = 4
+} p2p_layout;
 
 /* fp64 is paper-faithful ("stored as Double"); fp32 uses
  * box-local coordinates and the SFU lg2. */
@@ -208,6 +226,9 @@ typedef struct {
     int32_t items_per_unit;      /* TILED: 3 = one item per row-run (sorted item list), 1 = whole unit */
     int32_t flags;               /* TILED: bit 0 n9-ordered boxes, bit 1 flattened row-runs */
     int64_t interior_launches;   /* TILED: queue entries run by p2p_apply_dist_interior */
+    int64_t paper_model_bytes;   /* PAPER_INDEXING: Eq. 3 (40N + 4^L(2 + 10t)); PAPER_REPETITION: Eq. 8
+                                    (8N(3 + 27 ct)); else 0 */
+    int64_t record_stride;       /* PAPER_REPETITION: doubles per record (3 + 27 C); else 0 */
     int64_t launches;            /* queue entries of a full apply (tiles, tail tiles split) */
 } p2p_plan_info;
 
@@ -238,8 +259,12 @@ typedef enum {
     P2P_EXPORT_SLOT_OUTPUT = 17,    /* int64[slots]: TILED, tile-local output index of each slot (-1 = duplicate) */
     P2P_EXPORT_ITEM_OFFSETS = 18,   /* int64[tiles+1]: TILED NS = 3 plans, item-list offsets per tile */
     P2P_EXPORT_ITEMS = 19,          /* int64[items]: TILED NS = 3 plans, unit << 2 | row in kernel order */
-    P2P_EXPORT_LAUNCH = 20          /* int64[2*launches]: TILED, Morton-order slot of each queue entry, then its
+    P2P_EXPORT_LAUNCH = 20,         /* int64[2*launches]: TILED, Morton-order slot of each queue entry, then its
                                        part | nparts << 16 */
+    P2P_EXPORT_PAPER_NEI_OFFSETS = 21, /* int64[boxes+1]: PAPER_INDEXING, offsets into the E1 source lists */
+    P2P_EXPORT_PAPER_NEI_INDEX = 22,   /* int64[entries]: PAPER_INDEXING, original index of each E1 source */
+    P2P_EXPORT_PAPER_RECORDS = 23      /* int64[n_tgt*stride]: PAPER_REPETITION, the raw 8-byte record words
+                                          (bit patterns of the doubles; q slots as of the last apply) */
 } p2p_export_kind;
 
 /* Copy a plan array to host memory.  If host_dst is NULL, *bytes receives the

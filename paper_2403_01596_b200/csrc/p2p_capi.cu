@@ -43,7 +43,7 @@ struct p2p_plan_s {
     int device = -1;
     cudaStream_t stream = nullptr;
     // device arrays
-    DevBuf halo_lidx, tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, send_idx;
+    DevBuf pi_src_xy, pi_tgt_xy, pi_nei_off, pi_nei_idx, pr_records, pr_slot, phi_user, halo_lidx, tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
     DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uidx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, log_tab, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
@@ -52,6 +52,7 @@ struct p2p_plan_s {
     unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
     int64_t device_bytes = 0;
     double upload_seconds = 0.0;
+    bool paper_kernel_only = false;              // diagnostics: PAPER_REPETITION applies skip the weight pack
     int elem = 4;
 
     template <typename V>
@@ -69,7 +70,7 @@ struct p2p_plan_s {
         device_bytes += (int64_t)bytes;
     }
     void release() {
-        DevBuf *all[] = {&halo_lidx, &tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
+        DevBuf *all[] = {&pi_src_xy, &pi_tgt_xy, &pi_nei_off, &pi_nei_idx, &pr_records, &pr_slot, &phi_user, &halo_lidx, &tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
                          &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uidx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi,
@@ -133,7 +134,15 @@ void upload_plan(p2p_plan_s &P) {
         P.upload(P.halo_lidx, hp.halo_lidx);
         P.upload(P.send_idx, hp.send_idx);
     }
-    if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
+    if (hp.layout == P2P_LAYOUT_PAPER_INDEXING) {
+        P.upload(P.pi_src_xy, hp.pi_src_xy);
+        P.upload(P.pi_tgt_xy, hp.pi_tgt_xy);
+        P.upload(P.pi_nei_off, hp.pi_nei_off);
+        P.upload(P.pi_nei_idx, hp.pi_nei_idx);
+    } else if (hp.layout == P2P_LAYOUT_PAPER_REPETITION) {
+        P.upload(P.pr_records, hp.pr_records);
+        P.upload(P.pr_slot, hp.pr_slot);
+    } else if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
         P.upload(P.src_off, hp.src_off);
         P.upload(P.src_uv, lay.src_uv);
     } else if (hp.layout == P2P_LAYOUT_TILED) {
@@ -264,9 +273,51 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
     ck(cudaGetLastError(), "kernel launch");
 }
 
+// The paper's kernels (NEXT-1): native order is the caller's (their arrays index original
+// points); plan-order weights are scattered to caller's order first and the potentials gathered
+// back (no accumulate then).
+void apply_paper(p2p_plan_s &P, const void *d_q, void *d_out, int order, int accumulate, cudaStream_t s) {
+    const p2p::HostPlan &hp = P.hp;
+    if (order == P2P_ORDER_PLAN && accumulate)
+        throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "the paper's layouts: accumulate needs P2P_ORDER_USER");
+    const double *q = (const double *)d_q;
+    double *out = (double *)d_out;
+    if (order == P2P_ORDER_PLAN) {
+        if (hp.n_src)
+            p2p::dev::scatter_kernel<double><<<grid_for(hp.n_src), 256, 0, s>>>(
+                (const int32_t *)P.src_uidx.p, (const double *)d_q, (double *)P.io_q.p, hp.n_src, 0);
+        if (!P.phi_user.p) P.alloc(P.phi_user, (size_t)std::max<int64_t>(hp.n_tgt, 1) * sizeof(double));
+        q = (const double *)P.io_q.p;
+        out = (double *)P.phi_user.p;
+    }
+    const double eps2 = hp.eps * hp.eps;
+    if (hp.layout == P2P_LAYOUT_PAPER_INDEXING) {
+        if (hp.B)
+            p2p::dev::paper_indexing_kernel<<<(unsigned)((hp.B + 255) / 256), 256, 0, s>>>(
+                hp.B, (const int32_t *)P.tgt_off.p, (const int32_t *)P.tgt_uidx.p, (const int32_t *)P.pi_nei_off.p,
+                (const int32_t *)P.pi_nei_idx.p, (const double2 *)P.pi_src_xy.p, (const double2 *)P.pi_tgt_xy.p, q,
+                out, eps2, accumulate);
+    } else {
+        if (!P.paper_kernel_only && hp.n_tgt)
+            p2p::dev::paper_rep_pack_kernel<<<grid_for(hp.n_tgt * hp.pr_maxn), 256, 0, s>>>(
+                hp.n_tgt, hp.pr_maxn, hp.pr_stride, (const int32_t *)P.pr_slot.p, q, (double *)P.pr_records.p);
+        if (hp.n_tgt)
+            p2p::dev::paper_repetition_kernel<<<(unsigned)((hp.n_tgt + 255) / 256), 256, 0, s>>>(
+                hp.n_tgt, hp.pr_stride, (const double *)P.pr_records.p, out, eps2, accumulate);
+    }
+    if (order == P2P_ORDER_PLAN && hp.n_tgt)
+        p2p::dev::gather_kernel<double><<<grid_for(hp.n_tgt), 256, 0, s>>>(
+            (const int32_t *)P.tgt_uidx.p, (const double *)P.phi_user.p, (double *)d_out, hp.n_tgt);
+    ck(cudaGetLastError(), "paper apply launch");
+}
+
 template <typename T>
 void apply_impl(p2p_plan_s &P, const void *d_q, void *d_out, int order, int accumulate, cudaStream_t s) {
     const p2p::HostPlan &hp = P.hp;
+    if (hp.layout == P2P_LAYOUT_PAPER_INDEXING || hp.layout == P2P_LAYOUT_PAPER_REPETITION) {
+        if constexpr (sizeof(T) == 8) apply_paper(P, d_q, d_out, order, accumulate, s);
+        return;
+    }
     const T *q_local = (const T *)d_q;
     if (order == P2P_ORDER_USER && hp.layout == P2P_LAYOUT_TILED) {  // permutations fused into the kernel
         launch_p2p<T>(P, (const T *)d_q, (T *)d_out, accumulate, s, true);
@@ -580,6 +631,8 @@ p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *out) {
     info->items_per_unit = hp.layout == P2P_LAYOUT_TILED ? hp.ns : 3;
     info->flags = (hp.tsort ? 1 : 0) | (hp.flat ? 2 : 0);
     info->interior_launches = hp.layout == P2P_LAYOUT_TILED ? hp.n_interior : 0;
+    info->paper_model_bytes = hp.paper_model_bytes;
+    info->record_stride = hp.pr_stride;
     info->launches = (int64_t)hp.tiles.size();
     std::memcpy(out, info, n);
     return P2P_SUCCESS;
@@ -621,6 +674,18 @@ p2p_status p2p_plan_export(p2p_plan P, int32_t kind, void *host_dst, size_t *byt
             break;
         case P2P_EXPORT_ITEM_OFFSETS: take(hp.item_off); break;
         case P2P_EXPORT_ITEMS: take(hp.items); break;
+        case P2P_EXPORT_PAPER_NEI_OFFSETS: take(hp.pi_nei_off); break;
+        case P2P_EXPORT_PAPER_NEI_INDEX: take(hp.pi_nei_idx); break;
+        case P2P_EXPORT_PAPER_RECORDS: {
+            std::vector<double> rec = hp.pr_records;
+            if (P->pr_records.p && P->device >= 0) {  // as of the last apply (q slots filled)
+                DeviceGuard g(P->device);
+                ck(cudaMemcpy(rec.data(), P->pr_records.p, rec.size() * 8, cudaMemcpyDeviceToHost), "records D2H");
+            }
+            v.resize(rec.size());
+            std::memcpy(v.data(), rec.data(), rec.size() * 8);
+            break;
+        }
         case P2P_EXPORT_LAUNCH:
             take(hp.tile_slot);
             v.insert(v.end(), hp.tile_part.begin(), hp.tile_part.end());
@@ -660,6 +725,14 @@ int32_t p2p_abi_version(void) { return P2P_ABI_VERSION; }
 // kernel -- d_trace = device buffer of 8 x uint64 per tile (queue position):
 // {smid << 32 | cta, t_claim, t_data, t_units, -, t_end, units, entries}
 // in %globaltimer ns; NULL disables.
+// Undeclared diagnostics hook: PAPER_REPETITION applies skip the weight pack (the records keep the
+// weights of the last full apply), so the repetition kernel can be timed alone.
+p2p_status p2p_internal_paper_kernel_only(p2p_plan P, int on) {
+    if (!P) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan");
+    P->paper_kernel_only = on != 0;
+    return P2P_SUCCESS;
+}
+
 p2p_status p2p_internal_set_trace(p2p_plan P, void *d_trace) {
     if (!P) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan");
     P->trace = (unsigned long long *)d_trace;

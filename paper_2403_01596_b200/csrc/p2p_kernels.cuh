@@ -948,6 +948,61 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
     if (tid == 0) queue_exit(a.queue);
 }
 
+// ---------------------------------------------------------------- the paper's kernels (NEXT-1)
+// Reproduced as the paper describes them, global memory only ("none of ... pre-fetching,
+// exploiting Shared Memory ... were employed"), fp64, the library log.
+//   Indexing (§3.2): "A GPU thread is assigned to a single box" -- it walks the
+//   box's target index list and, per target, the box's E1 source index list.
+//   Repetition (§3.3): one thread per target reads its own fixed-stride record
+//   [x_t, y_t, count, (x_s, y_s, q_s) ...].
+__global__ void paper_indexing_kernel(int64_t nbox, const int32_t *__restrict__ tgt_off,
+                                      const int32_t *__restrict__ tgt_idx, const int32_t *__restrict__ nei_off,
+                                      const int32_t *__restrict__ nei_idx, const double2 *__restrict__ src_xy,
+                                      const double2 *__restrict__ tgt_xy, const double *__restrict__ q,
+                                      double *__restrict__ out, double eps2, int accumulate) {
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nbox) return;
+    for (int32_t i = tgt_off[b]; i < tgt_off[b + 1]; ++i) {
+        const int32_t t = tgt_idx[i];
+        const double2 pt = tgt_xy[t];
+        double acc = 0.0;
+        for (int32_t e = nei_off[b]; e < nei_off[b + 1]; ++e) {
+            const int32_t sidx = nei_idx[e];
+            const double2 ps = src_xy[sidx];
+            const double du = pt.x - ps.x, dv = pt.y - ps.y;
+            const double r2 = fma(dv, dv, du * du);
+            if (r2 >= eps2) acc = fma(q[sidx], log(r2), acc);
+        }
+        out[t] = accumulate ? out[t] - 0.5 * acc : -0.5 * acc;
+    }
+}
+
+// The per-execution part of the Repetition collection: the weights into the records' q slots.
+__global__ void paper_rep_pack_kernel(int64_t n_tgt, int64_t maxn, int64_t stride, const int32_t *__restrict__ slot,
+                                      const double *__restrict__ q, double *__restrict__ records) {
+    const int64_t n = n_tgt * maxn;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t sidx = slot[i];
+        if (sidx >= 0) records[(i / maxn) * stride + 3 + 3 * (i % maxn) + 2] = q[sidx];
+    }
+}
+
+__global__ void paper_repetition_kernel(int64_t n_tgt, int64_t stride, const double *__restrict__ records,
+                                        double *__restrict__ out, double eps2, int accumulate) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n_tgt) return;
+    const double *rec = records + r * stride;
+    const double xt = rec[0], yt = rec[1];
+    const int count = (int)(uint32_t)__double_as_longlong(rec[2]);  // integer in the slot's low 4 bytes
+    double acc = 0.0;
+    for (int k = 0; k < count; ++k) {
+        const double du = xt - rec[3 + 3 * k], dv = yt - rec[4 + 3 * k];
+        const double r2 = fma(dv, dv, du * du);
+        if (r2 >= eps2) acc = fma(rec[5 + 3 * k], log(r2), acc);
+    }
+    out[r] = accumulate ? out[r] - 0.5 * acc : -0.5 * acc;
+}
+
 // ---------------------------------------------------------------- data movement
 // R pack: q_halo[e] = q_local[halo_idx[e]] (0 for pads).
 template <typename T>

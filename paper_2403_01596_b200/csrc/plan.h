@@ -213,6 +213,13 @@ struct HostPlan {
     bool tsort = false;                           // ns 1: target boxes of a tile ordered by n9 (descending)
     bool flat = false;                            // lean path: row-runs swept as one sequence (sparse)
     std::vector<double> log_tab;                  // fp64: kLogTab x (c_inv, -log c_inv) for the table-driven log
+
+    // ---- the paper's layouts (PAPER_INDEXING / PAPER_REPETITION)
+    std::vector<int32_t> pi_nei_off, pi_nei_idx;  // per box (Morton): its E1 sources' original indices
+    std::vector<double> pi_src_xy, pi_tgt_xy;     // coordinates in the caller's order
+    std::vector<double> pr_records;               // n_tgt x pr_stride doubles, caller's target order
+    std::vector<int32_t> pr_slot;                 // n_tgt x pr_maxn: original source index per triple, -1 = none
+    int64_t pr_stride = 0, pr_maxn = 0, paper_model_bytes = 0;
     std::vector<int32_t> tile_slot;               // launch order -> slot
     std::vector<int32_t> tile_part;               // launch order -> part | nparts << 16 (tail splitting)
     int64_t reg_entries = 0;

@@ -177,8 +177,12 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     auto t0 = std::chrono::steady_clock::now();
     if (d.struct_size != sizeof(p2p_plan_desc)) fail(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
     if (d.kernel != P2P_KERNEL_LAPLACE_2D) fail(P2P_ERROR_NOT_SUPPORTED, "only P2P_KERNEL_LAPLACE_2D");
-    if (d.layout != P2P_LAYOUT_NONREDUNDANT && d.layout != P2P_LAYOUT_REDUNDANT && d.layout != P2P_LAYOUT_TILED)
+    if (d.layout < P2P_LAYOUT_NONREDUNDANT || d.layout > P2P_LAYOUT_PAPER_REPETITION)
         fail(P2P_ERROR_INVALID_ARGUMENT, "bad layout");
+    const bool paper = d.layout == P2P_LAYOUT_PAPER_INDEXING || d.layout == P2P_LAYOUT_PAPER_REPETITION;
+    if (paper && d.precision != P2P_FP64)
+        fail(P2P_ERROR_NOT_SUPPORTED, "the paper's layouts are fp64 (PAPER.md L98: stored as Double)");
+    if (paper && d.part_world != 1) fail(P2P_ERROR_NOT_SUPPORTED, "the paper's layouts are single-partition");
     if (d.precision != P2P_FP32 && d.precision != P2P_FP64) fail(P2P_ERROR_INVALID_ARGUMENT, "bad precision");
     if (!(d.epsilon > 0.0) || !std::isfinite(d.epsilon)) fail(P2P_ERROR_INVALID_ARGUMENT, "epsilon must be > 0");
     if (d.part_world < 1 || d.part_rank < 0 || d.part_rank >= d.part_world)
@@ -368,6 +372,10 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                 mx = std::max(mx, rg);
             }
             hp.src_cap = pad4(mx);
+        }
+        if (paper) {  // global-memory kernels: no tiles to size
+            hp.smem_bytes = 0;
+            break;
         }
         const int sc = (int)std::min<int64_t>(hp.src_cap, 1 << 24), tc = (int)std::min<int64_t>(hp.tgt_cap, 1 << 24);
         int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? (int64_t)nr_carve(k, sc, tc, e, hp.tpi).total
@@ -854,6 +862,71 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                 }
             }
         }, 64);
+    }
+    // ---- the paper's layouts, as written (§3.2-3.3; SPEC.md layouts)
+    if (paper) {
+        const std::vector<int64_t> nb = neighbors_export(hp);  // E1 per box, ascending Morton
+        if (d.layout == P2P_LAYOUT_PAPER_INDEXING) {
+            // per box, the original indices of its E1 sources: neighbour boxes ascending Morton,
+            // sources in per-box (original index) order; boxes in Morton order
+            hp.pi_nei_off.assign((size_t)hp.B + 1, 0);
+            int64_t tot = 0;
+            for (int64_t b = 0; b < hp.B; ++b) {
+                for (int c = 0; c < 9 && nb[9 * b + c] >= 0; ++c)
+                    tot += hp.src_off_g[nb[9 * b + c] + 1] - hp.src_off_g[nb[9 * b + c]];
+                if (tot > INT32_MAX) fail(P2P_ERROR_NOT_SUPPORTED, "PAPER_INDEXING: > 2^31 neighbour entries");
+                hp.pi_nei_off[b + 1] = (int32_t)tot;
+            }
+            hp.pi_nei_idx.resize((size_t)tot);
+            hp.pi_src_xy.assign(d.src_xy, d.src_xy + 2 * hp.n_src);
+            hp.pi_tgt_xy.assign(d.tgt_xy, d.tgt_xy + 2 * hp.n_tgt);
+            parallel_for(hp.B, [&](int64_t a, int64_t bnd) {
+                for (int64_t b = a; b < bnd; ++b) {
+                    int64_t e = hp.pi_nei_off[b];
+                    for (int c = 0; c < 9 && nb[9 * b + c] >= 0; ++c)
+                        for (int32_t g = hp.src_off_g[nb[9 * b + c]]; g < hp.src_off_g[nb[9 * b + c] + 1]; ++g)
+                            hp.pi_nei_idx[e++] = hp.src_perm_g[g];
+                }
+            }, 4096);
+            // Eq. 3: 5N Double + 4^(L-1)(2 + t + 9t) Integer (source/target counts may differ)
+            int64_t four_L = 1;
+            for (int i = 0; i < L; ++i) four_L *= 4;
+            hp.paper_model_bytes = 8 * (3 * hp.n_src + 2 * hp.n_tgt) + four_L * (2 + 10 * hp.t_max);
+        } else {
+            // one record per target (caller's order): [x_t, y_t, count, (x_s, y_s, q_s) x count],
+            // stride 3 + 27 C with C = max(ct, t): a record must hold 9t sources (levels below the
+            // CT loop's choice, level_delta < 0, exceed ct) -- DESIGN.md R20
+            const int64_t C = std::max<int64_t>(d.ct, hp.t_max);
+            hp.pr_maxn = 9 * C;
+            hp.pr_stride = 3 + 27 * C;
+            const double bytes = 8.0 * (double)hp.n_tgt * (double)hp.pr_stride;
+            if (bytes > 16.0e9) fail(P2P_ERROR_NOT_SUPPORTED, "PAPER_REPETITION records would exceed 16 GB");
+            hp.pr_records.assign((size_t)(hp.n_tgt * hp.pr_stride), 0.0);
+            hp.pr_slot.assign((size_t)(hp.n_tgt * hp.pr_maxn), -1);
+            const double *sxy = d.src_xy, *txy = d.tgt_xy;
+            parallel_for(hp.B, [&](int64_t a, int64_t bnd) {
+                for (int64_t b = a; b < bnd; ++b)
+                    for (int32_t i = hp.tgt_off_g[b]; i < hp.tgt_off_g[b + 1]; ++i) {
+                        const int64_t r = hp.tgt_perm_g[i];
+                        double *rec = &hp.pr_records[(size_t)(r * hp.pr_stride)];
+                        int32_t *sl = &hp.pr_slot[(size_t)(r * hp.pr_maxn)];
+                        rec[0] = txy[2 * r];
+                        rec[1] = txy[2 * r + 1];
+                        int64_t cnt = 0;
+                        for (int c = 0; c < 9 && nb[9 * b + c] >= 0; ++c)
+                            for (int32_t g = hp.src_off_g[nb[9 * b + c]]; g < hp.src_off_g[nb[9 * b + c] + 1]; ++g) {
+                                const int64_t s = hp.src_perm_g[g];
+                                rec[3 + 3 * cnt] = sxy[2 * s];
+                                rec[3 + 3 * cnt + 1] = sxy[2 * s + 1];
+                                sl[cnt++] = (int32_t)s;
+                            }
+                        // the count: an integer in the low 4 bytes of a double slot (SPEC.md layouts)
+                        const uint64_t bits = (uint64_t)(uint32_t)cnt;
+                        std::memcpy(&rec[2], &bits, 8);
+                    }
+            }, 1024);
+            hp.paper_model_bytes = 8 * hp.n_tgt * (3 + 27 * (int64_t)d.ct);  // Eq. 8
+        }
     }
     hp.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }

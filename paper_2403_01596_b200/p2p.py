@@ -32,6 +32,8 @@ P2P_KERNEL_LAPLACE_2D = 0
 P2P_LAYOUT_NONREDUNDANT = 0
 P2P_LAYOUT_REDUNDANT = 1
 P2P_LAYOUT_TILED = 2
+P2P_LAYOUT_PAPER_INDEXING = 3
+P2P_LAYOUT_PAPER_REPETITION = 4
 P2P_FP64 = 0
 P2P_FP32 = 1
 P2P_ORDER_PLAN = 0
@@ -42,7 +44,7 @@ EXPORT = {
     "neighbors": 4, "partition": 5, "src_global": 6, "halo_counts": 7, "tiles": 8,
     "halo_index": 9, "send_index": 10, "halo_offsets": 11, "region_offsets": 12, "region_index": 13,
     "region_table": 14, "slot_offsets": 15, "slot_base": 16, "slot_output": 17, "item_offsets": 18,
-    "items": 19, "launch": 20,
+    "items": 19, "launch": 20, "paper_nei_offsets": 21, "paper_nei_index": 22, "paper_records": 23,
 }
 
 # Symbols declared in include/p2p.h (checked by tests/test_abi.py).
@@ -82,7 +84,7 @@ class PlanInfo(C.Structure):
         ("layout_bytes_apply", C.c_int64), ("device_bytes", C.c_int64), ("build_seconds", C.c_double),
         ("upload_seconds", C.c_double), ("cta_threads", C.c_int32), ("slots_per_unit", C.c_int32),
         ("items_per_unit", C.c_int32), ("flags", C.c_int32), ("interior_launches", C.c_int64),
-        ("launches", C.c_int64),
+        ("paper_model_bytes", C.c_int64), ("record_stride", C.c_int64), ("launches", C.c_int64),
     ]
 
 
@@ -214,7 +216,8 @@ class Plan:
 
     src_xy / tgt_xy: numpy float64 [n, 2] in [0,1]^2 (copied by the library).
     layout: "nr" (non-redundant), "r" (redundant per box) or "tiled" (redundant on
-    the tile ring only); precision: "fp32" or "fp64".
+    the tile ring only); "paper_i" / "paper_r": the paper's own Indexing / Repetition
+    layouts and kernels (fp64); precision: "fp32" or "fp64".
     device: CUDA ordinal, or -1 for a host-only plan (build + export only).
     """
 
@@ -232,7 +235,8 @@ class Plan:
         d.tgt_xy = self._tgt.ctypes.data
         d.level, d.ct, d.l_start, d.l_max, d.level_delta = level, ct, l_start, l_max, level_delta
         d.epsilon = epsilon
-        d.layout = {"nr": P2P_LAYOUT_NONREDUNDANT, "r": P2P_LAYOUT_REDUNDANT, "tiled": P2P_LAYOUT_TILED}[layout]
+        d.layout = {"nr": P2P_LAYOUT_NONREDUNDANT, "r": P2P_LAYOUT_REDUNDANT, "tiled": P2P_LAYOUT_TILED,
+                    "paper_i": P2P_LAYOUT_PAPER_INDEXING, "paper_r": P2P_LAYOUT_PAPER_REPETITION}[layout]
         d.precision = {"fp32": P2P_FP32, "fp64": P2P_FP64}[precision]
         d.device, d.tile_log2, d.stream = device, tile_log2, stream or None
         d.part_world, d.part_rank = part_world, part_rank

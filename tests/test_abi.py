@@ -94,3 +94,18 @@ def test_plan_info_struct_size_prefix():
         assert bytes(buf[cut:]) == bytes([0xAB] * (C.sizeof(p2p.PlanInfo) - cut))
         info.struct_size = 2  # smaller than the struct_size field itself: rejected
         assert lib.p2p_plan_get_info(h.handle, C.byref(info)) == p2p.P2P_ERROR_INVALID_ARGUMENT
+
+
+def test_plan_info_field_order_matches_header():
+    """The ctypes PlanInfo follows include/p2p.h field by field (names and order)."""
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "p2p.h")).read()
+    body = hdr[hdr.index("typedef struct {", hdr.index("p2p_status p2p_destroy")):hdr.index("} p2p_plan_info;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = []
+    for decl in body.split(";"):
+        decl = decl.replace("typedef struct {", "").strip()
+        if not decl:
+            continue
+        parts = decl.split(None, 1)
+        names += [n.strip() for n in parts[1].split(",")]
+    assert names == [n for n, _ in p2p.PlanInfo._fields_]

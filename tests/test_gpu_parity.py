@@ -209,3 +209,31 @@ def test_tail_split_bit_identical(prec, level, monkeypatch):
             assert np.any((launch[1] >> 16) == parts)
             assert np.array_equal(gpu_apply(pl, q), base)
             check(pl, src, tgt, q, level)
+
+
+@pytest.mark.parametrize("layout", ["paper_i", "paper_r"])
+@pytest.mark.parametrize("level", [1, 3, 4, 6])
+def test_paper_layouts_parity(layout, level):
+    """The paper's own Indexing / Repetition kernels vs the oracle, fp64,
+    plan and user order, accumulate."""
+    src, tgt, q = W.make_problem("tiny")
+    with p2p.Plan(src, tgt, level=level, layout=layout, precision="fp64") as pl:
+        check(pl, src, tgt, q, level)
+        ref, _ = oracle.direct(src, q, tgt, level)
+        got = gpu_apply(pl, q, order="user")
+        assert rel_l2(got, ref) <= TOL["fp64"]
+        out = torch.full((len(tgt),), 2.0, dtype=torch.float64, device="cuda")
+        pl.apply(torch.as_tensor(q, dtype=torch.float64, device="cuda"), out, order="user", accumulate=True)
+        torch.cuda.synchronize()
+        assert rel_l2(out.cpu().numpy() - 2.0, ref) <= TOL["fp64"]
+
+
+@pytest.mark.parametrize("layout", ["paper_i", "paper_r"])
+def test_paper_layouts_parity_sparse_and_ct(layout):
+    """20k points at ~1 per box, and the CT loop's own level (CT = 15)."""
+    c = W.CONFIGS["lowd1_1e7"]
+    src, tgt, q = W.make_problem(c, n=20000)
+    with p2p.Plan(src, tgt, level=c.level - 5, layout=layout, precision="fp64") as pl:
+        check(pl, src, tgt, q, c.level - 5)
+    with p2p.Plan(src, tgt, level=0, layout=layout, precision="fp64", ct=15) as pl:
+        check(pl, src, tgt, q, pl.info["level"])
