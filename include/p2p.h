@@ -129,6 +129,21 @@ void p2p_plan_desc_init(p2p_plan_desc *desc);
  * NOT_SUPPORTED, OUT_OF_MEMORY, CUDA. */
 p2p_status p2p_plan_create(const p2p_plan_desc *desc, p2p_plan *out);
 
+/* Build the same plan ON THE GPU from device-resident coordinates (SURVEY.md §8(f) NEXT-2:
+ * the paper's "collection", its dominant cost -- PAPER.md §3.2, §3.3, alpha ~ 0.82 of
+ * the total at L337-343 -- done by sm_100a kernels: Morton codes, stable radix sort, CSR offsets,
+ * box statistics, tiles, the NR / TILED layouts and the launch queue).
+ *   d_src_xy, d_tgt_xy: device, [n][2] interleaved fp64 x,y in [0,1]^2 on desc->device (may
+ *                       alias); read during the call only (the caller keeps ownership).
+ *   desc->src_xy / tgt_xy are ignored; every other field means what it means for
+ *   p2p_plan_create, and the plan (every exported array, the info, every apply result) is
+ *   bit-identical to the one p2p_plan_create builds from the same coordinates.
+ * Work runs on desc->stream and the call synchronises it.  Scope: layouts NONREDUNDANT and
+ * TILED, part_world = 1.  Errors: as p2p_plan_create, plus NOT_SUPPORTED (other layouts,
+ * part_world > 1), NO_DEVICE (device < 0 or no GPU). */
+p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src_xy, const double *d_tgt_xy,
+                                  p2p_plan *out);
+
 /* phi = A q on the plan's device, asynchronously on `stream` (cudaStream_t,
  * NULL = default stream).
  *   d_q   : device, weights in the plan precision (float or double).

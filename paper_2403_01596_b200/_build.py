@@ -13,7 +13,7 @@ PEAKS_LIB = os.path.join(LIBDIR, "libp2p_peaks.so")
 INCLUDE = os.path.join(ROOT, "include")
 
 SOURCES = ["p2p_capi.cu", "plan_builder.cpp"]
-DEPS = SOURCES + ["p2p_kernels.cuh", "plan.h"]
+DEPS = SOURCES + ["p2p_kernels.cuh", "plan.h", "plan_device.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

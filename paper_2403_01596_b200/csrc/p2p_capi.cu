@@ -3,13 +3,16 @@
 #include <algorithm>
 #include <chrono>
 #include <cstddef>
+#include <cmath>
 #include <cstring>
 #include <memory>
+#include <numeric>
 #include <string>
 
 #include "p2p.h"
 #include "p2p_kernels.cuh"
 #include "plan.h"
+#include "plan_device.cuh"
 
 namespace {
 
@@ -120,6 +123,9 @@ const void *tiled_fn(int tpi, int nt, bool pad, int ns) {
 }
 
 template <typename T>
+void finalize_plan(p2p_plan_s &P);
+
+template <typename T>
 void upload_plan(p2p_plan_s &P) {
     const p2p::HostPlan &hp = P.hp;
     const p2p::Layout<T> &lay = layout_of<T>(hp);
@@ -166,6 +172,13 @@ void upload_plan(p2p_plan_s &P) {
         P.upload(P.halo_uv, lay.halo_uv);
         P.alloc(P.halo_q, (size_t)hp.halo_entries * sizeof(T));
     }
+    finalize_plan<T>(P);
+}
+
+// Kernel attributes, persistent grid size and apply workspace of a plan whose layout is on the device.
+template <typename T>
+void finalize_plan(p2p_plan_s &P) {
+    const p2p::HostPlan &hp = P.hp;
     // Dynamic shared memory is fixed per plan: opt in once (a permission, not a
     // reservation, so one value serves all plans), then size the persistent grid.
     const bool two = hp.tpi == 2;
@@ -406,6 +419,416 @@ void require_device(const p2p_plan_s *P) {
     if (P->device < 0) throw p2p::Error(P2P_ERROR_NO_DEVICE, "host-only plan (device < 0): no apply; there is no CPU fallback");
 }
 
+
+// ---- the plan build on the device (plan_device.cuh) ----
+
+// Stream-ordered temporaries of a device build, released on exit.
+struct DevTmp {
+    cudaStream_t s;
+    std::vector<void *> held;
+    explicit DevTmp(cudaStream_t st) : s(st) {}
+    template <typename V>
+    V *get(int64_t n) {
+        void *p = nullptr;
+        ck(cudaMallocAsync(&p, (size_t)std::max<int64_t>(n, 1) * sizeof(V), s), "cudaMallocAsync (build temporaries)");
+        held.push_back(p);
+        return (V *)p;
+    }
+    ~DevTmp() {
+        for (void *p : held) cudaFreeAsync(p, s);
+    }
+};
+
+template <typename V>
+void d2h(V *dst, const void *src, int64_t n, cudaStream_t s) {
+    if (n <= 0) return;
+    ck(cudaMemcpyAsync(dst, src, (size_t)n * sizeof(V), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync D2H");
+    ck(cudaStreamSynchronize(s), "device build sync");
+}
+
+// Exclusive scan of n uint32 counts into off[0..n] (off[0] = 0); returns off[n].
+int64_t scan_offsets(DevTmp &tmp, const uint32_t *cnt, uint32_t *off, int64_t n, cudaStream_t s) {
+    ck(cudaMemsetAsync(off, 0, sizeof(uint32_t), s), "memset");
+    if (n > 0) {
+        size_t tb = 0;
+        ck(cub::DeviceScan::InclusiveSum(nullptr, tb, cnt, off + 1, (int)n, s), "cub scan");
+        void *t = tmp.get<char>((int64_t)tb);
+        ck(cub::DeviceScan::InclusiveSum(t, tb, cnt, off + 1, (int)n, s), "cub scan");
+    }
+    uint32_t last = 0;
+    d2h(&last, off + n, 1, s);
+    return last;
+}
+
+// a2 + a3 on the device: codes at grid side S, stable radix sort of (code, index), CSR offsets.
+void device_csr(DevTmp &tmp, const double *xy, int64_t n, int L, int64_t S, int64_t B, int32_t *perm, int32_t *off,
+                cudaStream_t s) {
+    using namespace p2p::dbuild;
+    uint32_t *code = tmp.get<uint32_t>(n), *code_s = tmp.get<uint32_t>(n);
+    int32_t *idx = tmp.get<int32_t>(n);
+    codes_kernel<<<nblocks(n), kB, 0, s>>>((const double2 *)xy, n, S, code, idx);
+    const int bits = 2 * (L - 1);
+    if (bits > 0) {
+        size_t tb = 0;
+        ck(cub::DeviceRadixSort::SortPairs(nullptr, tb, code, code_s, idx, perm, (int)n, 0, bits, s), "cub sort");
+        void *t = tmp.get<char>((int64_t)tb);
+        ck(cub::DeviceRadixSort::SortPairs(t, tb, code, code_s, idx, perm, (int)n, 0, bits, s), "cub sort");
+    } else {  // one box: the identity
+        ck(cudaMemcpyAsync(code_s, code, (size_t)n * 4, cudaMemcpyDeviceToDevice, s), "copy");
+        ck(cudaMemcpyAsync(perm, idx, (size_t)n * 4, cudaMemcpyDeviceToDevice, s), "copy");
+    }
+    offsets_kernel<<<nblocks(B + 1), kB, 0, s>>>(code_s, n, B, off);
+}
+
+// a1 CT loop on the device: codes at l_max sorted once; the most points in a box at each level
+// is the longest run of equal code prefixes (§3.1; the host's ct_loop_level).
+int device_ct_level(DevTmp &tmp, const p2p_plan_desc &d, const double *dsrc, const double *dtgt, cudaStream_t s) {
+    using namespace p2p::dbuild;
+    const int lmax = std::min(d.l_max, p2p::kMaxLevel);
+    if (d.l_start < 1) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "l_start must be >= 1");
+    if (d.ct < 1) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "ct must be >= 1");
+    const int64_t Sref = int64_t(1) << (lmax - 1);
+    const int l0 = std::max(1, d.l_start);
+    int64_t *mr = tmp.get<int64_t>(32);
+    ck(cudaMemsetAsync(mr, 0, 32 * sizeof(int64_t), s), "memset");
+    const double *xy[2] = {dsrc, dtgt};
+    const int64_t nn[2] = {d.n_src, d.n_tgt};
+    for (int w = 0; w < 2; ++w) {
+        const int64_t n = nn[w];
+        uint32_t *code = tmp.get<uint32_t>(n), *code_s = tmp.get<uint32_t>(n);
+        codes_kernel<<<nblocks(n), kB, 0, s>>>((const double2 *)xy[w], n, Sref, code, nullptr);
+        const int bits = 2 * (lmax - 1);
+        if (bits > 0) {
+            size_t tb = 0;
+            ck(cub::DeviceRadixSort::SortKeys(nullptr, tb, code, code_s, (int)n, 0, bits, s), "cub sort");
+            void *t = tmp.get<char>((int64_t)tb);
+            ck(cub::DeviceRadixSort::SortKeys(t, tb, code, code_s, (int)n, 0, bits, s), "cub sort");
+        } else {
+            ck(cudaMemcpyAsync(code_s, code, (size_t)n * 4, cudaMemcpyDeviceToDevice, s), "copy");
+        }
+        if (l0 <= lmax) maxrun_kernel<<<nblocks(n), kB, 0, s>>>(code_s, n, l0, lmax, lmax, mr + 16 * w);
+    }
+    int64_t h[32];
+    d2h(h, mr, 32, s);
+    for (int L = l0; L <= lmax; ++L)
+        if (h[L] <= d.ct && h[16 + L] <= d.ct) return L;
+    throw p2p::Error(P2P_ERROR_CONSTRUCTION_FAILURE,
+                     "CT loop: some leaf box still holds more than CT points at L = " + std::to_string(lmax) +
+                         " (cap; SPEC.md L75)");
+}
+
+// The whole plan on the device, bit-identical to build_host_plan for one partition and the NR /
+// TILED layouts.  Device arrays go straight into P's buffers; hp gets the scalars and the launch
+// list (host arrays for export are mirrored on demand, mirror_device_plan).
+template <typename T>
+void build_device_plan(p2p_plan_s &P, const p2p_plan_desc &d, const double *dsrc, const double *dtgt) {
+    using namespace p2p::dbuild;
+    p2p::HostPlan &hp = P.hp;
+    cudaStream_t s = P.stream;
+    const auto t0 = std::chrono::steady_clock::now();
+    DevTmp tmp(s);
+    hp.device_built = true;
+    hp.layout = d.layout;
+    hp.precision = d.precision;
+    hp.device = d.device;
+    hp.eps = d.epsilon;
+    hp.part_world = 1;
+    hp.part_rank = 0;
+    hp.n_src = d.n_src;
+    hp.n_tgt = d.n_tgt;
+    const int e = sizeof(T);
+
+    {   // coordinates inside the unit square, NaN rejected
+        unsigned long long *bad = tmp.get<unsigned long long>(2), hb[2];
+        ck(cudaMemsetAsync(bad, 0xFF, 2 * sizeof(unsigned long long), s), "memset");
+        validate_kernel<<<nblocks(2 * d.n_src), kB, 0, s>>>(dsrc, 2 * d.n_src, bad);
+        validate_kernel<<<nblocks(2 * d.n_tgt), kB, 0, s>>>(dtgt, 2 * d.n_tgt, bad + 1);
+        d2h(hb, bad, 2, s);
+        for (int w = 0; w < 2; ++w)
+            if (hb[w] != ~0ull)
+                throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, std::string(w ? "targets" : "sources") + ": coordinate " +
+                                                                 std::to_string(hb[w] / 2) +
+                                                                 " outside the unit square [0,1]^2 (SPEC.md L119)");
+    }
+    // ---- a1 level
+    int L = d.level > 0 ? d.level : device_ct_level(tmp, d, dsrc, dtgt, s);
+    L += d.level_delta;
+    if (L < 1) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "L + level_delta < 1 (SPEC.md L85)");
+    if (L > p2p::kMaxLevel) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "L > 15 (full-grid CSR offsets; see DESIGN.md)");
+    hp.L = L;
+    hp.S = int64_t(1) << (L - 1);
+    hp.B = hp.S * hp.S;
+    hp.h = 1.0 / (double)hp.S;
+    const int64_t S = hp.S, B = hp.B;
+
+    // ---- a2, a3 (P = 1: the local sets are the global ones)
+    P.alloc(P.src_uidx, (size_t)d.n_src * 4);
+    P.alloc(P.tgt_uidx, (size_t)d.n_tgt * 4);
+    P.alloc(P.src_off, (size_t)(B + 1) * 4);
+    P.alloc(P.tgt_off, (size_t)(B + 1) * 4);
+    int32_t *sperm = (int32_t *)P.src_uidx.p, *tperm = (int32_t *)P.tgt_uidx.p;
+    int32_t *so = (int32_t *)P.src_off.p, *to = (int32_t *)P.tgt_off.p;
+    device_csr(tmp, dsrc, d.n_src, L, S, B, sperm, so, s);
+    device_csr(tmp, dtgt, d.n_tgt, L, S, B, tperm, to, s);
+
+    // ---- box statistics and E1 source counts
+    int32_t *n9 = tmp.get<int32_t>(B);
+    {
+        unsigned long long *acc = tmp.get<unsigned long long>(3), ha[3];
+        ck(cudaMemsetAsync(acc, 0, 3 * sizeof(unsigned long long), s), "memset");
+        box_stats_kernel<<<nblocks(B), kB, 0, s>>>(so, to, B, S, n9, acc);
+        d2h(ha, acc, 3, s);
+        hp.occ_src = (int64_t)ha[0];
+        hp.occ_tgt = (int64_t)ha[1];
+        hp.t_max = (int64_t)ha[2];
+    }
+    hp.density = (double)hp.n_tgt / (double)hp.B;
+    hp.density_occ = hp.occ_tgt ? (double)hp.n_tgt / (double)hp.occ_tgt : 0.0;
+
+    // ---- CTA tile size (the host builder's rule: smallest k whose non-empty tiles hold >= 115 targets)
+    const int kmax = std::min(L - 1, p2p::kMaxTileLog2);
+    int k;
+    if (d.tile_log2 >= 0) {
+        k = std::min(d.tile_log2, kmax);
+    } else {
+        unsigned long long *ne = tmp.get<unsigned long long>(8), hn[8];
+        ck(cudaMemsetAsync(ne, 0, 8 * sizeof(unsigned long long), s), "memset");
+        tile_count_kernel<<<nblocks(B), kB, 0, s>>>(to, B, kmax, ne);
+        d2h(hn, ne, kmax + 1, s);
+        k = kmax;
+        for (int kk = 0; kk <= kmax; ++kk)
+            if ((double)hp.n_tgt / (double)std::max<int64_t>((int64_t)hn[kk], 1) >= 115.0) {
+                k = kk;
+                break;
+            }
+    }
+    int32_t *tiles_m = nullptr;  // non-empty tiles, Morton order (= TILED slot order)
+    int64_t *tile_pairs = nullptr;
+    int64_t nt = 0;
+    unsigned long long hs[6];
+    for (;; --k) {
+        const int64_t WW = int64_t(1) << (2 * k), ntile_all = B / WW;
+        int32_t *flag = tmp.get<int32_t>(ntile_all), *pos = tmp.get<int32_t>(ntile_all);
+        tile_flag_kernel<<<nblocks(ntile_all), kB, 0, s>>>(to, ntile_all, WW, flag);
+        size_t tb = 0;
+        ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, (int)ntile_all, s), "cub scan");
+        void *t = tmp.get<char>((int64_t)tb);
+        ck(cub::DeviceScan::ExclusiveSum(t, tb, flag, pos, (int)ntile_all, s), "cub scan");
+        int32_t lastp[2];
+        ck(cudaMemcpyAsync(&lastp[0], pos + ntile_all - 1, 4, cudaMemcpyDeviceToHost, s), "D2H");
+        d2h(&lastp[1], flag + ntile_all - 1, 1, s);
+        nt = (int64_t)lastp[0] + lastp[1];
+        tiles_m = tmp.get<int32_t>(nt);
+        tile_pairs = tmp.get<int64_t>(nt);
+        compact_kernel<<<nblocks(ntile_all), kB, 0, s>>>(flag, pos, ntile_all, tiles_m);
+        unsigned long long *st = tmp.get<unsigned long long>(6);
+        ck(cudaMemsetAsync(st, 0, 6 * sizeof(unsigned long long), s), "memset");
+        if (nt) tile_stats_kernel<<<nblocks(nt, 64), 64, 0, s>>>(tiles_m, nt, k, S, so, to, n9, tile_pairs, st);
+        d2h(hs, st, 6, s);
+        p2p::TileStats ts;
+        ts.ntiles = nt;
+        ts.max_region_pad = (int64_t)hs[0];
+        ts.max_region = (int64_t)hs[1];
+        ts.max_tcount = (int64_t)hs[2];
+        ts.max_tcount2 = (int64_t)hs[3];
+        const int64_t smem = p2p::choose_tile_params(d, hp, k, ts);
+        if (smem <= p2p::kSmemLimit) break;
+        if (k == 0 || d.tile_log2 >= 0)
+            throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "a tile's near-field sources need " + std::to_string(smem) +
+                                                          " B of shared memory (> 200 KB); use a deeper level (CT loop) -- see DESIGN.md");
+    }
+    hp.k = k;
+    {
+        int g = 1;
+        while (g < 5 && (double)(1 << g) < hp.density_occ) ++g;
+        hp.group_log2 = g;
+    }
+    const int64_t W = int64_t(1) << k, WW = W * W, R = W + 2;
+    hp.pairs_global = hp.pairs = (int64_t)hs[5];
+    hp.part_tile = {0, nt};
+    hp.part_src = {0, hp.n_src};
+    hp.part_tgt = {0, hp.n_tgt};
+    hp.boxes_in_tiles = nt * WW;
+    hp.src_owned_begin = 0;
+    hp.n_src_owned = hp.n_src_local = hp.n_src;
+    hp.tgt_begin = 0;
+    hp.n_tgt_local = hp.n_tgt;
+    hp.owned_local_begin = 0;
+    hp.n_halo = hp.n_send = 0;
+    hp.recv_counts.assign(1, 0);
+    hp.send_counts.assign(1, 0);
+
+    // ---- a5 point coordinates: box-local (NR sources; targets for every layout)
+    P.alloc(P.tgt_uv, (size_t)hp.n_tgt * 2 * e);
+    uv_kernel<T><<<nblocks(hp.n_tgt), kB, 0, s>>>((const double2 *)dtgt, tperm, hp.n_tgt, S, hp.h, (T *)P.tgt_uv.p);
+    if (d.layout == P2P_LAYOUT_NONREDUNDANT) {
+        P.alloc(P.src_uv, (size_t)hp.n_src * 2 * e);
+        uv_kernel<T><<<nblocks(hp.n_src), kB, 0, s>>>((const double2 *)dsrc, sperm, hp.n_src, S, hp.h, (T *)P.src_uv.p);
+    }
+
+    // ---- TILED layout (per Morton-order tile = slot)
+    int32_t *nparts = tmp.get<int32_t>(nt);
+    if (d.layout == P2P_LAYOUT_TILED) {
+        const int ts = p2p::tiled_table_stride(k);
+        hp.table_entries = nt * ts;
+        P.alloc(P.reg_table, (size_t)hp.table_entries * 2);
+        if (hp.table_entries) ck(cudaMemsetAsync(P.reg_table.p, 0, P.reg_table.bytes, s), "memset");
+        uint32_t *reg_sz = tmp.get<uint32_t>(nt), *slot_sz = tmp.get<uint32_t>(nt), *item_sz = tmp.get<uint32_t>(nt);
+        int *err = tmp.get<int>(1);
+        ck(cudaMemsetAsync(err, 0, sizeof(int), s), "memset");
+        P.alloc(P.tile_tgt_base, (size_t)nt * 4);
+        if (nt)
+            tiled_table_kernel<<<nblocks(nt, 64), 64, 0, s>>>(tiles_m, nt, k, S, ts, hp.pad, hp.tpi, hp.ns, so, to,
+                                                             (uint16_t *)P.reg_table.p, reg_sz, slot_sz, item_sz,
+                                                             (int32_t *)P.tile_tgt_base.p, err);
+        int herr = 0;
+        d2h(&herr, err, 1, s);
+        if (herr & 1) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "TILED region exceeds 65535 entries; use NR");
+        if (herr & 2)
+            throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "TILED tile exceeds its target-slot limit; use a deeper level or NR");
+        P.alloc(P.reg_off, (size_t)(nt + 1) * 4);
+        P.alloc(P.tgt_pack_off, (size_t)(nt + 1) * 4);
+        hp.reg_entries = scan_offsets(tmp, reg_sz, (uint32_t *)P.reg_off.p, nt, s);
+        const int64_t np = scan_offsets(tmp, slot_sz, (uint32_t *)P.tgt_pack_off.p, nt, s);
+        // packed regions: pads keep index -1 and coordinate 1e4
+        P.alloc(P.reg_idx, (size_t)hp.reg_entries * 4);
+        P.alloc(P.reg_uidx, (size_t)hp.reg_entries * 4);
+        P.alloc(P.reg_uv, (size_t)hp.reg_entries * 2 * e);
+        fill_kernel<int32_t><<<nblocks(hp.reg_entries), kB, 0, s>>>((int32_t *)P.reg_idx.p, hp.reg_entries, -1);
+        fill_kernel<int32_t><<<nblocks(hp.reg_entries), kB, 0, s>>>((int32_t *)P.reg_uidx.p, hp.reg_entries, -1);
+        fill_kernel<T><<<nblocks(2 * hp.reg_entries), kB, 0, s>>>((T *)P.reg_uv.p, 2 * hp.reg_entries, (T)1.0e4);
+        if (nt)
+            tiled_region_kernel<T><<<nblocks(nt, 1), 128, 0, s>>>(tiles_m, nt, k, S, hp.h, ts, hp.pad, so, sperm,
+                                                                  (const double2 *)dsrc, (const uint16_t *)P.reg_table.p,
+                                                                  (const uint32_t *)P.reg_off.p, (int32_t *)P.reg_idx.p,
+                                                                  (int32_t *)P.reg_uidx.p, (T *)P.reg_uv.p);
+        // target slots
+        P.alloc(P.tgt_bl, (size_t)np * 2);
+        P.alloc(P.tgt_oix, (size_t)np * 2);
+        P.alloc(P.tgt_ruv, (size_t)np * 2 * e);
+        if (np) {
+            ck(cudaMemsetAsync(P.tgt_bl.p, 0, P.tgt_bl.bytes, s), "memset");
+            ck(cudaMemsetAsync(P.tgt_oix.p, 0xFF, P.tgt_oix.bytes, s), "memset");
+            ck(cudaMemsetAsync(P.tgt_ruv.p, 0, P.tgt_ruv.bytes, s), "memset");
+        }
+        const size_t slot_smem = (size_t)3 * WW * 4;
+        ck(cudaFuncSetAttribute(tiled_slots_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024),
+           "smem attr");
+        if (nt)
+            tiled_slots_kernel<T><<<nblocks(nt, 1), 128, slot_smem, s>>>(
+                tiles_m, nt, k, hp.h, hp.tpi, hp.tsort ? 1 : 0, to, n9, tperm, (const double2 *)dtgt,
+                (const uint32_t *)P.tgt_pack_off.p, (uint16_t *)P.tgt_bl.p, (uint16_t *)P.tgt_oix.p, (T *)P.tgt_ruv.p);
+        // ---- queue order: longest first when the working set fits L2, else Morton with the tail split
+        if (hp.ns == 3) {
+            P.alloc(P.item_off, (size_t)(nt + 1) * 4);
+            const int64_t ni = scan_offsets(tmp, item_sz, (uint32_t *)P.item_off.p, nt, s);
+            P.alloc(P.items, (size_t)ni * 2);
+            if (ni) ck(cudaMemsetAsync(P.items.p, 0, P.items.bytes, s), "memset");
+        }
+    }
+    const int64_t ws = (hp.n_src_local + hp.n_tgt_local) * 3 * (int64_t)e + 8 * hp.boxes_in_tiles +
+                       (hp.halo_entries + hp.reg_entries) * 3 * (int64_t)e;
+    hp.lpt = ws < (int64_t)100 << 20;
+    if (const char *v = std::getenv("P2P_LPT")) hp.lpt = std::atoi(v) != 0;
+    int32_t *order = nullptr;
+    if (hp.lpt && nt > 1) {  // stable sort by descending pair count (CUB's radix sort is stable)
+        uint64_t *ks = tmp.get<uint64_t>(nt);
+        int32_t *iot = tmp.get<int32_t>(nt);
+        order = tmp.get<int32_t>(nt);
+        iota_kernel<<<nblocks(nt), kB, 0, s>>>(iot, nt);
+        size_t tb = 0;
+        ck(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, (const uint64_t *)tile_pairs, ks, iot, order, (int)nt,
+                                                      0, 64, s),
+           "cub sort");
+        void *t = tmp.get<char>((int64_t)tb);
+        ck(cub::DeviceRadixSort::SortPairsDescending(t, tb, (const uint64_t *)tile_pairs, ks, iot, order, (int)nt, 0, 64,
+                                                      s),
+           "cub sort");
+    }
+    int64_t keep = nt;
+    int parts = 1;
+    if (d.layout == P2P_LAYOUT_TILED) {
+        int64_t tail = hp.lpt ? 0 : 148 * 4;
+        int pp = 4;
+        if (const char *v = std::getenv("P2P_TAIL_TILES")) tail = std::atoll(v);
+        if (const char *v = std::getenv("P2P_TAIL_PARTS")) pp = std::max(1, std::min(16, std::atoi(v)));
+        tail = std::min<int64_t>(tail, nt / 2);
+        if (pp > 1 && tail > 0) {
+            keep = nt - tail;
+            parts = pp;
+        }
+    }
+    const int64_t nent = keep + (nt - keep) * parts;
+    P.alloc(P.tiles, (size_t)nent * 4);
+    P.alloc(P.tile_slot, (size_t)nent * 4);
+    P.alloc(P.tile_part, (size_t)nent * 4);
+    if (nent)
+        queue_kernel<<<nblocks(nent), kB, 0, s>>>(order, tiles_m, nt, keep, parts, (int32_t *)P.tiles.p,
+                                                  (int32_t *)P.tile_slot.p, (int32_t *)P.tile_part.p, nparts);
+    hp.n_interior = nent;
+    hp.tiles.resize((size_t)nent);
+    d2h(hp.tiles.data(), P.tiles.p, nent, s);
+    // ---- NS = 3 item lists (TILED)
+    if (d.layout == P2P_LAYOUT_TILED && hp.ns == 3 && nt) {
+        const int64_t maxitems = 3 * (hp.tgt_cap / hp.tpi) + 8;
+        const size_t ism = (size_t)maxitems * 3 * 4;
+        if (ism > 160 * 1024) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "device build: tile item list too large");
+        ck(cudaFuncSetAttribute(tiled_items_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
+           "smem attr");
+        tiled_items_kernel<<<nblocks(nt, 1), 128, ism, s>>>(nt, k, p2p::tiled_table_stride(k), hp.tpi, hp.nt,
+                                                           (const uint16_t *)P.reg_table.p,
+                                                           (const uint32_t *)P.tgt_pack_off.p,
+                                                           (const uint16_t *)P.tgt_bl.p, nparts,
+                                                           (const uint32_t *)P.item_off.p, (uint16_t *)P.items.p);
+    }
+    (void)R;
+    if (d.precision == P2P_FP64) {
+        p2p::build_log_table(hp);
+        P.upload(P.log_tab, hp.log_tab);
+    }
+    ck(cudaGetLastError(), "device build launch");
+    finalize_plan<T>(P);
+    ck(cudaStreamSynchronize(s), "device build sync");
+    hp.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Host copies of a device-built plan's arrays, for p2p_plan_export (on first use).
+void mirror_device_plan(p2p_plan_s &P) {
+    p2p::HostPlan &hp = P.hp;
+    if (!hp.device_built || !hp.src_off_g.empty()) return;
+    DeviceGuard g(P.device);
+    cudaStream_t s = P.stream;
+    auto get = [&](auto &vec, const DevBuf &b) {
+        using V = typename std::decay_t<decltype(vec)>::value_type;
+        vec.resize(b.bytes / sizeof(V));
+        d2h(vec.data(), b.p, (int64_t)vec.size(), s);
+    };
+    get(hp.src_uidx, P.src_uidx);
+    get(hp.tgt_uidx, P.tgt_uidx);
+    hp.src_perm_g = hp.src_uidx;
+    hp.tgt_perm_g = hp.tgt_uidx;
+    get(hp.src_off_g, P.src_off);
+    get(hp.tgt_off_g, P.tgt_off);
+    hp.src_off = hp.src_off_g;
+    hp.tgt_off = hp.tgt_off_g;
+    hp.src_gidx.resize((size_t)hp.n_src);
+    std::iota(hp.src_gidx.begin(), hp.src_gidx.end(), 0);
+    get(hp.tile_slot, P.tile_slot);
+    get(hp.tile_part, P.tile_part);
+    if (hp.layout == P2P_LAYOUT_TILED) {
+        get(hp.reg_off, P.reg_off);
+        get(hp.reg_idx, P.reg_idx);
+        get(hp.reg_uidx, P.reg_uidx);
+        get(hp.reg_table, P.reg_table);
+        get(hp.tgt_pack_off, P.tgt_pack_off);
+        get(hp.tgt_bl, P.tgt_bl);
+        get(hp.tgt_oix, P.tgt_oix);
+        get(hp.tile_tgt_base, P.tile_tgt_base);
+        get(hp.item_off, P.item_off);
+        get(hp.items, P.items);
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -457,6 +880,48 @@ p2p_status p2p_plan_create(const p2p_plan_desc *desc, p2p_plan *out) {
                 throw;
             }
             P->upload_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+    if (st == P2P_SUCCESS) *out = P.release();
+    return st;
+}
+
+p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src_xy, const double *d_tgt_xy,
+                                  p2p_plan *out) {
+    if (out) *out = nullptr;
+    if (!desc || !out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL desc or out");
+    std::unique_ptr<p2p_plan_s> P(new (std::nothrow) p2p_plan_s());
+    if (!P) return set_error(P2P_ERROR_OUT_OF_MEMORY, "host allocation failed");
+    p2p_status st = guarded([&] {
+        const p2p_plan_desc &d = *desc;
+        if (d.struct_size != sizeof(p2p_plan_desc)) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
+        if (d.kernel != P2P_KERNEL_LAPLACE_2D) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "only P2P_KERNEL_LAPLACE_2D");
+        if (d.precision != P2P_FP32 && d.precision != P2P_FP64) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "bad precision");
+        if (d.layout != P2P_LAYOUT_NONREDUNDANT && d.layout != P2P_LAYOUT_TILED)
+            throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "device build: NR and TILED layouts only (others: p2p_plan_create)");
+        if (d.part_world != 1 || d.part_rank != 0)
+            throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "device build: one partition only (part_world = 1)");
+        if (!(d.epsilon > 0.0) || !std::isfinite(d.epsilon)) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "epsilon must be > 0");
+        if (d.n_src < 1 || d.n_tgt < 1) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "n must be >= 1 (SPEC.md L55)");
+        if (!d_src_xy || !d_tgt_xy) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "NULL device coordinates");
+        if (d.n_src > INT32_MAX - 8 || d.n_tgt > INT32_MAX - 8)
+            throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "more than 2^31 points per set");
+        if (d.device < 0) throw p2p::Error(P2P_ERROR_NO_DEVICE, "device build needs a CUDA device (device >= 0)");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw p2p::Error(P2P_ERROR_NO_DEVICE, "no CUDA device visible");
+        if (d.device >= ndev) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "device ordinal out of range");
+        DeviceGuard g(d.device);
+        P->device = d.device;
+        P->elem = d.precision == P2P_FP32 ? 4 : 8;
+        P->stream = (cudaStream_t)d.stream;
+        try {
+            if (d.precision == P2P_FP32) build_device_plan<float>(*P, d, d_src_xy, d_tgt_xy);
+            else build_device_plan<double>(*P, d, d_src_xy, d_tgt_xy);
+        } catch (...) {
+            cudaStreamSynchronize(P->stream);
+            P->release();
+            throw;
         }
     });
     if (st == P2P_SUCCESS) *out = P.release();
@@ -617,7 +1082,7 @@ p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *out) {
         // targets: region-relative coords + row-run base (+ output index) + out; region: coords +
         // index; tables; weights gathered once from plan order
         info->layout_bytes_apply = hp.n_tgt_local * (3 * e + 2 + (hp.lean ? 2 : 0)) +
-                                   hp.reg_entries * (2 * e + 4) + (int64_t)hp.reg_table.size() * 2 +
+                                   hp.reg_entries * (2 * e + 4) + hp.table_entries * 2 +
                                    hp.n_src_local * e;
     } else {
         info->layout_bytes_apply = hp.n_tgt_local * 3 * e + hp.halo_entries * 3 * e + offs +
@@ -641,6 +1106,7 @@ p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *out) {
 p2p_status p2p_plan_export(p2p_plan P, int32_t kind, void *host_dst, size_t *bytes) {
     if (!P || !bytes) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or bytes");
     return guarded([&] {
+        mirror_device_plan(*P);
         const p2p::HostPlan &hp = P->hp;
         std::vector<int64_t> v;
         auto take = [&](const auto &src) { v.assign(src.begin(), src.end()); };

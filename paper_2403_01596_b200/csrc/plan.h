@@ -223,6 +223,8 @@ struct HostPlan {
     std::vector<int32_t> tile_slot;               // launch order -> slot
     std::vector<int32_t> tile_part;               // launch order -> part | nparts << 16 (tail splitting)
     int64_t reg_entries = 0;
+    int64_t table_entries = 0;                    // TILED: uint16 entries of the region tables (tiles x stride)
+    bool device_built = false;                    // built by the device builder (p2p_plan_create_device)
 
     Layout<float> f32;
     Layout<double> f64;
@@ -237,7 +239,21 @@ struct HostPlan {
     double density = 0.0, density_occ = 0.0, build_seconds = 0.0;
 };
 
+// Per-tile maxima at a candidate tile size (the inputs of the kernel-option choice).
+struct TileStats {
+    int64_t ntiles = 0;          // non-empty tiles
+    int64_t max_region_pad = 0;  // region (tile + ring) sources, boxes padded to even counts
+    int64_t max_region = 0;      // region sources, unpadded
+    int64_t max_tile_halo = 0;   // R layout: packed halo entries of a tile
+    int64_t max_tcount = 0;      // targets of a tile
+    int64_t max_tcount2 = 0;     // target slots of a tile with 2-slot units (odd boxes padded)
+};
+// Kernel options (tpi, pad, ns, nt, lean, tsort, flat, caps) and shared memory per CTA at tile
+// size k; used by both builders so they take the same decisions.  Returns hp.smem_bytes.
+int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const TileStats &st);
+
 void build_host_plan(const p2p_plan_desc &desc, HostPlan &hp);
+void build_log_table(HostPlan &hp);
 std::vector<int64_t> neighbors_export(const HostPlan &hp);
 
 }  // namespace p2p

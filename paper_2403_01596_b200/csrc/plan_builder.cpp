@@ -173,6 +173,84 @@ void balance_batches(const std::vector<int32_t> &ord, const std::vector<int32_t>
 
 }  // namespace
 
+// fp64 log table: (c_inv_k, -log c_inv_k), c_inv_k = 1 / (1 + (k + 1/2) / 128) rounded to double,
+// the log from the 64-bit-mantissa long double logl (the kernels' `log_tab`).
+void build_log_table(HostPlan &hp) {
+    hp.log_tab.resize(2 * kLogTab);
+    for (int kk = 0; kk < kLogTab; ++kk) {
+        const double c = 1.0 + (kk + 0.5) / kLogTab;
+        const double cinv = 1.0 / c;
+        hp.log_tab[2 * kk] = cinv;
+        hp.log_tab[2 * kk + 1] = (double)(-logl((long double)cinv));
+    }
+}
+
+// Kernel options and shared-memory size of a plan at tile size k, from its tile statistics
+// (shared by the host and the device builders, so both make the same decisions).
+int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const TileStats &st) {
+    const int e = d.precision == P2P_FP32 ? 4 : 8;
+    hp.max_region = st.max_region_pad;
+    hp.max_tile_halo = st.max_tile_halo;
+    hp.src_cap = d.layout == P2P_LAYOUT_REDUNDANT ? hp.max_tile_halo : pad4(hp.max_region);
+    hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= 8.0 && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT) ? 2 : 1;
+    // TILED defaults: dense fp32 -> padded pairs, 2 targets per unit, (unit, row) items;
+    // sparse or fp64 -> unpadded, one item per target; 128-thread CTAs.
+    hp.pad = d.layout == P2P_LAYOUT_TILED ? (hp.tpi == 2) : true;
+    // fp64 dense boxes: (target, row-run) items too (sorted), 256-thread CTAs (tools/gpu_ab11.sh)
+    const bool dense64 = d.precision == P2P_FP64 && hp.density_occ >= 8.0;
+    hp.ns = hp.tpi > 1 || dense64 ? 3 : 1;
+    hp.nbuf = 1;
+    // measured best (tools/gpu_ab*.sh): 128 threads for dense fp32 units and sparse fp64,
+    // 256 for dense fp64, 64 (or 32, below) for sparse fp32
+    hp.nt = d.layout == P2P_LAYOUT_TILED
+                ? (dense64 ? 256 : hp.tpi > 1 || d.precision == P2P_FP64 ? 128 : 64) : kThreads;
+    // tuning hooks (experiments only): P2P_TPI, P2P_NS, P2P_NBUF, P2P_PAD, P2P_NT
+    if (const char *v = std::getenv("P2P_TPI"))
+        if (d.precision == P2P_FP32 && d.layout != P2P_LAYOUT_REDUNDANT) {
+            const int x = std::atoi(v);
+            hp.tpi = x == 2 ? 2 : 1;
+        }
+    if (const char *v = std::getenv("P2P_PAD"))
+        if (d.layout == P2P_LAYOUT_TILED && d.precision == P2P_FP32) hp.pad = std::atoi(v) != 0;
+    if (hp.tpi > 1) hp.pad = true;
+    if (d.precision == P2P_FP64 && d.layout == P2P_LAYOUT_TILED) hp.pad = false;
+    if (const char *v = std::getenv("P2P_NS")) hp.ns = std::atoi(v) == 3 ? 3 : 1;
+    if (const char *v = std::getenv("P2P_NBUF")) hp.nbuf = std::atoi(v) == 2 ? 2 : 1;
+    if (const char *v = std::getenv("P2P_NT"))
+        if (d.layout == P2P_LAYOUT_TILED) {
+            const int x = std::atoi(v);
+            hp.nt = x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : 256;
+        }
+    // lean sparse path: targets of a tile sorted by neighbourhood size (n9), so the
+    // lanes of a warp sweep near-equal pair counts (P2P_TSORT=0 disables)
+    hp.lean = d.layout == P2P_LAYOUT_TILED && hp.tpi == 1 && hp.ns == 1 && !hp.pad;
+    hp.tsort = hp.lean;
+    if (hp.nt == 32 && !hp.lean) hp.nt = 64;  // one-warp CTAs: lean instances only
+    // lean fp32: ~4 targets per thread measured best (tools/gpu_prof5.sh): one-warp CTAs for small tiles
+    if (hp.lean && d.precision == P2P_FP32 && !std::getenv("P2P_NT") &&
+        (double)hp.n_tgt / (double)std::max<int64_t>(st.ntiles, 1) < 192.0)
+        hp.nt = 32;
+    if (const char *v = std::getenv("P2P_TSORT")) hp.tsort = hp.ns == 1 && std::atoi(v) != 0;
+    // flattened row-runs pay below ~3 sources per box (more index work per pair,
+    // fewer idle lanes) and always in fp64 (the log dwarfs the index work); above,
+    // row loops (P2P_FLAT overrides)
+    hp.flat = hp.lean && (hp.density_occ < 3.0 || d.precision == P2P_FP64);
+    if (const char *v = std::getenv("P2P_FLAT")) hp.flat = hp.lean && std::atoi(v) != 0;
+    hp.tgt_cap = pad8(d.layout == P2P_LAYOUT_TILED && hp.tpi == 2 ? st.max_tcount2 : st.max_tcount);
+    if (d.layout == P2P_LAYOUT_TILED && !hp.pad) hp.src_cap = pad4(st.max_region);  // unpadded region sizes
+    if (d.layout == P2P_LAYOUT_PAPER_INDEXING || d.layout == P2P_LAYOUT_PAPER_REPETITION) {
+        hp.smem_bytes = 0;  // global-memory kernels: no tiles to size
+        return 0;
+    }
+    const int sc = (int)std::min<int64_t>(hp.src_cap, 1 << 24), tc = (int)std::min<int64_t>(hp.tgt_cap, 1 << 24);
+    int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? (int64_t)nr_carve(k, sc, tc, e, hp.tpi).total
+                   : d.layout == P2P_LAYOUT_TILED
+                       ? (int64_t)tiled_carve(k, sc, tc, e, hp.tpi, hp.ns, hp.nbuf).total
+                                                       : (int64_t)r_carve(k, sc, tc, e).total;
+    hp.smem_bytes = smem;
+    return smem;
+}
+
 void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     auto t0 = std::chrono::steady_clock::now();
     if (d.struct_size != sizeof(p2p_plan_desc)) fail(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
@@ -278,7 +356,8 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             if (to[(t + 1) * WW] > to[t * WW]) hp.tiles_g.push_back((int32_t)t);
         const int64_t nt = (int64_t)hp.tiles_g.size();
         hp.tile_pairs_g.assign((size_t)nt, 0);
-        std::vector<int64_t> region((size_t)nt, 0), halo((size_t)nt, 0), tcount((size_t)nt, 0), tcount2((size_t)nt, 0);
+        std::vector<int64_t> region((size_t)nt, 0), region_u((size_t)nt, 0), halo((size_t)nt, 0), tcount((size_t)nt, 0),
+            tcount2((size_t)nt, 0);
         parallel_for(nt, [&](int64_t a, int64_t bnd) {
             for (int64_t i = a; i < bnd; ++i) {
                 int64_t t = hp.tiles_g[i];
@@ -292,13 +371,16 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                 }
                 uint32_t tx, ty;
                 morton_decode((uint32_t)t, tx, ty);
-                int64_t X0 = (int64_t)tx * W - 1, Y0 = (int64_t)ty * W - 1, rg = 0;
+                int64_t X0 = (int64_t)tx * W - 1, Y0 = (int64_t)ty * W - 1, rg = 0, rgu = 0;
                 for (int64_t ly = 0; ly < R; ++ly)
                     for (int64_t lx = 0; lx < R; ++lx) {
                         int64_t x = X0 + lx, y = Y0 + ly;
                         if (x < 0 || y < 0 || x >= S || y >= S) continue;
-                        rg += pad2(ns(morton_encode((uint32_t)x, (uint32_t)y)));
+                        const int64_t c = ns(morton_encode((uint32_t)x, (uint32_t)y));
+                        rg += pad2(c);
+                        rgu += c;
                     }
+                region_u[i] = rgu;
                 hp.tile_pairs_g[i] = pr;
                 tcount[i] = to[(t + 1) * WW] - to[t * WW];
                 tcount2[i] = sl2;
@@ -306,83 +388,16 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                 halo[i] = pad4(hl);
             }
         }, 256);
-        hp.max_region = region.empty() ? 0 : *std::max_element(region.begin(), region.end());
-        hp.max_tile_halo = halo.empty() ? 0 : *std::max_element(halo.begin(), halo.end());
-        hp.src_cap = d.layout == P2P_LAYOUT_REDUNDANT ? hp.max_tile_halo : pad4(hp.max_region);
-        hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= 8.0 && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT) ? 2 : 1;
-        // TILED defaults: dense fp32 -> padded pairs, 2 targets per unit, (unit, row) items;
-        // sparse or fp64 -> unpadded, one item per target; 128-thread CTAs.
-        hp.pad = d.layout == P2P_LAYOUT_TILED ? (hp.tpi == 2) : true;
-        // fp64 dense boxes: (target, row-run) items too (sorted), 256-thread CTAs (tools/gpu_ab11.sh)
-        const bool dense64 = d.precision == P2P_FP64 && hp.density_occ >= 8.0;
-        hp.ns = hp.tpi > 1 || dense64 ? 3 : 1;
-        hp.nbuf = 1;
-        // measured best (tools/gpu_ab*.sh): 128 threads for dense fp32 units and sparse fp64,
-        // 256 for dense fp64, 64 (or 32, below) for sparse fp32
-        hp.nt = d.layout == P2P_LAYOUT_TILED
-                    ? (dense64 ? 256 : hp.tpi > 1 || d.precision == P2P_FP64 ? 128 : 64) : kThreads;
-        // tuning hooks (experiments only): P2P_TPI, P2P_NS, P2P_NBUF, P2P_PAD, P2P_NT
-        if (const char *v = std::getenv("P2P_TPI"))
-            if (d.precision == P2P_FP32 && d.layout != P2P_LAYOUT_REDUNDANT) {
-                const int x = std::atoi(v);
-                hp.tpi = x == 2 ? 2 : 1;
-            }
-        if (const char *v = std::getenv("P2P_PAD"))
-            if (d.layout == P2P_LAYOUT_TILED && d.precision == P2P_FP32) hp.pad = std::atoi(v) != 0;
-        if (hp.tpi > 1) hp.pad = true;
-        if (d.precision == P2P_FP64 && d.layout == P2P_LAYOUT_TILED) hp.pad = false;
-        if (const char *v = std::getenv("P2P_NS")) hp.ns = std::atoi(v) == 3 ? 3 : 1;
-        if (const char *v = std::getenv("P2P_NBUF")) hp.nbuf = std::atoi(v) == 2 ? 2 : 1;
-        if (const char *v = std::getenv("P2P_NT"))
-            if (d.layout == P2P_LAYOUT_TILED) {
-                const int x = std::atoi(v);
-                hp.nt = x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : 256;
-            }
-        // lean sparse path: targets of a tile sorted by neighbourhood size (n9), so the
-        // lanes of a warp sweep near-equal pair counts (P2P_TSORT=0 disables)
-        hp.lean = d.layout == P2P_LAYOUT_TILED && hp.tpi == 1 && hp.ns == 1 && !hp.pad;
-        hp.tsort = hp.lean;
-        if (hp.nt == 32 && !hp.lean) hp.nt = 64;  // one-warp CTAs: lean instances only
-        // lean fp32: ~4 targets per thread measured best (tools/gpu_prof5.sh): one-warp CTAs for small tiles
-        if (hp.lean && d.precision == P2P_FP32 && !std::getenv("P2P_NT") &&
-            (double)hp.n_tgt / (double)std::max<size_t>(hp.tiles_g.size(), 1) < 192.0)
-            hp.nt = 32;
-        if (const char *v = std::getenv("P2P_TSORT")) hp.tsort = hp.ns == 1 && std::atoi(v) != 0;
-        // flattened row-runs pay below ~3 sources per box (more index work per pair,
-        // fewer idle lanes) and always in fp64 (the log dwarfs the index work); above,
-        // row loops (P2P_FLAT overrides)
-        hp.flat = hp.lean && (hp.density_occ < 3.0 || d.precision == P2P_FP64);
-        if (const char *v = std::getenv("P2P_FLAT")) hp.flat = hp.lean && std::atoi(v) != 0;
-        {
-            const auto &tc = d.layout == P2P_LAYOUT_TILED && hp.tpi == 2 ? tcount2 : tcount;
-            hp.tgt_cap = pad8(tc.empty() ? 0 : *std::max_element(tc.begin(), tc.end()));
-        }
-        if (d.layout == P2P_LAYOUT_TILED && !hp.pad) {  // unpadded region sizes
-            int64_t mx = 0;
-            for (int64_t i = 0; i < nt; ++i) {
-                uint32_t tx, ty;
-                morton_decode((uint32_t)hp.tiles_g[i], tx, ty);
-                int64_t X0 = (int64_t)tx * W - 1, Y0 = (int64_t)ty * W - 1, rg = 0;
-                for (int64_t ly = 0; ly < R; ++ly)
-                    for (int64_t lx = 0; lx < R; ++lx) {
-                        int64_t x = X0 + lx, y = Y0 + ly;
-                        if (x < 0 || y < 0 || x >= S || y >= S) continue;
-                        rg += ns(morton_encode((uint32_t)x, (uint32_t)y));
-                    }
-                mx = std::max(mx, rg);
-            }
-            hp.src_cap = pad4(mx);
-        }
-        if (paper) {  // global-memory kernels: no tiles to size
-            hp.smem_bytes = 0;
-            break;
-        }
-        const int sc = (int)std::min<int64_t>(hp.src_cap, 1 << 24), tc = (int)std::min<int64_t>(hp.tgt_cap, 1 << 24);
-        int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? (int64_t)nr_carve(k, sc, tc, e, hp.tpi).total
-                       : d.layout == P2P_LAYOUT_TILED
-                           ? (int64_t)tiled_carve(k, sc, tc, e, hp.tpi, hp.ns, hp.nbuf).total
-                                                           : (int64_t)r_carve(k, sc, tc, e).total;
-        hp.smem_bytes = smem;
+        auto vmax = [](const std::vector<int64_t> &v) { return v.empty() ? int64_t(0) : *std::max_element(v.begin(), v.end()); };
+        TileStats st;
+        st.ntiles = nt;
+        st.max_region_pad = vmax(region);
+        st.max_region = vmax(region_u);
+        st.max_tile_halo = vmax(halo);
+        st.max_tcount = vmax(tcount);
+        st.max_tcount2 = vmax(tcount2);
+        const int64_t smem = choose_tile_params(d, hp, k, st);
+        if (paper) break;
         if (smem <= kSmemLimit) break;
         if (k == 0 || d.tile_log2 >= 0)
             fail(P2P_ERROR_NOT_SUPPORTED,
@@ -630,6 +645,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             hp.reg_off[i + 1] = hp.reg_off[i] + (uint32_t)pad4(run);
         }
         hp.reg_entries = hp.reg_off[nlt];
+        hp.table_entries = (int64_t)hp.reg_table.size();
         hp.reg_idx.assign((size_t)hp.reg_entries, -1);
         hp.reg_uidx.assign((size_t)hp.reg_entries, -1);
         const double PADC = 1.0e4;
@@ -816,15 +832,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     // ---- fp64 log table: log x = e ln2 + L_k + log1p(t), t = m c_inv_k - 1, |t| < 2^-8, with
     // c_inv_k = 1 / (1 + (k + 1/2) / 128) rounded to double and L_k = -log(c_inv_k) from the
     // 64-bit-mantissa long double log (the kernel's `log_tab`)
-    if (d.precision == P2P_FP64) {
-        hp.log_tab.resize(2 * kLogTab);
-        for (int kk = 0; kk < kLogTab; ++kk) {
-            const double c = 1.0 + (kk + 0.5) / kLogTab;
-            const double cinv = 1.0 / c;
-            hp.log_tab[2 * kk] = cinv;
-            hp.log_tab[2 * kk + 1] = (double)(-logl((long double)cinv));
-        }
-    }
+    if (d.precision == P2P_FP64) build_log_table(hp);
     // ---- NS = 3 item lists (TILED): per tile, the (unit, row-run) items of each
     // part's unit range [nu*ip/np, nu*(ip+1)/np) sorted by row-run length
     // (descending, stable), so the lanes of a warp sweep near-equal runs.

@@ -49,7 +49,7 @@ EXPORT = {
 
 # Symbols declared in include/p2p.h (checked by tests/test_abi.py).
 ABI_SYMBOLS = (
-    "p2p_plan_desc_init", "p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async",
+    "p2p_plan_desc_init", "p2p_plan_create", "p2p_plan_create_device", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async",
     "p2p_apply_dist", "p2p_apply_dist_interior", "p2p_apply_dist_boundary",
     "p2p_halo_pack", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
     "p2p_status_string", "p2p_last_error", "p2p_abi_version",
@@ -109,6 +109,7 @@ def load_library() -> C.CDLL:
     lib.p2p_plan_desc_init.argtypes = [C.POINTER(PlanDesc)]
     lib.p2p_plan_desc_init.restype = None
     lib.p2p_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(P)]
+    lib.p2p_plan_create_device.argtypes = [C.POINTER(PlanDesc), P, P, C.POINTER(P)]
     lib.p2p_apply.argtypes = [P, P, P, i32, i32, P]
     lib.p2p_apply_host.argtypes = [P, P, P, i32, i32, P]
     lib.p2p_apply_host_async.argtypes = [P, P, P, i32, i32, P]
@@ -123,7 +124,7 @@ def load_library() -> C.CDLL:
     lib.p2p_status_string.restype = C.c_char_p
     lib.p2p_last_error.restype = C.c_char_p
     lib.p2p_abi_version.restype = i32
-    for name in ("p2p_plan_create", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async", "p2p_apply_dist", "p2p_apply_dist_interior",
+    for name in ("p2p_plan_create", "p2p_plan_create_device", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async", "p2p_apply_dist", "p2p_apply_dist_interior",
                  "p2p_apply_dist_boundary", "p2p_halo_pack",
                  "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export"):
         getattr(lib, name).restype = i32
@@ -153,6 +154,14 @@ def p2p_plan_desc_init() -> PlanDesc:
 def p2p_plan_create(desc: PlanDesc) -> C.c_void_p:
     h = C.c_void_p()
     _check(load_library().p2p_plan_create(C.byref(desc), C.byref(h)), "p2p_plan_create")
+    return h
+
+
+def p2p_plan_create_device(desc: PlanDesc, d_src_xy: int, d_tgt_xy: int) -> C.c_void_p:
+    """Plan built on the GPU from device coordinates (fp64 [n][2] on desc.device)."""
+    h = C.c_void_p()
+    _check(load_library().p2p_plan_create_device(C.byref(desc), d_src_xy, d_tgt_xy, C.byref(h)),
+           "p2p_plan_create_device")
     return h
 
 
@@ -219,20 +228,35 @@ class Plan:
     the tile ring only); "paper_i" / "paper_r": the paper's own Indexing / Repetition
     layouts and kernels (fp64); precision: "fp32" or "fp64".
     device: CUDA ordinal, or -1 for a host-only plan (build + export only).
+    build: "host" (p2p_plan_create: the C++ builder on the CPU) or "device"
+    (p2p_plan_create_device: the same plan built by GPU kernels; src_xy / tgt_xy may then
+    be CUDA float64 [n, 2] tensors, numpy input is copied to the device first).
     """
 
     def __init__(self, src_xy, tgt_xy=None, *, level: int = 0, ct: int = 15, l_start: int = 3,
                  l_max: int = 15, level_delta: int = 0, epsilon: float = 1e-12, layout: str = "nr",
                  precision: str = "fp32", device: int = 0, tile_log2: int = -1, stream: int = 0,
-                 part_world: int = 1, part_rank: int = 0):
-        self._src = np.ascontiguousarray(src_xy, dtype=np.float64)
-        self._tgt = self._src if tgt_xy is None else np.ascontiguousarray(tgt_xy, dtype=np.float64)
-        if self._src.ndim != 2 or self._src.shape[1] != 2 or self._tgt.ndim != 2 or self._tgt.shape[1] != 2:
-            raise ValueError("points must be [n, 2] arrays")
+                 part_world: int = 1, part_rank: int = 0, build: str = "host"):
+        if build not in ("host", "device"):
+            raise ValueError("build must be 'host' or 'device'")
         d = p2p_plan_desc_init()
-        d.n_src, d.n_tgt = len(self._src), len(self._tgt)
-        d.src_xy = self._src.ctypes.data
-        d.tgt_xy = self._tgt.ctypes.data
+        if build == "device":
+            import torch
+            dev = torch.device("cuda", device)
+            self._src = torch.as_tensor(src_xy, dtype=torch.float64, device=dev).contiguous()
+            self._tgt = self._src if tgt_xy is None else \
+                torch.as_tensor(tgt_xy, dtype=torch.float64, device=dev).contiguous()
+            if self._src.dim() != 2 or self._src.shape[1] != 2 or self._tgt.dim() != 2 or self._tgt.shape[1] != 2:
+                raise ValueError("points must be [n, 2] arrays")
+            d.n_src, d.n_tgt = self._src.shape[0], self._tgt.shape[0]
+        else:
+            self._src = np.ascontiguousarray(src_xy, dtype=np.float64)
+            self._tgt = self._src if tgt_xy is None else np.ascontiguousarray(tgt_xy, dtype=np.float64)
+            if self._src.ndim != 2 or self._src.shape[1] != 2 or self._tgt.ndim != 2 or self._tgt.shape[1] != 2:
+                raise ValueError("points must be [n, 2] arrays")
+            d.n_src, d.n_tgt = len(self._src), len(self._tgt)
+            d.src_xy = self._src.ctypes.data
+            d.tgt_xy = self._tgt.ctypes.data
         d.level, d.ct, d.l_start, d.l_max, d.level_delta = level, ct, l_start, l_max, level_delta
         d.epsilon = epsilon
         d.layout = {"nr": P2P_LAYOUT_NONREDUNDANT, "r": P2P_LAYOUT_REDUNDANT, "tiled": P2P_LAYOUT_TILED,
@@ -240,8 +264,15 @@ class Plan:
         d.precision = {"fp32": P2P_FP32, "fp64": P2P_FP64}[precision]
         d.device, d.tile_log2, d.stream = device, tile_log2, stream or None
         d.part_world, d.part_rank = part_world, part_rank
-        self.layout, self.precision, self.device = layout, precision, device
-        self._h = p2p_plan_create(d)
+        self.layout, self.precision, self.device, self.build = layout, precision, device, build
+        if build == "device":
+            if not stream:
+                import torch
+                d.stream = torch.cuda.current_stream(device).cuda_stream or None
+            self._h = p2p_plan_create_device(d, self._src.data_ptr(), self._tgt.data_ptr())
+            self._src = self._tgt = None  # read during the call only
+        else:
+            self._h = p2p_plan_create(d)
         self.info = p2p_plan_get_info(self._h)
 
     @property
