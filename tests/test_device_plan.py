@@ -144,7 +144,10 @@ def test_morton_queue_with_split_tail_matches_host(monkeypatch, prec, name):
     cfg = SMALL[name]
     src, tgt, q = W.make_problem(cfg)
     info = _compare(src, tgt, q, level=cfg.level, layout="tiled", precision=prec)
-    assert info["launches"] > info["tiles"] or info["tiles"] < 2
+    with p2p.Plan(src, tgt, level=cfg.level, layout="tiled", precision=prec, build="device") as pl:
+        launch = pl.export("launch")
+    nparts = launch[info["launches"]:] >> 16
+    assert (nparts == 4).any() and (nparts == 1).any()  # a whole-tile head and a split tail
 
 
 @pytest.mark.gpu
