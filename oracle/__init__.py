@@ -76,6 +76,12 @@ def lib():
         _lib.oracle_box_tmax.restype = i64
         _lib.oracle_pair_count.restype = i64
         _lib.oracle_num_threads.restype = i32
+        _lib.oracle_direct_helmholtz.argtypes = [i64, P, P, i64, P, i32, f64, f64, i64, P, P, i32, P]
+        _lib.oracle_direct_helmholtz.restype = i32
+        _lib.oracle_bruteforce_helmholtz.argtypes = [i64, P, P, i64, P, i32, f64, f64, P, P]
+        _lib.oracle_bruteforce_helmholtz.restype = i32
+        _lib.oracle_pair_helmholtz.argtypes = [f64] * 8 + [P]
+        _lib.oracle_pair_helmholtz.restype = None
     return _lib
 
 
@@ -173,3 +179,46 @@ def box_tmax(src_xy, tgt_xy, level: int) -> int:
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+# ---- NEXT-3: the 2D Helmholtz kernel G = (i/4) H0^(1)(kappa r) (oracle.c) ----
+def _c128(a) -> np.ndarray:
+    """complex input -> interleaved (re, im) float64"""
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    return a.view(np.float64)
+
+
+def direct_helmholtz(src_xy, q, tgt_xy, level: int, kappa: float, eps: float = 1e-12, targets=None,
+                     nthreads: int = 0) -> tuple[np.ndarray, int]:
+    """complex phi for all targets (or the index subset ``targets``) and the pair count."""
+    src_xy, tgt_xy = _f64(src_xy), _f64(tgt_xy)
+    qi = _c128(q)
+    sel = None if targets is None else np.ascontiguousarray(targets, dtype=np.int64)
+    n_out = len(tgt_xy) if sel is None else len(sel)
+    phi = np.empty(n_out, dtype=np.complex128)
+    pairs = C.c_int64(0)
+    rc = lib().oracle_direct_helmholtz(len(src_xy), _ptr(src_xy), _ptr(qi), len(tgt_xy), _ptr(tgt_xy),
+                                       level, eps, kappa, 0 if sel is None else len(sel),
+                                       None if sel is None else _ptr(sel), _ptr(phi), nthreads,
+                                       C.byref(pairs))
+    if rc:
+        raise MemoryError("oracle_direct_helmholtz allocation failed")
+    return phi, pairs.value
+
+
+def bruteforce_helmholtz(src_xy, q, tgt_xy, level: int, kappa: float, eps: float = 1e-12):
+    src_xy, tgt_xy = _f64(src_xy), _f64(tgt_xy)
+    qi = _c128(q)
+    phi = np.empty(len(tgt_xy), dtype=np.complex128)
+    pairs = C.c_int64(0)
+    lib().oracle_bruteforce_helmholtz(len(src_xy), _ptr(src_xy), _ptr(qi), len(tgt_xy), _ptr(tgt_xy),
+                                      level, eps, kappa, _ptr(phi), C.byref(pairs))
+    return phi, pairs.value
+
+
+def pair_helmholtz(t, s, q: complex, kappa: float, eps: float = 1e-12) -> complex:
+    out = np.zeros(2, dtype=np.float64)
+    q = complex(q)
+    lib().oracle_pair_helmholtz(float(t[0]), float(t[1]), float(s[0]), float(s[1]), q.real, q.imag,
+                                eps, kappa, _ptr(out))
+    return complex(out[0], out[1])

@@ -27,6 +27,7 @@
  * values, brute force, reciprocity, linearity, permutation, pair-count closed
  * form, SPEC geometry examples).
  */
+#define _DEFAULT_SOURCE /* j0 / y0 (XSI Bessel functions of glibc's libm) under -std=c11 */
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -337,4 +338,112 @@ int64_t oracle_box_tmax(int64_t ns, const double *src_xy, int64_t nt, const doub
     free(cs);
     free(ctg);
     return t;
+}
+
+/* ---- NEXT-3: the 2D Helmholtz kernel -------------------------------
+ * Outside the paper's own (electrostatic) kernel -- SPEC.md L176 lists oscillatory kernels as a
+ * non-goal of its CPU program -- but the workloads the paper motivates its redundancy with are
+ * the "high-frequency" MLFMA problems (refs [2], [3] at L390-391).  The 2D
+ * Helmholtz free-space Green's function (the textbook fundamental solution of
+ * (Delta + kappa^2) G = -delta):
+ *
+ *     G(r) = (i/4) H0^(1)(kappa r) = (i/4) (J0(kappa r) + i Y0(kappa r)) = (-Y0(kappa r) + i J0(kappa r)) / 4
+ *
+ *     phi_t = sum_{s : box(s) in E1(box(t)), r_ts >= eps} q_s G(r_ts),   q_s, phi_t complex
+ *
+ * with the same leaf grid, E1 and guard as the Laplace oracle above (R20).  J0 and Y0
+ * are the C library's j0 / y0 (glibc, double).  q and phi are interleaved (re, im) pairs.
+ * (a + ib)(-Y + iJ)/4 = (-aY - bJ)/4 + i (aJ - bY)/4. */
+static void helmholtz_pair(double r2, double kappa, double qr, double qi, double *re, double *im)
+{
+    double x = kappa * sqrt(r2);
+    double J = j0(x), Y = y0(x);
+    *re += 0.25 * (-qr * Y - qi * J);
+    *im += 0.25 * (qr * J - qi * Y);
+}
+
+int oracle_direct_helmholtz(int64_t ns, const double *src_xy, const double *q,
+                            int64_t nt, const double *tgt_xy, int L, double eps, double kappa,
+                            int64_t nsel, const int64_t *sel, double *phi_out,
+                            int nthreads, int64_t *pairs_out)
+{
+    int64_t S = grid_side(L);
+    int64_t *start = NULL, *items = NULL;
+    if (bucket_sources(ns, src_xy, S, &start, &items)) return -1;
+    int64_t count = sel ? nsel : nt;
+    double eps2 = eps * eps;
+    int64_t pairs = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : pairs)
+    for (int64_t k = 0; k < count; ++k) {
+        int64_t t = sel ? sel[k] : k;
+        double xt = tgt_xy[2 * t], yt = tgt_xy[2 * t + 1];
+        int64_t ix = cell_of(xt, S), iy = cell_of(yt, S);
+        double re = 0.0, im = 0.0;
+        for (int64_t dy = -1; dy <= 1; ++dy) {
+            int64_t cy = iy + dy;
+            if (cy < 0 || cy >= S) continue;
+            for (int64_t dx = -1; dx <= 1; ++dx) {
+                int64_t cx = ix + dx;
+                if (cx < 0 || cx >= S) continue;
+                int64_t c = cy * S + cx;
+                for (int64_t j = start[c]; j < start[c + 1]; ++j) {
+                    int64_t s = items[j];
+                    double ddx = xt - src_xy[2 * s], ddy = yt - src_xy[2 * s + 1];
+                    double r2 = ddx * ddx + ddy * ddy;
+                    pairs += 1;
+                    if (r2 < eps2) continue; /* coincident points contribute 0 (R3) */
+                    helmholtz_pair(r2, kappa, q[2 * s], q[2 * s + 1], &re, &im);
+                }
+            }
+        }
+        phi_out[2 * k] = re;
+        phi_out[2 * k + 1] = im;
+    }
+    free(start);
+    free(items);
+    if (pairs_out) *pairs_out = pairs;
+    return 0;
+}
+
+/* Brute force (no buckets): every (t, s) pair filtered by the 3x3 adjacency predicate. */
+int oracle_bruteforce_helmholtz(int64_t ns, const double *src_xy, const double *q,
+                                int64_t nt, const double *tgt_xy, int L, double eps, double kappa,
+                                double *phi_out, int64_t *pairs_out)
+{
+    int64_t S = grid_side(L);
+    double eps2 = eps * eps;
+    int64_t pairs = 0;
+    for (int64_t t = 0; t < nt; ++t) {
+        int64_t ixt = cell_of(tgt_xy[2 * t], S), iyt = cell_of(tgt_xy[2 * t + 1], S);
+        double re = 0.0, im = 0.0;
+        for (int64_t s = 0; s < ns; ++s) {
+            int64_t ixs = cell_of(src_xy[2 * s], S), iys = cell_of(src_xy[2 * s + 1], S);
+            if (llabs(ixs - ixt) > 1 || llabs(iys - iyt) > 1) continue;
+            pairs += 1;
+            double ddx = tgt_xy[2 * t] - src_xy[2 * s];
+            double ddy = tgt_xy[2 * t + 1] - src_xy[2 * s + 1];
+            double r2 = ddx * ddx + ddy * ddy;
+            if (r2 < eps2) continue;
+            helmholtz_pair(r2, kappa, q[2 * s], q[2 * s + 1], &re, &im);
+        }
+        phi_out[2 * t] = re;
+        phi_out[2 * t + 1] = im;
+    }
+    if (pairs_out) *pairs_out = pairs;
+    return 0;
+}
+
+/* One pair: out[0] + i out[1] = q G(r), q = qr + i qi; 0 when r < eps. */
+void oracle_pair_helmholtz(double xt, double yt, double xs, double ys, double qr, double qi,
+                           double eps, double kappa, double *out)
+{
+    double ddx = xt - xs, ddy = yt - ys;
+    double r2 = ddx * ddx + ddy * ddy;
+    out[0] = 0.0;
+    out[1] = 0.0;
+    if (r2 < eps * eps) return;
+    helmholtz_pair(r2, kappa, qr, qi, &out[0], &out[1]);
 }
