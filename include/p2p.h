@@ -55,7 +55,15 @@ typedef enum {
     P2P_ERROR_NO_DEVICE = 7             /* apply on a host-only plan, or no CUDA device */
 } p2p_status;
 
-typedef enum { P2P_KERNEL_LAPLACE_2D = 0 /* q ln(1/r); 0 when r < eps */ } p2p_kernel;
+/* Kernel functions G(r) of phi_t = sum_{s in E1(t), r >= eps} q_s G(r_ts):
+ *   LAPLACE_2D   (the paper's): G = ln(1/r), real q and phi.
+ *   HELMHOLTZ_2D (beyond the paper's kernel; R20):
+ *                G = (i/4) H0^(1)(kappa r) = (-Y0(kappa r) + i J0(kappa r)) / 4, the 2D
+ *                free-space Green's function of the oscillatory ("high-frequency", PAPER.md
+ *                L17, L299) MLFMA problems; kappa = desc.wavenumber > 0; q and phi complex,
+ *                interleaved (re, im) pairs in the plan precision (C99 complex / torch
+ *                complex64 / complex128 layout).  TILED layout, one partition. */
+typedef enum { P2P_KERNEL_LAPLACE_2D = 0, P2P_KERNEL_HELMHOLTZ_2D = 1 } p2p_kernel;
 
 /* Source layouts (§3.2 Indexing = non-redundant; §3.3 Repetition =
  * redundant), re-derived for B200:
@@ -117,10 +125,11 @@ typedef struct {
     void *stream;          /* cudaStream_t for plan-time uploads (NULL = default stream) */
     int32_t part_world;    /* number of Morton-range partitions (ranks); 1 = whole problem */
     int32_t part_rank;     /* partition owned by this plan, 0 <= part_rank < part_world */
+    double wavenumber;     /* HELMHOLTZ_2D: kappa > 0 (radians per unit length); ignored for LAPLACE_2D */
 } p2p_plan_desc;
 
 /* Fill *desc with defaults (level 0 -> CT loop, ct 15, l_start 3, l_max 15,
- * epsilon 1e-12, NR, fp32, device 0, auto tile, 1 partition). */
+ * epsilon 1e-12, NR, fp32, device 0, auto tile, 1 partition, LAPLACE_2D, wavenumber 0). */
 void p2p_plan_desc_init(p2p_plan_desc *desc);
 
 /* Build a plan.  Copies the host inputs; allocates all device memory and
@@ -146,7 +155,8 @@ p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src
 
 /* phi = A q on the plan's device, asynchronously on `stream` (cudaStream_t,
  * NULL = default stream).
- *   d_q   : device, weights in the plan precision (float or double).
+ *   d_q   : device, weights in the plan precision (float or double; HELMHOLTZ_2D: complex,
+ *           i.e. 2 values (re, im) per point -- every count below is then in complex elements).
  *           ORDER_PLAN: n_src elements in global plan order.
  *           ORDER_USER: n_src elements in the caller's point order.
  *   d_out : device, results in the plan precision.
@@ -245,6 +255,9 @@ typedef struct {
                                     (8N(3 + 27 ct)); else 0 */
     int64_t record_stride;       /* PAPER_REPETITION: doubles per record (3 + 27 C); else 0 */
     int64_t launches;            /* queue entries of a full apply (tiles, tail tiles split) */
+    int32_t kernel;              /* p2p_kernel */
+    int32_t components;          /* values per weight / result: 1 (real), 2 (complex) */
+    double wavenumber;           /* HELMHOLTZ_2D: kappa */
 } p2p_plan_info;
 
 /* Plan statistics.  Versioning: a caller compiled against an older (smaller)

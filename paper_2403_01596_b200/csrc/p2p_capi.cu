@@ -57,6 +57,7 @@ struct p2p_plan_s {
     double upload_seconds = 0.0;
     bool paper_kernel_only = false;              // diagnostics: PAPER_REPETITION applies skip the weight pack
     int elem = 4;
+    int comps = 1;                               // values per weight / result (2: complex, HELMHOLTZ_2D)
 
     template <typename V>
     void upload(DevBuf &b, const std::vector<V> &v) {
@@ -126,6 +127,17 @@ template <typename T>
 void finalize_plan(p2p_plan_s &P);
 
 template <typename T>
+const void *helm_fn(int nt) {
+    using namespace p2p::dev;
+    switch (nt) {
+    case 32: return (const void *)p2p_tiled_helm_kernel<T, 32>;
+    case 64: return (const void *)p2p_tiled_helm_kernel<T, 64>;
+    case 256: return (const void *)p2p_tiled_helm_kernel<T, 256>;
+    default: return (const void *)p2p_tiled_helm_kernel<T, 128>;
+    }
+}
+
+template <typename T>
 void upload_plan(p2p_plan_s &P) {
     const p2p::HostPlan &hp = P.hp;
     const p2p::Layout<T> &lay = layout_of<T>(hp);
@@ -182,7 +194,8 @@ void finalize_plan(p2p_plan_s &P) {
     // Dynamic shared memory is fixed per plan: opt in once (a permission, not a
     // reservation, so one value serves all plans), then size the persistent grid.
     const bool two = hp.tpi == 2;
-    const void *kfn = hp.layout == P2P_LAYOUT_REDUNDANT ? (const void *)p2p::dev::p2p_r_kernel<T>
+    const void *kfn = hp.kernel == P2P_KERNEL_HELMHOLTZ_2D ? helm_fn<T>(hp.nt)
+                      : hp.layout == P2P_LAYOUT_REDUNDANT ? (const void *)p2p::dev::p2p_r_kernel<T>
                       : hp.layout == P2P_LAYOUT_TILED
                           ? tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns)
                           : (two ? (const void *)p2p::dev::p2p_nr_kernel<T, sizeof(T) == 4 ? 2 : 1>
@@ -199,10 +212,11 @@ void finalize_plan(p2p_plan_s &P) {
     ck(cudaMemsetAsync(P.queue.p, 0, 16, P.stream), "queue init");  // kernels reset it on exit
     ck(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
        "carveout");
-    P.alloc(P.q_local, (size_t)std::max<int64_t>(hp.n_src_local, 1) * sizeof(T));
-    P.alloc(P.phi, (size_t)std::max<int64_t>(hp.n_tgt_local, 1) * sizeof(T));
-    P.alloc(P.io_q, (size_t)std::max<int64_t>(hp.n_src, 1) * sizeof(T));
-    P.alloc(P.io_out, (size_t)std::max<int64_t>(hp.n_tgt, 1) * sizeof(T));
+    const size_t cs = (size_t)P.comps * sizeof(T);  // bytes per weight / result
+    P.alloc(P.q_local, (size_t)std::max<int64_t>(hp.n_src_local, 1) * cs);
+    P.alloc(P.phi, (size_t)std::max<int64_t>(hp.n_tgt_local, 1) * cs);
+    P.alloc(P.io_q, (size_t)std::max<int64_t>(hp.n_src, 1) * cs);
+    P.alloc(P.io_out, (size_t)std::max<int64_t>(hp.n_tgt, 1) * cs);
 }
 
 int grid_for(int64_t n) {
@@ -269,11 +283,12 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.ns = hp.ns;
         a.flat = hp.flat ? 1 : 0;
         a.nbuf = hp.nbuf;
+        a.kappa = (T)hp.kappa;
         void *args[] = {&a};
         const int grid = (int)std::min<int64_t>(ntiles, P.occ_sms);
-        ck(cudaLaunchKernel(tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns), dim3(grid), dim3(hp.nt), args,
-                            (size_t)hp.smem_bytes, s),
-           "tiled launch");
+        const void *fn = hp.kernel == P2P_KERNEL_HELMHOLTZ_2D ? helm_fn<T>(hp.nt)
+                                                              : tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns);
+        ck(cudaLaunchKernel(fn, dim3(grid), dim3(hp.nt), args, (size_t)hp.smem_bytes, s), "tiled launch");
     } else {
         if (hp.halo_entries > 0)
             p2p::dev::pack_r_kernel<T><<<grid_for(hp.halo_entries), 256, 0, s>>>(
@@ -366,6 +381,7 @@ void apply_impl(p2p_plan_s &P, const void *d_q, void *d_out, int order, int accu
 template <typename T>
 void apply_dist_interior_impl(p2p_plan_s &P, const void *d_q_owned, void *d_out, int accumulate, cudaStream_t s) {
     const p2p::HostPlan &hp = P.hp;
+    if (P.comps != 1) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "distributed apply: real kernels only");
     if (hp.n_src_owned)
         ck(cudaMemcpyAsync((T *)P.q_local.p + hp.owned_local_begin, d_q_owned, (size_t)hp.n_src_owned * sizeof(T),
                            cudaMemcpyDeviceToDevice, s),
@@ -378,6 +394,7 @@ void apply_dist_interior_impl(p2p_plan_s &P, const void *d_q_owned, void *d_out,
 template <typename T>
 void apply_dist_boundary_impl(p2p_plan_s &P, const void *d_q_halo, void *d_out, int accumulate, cudaStream_t s) {
     const p2p::HostPlan &hp = P.hp;
+    if (P.comps != 1) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "distributed apply: real kernels only");
     if (hp.n_halo)
         p2p::dev::scatter_kernel<T><<<grid_for(hp.n_halo), 256, 0, s>>>(
             (const int32_t *)P.halo_lidx.p, (const T *)d_q_halo, (T *)P.q_local.p, hp.n_halo, 0);
@@ -528,6 +545,8 @@ void build_device_plan(p2p_plan_s &P, const p2p_plan_desc &d, const double *dsrc
     const auto t0 = std::chrono::steady_clock::now();
     DevTmp tmp(s);
     hp.device_built = true;
+    hp.kernel = d.kernel;
+    hp.kappa = d.kernel == P2P_KERNEL_HELMHOLTZ_2D ? d.wavenumber : 0.0;
     hp.layout = d.layout;
     hp.precision = d.precision;
     hp.device = d.device;
@@ -863,6 +882,7 @@ p2p_status p2p_plan_create(const p2p_plan_desc *desc, p2p_plan *out) {
         p2p::build_host_plan(*desc, P->hp);
         P->device = desc->device;
         P->elem = desc->precision == P2P_FP32 ? 4 : 8;
+        P->comps = desc->kernel == P2P_KERNEL_HELMHOLTZ_2D ? 2 : 1;
         if (desc->device >= 0) {
             int ndev = 0;
             if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -895,7 +915,7 @@ p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src
     p2p_status st = guarded([&] {
         const p2p_plan_desc &d = *desc;
         if (d.struct_size != sizeof(p2p_plan_desc)) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
-        if (d.kernel != P2P_KERNEL_LAPLACE_2D) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "only P2P_KERNEL_LAPLACE_2D");
+        p2p::check_kernel(d);
         if (d.precision != P2P_FP32 && d.precision != P2P_FP64) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "bad precision");
         if (d.layout != P2P_LAYOUT_NONREDUNDANT && d.layout != P2P_LAYOUT_TILED)
             throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "device build: NR and TILED layouts only (others: p2p_plan_create)");
@@ -914,6 +934,7 @@ p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src
         DeviceGuard g(d.device);
         P->device = d.device;
         P->elem = d.precision == P2P_FP32 ? 4 : 8;
+        P->comps = d.kernel == P2P_KERNEL_HELMHOLTZ_2D ? 2 : 1;
         P->stream = (cudaStream_t)d.stream;
         try {
             if (d.precision == P2P_FP32) build_device_plan<float>(*P, d, d_src_xy, d_tgt_xy);
@@ -949,8 +970,8 @@ static p2p_status apply_host_common(p2p_plan P, const void *h_q, void *h_out, in
         DeviceGuard g(P->device);
         cudaStream_t s = (cudaStream_t)stream;
         const p2p::HostPlan &hp = P->hp;
-        const size_t qb = (size_t)hp.n_src * P->elem;
-        const size_t ob = (size_t)(order == P2P_ORDER_USER ? hp.n_tgt : hp.n_tgt_local) * P->elem;
+        const size_t qb = (size_t)hp.n_src * P->elem * P->comps;
+        const size_t ob = (size_t)(order == P2P_ORDER_USER ? hp.n_tgt : hp.n_tgt_local) * P->elem * P->comps;
         ck(cudaMemcpyAsync(P->io_q.p, h_q, qb, cudaMemcpyHostToDevice, s), "H2D q");
         if (accumulate) ck(cudaMemcpyAsync(P->io_out.p, h_out, ob, cudaMemcpyHostToDevice, s), "H2D out");
         if (P->elem == 4) apply_impl<float>(*P, P->io_q.p, P->io_out.p, order, accumulate ? 1 : 0, s);
@@ -1073,7 +1094,7 @@ p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *out) {
     info->tiles = (int64_t)hp.tiles.size();
     info->smem_bytes = hp.smem_bytes;
     info->halo_entries = hp.halo_entries;
-    const int64_t e = hp.precision == P2P_FP32 ? 4 : 8;
+    const int64_t e = (hp.precision == P2P_FP32 ? 4 : 8) * (int64_t)P->comps;  // bytes per weight / result
     const int64_t offs = 8 * hp.boxes_in_tiles;  // tgt + src CSR offsets of the tiles' boxes
     info->alg_bytes_kernel = hp.n_tgt_local * 3 * e + hp.n_src_local * 3 * e + offs;
     if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
@@ -1099,6 +1120,9 @@ p2p_status p2p_plan_get_info(p2p_plan P, p2p_plan_info *out) {
     info->paper_model_bytes = hp.paper_model_bytes;
     info->record_stride = hp.pr_stride;
     info->launches = (int64_t)hp.tiles.size();
+    info->kernel = hp.kernel;
+    info->components = P->comps;
+    info->wavenumber = hp.kappa;
     std::memcpy(out, info, n);
     return P2P_SUCCESS;
 }

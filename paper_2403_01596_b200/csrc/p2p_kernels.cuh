@@ -306,6 +306,7 @@ struct P2PArgs {
     unsigned long long *trace;  // optional per-tile timeline (diagnostics; nullptr = off)
     T *out;
     int accumulate;
+    T kappa;                    // HELMHOLTZ_2D wavenumber
 };
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -944,6 +945,171 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         tb = s_base_next[it & 1];
         if (db) buf ^= 1;
         else if (tid == 0 && cur < a.ntiles) issue(cur, 0);
+    }
+    if (tid == 0) queue_exit(a.queue);
+}
+
+// ---------------------------------------------------------------- TILED Helmholtz kernel (NEXT-3)
+// G(r) = (i/4) H0^(1)(kappa r) = (-Y0(kappa r) + i J0(kappa r)) / 4 (include/p2p.h; R20),
+// complex weights and results as (re, im) pairs.  Same TILED record, queue and TMA staging as the
+// lean Laplace path; one thread per target slot (boxes ordered by n9), its three row-runs swept
+// as one flattened sequence.  Per pair: r^2, guard, sqrt, J0 and Y0 (CUDA's j0f/y0f, j0/y0:
+// rational / asymptotic approximations on the FMA pipe + one sincos and one log beyond the
+// small-argument branch), 4 FMA for the complex multiply-add.
+template <typename T>
+__device__ __forceinline__ void bessel_j0y0(T x, T &J, T &Y);
+template <>
+__device__ __forceinline__ void bessel_j0y0<float>(float x, float &J, float &Y) {
+    J = j0f(x);
+    Y = y0f(x);
+}
+template <>
+__device__ __forceinline__ void bessel_j0y0<double>(double x, double &J, double &Y) {
+    J = j0(x);
+    Y = y0(x);
+}
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) p2p_tiled_helm_kernel(const P2PArgs<T> a) {
+    using C2 = typename V2<T>::type;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ int s_next[2], s_base_next[2];
+    const int k = a.k, W = 1 << k, R = W + 2, RR = R * R;
+    const HCarve hc = helm_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T));
+    const TCarve &c = hc.t;
+    C2 *s_q = reinterpret_cast<C2 *>(smem + hc.q);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + hc.bar);
+    const C2 *q2 = reinterpret_cast<const C2 *>(a.q);
+    C2 *out2 = reinterpret_cast<C2 *>(a.out);
+    const int tid = threadIdx.x;
+
+    auto issue = [&](int ti) {  // one elected thread: bulk-copy tile ti's record (no item list)
+        const int slot = a.tile_slot[ti];
+        unsigned char *buf = smem + c.buf0;
+        const uint32_t rb = a.reg_off[slot], nent = a.reg_off[slot + 1] - rb;
+        const uint32_t tb = a.tgt_pack_off[slot], ntp = a.tgt_pack_off[slot + 1] - tb;
+        const uint32_t b_tab = (uint32_t)c.tstride * 2u, b_uv = nent * 2 * (uint32_t)sizeof(T), b_ix = nent * 4u;
+        const uint32_t b_tuv = ntp * 2 * (uint32_t)sizeof(T), b_t16 = ntp * 2u;
+        const uint32_t bar = smem_addr(mbar);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(b_tab + b_uv + b_ix + b_tuv + 2 * b_t16)
+                     : "memory");
+#define P2P_BULK(dst, src, bytes)                                                                        \
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" \
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(bar)                                   \
+                 : "memory")
+        P2P_BULK(buf + c.table, a.reg_table + (size_t)slot * c.tstride, b_tab);
+        if (nent) {
+            P2P_BULK(buf + c.uv, a.reg_uv + 2 * (size_t)rb, b_uv);
+            P2P_BULK(buf + c.idx, a.reg_idx + rb, b_ix);
+        }
+        if (ntp) {
+            P2P_BULK(buf + c.tuv, a.tgt_ruv + 2 * (size_t)tb, b_tuv);
+            P2P_BULK(buf + c.tbl, a.tgt_bl + tb, b_t16);
+            P2P_BULK(buf + c.oix, a.tgt_oix + tb, b_t16);
+        }
+#undef P2P_BULK
+    };
+
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const int t0 = atomicAdd(a.queue, 1);
+        s_next[0] = t0;
+        if (t0 < a.ntiles) {
+            s_base_next[0] = a.tile_tgt_base[a.tile_slot[t0]];
+            issue(t0);
+        }
+    }
+    __syncthreads();
+    int cur = s_next[0], tb = s_base_next[0], it = 0;
+    uint32_t parity = 0u;
+    const T kap = a.kappa, quarter = (T)0.25;
+    while (cur < a.ntiles) {
+        const unsigned char *B = smem + c.buf0;
+        const uint16_t *table = reinterpret_cast<const uint16_t *>(B + c.table);
+        const C2 *s_uv = reinterpret_cast<const C2 *>(B + c.uv);
+        const int32_t *s_idx = reinterpret_cast<const int32_t *>(B + c.idx);
+        const T *tuv = reinterpret_cast<const T *>(B + c.tuv);
+        const uint16_t *tbl = reinterpret_cast<const uint16_t *>(B + c.tbl);
+        const uint16_t *oix = reinterpret_cast<const uint16_t *>(B + c.oix);
+        if (tid == 0) {
+            const int nx = atomicAdd(a.queue, 1);
+            s_next[(it + 1) & 1] = nx;
+            if (nx < a.ntiles) s_base_next[(it + 1) & 1] = a.tile_tgt_base[a.tile_slot[nx]];
+        }
+        {
+            const uint32_t bar = smem_addr(mbar);
+            asm volatile(
+                "{\n\t.reg .pred P;\n"
+                "WAIT_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+                "@!P bra WAIT_%=;\n}" ::"r"(bar),
+                "r"(parity)
+                : "memory");
+            parity ^= 1u;
+        }
+        const int nent = (int)table[RR], nu = (int)table[RR + 1];
+        // complex weights through the per-entry index, 4 loads in flight per thread
+        for (int base = tid; base < nent; base += 4 * NT) {
+            C2 v[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const int i = base + x * NT;
+                const int32_t j = i < nent ? s_idx[i] : -1;
+                if (j >= 0) v[x] = q2[j];
+                else v[x].x = v[x].y = (T)0;
+            }
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const int i = base + x * NT;
+                if (i < nent) s_q[i] = v[x];
+            }
+        }
+        __syncthreads();
+        const int pinfo = a.tile_part[cur], npart = pinfo >> 16, ipart = pinfo & 0xffff;
+        int ub = 0, ue = nu;
+        if (npart > 1) {
+            ub = (nu * ipart) / npart;
+            ue = (nu * (ipart + 1)) / npart;
+        }
+        for (int t = ub + tid; t < ue; t += NT) {
+            const int jb = tbl[t];
+            const T ux = tuv[2 * t], uy = tuv[2 * t + 1];
+            const Runs3 runs(table[jb], table[jb + 3], table[jb + R], table[jb + R + 3], table[jb + 2 * R],
+                             table[jb + 2 * R + 3]);
+            T re = (T)0, im = (T)0;
+            const int v1 = runs.v0 + runs.n;
+            for (int v = runs.v0; v < v1; ++v) {
+                const int j = runs.at(v);
+                const C2 sp = s_uv[j];
+                const T du = ux - sp.x, dv = uy - sp.y;
+                const T r2 = du * du + dv * dv;
+                if (r2 < a.eps2) continue;  // coincident points contribute 0 (R3)
+                T J, Y;
+                bessel_j0y0<T>(kap * sqrt(r2), J, Y);
+                const C2 qv = s_q[j];
+                re = fma(-qv.x, Y, fma(-qv.y, J, re));
+                im = fma(qv.x, J, fma(-qv.y, Y, im));
+            }
+            const int o = oix[t];
+            const int oi = a.out_idx ? a.out_idx[tb + o] : tb + o;
+            C2 r;
+            r.x = quarter * re;
+            r.y = quarter * im;
+            if (a.accumulate) {
+                const C2 p = out2[oi];
+                r.x += p.x;
+                r.y += p.y;
+            }
+            out2[oi] = r;
+        }
+        __syncthreads();
+        ++it;
+        cur = s_next[it & 1];
+        tb = s_base_next[it & 1];
+        if (tid == 0 && cur < a.ntiles) issue(cur);
     }
     if (tid == 0) queue_exit(a.queue);
 }

@@ -112,6 +112,21 @@ P2P_HD inline TCarve tiled_carve(int k, int src_cap, int slot_cap, int e, int tp
     return c;
 }
 
+// TILED Helmholtz kernel: the TILED record buffer, then complex weights (2 values per region
+// entry) and the mbarrier.
+struct HCarve {
+    TCarve t;
+    int q, bar, total;
+};
+P2P_HD inline HCarve helm_carve(int k, int src_cap, int slot_cap, int e) {
+    HCarve h;
+    h.t = tiled_carve(k, src_cap, slot_cap, e, 1, 1, 1);
+    h.q = h.t.q;
+    h.bar = align16(h.q + 2 * e * src_cap);
+    h.total = h.bar + 16;
+    return h;
+}
+
 struct Error : std::runtime_error {
     p2p_status code;
     Error(p2p_status c, const std::string &m) : std::runtime_error(m), code(c) {}
@@ -159,6 +174,8 @@ struct Layout {
 struct HostPlan {
     // ---- parameters
     int L = 0, k = 0, layout = 0, precision = 0, device = -1;
+    int kernel = P2P_KERNEL_LAPLACE_2D;          // p2p_kernel
+    double kappa = 0.0;                          // HELMHOLTZ_2D wavenumber
     int part_world = 1, part_rank = 0;
     int64_t S = 0, B = 0;        // grid side, number of leaf boxes
     double h = 0.0, eps = 1e-12;
@@ -251,6 +268,7 @@ struct TileStats {
 // Kernel options (tpi, pad, ns, nt, lean, tsort, flat, caps) and shared memory per CTA at tile
 // size k; used by both builders so they take the same decisions.  Returns hp.smem_bytes.
 int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const TileStats &st);
+void check_kernel(const p2p_plan_desc &d);  // kernel function + envelope (throws Error)
 
 void build_host_plan(const p2p_plan_desc &desc, HostPlan &hp);
 void build_log_table(HostPlan &hp);

@@ -185,6 +185,17 @@ void build_log_table(HostPlan &hp) {
     }
 }
 
+// Kernel function and its envelope (include/p2p.h p2p_kernel): Helmholtz runs on the TILED
+// layout, one partition.
+void check_kernel(const p2p_plan_desc &d) {
+    if (d.kernel == P2P_KERNEL_LAPLACE_2D) return;
+    if (d.kernel != P2P_KERNEL_HELMHOLTZ_2D) fail(P2P_ERROR_INVALID_ARGUMENT, "bad kernel");
+    if (!(d.wavenumber > 0.0) || !std::isfinite(d.wavenumber))
+        fail(P2P_ERROR_INVALID_ARGUMENT, "HELMHOLTZ_2D needs wavenumber > 0");
+    if (d.layout != P2P_LAYOUT_TILED) fail(P2P_ERROR_NOT_SUPPORTED, "HELMHOLTZ_2D runs on the TILED layout");
+    if (d.part_world != 1) fail(P2P_ERROR_NOT_SUPPORTED, "HELMHOLTZ_2D: one partition");
+}
+
 // Kernel options and shared-memory size of a plan at tile size k, from its tile statistics
 // (shared by the host and the device builders, so both make the same decisions).
 int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const TileStats &st) {
@@ -236,6 +247,18 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     // row loops (P2P_FLAT overrides)
     hp.flat = hp.lean && (hp.density_occ < 3.0 || d.precision == P2P_FP64);
     if (const char *v = std::getenv("P2P_FLAT")) hp.flat = hp.lean && std::atoi(v) != 0;
+    if (d.kernel == P2P_KERNEL_HELMHOLTZ_2D) {  // one thread per target, n9-sorted, flattened runs
+        hp.tpi = 1;
+        hp.pad = false;
+        hp.ns = 1;
+        hp.nbuf = 1;
+        hp.lean = hp.tsort = hp.flat = true;
+        hp.nt = 128;
+        if (const char *v = std::getenv("P2P_NT")) {
+            const int x = std::atoi(v);
+            hp.nt = x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : 256;
+        }
+    }
     hp.tgt_cap = pad8(d.layout == P2P_LAYOUT_TILED && hp.tpi == 2 ? st.max_tcount2 : st.max_tcount);
     if (d.layout == P2P_LAYOUT_TILED && !hp.pad) hp.src_cap = pad4(st.max_region);  // unpadded region sizes
     if (d.layout == P2P_LAYOUT_PAPER_INDEXING || d.layout == P2P_LAYOUT_PAPER_REPETITION) {
@@ -243,6 +266,10 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
         return 0;
     }
     const int sc = (int)std::min<int64_t>(hp.src_cap, 1 << 24), tc = (int)std::min<int64_t>(hp.tgt_cap, 1 << 24);
+    if (d.kernel == P2P_KERNEL_HELMHOLTZ_2D) {
+        hp.smem_bytes = helm_carve(k, sc, tc, e).total;
+        return hp.smem_bytes;
+    }
     int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? (int64_t)nr_carve(k, sc, tc, e, hp.tpi).total
                    : d.layout == P2P_LAYOUT_TILED
                        ? (int64_t)tiled_carve(k, sc, tc, e, hp.tpi, hp.ns, hp.nbuf).total
@@ -254,7 +281,7 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
 void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     auto t0 = std::chrono::steady_clock::now();
     if (d.struct_size != sizeof(p2p_plan_desc)) fail(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
-    if (d.kernel != P2P_KERNEL_LAPLACE_2D) fail(P2P_ERROR_NOT_SUPPORTED, "only P2P_KERNEL_LAPLACE_2D");
+    check_kernel(d);
     if (d.layout < P2P_LAYOUT_NONREDUNDANT || d.layout > P2P_LAYOUT_PAPER_REPETITION)
         fail(P2P_ERROR_INVALID_ARGUMENT, "bad layout");
     const bool paper = d.layout == P2P_LAYOUT_PAPER_INDEXING || d.layout == P2P_LAYOUT_PAPER_REPETITION;
@@ -274,6 +301,8 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     hp.precision = d.precision;
     hp.device = d.device;
     hp.eps = d.epsilon;
+    hp.kernel = d.kernel;
+    hp.kappa = d.kernel == P2P_KERNEL_HELMHOLTZ_2D ? d.wavenumber : 0.0;
     hp.part_world = d.part_world;
     hp.part_rank = d.part_rank;
     hp.n_src = d.n_src;

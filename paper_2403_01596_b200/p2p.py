@@ -29,6 +29,7 @@ P2P_ERROR_NOT_SUPPORTED = 6
 P2P_ERROR_NO_DEVICE = 7
 
 P2P_KERNEL_LAPLACE_2D = 0
+P2P_KERNEL_HELMHOLTZ_2D = 1
 P2P_LAYOUT_NONREDUNDANT = 0
 P2P_LAYOUT_REDUNDANT = 1
 P2P_LAYOUT_TILED = 2
@@ -65,7 +66,7 @@ class PlanDesc(C.Structure):
         ("level_delta", C.c_int32), ("kernel", C.c_int32), ("epsilon", C.c_double),
         ("layout", C.c_int32), ("precision", C.c_int32), ("device", C.c_int32),
         ("tile_log2", C.c_int32), ("stream", C.c_void_p),
-        ("part_world", C.c_int32), ("part_rank", C.c_int32),
+        ("part_world", C.c_int32), ("part_rank", C.c_int32), ("wavenumber", C.c_double),
     ]
 
 
@@ -85,6 +86,7 @@ class PlanInfo(C.Structure):
         ("upload_seconds", C.c_double), ("cta_threads", C.c_int32), ("slots_per_unit", C.c_int32),
         ("items_per_unit", C.c_int32), ("flags", C.c_int32), ("interior_launches", C.c_int64),
         ("paper_model_bytes", C.c_int64), ("record_stride", C.c_int64), ("launches", C.c_int64),
+        ("kernel", C.c_int32), ("components", C.c_int32), ("wavenumber", C.c_double),
     ]
 
 
@@ -227,6 +229,8 @@ class Plan:
     layout: "nr" (non-redundant), "r" (redundant per box) or "tiled" (redundant on
     the tile ring only); "paper_i" / "paper_r": the paper's own Indexing / Repetition
     layouts and kernels (fp64); precision: "fp32" or "fp64".
+    kernel: "laplace" (the paper's ln(1/r)) or "helmholtz" ((i/4) H0^(1)(kappa r) with
+    ``wavenumber`` = kappa; complex q / phi; TILED layout).
     device: CUDA ordinal, or -1 for a host-only plan (build + export only).
     build: "host" (p2p_plan_create: the C++ builder on the CPU) or "device"
     (p2p_plan_create_device: the same plan built by GPU kernels; src_xy / tgt_xy may then
@@ -236,7 +240,8 @@ class Plan:
     def __init__(self, src_xy, tgt_xy=None, *, level: int = 0, ct: int = 15, l_start: int = 3,
                  l_max: int = 15, level_delta: int = 0, epsilon: float = 1e-12, layout: str = "nr",
                  precision: str = "fp32", device: int = 0, tile_log2: int = -1, stream: int = 0,
-                 part_world: int = 1, part_rank: int = 0, build: str = "host"):
+                 part_world: int = 1, part_rank: int = 0, build: str = "host", kernel: str = "laplace",
+                 wavenumber: float = 0.0):
         if build not in ("host", "device"):
             raise ValueError("build must be 'host' or 'device'")
         d = p2p_plan_desc_init()
@@ -264,6 +269,9 @@ class Plan:
         d.precision = {"fp32": P2P_FP32, "fp64": P2P_FP64}[precision]
         d.device, d.tile_log2, d.stream = device, tile_log2, stream or None
         d.part_world, d.part_rank = part_world, part_rank
+        d.kernel = {"laplace": P2P_KERNEL_LAPLACE_2D, "helmholtz": P2P_KERNEL_HELMHOLTZ_2D}[kernel]
+        d.wavenumber = wavenumber
+        self.kernel = kernel
         self.layout, self.precision, self.device, self.build = layout, precision, device, build
         if build == "device":
             if not stream:
@@ -281,11 +289,16 @@ class Plan:
 
     @property
     def torch_dtype(self):
+        """Element type of q and phi: real, or complex for the Helmholtz kernel."""
         import torch
+        if self.kernel == "helmholtz":
+            return torch.complex64 if self.precision == "fp32" else torch.complex128
         return torch.float32 if self.precision == "fp32" else torch.float64
 
     @property
     def np_dtype(self):
+        if self.kernel == "helmholtz":
+            return np.complex64 if self.precision == "fp32" else np.complex128
         return np.float32 if self.precision == "fp32" else np.float64
 
     def export(self, kind) -> np.ndarray:

@@ -87,6 +87,9 @@ CONFIGS: dict[str, PlateConfig] = {
         PlateConfig("lowd4_1e7", 2000, 1250, 12, 10_000_000),
         PlateConfig("surf_2e7", 1250, 1000, 12, 20_000_000),
         PlateConfig("d32_7e7", 1750, 1250, 12, 70_000_000),
+        # NEXT-3 (Helmholtz): a 1e6-point plate at 4 points per leaf box (leaf = a quarter
+        # wavelength at the helmholtz workload's kappa: ~8 samples per wavelength along x and y)
+        PlateConfig("d4_1e6", 500, 500, 10, 1_000_000),
     ]
 }
 
