@@ -969,6 +969,63 @@ __device__ __forceinline__ void bessel_j0y0<double>(double x, double &J, double 
     Y = y0(x);
 }
 
+// Small arguments (z = (kappa r / 2)^2 <= kHelmZmax): J0 and Y0 from their ascending series
+// (Abramowitz & Stegun 9.1.12, 9.1.13) sharing one log and one z:
+//   J0 = sum_k (-z)^k / (k!)^2,
+//   Y0 = (2/pi) [ (ln(x/2) + gamma) J0 + sum_{k>=1} (-1)^{k+1} H_k z^k / (k!)^2 ],  ln(x/2) = ln(z)/2,
+// Horner in z: 2 x 11 FFMA + one MUFU.LG2 (fp32, x <= 4.5: |error| <= 8e-7), 2 x 19 DFMA + the
+// table log (fp64, x <= 6: <= 1.1e-14); larger arguments take CUDA's j0/y0.
+template <typename T>
+struct HelmSeries;
+template <>
+struct HelmSeries<float> {
+    static constexpr float kZmax = 4.5f * 4.5f / 4.f;
+    static __device__ __forceinline__ void eval(float z, float &J, float &Y, const double2 *) {
+        constexpr float A[11] = {1.0f, -1.0f, 0.25f, -0.027777777777777776f, 0.001736111111111111f,
+                                 -6.944444444444444e-05f, 1.9290123456790124e-06f, -3.936759889140842e-08f,
+                                 6.151187326782565e-10f, -7.594058428126624e-12f, 7.594058428126623e-14f};
+        constexpr float B[11] = {0.0f, 1.0f, -0.375f, 0.05092592592592592f, -0.003616898148148148f,
+                                 0.0001585648148148148f, -4.72608024691358e-06f, 1.0207455998272325e-07f,
+                                 -1.6718048413148328e-09f, 2.1483350211950277e-11f, -2.224275605476294e-13f};
+        float j = A[10], s = B[10];
+#pragma unroll
+        for (int k = 9; k >= 0; --k) {
+            j = fmaf(j, z, A[k]);
+            s = fmaf(s, z, B[k]);
+        }
+        const float hl = fmaf(lg2_approx(z), 0.5f * kLn2, 0.5772156649015329f);  // ln(x/2) + gamma
+        J = j;
+        Y = 0.6366197723675814f * fmaf(hl, j, s);
+    }
+};
+template <>
+struct HelmSeries<double> {
+    static constexpr double kZmax = 6.0 * 6.0 / 4.0;
+    static __device__ __forceinline__ void eval(double z, double &J, double &Y, const double2 *LT) {
+        constexpr double A[19] = {1.0, -1.0, 0.25, -0.027777777777777776, 0.001736111111111111,
+                                  -6.944444444444444e-05, 1.9290123456790124e-06, -3.936759889140842e-08,
+                                  6.151187326782565e-10, -7.594058428126624e-12, 7.594058428126623e-14,
+                                  -6.276081345559193e-16, 4.358389823304995e-18, -2.5789288895295828e-20,
+                                  1.3157800456783586e-22, -5.8479113141260385e-25, 2.2843403570804838e-27,
+                                  -7.904291893012054e-30, 2.4395962632753253e-32};
+        constexpr double B[19] = {0.0, 1.0, -0.375, 0.05092592592592592, -0.003616898148148148,
+                                  0.0001585648148148148, -4.72608024691358e-06, 1.0207455998272325e-07,
+                                  -1.6718048413148328e-09, 2.1483350211950277e-11, -2.224275605476294e-13,
+                                  1.895299587006153e-15, -1.3525001839484812e-17, 8.201338813682637e-20,
+                                  -4.278340826570208e-22, 1.9404708872364884e-24, -7.722735675585063e-27,
+                                  2.71872271202985e-29, -8.52665260731113e-32};
+        double j = A[18], s = B[18];
+#pragma unroll
+        for (int k = 17; k >= 0; --k) {
+            j = fma(j, z, A[k]);
+            s = fma(s, z, B[k]);
+        }
+        const double hl = fma(log_tab(z, LT), 0.5, 0.5772156649015329);  // ln(x/2) + gamma
+        J = j;
+        Y = 0.6366197723675814 * fma(hl, j, s);
+    }
+};
+
 template <typename T, int NT>
 __global__ void __launch_bounds__(NT) p2p_tiled_helm_kernel(const P2PArgs<T> a) {
     using C2 = typename V2<T>::type;
@@ -978,7 +1035,10 @@ __global__ void __launch_bounds__(NT) p2p_tiled_helm_kernel(const P2PArgs<T> a) 
     const HCarve hc = helm_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T));
     const TCarve &c = hc.t;
     C2 *s_q = reinterpret_cast<C2 *>(smem + hc.q);
+    double2 *s_lt = reinterpret_cast<double2 *>(smem + hc.ltab);
     uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + hc.bar);
+    if constexpr (sizeof(T) == 8)
+        for (int i = threadIdx.x; i < kLogTab; i += NT) s_lt[i] = a.log_tab[i];
     const C2 *q2 = reinterpret_cast<const C2 *>(a.q);
     C2 *out2 = reinterpret_cast<C2 *>(a.out);
     const int tid = threadIdx.x;
@@ -1025,7 +1085,7 @@ __global__ void __launch_bounds__(NT) p2p_tiled_helm_kernel(const P2PArgs<T> a) 
     __syncthreads();
     int cur = s_next[0], tb = s_base_next[0], it = 0;
     uint32_t parity = 0u;
-    const T kap = a.kappa, quarter = (T)0.25;
+    const T kap = a.kappa, kq = (T)0.25 * a.kappa * a.kappa, quarter = (T)0.25;
     while (cur < a.ntiles) {
         const unsigned char *B = smem + c.buf0;
         const uint16_t *table = reinterpret_cast<const uint16_t *>(B + c.table);
@@ -1088,7 +1148,9 @@ __global__ void __launch_bounds__(NT) p2p_tiled_helm_kernel(const P2PArgs<T> a) 
                 const T r2 = du * du + dv * dv;
                 if (r2 < a.eps2) continue;  // coincident points contribute 0 (R3)
                 T J, Y;
-                bessel_j0y0<T>(kap * sqrt(r2), J, Y);
+                const T z = kq * r2;  // (kappa r / 2)^2
+                if (z <= HelmSeries<T>::kZmax) HelmSeries<T>::eval(z, J, Y, s_lt);
+                else bessel_j0y0<T>(kap * sqrt(r2), J, Y);
                 const C2 qv = s_q[j];
                 re = fma(-qv.x, Y, fma(-qv.y, J, re));
                 im = fma(qv.x, J, fma(-qv.y, Y, im));

@@ -113,16 +113,17 @@ P2P_HD inline TCarve tiled_carve(int k, int src_cap, int slot_cap, int e, int tp
 }
 
 // TILED Helmholtz kernel: the TILED record buffer, then complex weights (2 values per region
-// entry) and the mbarrier.
+// entry), the fp64 log table and the mbarrier.
 struct HCarve {
     TCarve t;
-    int q, bar, total;
+    int q, ltab, bar, total;
 };
 P2P_HD inline HCarve helm_carve(int k, int src_cap, int slot_cap, int e) {
     HCarve h;
     h.t = tiled_carve(k, src_cap, slot_cap, e, 1, 1, 1);
     h.q = h.t.q;
-    h.bar = align16(h.q + 2 * e * src_cap);
+    h.ltab = align16(h.q + 2 * e * src_cap);
+    h.bar = align16(h.ltab + (e == 8 ? 16 * kLogTab : 0));
     h.total = h.bar + 16;
     return h;
 }
