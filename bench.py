@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import sys
 import threading
@@ -40,6 +41,7 @@ WORKLOADS = {
     "surface_2e7": ["surf_2e7"],                                # configs[3]
     "d32_7e7": ["d32_7e7"],                                     # configs[4]
     "tiny": ["tiny"],                                           # configs[0]
+    "helmholtz_1e6": ["d16_1e6", "d4_1e6"],                     # NEXT-3: 2D Helmholtz, leaf = lambda/4
 }
 METRIC = "P2P pair-interactions/s"
 MUFU_LG2_PER_CLK_PER_SM = 16       # SFU issue rate (checked by libp2p_peaks)
@@ -68,7 +70,28 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras/baseline)")
     ap.add_argument("--configs", default="", help="comma list of config names overriding --workload")
     ap.add_argument("--tile", type=int, default=-1, help="force CTA tile side 2^tile (default: plan's choice)")
-    return ap.parse_args()
+    ap.add_argument("--kernel", default=None, choices=["laplace", "helmholtz"],
+                    help="kernel function (default: helmholtz for the helmholtz_1e6 workload, else laplace)")
+    ap.add_argument("--kh", type=float, default=math.pi / 2,
+                    help="helmholtz: kappa * leaf box side (pi/2 = a quarter-wavelength box)")
+    a = ap.parse_args()
+    if a.kernel is None:
+        a.kernel = "helmholtz" if a.workload == "helmholtz_1e6" else "laplace"
+    if a.kernel == "helmholtz":
+        a.layout = "tiled"
+        a.no_extras = True
+    return a
+
+
+def _kernel_kw(args, cfg):
+    """Plan keywords of the kernel function (Helmholtz: kappa from the leaf box side)."""
+    if args.kernel != "helmholtz":
+        return {}
+    return {"kernel": "helmholtz", "wavenumber": args.kh * (1 << (cfg.level - 1))}
+
+
+def _weights(args, cfg, q):
+    return W.weights_complex(cfg.n, cfg.seed) if args.kernel == "helmholtz" else q
 
 
 # ---------------------------------------------------------------- clocks
@@ -135,7 +158,7 @@ def _hbm_peak():
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle)
-def cpu_baseline(cfg_names, kind, budget_s, seed_stream=0):
+def cpu_baseline(cfg_names, kind, budget_s, seed_stream=0, kernel="laplace", kh=math.pi / 2):
     """The fp64 oracle as it stands (never tuned), on a bounded, seeded sample of
     the targets of each config, timed on this host's cores."""
     import oracle
@@ -146,7 +169,11 @@ def cpu_baseline(cfg_names, kind, budget_s, seed_stream=0):
     def run(cfg, s, t, q, frac):
         sel = np.sort(rng.choice(len(t), max(1, int(frac * len(t))), replace=False))
         tic = time.perf_counter()
-        _, p = oracle.direct(s, q, t, cfg.level, targets=sel)
+        if kernel == "helmholtz":
+            _, p = oracle.direct_helmholtz(s, W.weights_complex(cfg.n, cfg.seed), t, cfg.level,
+                                           kh * (1 << (cfg.level - 1)), targets=sel)
+        else:
+            _, p = oracle.direct(s, q, t, cfg.level, targets=sel)
         return p, time.perf_counter() - tic
 
     # per config: a 5% probe, then a sample sized to this config's share of the budget
@@ -161,7 +188,7 @@ def cpu_baseline(cfg_names, kind, budget_s, seed_stream=0):
         fracs.append(f)
     return {"value": pairs / secs, "unit": "pair-interactions/s", "cores": nthreads, "kind": "oracle",
             "sample": f"{100 * min(fracs):.2f}-{100 * max(fracs):.2f}% of the targets of each of "
-                      f"{','.join(cfg_names)} (seeded); fp64 direct sum incl. source bucketing; "
+                      f"{','.join(cfg_names)} (seeded); fp64 {kernel} direct sum incl. source bucketing; "
                       f"{pairs} pairs in {secs:.1f} s",
             "pairs": pairs, "seconds": secs}
 
@@ -172,16 +199,17 @@ def run_reference(args):
         return 0
     names = WORKLOADS[args.workload]
     per_step = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    kk = dict(kernel=args.kernel, kh=args.kh)
     for _ in range(args.warmup):
-        cpu_baseline(names, args.kind, per_step / 4)
+        cpu_baseline(names, args.kind, per_step / 4, **kk)
     vals, pairs, secs = [], 0, 0.0
     last = None
     for k in range(args.steps):
-        last = cpu_baseline(names, args.kind, per_step, seed_stream=k + 1)
+        last = cpu_baseline(names, args.kind, per_step, seed_stream=k + 1, **kk)
         pairs += last["pairs"]
         secs += last["seconds"]
     v = pairs / secs
-    cfg = {"workload": args.workload, "configs": names, "layout": "oracle", "kind": args.kind}
+    cfg = {"workload": args.workload, "configs": names, "layout": "oracle", "kind": args.kind, "kernel": args.kernel}
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "pair-interactions/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
@@ -229,7 +257,9 @@ def main():
         cfg = W.widened(W.CONFIGS[name], world) if weak else W.CONFIGS[name]
         src, tgt, q = W.make_problem(cfg, kind=args.kind)
         name = cfg.name
-        kw = dict(level=cfg.level, layout=args.layout, precision=args.precision, tile_log2=args.tile)
+        kw = dict(level=cfg.level, layout=args.layout, precision=args.precision, tile_log2=args.tile,
+                  **_kernel_kw(args, cfg))
+        q = _weights(args, cfg, q)
         if world == 1:
             if args.build == "device" and args.layout in ("nr", "tiled"):  # built on the GPU (NEXT-2)
                 pl = p2p.Plan(torch.as_tensor(src, device=dev), torch.as_tensor(tgt, device=dev), device=local,
@@ -323,7 +353,17 @@ def main():
     t_mufu = sum(j["info"]["pairs"] / (peak_mufu * 1e9) for j in jobs)
     t_hbm = sum(j["info"]["alg_bytes_kernel"] / (peak_hbm * 1e9) for j in jobs)
     traffic = _ncu_traffic(args, [j["name"] for j in jobs]) if world == 1 else None
-    if t_mufu >= t_hbm:
+    if args.kernel == "helmholtz":  # issue-bound: instructions per pair from ncu
+        achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
+        ipp = _helm_inst_per_pair(args.precision)
+        peak = 128 * SM_COUNT * peak_clk / ipp / 1e9 if ipp else None
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak,
+                    "unit": f"Gpair/s (issue slots at {ipp} thread-instructions per pair)" if ipp else "Gpair/s",
+                    "frac": achieved / peak if peak else None, "traffic": traffic,
+                    "peak_basis": f"128 lanes x {SM_COUNT} SMs x {peak_clk / 1e6:.0f} MHz issue / thread-instructions "
+                                  "per pair (ncu smsp__thread_inst_executed.sum / pairs, "
+                                  "profiles/helm_inst_per_pair.json)"}
+    elif t_mufu >= t_hbm:
         achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak_mufu, "unit": "Gpair/s (1 MUFU.LG2 per pair)",
                     "frac": achieved / peak_mufu, "traffic": traffic,
@@ -359,6 +399,7 @@ def main():
         "config": {"workload": args.workload + (f" x{world} (plates widened, weak scaling)" if weak else ""),
                    "configs": [j["cfg"].name for j in jobs], "layout": args.layout,
                    "precision": args.precision, "kind": args.kind, "pairs_per_step": pairs_step,
+                   "kernel": args.kernel, **({"kappa_h": args.kh} if args.kernel == "helmholtz" else {}),
                    "order": "plan", "l2": "flushed (256 MiB write) between timed steps",
                    "parallelism": f"morton-range x{world}" + (
                        (" + host-staged gloo halo exchange, ranks sharing GPUs (TEST MODE)" if shared
@@ -367,7 +408,8 @@ def main():
         "roofline": roofline, "clocks": clocks, "e2e": e2e, "per_config": per_cfg,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
-        out["cpu_baseline"] = {k: v for k, v in cpu_baseline(names, args.kind, args.cpu_seconds).items()
+        out["cpu_baseline"] = {k: v for k, v in cpu_baseline(names, args.kind, args.cpu_seconds, kernel=args.kernel,
+                                                             kh=args.kh).items()
                                if k not in ("pairs", "seconds")}
     if rank == 0 and world == 1 and not args.profile and args.layout in ("nr", "tiled"):
         out["plan_build"] = _plan_build(args, jobs, dev)
@@ -442,6 +484,14 @@ def _e2e_dist(args, jobs, stream, pairs_step, barrier):
                     "potentials; max over ranks"}
 
 
+def _helm_inst_per_pair(precision):
+    """Thread-instructions per pair of the Helmholtz kernel, measured by ncu (tools/helm_ipp.py)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "profiles", "helm_inst_per_pair.json")))[precision])
+    except Exception:
+        return None
+
+
 def _ncu_traffic(args, names):
     """dram bytes per launch of the P2P kernel from the committed ncu --set full summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -504,7 +554,8 @@ def _plan_build(args, jobs, dev):
     for j in jobs:
         cfg = j["cfg"]
         src, tgt, _ = W.make_problem(cfg, kind=args.kind)
-        kw = dict(level=cfg.level, layout=args.layout, precision=args.precision, tile_log2=args.tile)
+        kw = dict(level=cfg.level, layout=args.layout, precision=args.precision, tile_log2=args.tile,
+                  **_kernel_kw(args, cfg))
         with p2p.Plan(src, tgt, device=dev.index, **kw) as pl:
             host += pl.info["build_seconds"] + pl.info["upload_seconds"]
         ds, dt = torch.as_tensor(src, device=dev), torch.as_tensor(tgt, device=dev)

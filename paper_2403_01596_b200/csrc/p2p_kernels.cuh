@@ -998,22 +998,24 @@ struct HelmSeries<float> {
         Y = 0.6366197723675814f * fmaf(hl, j, s);
     }
 };
+// fp64 series coefficients (a_k, b_k of HelmSeries<float>, 19 terms) in the constant bank
+__constant__ double kHelmA64[19] = {1.0, -1.0, 0.25, -0.027777777777777776, 0.001736111111111111,
+                          -6.944444444444444e-05, 1.9290123456790124e-06, -3.936759889140842e-08,
+                          6.151187326782565e-10, -7.594058428126624e-12, 7.594058428126623e-14,
+                          -6.276081345559193e-16, 4.358389823304995e-18, -2.5789288895295828e-20,
+                          1.3157800456783586e-22, -5.8479113141260385e-25, 2.2843403570804838e-27,
+                          -7.904291893012054e-30, 2.4395962632753253e-32};
+__constant__ double kHelmB64[19] = {0.0, 1.0, -0.375, 0.05092592592592592, -0.003616898148148148,
+                          0.0001585648148148148, -4.72608024691358e-06, 1.0207455998272325e-07,
+                          -1.6718048413148328e-09, 2.1483350211950277e-11, -2.224275605476294e-13,
+                          1.895299587006153e-15, -1.3525001839484812e-17, 8.201338813682637e-20,
+                          -4.278340826570208e-22, 1.9404708872364884e-24, -7.722735675585063e-27,
+                          2.71872271202985e-29, -8.52665260731113e-32};
 template <>
 struct HelmSeries<double> {
     static constexpr double kZmax = 6.0 * 6.0 / 4.0;
     static __device__ __forceinline__ void eval(double z, double &J, double &Y, const double2 *LT) {
-        constexpr double A[19] = {1.0, -1.0, 0.25, -0.027777777777777776, 0.001736111111111111,
-                                  -6.944444444444444e-05, 1.9290123456790124e-06, -3.936759889140842e-08,
-                                  6.151187326782565e-10, -7.594058428126624e-12, 7.594058428126623e-14,
-                                  -6.276081345559193e-16, 4.358389823304995e-18, -2.5789288895295828e-20,
-                                  1.3157800456783586e-22, -5.8479113141260385e-25, 2.2843403570804838e-27,
-                                  -7.904291893012054e-30, 2.4395962632753253e-32};
-        constexpr double B[19] = {0.0, 1.0, -0.375, 0.05092592592592592, -0.003616898148148148,
-                                  0.0001585648148148148, -4.72608024691358e-06, 1.0207455998272325e-07,
-                                  -1.6718048413148328e-09, 2.1483350211950277e-11, -2.224275605476294e-13,
-                                  1.895299587006153e-15, -1.3525001839484812e-17, 8.201338813682637e-20,
-                                  -4.278340826570208e-22, 1.9404708872364884e-24, -7.722735675585063e-27,
-                                  2.71872271202985e-29, -8.52665260731113e-32};
+        const double *A = kHelmA64, *B = kHelmB64;  // constant-bank operands of DFMA (no UMOV pairs)
         double j = A[18], s = B[18];
 #pragma unroll
         for (int k = 17; k >= 0; --k) {

@@ -154,6 +154,11 @@ def weights(n: int, seed: int, stream: int = 4) -> np.ndarray:
     return 2.0 * uniform01(seed, stream, np.arange(n, dtype=np.uint64)) - 1.0
 
 
+def weights_complex(n: int, seed: int) -> np.ndarray:
+    """Complex weights for the Helmholtz kernel (NEXT-3): re, im ~ U[-1, 1) (streams 4 and 5)."""
+    return weights(n, seed) + 1j * weights(n, seed, stream=5)
+
+
 def make_problem(cfg: PlateConfig | str, kind: str = "iid", seed: int | None = None,
                  collocated: bool = False, n: int | None = None):
     """(src_xy, tgt_xy, q) float64 arrays for one workload."""

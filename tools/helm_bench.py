@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--kh", type=float, default=math.pi / 2)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--sample", type=int, default=20000)
+    ap.add_argument("--precisions", default="fp32,fp64")
     ap.add_argument("--json", default=None)
     a = ap.parse_args()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=DEV)
@@ -44,7 +45,7 @@ def main():
         t = time.perf_counter()
         ref, sp = oracle.direct_helmholtz(src, q, tgt, cfg.level, kappa, targets=sel)
         cpu_s = time.perf_counter() - t
-        for prec in ("fp32", "fp64"):
+        for prec in a.precisions.split(","):
             with p2p.Plan(torch.as_tensor(src, device=DEV), torch.as_tensor(tgt, device=DEV), level=cfg.level,
                           layout="tiled", precision=prec, kernel="helmholtz", wavenumber=kappa,
                           build="device") as pl:
