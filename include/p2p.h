@@ -57,7 +57,7 @@ typedef enum {
 
 /* Kernel functions G(r) of phi_t = sum_{s in E1(t), r >= eps} q_s G(r_ts):
  *   LAPLACE_2D   (the paper's): G = ln(1/r), real q and phi.
- *   HELMHOLTZ_2D (beyond the paper's kernel; R20):
+ *   HELMHOLTZ_2D (beyond the paper's kernel; R23):
  *                G = (i/4) H0^(1)(kappa r) = (-Y0(kappa r) + i J0(kappa r)) / 4, the 2D
  *                free-space Green's function of the oscillatory ("high-frequency", PAPER.md
  *                L17, L299) MLFMA problems; kappa = desc.wavenumber > 0; q and phi complex,

@@ -351,7 +351,7 @@ int64_t oracle_box_tmax(int64_t ns, const double *src_xy, int64_t nt, const doub
  *
  *     phi_t = sum_{s : box(s) in E1(box(t)), r_ts >= eps} q_s G(r_ts),   q_s, phi_t complex
  *
- * with the same leaf grid, E1 and guard as the Laplace oracle above (R20).  J0 and Y0
+ * with the same leaf grid, E1 and guard as the Laplace oracle above (R23).  J0 and Y0
  * are the C library's j0 / y0 (glibc, double).  q and phi are interleaved (re, im) pairs.
  * (a + ib)(-Y + iJ)/4 = (-aY - bJ)/4 + i (aJ - bY)/4. */
 static void helmholtz_pair(double r2, double kappa, double qr, double qi, double *re, double *im)

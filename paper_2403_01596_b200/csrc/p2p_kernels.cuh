@@ -950,7 +950,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
 }
 
 // ---------------------------------------------------------------- TILED Helmholtz kernel (NEXT-3)
-// G(r) = (i/4) H0^(1)(kappa r) = (-Y0(kappa r) + i J0(kappa r)) / 4 (include/p2p.h; R20),
+// G(r) = (i/4) H0^(1)(kappa r) = (-Y0(kappa r) + i J0(kappa r)) / 4 (include/p2p.h; R23),
 // complex weights and results as (re, im) pairs.  Same TILED record, queue and TMA staging as the
 // lean Laplace path; one thread per target slot (boxes ordered by n9), its three row-runs swept
 // as one flattened sequence.  Per pair: r^2, guard, sqrt, J0 and Y0 (CUDA's j0f/y0f, j0/y0:

@@ -2,7 +2,7 @@
 through the C ABI against the fp64 oracle (oracle.direct_helmholtz, pinned in
 tests/test_oracle_helmholtz.py).
 
-Gate (R20): relative L2 <= 1e-5 (fp32), <= 1e-12 (fp64) while kappa r < 8 for every
+Gate (R23): relative L2 <= 1e-5 (fp32), <= 1e-12 (fp64) while kappa r < 8 for every
 E1 pair (CUDA's j0/y0 are ulp-accurate there); beyond, <= 1e-10 (their documented absolute
 error, 5e-12)."""
 import math

@@ -1,4 +1,4 @@
-"""Pins of the 2D Helmholtz oracle (oracle.c; R20):
+"""Pins of the 2D Helmholtz oracle (oracle.c; R23):
 G(r) = (i/4) H0^(1)(kappa r) = (-Y0(kappa r) + i J0(kappa r)) / 4, phi_t = sum_{E1} q_s G(r_ts).
 
 Each pin checks the oracle against something other than itself:

@@ -1,6 +1,6 @@
 """2D Helmholtz near field on B200: G = (i/4) H0^(1)(kappa r), complex
 weights, TILED layout.  Workload: the d16_1e6 and d4_1e6 plates with the leaf box a quarter
-wavelength (kappa h = pi/2, R20), iid points, fp32 and fp64; per config the median of
+wavelength (kappa h = pi/2, R23), iid points, fp32 and fp64; per config the median of
 `--reps` L2-flushed applies (CUDA events), pairs/s, the oracle on a sample of targets (all host
 cores) and the fp32 relative L2 error on that sample.
 
