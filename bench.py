@@ -42,7 +42,10 @@ WORKLOADS = {
     "d32_7e7": ["d32_7e7"],                                     # configs[4]
     "tiny": ["tiny"],                                           # configs[0]
     "helmholtz_1e6": ["d16_1e6", "d4_1e6"],                     # NEXT-3: 2D Helmholtz, leaf = lambda/4
+    "contour_2e5": ["contour_2e5"],                             # NEXT-4: curve cloud, Laplace
+    "contour_helmholtz": ["contour_1e5"],                       # NEXT-4: curve cloud, Helmholtz, leaf = lambda/4
 }
+HELMHOLTZ_WORKLOADS = ("helmholtz_1e6", "contour_helmholtz")
 METRIC = "P2P pair-interactions/s"
 MUFU_LG2_PER_CLK_PER_SM = 16       # SFU issue rate (checked by libp2p_peaks)
 SM_COUNT = 148
@@ -76,7 +79,7 @@ def parse():
                     help="helmholtz: kappa * leaf box side (pi/2 = a quarter-wavelength box)")
     a = ap.parse_args()
     if a.kernel is None:
-        a.kernel = "helmholtz" if a.workload == "helmholtz_1e6" else "laplace"
+        a.kernel = "helmholtz" if a.workload in HELMHOLTZ_WORKLOADS else "laplace"
     if a.kernel == "helmholtz":
         a.layout = "tiled"
         a.no_extras = True

@@ -74,8 +74,39 @@ class PlateConfig:
         return d * d * (3 * self.sx - 2) * (3 * self.sy - 2)
 
 
+@dataclass(frozen=True)
+class ContourConfig:
+    """a curve-concentrated ("surface-like") 2D cloud -- the nodes of a
+    boundary discretisation of a 2D scatterer (the 2D MLFMA / EFIE setting of PAPER.md refs
+    [2], [4]-[6]): n points on the closed star curve r(t) = r0 (1 + a cos(m t)) around
+    (1/2, 1/2), equispaced in t with a seeded jitter of +-1/8 spacing; sources = targets
+    (collocation; the self pair is removed by the eps guard).  Most leaf boxes are empty; the
+    occupied ones hold about n h / (curve length) points (curve length ~ 3.16)."""
+    name: str
+    n: int
+    level: int
+    r0: float = 0.35
+    a: float = 0.3
+    m: int = 5
+    seed: int = 20240303
+
+    @property
+    def side(self) -> int:
+        return 1 << (self.level - 1)
+
+
+def contour_points(cfg: ContourConfig, seed: int | None = None, n: int | None = None) -> np.ndarray:
+    """[n, 2] float64 points on the star curve of ``cfg`` (inside [0.045, 0.955]^2)."""
+    seed = cfg.seed if seed is None else seed
+    n = cfg.n if n is None else n
+    u = uniform01(seed, 6, np.arange(n, dtype=np.uint64))
+    t = 2.0 * np.pi * (np.arange(n, dtype=np.float64) + 0.5 + 0.25 * (u - 0.5)) / n
+    r = cfg.r0 * (1.0 + cfg.a * np.cos(cfg.m * t))
+    return np.stack([0.5 + r * np.cos(t), 0.5 + r * np.sin(t)], axis=1)
+
+
 # SURVEY.md §8(d) table; BASELINE.json "configs".
-CONFIGS: dict[str, PlateConfig] = {
+CONFIGS: dict[str, PlateConfig | ContourConfig] = {
     c.name: c for c in [
         PlateConfig("tiny", 8, 8, 4, 1024, seed=1),
         PlateConfig("d16_1e6", 250, 250, 9, 1_000_000),
@@ -92,6 +123,13 @@ CONFIGS: dict[str, PlateConfig] = {
         PlateConfig("d4_1e6", 500, 500, 10, 1_000_000),
     ]
 }
+# NEXT-4 curve clouds: Laplace at ~12 points per occupied leaf box (t = 43); Helmholtz with the
+# leaf box a quarter wavelength at ~7.7 samples per wavelength along the curve (~1.8 points per
+# occupied box).
+CONFIGS.update({c.name: c for c in [
+    ContourConfig("contour_2e5", 200_000, 13),
+    ContourConfig("contour_1e5", 100_000, 15, seed=20240304),
+]})
 
 
 MAX_LEVEL = 15  # the plan builder's level cap (R16)
@@ -103,6 +141,8 @@ def widened(cfg: PlateConfig, factor: int) -> PlateConfig:
     wider plate no longer fits the grid (boxes stay boxes: D is unchanged)."""
     if factor == 1:
         return cfg
+    if not isinstance(cfg, PlateConfig):
+        raise ValueError(f"{cfg.name}: weak scaling widens plates only")
     sx, sy = cfg.sx, cfg.sy
     if sx <= sy:
         sx *= factor
@@ -166,6 +206,9 @@ def make_problem(cfg: PlateConfig | str, kind: str = "iid", seed: int | None = N
         cfg = CONFIGS[cfg]
     seed = cfg.seed if seed is None else seed
     n = cfg.n if n is None else n
+    if isinstance(cfg, ContourConfig):  # collocated boundary nodes (kind does not apply)
+        src = contour_points(cfg, seed, n)
+        return src, src.copy(), weights(n, seed)
     src = plate_points(cfg, 2, 3, kind, seed, n)
     tgt = src.copy() if collocated else plate_points(cfg, 0, 1, kind, seed, n)
     q = weights(n, seed)
