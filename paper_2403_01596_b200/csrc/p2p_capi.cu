@@ -777,13 +777,18 @@ void build_device_plan(p2p_plan_s &P, const p2p_plan_desc &d, const double *dsrc
             parts = pp;
         }
     }
-    const int64_t nent = keep + (nt - keep) * parts;
+    // entries per queue position (tail and heavy-tile splits, TILED only), then their offsets
+    uint32_t *cnt = tmp.get<uint32_t>(nt), *eoff = tmp.get<uint32_t>(nt + 1);
+    const int64_t share = d.layout == P2P_LAYOUT_TILED
+                              ? std::max<int64_t>(1, (hp.pairs + p2p::kSplitShare - 1) / p2p::kSplitShare) : 0;
+    if (nt) split_count_kernel<<<nblocks(nt), kB, 0, s>>>(order, tile_pairs, nt, keep, parts, share, cnt);
+    const int64_t nent = scan_offsets(tmp, cnt, eoff, nt, s);
     P.alloc(P.tiles, (size_t)nent * 4);
     P.alloc(P.tile_slot, (size_t)nent * 4);
     P.alloc(P.tile_part, (size_t)nent * 4);
-    if (nent)
-        queue_kernel<<<nblocks(nent), kB, 0, s>>>(order, tiles_m, nt, keep, parts, (int32_t *)P.tiles.p,
-                                                  (int32_t *)P.tile_slot.p, (int32_t *)P.tile_part.p, nparts);
+    if (nt)
+        queue_kernel<<<nblocks(nt), kB, 0, s>>>(order, tiles_m, nt, cnt, eoff, (int32_t *)P.tiles.p,
+                                                (int32_t *)P.tile_slot.p, (int32_t *)P.tile_part.p, nparts);
     hp.n_interior = nent;
     hp.tiles.resize((size_t)nent);
     d2h(hp.tiles.data(), P.tiles.p, nent, s);

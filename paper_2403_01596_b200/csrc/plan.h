@@ -137,6 +137,14 @@ constexpr int kMaxLevel = 15;          // full-grid CSR offsets: 4^(L-1) <= 2^28
 constexpr int kThreads = 256;          // CTA size of the P2P kernels
 constexpr int kMaxTileLog2 = 6;
 constexpr int64_t kSmemLimit = 200 * 1024;
+constexpr int64_t kSplitShare = 148 * 8;  // TILED: a tile above 1/1184 of the pairs is split (heavy tiles)
+constexpr int64_t kSplitMax = 32;         // at most 32 launch entries per tile
+// Launch entries of a tile with `tile_pairs` pairs: ceil(tile_pairs / share) (<= 32), at least `base`.
+P2P_HD inline int64_t split_parts(int64_t tile_pairs, int64_t share, int64_t base) {
+    int64_t p = (tile_pairs + share - 1) / share;
+    p = p > kSplitMax ? kSplitMax : p;
+    return p > base ? p : base;
+}
 
 // ---- Morton (Z-order) codes: x in the even bits, y in the odd bits
 // ("the order of the boxes' morton index").

@@ -832,31 +832,37 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         hp.tile_slot.swap(s2);
         hp.n_interior = std::count(interior.begin(), interior.end(), (uint8_t)1);
     }
-    // ---- tail splitting (TILED): the last tiles of the queue are split into unit
-    // ranges so the final wave is fine-grained (each target is still computed
-    // whole by one thread: results do not depend on the split).
+    // ---- tile splitting (TILED): a queue entry may run a unit range of its tile (each target is
+    // still computed whole by one thread: results do not depend on the split).
+    //   tail: without LPT, the last 592 queue entries are split in 4 so the final wave is
+    //         fine-grained (LPT already ends on the short tiles);
+    //   heavy: a tile holding more than 1/1184 of the partition's pairs is split into
+    //         ceil(pairs / that share) parts (<= 32) -- clustered clouds (a curve, NEXT-4) put
+    //         a large share of the work in a few tiles, and one CTA per tile would serialise it.
     hp.tile_part.assign(hp.tiles.size(), 1 << 16);
     if (d.layout == P2P_LAYOUT_TILED) {
-        int64_t tail = hp.lpt ? 0 : 148 * 4, parts = 4;  // LPT already ends on the short tiles
+        int64_t tail = hp.lpt ? 0 : 148 * 4, parts = 4;
         if (const char *v = std::getenv("P2P_TAIL_TILES")) tail = std::atoll(v);
         if (const char *v = std::getenv("P2P_TAIL_PARTS")) parts = std::max(1, std::min(16, std::atoi(v)));
         tail = std::min<int64_t>(tail, (int64_t)hp.tiles.size() / 2);
-        if (parts > 1 && tail > 0) {
-            const size_t keep = hp.tiles.size() - (size_t)tail;
-            std::vector<int32_t> t2(hp.tiles.begin(), hp.tiles.begin() + keep),
-                s2(hp.tile_slot.begin(), hp.tile_slot.begin() + keep), p2(keep, 1 << 16);
-            for (size_t i = keep; i < hp.tiles.size(); ++i)
-                for (int64_t q = 0; q < parts; ++q) {
-                    t2.push_back(hp.tiles[i]);
-                    s2.push_back(hp.tile_slot[i]);
-                    p2.push_back((int32_t)(q | (parts << 16)));
-                }
-            hp.tiles.swap(t2);
-            hp.tile_slot.swap(s2);
-            hp.tile_part.swap(p2);
-            // interior tiles that fell in the split tail become `parts` launch entries each
-            if (hp.n_interior > (int64_t)keep) hp.n_interior = (int64_t)keep + (hp.n_interior - (int64_t)keep) * parts;
+        const int64_t keep = parts > 1 && tail > 0 ? (int64_t)hp.tiles.size() - tail : (int64_t)hp.tiles.size();
+        const int64_t share = std::max<int64_t>(1, (hp.pairs + kSplitShare - 1) / kSplitShare);
+        std::vector<int32_t> t2, s2, p2;
+        int64_t n_int = 0;
+        for (int64_t i = 0; i < (int64_t)hp.tiles.size(); ++i) {
+            const int64_t tp = hp.tile_pairs_g[hp.part_tile[r] + hp.tile_slot[i]];
+            const int64_t np_ = split_parts(tp, share, i >= keep ? parts : 1);
+            for (int64_t q = 0; q < np_; ++q) {
+                t2.push_back(hp.tiles[i]);
+                s2.push_back(hp.tile_slot[i]);
+                p2.push_back((int32_t)(q | (np_ << 16)));
+            }
+            if (i < hp.n_interior) n_int += np_;
         }
+        hp.tiles.swap(t2);
+        hp.tile_slot.swap(s2);
+        hp.tile_part.swap(p2);
+        hp.n_interior = n_int;
     }
     // ---- fp64 log table: log x = e ln2 + L_k + log1p(t), t = m c_inv_k - 1, |t| < 2^-8, with
     // c_inv_k = 1 / (1 + (k + 1/2) / 128) rounded to double and L_k = -log(c_inv_k) from the

@@ -405,26 +405,31 @@ __global__ void tiled_slots_kernel(const int32_t *__restrict__ tiles, int64_t nt
     }
 }
 
-// Queue order: launch entry e -> slot (Morton-order tile index) and part | nparts << 16.
-// The first `keep` entries are order[e] whole; the rest are the remaining tiles split in `parts`.
-__global__ void queue_kernel(const int32_t *__restrict__ order, const int32_t *__restrict__ tiles_m, int64_t nt,
-                             int64_t keep, int parts, int32_t *__restrict__ tiles_out, int32_t *__restrict__ slot_out,
-                             int32_t *__restrict__ part_out, int32_t *__restrict__ nparts) {
-    const int64_t nent = keep + (nt - keep) * parts;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nent; e += (int64_t)gridDim.x * blockDim.x) {
-        int64_t li, q = 0;
-        int np = 1;
-        if (e < keep) li = e;
-        else {
-            li = keep + (e - keep) / parts;
-            q = (e - keep) % parts;
-            np = parts;
-        }
+// Queue order, step 1: launch entries of queue position li (tile order[li]): the tail split
+// (li >= keep: `parts`) and the heavy-tile split (split_parts, plan.h), as the host builder.
+__global__ void split_count_kernel(const int32_t *__restrict__ order, const int64_t *__restrict__ tile_pairs,
+                                   int64_t nt, int64_t keep, int parts, int64_t share, uint32_t *__restrict__ cnt) {
+    for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < nt; li += (int64_t)gridDim.x * blockDim.x) {
         const int32_t s = order ? order[li] : (int32_t)li;
-        tiles_out[e] = tiles_m[s];
-        slot_out[e] = s;
-        part_out[e] = (int32_t)(q | ((int64_t)np << 16));
-        if (q == 0 && nparts) nparts[s] = np;
+        cnt[li] = share > 0 ? (uint32_t)split_parts(tile_pairs[s], share, li >= keep ? parts : 1) : 1u;
+    }
+}
+
+// Step 2: launch entry off[li] + q -> tile, slot (Morton-order tile index), q | nparts << 16.
+__global__ void queue_kernel(const int32_t *__restrict__ order, const int32_t *__restrict__ tiles_m, int64_t nt,
+                             const uint32_t *__restrict__ cnt, const uint32_t *__restrict__ off,
+                             int32_t *__restrict__ tiles_out, int32_t *__restrict__ slot_out,
+                             int32_t *__restrict__ part_out, int32_t *__restrict__ nparts) {
+    for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < nt; li += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t s = order ? order[li] : (int32_t)li;
+        const int np = (int)cnt[li];
+        for (int q = 0; q < np; ++q) {
+            const int64_t e = (int64_t)off[li] + q;
+            tiles_out[e] = tiles_m[s];
+            slot_out[e] = s;
+            part_out[e] = (int32_t)(q | (np << 16));
+        }
+        if (nparts) nparts[s] = np;
     }
 }
 

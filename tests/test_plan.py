@@ -257,3 +257,45 @@ def test_interior_launches_read_owned_sources_only(world, level):
             owned = np.all((g >= lo) & (g < hi))
             assert owned == (e < n_int), (r, e, n_int)
         pl.close()
+
+
+def _compact_bits(v):
+    v = v & 0x55555555
+    v = (v | (v >> 1)) & 0x33333333
+    v = (v | (v >> 2)) & 0x0F0F0F0F
+    v = (v | (v >> 4)) & 0x00FF00FF
+    return (v | (v >> 8)) & 0x0000FFFF
+
+
+def test_heavy_tiles_are_split():
+    """A curve cloud concentrates its pairs in few tiles: every tile above 1/1184 of the pairs runs
+    as ceil(pairs / share) consecutive launch entries (<= 32), each a unit range, so no single CTA
+    serialises a large share of the work (tile pair counts recomputed here from the offsets)."""
+    cfg = W.CONFIGS["contour_2e5"]
+    src, tgt, _ = W.make_problem(cfg)
+    pl = _plan(src, tgt, level=cfg.level, layout="tiled", precision="fp32")
+    info = pl.info
+    k, S = info["tile_log2"], info["side"]
+    so, to = pl.export("src_box_offsets"), pl.export("tgt_box_offsets")
+    ns, nt_ = np.diff(so), np.diff(to)
+    b = np.arange(S * S, dtype=np.int64)
+    ix, iy = _compact_bits(b), _compact_bits(b >> 1)
+    grid = np.zeros((S + 2, S + 2), dtype=np.int64)
+    grid[iy + 1, ix + 1] = ns
+    n9 = sum(grid[iy + 1 + dy, ix + 1 + dx] for dy in (-1, 0, 1) for dx in (-1, 0, 1))
+    tile_pairs = np.bincount(b >> (2 * k), weights=nt_ * n9, minlength=(S * S) >> (2 * k)).astype(np.int64)
+    assert tile_pairs.sum() == info["pairs"]
+    share = -(-info["pairs"] // 1184)
+    tiles, launch = pl.export("tiles"), pl.export("launch").reshape(2, -1)
+    parts, q = launch[1] >> 16, launch[1] & 0xFFFF
+    e = 0
+    n_split = 0
+    while e < len(tiles):
+        np_ = parts[e]
+        want = min(32, max(1, -(-tile_pairs[tiles[e]] // share)))
+        assert np_ == want, (e, np_, want)
+        assert list(q[e:e + np_]) == list(range(np_)) and len(set(tiles[e:e + np_])) == 1
+        n_split += np_ > 1
+        e += np_
+    assert n_split > 0
+    pl.close()
