@@ -82,6 +82,10 @@ def lib():
         _lib.oracle_bruteforce_helmholtz.restype = i32
         _lib.oracle_pair_helmholtz.argtypes = [f64] * 8 + [P]
         _lib.oracle_pair_helmholtz.restype = None
+        _lib.oracle_direct_3d.argtypes = [i64, P, P, i64, P, i32, f64, i32, f64, i64, P, P, i32, P]
+        _lib.oracle_direct_3d.restype = i32
+        _lib.oracle_bruteforce_3d.argtypes = [i64, P, P, i64, P, i32, f64, i32, f64, P, P]
+        _lib.oracle_bruteforce_3d.restype = i32
     return _lib
 
 
@@ -222,3 +226,35 @@ def pair_helmholtz(t, s, q: complex, kappa: float, eps: float = 1e-12) -> comple
     lib().oracle_pair_helmholtz(float(t[0]), float(t[1]), float(s[0]), float(s[1]), q.real, q.imag,
                                 eps, kappa, _ptr(out))
     return complex(out[0], out[1])
+
+
+# ---- NEXT-3: 3D kernels on the octree leaf grid (oracle.c oracle_direct_3d) ----
+def direct_3d(src_xyz, q, tgt_xyz, level: int, kernel: str = "laplace", kappa: float = 0.0,
+              eps: float = 1e-12, targets=None, nthreads: int = 0):
+    """phi (real for "laplace": 1/(4 pi r); complex for "helmholtz": e^{i kappa r}/(4 pi r)) and
+    the pair count, over the 3x3x3 neighbour boxes."""
+    src, tgt = _f64(src_xyz), _f64(tgt_xyz)
+    helm = kernel == "helmholtz"
+    qa = _c128(q) if helm else _f64(q)
+    sel = None if targets is None else np.ascontiguousarray(targets, dtype=np.int64)
+    n_out = len(tgt) if sel is None else len(sel)
+    phi = np.empty(n_out, dtype=np.complex128 if helm else np.float64)
+    pairs = C.c_int64(0)
+    rc = lib().oracle_direct_3d(len(src), _ptr(src), _ptr(qa), len(tgt), _ptr(tgt), level, eps, int(helm),
+                                kappa, 0 if sel is None else len(sel), None if sel is None else _ptr(sel),
+                                _ptr(phi), nthreads, C.byref(pairs))
+    if rc:
+        raise MemoryError("oracle_direct_3d allocation failed")
+    return phi, pairs.value
+
+
+def bruteforce_3d(src_xyz, q, tgt_xyz, level: int, kernel: str = "laplace", kappa: float = 0.0,
+                  eps: float = 1e-12):
+    src, tgt = _f64(src_xyz), _f64(tgt_xyz)
+    helm = kernel == "helmholtz"
+    qa = _c128(q) if helm else _f64(q)
+    phi = np.empty(len(tgt), dtype=np.complex128 if helm else np.float64)
+    pairs = C.c_int64(0)
+    lib().oracle_bruteforce_3d(len(src), _ptr(src), _ptr(qa), len(tgt), _ptr(tgt), level, eps, int(helm),
+                               kappa, _ptr(phi), C.byref(pairs))
+    return phi, pairs.value

@@ -447,3 +447,107 @@ void oracle_pair_helmholtz(double xt, double yt, double xs, double ys, double qr
     if (r2 < eps * eps) return;
     helmholtz_pair(r2, kappa, qr, qi, &out[0], &out[1]);
 }
+
+/* ---- NEXT-3: the 3D kernels on an octree leaf grid (R24) ---
+ * The 3D analogue of the paper's operator (the "4x4x4 leaf boxes" reading of BASELINE.json's
+ * tiny config, and the 3D EM workloads of the prior art): leaf grid S = 2^(L-1)
+ * per side on the unit cube, box(p) = (cell(x), cell(y), cell(z)) as in 2D, E1 =
+ * the 3x3x3 block of boxes clipped at the domain edge (27 in the interior), and
+ *   LAPLACE_3D:   G(r) = 1 / (4 pi r)                 (real q, phi)
+ *   HELMHOLTZ_3D: G(r) = exp(i kappa r) / (4 pi r)     (complex q, phi; the outgoing free-space
+ *                                                       Green's function of Delta + kappa^2)
+ * with the same guard (r < eps contributes 0).  Points are [n][3]; complex values (re, im). */
+static void kernel3(double r2, int helm, double kappa, const double *q, double *acc)
+{
+    double r = sqrt(r2);
+    double g = 1.0 / (4.0 * M_PI * r);
+    if (!helm) {
+        acc[0] += q[0] * g;
+        return;
+    }
+    double c = cos(kappa * r) * g, s = sin(kappa * r) * g; /* G = (c + i s) */
+    acc[0] += q[0] * c - q[1] * s;
+    acc[1] += q[0] * s + q[1] * c;
+}
+
+int oracle_direct_3d(int64_t ns, const double *src, const double *q, int64_t nt, const double *tgt,
+                     int L, double eps, int helm, double kappa, int64_t nsel, const int64_t *sel,
+                     double *phi_out, int nthreads, int64_t *pairs_out)
+{
+    int64_t S = grid_side(L), cells = S * S * S;
+    int64_t *start = (int64_t *)calloc((size_t)(cells + 1), sizeof(int64_t));
+    int64_t *items = (int64_t *)malloc((size_t)(ns > 0 ? ns : 1) * sizeof(int64_t));
+    int64_t *fill = (int64_t *)malloc((size_t)cells * sizeof(int64_t));
+    if (!start || !items || !fill) { free(start); free(items); free(fill); return -1; }
+    for (int64_t s = 0; s < ns; ++s) {  /* bucket the sources, original index order per cell */
+        int64_t c = (cell_of(src[3 * s + 2], S) * S + cell_of(src[3 * s + 1], S)) * S + cell_of(src[3 * s], S);
+        start[c + 1] += 1;
+    }
+    for (int64_t c = 0; c < cells; ++c) start[c + 1] += start[c];
+    memcpy(fill, start, (size_t)cells * sizeof(int64_t));
+    for (int64_t s = 0; s < ns; ++s) {
+        int64_t c = (cell_of(src[3 * s + 2], S) * S + cell_of(src[3 * s + 1], S)) * S + cell_of(src[3 * s], S);
+        items[fill[c]++] = s;
+    }
+    free(fill);
+    int64_t count = sel ? nsel : nt, pairs = 0;
+    int w = helm ? 2 : 1;
+    double eps2 = eps * eps;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 64) reduction(+ : pairs)
+    for (int64_t k = 0; k < count; ++k) {
+        int64_t t = sel ? sel[k] : k;
+        double xt = tgt[3 * t], yt = tgt[3 * t + 1], zt = tgt[3 * t + 2];
+        int64_t ix = cell_of(xt, S), iy = cell_of(yt, S), iz = cell_of(zt, S);
+        double acc[2] = {0.0, 0.0};
+        for (int64_t dz = -1; dz <= 1; ++dz)
+            for (int64_t dy = -1; dy <= 1; ++dy)
+                for (int64_t dx = -1; dx <= 1; ++dx) {
+                    int64_t cx = ix + dx, cy = iy + dy, cz = iz + dz;
+                    if (cx < 0 || cy < 0 || cz < 0 || cx >= S || cy >= S || cz >= S) continue;
+                    int64_t c = (cz * S + cy) * S + cx;
+                    for (int64_t j = start[c]; j < start[c + 1]; ++j) {
+                        int64_t s = items[j];
+                        double ddx = xt - src[3 * s], ddy = yt - src[3 * s + 1], ddz = zt - src[3 * s + 2];
+                        double r2 = ddx * ddx + ddy * ddy + ddz * ddz;
+                        pairs += 1;
+                        if (r2 < eps2) continue;
+                        kernel3(r2, helm, kappa, &q[w * s], acc);
+                    }
+                }
+        for (int i = 0; i < w; ++i) phi_out[w * k + i] = acc[i];
+    }
+    free(start);
+    free(items);
+    if (pairs_out) *pairs_out = pairs;
+    return 0;
+}
+
+/* Brute force: every (t, s) pair filtered by the 3x3x3 adjacency predicate. */
+int oracle_bruteforce_3d(int64_t ns, const double *src, const double *q, int64_t nt, const double *tgt,
+                         int L, double eps, int helm, double kappa, double *phi_out, int64_t *pairs_out)
+{
+    int64_t S = grid_side(L), pairs = 0;
+    int w = helm ? 2 : 1;
+    double eps2 = eps * eps;
+    for (int64_t t = 0; t < nt; ++t) {
+        double acc[2] = {0.0, 0.0};
+        for (int64_t s = 0; s < ns; ++s) {
+            int near = 1;
+            for (int d = 0; d < 3; ++d)
+                if (llabs(cell_of(src[3 * s + d], S) - cell_of(tgt[3 * t + d], S)) > 1) near = 0;
+            if (!near) continue;
+            pairs += 1;
+            double ddx = tgt[3 * t] - src[3 * s], ddy = tgt[3 * t + 1] - src[3 * s + 1];
+            double ddz = tgt[3 * t + 2] - src[3 * s + 2];
+            double r2 = ddx * ddx + ddy * ddy + ddz * ddz;
+            if (r2 < eps2) continue;
+            kernel3(r2, helm, kappa, &q[w * s], acc);
+        }
+        for (int i = 0; i < w; ++i) phi_out[w * t + i] = acc[i];
+    }
+    if (pairs_out) *pairs_out = pairs;
+    return 0;
+}
