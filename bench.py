@@ -44,8 +44,12 @@ WORKLOADS = {
     "helmholtz_1e6": ["d16_1e6", "d4_1e6"],                     # NEXT-3: 2D Helmholtz, leaf = lambda/4
     "contour_2e5": ["contour_2e5"],                             # NEXT-4: curve cloud, Laplace
     "contour_helmholtz": ["contour_1e5"],                       # NEXT-4: curve cloud, Helmholtz, leaf = lambda/4
+    "cube3d_1e6": ["cube3d_1e6"],                               # NEXT-3: 3D Laplace, 16 per box
+    "cube3d_helmholtz": ["cube3d_1e6"],                         # NEXT-3: 3D Helmholtz, leaf = lambda/4
 }
-HELMHOLTZ_WORKLOADS = ("helmholtz_1e6", "contour_helmholtz")
+DEFAULT_KERNEL = {"helmholtz_1e6": "helmholtz", "contour_helmholtz": "helmholtz", "cube3d_1e6": "laplace3d",
+                  "cube3d_helmholtz": "helmholtz3d"}
+MUFU_PER_PAIR_3D = {"laplace3d": 1, "helmholtz3d": 3}  # RSQ; RSQ + SIN + COS
 METRIC = "P2P pair-interactions/s"
 MUFU_LG2_PER_CLK_PER_SM = 16       # SFU issue rate (checked by libp2p_peaks)
 SM_COUNT = 148
@@ -73,28 +77,35 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras/baseline)")
     ap.add_argument("--configs", default="", help="comma list of config names overriding --workload")
     ap.add_argument("--tile", type=int, default=-1, help="force CTA tile side 2^tile (default: plan's choice)")
-    ap.add_argument("--kernel", default=None, choices=["laplace", "helmholtz"],
+    ap.add_argument("--kernel", default=None, choices=["laplace", "helmholtz", "laplace3d", "helmholtz3d"],
                     help="kernel function (default: helmholtz for the helmholtz_1e6 workload, else laplace)")
     ap.add_argument("--kh", type=float, default=math.pi / 2,
                     help="helmholtz: kappa * leaf box side (pi/2 = a quarter-wavelength box)")
     a = ap.parse_args()
     if a.kernel is None:
-        a.kernel = "helmholtz" if a.workload in HELMHOLTZ_WORKLOADS else "laplace"
+        a.kernel = DEFAULT_KERNEL.get(a.workload, "laplace")
     if a.kernel == "helmholtz":
         a.layout = "tiled"
         a.no_extras = True
+    if a.kernel.endswith("3d"):  # the box-per-CTA NR path, host plan build
+        a.layout = "nr"
+        a.no_extras = True
+        a.build = "host"
     return a
 
 
 def _kernel_kw(args, cfg):
     """Plan keywords of the kernel function (Helmholtz: kappa from the leaf box side)."""
-    if args.kernel != "helmholtz":
+    if args.kernel == "laplace":
         return {}
-    return {"kernel": "helmholtz", "wavenumber": args.kh * (1 << (cfg.level - 1))}
+    kw = {"kernel": args.kernel}
+    if args.kernel.startswith("helmholtz"):
+        kw["wavenumber"] = args.kh * (1 << (cfg.level - 1))
+    return kw
 
 
 def _weights(args, cfg, q):
-    return W.weights_complex(cfg.n, cfg.seed) if args.kernel == "helmholtz" else q
+    return W.weights_complex(cfg.n, cfg.seed) if args.kernel.startswith("helmholtz") else q
 
 
 # ---------------------------------------------------------------- clocks
@@ -175,6 +186,11 @@ def cpu_baseline(cfg_names, kind, budget_s, seed_stream=0, kernel="laplace", kh=
         if kernel == "helmholtz":
             _, p = oracle.direct_helmholtz(s, W.weights_complex(cfg.n, cfg.seed), t, cfg.level,
                                            kh * (1 << (cfg.level - 1)), targets=sel)
+        elif kernel == "laplace3d":
+            _, p = oracle.direct_3d(s, q, t, cfg.level, targets=sel)
+        elif kernel == "helmholtz3d":
+            _, p = oracle.direct_3d(s, W.weights_complex(cfg.n, cfg.seed), t, cfg.level, "helmholtz",
+                                    kh * (1 << (cfg.level - 1)), targets=sel)
         else:
             _, p = oracle.direct(s, q, t, cfg.level, targets=sel)
         return p, time.perf_counter() - tic
@@ -356,7 +372,14 @@ def main():
     t_mufu = sum(j["info"]["pairs"] / (peak_mufu * 1e9) for j in jobs)
     t_hbm = sum(j["info"]["alg_bytes_kernel"] / (peak_hbm * 1e9) for j in jobs)
     traffic = _ncu_traffic(args, [j["name"] for j in jobs]) if world == 1 else None
-    if args.kernel == "helmholtz":  # issue-bound: instructions per pair from ncu
+    if args.kernel in MUFU_PER_PAIR_3D:  # 3D: MUFU ops per pair (RSQ [+ SIN + COS])
+        m = MUFU_PER_PAIR_3D[args.kernel]
+        achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak_mufu / m,
+                    "unit": f"Gpair/s ({m} MUFU per pair)", "frac": achieved / (peak_mufu / m), "traffic": traffic,
+                    "peak_basis": f"{MUFU_LG2_PER_CLK_PER_SM} MUFU/clk/SM x {SM_COUNT} SMs x {peak_clk / 1e6:.0f} MHz "
+                                  f"/ {m} per pair; DESIGN.md §9e"}
+    elif args.kernel == "helmholtz":  # issue-bound: instructions per pair from ncu
         achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
         ipp = _helm_inst_per_pair(args.precision)
         peak = 128 * SM_COUNT * peak_clk / ipp / 1e9 if ipp else None
@@ -402,7 +425,7 @@ def main():
         "config": {"workload": args.workload + (f" x{world} (plates widened, weak scaling)" if weak else ""),
                    "configs": [j["cfg"].name for j in jobs], "layout": args.layout,
                    "precision": args.precision, "kind": args.kind, "pairs_per_step": pairs_step,
-                   "kernel": args.kernel, **({"kappa_h": args.kh} if args.kernel == "helmholtz" else {}),
+                   "kernel": args.kernel, **({"kappa_h": args.kh} if args.kernel.startswith("helmholtz") else {}),
                    "order": "plan", "l2": "flushed (256 MiB write) between timed steps",
                    "parallelism": f"morton-range x{world}" + (
                        (" + host-staged gloo halo exchange, ranks sharing GPUs (TEST MODE)" if shared
@@ -414,7 +437,7 @@ def main():
         out["cpu_baseline"] = {k: v for k, v in cpu_baseline(names, args.kind, args.cpu_seconds, kernel=args.kernel,
                                                              kh=args.kh).items()
                                if k not in ("pairs", "seconds")}
-    if rank == 0 and world == 1 and not args.profile and args.layout in ("nr", "tiled"):
+    if rank == 0 and world == 1 and not args.profile and args.layout in ("nr", "tiled") and not args.kernel.endswith("3d"):
         out["plan_build"] = _plan_build(args, jobs, dev)
     if rank == 0 and world == 1 and not args.no_extras and not args.profile:
         out["extras"] = _extras(args, names, stream, dev)

@@ -62,8 +62,20 @@ typedef enum {
  *                free-space Green's function of the oscillatory ("high-frequency", PAPER.md
  *                L17, L299) MLFMA problems; kappa = desc.wavenumber > 0; q and phi complex,
  *                interleaved (re, im) pairs in the plan precision (C99 complex / torch
- *                complex64 / complex128 layout).  TILED layout, one partition. */
-typedef enum { P2P_KERNEL_LAPLACE_2D = 0, P2P_KERNEL_HELMHOLTZ_2D = 1 } p2p_kernel;
+ *                complex64 / complex128 layout).  TILED layout, one partition.
+ *   LAPLACE_3D / HELMHOLTZ_3D (R24): the operator on an octree
+ *                leaf grid of the unit cube -- boxes 2^(L-1) per side (L <= 9), E1 = the 3x3x3 block
+ *                clipped at the faces, 3D Morton order (x bit 3i, y 3i+1, z 3i+2); G = 1/(4 pi r)
+ *                (real) or e^{i kappa r}/(4 pi r) (complex, interleaved (re, im)).  Coordinates
+ *                are [n][3] (src_xy / tgt_xy hold x, y, z); explicit level only; NONREDUNDANT
+ *                layout (one CTA per target box stages its 27 neighbour boxes); one partition;
+ *                host plan build. */
+typedef enum {
+    P2P_KERNEL_LAPLACE_2D = 0,
+    P2P_KERNEL_HELMHOLTZ_2D = 1,
+    P2P_KERNEL_LAPLACE_3D = 2,
+    P2P_KERNEL_HELMHOLTZ_3D = 3
+} p2p_kernel;
 
 /* Source layouts (§3.2 Indexing = non-redundant; §3.3 Repetition =
  * redundant), re-derived for B200:

@@ -127,6 +127,12 @@ template <typename T>
 void finalize_plan(p2p_plan_s &P);
 
 template <typename T>
+const void *box3d_fn(bool helm) {
+    return helm ? (const void *)p2p::dev::p2p_box3d_kernel<T, true, p2p::kBox3Threads>
+                : (const void *)p2p::dev::p2p_box3d_kernel<T, false, p2p::kBox3Threads>;
+}
+
+template <typename T>
 const void *helm_fn(int nt) {
     using namespace p2p::dev;
     switch (nt) {
@@ -194,7 +200,8 @@ void finalize_plan(p2p_plan_s &P) {
     // Dynamic shared memory is fixed per plan: opt in once (a permission, not a
     // reservation, so one value serves all plans), then size the persistent grid.
     const bool two = hp.tpi == 2;
-    const void *kfn = hp.kernel == P2P_KERNEL_HELMHOLTZ_2D ? helm_fn<T>(hp.nt)
+    const void *kfn = hp.dim == 3 ? box3d_fn<T>(hp.kernel == P2P_KERNEL_HELMHOLTZ_3D)
+                      : hp.kernel == P2P_KERNEL_HELMHOLTZ_2D ? helm_fn<T>(hp.nt)
                       : hp.layout == P2P_LAYOUT_REDUNDANT ? (const void *)p2p::dev::p2p_r_kernel<T>
                       : hp.layout == P2P_LAYOUT_TILED
                           ? tiled_fn<T>(hp.tpi, hp.nt, hp.pad, hp.ns)
@@ -339,9 +346,46 @@ void apply_paper(p2p_plan_s &P, const void *d_q, void *d_out, int order, int acc
     ck(cudaGetLastError(), "paper apply launch");
 }
 
+// 3D kernels (NEXT-3): one CTA per target box; user order fused (weights gathered through the
+// sources' user indices while staging, results written through the targets' user indices).
+template <typename T>
+void launch_box3d(p2p_plan_s &P, const T *q, T *out, bool user, int accumulate, cudaStream_t s) {
+    const p2p::HostPlan &hp = P.hp;
+    const int ntiles = (int)hp.tiles.size();
+    if (ntiles <= 0) return;
+    p2p::dev::P2PArgs<T> a{};
+    a.tiles = (const int32_t *)P.tiles.p;
+    a.ntiles = ntiles;
+    a.queue = (int *)P.queue.p;
+    a.S = hp.S;
+    a.src_cap = (int)hp.src_cap;
+    a.src_off = (const int32_t *)P.src_off.p;
+    a.tgt_off = (const int32_t *)P.tgt_off.p;
+    a.src_p4 = (const T *)P.src_uv.p;
+    a.tgt_p4 = (const T *)P.tgt_uv.p;
+    a.src_idx = user ? (const int32_t *)P.src_uidx.p : nullptr;
+    a.out_idx = user ? (const int32_t *)P.tgt_uidx.p : nullptr;
+    a.q = q;
+    a.out = out;
+    a.accumulate = accumulate;
+    const double eh = hp.eps * (double)hp.S;  // eps in units of h
+    a.eps2 = (T)(eh * eh);
+    a.scale = (T)(1.0 / (4.0 * 3.14159265358979323846 * hp.h));
+    a.kh = (T)(hp.kappa * hp.h);
+    void *args[] = {&a};
+    const int grid = (int)std::min<int64_t>(ntiles, P.occ_sms);
+    ck(cudaLaunchKernel(box3d_fn<T>(hp.kernel == P2P_KERNEL_HELMHOLTZ_3D), dim3(grid), dim3(p2p::kBox3Threads), args,
+                        (size_t)hp.smem_bytes, s),
+       "box3d launch");
+}
+
 template <typename T>
 void apply_impl(p2p_plan_s &P, const void *d_q, void *d_out, int order, int accumulate, cudaStream_t s) {
     const p2p::HostPlan &hp = P.hp;
+    if (hp.dim == 3) {
+        launch_box3d<T>(P, (const T *)d_q, (T *)d_out, order == P2P_ORDER_USER, accumulate, s);
+        return;
+    }
     if (hp.layout == P2P_LAYOUT_PAPER_INDEXING || hp.layout == P2P_LAYOUT_PAPER_REPETITION) {
         if constexpr (sizeof(T) == 8) apply_paper(P, d_q, d_out, order, accumulate, s);
         return;
@@ -887,7 +931,7 @@ p2p_status p2p_plan_create(const p2p_plan_desc *desc, p2p_plan *out) {
         p2p::build_host_plan(*desc, P->hp);
         P->device = desc->device;
         P->elem = desc->precision == P2P_FP32 ? 4 : 8;
-        P->comps = desc->kernel == P2P_KERNEL_HELMHOLTZ_2D ? 2 : 1;
+        P->comps = (desc->kernel == P2P_KERNEL_HELMHOLTZ_2D || desc->kernel == P2P_KERNEL_HELMHOLTZ_3D) ? 2 : 1;
         if (desc->device >= 0) {
             int ndev = 0;
             if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -921,6 +965,7 @@ p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src
         const p2p_plan_desc &d = *desc;
         if (d.struct_size != sizeof(p2p_plan_desc)) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
         p2p::check_kernel(d);
+        if (p2p::kernel_dim(d.kernel) == 3) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "device build: 2D kernels");
         if (d.precision != P2P_FP32 && d.precision != P2P_FP64) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "bad precision");
         if (d.layout != P2P_LAYOUT_NONREDUNDANT && d.layout != P2P_LAYOUT_TILED)
             throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "device build: NR and TILED layouts only (others: p2p_plan_create)");

@@ -307,6 +307,11 @@ struct P2PArgs {
     T *out;
     int accumulate;
     T kappa;                    // HELMHOLTZ_2D wavenumber
+    // 3D box kernel (NEXT-3)
+    const T *src_p4, *tgt_p4;   // box-local coordinates in units of h, 4 per point (x, y, z, 0), plan order
+    const int32_t *src_idx;     // ORDER_USER: user index of each plan-order source (weights gathered through it)
+    T scale;                    // 1 / (4 pi h)
+    T kh;                       // kappa h (HELMHOLTZ_3D)
 };
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -1174,6 +1179,189 @@ __global__ void __launch_bounds__(NT) p2p_tiled_helm_kernel(const P2PArgs<T> a) 
         cur = s_next[it & 1];
         tb = s_base_next[it & 1];
         if (tid == 0 && cur < a.ntiles) issue(cur);
+    }
+    if (tid == 0) queue_exit(a.queue);
+}
+
+// ---------------------------------------------------------------- 3D box kernel (NEXT-3)
+// Octree leaf grid of the unit cube (include/p2p.h LAPLACE_3D / HELMHOLTZ_3D; R24).
+// Persistent CTAs pull target boxes from the queue (longest first); per box the 27 neighbour
+// boxes' CSR segments are staged into shared memory, each source shifted by its box offset so
+// all coordinates are relative to the target box origin in units of h (x, y, z, q); the box's
+// targets are then swept against the staged sources -- every lane of a warp reads the same
+// source (a broadcast, no bank conflicts).  Boxes with fewer targets than threads split the
+// sources into C = NT / n_t chunks per target (fixed chunking, fixed-order reduction: results
+// are bit-reproducible).  Per pair: Laplace 1 MUFU.RSQ + 7 FP32; Helmholtz adds r, the phase
+// kappa h r reduced to [-pi, pi] and __sincosf (2 MUFU).  fp64: rsqrt, sincos.
+__device__ __forceinline__ uint32_t compact3(uint32_t v) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int b = 0; b < 10; ++b) r |= ((v >> (3 * b)) & 1u) << b;
+    return r;
+}
+__device__ __forceinline__ uint32_t spread3d(uint32_t v) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int b = 0; b < 10; ++b) r |= ((v >> b) & 1u) << (3 * b);
+    return r;
+}
+
+template <typename T, bool HELM>
+__device__ __forceinline__ void box3d_pairs(const T *__restrict__ P, const T *__restrict__ QI, int s0, int s1, T tx,
+                                            T ty, T tz, T eps2, T kh, T &re, T &im) {
+    for (int s = s0; s < s1; ++s) {
+        T px, py, pz, q;
+        if constexpr (sizeof(T) == 4) {
+            const float4 v = reinterpret_cast<const float4 *>(P)[s];
+            px = v.x; py = v.y; pz = v.z; q = v.w;
+        } else {
+            const double2 a = reinterpret_cast<const double2 *>(P)[2 * s], b = reinterpret_cast<const double2 *>(P)[2 * s + 1];
+            px = a.x; py = a.y; pz = b.x; q = b.y;
+        }
+        const T dx = tx - px, dy = ty - py, dz = tz - pz;
+        const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        if (!(r2 >= eps2)) continue;  // coincident points contribute 0 (R3)
+        const T rs = rsqrt(r2);
+        if constexpr (!HELM) {
+            re = fma(q, rs, re);
+        } else {
+            const T qi = QI[s];
+            T sn, cs;
+            const T ph = kh * (r2 * rs);
+            if constexpr (sizeof(T) == 4) {
+                const float n = rintf(ph * 0.15915494309189535f);  // to [-pi, pi]
+                const float x = fmaf(-n, 6.28318548202514648f, fmaf(-n, -1.7484556e-07f, ph));
+                __sincosf(x, &sn, &cs);
+            } else {
+                sincos(ph, &sn, &cs);
+            }
+            const T gc = cs * rs, gs = sn * rs;
+            re = fma(q, gc, fma(-qi, gs, re));
+            im = fma(q, gs, fma(qi, gc, im));
+        }
+    }
+}
+
+template <typename T, bool HELM, int NT>
+__global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_box;
+    constexpr int comps = HELM ? 2 : 1;
+    const B3Carve c = box3d_carve(a.src_cap, (int)sizeof(T), comps, NT);
+    T *s_p = reinterpret_cast<T *>(smem + c.p);
+    T *s_qi = reinterpret_cast<T *>(smem + c.qi);
+    T *s_part = reinterpret_cast<T *>(smem + c.part);
+    int *s_nbs = reinterpret_cast<int *>(smem + c.nbs), *s_pre = reinterpret_cast<int *>(smem + c.pre);
+    int *s_nbd = reinterpret_cast<int *>(smem + c.nbd);
+    const int tid = threadIdx.x;
+    const int64_t S = a.S;
+    for (;;) {
+        if (tid == 0) {
+            const int e = atomicAdd(a.queue, 1);
+            s_box = e < a.ntiles ? a.tiles[e] : -1;
+        }
+        __syncthreads();
+        const int b = s_box;
+        if (b < 0) break;
+        if (tid < 32) {  // neighbour boxes: start, count (0 outside the cube), shift; prefix of counts
+            int cnt = 0, st = 0, code = 0;
+            if (tid < 27) {
+                const int dx = tid % 3 - 1, dy = (tid / 3) % 3 - 1, dz = tid / 9 - 1;
+                const int64_t x = (int64_t)compact3((uint32_t)b) + dx, y = (int64_t)compact3((uint32_t)b >> 1) + dy,
+                              z = (int64_t)compact3((uint32_t)b >> 2) + dz;
+                if (x >= 0 && y >= 0 && z >= 0 && x < S && y < S && z < S) {
+                    const uint32_t m = spread3d((uint32_t)x) | spread3d((uint32_t)y) << 1 | spread3d((uint32_t)z) << 2;
+                    st = a.src_off[m];
+                    cnt = a.src_off[m + 1] - st;
+                }
+                code = (dx + 1) | (dy + 1) << 2 | (dz + 1) << 4;
+            }
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += v;
+            }
+            if (tid < 27) {
+                s_nbs[tid] = st;
+                s_pre[tid] = incl - cnt;
+                s_nbd[tid] = code;
+            }
+            if (tid == 26) s_pre[27] = incl;
+        }
+        __syncthreads();
+        const int total = s_pre[27];
+        for (int i = tid; i < total; i += NT) {  // stage: source i of neighbour nb, shifted into the target box frame
+            int nb = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1)
+                if (nb + step < 27 && s_pre[nb + step] <= i) nb += step;
+            const int j = s_nbs[nb] + (i - s_pre[nb]);
+            const int code = s_nbd[nb];
+            const T sx = (T)((code & 3) - 1), sy = (T)(((code >> 2) & 3) - 1), sz = (T)(((code >> 4) & 3) - 1);
+            const int jq = a.src_idx ? a.src_idx[j] : j;
+            T q, qi = (T)0;
+            if constexpr (HELM) {
+                q = a.q[2 * (int64_t)jq];
+                qi = a.q[2 * (int64_t)jq + 1];
+                s_qi[i] = qi;
+            } else {
+                q = a.q[jq];
+            }
+            const T *sp = a.src_p4 + 4 * (int64_t)j;
+            if constexpr (sizeof(T) == 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(sp);
+                reinterpret_cast<float4 *>(s_p)[i] = make_float4(v.x + sx, v.y + sy, v.z + sz, q);
+            } else {
+                const double2 u = reinterpret_cast<const double2 *>(sp)[0], w = reinterpret_cast<const double2 *>(sp)[1];
+                reinterpret_cast<double2 *>(s_p)[2 * i] = make_double2(u.x + sx, u.y + sy);
+                reinterpret_cast<double2 *>(s_p)[2 * i + 1] = make_double2(w.x + sz, q);
+            }
+        }
+        __syncthreads();
+        const int t0 = a.tgt_off[b], nt = a.tgt_off[b + 1] - t0;
+        const int C = nt >= NT ? 1 : NT / nt;  // source chunks per target
+        auto finish = [&](int t, T re, T im) {
+            const int64_t o = a.out_idx ? a.out_idx[t0 + t] : t0 + t;
+            re *= a.scale;
+            if constexpr (HELM) {
+                im *= a.scale;
+                if (a.accumulate) {
+                    re += a.out[2 * o];
+                    im += a.out[2 * o + 1];
+                }
+                a.out[2 * o] = re;
+                a.out[2 * o + 1] = im;
+            } else {
+                a.out[o] = a.accumulate ? a.out[o] + re : re;
+            }
+        };
+        for (int it = tid; it < nt * C; it += NT) {
+            const int t = it % nt, ch = it / nt;
+            const T *tp = a.tgt_p4 + 4 * (int64_t)(t0 + t);
+            const T tx = tp[0], ty = tp[1], tz = tp[2];
+            T re = (T)0, im = (T)0;
+            box3d_pairs<T, HELM>(s_p, s_qi, (int)((int64_t)total * ch / C), (int)((int64_t)total * (ch + 1) / C), tx,
+                                 ty, tz, a.eps2, a.kh, re, im);
+            if (C == 1) {
+                finish(t, re, im);
+            } else {
+                s_part[comps * it] = re;
+                if constexpr (HELM) s_part[comps * it + 1] = im;
+            }
+        }
+        if (C > 1) {
+            __syncthreads();
+            for (int t = tid; t < nt; t += NT) {  // chunks summed in order
+                T re = (T)0, im = (T)0;
+                for (int ch = 0; ch < C; ++ch) {
+                    re += s_part[comps * (ch * nt + t)];
+                    if constexpr (HELM) im += s_part[comps * (ch * nt + t) + 1];
+                }
+                finish(t, re, im);
+            }
+        }
+        __syncthreads();
     }
     if (tid == 0) queue_exit(a.queue);
 }

@@ -134,6 +134,29 @@ struct Error : std::runtime_error {
 };
 
 constexpr int kMaxLevel = 15;          // full-grid CSR offsets: 4^(L-1) <= 2^28 boxes
+constexpr int kMaxLevel3 = 9;          // 3D: 8^(L-1) <= 2^24 boxes
+constexpr int kBox3Threads = 128;      // 3D: threads per CTA (one target box per CTA)
+P2P_HD inline int kernel_dim(int kernel) { return kernel >= P2P_KERNEL_LAPLACE_3D ? 3 : 2; }
+// 3D box kernel shared memory: staged sources (x, y, z, q_re) and q_im (complex), per-thread
+// partial sums (comps values), and per neighbour box its source start, prefix and shift code.
+struct B3Carve {
+    int p, qi, part, nbs, pre, nbd, total;
+};
+P2P_HD inline B3Carve box3d_carve(int src_cap, int e, int comps, int nt) {
+    B3Carve c;
+    c.p = 0;
+    c.qi = c.p + 4 * e * src_cap;
+    c.part = align16(c.qi + (comps == 2 ? e * src_cap : 0));
+    c.nbs = align16(c.part + nt * comps * e);
+    c.pre = c.nbs + 4 * 28;
+    c.nbd = c.pre + 4 * 28;
+    c.total = c.nbd + 4 * 28;
+    return c;
+}
+inline int64_t box3d_smem(int64_t src_cap, int e, int comps, int nt) {
+    if (src_cap > (1 << 20)) return int64_t(1) << 40;
+    return box3d_carve((int)src_cap, e, comps, nt).total;
+}
 constexpr int kThreads = 256;          // CTA size of the P2P kernels
 constexpr int kMaxTileLog2 = 6;
 constexpr int64_t kSmemLimit = 200 * 1024;
@@ -184,6 +207,7 @@ struct HostPlan {
     // ---- parameters
     int L = 0, k = 0, layout = 0, precision = 0, device = -1;
     int kernel = P2P_KERNEL_LAPLACE_2D;          // p2p_kernel
+    int dim = 2;                                 // 3 for the 3D kernels (octree leaf grid)
     double kappa = 0.0;                          // HELMHOLTZ_2D wavenumber
     int part_world = 1, part_rank = 0;
     int64_t S = 0, B = 0;        // grid side, number of leaf boxes
@@ -280,6 +304,7 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
 void check_kernel(const p2p_plan_desc &d);  // kernel function + envelope (throws Error)
 
 void build_host_plan(const p2p_plan_desc &desc, HostPlan &hp);
+void build_host_plan_3d(const p2p_plan_desc &desc, HostPlan &hp);
 void build_log_table(HostPlan &hp);
 std::vector<int64_t> neighbors_export(const HostPlan &hp);
 

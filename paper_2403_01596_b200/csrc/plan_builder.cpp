@@ -189,11 +189,168 @@ void build_log_table(HostPlan &hp) {
 // layout, one partition.
 void check_kernel(const p2p_plan_desc &d) {
     if (d.kernel == P2P_KERNEL_LAPLACE_2D) return;
-    if (d.kernel != P2P_KERNEL_HELMHOLTZ_2D) fail(P2P_ERROR_INVALID_ARGUMENT, "bad kernel");
-    if (!(d.wavenumber > 0.0) || !std::isfinite(d.wavenumber))
-        fail(P2P_ERROR_INVALID_ARGUMENT, "HELMHOLTZ_2D needs wavenumber > 0");
-    if (d.layout != P2P_LAYOUT_TILED) fail(P2P_ERROR_NOT_SUPPORTED, "HELMHOLTZ_2D runs on the TILED layout");
-    if (d.part_world != 1) fail(P2P_ERROR_NOT_SUPPORTED, "HELMHOLTZ_2D: one partition");
+    if (d.kernel < P2P_KERNEL_HELMHOLTZ_2D || d.kernel > P2P_KERNEL_HELMHOLTZ_3D)
+        fail(P2P_ERROR_INVALID_ARGUMENT, "bad kernel");
+    if (d.kernel != P2P_KERNEL_LAPLACE_3D && (!(d.wavenumber > 0.0) || !std::isfinite(d.wavenumber)))
+        fail(P2P_ERROR_INVALID_ARGUMENT, "Helmholtz kernels need wavenumber > 0");
+    if (d.kernel == P2P_KERNEL_HELMHOLTZ_2D && d.layout != P2P_LAYOUT_TILED)
+        fail(P2P_ERROR_NOT_SUPPORTED, "HELMHOLTZ_2D runs on the TILED layout");
+    if (kernel_dim(d.kernel) == 3 && d.layout != P2P_LAYOUT_NONREDUNDANT)
+        fail(P2P_ERROR_NOT_SUPPORTED, "3D kernels run on the NONREDUNDANT (box-per-CTA) layout");
+    if (d.part_world != 1) fail(P2P_ERROR_NOT_SUPPORTED, "kernels other than LAPLACE_2D: one partition");
+}
+
+// ---- 3D: octree leaf grid, 3D Morton order (x bit 3i, y 3i+1, z 3i+2),
+// E1 = the 3x3x3 block clipped at the faces; one CTA per target box stages its <= 27 neighbour
+// boxes (p2p_box3d_kernel).
+namespace {
+inline uint32_t spread3(uint32_t v) {
+    uint32_t r = 0;
+    for (int b = 0; b < 10; ++b) r |= ((v >> b) & 1u) << (3 * b);
+    return r;
+}
+inline uint32_t morton3(uint32_t x, uint32_t y, uint32_t z) { return spread3(x) | spread3(y) << 1 | spread3(z) << 2; }
+}  // namespace
+
+void build_host_plan_3d(const p2p_plan_desc &d, HostPlan &hp) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (d.layout != P2P_LAYOUT_NONREDUNDANT) fail(P2P_ERROR_NOT_SUPPORTED, "3D: NONREDUNDANT layout");
+    if (d.precision != P2P_FP32 && d.precision != P2P_FP64) fail(P2P_ERROR_INVALID_ARGUMENT, "bad precision");
+    if (!(d.epsilon > 0.0) || !std::isfinite(d.epsilon)) fail(P2P_ERROR_INVALID_ARGUMENT, "epsilon must be > 0");
+    if (d.part_world != 1 || d.part_rank != 0) fail(P2P_ERROR_NOT_SUPPORTED, "3D: one partition");
+    auto validate3 = [&](const double *xyz, int64_t n, const char *what) {
+        if (n < 1) fail(P2P_ERROR_INVALID_ARGUMENT, std::string(what) + ": n must be >= 1 (SPEC.md L55)");
+        if (!xyz) fail(P2P_ERROR_INVALID_ARGUMENT, std::string(what) + ": NULL coordinates");
+        for (int64_t i = 0; i < 3 * n; ++i)
+            if (!(xyz[i] >= 0.0 && xyz[i] <= 1.0))
+                fail(P2P_ERROR_INVALID_ARGUMENT, std::string(what) + ": coordinate " + std::to_string(i / 3) +
+                                                     " outside the unit cube [0,1]^3");
+    };
+    validate3(d.src_xy, d.n_src, "sources");
+    validate3(d.tgt_xy, d.n_tgt, "targets");
+    if (d.n_src > INT32_MAX - 8 || d.n_tgt > INT32_MAX - 8) fail(P2P_ERROR_NOT_SUPPORTED, "more than 2^31 points per set");
+    if (d.level < 1) fail(P2P_ERROR_NOT_SUPPORTED, "3D: give the leaf level (no CT loop)");
+    const int L = d.level + d.level_delta;
+    if (L < 1) fail(P2P_ERROR_INVALID_ARGUMENT, "L + level_delta < 1 (SPEC.md L85)");
+    if (L > kMaxLevel3) fail(P2P_ERROR_NOT_SUPPORTED, "3D: L > 9 (8^(L-1) <= 2^24 boxes)");
+    hp.dim = 3;
+    hp.kernel = d.kernel;
+    hp.kappa = d.kernel == P2P_KERNEL_HELMHOLTZ_3D ? d.wavenumber : 0.0;
+    hp.layout = d.layout;
+    hp.precision = d.precision;
+    hp.device = d.device;
+    hp.eps = d.epsilon;
+    hp.n_src = d.n_src;
+    hp.n_tgt = d.n_tgt;
+    hp.L = L;
+    hp.S = int64_t(1) << (L - 1);
+    hp.B = hp.S * hp.S * hp.S;
+    hp.h = 1.0 / (double)hp.S;
+    const int64_t S = hp.S, B = hp.B;
+    auto sort3 = [&](const double *xyz, int64_t n, std::vector<int32_t> &off, std::vector<int32_t> &perm) {
+        std::vector<uint32_t> code((size_t)n);
+        parallel_for(n, [&](int64_t a, int64_t b) {
+            for (int64_t i = a; i < b; ++i)
+                code[i] = morton3(cell_of(xyz[3 * i], S), cell_of(xyz[3 * i + 1], S), cell_of(xyz[3 * i + 2], S));
+        });
+        off.assign((size_t)B + 1, 0);
+        for (int64_t i = 0; i < n; ++i) off[code[i] + 1] += 1;
+        for (int64_t b = 0; b < B; ++b) off[b + 1] += off[b];
+        std::vector<int32_t> pos(off.begin(), off.end() - 1);
+        perm.resize((size_t)n);
+        for (int64_t i = 0; i < n; ++i) perm[pos[code[i]]++] = (int32_t)i;
+    };
+    sort3(d.src_xy, d.n_src, hp.src_off_g, hp.src_perm_g);
+    sort3(d.tgt_xy, d.n_tgt, hp.tgt_off_g, hp.tgt_perm_g);
+    const int32_t *so = hp.src_off_g.data(), *to = hp.tgt_off_g.data();
+    // occupied target boxes, their E1 source counts and pairs
+    std::vector<int32_t> boxes;
+    std::vector<int64_t> bpairs;
+    int64_t max27 = 0;
+    for (int64_t b = 0; b < B; ++b) {
+        const int64_t a = so[b + 1] - so[b], t = to[b + 1] - to[b];
+        hp.occ_src += a > 0;
+        hp.occ_tgt += t > 0;
+        hp.t_max = std::max(hp.t_max, std::max(a, t));
+        if (!t) continue;
+        uint32_t ix = 0, iy = 0, iz = 0;
+        for (int bit = 0; bit < 10; ++bit) {
+            ix |= ((uint32_t)(b >> (3 * bit)) & 1u) << bit;
+            iy |= ((uint32_t)(b >> (3 * bit + 1)) & 1u) << bit;
+            iz |= ((uint32_t)(b >> (3 * bit + 2)) & 1u) << bit;
+        }
+        int64_t c = 0;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int64_t x = (int64_t)ix + dx, y = (int64_t)iy + dy, z = (int64_t)iz + dz;
+                    if (x < 0 || y < 0 || z < 0 || x >= S || y >= S || z >= S) continue;
+                    const uint32_t m = morton3((uint32_t)x, (uint32_t)y, (uint32_t)z);
+                    c += so[m + 1] - so[m];
+                }
+        boxes.push_back((int32_t)b);
+        bpairs.push_back(t * c);
+        max27 = std::max(max27, c);
+        hp.pairs += t * c;
+        hp.tgt_cap = std::max(hp.tgt_cap, t);
+    }
+    hp.pairs_global = hp.pairs;
+    hp.density = (double)hp.n_tgt / (double)B;
+    hp.density_occ = hp.occ_tgt ? (double)hp.n_tgt / (double)hp.occ_tgt : 0.0;
+    // queue: boxes by decreasing pair count (stable), so the last wave holds the short boxes
+    std::vector<int64_t> ord(boxes.size());
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return bpairs[x] > bpairs[y]; });
+    hp.tiles.resize(boxes.size());
+    for (size_t i = 0; i < ord.size(); ++i) hp.tiles[i] = boxes[ord[i]];
+    hp.tile_slot.assign(hp.tiles.size(), 0);
+    std::iota(hp.tile_slot.begin(), hp.tile_slot.end(), 0);
+    hp.tile_part.assign(hp.tiles.size(), 1 << 16);
+    hp.n_interior = (int64_t)hp.tiles.size();
+    hp.k = 0;
+    hp.boxes_in_tiles = (int64_t)hp.tiles.size();
+    hp.src_cap = max27;
+    hp.nt = kBox3Threads;
+    const int e = d.precision == P2P_FP32 ? 4 : 8, comps = d.kernel == P2P_KERNEL_HELMHOLTZ_3D ? 2 : 1;
+    hp.smem_bytes = box3d_smem(hp.src_cap, e, comps, hp.nt);
+    if (hp.smem_bytes > kSmemLimit)
+        fail(P2P_ERROR_NOT_SUPPORTED, "3D: a box's 27 neighbours hold " + std::to_string(max27) +
+                                          " sources (> shared memory); use a deeper level");
+    // partition / local sets (one partition)
+    hp.part_tile = {0, (int64_t)hp.tiles.size()};
+    hp.part_src = {0, hp.n_src};
+    hp.part_tgt = {0, hp.n_tgt};
+    hp.src_off = hp.src_off_g;
+    hp.tgt_off = hp.tgt_off_g;
+    hp.n_src_local = hp.n_src_owned = hp.n_src;
+    hp.n_tgt_local = hp.n_tgt;
+    hp.src_gidx.resize((size_t)hp.n_src);
+    std::iota(hp.src_gidx.begin(), hp.src_gidx.end(), 0);
+    hp.src_uidx = hp.src_perm_g;
+    hp.tgt_uidx = hp.tgt_perm_g;
+    hp.recv_counts.assign(1, 0);
+    hp.send_counts.assign(1, 0);
+    // box-local coordinates in units of h: u = (x - ix h) S (exact in fp64), 4 per point
+    auto fill4 = [&](auto &vec, const double *xyz, const std::vector<int32_t> &perm) {
+        using V = typename std::decay_t<decltype(vec)>::value_type;
+        const int64_t n = (int64_t)perm.size();
+        vec.assign((size_t)(4 * n), (V)0);
+        parallel_for(n, [&](int64_t a, int64_t b) {
+            for (int64_t i = a; i < b; ++i)
+                for (int c = 0; c < 3; ++c) {
+                    const double x = xyz[3 * (int64_t)perm[i] + c];
+                    vec[4 * i + c] = (V)((x - (double)cell_of(x, S) * hp.h) * (double)S);
+                }
+        });
+    };
+    if (d.precision == P2P_FP32) {
+        fill4(hp.f32.src_uv, d.src_xy, hp.src_uidx);
+        fill4(hp.f32.tgt_uv, d.tgt_xy, hp.tgt_uidx);
+    } else {
+        fill4(hp.f64.src_uv, d.src_xy, hp.src_uidx);
+        fill4(hp.f64.tgt_uv, d.tgt_xy, hp.tgt_uidx);
+    }
+    hp.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 // Kernel options and shared-memory size of a plan at tile size k, from its tile statistics
@@ -282,6 +439,10 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     auto t0 = std::chrono::steady_clock::now();
     if (d.struct_size != sizeof(p2p_plan_desc)) fail(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
     check_kernel(d);
+    if (kernel_dim(d.kernel) == 3) {
+        build_host_plan_3d(d, hp);
+        return;
+    }
     if (d.layout < P2P_LAYOUT_NONREDUNDANT || d.layout > P2P_LAYOUT_PAPER_REPETITION)
         fail(P2P_ERROR_INVALID_ARGUMENT, "bad layout");
     const bool paper = d.layout == P2P_LAYOUT_PAPER_INDEXING || d.layout == P2P_LAYOUT_PAPER_REPETITION;
@@ -975,6 +1136,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
 }
 
 std::vector<int64_t> neighbors_export(const HostPlan &hp) {
+    if (hp.dim == 3) fail(P2P_ERROR_NOT_SUPPORTED, "neighbour export: 2D plans");
     std::vector<int64_t> nb((size_t)hp.B * 9, -1);
     for (int64_t b = 0; b < hp.B; ++b) {
         uint32_t ix, iy;

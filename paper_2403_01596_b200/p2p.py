@@ -30,6 +30,10 @@ P2P_ERROR_NO_DEVICE = 7
 
 P2P_KERNEL_LAPLACE_2D = 0
 P2P_KERNEL_HELMHOLTZ_2D = 1
+P2P_KERNEL_LAPLACE_3D = 2
+P2P_KERNEL_HELMHOLTZ_3D = 3
+KERNELS = {"laplace": P2P_KERNEL_LAPLACE_2D, "helmholtz": P2P_KERNEL_HELMHOLTZ_2D,
+           "laplace3d": P2P_KERNEL_LAPLACE_3D, "helmholtz3d": P2P_KERNEL_HELMHOLTZ_3D}
 P2P_LAYOUT_NONREDUNDANT = 0
 P2P_LAYOUT_REDUNDANT = 1
 P2P_LAYOUT_TILED = 2
@@ -230,7 +234,8 @@ class Plan:
     the tile ring only); "paper_i" / "paper_r": the paper's own Indexing / Repetition
     layouts and kernels (fp64); precision: "fp32" or "fp64".
     kernel: "laplace" (the paper's ln(1/r)) or "helmholtz" ((i/4) H0^(1)(kappa r) with
-    ``wavenumber`` = kappa; complex q / phi; TILED layout).
+    ``wavenumber`` = kappa; complex q / phi; TILED layout); "laplace3d" (1/(4 pi r)) or
+    "helmholtz3d" (e^{i kappa r}/(4 pi r)) on the octree leaf grid: points [n, 3], layout "nr".
     device: CUDA ordinal, or -1 for a host-only plan (build + export only).
     build: "host" (p2p_plan_create: the C++ builder on the CPU) or "device"
     (p2p_plan_create_device: the same plan built by GPU kernels; src_xy / tgt_xy may then
@@ -244,6 +249,7 @@ class Plan:
                  wavenumber: float = 0.0):
         if build not in ("host", "device"):
             raise ValueError("build must be 'host' or 'device'")
+        dim = 3 if kernel.endswith("3d") else 2
         d = p2p_plan_desc_init()
         if build == "device":
             import torch
@@ -251,14 +257,14 @@ class Plan:
             self._src = torch.as_tensor(src_xy, dtype=torch.float64, device=dev).contiguous()
             self._tgt = self._src if tgt_xy is None else \
                 torch.as_tensor(tgt_xy, dtype=torch.float64, device=dev).contiguous()
-            if self._src.dim() != 2 or self._src.shape[1] != 2 or self._tgt.dim() != 2 or self._tgt.shape[1] != 2:
-                raise ValueError("points must be [n, 2] arrays")
+            if self._src.dim() != 2 or self._src.shape[1] != dim or self._tgt.dim() != 2 or self._tgt.shape[1] != dim:
+                raise ValueError(f"points must be [n, {dim}] arrays")
             d.n_src, d.n_tgt = self._src.shape[0], self._tgt.shape[0]
         else:
             self._src = np.ascontiguousarray(src_xy, dtype=np.float64)
             self._tgt = self._src if tgt_xy is None else np.ascontiguousarray(tgt_xy, dtype=np.float64)
-            if self._src.ndim != 2 or self._src.shape[1] != 2 or self._tgt.ndim != 2 or self._tgt.shape[1] != 2:
-                raise ValueError("points must be [n, 2] arrays")
+            if self._src.ndim != 2 or self._src.shape[1] != dim or self._tgt.ndim != 2 or self._tgt.shape[1] != dim:
+                raise ValueError(f"points must be [n, {dim}] arrays")
             d.n_src, d.n_tgt = len(self._src), len(self._tgt)
             d.src_xy = self._src.ctypes.data
             d.tgt_xy = self._tgt.ctypes.data
@@ -269,7 +275,7 @@ class Plan:
         d.precision = {"fp32": P2P_FP32, "fp64": P2P_FP64}[precision]
         d.device, d.tile_log2, d.stream = device, tile_log2, stream or None
         d.part_world, d.part_rank = part_world, part_rank
-        d.kernel = {"laplace": P2P_KERNEL_LAPLACE_2D, "helmholtz": P2P_KERNEL_HELMHOLTZ_2D}[kernel]
+        d.kernel = KERNELS[kernel]
         d.wavenumber = wavenumber
         self.kernel = kernel
         self.layout, self.precision, self.device, self.build = layout, precision, device, build
@@ -291,13 +297,13 @@ class Plan:
     def torch_dtype(self):
         """Element type of q and phi: real, or complex for the Helmholtz kernel."""
         import torch
-        if self.kernel == "helmholtz":
+        if self.kernel.startswith("helmholtz"):
             return torch.complex64 if self.precision == "fp32" else torch.complex128
         return torch.float32 if self.precision == "fp32" else torch.float64
 
     @property
     def np_dtype(self):
-        if self.kernel == "helmholtz":
+        if self.kernel.startswith("helmholtz"):
             return np.complex64 if self.precision == "fp32" else np.complex128
         return np.float32 if self.precision == "fp32" else np.float64
 

@@ -95,6 +95,35 @@ class ContourConfig:
         return 1 << (self.level - 1)
 
 
+@dataclass(frozen=True)
+class CubeConfig:
+    """SURVEY.md §8(f) NEXT-3 (3D kernels): n points uniform in an s x s x s block of leaf boxes of
+    the octree leaf grid at level L (grid 2^(L-1) per side on the unit cube), embedded at the
+    origin -- the "4x4x4 uniform leaf boxes" reading of BASELINE.json's tiny config in 3D, and a
+    1e6-point volume at 16 points per box."""
+    name: str
+    s: int
+    level: int
+    n: int
+    seed: int = 20240303
+
+    @property
+    def side(self) -> int:
+        return 1 << (self.level - 1)
+
+    @property
+    def density(self) -> float:
+        return self.n / self.s ** 3
+
+
+def cube_points(cfg: CubeConfig, streams=(0, 1, 7), seed: int | None = None) -> np.ndarray:
+    """[n, 3] float64 points uniform in the box block of ``cfg``."""
+    seed = cfg.seed if seed is None else seed
+    idx = np.arange(cfg.n, dtype=np.uint64)
+    w = cfg.s / cfg.side
+    return np.stack([_below(w, uniform01(seed, st, idx) * w) for st in streams], axis=1)
+
+
 def contour_points(cfg: ContourConfig, seed: int | None = None, n: int | None = None) -> np.ndarray:
     """[n, 2] float64 points on the star curve of ``cfg`` (inside [0.045, 0.955]^2)."""
     seed = cfg.seed if seed is None else seed
@@ -127,6 +156,8 @@ CONFIGS: dict[str, PlateConfig | ContourConfig] = {
 # leaf box a quarter wavelength at ~7.7 samples per wavelength along the curve (~1.8 points per
 # occupied box).
 CONFIGS.update({c.name: c for c in [
+    CubeConfig("tiny3d", 4, 3, 1024, seed=1),
+    CubeConfig("cube3d_1e6", 40, 7, 1_024_000),
     ContourConfig("contour_2e5", 200_000, 13),
     ContourConfig("contour_1e5", 100_000, 15, seed=20240304),
 ]})
@@ -206,6 +237,8 @@ def make_problem(cfg: PlateConfig | str, kind: str = "iid", seed: int | None = N
         cfg = CONFIGS[cfg]
     seed = cfg.seed if seed is None else seed
     n = cfg.n if n is None else n
+    if isinstance(cfg, CubeConfig):  # 3D: targets streams (0, 1, 7), sources (2, 3, 8)
+        return cube_points(cfg, (2, 3, 8), seed), cube_points(cfg, (0, 1, 7), seed), weights(cfg.n, seed)
     if isinstance(cfg, ContourConfig):  # collocated boundary nodes (kind does not apply)
         src = contour_points(cfg, seed, n)
         return src, src.copy(), weights(n, seed)
