@@ -127,9 +127,9 @@ template <typename T>
 void finalize_plan(p2p_plan_s &P);
 
 template <typename T>
-const void *box3d_fn(bool helm) {
-    return helm ? (const void *)p2p::dev::p2p_box3d_kernel<T, true, p2p::kBox3Threads>
-                : (const void *)p2p::dev::p2p_box3d_kernel<T, false, p2p::kBox3Threads>;
+const void *box3d_fn(bool helm) {  // CTA sizes of p2p::box3d_threads
+    return helm ? (const void *)p2p::dev::p2p_box3d_kernel<T, true, 128>
+                : (const void *)p2p::dev::p2p_box3d_kernel<T, false, 64>;
 }
 
 template <typename T>
@@ -374,7 +374,7 @@ void launch_box3d(p2p_plan_s &P, const T *q, T *out, bool user, int accumulate, 
     a.kh = (T)(hp.kappa * hp.h);
     void *args[] = {&a};
     const int grid = (int)std::min<int64_t>(ntiles, P.occ_sms);
-    ck(cudaLaunchKernel(box3d_fn<T>(hp.kernel == P2P_KERNEL_HELMHOLTZ_3D), dim3(grid), dim3(p2p::kBox3Threads), args,
+    ck(cudaLaunchKernel(box3d_fn<T>(hp.kernel == P2P_KERNEL_HELMHOLTZ_3D), dim3(grid), dim3(hp.nt), args,
                         (size_t)hp.smem_bytes, s),
        "box3d launch");
 }

@@ -1229,9 +1229,7 @@ __device__ __forceinline__ void box3d_pairs(const T *__restrict__ P, const T *__
             T sn, cs;
             const T ph = kh * (r2 * rs);
             if constexpr (sizeof(T) == 4) {
-                const float n = rintf(ph * 0.15915494309189535f);  // to [-pi, pi]
-                const float x = fmaf(-n, 6.28318548202514648f, fmaf(-n, -1.7484556e-07f, ph));
-                __sincosf(x, &sn, &cs);
+                __sincosf(ph, &sn, &cs);  // |ph| <= 2 sqrt(3) kappa h: MUFU accuracy holds
             } else {
                 sincos(ph, &sn, &cs);
             }
@@ -1242,12 +1240,38 @@ __device__ __forceinline__ void box3d_pairs(const T *__restrict__ P, const T *__
     }
 }
 
+// fp32 Laplace, two targets per thread sharing each broadcast source load, f32x2 math:
+// 3 FADD2 + FMUL2 + 2 FFMA2 + 2 MUFU.RSQ + FFMA2 per two pairs.  No guard in the loop: a
+// coincident pair gives rsqrt(0) = inf and a non-finite sum, and that unit is recomputed with
+// the guard (R17).
+__device__ __forceinline__ float rsq_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void box3d_pairs2_f32(const float4 *__restrict__ P, int s0, int s1, float x0, float y0,
+                                                 float z0, float x1, float y1, float z1, float &a0, float &a1) {
+    const f2_t X = f2_pack(x0, x1), Y = f2_pack(y0, y1), Z = f2_pack(z0, z1);
+    f2_t acc = 0ull;
+#pragma unroll 4
+    for (int s = s0; s < s1; ++s) {
+        const float4 p = P[s];
+        const f2_t dx = f2_sub(X, f2_pack(p.x, p.x)), dy = f2_sub(Y, f2_pack(p.y, p.y)), dz = f2_sub(Z, f2_pack(p.z, p.z));
+        const f2_t r2 = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+        float u0, u1;
+        f2_unpack(r2, u0, u1);
+        acc = f2_fma(f2_pack(p.w, p.w), f2_pack(rsq_approx(u0), rsq_approx(u1)), acc);
+    }
+    f2_unpack(acc, a0, a1);
+}
+
 template <typename T, bool HELM, int NT>
 __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_box;
     constexpr int comps = HELM ? 2 : 1;
-    const B3Carve c = box3d_carve(a.src_cap, (int)sizeof(T), comps, NT);
+    // partial sums: 2 per thread for complex values and for the fp32 two-target units
+    const B3Carve c = box3d_carve(a.src_cap, (int)sizeof(T), comps, NT, (HELM || sizeof(T) == 4) ? 2 : 1);
     T *s_p = reinterpret_cast<T *>(smem + c.p);
     T *s_qi = reinterpret_cast<T *>(smem + c.qi);
     T *s_part = reinterpret_cast<T *>(smem + c.part);
@@ -1320,7 +1344,9 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
         }
         __syncthreads();
         const int t0 = a.tgt_off[b], nt = a.tgt_off[b + 1] - t0;
-        const int C = nt >= NT ? 1 : NT / nt;  // source chunks per target
+        constexpr bool PAIR = sizeof(T) == 4 && !HELM;  // two targets per thread (f32x2)
+        const int nu = PAIR ? (nt + 1) / 2 : nt;        // work units (odd box: the last unit's second slot idle)
+        const int C = nu >= NT ? 1 : NT / nu;           // source chunks per unit
         auto finish = [&](int t, T re, T im) {
             const int64_t o = a.out_idx ? a.out_idx[t0 + t] : t0 + t;
             re *= a.scale;
@@ -1336,18 +1362,43 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
                 a.out[o] = a.accumulate ? a.out[o] + re : re;
             }
         };
-        for (int it = tid; it < nt * C; it += NT) {
-            const int t = it % nt, ch = it / nt;
-            const T *tp = a.tgt_p4 + 4 * (int64_t)(t0 + t);
-            const T tx = tp[0], ty = tp[1], tz = tp[2];
-            T re = (T)0, im = (T)0;
-            box3d_pairs<T, HELM>(s_p, s_qi, (int)((int64_t)total * ch / C), (int)((int64_t)total * (ch + 1) / C), tx,
-                                 ty, tz, a.eps2, a.kh, re, im);
-            if (C == 1) {
-                finish(t, re, im);
+        for (int it = tid; it < nu * C; it += NT) {
+            const int u = it % nu, ch = it / nu;
+            const int c0 = (int)((int64_t)total * ch / C), c1 = (int)((int64_t)total * (ch + 1) / C);
+            if constexpr (PAIR) {
+                const int ta = 2 * u, tb = min(2 * u + 1, nt - 1);
+                const float *pa = reinterpret_cast<const float *>(a.tgt_p4) + 4 * (int64_t)(t0 + ta);
+                const float *pb = reinterpret_cast<const float *>(a.tgt_p4) + 4 * (int64_t)(t0 + tb);
+                float r0, r1, dummy;
+                box3d_pairs2_f32(reinterpret_cast<const float4 *>(s_p), c0, c1, pa[0], pa[1], pa[2], pb[0], pb[1],
+                                 pb[2], r0, r1);
+                if (!isfinite(r0)) {
+                    r0 = 0.f;
+                    box3d_pairs<float, false>(reinterpret_cast<const float *>(s_p), nullptr, c0, c1, pa[0], pa[1],
+                                              pa[2], (float)a.eps2, 0.f, r0, dummy);
+                }
+                if (!isfinite(r1)) {
+                    r1 = 0.f;
+                    box3d_pairs<float, false>(reinterpret_cast<const float *>(s_p), nullptr, c0, c1, pb[0], pb[1],
+                                              pb[2], (float)a.eps2, 0.f, r1, dummy);
+                }
+                if (C == 1) {
+                    finish(ta, (T)r0, (T)0);
+                    if (tb != ta) finish(tb, (T)r1, (T)0);
+                } else {
+                    s_part[2 * it] = (T)r0;
+                    s_part[2 * it + 1] = (T)r1;
+                }
             } else {
-                s_part[comps * it] = re;
-                if constexpr (HELM) s_part[comps * it + 1] = im;
+                const T *tp = a.tgt_p4 + 4 * (int64_t)(t0 + u);
+                T re = (T)0, im = (T)0;
+                box3d_pairs<T, HELM>(s_p, s_qi, c0, c1, tp[0], tp[1], tp[2], a.eps2, a.kh, re, im);
+                if (C == 1) {
+                    finish(u, re, im);
+                } else {
+                    s_part[comps * it] = re;
+                    if constexpr (HELM) s_part[comps * it + 1] = im;
+                }
             }
         }
         if (C > 1) {
@@ -1355,8 +1406,12 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
             for (int t = tid; t < nt; t += NT) {  // chunks summed in order
                 T re = (T)0, im = (T)0;
                 for (int ch = 0; ch < C; ++ch) {
-                    re += s_part[comps * (ch * nt + t)];
-                    if constexpr (HELM) im += s_part[comps * (ch * nt + t) + 1];
+                    if constexpr (PAIR) {
+                        re += s_part[2 * (ch * nu + t / 2) + (t & 1)];
+                    } else {
+                        re += s_part[comps * (ch * nu + t)];
+                        if constexpr (HELM) im += s_part[comps * (ch * nu + t) + 1];
+                    }
                 }
                 finish(t, re, im);
             }

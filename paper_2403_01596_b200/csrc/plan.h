@@ -135,27 +135,30 @@ struct Error : std::runtime_error {
 
 constexpr int kMaxLevel = 15;          // full-grid CSR offsets: 4^(L-1) <= 2^28 boxes
 constexpr int kMaxLevel3 = 9;          // 3D: 8^(L-1) <= 2^24 boxes
-constexpr int kBox3Threads = 128;      // 3D: threads per CTA (one target box per CTA)
+// 3D: threads per CTA (one target box per CTA): 64 for Laplace, 128 for Helmholtz (measured,
+// tools/gpu_ab16.sh)
+inline int box3d_threads(int kernel) { return kernel == P2P_KERNEL_HELMHOLTZ_3D ? 128 : 64; }
 P2P_HD inline int kernel_dim(int kernel) { return kernel >= P2P_KERNEL_LAPLACE_3D ? 3 : 2; }
 // 3D box kernel shared memory: staged sources (x, y, z, q_re) and q_im (complex), per-thread
 // partial sums (comps values), and per neighbour box its source start, prefix and shift code.
 struct B3Carve {
     int p, qi, part, nbs, pre, nbd, total;
 };
-P2P_HD inline B3Carve box3d_carve(int src_cap, int e, int comps, int nt) {
+// comps: values per weight (2: complex, staged q_im); parts: partial sums per thread
+P2P_HD inline B3Carve box3d_carve(int src_cap, int e, int comps, int nt, int parts) {
     B3Carve c;
     c.p = 0;
     c.qi = c.p + 4 * e * src_cap;
     c.part = align16(c.qi + (comps == 2 ? e * src_cap : 0));
-    c.nbs = align16(c.part + nt * comps * e);
+    c.nbs = align16(c.part + nt * parts * e);
     c.pre = c.nbs + 4 * 28;
     c.nbd = c.pre + 4 * 28;
     c.total = c.nbd + 4 * 28;
     return c;
 }
-inline int64_t box3d_smem(int64_t src_cap, int e, int comps, int nt) {
+inline int64_t box3d_smem(int64_t src_cap, int e, int comps, int nt, int parts) {
     if (src_cap > (1 << 20)) return int64_t(1) << 40;
-    return box3d_carve((int)src_cap, e, comps, nt).total;
+    return box3d_carve((int)src_cap, e, comps, nt, parts).total;
 }
 constexpr int kThreads = 256;          // CTA size of the P2P kernels
 constexpr int kMaxTileLog2 = 6;
