@@ -163,7 +163,10 @@ inline int64_t box3d_smem(int64_t src_cap, int e, int comps, int nt, int parts) 
 constexpr int kThreads = 256;          // CTA size of the P2P kernels
 constexpr int kMaxTileLog2 = 6;
 constexpr int64_t kSmemLimit = 200 * 1024;
-constexpr int64_t kSplitShare = 148 * 8;  // TILED: a tile above 1/1184 of the pairs is split (heavy tiles)
+#ifndef P2P_SPLIT_SHARE
+#define P2P_SPLIT_SHARE (148 * 8)
+#endif
+constexpr int64_t kSplitShare = P2P_SPLIT_SHARE;  // TILED: a tile above 1/1184 of the pairs is split (heavy tiles)
 constexpr int64_t kSplitMax = 32;         // at most 32 launch entries per tile
 // Launch entries of a tile with `tile_pairs` pairs: ceil(tile_pairs / share) (<= 32), at least `base`.
 P2P_HD inline int64_t split_parts(int64_t tile_pairs, int64_t share, int64_t base) {

@@ -206,7 +206,7 @@ def test_tail_split_bit_identical(prec, level, monkeypatch):
         monkeypatch.setenv("P2P_TAIL_PARTS", str(parts))
         with p2p.Plan(src, tgt, level=level, layout="tiled", precision=prec) as pl:
             launch = pl.export("launch").reshape(2, -1)
-            assert np.any((launch[1] >> 16) == parts)
+            assert np.any((launch[1] >> 16) >= parts)  # heavy tiles may split further
             assert np.array_equal(gpu_apply(pl, q), base)
             check(pl, src, tgt, q, level)
 
