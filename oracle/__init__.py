@@ -86,6 +86,10 @@ def lib():
         _lib.oracle_direct_3d.restype = i32
         _lib.oracle_bruteforce_3d.argtypes = [i64, P, P, i64, P, i32, f64, i32, f64, P, P]
         _lib.oracle_bruteforce_3d.restype = i32
+        _lib.oracle_adaptive_tree.argtypes = [i64, P, i64, P, i64, i64, P, i64]
+        _lib.oracle_adaptive_tree.restype = i64
+        _lib.oracle_adaptive_direct.argtypes = [i64, P, P, i64, P, i64, i64, f64, P, P]
+        _lib.oracle_adaptive_direct.restype = i32
     return _lib
 
 
@@ -257,4 +261,27 @@ def bruteforce_3d(src_xyz, q, tgt_xyz, level: int, kernel: str = "laplace", kapp
     pairs = C.c_int64(0)
     lib().oracle_bruteforce_3d(len(src), _ptr(src), _ptr(qa), len(tgt), _ptr(tgt), level, eps, int(helm),
                                kappa, _ptr(phi), C.byref(pairs))
+    return phi, pairs.value
+
+
+# ---- NEXT-4: CT-driven adaptive quadtree (oracle.c oracle_adaptive_*) ----
+def adaptive_tree(src_xy, tgt_xy, ct: int, l_max: int) -> np.ndarray:
+    """Leaves [(level, ix, iy)] in Morton (depth-first) order."""
+    s, t = _f64(src_xy), _f64(tgt_xy)
+    cap = 1 + 3 * (len(s) + len(t)) * l_max + 4
+    out = np.empty(3 * cap, dtype=np.int64)
+    n = lib().oracle_adaptive_tree(len(s), _ptr(s), len(t), _ptr(t), ct, l_max, _ptr(out), cap)
+    if n < 0:
+        raise MemoryError
+    return out[:3 * n].reshape(-1, 3)
+
+
+def adaptive_direct(src_xy, q, tgt_xy, ct: int, l_max: int, eps: float = 1e-12):
+    """phi over the U-lists (leaves touching the target's leaf) and the pair count (brute force)."""
+    s, t, qq = _f64(src_xy), _f64(tgt_xy), _f64(q)
+    phi = np.empty(len(t), dtype=np.float64)
+    pairs = C.c_int64(0)
+    if lib().oracle_adaptive_direct(len(s), _ptr(s), _ptr(qq), len(t), _ptr(t), ct, l_max, eps, _ptr(phi),
+                                    C.byref(pairs)):
+        raise MemoryError
     return phi, pairs.value

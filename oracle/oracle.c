@@ -551,3 +551,105 @@ int oracle_bruteforce_3d(int64_t ns, const double *src, const double *q, int64_t
     if (pairs_out) *pairs_out = pairs;
     return 0;
 }
+
+/* ---- NEXT-4: CT-driven adaptive quadtree (R25) -------------
+ * The tree construction of PAPER.md §3.1 L67-69 applied per box instead of globally: a box is
+ * split into its 4 children while it holds more than CT sources or more than CT targets and its
+ * level is below l_max; the leaves partition the unit square.  E1 generalises to the U-list: a
+ * target in leaf A interacts with every source in a leaf B whose closed square touches A's
+ * closed square (A itself included) -- on a uniform tree this is exactly the 3x3 block.
+ * Everything below is brute force: counts by scanning all points, touching by comparing
+ * closed intervals, the sum over all (t, s) pairs. */
+typedef struct { int64_t level, ix, iy; } leaf_t;
+
+static int in_box(double x, double y, int64_t L, int64_t ix, int64_t iy)
+{
+    int64_t S = grid_side((int)L);
+    return cell_of(x, S) == ix && cell_of(y, S) == iy;
+}
+
+static void split_box(int64_t L, int64_t ix, int64_t iy, int64_t ns, const double *src, int64_t nt,
+                      const double *tgt, int64_t ct, int64_t lmax, leaf_t *out, int64_t *n_out)
+{
+    int64_t a = 0, b = 0;
+    for (int64_t s = 0; s < ns; ++s) a += in_box(src[2 * s], src[2 * s + 1], L, ix, iy);
+    for (int64_t t = 0; t < nt; ++t) b += in_box(tgt[2 * t], tgt[2 * t + 1], L, ix, iy);
+    if ((a > ct || b > ct) && L < lmax) {
+        for (int c = 0; c < 4; ++c) /* children in Morton order: x bit first */
+            split_box(L + 1, 2 * ix + (c & 1), 2 * iy + (c >> 1), ns, src, nt, tgt, ct, lmax, out, n_out);
+        return;
+    }
+    out[*n_out].level = L;
+    out[*n_out].ix = ix;
+    out[*n_out].iy = iy;
+    *n_out += 1;
+}
+
+/* Leaves of the tree in Morton (depth-first) order: leaves_out[3*i..] = (level, ix, iy); returns
+ * the number of leaves (capacity cap; -1 if exceeded). */
+int64_t oracle_adaptive_tree(int64_t ns, const double *src, int64_t nt, const double *tgt, int64_t ct,
+                             int64_t lmax, int64_t *leaves_out, int64_t cap)
+{
+    int64_t bound = 1 + 3 * (ns + nt) * lmax + 4; /* leaves <= 1 + 3 * (internal nodes) */
+    leaf_t *lv = (leaf_t *)malloc((size_t)bound * sizeof(leaf_t));
+    if (!lv) return -1;
+    int64_t n = 0;
+    split_box(1, 0, 0, ns, src, nt, tgt, ct, lmax, lv, &n);
+    if (n > cap) { free(lv); return -1; }
+    for (int64_t i = 0; i < n; ++i) {
+        leaves_out[3 * i] = lv[i].level;
+        leaves_out[3 * i + 1] = lv[i].ix;
+        leaves_out[3 * i + 2] = lv[i].iy;
+    }
+    free(lv);
+    return n;
+}
+
+/* closed squares of two leaves touch (in units of the level-lmax grid) */
+static int leaves_touch(const int64_t *A, const int64_t *B, int64_t lmax)
+{
+    int64_t sa = (int64_t)1 << (lmax - A[0]), sb = (int64_t)1 << (lmax - B[0]);
+    int64_t ax0 = A[1] * sa, ax1 = ax0 + sa, ay0 = A[2] * sa, ay1 = ay0 + sa;
+    int64_t bx0 = B[1] * sb, bx1 = bx0 + sb, by0 = B[2] * sb, by1 = by0 + sb;
+    return ax0 <= bx1 && bx0 <= ax1 && ay0 <= by1 && by0 <= ay1;
+}
+
+static int64_t leaf_of(double x, double y, const int64_t *leaves, int64_t nl)
+{
+    for (int64_t i = 0; i < nl; ++i)
+        if (in_box(x, y, leaves[3 * i], leaves[3 * i + 1], leaves[3 * i + 2])) return i;
+    return -1;
+}
+
+/* phi_t = sum over sources in leaves touching t's leaf (r >= eps) of -1/2 q ln r^2. */
+int oracle_adaptive_direct(int64_t ns, const double *src, const double *q, int64_t nt, const double *tgt,
+                           int64_t ct, int64_t lmax, double eps, double *phi_out, int64_t *pairs_out)
+{
+    int64_t cap = 1 + 3 * (ns + nt) * lmax + 4;
+    int64_t *leaves = (int64_t *)malloc((size_t)(3 * cap) * sizeof(int64_t));
+    int64_t *ls = (int64_t *)malloc((size_t)(ns > 0 ? ns : 1) * sizeof(int64_t));
+    if (!leaves || !ls) { free(leaves); free(ls); return -1; }
+    int64_t nl = oracle_adaptive_tree(ns, src, nt, tgt, ct, lmax, leaves, cap);
+    if (nl < 0) { free(leaves); free(ls); return -1; }
+    for (int64_t s = 0; s < ns; ++s) ls[s] = leaf_of(src[2 * s], src[2 * s + 1], leaves, nl);
+    double eps2 = eps * eps;
+    int64_t pairs = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : pairs)
+    for (int64_t t = 0; t < nt; ++t) {
+        int64_t lt = leaf_of(tgt[2 * t], tgt[2 * t + 1], leaves, nl);
+        double acc = 0.0;
+        for (int64_t s = 0; s < ns; ++s) {
+            if (!leaves_touch(&leaves[3 * lt], &leaves[3 * ls[s]], lmax)) continue;
+            pairs += 1;
+            double ddx = tgt[2 * t] - src[2 * s], ddy = tgt[2 * t + 1] - src[2 * s + 1];
+            double r2 = ddx * ddx + ddy * ddy;
+            if (r2 < eps2) continue;
+            acc += q[s] * log(r2);
+        }
+        phi_out[t] = -0.5 * acc;
+    }
+    free(leaves);
+    free(ls);
+    if (pairs_out) *pairs_out = pairs;
+    return 0;
+}
