@@ -105,7 +105,13 @@ typedef enum {
      *     occupancy); one GPU thread per target; each apply first writes q into the records
      *     (the paper's per-execution collection of potentials).  Eq. 8 bytes (with C = ct). */
     P2P_LAYOUT_PAPER_INDEXING = 3,
-    P2P_LAYOUT_PAPER_REPETITION = 4
+    P2P_LAYOUT_PAPER_REPETITION = 4,
+    /* a CT-driven ADAPTIVE quadtree -- a box is split while
+     * it holds more than desc.ct sources or targets and its level is below desc.l_max (desc.level
+     * is ignored); E1 becomes the U-list: the leaves whose closed squares touch the target's leaf
+     * (the 3x3 block on a uniform tree).  One CTA per target leaf stages its U-list's sources.
+     * LAPLACE_2D, one partition, host plan build. */
+    P2P_LAYOUT_ADAPTIVE = 5
 } p2p_layout;
 
 /* fp64 is paper-faithful ("stored as Double"); fp32 uses
@@ -303,8 +309,11 @@ typedef enum {
                                        part | nparts << 16 */
     P2P_EXPORT_PAPER_NEI_OFFSETS = 21, /* int64[boxes+1]: PAPER_INDEXING, offsets into the E1 source lists */
     P2P_EXPORT_PAPER_NEI_INDEX = 22,   /* int64[entries]: PAPER_INDEXING, original index of each E1 source */
-    P2P_EXPORT_PAPER_RECORDS = 23      /* int64[n_tgt*stride]: PAPER_REPETITION, the raw 8-byte record words
+    P2P_EXPORT_PAPER_RECORDS = 23,     /* int64[n_tgt*stride]: PAPER_REPETITION, the raw 8-byte record words
                                           (bit patterns of the doubles; q slots as of the last apply) */
+    P2P_EXPORT_LEAVES = 24,            /* int64[3*leaves]: ADAPTIVE, (level, ix, iy) per leaf, Morton order */
+    P2P_EXPORT_ULIST_OFFSETS = 25,     /* int64[leaves+1]: ADAPTIVE, U-list offsets per leaf (Morton order) */
+    P2P_EXPORT_ULIST = 26              /* int64[entries]: ADAPTIVE, U-list leaf indices (ascending) */
 } p2p_export_kind;
 
 /* Copy a plan array to host memory.  If host_dst is NULL, *bytes receives the

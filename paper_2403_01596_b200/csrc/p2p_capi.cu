@@ -50,6 +50,7 @@ struct p2p_plan_s {
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
     DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uidx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, log_tab, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
+    DevBuf leaf_rng, leaf_org, ul_off, ul_leaf, src_cell, tgt_cell;  // ADAPTIVE (NEXT-4)
     int grid = 0;                                // persistent CTAs per launch
     int64_t occ_sms = 1;                         // resident CTAs per SM x SMs (grid cap of a launch)
     unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
@@ -77,7 +78,8 @@ struct p2p_plan_s {
         DevBuf *all[] = {&pi_src_xy, &pi_tgt_xy, &pi_nei_off, &pi_nei_idx, &pr_records, &pr_slot, &phi_user, &halo_lidx, &tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
                          &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uidx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
-                         &tgt_pack_off, &tile_tgt_base, &q_local, &phi,
+                         &tgt_pack_off, &tile_tgt_base, &q_local, &phi, &leaf_rng, &leaf_org, &ul_off, &ul_leaf,
+                         &src_cell, &tgt_cell,
                          &io_q, &io_out, &queue};
         for (DevBuf *b : all) {
             if (b->p) cudaFree(b->p);
@@ -166,6 +168,25 @@ void upload_plan(p2p_plan_s &P) {
     } else if (hp.layout == P2P_LAYOUT_PAPER_REPETITION) {
         P.upload(P.pr_records, hp.pr_records);
         P.upload(P.pr_slot, hp.pr_slot);
+    } else if (hp.layout == P2P_LAYOUT_ADAPTIVE) {
+        const size_t nl = hp.leaf_lvl.size();
+        std::vector<int32_t> rng(4 * nl), org(2 * nl);
+        for (size_t i = 0; i < nl; ++i) {
+            rng[4 * i] = hp.leaf_s0[i];
+            rng[4 * i + 1] = hp.leaf_s1[i];
+            rng[4 * i + 2] = hp.leaf_t0[i];
+            rng[4 * i + 3] = hp.leaf_t1[i];
+            const int sz = 1 << (hp.L - hp.leaf_lvl[i]);
+            org[2 * i] = hp.leaf_ix[i] * sz;
+            org[2 * i + 1] = hp.leaf_iy[i] * sz;
+        }
+        P.upload(P.leaf_rng, rng);
+        P.upload(P.leaf_org, org);
+        P.upload(P.ul_off, hp.ul_off);
+        P.upload(P.ul_leaf, hp.ul_leaf);
+        P.upload(P.src_cell, hp.pt_cell_s);
+        P.upload(P.tgt_cell, hp.pt_cell_t);
+        P.upload(P.src_uv, lay.src_uv);
     } else if (hp.layout == P2P_LAYOUT_NONREDUNDANT) {
         P.upload(P.src_off, hp.src_off);
         P.upload(P.src_uv, lay.src_uv);
@@ -200,7 +221,8 @@ void finalize_plan(p2p_plan_s &P) {
     // Dynamic shared memory is fixed per plan: opt in once (a permission, not a
     // reservation, so one value serves all plans), then size the persistent grid.
     const bool two = hp.tpi == 2;
-    const void *kfn = hp.dim == 3 ? box3d_fn<T>(hp.kernel == P2P_KERNEL_HELMHOLTZ_3D)
+    const void *kfn = hp.layout == P2P_LAYOUT_ADAPTIVE ? (const void *)p2p::dev::p2p_adaptive_kernel<T, p2p::kAdaptiveThreads>
+                      : hp.dim == 3 ? box3d_fn<T>(hp.kernel == P2P_KERNEL_HELMHOLTZ_3D)
                       : hp.kernel == P2P_KERNEL_HELMHOLTZ_2D ? helm_fn<T>(hp.nt)
                       : hp.layout == P2P_LAYOUT_REDUNDANT ? (const void *)p2p::dev::p2p_r_kernel<T>
                       : hp.layout == P2P_LAYOUT_TILED
@@ -379,9 +401,46 @@ void launch_box3d(p2p_plan_s &P, const T *q, T *out, bool user, int accumulate, 
        "box3d launch");
 }
 
+// ADAPTIVE (NEXT-4): one CTA per target leaf over its U-list; user order fused.
+template <typename T>
+void launch_adaptive(p2p_plan_s &P, const T *q, T *out, bool user, int accumulate, cudaStream_t s) {
+    const p2p::HostPlan &hp = P.hp;
+    const int ntiles = (int)hp.tiles.size();
+    if (ntiles <= 0) return;
+    p2p::dev::P2PArgs<T> a{};
+    a.tiles = (const int32_t *)P.tiles.p;
+    a.ntiles = ntiles;
+    a.queue = (int *)P.queue.p;
+    a.src_cap = (int)hp.src_cap;
+    a.h = (T)hp.h;
+    a.eps2 = (T)(hp.eps * hp.eps);
+    a.leaf_rng = (const int4 *)P.leaf_rng.p;
+    a.leaf_org = (const int2 *)P.leaf_org.p;
+    a.ul_off = (const int32_t *)P.ul_off.p;
+    a.ul_leaf = (const int32_t *)P.ul_leaf.p;
+    a.src_cell = (const int2 *)P.src_cell.p;
+    a.tgt_cell = (const int2 *)P.tgt_cell.p;
+    a.src_uv = (const typename p2p::dev::V2<T>::type *)P.src_uv.p;
+    a.tgt_uv = (const typename p2p::dev::V2<T>::type *)P.tgt_uv.p;
+    a.src_idx = user ? (const int32_t *)P.src_uidx.p : nullptr;
+    a.out_idx = user ? (const int32_t *)P.tgt_uidx.p : nullptr;
+    a.q = q;
+    a.out = out;
+    a.accumulate = accumulate;
+    void *args[] = {&a};
+    const int grid = (int)std::min<int64_t>(ntiles, P.occ_sms);
+    ck(cudaLaunchKernel((const void *)p2p::dev::p2p_adaptive_kernel<T, p2p::kAdaptiveThreads>, dim3(grid),
+                        dim3(p2p::kAdaptiveThreads), args, (size_t)hp.smem_bytes, s),
+       "adaptive launch");
+}
+
 template <typename T>
 void apply_impl(p2p_plan_s &P, const void *d_q, void *d_out, int order, int accumulate, cudaStream_t s) {
     const p2p::HostPlan &hp = P.hp;
+    if (hp.layout == P2P_LAYOUT_ADAPTIVE) {
+        launch_adaptive<T>(P, (const T *)d_q, (T *)d_out, order == P2P_ORDER_USER, accumulate, s);
+        return;
+    }
     if (hp.dim == 3) {
         launch_box3d<T>(P, (const T *)d_q, (T *)d_out, order == P2P_ORDER_USER, accumulate, s);
         return;
@@ -1226,6 +1285,15 @@ p2p_status p2p_plan_export(p2p_plan P, int32_t kind, void *host_dst, size_t *byt
             std::memcpy(v.data(), rec.data(), rec.size() * 8);
             break;
         }
+        case P2P_EXPORT_LEAVES:
+            for (size_t i = 0; i < hp.leaf_lvl.size(); ++i) {
+                v.push_back(hp.leaf_lvl[i]);
+                v.push_back(hp.leaf_ix[i]);
+                v.push_back(hp.leaf_iy[i]);
+            }
+            break;
+        case P2P_EXPORT_ULIST_OFFSETS: take(hp.ul_off); break;
+        case P2P_EXPORT_ULIST: take(hp.ul_leaf); break;
         case P2P_EXPORT_LAUNCH:
             take(hp.tile_slot);
             v.insert(v.end(), hp.tile_part.begin(), hp.tile_part.end());

@@ -312,6 +312,11 @@ struct P2PArgs {
     const int32_t *src_idx;     // ORDER_USER: user index of each plan-order source (weights gathered through it)
     T scale;                    // 1 / (4 pi h)
     T kh;                       // kappa h (HELMHOLTZ_3D)
+    // ADAPTIVE (NEXT-4)
+    const int4 *leaf_rng;       // per leaf: source range, target range (plan order)
+    const int2 *leaf_org;       // per leaf: origin in finest-grid cells
+    const int32_t *ul_off, *ul_leaf;  // U-lists (CSR over leaves)
+    const int2 *src_cell, *tgt_cell;  // per point: finest cell (plan order); src_uv / tgt_uv: offsets in the cell
 };
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -1414,6 +1419,100 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
                     }
                 }
                 finish(t, re, im);
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) queue_exit(a.queue);
+}
+
+// ---------------------------------------------------------------- ADAPTIVE kernel (NEXT-4)
+// CT-driven quadtree (include/p2p.h P2P_LAYOUT_ADAPTIVE; R25).  Persistent CTAs pull
+// target leaves (most pairs first); per leaf the sources of its U-list leaves are staged into
+// shared memory as (x, y, q) relative to the target leaf's origin -- exact integer cell offsets
+// times the finest cell size plus the in-cell offset, rounded once -- and the leaf's targets
+// (<= CT) sweep them, C = NT / n_t source chunks per target with a fixed-order reduction.
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) p2p_adaptive_kernel(const P2PArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_leaf;
+    const int sbytes = ((a.src_cap * 4 * (int)sizeof(T)) + 15) & ~15;
+    T *s_p = reinterpret_cast<T *>(smem);
+    int *s_st = reinterpret_cast<int *>(smem + sbytes);
+    int *s_pre = s_st + kMaxUlist;
+    T *s_part = reinterpret_cast<T *>(smem + sbytes + 8 * kMaxUlist + 16);  // 16-B aligned
+    const int tid = threadIdx.x;
+    using C2 = typename V2<T>::type;
+    const C2 *suv = reinterpret_cast<const C2 *>(a.src_uv), *tuv = reinterpret_cast<const C2 *>(a.tgt_uv);
+    const T hf = a.h;
+    for (;;) {
+        if (tid == 0) {
+            const int e = atomicAdd(a.queue, 1);
+            s_leaf = e < a.ntiles ? a.tiles[e] : -1;
+        }
+        __syncthreads();
+        const int b = s_leaf;
+        if (b < 0) break;
+        const int u0 = a.ul_off[b], nu = a.ul_off[b + 1] - u0;
+        const int2 org = a.leaf_org[b];
+        if (tid == 0) {  // U-list source starts and prefix (a U-list holds ~9-20 leaves)
+            int run = 0;
+            for (int k = 0; k < nu; ++k) {
+                const int4 r = a.leaf_rng[a.ul_leaf[u0 + k]];
+                s_st[k] = r.x;
+                s_pre[k] = run;
+                run += r.y - r.x;
+            }
+            s_pre[nu] = run;
+        }
+        __syncthreads();
+        const int total = s_pre[nu];
+        for (int i = tid; i < total; i += NT) {  // stage (x, y, q) relative to the leaf origin
+            int k = 0;
+#pragma unroll
+            for (int step = 128; step; step >>= 1)
+                if (k + step < nu && s_pre[k + step] <= i) k += step;
+            const int j = s_st[k] + (i - s_pre[k]);
+            const int2 cl = a.src_cell[j];
+            const C2 o = suv[j];
+            const T x = fma((T)(cl.x - org.x), hf, o.x), y = fma((T)(cl.y - org.y), hf, o.y);
+            const T q = a.q[a.src_idx ? a.src_idx[j] : j];
+            s_p[4 * i] = x;
+            s_p[4 * i + 1] = y;
+            s_p[4 * i + 2] = q;
+        }
+        __syncthreads();
+        const int4 tr = a.leaf_rng[b];
+        const int t0 = tr.z, nt = tr.w - tr.z;
+        const int C = nt >= NT ? 1 : NT / nt;
+        auto finish = [&](int t, T acc) {
+            const int64_t o = a.out_idx ? a.out_idx[t0 + t] : t0 + t;
+            const T v = sizeof(T) == 4 ? (T)(-0.5f * kLn2) * acc : (T)-0.5 * acc;
+            a.out[o] = a.accumulate ? a.out[o] + v : v;
+        };
+        for (int it = tid; it < nt * C; it += NT) {
+            const int t = it % nt, ch = it / nt;
+            const int2 cl = a.tgt_cell[t0 + t];
+            const C2 o = tuv[t0 + t];
+            const T tx = fma((T)(cl.x - org.x), hf, o.x), ty = fma((T)(cl.y - org.y), hf, o.y);
+            const int s0 = (int)((int64_t)total * ch / C), s1 = (int)((int64_t)total * (ch + 1) / C);
+            T acc = (T)0;
+            for (int s = s0; s < s1; ++s) {
+                const T dx = tx - s_p[4 * s], dy = ty - s_p[4 * s + 1];
+                const T r2 = fma(dy, dy, dx * dx);
+                if (r2 < a.eps2) continue;  // coincident points contribute 0 (R3)
+                if constexpr (sizeof(T) == 4) acc = fmaf(s_p[4 * s + 2], lg2_approx(r2), acc);
+                else acc = fma(s_p[4 * s + 2], log(r2), acc);
+            }
+            if (C == 1) finish(t, acc);
+            else s_part[it] = acc;
+        }
+        if (C > 1) {
+            __syncthreads();
+            for (int t = tid; t < nt; t += NT) {
+                T acc = (T)0;
+                for (int ch = 0; ch < C; ++ch) acc += s_part[ch * nt + t];
+                finish(t, acc);
             }
         }
         __syncthreads();

@@ -276,6 +276,11 @@ struct HostPlan {
     std::vector<double> pr_records;               // n_tgt x pr_stride doubles, caller's target order
     std::vector<int32_t> pr_slot;                 // n_tgt x pr_maxn: original source index per triple, -1 = none
     int64_t pr_stride = 0, pr_maxn = 0, paper_model_bytes = 0;
+    // ---- ADAPTIVE (NEXT-4): leaves in Morton order, U-lists over leaves (CSR)
+    std::vector<int32_t> leaf_lvl, leaf_ix, leaf_iy;   // per leaf
+    std::vector<int32_t> leaf_s0, leaf_s1, leaf_t0, leaf_t1;  // source / target ranges (plan order)
+    std::vector<int32_t> ul_off, ul_leaf;              // [leaves+1], U-list leaf indices (ascending)
+    std::vector<int32_t> pt_cell_s, pt_cell_t;         // per point: finest-grid cell (x, y) pairs
     std::vector<int32_t> tile_slot;               // launch order -> slot
     std::vector<int32_t> tile_part;               // launch order -> part | nparts << 16 (tail splitting)
     int64_t reg_entries = 0;
@@ -311,6 +316,14 @@ void check_kernel(const p2p_plan_desc &d);  // kernel function + envelope (throw
 
 void build_host_plan(const p2p_plan_desc &desc, HostPlan &hp);
 void build_host_plan_3d(const p2p_plan_desc &desc, HostPlan &hp);
+void build_host_plan_adaptive(const p2p_plan_desc &desc, HostPlan &hp);
+// ADAPTIVE kernel shared memory: staged sources (x, y, q) relative to the target leaf, the
+// U-list source starts and prefix (up to kMaxUlist leaves), partial sums per thread.
+constexpr int kMaxUlist = 256;
+constexpr int kAdaptiveThreads = 64;
+inline int64_t adaptive_smem(int64_t src_cap, int e) {
+    return ((src_cap * 4 * e + 15) & ~int64_t(15)) + 8 * kMaxUlist + 16 + kAdaptiveThreads * e + 16;
+}
 void build_log_table(HostPlan &hp);
 std::vector<int64_t> neighbors_export(const HostPlan &hp);
 

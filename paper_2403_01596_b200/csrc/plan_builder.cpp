@@ -200,6 +200,210 @@ void check_kernel(const p2p_plan_desc &d) {
     if (d.part_world != 1) fail(P2P_ERROR_NOT_SUPPORTED, "kernels other than LAPLACE_2D: one partition");
 }
 
+// ---- ADAPTIVE: the CT-driven quadtree, per box (§3.1
+// applied locally), and U-lists of touching leaves.
+void build_host_plan_adaptive(const p2p_plan_desc &d, HostPlan &hp) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (d.kernel != P2P_KERNEL_LAPLACE_2D) fail(P2P_ERROR_NOT_SUPPORTED, "ADAPTIVE: LAPLACE_2D");
+    if (d.precision != P2P_FP32 && d.precision != P2P_FP64) fail(P2P_ERROR_INVALID_ARGUMENT, "bad precision");
+    if (!(d.epsilon > 0.0) || !std::isfinite(d.epsilon)) fail(P2P_ERROR_INVALID_ARGUMENT, "epsilon must be > 0");
+    if (d.part_world != 1 || d.part_rank != 0) fail(P2P_ERROR_NOT_SUPPORTED, "ADAPTIVE: one partition");
+    if (d.ct < 1) fail(P2P_ERROR_INVALID_ARGUMENT, "ct must be >= 1");
+    validate_points(d.src_xy, d.n_src, "sources");
+    validate_points(d.tgt_xy, d.n_tgt, "targets");
+    if (d.n_src > INT32_MAX - 8 || d.n_tgt > INT32_MAX - 8) fail(P2P_ERROR_NOT_SUPPORTED, "more than 2^31 points per set");
+    const int lmax = std::min(d.l_max, kMaxLevel);
+    if (lmax < 1) fail(P2P_ERROR_INVALID_ARGUMENT, "l_max must be >= 1");
+    hp.layout = d.layout;
+    hp.precision = d.precision;
+    hp.device = d.device;
+    hp.eps = d.epsilon;
+    hp.kernel = d.kernel;
+    hp.n_src = d.n_src;
+    hp.n_tgt = d.n_tgt;
+    hp.L = lmax;
+    hp.S = int64_t(1) << (lmax - 1);
+    hp.h = 1.0 / (double)hp.S;
+    const int64_t Sf = hp.S;
+    // finest-grid codes, stable sort (plan order = Morton order of the finest cell, then index)
+    auto sortf = [&](const double *xy, int64_t n, std::vector<uint32_t> &codes, std::vector<int32_t> &perm,
+                     std::vector<int32_t> &cells) {
+        std::vector<uint32_t> c((size_t)n);
+        parallel_for(n, [&](int64_t a, int64_t b) {
+            for (int64_t i = a; i < b; ++i)
+                c[i] = morton_encode(cell_of(xy[2 * i], Sf), cell_of(xy[2 * i + 1], Sf));
+        });
+        perm.resize((size_t)n);
+        std::iota(perm.begin(), perm.end(), 0);
+        std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return c[x] < c[y]; });
+        codes.resize((size_t)n);
+        cells.resize((size_t)(2 * n));
+        for (int64_t i = 0; i < n; ++i) {
+            codes[i] = c[perm[i]];
+            cells[2 * i] = (int32_t)cell_of(xy[2 * (int64_t)perm[i]], Sf);
+            cells[2 * i + 1] = (int32_t)cell_of(xy[2 * (int64_t)perm[i] + 1], Sf);
+        }
+    };
+    std::vector<uint32_t> cs, ctg;
+    sortf(d.src_xy, d.n_src, cs, hp.src_perm_g, hp.pt_cell_s);
+    sortf(d.tgt_xy, d.n_tgt, ctg, hp.tgt_perm_g, hp.pt_cell_t);
+    auto range = [](const std::vector<uint32_t> &c, uint64_t lo, uint64_t hi) {  // [lo, hi) finest codes
+        const int64_t a = std::lower_bound(c.begin(), c.end(), (uint32_t)std::min<uint64_t>(lo, UINT32_MAX)) - c.begin();
+        const int64_t b = hi > UINT32_MAX ? (int64_t)c.size()
+                                          : std::lower_bound(c.begin(), c.end(), (uint32_t)hi) - c.begin();
+        return std::make_pair(a, b);
+    };
+    // depth-first split, children in Morton order
+    std::vector<std::pair<int32_t, uint32_t>> stack{{1, 0u}};  // (level, Morton code at that level)
+    while (!stack.empty()) {
+        const auto [L, P] = stack.back();
+        stack.pop_back();
+        const int sh = 2 * (lmax - L);
+        const uint64_t lo = (uint64_t)P << sh, hi = ((uint64_t)P + 1) << sh;
+        const auto rs = range(cs, lo, hi), rt = range(ctg, lo, hi);
+        if ((rs.second - rs.first > d.ct || rt.second - rt.first > d.ct) && L < lmax) {
+            for (int c = 3; c >= 0; --c) stack.push_back({L + 1, (P << 2) | (uint32_t)c});
+            continue;
+        }
+        uint32_t ix, iy;
+        morton_decode(P, ix, iy);
+        hp.leaf_lvl.push_back(L);
+        hp.leaf_ix.push_back((int32_t)ix);
+        hp.leaf_iy.push_back((int32_t)iy);
+        hp.leaf_s0.push_back((int32_t)rs.first);
+        hp.leaf_s1.push_back((int32_t)rs.second);
+        hp.leaf_t0.push_back((int32_t)rt.first);
+        hp.leaf_t1.push_back((int32_t)rt.second);
+    }
+    const int64_t nl = (int64_t)hp.leaf_lvl.size();
+    hp.B = nl;
+    std::vector<uint64_t> lstart((size_t)nl);  // first finest code of each leaf (ascending: Morton DFS)
+    for (int64_t i = 0; i < nl; ++i) {
+        const uint32_t P = morton_encode((uint32_t)hp.leaf_ix[i], (uint32_t)hp.leaf_iy[i]);
+        lstart[i] = (uint64_t)P << (2 * (lmax - hp.leaf_lvl[i]));
+    }
+    auto lookup = [&](int64_t cx, int64_t cy) -> int64_t {  // the leaf holding finest cell (cx, cy)
+        const uint64_t m = morton_encode((uint32_t)cx, (uint32_t)cy);
+        return (std::upper_bound(lstart.begin(), lstart.end(), m) - lstart.begin()) - 1;
+    };
+    // U-lists: the leaf itself + every leaf met walking just outside its four sides and corners
+    hp.ul_off.assign((size_t)nl + 1, 0);
+    std::vector<int64_t> lp((size_t)nl, 0);
+    int64_t max_src = 0, max_ul = 0;
+    std::vector<int32_t> u;
+    for (int64_t i = 0; i < nl; ++i) {
+        u.clear();
+        if (hp.leaf_t1[i] > hp.leaf_t0[i]) {
+            const int64_t sz = int64_t(1) << (lmax - hp.leaf_lvl[i]);
+            const int64_t x0 = hp.leaf_ix[i] * sz, y0 = hp.leaf_iy[i] * sz, x1 = x0 + sz, y1 = y0 + sz;
+            u.push_back((int32_t)i);
+            auto extent = [&](int64_t j, int64_t &ex0, int64_t &ex1, int64_t &ey0, int64_t &ey1) {
+                const int64_t s2 = int64_t(1) << (lmax - hp.leaf_lvl[j]);
+                ex0 = hp.leaf_ix[j] * s2;
+                ex1 = ex0 + s2;
+                ey0 = hp.leaf_iy[j] * s2;
+                ey1 = ey0 + s2;
+            };
+            for (int side = 0; side < 2; ++side) {  // rows below / above
+                const int64_t y = side ? y1 : y0 - 1;
+                if (y < 0 || y >= Sf) continue;
+                for (int64_t x = x0; x < x1;) {
+                    const int64_t j = lookup(x, y);
+                    u.push_back((int32_t)j);
+                    int64_t ex0, ex1, ey0, ey1;
+                    extent(j, ex0, ex1, ey0, ey1);
+                    x = ex1;
+                }
+            }
+            for (int side = 0; side < 2; ++side) {  // columns left / right
+                const int64_t x = side ? x1 : x0 - 1;
+                if (x < 0 || x >= Sf) continue;
+                for (int64_t y = y0; y < y1;) {
+                    const int64_t j = lookup(x, y);
+                    u.push_back((int32_t)j);
+                    int64_t ex0, ex1, ey0, ey1;
+                    extent(j, ex0, ex1, ey0, ey1);
+                    y = ey1;
+                }
+            }
+            const int64_t cx[2] = {x0 - 1, x1}, cy[2] = {y0 - 1, y1};
+            for (int a = 0; a < 2; ++a)
+                for (int b = 0; b < 2; ++b)
+                    if (cx[a] >= 0 && cx[a] < Sf && cy[b] >= 0 && cy[b] < Sf) u.push_back((int32_t)lookup(cx[a], cy[b]));
+            std::sort(u.begin(), u.end());
+            u.erase(std::unique(u.begin(), u.end()), u.end());
+        }
+        int64_t ns_u = 0;
+        for (int32_t j : u) ns_u += hp.leaf_s1[j] - hp.leaf_s0[j];
+        hp.ul_leaf.insert(hp.ul_leaf.end(), u.begin(), u.end());
+        hp.ul_off[i + 1] = (int32_t)hp.ul_leaf.size();
+        const int64_t ntl = hp.leaf_t1[i] - hp.leaf_t0[i];
+        lp[i] = ntl * ns_u;
+        hp.pairs += lp[i];
+        if (ntl) {
+            max_src = std::max(max_src, ns_u);
+            max_ul = std::max<int64_t>(max_ul, (int64_t)u.size());
+            hp.tgt_cap = std::max(hp.tgt_cap, ntl);
+            hp.occ_tgt += 1;
+        }
+        if (hp.leaf_s1[i] > hp.leaf_s0[i]) hp.occ_src += 1;
+        hp.t_max = std::max<int64_t>(hp.t_max, std::max<int64_t>(hp.leaf_s1[i] - hp.leaf_s0[i], ntl));
+    }
+    if (max_ul > kMaxUlist) fail(P2P_ERROR_NOT_SUPPORTED, "ADAPTIVE: a U-list exceeds 256 leaves");
+    hp.pairs_global = hp.pairs;
+    hp.density = (double)hp.n_tgt / (double)std::max<int64_t>(nl, 1);
+    hp.density_occ = hp.occ_tgt ? (double)hp.n_tgt / (double)hp.occ_tgt : 0.0;
+    // queue: target leaves by decreasing pairs (stable)
+    std::vector<int32_t> tl;
+    for (int64_t i = 0; i < nl; ++i)
+        if (hp.leaf_t1[i] > hp.leaf_t0[i]) tl.push_back((int32_t)i);
+    std::stable_sort(tl.begin(), tl.end(), [&](int32_t x, int32_t y) { return lp[x] > lp[y]; });
+    hp.tiles = tl;
+    hp.tile_slot.resize(tl.size());
+    std::iota(hp.tile_slot.begin(), hp.tile_slot.end(), 0);
+    hp.tile_part.assign(tl.size(), 1 << 16);
+    hp.n_interior = (int64_t)tl.size();
+    hp.boxes_in_tiles = (int64_t)tl.size();
+    hp.src_cap = max_src;
+    hp.nt = kAdaptiveThreads;
+    const int e = d.precision == P2P_FP32 ? 4 : 8;
+    hp.smem_bytes = adaptive_smem(hp.src_cap, e);
+    if (hp.smem_bytes > kSmemLimit)
+        fail(P2P_ERROR_NOT_SUPPORTED, "ADAPTIVE: a U-list holds " + std::to_string(max_src) +
+                                          " sources (> shared memory); lower ct");
+    // one partition, local = global
+    hp.part_tile = {0, (int64_t)tl.size()};
+    hp.part_src = {0, hp.n_src};
+    hp.part_tgt = {0, hp.n_tgt};
+    hp.n_src_local = hp.n_src_owned = hp.n_src;
+    hp.n_tgt_local = hp.n_tgt;
+    hp.src_gidx.resize((size_t)hp.n_src);
+    std::iota(hp.src_gidx.begin(), hp.src_gidx.end(), 0);
+    hp.src_uidx = hp.src_perm_g;
+    hp.tgt_uidx = hp.tgt_perm_g;
+    hp.recv_counts.assign(1, 0);
+    hp.send_counts.assign(1, 0);
+    // per point: offset within its finest cell (x - cx hf), plan order; cells in pt_cell_*
+    auto fillc = [&](auto &vec, const double *xy, const std::vector<int32_t> &perm) {
+        using V = typename std::decay_t<decltype(vec)>::value_type;
+        const int64_t n = (int64_t)perm.size();
+        vec.resize((size_t)(2 * n));
+        for (int64_t i = 0; i < n; ++i)
+            for (int c = 0; c < 2; ++c) {
+                const double x = xy[2 * (int64_t)perm[i] + c];
+                vec[2 * i + c] = (V)(x - (double)cell_of(x, Sf) * hp.h);
+            }
+    };
+    if (d.precision == P2P_FP32) {
+        fillc(hp.f32.src_uv, d.src_xy, hp.src_uidx);
+        fillc(hp.f32.tgt_uv, d.tgt_xy, hp.tgt_uidx);
+    } else {
+        fillc(hp.f64.src_uv, d.src_xy, hp.src_uidx);
+        fillc(hp.f64.tgt_uv, d.tgt_xy, hp.tgt_uidx);
+    }
+    hp.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 // ---- 3D: octree leaf grid, 3D Morton order (x bit 3i, y 3i+1, z 3i+2),
 // E1 = the 3x3x3 block clipped at the faces; one CTA per target box stages its <= 27 neighbour
 // boxes (p2p_box3d_kernel).
@@ -443,7 +647,11 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         build_host_plan_3d(d, hp);
         return;
     }
-    if (d.layout < P2P_LAYOUT_NONREDUNDANT || d.layout > P2P_LAYOUT_PAPER_REPETITION)
+    if (d.layout == P2P_LAYOUT_ADAPTIVE) {
+        build_host_plan_adaptive(d, hp);
+        return;
+    }
+    if (d.layout < P2P_LAYOUT_NONREDUNDANT || d.layout > P2P_LAYOUT_ADAPTIVE)
         fail(P2P_ERROR_INVALID_ARGUMENT, "bad layout");
     const bool paper = d.layout == P2P_LAYOUT_PAPER_INDEXING || d.layout == P2P_LAYOUT_PAPER_REPETITION;
     if (paper && d.precision != P2P_FP64)
@@ -1136,7 +1344,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
 }
 
 std::vector<int64_t> neighbors_export(const HostPlan &hp) {
-    if (hp.dim == 3) fail(P2P_ERROR_NOT_SUPPORTED, "neighbour export: 2D plans");
+    if (hp.dim == 3 || hp.layout == P2P_LAYOUT_ADAPTIVE) fail(P2P_ERROR_NOT_SUPPORTED, "neighbour export: uniform 2D plans");
     std::vector<int64_t> nb((size_t)hp.B * 9, -1);
     for (int64_t b = 0; b < hp.B; ++b) {
         uint32_t ix, iy;

@@ -39,6 +39,7 @@ P2P_LAYOUT_REDUNDANT = 1
 P2P_LAYOUT_TILED = 2
 P2P_LAYOUT_PAPER_INDEXING = 3
 P2P_LAYOUT_PAPER_REPETITION = 4
+P2P_LAYOUT_ADAPTIVE = 5
 P2P_FP64 = 0
 P2P_FP32 = 1
 P2P_ORDER_PLAN = 0
@@ -50,6 +51,7 @@ EXPORT = {
     "halo_index": 9, "send_index": 10, "halo_offsets": 11, "region_offsets": 12, "region_index": 13,
     "region_table": 14, "slot_offsets": 15, "slot_base": 16, "slot_output": 17, "item_offsets": 18,
     "items": 19, "launch": 20, "paper_nei_offsets": 21, "paper_nei_index": 22, "paper_records": 23,
+    "leaves": 24, "ulist_offsets": 25, "ulist": 26,
 }
 
 # Symbols declared in include/p2p.h (checked by tests/test_abi.py).
@@ -271,7 +273,8 @@ class Plan:
         d.level, d.ct, d.l_start, d.l_max, d.level_delta = level, ct, l_start, l_max, level_delta
         d.epsilon = epsilon
         d.layout = {"nr": P2P_LAYOUT_NONREDUNDANT, "r": P2P_LAYOUT_REDUNDANT, "tiled": P2P_LAYOUT_TILED,
-                    "paper_i": P2P_LAYOUT_PAPER_INDEXING, "paper_r": P2P_LAYOUT_PAPER_REPETITION}[layout]
+                    "paper_i": P2P_LAYOUT_PAPER_INDEXING, "paper_r": P2P_LAYOUT_PAPER_REPETITION,
+                    "adaptive": P2P_LAYOUT_ADAPTIVE}[layout]
         d.precision = {"fp32": P2P_FP32, "fp64": P2P_FP64}[precision]
         d.device, d.tile_log2, d.stream = device, tile_log2, stream or None
         d.part_world, d.part_rank = part_world, part_rank
