@@ -227,6 +227,27 @@ p2p_status p2p_apply_dist_interior(p2p_plan plan, const void *d_q_owned, void *d
 p2p_status p2p_apply_dist_boundary(p2p_plan plan, const void *d_q_halo, void *d_out, int32_t accumulate,
                                    void *stream);
 
+/* Distributed apply with the halo read straight from the owners' device memory (SURVEY.md
+ * §8(e): the peer-memory alternative to the NCCL exchange -- over NVLink / NVSwitch on a B200
+ * node these are P2P loads, no send buffer, no collective, one gather kernel):
+ *   d_peer_q: HOST array of part_world DEVICE pointers; d_peer_q[r] = rank r's owned weights
+ *             (its n_src_owned elements in plan order), mapped into this process with
+ *             p2p_ipc_open (or any peer-accessible pointer); d_peer_q[part_rank] is ignored
+ *             (d_q_owned is used).  Read during the call's stream work only.
+ *   The caller orders the peers: their buffers must hold this apply's weights before the
+ *   gather runs and must not change until it has finished (e.g. barriers around the apply).
+ * part_world <= 16.  Errors: INVALID_ARGUMENT (NULL pointers, part_world > 16), NO_DEVICE, CUDA. */
+p2p_status p2p_apply_dist_peer(p2p_plan plan, const void *d_q_owned, const void *const *d_peer_q, void *d_out,
+                               int32_t accumulate, void *stream);
+
+/* CUDA IPC for p2p_apply_dist_peer.  p2p_ipc_export: the 64-byte handle (host buffer) of the
+ * allocation holding d_ptr and d_ptr's byte offset in it (pointers from sub-allocating
+ * allocators, e.g. torch's, are fine).  p2p_ipc_open: map a peer's handle on `device` and
+ * return the mapping + offset; p2p_ipc_close releases it (pass the pointer p2p_ipc_open gave). */
+p2p_status p2p_ipc_export(const void *d_ptr, void *handle64, int64_t *offset);
+p2p_status p2p_ipc_open(const void *handle64, int64_t offset, int32_t device, void **d_ptr);
+p2p_status p2p_ipc_close(void *d_ptr, int64_t offset);
+
 /* Gather this partition's owned weights that the other partitions need into
  * d_send (device, n_send elements), grouped by destination rank ascending,
  * within a destination by global plan index ascending. */

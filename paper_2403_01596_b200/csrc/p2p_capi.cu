@@ -51,6 +51,7 @@ struct p2p_plan_s {
     DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uidx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, log_tab, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     DevBuf leaf_rng, leaf_org, ul_off, ul_leaf, src_cell, tgt_cell;  // ADAPTIVE (NEXT-4)
+    DevBuf halo_owner, halo_oidx;                // peer-memory halo: owner rank, owner-local index per halo slot
     int grid = 0;                                // persistent CTAs per launch
     int64_t occ_sms = 1;                         // resident CTAs per SM x SMs (grid cap of a launch)
     unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
@@ -79,7 +80,7 @@ struct p2p_plan_s {
                          &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
                          &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uidx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi, &leaf_rng, &leaf_org, &ul_off, &ul_leaf,
-                         &src_cell, &tgt_cell,
+                         &src_cell, &tgt_cell, &halo_owner, &halo_oidx,
                          &io_q, &io_out, &queue};
         for (DevBuf *b : all) {
             if (b->p) cudaFree(b->p);
@@ -159,6 +160,17 @@ void upload_plan(p2p_plan_s &P) {
         P.upload(P.src_gidx, hp.src_gidx);
         P.upload(P.halo_lidx, hp.halo_lidx);
         P.upload(P.send_idx, hp.send_idx);
+        // peer-memory halo: owner rank and owner-local index of each halo slot (the owner of a
+        // global plan index is the last rank whose source range starts at or before it)
+        std::vector<int32_t> own(hp.halo_lidx.size()), oix(hp.halo_lidx.size());
+        for (size_t h = 0; h < hp.halo_lidx.size(); ++h) {
+            const int64_t g = hp.src_gidx[hp.halo_lidx[h]];
+            const int r = (int)(std::upper_bound(hp.part_src.begin(), hp.part_src.end(), g) - hp.part_src.begin()) - 1;
+            own[h] = r;
+            oix[h] = (int32_t)(g - hp.part_src[r]);
+        }
+        P.upload(P.halo_owner, own);
+        P.upload(P.halo_oidx, oix);
     }
     if (hp.layout == P2P_LAYOUT_PAPER_INDEXING) {
         P.upload(P.pi_src_xy, hp.pi_src_xy);
@@ -1130,6 +1142,79 @@ p2p_status p2p_apply_dist_boundary(p2p_plan P, const void *d_q_halo, void *d_out
         if (P->elem == 4) apply_dist_boundary_impl<float>(*P, d_q_halo, d_out, accumulate ? 1 : 0, s);
         else apply_dist_boundary_impl<double>(*P, d_q_halo, d_out, accumulate ? 1 : 0, s);
     });
+}
+
+p2p_status p2p_apply_dist_peer(p2p_plan P, const void *d_q_owned, const void *const *d_peer_q, void *d_out,
+                               int32_t accumulate, void *stream) {
+    if (!P || !d_out || !d_peer_q) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan, output or peer array");
+    if (P->hp.n_src_owned && !d_q_owned) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_q_owned");
+    if (P->hp.part_world > 16) return set_error(P2P_ERROR_INVALID_ARGUMENT, "part_world > 16");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        const p2p::HostPlan &hp = P->hp;
+        if (P->comps != 1) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "distributed apply: real kernels only");
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            p2p::dev::PeerPtrs<T> pp{};
+            for (int r = 0; r < hp.part_world; ++r) {
+                pp.p[r] = r == hp.part_rank ? (const T *)d_q_owned : (const T *)d_peer_q[r];
+                if (!pp.p[r] && r != hp.part_rank) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "NULL peer pointer");
+            }
+            if (hp.n_src_owned)
+                ck(cudaMemcpyAsync((T *)P->q_local.p + hp.owned_local_begin, d_q_owned,
+                                   (size_t)hp.n_src_owned * sizeof(T), cudaMemcpyDeviceToDevice, s),
+                   "owned weights");
+            if (hp.n_halo)
+                p2p::dev::halo_peer_kernel<T><<<grid_for(hp.n_halo), 256, 0, s>>>(
+                    pp, (const int32_t *)P->halo_owner.p, (const int32_t *)P->halo_oidx.p,
+                    (const int32_t *)P->halo_lidx.p, (T *)P->q_local.p, hp.n_halo);
+            launch_p2p<T>(*P, (const T *)P->q_local.p, (T *)d_out, accumulate ? 1 : 0, s);
+            ck(cudaGetLastError(), "apply_dist_peer launch");
+        };
+        if (P->elem == 4) run(float{});
+        else run(double{});
+    });
+}
+
+p2p_status p2p_ipc_export(const void *d_ptr, void *handle64, int64_t *offset) {
+    if (!d_ptr || !handle64 || !offset) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL pointer");
+    return guarded([&] {
+        // base of the allocation holding d_ptr (driver cuMemGetAddressRange through the runtime)
+        typedef int (*range_fn)(unsigned long long *, size_t *, unsigned long long);
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        ck(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q), "driver entry point");
+        if (!fn || q != cudaDriverEntryPointSuccess) throw p2p::Error(P2P_ERROR_CUDA, "cuMemGetAddressRange unavailable");
+        unsigned long long base = 0;
+        size_t size = 0;
+        if (((range_fn)fn)(&base, &size, (unsigned long long)(uintptr_t)d_ptr) != 0)
+            throw p2p::Error(P2P_ERROR_CUDA, "cuMemGetAddressRange failed");
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base), "cudaIpcGetMemHandle");
+        static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+        std::memcpy(handle64, &h, sizeof(h));
+        *offset = (int64_t)((uintptr_t)d_ptr - base);
+    });
+}
+
+p2p_status p2p_ipc_open(const void *handle64, int64_t offset, int32_t device, void **d_ptr) {
+    if (!handle64 || !d_ptr) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL pointer");
+    *d_ptr = nullptr;
+    return guarded([&] {
+        DeviceGuard g(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, sizeof(h));
+        void *base = nullptr;
+        ck(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        *d_ptr = (char *)base + offset;
+    });
+}
+
+p2p_status p2p_ipc_close(void *d_ptr, int64_t offset) {
+    if (!d_ptr) return P2P_SUCCESS;
+    return guarded([&] { ck(cudaIpcCloseMemHandle((char *)d_ptr - offset), "cudaIpcCloseMemHandle"); });
 }
 
 p2p_status p2p_halo_pack(p2p_plan P, const void *d_q_owned, void *d_send, void *stream) {

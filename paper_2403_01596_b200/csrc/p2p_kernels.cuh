@@ -1587,6 +1587,19 @@ __global__ void pack_r_kernel(const int32_t *__restrict__ idx, const T *__restri
 }
 
 // dst[i] = src[idx[i]]  (ORDER_USER import / replicated-weight gather)
+// Peer-memory halo (p2p_apply_dist_peer): q_local[lidx[h]] = peer[owner[h]][oidx[h]], the
+// owners' buffers read directly (NVLink P2P loads on a multi-GPU node, CUDA IPC mappings).
+template <typename T>
+struct PeerPtrs {
+    const T *p[16];
+};
+template <typename T>
+__global__ void halo_peer_kernel(PeerPtrs<T> peers, const int32_t *__restrict__ owner, const int32_t *__restrict__ oidx,
+                                 const int32_t *__restrict__ lidx, T *__restrict__ q_local, int64_t n) {
+    for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < n; h += (int64_t)gridDim.x * blockDim.x)
+        q_local[lidx[h]] = peers.p[owner[h]][oidx[h]];
+}
+
 template <typename T>
 __global__ void gather_kernel(const int32_t *__restrict__ idx, const T *__restrict__ src, T *__restrict__ dst,
                               int64_t n) {

@@ -110,6 +110,42 @@ class DistributedP2P:
         ev = self.exchange_async(q_owned, comm_stream, after=cur)
         return self.apply(q_owned, out, accumulate=accumulate, stream=stream, halo_ready=ev)
 
+    # ---- peer-memory halo (SURVEY.md §8(e) alternative; p2p_apply_dist_peer): the halo weights
+    # are read straight from the owners' buffers -- NVLink P2P loads on a B200 node -- by one
+    # gather kernel, instead of pack + all_to_all + scatter.
+    def enable_peer(self):
+        """Allocate this rank's shared owned-weight buffer and map every peer's (CUDA IPC)."""
+        torch = self.torch
+        self._qpeer = torch.zeros(max(1, self.n_src_owned), dtype=self.plan.torch_dtype,
+                                  device=torch.device("cuda", self.device))
+        mine = p2p.p2p_ipc_export(self._qpeer.data_ptr())
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        self._peers = [(0, 0) if r == self.rank else (p2p.p2p_ipc_open(allh[r][0], allh[r][1], self.device), allh[r][1])
+                       for r in range(self.world)]
+
+    def apply_peer(self, q_owned, out=None, *, accumulate: bool = False, stream=None):
+        """phi for this rank's targets with the peer-memory halo.  Protocol: publish q_owned in
+        the shared buffer, barrier (every rank's weights are in place), gather + apply, barrier
+        (no rank overwrites its buffer while a peer may still read it)."""
+        torch = self.torch
+        if not hasattr(self, "_peers"):
+            self.enable_peer()
+        n = self.n_src_owned
+        if n:
+            self._qpeer[:n].copy_(q_owned[:n])
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier(group=self.group)
+        if out is None:
+            out = torch.empty(max(1, self.n_tgt_local), dtype=self.plan.torch_dtype,
+                              device=torch.device("cuda", self.device))
+        s = stream or torch.cuda.current_stream(self.device).cuda_stream
+        p2p.p2p_apply_dist_peer(self.plan.handle, self._qpeer.data_ptr() if n else 0, [p for p, _ in self._peers],
+                                out.data_ptr(), int(accumulate), s)
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier(group=self.group)
+        return out
+
     def gather(self, phi_local):
         """allgatherv (a11): every rank receives phi for all targets in global plan order."""
         torch = self.torch
@@ -126,4 +162,8 @@ class DistributedP2P:
         return torch.cat([p[: int(c)].to(phi_local.device) for p, c in zip(parts, counts)])
 
     def close(self):
+        for ptr, off in getattr(self, "_peers", []):
+            if ptr:
+                p2p.p2p_ipc_close(ptr, off)
+        self._peers = []
         self.plan.close()

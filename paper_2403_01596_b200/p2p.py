@@ -58,7 +58,7 @@ EXPORT = {
 ABI_SYMBOLS = (
     "p2p_plan_desc_init", "p2p_plan_create", "p2p_plan_create_device", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async",
     "p2p_apply_dist", "p2p_apply_dist_interior", "p2p_apply_dist_boundary",
-    "p2p_halo_pack", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
+    "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_ipc_export", "p2p_ipc_open", "p2p_ipc_close", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
     "p2p_status_string", "p2p_last_error", "p2p_abi_version",
 )
 
@@ -125,6 +125,10 @@ def load_library() -> C.CDLL:
     lib.p2p_apply_dist_interior.argtypes = [P, P, P, i32, P]
     lib.p2p_apply_dist_boundary.argtypes = [P, P, P, i32, P]
     lib.p2p_halo_pack.argtypes = [P, P, P, P]
+    lib.p2p_apply_dist_peer.argtypes = [P, P, C.POINTER(P), P, i32, P]
+    lib.p2p_ipc_export.argtypes = [P, P, C.POINTER(i64)]
+    lib.p2p_ipc_open.argtypes = [P, i64, i32, C.POINTER(P)]
+    lib.p2p_ipc_close.argtypes = [P, i64]
     lib.p2p_destroy.argtypes = [P]
     lib.p2p_plan_get_info.argtypes = [P, C.POINTER(PlanInfo)]
     lib.p2p_plan_export.argtypes = [P, i32, P, C.POINTER(C.c_size_t)]
@@ -133,7 +137,8 @@ def load_library() -> C.CDLL:
     lib.p2p_last_error.restype = C.c_char_p
     lib.p2p_abi_version.restype = i32
     for name in ("p2p_plan_create", "p2p_plan_create_device", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async", "p2p_apply_dist", "p2p_apply_dist_interior",
-                 "p2p_apply_dist_boundary", "p2p_halo_pack",
+                 "p2p_apply_dist_boundary", "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_ipc_export",
+                 "p2p_ipc_open", "p2p_ipc_close",
                  "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export"):
         getattr(lib, name).restype = i32
     _lib = lib
@@ -204,6 +209,30 @@ def p2p_apply_dist(plan, d_q_owned: int, d_q_halo: int, d_out: int, accumulate: 
 
 def p2p_halo_pack(plan, d_q_owned: int, d_send: int, stream: int = 0):
     _check(load_library().p2p_halo_pack(plan, d_q_owned or None, d_send or None, stream or None), "p2p_halo_pack")
+
+
+def p2p_apply_dist_peer(plan, d_q_owned: int, peer_ptrs, d_out: int, accumulate: int = 0, stream: int = 0):
+    arr = (C.c_void_p * len(peer_ptrs))(*[p or None for p in peer_ptrs])
+    _check(load_library().p2p_apply_dist_peer(plan, d_q_owned or None, arr, d_out, accumulate, stream or None),
+           "p2p_apply_dist_peer")
+
+
+def p2p_ipc_export(d_ptr: int) -> tuple[bytes, int]:
+    """(64-byte IPC handle of the allocation holding d_ptr, d_ptr's offset in it)."""
+    buf = C.create_string_buffer(64)
+    off = C.c_int64(0)
+    _check(load_library().p2p_ipc_export(d_ptr, buf, C.byref(off)), "p2p_ipc_export")
+    return buf.raw, off.value
+
+
+def p2p_ipc_open(handle: bytes, offset: int, device: int) -> int:
+    out = C.c_void_p()
+    _check(load_library().p2p_ipc_open(C.c_char_p(handle), offset, device, C.byref(out)), "p2p_ipc_open")
+    return out.value
+
+
+def p2p_ipc_close(d_ptr: int, offset: int):
+    _check(load_library().p2p_ipc_close(d_ptr or None, offset), "p2p_ipc_close")
 
 
 def p2p_destroy(plan):

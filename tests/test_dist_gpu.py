@@ -1,7 +1,8 @@
 """DistributedP2P end to end on the GPU (ranks share the box's GPU; gloo, host-staged exchange):
 each rank exchanges halo weights (synchronously, and pipelined through exchange_async on a
-communication stream as bench.py does), applies its partition, and gathers all targets; the
-gathered result must be bit-identical to the single-plan apply (same tiles, same sum order)."""
+communication stream as bench.py does; and with the peer-memory halo, the owners' buffers read
+through CUDA IPC mappings), applies its partition, and gathers all targets; the gathered result
+must be bit-identical to the single-plan apply (same tiles, same sum order)."""
 import os
 import socket
 
@@ -45,10 +46,13 @@ def _worker(rank, world, port, level, prec, results):
         ev = dp.exchange_async(q_owned, comm)
         out_async = dp.apply(q_owned, halo_ready=ev)
         torch.cuda.synchronize()
+        out_peer = dp.apply_peer(q_owned)  # halo read from the peers' memory (CUDA IPC)
+        torch.cuda.synchronize()
         g_sync = dp.gather(out_sync).double().cpu().numpy()
         g_async = dp.gather(out_async).double().cpu().numpy()
+        g_peer = dp.gather(out_peer).double().cpu().numpy()
         if rank == 0:
-            results.put((g_sync, g_async))
+            results.put((g_sync, g_async, g_peer))
         dp.close()
     finally:
         dist.destroy_process_group()
@@ -68,8 +72,9 @@ def test_distributed_apply_bit_identical(world, level, prec):
     results = ctx.Queue()
     procs = mp.start_processes(_worker, args=(world, _free_port(), level, prec, results), nprocs=world,
                                start_method="spawn", join=False)
-    g_sync, g_async = results.get(timeout=180)  # drain before joining (a blocked queue pipe deadlocks)
+    g_sync, g_async, g_peer = results.get(timeout=180)  # drain before joining (a blocked queue pipe deadlocks)
     while not procs.join():
         pass
     assert np.array_equal(g_sync, ref)
     assert np.array_equal(g_async, ref)
+    assert np.array_equal(g_peer, ref)
