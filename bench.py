@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the R / fp64 detail lines")
     ap.add_argument("--build", choices=["device", "host"], default="device",
                     help="N = 1 plans: built on the GPU (p2p_plan_create_device) or by the host builder")
+    ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
+                    help="N > 1 halo exchange: NCCL all_to_all (default) or peer-memory reads (CUDA IPC / NVLink)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras/baseline)")
@@ -308,6 +310,10 @@ def main():
     comm = torch.cuda.Stream(dev) if world > 1 else None
 
     def step():
+        if world > 1 and args.exchange == "peer":  # halo read from the owners' memory (barriers inside)
+            for j in jobs:
+                j["dp"].apply_peer(j["q_owned"], j["out"], stream=stream.cuda_stream)
+            return
         if world > 1:  # all halo exchanges first on the comm stream: config i's overlaps kernel i-1
             comm.wait_stream(stream)
             ready = [j["dp"].exchange_async(j["q_owned"], comm) for j in jobs]
@@ -338,12 +344,15 @@ def main():
         for k in range(args.steps):
             flush.zero_()
             ev[k][0].record(stream)
-            if world > 1:  # halo exchanges up front on the comm stream (config i's overlaps kernel i-1)
+            peer = world > 1 and args.exchange == "peer"
+            if world > 1 and not peer:  # halo exchanges up front on the comm stream (config i's overlaps kernel i-1)
                 comm.wait_stream(stream)
                 ready = [j["dp"].exchange_async(j["q_owned"], comm) for j in jobs]
             for i, j in enumerate(jobs):
                 kev[k][i][0].record(stream)
-                if world > 1:
+                if peer:
+                    j["dp"].apply_peer(j["q_owned"], j["out"], stream=stream.cuda_stream)
+                elif world > 1:
                     j["dp"].apply(j["q_owned"], j["out"], stream=stream.cuda_stream, halo_ready=ready[i])
                 else:
                     one_apply(j)
@@ -428,8 +437,10 @@ def main():
                    "kernel": args.kernel, **({"kappa_h": args.kh} if args.kernel.startswith("helmholtz") else {}),
                    "order": "plan", "l2": "flushed (256 MiB write) between timed steps",
                    "parallelism": f"morton-range x{world}" + (
-                       (" + host-staged gloo halo exchange, ranks sharing GPUs (TEST MODE)" if shared
-                        else " + NCCL halo exchange") if world > 1 else "")},
+                       ((" + peer-memory halo (CUDA IPC)" if args.exchange == "peer" else
+                         " + host-staged gloo halo exchange") + ", ranks sharing GPUs (TEST MODE)" if shared
+                        else (" + peer-memory halo (CUDA IPC / NVLink)" if args.exchange == "peer"
+                              else " + NCCL halo exchange")) if world > 1 else "")},
         "gpu_launches": args.steps * len(jobs) * (1 if world == 1 else 3),
         "roofline": roofline, "clocks": clocks, "e2e": e2e, "per_config": per_cfg,
     }
