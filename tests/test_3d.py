@@ -114,3 +114,22 @@ def test_full_size_sampled(kernel):
     sel = np.random.default_rng(2).choice(cfg.n, 3000, replace=False)
     ref, _ = oracle.direct_3d(src, q, tgt, cfg.level, "helmholtz" if helm else "laplace", kappa, targets=sel)
     assert np.linalg.norm(got[sel] - ref) / np.linalg.norm(ref) <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("level", [1, 2])
+@pytest.mark.parametrize("kernel", ["laplace3d", "helmholtz3d"])
+def test_coarse_levels(level, kernel):
+    """One box (L = 1) and 2x2x2 boxes (L = 2): every box neighbours every other."""
+    import torch
+    rng = np.random.default_rng(level)
+    src, tgt = rng.random((300, 3)), rng.random((200, 3))
+    helm = kernel == "helmholtz3d"
+    q = rng.uniform(-1, 1, 300) + (1j * rng.uniform(-1, 1, 300) if helm else 0)
+    ref, pairs = oracle.direct_3d(src, q, tgt, level, "helmholtz" if helm else "laplace", 3.0)
+    assert pairs == 300 * 200
+    with p2p.Plan(src, tgt, level=level, layout="nr", precision="fp64", kernel=kernel, wavenumber=3.0) as pl:
+        out = pl.apply(torch.as_tensor(q, dtype=pl.torch_dtype, device="cuda"), order="user")
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12

@@ -97,3 +97,20 @@ def test_uniform_tree_matches_the_grid_path():
         a, b = pa.apply(qd, order="user"), pt.apply(qd, order="user")
         torch.cuda.synchronize()
         assert torch.allclose(a, b, rtol=0, atol=1e-12 * float(b.abs().max()))
+
+
+@pytest.mark.gpu
+def test_single_leaf_and_deep_cap():
+    """CT >= n: the root is the only leaf (every pair interacts); l_max = 1 caps the split."""
+    import torch
+    rng = np.random.default_rng(5)
+    src, tgt = rng.random((400, 2)), rng.random((300, 2))
+    q = rng.uniform(-1, 1, 400)
+    for ct, lmax in ((1000, 12), (5, 1)):
+        ref, pairs = oracle.adaptive_direct(src, q, tgt, ct, lmax)
+        assert pairs == 400 * 300
+        with p2p.Plan(src, tgt, layout="adaptive", ct=ct, l_max=lmax, precision="fp64") as pl:
+            assert pl.export("leaves").tolist() == [1, 0, 0]
+            out = pl.apply(torch.as_tensor(q, device="cuda"), order="user")
+            torch.cuda.synchronize()
+            assert np.linalg.norm(out.cpu().numpy() - ref) / np.linalg.norm(ref) <= 1e-12
