@@ -1455,15 +1455,29 @@ __global__ void __launch_bounds__(NT) p2p_adaptive_kernel(const P2PArgs<T> a) {
         if (b < 0) break;
         const int u0 = a.ul_off[b], nu = a.ul_off[b + 1] - u0;
         const int2 org = a.leaf_org[b];
-        if (tid == 0) {  // U-list source starts and prefix (a U-list holds ~9-20 leaves)
+        if (tid < 32) {  // U-list source starts and prefix: lanes load 32 entries at a time, warp scan
             int run = 0;
-            for (int k = 0; k < nu; ++k) {
-                const int4 r = a.leaf_rng[a.ul_leaf[u0 + k]];
-                s_st[k] = r.x;
-                s_pre[k] = run;
-                run += r.y - r.x;
+            for (int k0 = 0; k0 < nu; k0 += 32) {
+                const int k = k0 + tid;
+                int st = 0, cnt = 0;
+                if (k < nu) {
+                    const int4 r = a.leaf_rng[a.ul_leaf[u0 + k]];
+                    st = r.x;
+                    cnt = r.y - r.x;
+                }
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (tid >= o) incl += v;
+                }
+                if (k < nu) {
+                    s_st[k] = st;
+                    s_pre[k] = run + incl - cnt;
+                }
+                run += __shfl_sync(0xffffffffu, incl, 31);
             }
-            s_pre[nu] = run;
+            if (tid == 0) s_pre[nu] = run;
         }
         __syncthreads();
         const int total = s_pre[nu];
