@@ -233,7 +233,9 @@ void finalize_plan(p2p_plan_s &P) {
     // Dynamic shared memory is fixed per plan: opt in once (a permission, not a
     // reservation, so one value serves all plans), then size the persistent grid.
     const bool two = hp.tpi == 2;
-    const void *kfn = hp.layout == P2P_LAYOUT_ADAPTIVE ? (const void *)p2p::dev::p2p_adaptive_kernel<T, p2p::kAdaptiveThreads>
+    const void *kfn = hp.layout == P2P_LAYOUT_ADAPTIVE
+                          ? (hp.warp_leaf ? (const void *)p2p::dev::p2p_adaptive_warp_kernel<T, 128>
+                                          : (const void *)p2p::dev::p2p_adaptive_kernel<T, p2p::kAdaptiveThreads>)
                       : hp.dim == 3 ? box3d_fn<T>(hp.kernel == P2P_KERNEL_HELMHOLTZ_3D)
                       : hp.kernel == P2P_KERNEL_HELMHOLTZ_2D ? helm_fn<T>(hp.nt)
                       : hp.layout == P2P_LAYOUT_REDUNDANT ? (const void *)p2p::dev::p2p_r_kernel<T>
@@ -441,6 +443,13 @@ void launch_adaptive(p2p_plan_s &P, const T *q, T *out, bool user, int accumulat
     a.accumulate = accumulate;
     void *args[] = {&a};
     const int grid = (int)std::min<int64_t>(ntiles, P.occ_sms);
+    if (hp.warp_leaf) {
+        const int g = (int)std::min<int64_t>((ntiles + 3) / 4, P.occ_sms);
+        ck(cudaLaunchKernel((const void *)p2p::dev::p2p_adaptive_warp_kernel<T, 128>, dim3(g), dim3(128), args,
+                            (size_t)hp.smem_bytes, s),
+           "adaptive launch");
+        return;
+    }
     ck(cudaLaunchKernel((const void *)p2p::dev::p2p_adaptive_kernel<T, p2p::kAdaptiveThreads>, dim3(grid),
                         dim3(p2p::kAdaptiveThreads), args, (size_t)hp.smem_bytes, s),
        "adaptive launch");

@@ -1534,6 +1534,108 @@ __global__ void __launch_bounds__(NT) p2p_adaptive_kernel(const P2PArgs<T> a) {
     if (tid == 0) queue_exit(a.queue);
 }
 
+// ADAPTIVE, one WARP per target leaf (small leaves, CT <= 64): each warp claims leaves from the
+// queue on its own and stages into its own shared-memory slice, with __syncwarp between phases --
+// NT / 32 leaves in flight per CTA instead of one, no CTA-wide barriers.
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) p2p_adaptive_warp_kernel(const P2PArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sbytes = align16(a.src_cap * 4 * (int)sizeof(T));
+    unsigned char *base = smem + (size_t)warp * adaptive_warp_slice(a.src_cap, (int)sizeof(T));
+    T *s_p = reinterpret_cast<T *>(base);
+    int *s_st = reinterpret_cast<int *>(base + sbytes);
+    int *s_pre = s_st + kMaxUlist;
+    T *s_part = reinterpret_cast<T *>(base + sbytes + 8 * kMaxUlist + 16);
+    using C2 = typename V2<T>::type;
+    const C2 *suv = reinterpret_cast<const C2 *>(a.src_uv), *tuv = reinterpret_cast<const C2 *>(a.tgt_uv);
+    const T hf = a.h;
+    for (;;) {
+        int b = -1;
+        if (lane == 0) {
+            const int e = atomicAdd(a.queue, 1);
+            b = e < a.ntiles ? a.tiles[e] : -1;
+        }
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (b < 0) break;
+        const int u0 = a.ul_off[b], nu = a.ul_off[b + 1] - u0;
+        const int2 org = a.leaf_org[b];
+        int run = 0;
+        for (int k0 = 0; k0 < nu; k0 += 32) {  // U-list starts and prefix (warp scan)
+            const int k = k0 + lane;
+            int st = 0, cnt = 0;
+            if (k < nu) {
+                const int4 r = a.leaf_rng[a.ul_leaf[u0 + k]];
+                st = r.x;
+                cnt = r.y - r.x;
+            }
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (k < nu) {
+                s_st[k] = st;
+                s_pre[k] = run + incl - cnt;
+            }
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) s_pre[nu] = run;
+        __syncwarp();
+        const int total = run;
+        for (int i = lane; i < total; i += 32) {
+            int k = 0;
+#pragma unroll
+            for (int step = 128; step; step >>= 1)
+                if (k + step < nu && s_pre[k + step] <= i) k += step;
+            const int j = s_st[k] + (i - s_pre[k]);
+            const int2 cl = a.src_cell[j];
+            const C2 o = suv[j];
+            s_p[4 * i] = fma((T)(cl.x - org.x), hf, o.x);
+            s_p[4 * i + 1] = fma((T)(cl.y - org.y), hf, o.y);
+            s_p[4 * i + 2] = a.q[a.src_idx ? a.src_idx[j] : j];
+        }
+        __syncwarp();
+        const int4 tr = a.leaf_rng[b];
+        const int t0 = tr.z, nt = tr.w - tr.z;
+        const int C = nt >= 32 ? 1 : 32 / nt;
+        auto finish = [&](int t, T acc) {
+            const int64_t o = a.out_idx ? a.out_idx[t0 + t] : t0 + t;
+            const T v = sizeof(T) == 4 ? (T)(-0.5f * kLn2) * acc : (T)-0.5 * acc;
+            a.out[o] = a.accumulate ? a.out[o] + v : v;
+        };
+        for (int it = lane; it < nt * C; it += 32) {
+            const int t = it % nt, ch = it / nt;
+            const int2 cl = a.tgt_cell[t0 + t];
+            const C2 o = tuv[t0 + t];
+            const T tx = fma((T)(cl.x - org.x), hf, o.x), ty = fma((T)(cl.y - org.y), hf, o.y);
+            const int s0 = (int)((int64_t)total * ch / C), s1 = (int)((int64_t)total * (ch + 1) / C);
+            T acc = (T)0;
+            for (int s = s0; s < s1; ++s) {
+                const T dx = tx - s_p[4 * s], dy = ty - s_p[4 * s + 1];
+                const T r2 = fma(dy, dy, dx * dx);
+                if (r2 < a.eps2) continue;  // coincident points contribute 0 (R3)
+                if constexpr (sizeof(T) == 4) acc = fmaf(s_p[4 * s + 2], lg2_approx(r2), acc);
+                else acc = fma(s_p[4 * s + 2], log(r2), acc);
+            }
+            if (C == 1) finish(t, acc);
+            else s_part[it] = acc;
+        }
+        if (C > 1) {
+            __syncwarp();
+            for (int t = lane; t < nt; t += 32) {
+                T acc = (T)0;
+                for (int ch = 0; ch < C; ++ch) acc += s_part[ch * nt + t];
+                finish(t, acc);
+            }
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) queue_exit(a.queue);
+}
+
 // ---------------------------------------------------------------- the paper's kernels (NEXT-1)
 // Reproduced as the paper describes them, global memory only ("none of ... pre-fetching,
 // exploiting Shared Memory ... were employed"), fp64, the library log.

@@ -214,6 +214,7 @@ struct HostPlan {
     int L = 0, k = 0, layout = 0, precision = 0, device = -1;
     int kernel = P2P_KERNEL_LAPLACE_2D;          // p2p_kernel
     int dim = 2;                                 // 3 for the 3D kernels (octree leaf grid)
+    bool warp_leaf = false;                      // ADAPTIVE: one warp per target leaf (small leaves)
     double kappa = 0.0;                          // HELMHOLTZ_2D wavenumber
     int part_world = 1, part_rank = 0;
     int64_t S = 0, B = 0;        // grid side, number of leaf boxes
@@ -321,6 +322,10 @@ void build_host_plan_adaptive(const p2p_plan_desc &desc, HostPlan &hp);
 // U-list source starts and prefix (up to kMaxUlist leaves), partial sums per thread.
 constexpr int kMaxUlist = 256;
 constexpr int kAdaptiveThreads = 64;
+// ADAPTIVE warp-per-leaf kernel: one slice per warp (staged sources, U-list starts / prefix, partials)
+P2P_HD inline int adaptive_warp_slice(int src_cap, int e) {
+    return align16(src_cap * 4 * e) + 8 * kMaxUlist + 16 + align16(32 * e);
+}
 inline int64_t adaptive_smem(int64_t src_cap, int e) {
     return ((src_cap * 4 * e + 15) & ~int64_t(15)) + 8 * kMaxUlist + 16 + kAdaptiveThreads * e + 16;
 }

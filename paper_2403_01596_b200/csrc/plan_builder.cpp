@@ -368,6 +368,14 @@ void build_host_plan_adaptive(const p2p_plan_desc &d, HostPlan &hp) {
     hp.nt = kAdaptiveThreads;
     const int e = d.precision == P2P_FP32 ? 4 : 8;
     hp.smem_bytes = adaptive_smem(hp.src_cap, e);
+    // fp32 leaves of <= 32 targets: one warp per leaf, 4 warps per CTA (measured: +38 % at CT = 16,
+    // +12 % at CT = 32; slower for larger leaves and for fp64, tools/gpu_ab20.sh); P2P_ADAPTIVE_WARP=0: off
+    hp.warp_leaf = e == 4 && hp.tgt_cap <= 32;
+    if (const char *v = std::getenv("P2P_ADAPTIVE_WARP")) hp.warp_leaf = hp.warp_leaf && std::atoi(v) != 0;
+    if (hp.warp_leaf) {
+        hp.nt = 128;
+        hp.smem_bytes = 4 * (int64_t)adaptive_warp_slice((int)std::min<int64_t>(hp.src_cap, 1 << 20), e);
+    }
     if (hp.smem_bytes > kSmemLimit)
         fail(P2P_ERROR_NOT_SUPPORTED, "ADAPTIVE: a U-list holds " + std::to_string(max_src) +
                                           " sources (> shared memory); lower ct");
