@@ -14,8 +14,11 @@
  *
  * Life cycle: p2p_plan_create (host-side plan build: level selection, box
  * assignment, Morton sort, CSR offsets, tiles, partition, NR/R layout, upload)
- * -> p2p_apply (per matrix-vector product; stream-ordered, allocation-free)
- * -> p2p_destroy.
+ * or p2p_plan_create_device (the same plan built by GPU kernels from device
+ * coordinates) -> p2p_apply (per matrix-vector product; stream-ordered,
+ * allocation-free) -> p2p_destroy.  Beyond the paper's kernel and grid
+ * (SURVEY.md §8(f)): the 2D Helmholtz kernel, 3D octree kernels and an adaptive
+ * (CT-driven) quadtree layout -- see p2p_kernel and p2p_layout below.
  *
  * Conventions:
  *  - Every entry point returns a p2p_status; nothing throws or exits.  On
