@@ -65,7 +65,8 @@ typedef enum {
  *                free-space Green's function of the oscillatory ("high-frequency", PAPER.md
  *                L17, L299) MLFMA problems; kappa = desc.wavenumber > 0; q and phi complex,
  *                interleaved (re, im) pairs in the plan precision (C99 complex / torch
- *                complex64 / complex128 layout).  TILED layout, one partition.
+ *                complex64 / complex128 layout).  TILED layout; partitions (halo exchange,
+ *                distributed applies) move (re, im) pairs.
  *   LAPLACE_3D / HELMHOLTZ_3D (R24): the operator on an octree
  *                leaf grid of the unit cube -- boxes 2^(L-1) per side (L <= 9), E1 = the 3x3x3 block
  *                clipped at the faces, 3D Morton order (x bit 3i, y 3i+1, z 3i+2); G = 1/(4 pi r)

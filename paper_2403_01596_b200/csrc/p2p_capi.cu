@@ -482,7 +482,11 @@ void apply_impl(p2p_plan_s &P, const void *d_q, void *d_out, int order, int accu
                 (const int32_t *)P.src_uidx.p, (const T *)d_q, (T *)P.q_local.p, hp.n_src_local);
         q_local = (const T *)P.q_local.p;
     } else if (hp.part_world > 1) {  // replicated weights in global plan order
-        if (hp.n_src_local)
+        using V = typename p2p::dev::V2<T>::type;
+        if (hp.n_src_local && P.comps == 2)
+            p2p::dev::gather_kernel<V><<<grid_for(hp.n_src_local), 256, 0, s>>>(
+                (const int32_t *)P.src_gidx.p, (const V *)d_q, (V *)P.q_local.p, hp.n_src_local);
+        else if (hp.n_src_local)
             p2p::dev::gather_kernel<T><<<grid_for(hp.n_src_local), 256, 0, s>>>(
                 (const int32_t *)P.src_gidx.p, (const T *)d_q, (T *)P.q_local.p, hp.n_src_local);
         q_local = (const T *)P.q_local.p;
@@ -505,10 +509,9 @@ void apply_impl(p2p_plan_s &P, const void *d_q, void *d_out, int order, int accu
 template <typename T>
 void apply_dist_interior_impl(p2p_plan_s &P, const void *d_q_owned, void *d_out, int accumulate, cudaStream_t s) {
     const p2p::HostPlan &hp = P.hp;
-    if (P.comps != 1) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "distributed apply: real kernels only");
     if (hp.n_src_owned)
-        ck(cudaMemcpyAsync((T *)P.q_local.p + hp.owned_local_begin, d_q_owned, (size_t)hp.n_src_owned * sizeof(T),
-                           cudaMemcpyDeviceToDevice, s),
+        ck(cudaMemcpyAsync((T *)P.q_local.p + hp.owned_local_begin * P.comps, d_q_owned,
+                           (size_t)hp.n_src_owned * sizeof(T) * P.comps, cudaMemcpyDeviceToDevice, s),
            "owned weights");
     if (hp.layout == P2P_LAYOUT_TILED)
         launch_p2p<T>(P, (const T *)P.q_local.p, (T *)d_out, accumulate, s, false, 0, hp.n_interior);
@@ -518,10 +521,15 @@ void apply_dist_interior_impl(p2p_plan_s &P, const void *d_q_owned, void *d_out,
 template <typename T>
 void apply_dist_boundary_impl(p2p_plan_s &P, const void *d_q_halo, void *d_out, int accumulate, cudaStream_t s) {
     const p2p::HostPlan &hp = P.hp;
-    if (P.comps != 1) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "distributed apply: real kernels only");
-    if (hp.n_halo)
-        p2p::dev::scatter_kernel<T><<<grid_for(hp.n_halo), 256, 0, s>>>(
-            (const int32_t *)P.halo_lidx.p, (const T *)d_q_halo, (T *)P.q_local.p, hp.n_halo, 0);
+    if (hp.n_halo) {
+        using V = typename p2p::dev::V2<T>::type;  // complex weights: (re, im) moved as one element
+        if (P.comps == 2)
+            p2p::dev::copy_scatter_kernel<V><<<grid_for(hp.n_halo), 256, 0, s>>>(
+                (const int32_t *)P.halo_lidx.p, (const V *)d_q_halo, (V *)P.q_local.p, hp.n_halo);
+        else
+            p2p::dev::copy_scatter_kernel<T><<<grid_for(hp.n_halo), 256, 0, s>>>(
+                (const int32_t *)P.halo_lidx.p, (const T *)d_q_halo, (T *)P.q_local.p, hp.n_halo);
+    }
     if (hp.layout == P2P_LAYOUT_TILED)
         launch_p2p<T>(P, (const T *)P.q_local.p, (T *)d_out, accumulate, s, false, hp.n_interior,
                       (int64_t)hp.tiles.size());
@@ -1163,27 +1171,29 @@ p2p_status p2p_apply_dist_peer(p2p_plan P, const void *d_q_owned, const void *co
         DeviceGuard g(P->device);
         cudaStream_t s = (cudaStream_t)stream;
         const p2p::HostPlan &hp = P->hp;
-        if (P->comps != 1) throw p2p::Error(P2P_ERROR_NOT_SUPPORTED, "distributed apply: real kernels only");
-        auto run = [&](auto tag) {
-            using T = decltype(tag);
-            p2p::dev::PeerPtrs<T> pp{};
+        auto run = [&](auto tag, auto vtag) {
+            using T = decltype(tag);     // plan precision
+            using V = decltype(vtag);    // one weight: T, or (re, im) for complex kernels
+            p2p::dev::PeerPtrs<V> pp{};
             for (int r = 0; r < hp.part_world; ++r) {
-                pp.p[r] = r == hp.part_rank ? (const T *)d_q_owned : (const T *)d_peer_q[r];
+                pp.p[r] = r == hp.part_rank ? (const V *)d_q_owned : (const V *)d_peer_q[r];
                 if (!pp.p[r] && r != hp.part_rank) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "NULL peer pointer");
             }
             if (hp.n_src_owned)
-                ck(cudaMemcpyAsync((T *)P->q_local.p + hp.owned_local_begin, d_q_owned,
-                                   (size_t)hp.n_src_owned * sizeof(T), cudaMemcpyDeviceToDevice, s),
+                ck(cudaMemcpyAsync((V *)P->q_local.p + hp.owned_local_begin, d_q_owned,
+                                   (size_t)hp.n_src_owned * sizeof(V), cudaMemcpyDeviceToDevice, s),
                    "owned weights");
             if (hp.n_halo)
-                p2p::dev::halo_peer_kernel<T><<<grid_for(hp.n_halo), 256, 0, s>>>(
+                p2p::dev::halo_peer_kernel<V><<<grid_for(hp.n_halo), 256, 0, s>>>(
                     pp, (const int32_t *)P->halo_owner.p, (const int32_t *)P->halo_oidx.p,
-                    (const int32_t *)P->halo_lidx.p, (T *)P->q_local.p, hp.n_halo);
+                    (const int32_t *)P->halo_lidx.p, (V *)P->q_local.p, hp.n_halo);
             launch_p2p<T>(*P, (const T *)P->q_local.p, (T *)d_out, accumulate ? 1 : 0, s);
             ck(cudaGetLastError(), "apply_dist_peer launch");
         };
-        if (P->elem == 4) run(float{});
-        else run(double{});
+        if (P->elem == 4 && P->comps == 1) run(float{}, float{});
+        else if (P->elem == 4) run(float{}, float2{});
+        else if (P->comps == 1) run(double{}, double{});
+        else run(double{}, double2{});
     });
 }
 
@@ -1235,12 +1245,16 @@ p2p_status p2p_halo_pack(p2p_plan P, const void *d_q_owned, void *d_send, void *
         cudaStream_t s = (cudaStream_t)stream;
         const int64_t n = P->hp.n_send;
         if (!n) return;
-        if (P->elem == 4)
-            p2p::dev::gather_kernel<float><<<grid_for(n), 256, 0, s>>>((const int32_t *)P->send_idx.p,
-                                                                       (const float *)d_q_owned, (float *)d_send, n);
+        const int32_t *ix = (const int32_t *)P->send_idx.p;
+        if (P->elem == 4 && P->comps == 1)
+            p2p::dev::gather_kernel<float><<<grid_for(n), 256, 0, s>>>(ix, (const float *)d_q_owned, (float *)d_send, n);
+        else if (P->elem == 4)
+            p2p::dev::gather_kernel<float2><<<grid_for(n), 256, 0, s>>>(ix, (const float2 *)d_q_owned, (float2 *)d_send, n);
+        else if (P->comps == 1)
+            p2p::dev::gather_kernel<double><<<grid_for(n), 256, 0, s>>>(ix, (const double *)d_q_owned, (double *)d_send, n);
         else
-            p2p::dev::gather_kernel<double><<<grid_for(n), 256, 0, s>>>(
-                (const int32_t *)P->send_idx.p, (const double *)d_q_owned, (double *)d_send, n);
+            p2p::dev::gather_kernel<double2><<<grid_for(n), 256, 0, s>>>(ix, (const double2 *)d_q_owned, (double2 *)d_send,
+                                                                         n);
         ck(cudaGetLastError(), "halo_pack launch");
     });
 }

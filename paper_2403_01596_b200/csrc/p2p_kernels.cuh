@@ -1723,6 +1723,14 @@ __global__ void gather_kernel(const int32_t *__restrict__ idx, const T *__restri
         dst[i] = src[idx[i]];
 }
 
+// out[idx[i]] = v[i] for any element type (complex weights of the distributed Helmholtz apply)
+template <typename V>
+__global__ void copy_scatter_kernel(const int32_t *__restrict__ idx, const V *__restrict__ v, V *__restrict__ out,
+                                    int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[idx[i]] = v[i];
+}
+
 // dst[i] = i2 < n_owned ? owned[i2] : halo[i2 - n_owned], i2 = qidx[i]  (distributed import)
 // out[idx[i]] (+)= phi[i]  (ORDER_USER export)
 template <typename T>

@@ -197,7 +197,8 @@ void check_kernel(const p2p_plan_desc &d) {
         fail(P2P_ERROR_NOT_SUPPORTED, "HELMHOLTZ_2D runs on the TILED layout");
     if (kernel_dim(d.kernel) == 3 && d.layout != P2P_LAYOUT_NONREDUNDANT)
         fail(P2P_ERROR_NOT_SUPPORTED, "3D kernels run on the NONREDUNDANT (box-per-CTA) layout");
-    if (d.part_world != 1) fail(P2P_ERROR_NOT_SUPPORTED, "kernels other than LAPLACE_2D: one partition");
+    if (d.part_world != 1 && d.kernel != P2P_KERNEL_HELMHOLTZ_2D)
+        fail(P2P_ERROR_NOT_SUPPORTED, "3D kernels: one partition");
 }
 
 // ---- ADAPTIVE: the CT-driven quadtree, per box (§3.1

@@ -62,12 +62,16 @@ class DistributedP2P:
         if n_send:
             self.plan.halo_pack(q_owned, self._send, stream)
         send, halo = self._send[:n_send], self._halo[:n_halo]
+        rs, ss = self.recv_splits, self.send_splits
+        if send.is_complex():  # complex weights (Helmholtz) move as (re, im) float pairs
+            send, halo = self.torch.view_as_real(send).reshape(-1), self.torch.view_as_real(halo).reshape(-1)
+            rs, ss = [2 * x for x in rs], [2 * x for x in ss]
         if self.host_staged:
-            recv = self.torch.empty(n_halo, dtype=halo.dtype)
-            self.dist.all_to_all_single(recv, send.cpu(), self.recv_splits, self.send_splits, group=self.group)
+            recv = self.torch.empty(halo.numel(), dtype=halo.dtype)
+            self.dist.all_to_all_single(recv, send.cpu(), rs, ss, group=self.group)
             halo.copy_(recv)
         else:
-            self.dist.all_to_all_single(halo, send, self.recv_splits, self.send_splits, group=self.group)
+            self.dist.all_to_all_single(halo, send, rs, ss, group=self.group)
         return self._halo
 
     def exchange_async(self, q_owned, comm_stream, after=None):
@@ -153,6 +157,16 @@ class DistributedP2P:
         cmax = int(counts.max()) if len(counts) else 0
         pad = torch.zeros(max(1, cmax), dtype=phi_local.dtype, device=phi_local.device)
         pad[: self.n_tgt_local].copy_(phi_local[: self.n_tgt_local])
+        if pad.is_complex():  # collectives on the (re, im) float view
+            real = torch.view_as_real(pad).reshape(-1)
+            if self.host_staged:
+                pr = [torch.empty_like(real, device="cpu") for _ in range(self.world)]
+                self.dist.all_gather(pr, real.cpu(), group=self.group)
+            else:
+                pr = [torch.empty_like(real) for _ in range(self.world)]
+                self.dist.all_gather(pr, real, group=self.group)
+            parts = [torch.view_as_complex(p.reshape(-1, 2).contiguous()) for p in pr]
+            return torch.cat([p[: int(c)].to(phi_local.device) for p, c in zip(parts, counts)])
         if self.host_staged:
             parts = [torch.empty_like(pad, device="cpu") for _ in range(self.world)]
             self.dist.all_gather(parts, pad.cpu(), group=self.group)

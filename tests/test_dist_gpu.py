@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, level, prec, results):
+def _worker(rank, world, port, level, prec, results, kernel="laplace"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch
@@ -35,7 +35,11 @@ def _worker(rank, world, port, level, prec, results):
     try:
         torch.cuda.set_device(0)
         src, tgt, q = W.make_problem(W.widened(W.CONFIGS["tiny"], 4))
-        dp = DistributedP2P(src, tgt, device=0, host_staged=True, level=level, layout="tiled", precision=prec)
+        kw = {}
+        if kernel == "helmholtz":  # complex weights through the same exchange (re, im pairs)
+            q = W.weights_complex(len(src), 1)
+            kw = dict(kernel="helmholtz", wavenumber=1.2 * (1 << (level - 1)))
+        dp = DistributedP2P(src, tgt, device=0, host_staged=True, level=level, layout="tiled", precision=prec, **kw)
         dt = dp.plan.torch_dtype
         lo, hi = dp.owned_source_range()
         full = p2p.Plan(src, tgt, level=level, device=-1)
@@ -48,9 +52,9 @@ def _worker(rank, world, port, level, prec, results):
         torch.cuda.synchronize()
         out_peer = dp.apply_peer(q_owned)  # halo read from the peers' memory (CUDA IPC)
         torch.cuda.synchronize()
-        g_sync = dp.gather(out_sync).double().cpu().numpy()
-        g_async = dp.gather(out_async).double().cpu().numpy()
-        g_peer = dp.gather(out_peer).double().cpu().numpy()
+        conv = (lambda t: t.cpu().numpy().astype(np.complex128)) if kernel == "helmholtz" else \
+            (lambda t: t.double().cpu().numpy())
+        g_sync, g_async, g_peer = conv(dp.gather(out_sync)), conv(dp.gather(out_async)), conv(dp.gather(out_peer))
         if rank == 0:
             results.put((g_sync, g_async, g_peer))
         dp.close()
@@ -60,17 +64,23 @@ def _worker(rank, world, port, level, prec, results):
 
 @pytest.mark.timeout(240)
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("level,prec", [(5, "fp32"), (7, "fp32"), (5, "fp64")])
-def test_distributed_apply_bit_identical(world, level, prec):
+@pytest.mark.parametrize("level,prec,kernel", [(5, "fp32", "laplace"), (7, "fp32", "laplace"), (5, "fp64", "laplace"),
+                                               (5, "fp32", "helmholtz"), (6, "fp64", "helmholtz")])
+def test_distributed_apply_bit_identical(world, level, prec, kernel):
     from paper_2403_01596_b200 import p2p
     from paper_2403_01596_b200 import workloads as W
     src, tgt, q = W.make_problem(W.widened(W.CONFIGS["tiny"], 4))
-    with p2p.Plan(src, tgt, level=level, layout="tiled", precision=prec) as pl:
+    kw = {}
+    if kernel == "helmholtz":
+        q = W.weights_complex(len(src), 1)
+        kw = dict(kernel="helmholtz", wavenumber=1.2 * (1 << (level - 1)))
+    with p2p.Plan(src, tgt, level=level, layout="tiled", precision=prec, **kw) as pl:
         qd = torch.as_tensor(q[pl.export("src_perm")], dtype=pl.torch_dtype, device="cuda")
-        ref = pl.apply(qd).double().cpu().numpy()
+        out = pl.apply(qd)
+        ref = out.cpu().numpy().astype(np.complex128) if kernel == "helmholtz" else out.double().cpu().numpy()
     ctx = mp.get_context("spawn")
     results = ctx.Queue()
-    procs = mp.start_processes(_worker, args=(world, _free_port(), level, prec, results), nprocs=world,
+    procs = mp.start_processes(_worker, args=(world, _free_port(), level, prec, results, kernel), nprocs=world,
                                start_method="spawn", join=False)
     g_sync, g_async, g_peer = results.get(timeout=180)  # drain before joining (a blocked queue pipe deadlocks)
     while not procs.join():

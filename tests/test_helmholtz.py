@@ -24,8 +24,7 @@ def test_helmholtz_envelope_errors():
     src, tgt, _ = W.make_problem("tiny")
     for kw, st in ((dict(layout="nr", wavenumber=5.0), p2p.P2P_ERROR_NOT_SUPPORTED),
                    (dict(layout="tiled", wavenumber=0.0), p2p.P2P_ERROR_INVALID_ARGUMENT),
-                   (dict(layout="tiled", wavenumber=float("nan")), p2p.P2P_ERROR_INVALID_ARGUMENT),
-                   (dict(layout="tiled", wavenumber=5.0, part_world=2), p2p.P2P_ERROR_NOT_SUPPORTED)):
+                   (dict(layout="tiled", wavenumber=float("nan")), p2p.P2P_ERROR_INVALID_ARGUMENT)):
         with pytest.raises(p2p.P2PError) as ei:
             p2p.Plan(src, tgt, level=4, device=-1, kernel="helmholtz", **kw)
         assert ei.value.status == st, kw
