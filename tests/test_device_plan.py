@@ -31,6 +31,8 @@ def _desc(n_src, n_tgt, **kw):
     (dict(layout=p2p.P2P_LAYOUT_REDUNDANT), p2p.P2P_ERROR_NOT_SUPPORTED),
     (dict(layout=p2p.P2P_LAYOUT_PAPER_INDEXING, precision=p2p.P2P_FP64), p2p.P2P_ERROR_NOT_SUPPORTED),
     (dict(part_world=2), p2p.P2P_ERROR_NOT_SUPPORTED),
+    (dict(layout=p2p.P2P_LAYOUT_ADAPTIVE), p2p.P2P_ERROR_NOT_SUPPORTED),
+    (dict(kernel=p2p.P2P_KERNEL_LAPLACE_3D), p2p.P2P_ERROR_NOT_SUPPORTED),
     (dict(epsilon=0.0), p2p.P2P_ERROR_INVALID_ARGUMENT),
     (dict(device=-1), p2p.P2P_ERROR_NO_DEVICE),
 ])
