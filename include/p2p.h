@@ -244,6 +244,13 @@ p2p_status p2p_apply_dist_boundary(p2p_plan plan, const void *d_q_halo, void *d_
 p2p_status p2p_apply_dist_peer(p2p_plan plan, const void *d_q_owned, const void *const *d_peer_q, void *d_out,
                                int32_t accumulate, void *stream);
 
+/* Result gather (allgatherv) over peer memory: d_global (device, n_tgt
+ * elements, global plan order) receives every rank's shard, d_peer_out[r] = rank r's n_tgt_local
+ * results (plan order; mapped with p2p_ipc_open; d_peer_out[part_rank] may be this rank's own
+ * output).  Device-to-device copies on `stream` (NVLink reads on a node).  The caller orders the
+ * peers (every shard written before the call's copies run). */
+p2p_status p2p_gather_peer(p2p_plan plan, const void *const *d_peer_out, void *d_global, void *stream);
+
 /* CUDA IPC for p2p_apply_dist_peer.  p2p_ipc_export: the 64-byte handle (host buffer) of the
  * allocation holding d_ptr and d_ptr's byte offset in it (pointers from sub-allocating
  * allocators, e.g. torch's, are fine).  p2p_ipc_open: map a peer's handle on `device` and

@@ -1197,6 +1197,24 @@ p2p_status p2p_apply_dist_peer(p2p_plan P, const void *d_q_owned, const void *co
     });
 }
 
+p2p_status p2p_gather_peer(p2p_plan P, const void *const *d_peer_out, void *d_global, void *stream) {
+    if (!P || !d_peer_out || !d_global) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or buffer");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        const p2p::HostPlan &hp = P->hp;
+        const size_t el = (size_t)P->elem * P->comps;
+        for (int r = 0; r < hp.part_world; ++r) {
+            const int64_t n = hp.part_tgt[r + 1] - hp.part_tgt[r];
+            if (!n) continue;
+            if (!d_peer_out[r]) throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "NULL peer output");
+            ck(cudaMemcpyAsync((char *)d_global + (size_t)hp.part_tgt[r] * el, d_peer_out[r], (size_t)n * el,
+                               cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
+               "gather_peer copy");
+        }
+    });
+}
+
 p2p_status p2p_ipc_export(const void *d_ptr, void *handle64, int64_t *offset) {
     if (!d_ptr || !handle64 || !offset) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL pointer");
     return guarded([&] {

@@ -150,6 +150,31 @@ class DistributedP2P:
         self.dist.barrier(group=self.group)
         return out
 
+    def gather_peer(self, phi_local):
+        """allgatherv (a11) over peer memory: every rank copies every shard straight from its
+        owner's buffer (CUDA IPC mappings; NVLink reads on a node) -- no collective."""
+        torch = self.torch
+        dev = torch.device("cuda", self.device)
+        if not hasattr(self, "_out_peers"):
+            self._outbuf = torch.zeros(max(1, self.n_tgt_local), dtype=self.plan.torch_dtype, device=dev)
+            mine = p2p.p2p_ipc_export(self._outbuf.data_ptr())
+            allh = [None] * self.world
+            self.dist.all_gather_object(allh, mine, group=self.group)
+            self._out_peers = [(self._outbuf.data_ptr(), 0) if r == self.rank else
+                               (p2p.p2p_ipc_open(allh[r][0], allh[r][1], self.device), allh[r][1])
+                               for r in range(self.world)]
+        n = self.n_tgt_local
+        if n:
+            self._outbuf[:n].copy_(phi_local[:n])
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier(group=self.group)
+        out = torch.empty(int(self.tgt_begin[-1]), dtype=self.plan.torch_dtype, device=dev)
+        p2p.p2p_gather_peer(self.plan.handle, [p for p, _ in self._out_peers], out.data_ptr(),
+                            torch.cuda.current_stream(self.device).cuda_stream)
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier(group=self.group)
+        return out
+
     def gather(self, phi_local):
         """allgatherv (a11): every rank receives phi for all targets in global plan order."""
         torch = self.torch
@@ -180,4 +205,8 @@ class DistributedP2P:
             if ptr:
                 p2p.p2p_ipc_close(ptr, off)
         self._peers = []
+        for r, (ptr, off) in enumerate(getattr(self, "_out_peers", [])):
+            if ptr and r != self.rank:
+                p2p.p2p_ipc_close(ptr, off)
+        self._out_peers = []
         self.plan.close()

@@ -58,7 +58,7 @@ EXPORT = {
 ABI_SYMBOLS = (
     "p2p_plan_desc_init", "p2p_plan_create", "p2p_plan_create_device", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async",
     "p2p_apply_dist", "p2p_apply_dist_interior", "p2p_apply_dist_boundary",
-    "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_ipc_export", "p2p_ipc_open", "p2p_ipc_close", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
+    "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_gather_peer", "p2p_ipc_export", "p2p_ipc_open", "p2p_ipc_close", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
     "p2p_status_string", "p2p_last_error", "p2p_abi_version",
 )
 
@@ -126,6 +126,7 @@ def load_library() -> C.CDLL:
     lib.p2p_apply_dist_boundary.argtypes = [P, P, P, i32, P]
     lib.p2p_halo_pack.argtypes = [P, P, P, P]
     lib.p2p_apply_dist_peer.argtypes = [P, P, C.POINTER(P), P, i32, P]
+    lib.p2p_gather_peer.argtypes = [P, C.POINTER(P), P, P]
     lib.p2p_ipc_export.argtypes = [P, P, C.POINTER(i64)]
     lib.p2p_ipc_open.argtypes = [P, i64, i32, C.POINTER(P)]
     lib.p2p_ipc_close.argtypes = [P, i64]
@@ -137,7 +138,7 @@ def load_library() -> C.CDLL:
     lib.p2p_last_error.restype = C.c_char_p
     lib.p2p_abi_version.restype = i32
     for name in ("p2p_plan_create", "p2p_plan_create_device", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async", "p2p_apply_dist", "p2p_apply_dist_interior",
-                 "p2p_apply_dist_boundary", "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_ipc_export",
+                 "p2p_apply_dist_boundary", "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_gather_peer", "p2p_ipc_export",
                  "p2p_ipc_open", "p2p_ipc_close",
                  "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export"):
         getattr(lib, name).restype = i32
@@ -215,6 +216,11 @@ def p2p_apply_dist_peer(plan, d_q_owned: int, peer_ptrs, d_out: int, accumulate:
     arr = (C.c_void_p * len(peer_ptrs))(*[p or None for p in peer_ptrs])
     _check(load_library().p2p_apply_dist_peer(plan, d_q_owned or None, arr, d_out, accumulate, stream or None),
            "p2p_apply_dist_peer")
+
+
+def p2p_gather_peer(plan, peer_out_ptrs, d_global: int, stream: int = 0):
+    arr = (C.c_void_p * len(peer_out_ptrs))(*[p or None for p in peer_out_ptrs])
+    _check(load_library().p2p_gather_peer(plan, arr, d_global, stream or None), "p2p_gather_peer")
 
 
 def p2p_ipc_export(d_ptr: int) -> tuple[bytes, int]:

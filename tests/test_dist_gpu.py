@@ -55,6 +55,8 @@ def _worker(rank, world, port, level, prec, results, kernel="laplace"):
         conv = (lambda t: t.cpu().numpy().astype(np.complex128)) if kernel == "helmholtz" else \
             (lambda t: t.double().cpu().numpy())
         g_sync, g_async, g_peer = conv(dp.gather(out_sync)), conv(dp.gather(out_async)), conv(dp.gather(out_peer))
+        g_gp = conv(dp.gather_peer(out_peer))  # allgatherv over peer memory
+        assert np.array_equal(g_gp, g_peer)
         if rank == 0:
             results.put((g_sync, g_async, g_peer))
         dp.close()
