@@ -720,6 +720,9 @@ p2p_r_kernel(const P2PArgs<T> a) {
 //   by n9, the three runs optionally flattened into one sequence).
 // Every target's sum has a fixed order independent of the launch, the tile
 // split and the partition: results are bit-reproducible.
+#ifndef P2P_HELM_PAIR
+#define P2P_HELM_PAIR 1  // fp32 Helmholtz: two sources per step, series packed in f32x2
+#endif
 #ifndef P2P_DENSE_MINB
 #define P2P_DENSE_MINB 0  // > 0: register cap via min resident CTAs for the TPI = 2 instances (experiments)
 #endif
@@ -1006,6 +1009,27 @@ struct HelmSeries<float> {
         const float hl = fmaf(lg2_approx(z), 0.5f * kLn2, 0.5772156649015329f);  // ln(x/2) + gamma
         J = j;
         Y = 0.6366197723675814f * fmaf(hl, j, s);
+    }    // two arguments at once: each Horner chain packed over the two sources (f32x2), the two
+    // chains (J, S) independent
+    static __device__ __forceinline__ void eval2(float za, float zc, float &Ja, float &Ya, float &Jc, float &Yc) {
+        constexpr float A[11] = {1.0f, -1.0f, 0.25f, -0.027777777777777776f, 0.001736111111111111f,
+                                 -6.944444444444444e-05f, 1.9290123456790124e-06f, -3.936759889140842e-08f,
+                                 6.151187326782565e-10f, -7.594058428126624e-12f, 7.594058428126623e-14f};
+        constexpr float B[11] = {0.0f, 1.0f, -0.375f, 0.05092592592592592f, -0.003616898148148148f,
+                                 0.0001585648148148148f, -4.72608024691358e-06f, 1.0207455998272325e-07f,
+                                 -1.6718048413148328e-09f, 2.1483350211950277e-11f, -2.224275605476294e-13f};
+        const f2_t Z = f2_pack(za, zc);
+        f2_t j = f2_pack(A[10], A[10]), s = f2_pack(B[10], B[10]);
+#pragma unroll
+        for (int k = 9; k >= 0; --k) {
+            j = f2_fma(j, Z, f2_pack(A[k], A[k]));
+            s = f2_fma(s, Z, f2_pack(B[k], B[k]));
+        }
+        const f2_t hl = f2_fma(f2_pack(lg2_approx(za), lg2_approx(zc)), f2_pack(0.5f * kLn2, 0.5f * kLn2),
+                               f2_pack(0.5772156649015329f, 0.5772156649015329f));
+        const f2_t Y = f2_mul(f2_pack(0.6366197723675814f, 0.6366197723675814f), f2_fma(hl, j, s));
+        f2_unpack(j, Ja, Jc);
+        f2_unpack(Y, Ya, Yc);
     }
 };
 // fp64 series coefficients (a_k, b_k of HelmSeries<float>, 19 terms) in the constant bank
@@ -1153,12 +1177,11 @@ __global__ void __launch_bounds__(NT) p2p_tiled_helm_kernel(const P2PArgs<T> a) 
                              table[jb + 2 * R + 3]);
             T re = (T)0, im = (T)0;
             const int v1 = runs.v0 + runs.n;
-            for (int v = runs.v0; v < v1; ++v) {
-                const int j = runs.at(v);
+            auto one = [&](int j) {
                 const C2 sp = s_uv[j];
                 const T du = ux - sp.x, dv = uy - sp.y;
                 const T r2 = du * du + dv * dv;
-                if (r2 < a.eps2) continue;  // coincident points contribute 0 (R3)
+                if (r2 < a.eps2) return;  // coincident points contribute 0 (R3)
                 T J, Y;
                 const T z = kq * r2;  // (kappa r / 2)^2
                 if (z <= HelmSeries<T>::kZmax) HelmSeries<T>::eval(z, J, Y, s_lt);
@@ -1166,7 +1189,34 @@ __global__ void __launch_bounds__(NT) p2p_tiled_helm_kernel(const P2PArgs<T> a) 
                 const C2 qv = s_q[j];
                 re = fma(-qv.x, Y, fma(-qv.y, J, re));
                 im = fma(qv.x, J, fma(-qv.y, Y, im));
+            };
+            int v = runs.v0;
+            if constexpr (sizeof(T) == 4 && P2P_HELM_PAIR) {
+                // two sources per step: both series in packed f32x2 FMAs (two independent chains)
+                for (; v + 1 < v1; v += 2) {
+                    const int ja = runs.at(v), jc = runs.at(v + 1);
+                    const float2 pa = reinterpret_cast<const float2 *>(s_uv)[ja];
+                    const float2 pc = reinterpret_cast<const float2 *>(s_uv)[jc];
+                    const float dua = ux - pa.x, dva = uy - pa.y, duc = ux - pc.x, dvc = uy - pc.y;
+                    const float r2a = fmaf(dva, dva, dua * dua), r2c = fmaf(dvc, dvc, duc * duc);
+                    const float za = kq * r2a, zc = kq * r2c;
+                    if (r2a >= a.eps2 && r2c >= a.eps2 && za <= HelmSeries<float>::kZmax &&
+                        zc <= HelmSeries<float>::kZmax) {
+                        float Ja, Ya, Jc, Yc;
+                        HelmSeries<float>::eval2(za, zc, Ja, Ya, Jc, Yc);
+                        const float2 qa = reinterpret_cast<const float2 *>(s_q)[ja];
+                        const float2 qc = reinterpret_cast<const float2 *>(s_q)[jc];
+                        re = fmaf(-qa.x, Ya, fmaf(-qa.y, Ja, re));
+                        im = fmaf(qa.x, Ja, fmaf(-qa.y, Ya, im));
+                        re = fmaf(-qc.x, Yc, fmaf(-qc.y, Jc, re));
+                        im = fmaf(qc.x, Jc, fmaf(-qc.y, Yc, im));
+                    } else {
+                        one(ja);
+                        one(jc);
+                    }
+                }
             }
+            for (; v < v1; ++v) one(runs.at(v));
             const int o = oix[t];
             const int oi = a.out_idx ? a.out_idx[tb + o] : tb + o;
             C2 r;
