@@ -723,6 +723,9 @@ p2p_r_kernel(const P2PArgs<T> a) {
 #ifndef P2P_HELM_PAIR
 #define P2P_HELM_PAIR 1  // fp32 Helmholtz: two sources per step, series packed in f32x2
 #endif
+#ifndef P2P_BOX3_HELM_PAIR
+#define P2P_BOX3_HELM_PAIR 1  // 3D Helmholtz fp32: two targets per thread
+#endif
 #ifndef P2P_DENSE_MINB
 #define P2P_DENSE_MINB 0  // > 0: register cap via min resident CTAs for the TPI = 2 instances (experiments)
 #endif
@@ -1304,6 +1307,38 @@ __device__ __forceinline__ float rsq_approx(float x) {
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+// fp32 Helmholtz 3D, two targets per thread sharing each source load: distances in f32x2, then
+// per target rsqrt + sincos (3 MUFU) and the complex multiply-add.  Guarded in the loop.
+__device__ __forceinline__ void box3d_pairs2_helm_f32(const float4 *__restrict__ P, const float *__restrict__ QI,
+                                                      int s0, int s1, float x0, float y0, float z0, float x1,
+                                                      float y1, float z1, float eps2, float kh, float &re0,
+                                                      float &im0, float &re1, float &im1) {
+    const f2_t X = f2_pack(x0, x1), Y = f2_pack(y0, y1), Z = f2_pack(z0, z1);
+    re0 = im0 = re1 = im1 = 0.f;
+    for (int s = s0; s < s1; ++s) {
+        const float4 p = P[s];
+        const float qi = QI[s];
+        const f2_t dx = f2_sub(X, f2_pack(p.x, p.x)), dy = f2_sub(Y, f2_pack(p.y, p.y)), dz = f2_sub(Z, f2_pack(p.z, p.z));
+        float r20, r21;
+        f2_unpack(f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx))), r20, r21);
+        if (r20 >= eps2) {
+            const float rs = rsq_approx(r20);
+            float sn, cs;
+            __sincosf(kh * (r20 * rs), &sn, &cs);
+            const float gc = cs * rs, gs = sn * rs;
+            re0 = fmaf(p.w, gc, fmaf(-qi, gs, re0));
+            im0 = fmaf(p.w, gs, fmaf(qi, gc, im0));
+        }
+        if (r21 >= eps2) {
+            const float rs = rsq_approx(r21);
+            float sn, cs;
+            __sincosf(kh * (r21 * rs), &sn, &cs);
+            const float gc = cs * rs, gs = sn * rs;
+            re1 = fmaf(p.w, gc, fmaf(-qi, gs, re1));
+            im1 = fmaf(p.w, gs, fmaf(qi, gc, im1));
+        }
+    }
+}
 __device__ __forceinline__ void box3d_pairs2_f32(const float4 *__restrict__ P, int s0, int s1, float x0, float y0,
                                                  float z0, float x1, float y1, float z1, float &a0, float &a1) {
     const f2_t X = f2_pack(x0, x1), Y = f2_pack(y0, y1), Z = f2_pack(z0, z1);
@@ -1326,7 +1361,7 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
     __shared__ int s_box;
     constexpr int comps = HELM ? 2 : 1;
     // partial sums: 2 per thread for complex values and for the fp32 two-target units
-    const B3Carve c = box3d_carve(a.src_cap, (int)sizeof(T), comps, NT, (HELM || sizeof(T) == 4) ? 2 : 1);
+    const B3Carve c = box3d_carve(a.src_cap, (int)sizeof(T), comps, NT, box3d_parts(HELM, sizeof(T)));
     T *s_p = reinterpret_cast<T *>(smem + c.p);
     T *s_qi = reinterpret_cast<T *>(smem + c.qi);
     T *s_part = reinterpret_cast<T *>(smem + c.part);
@@ -1400,7 +1435,8 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
         __syncthreads();
         const int t0 = a.tgt_off[b], nt = a.tgt_off[b + 1] - t0;
         constexpr bool PAIR = sizeof(T) == 4 && !HELM;  // two targets per thread (f32x2)
-        const int nu = PAIR ? (nt + 1) / 2 : nt;        // work units (odd box: the last unit's second slot idle)
+        constexpr bool HPAIR = sizeof(T) == 4 && HELM && P2P_BOX3_HELM_PAIR;  // Helmholtz, two targets per thread
+        const int nu = (PAIR || HPAIR) ? (nt + 1) / 2 : nt;  // work units (odd box: the last unit's second slot idle)
         const int C = nu >= NT ? 1 : NT / nu;           // source chunks per unit
         auto finish = [&](int t, T re, T im) {
             const int64_t o = a.out_idx ? a.out_idx[t0 + t] : t0 + t;
@@ -1420,7 +1456,24 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
         for (int it = tid; it < nu * C; it += NT) {
             const int u = it % nu, ch = it / nu;
             const int c0 = (int)((int64_t)total * ch / C), c1 = (int)((int64_t)total * (ch + 1) / C);
-            if constexpr (PAIR) {
+            if constexpr (HPAIR) {
+                const int ta = 2 * u, tb = min(2 * u + 1, nt - 1);
+                const float *pa = reinterpret_cast<const float *>(a.tgt_p4) + 4 * (int64_t)(t0 + ta);
+                const float *pb = reinterpret_cast<const float *>(a.tgt_p4) + 4 * (int64_t)(t0 + tb);
+                float r0, i0, r1, i1;
+                box3d_pairs2_helm_f32(reinterpret_cast<const float4 *>(s_p), reinterpret_cast<const float *>(s_qi), c0,
+                                      c1, pa[0], pa[1], pa[2], pb[0], pb[1], pb[2], (float)a.eps2, (float)a.kh, r0, i0,
+                                      r1, i1);
+                if (C == 1) {
+                    finish(ta, (T)r0, (T)i0);
+                    if (tb != ta) finish(tb, (T)r1, (T)i1);
+                } else {
+                    s_part[4 * it] = (T)r0;
+                    s_part[4 * it + 1] = (T)i0;
+                    s_part[4 * it + 2] = (T)r1;
+                    s_part[4 * it + 3] = (T)i1;
+                }
+            } else if constexpr (PAIR) {
                 const int ta = 2 * u, tb = min(2 * u + 1, nt - 1);
                 const float *pa = reinterpret_cast<const float *>(a.tgt_p4) + 4 * (int64_t)(t0 + ta);
                 const float *pb = reinterpret_cast<const float *>(a.tgt_p4) + 4 * (int64_t)(t0 + tb);
@@ -1461,7 +1514,10 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
             for (int t = tid; t < nt; t += NT) {  // chunks summed in order
                 T re = (T)0, im = (T)0;
                 for (int ch = 0; ch < C; ++ch) {
-                    if constexpr (PAIR) {
+                    if constexpr (HPAIR) {
+                        re += s_part[4 * (ch * nu + t / 2) + 2 * (t & 1)];
+                        im += s_part[4 * (ch * nu + t / 2) + 2 * (t & 1) + 1];
+                    } else if constexpr (PAIR) {
                         re += s_part[2 * (ch * nu + t / 2) + (t & 1)];
                     } else {
                         re += s_part[comps * (ch * nu + t)];

@@ -141,6 +141,14 @@ inline int box3d_threads(int kernel) { return kernel == P2P_KERNEL_HELMHOLTZ_3D 
 P2P_HD inline int kernel_dim(int kernel) { return kernel >= P2P_KERNEL_LAPLACE_3D ? 3 : 2; }
 // 3D box kernel shared memory: staged sources (x, y, z, q_re) and q_im (complex), per-thread
 // partial sums (comps values), and per neighbour box its source start, prefix and shift code.
+#ifndef P2P_BOX3_HELM_PAIR
+#define P2P_BOX3_HELM_PAIR 1
+#endif
+// partial sums per thread of the 3D box kernel: fp32 Laplace 2 (two targets), complex 2 (re, im),
+// fp32 Helmholtz with two targets per thread 4
+P2P_HD inline int box3d_parts(bool helm, int e) {
+    return helm ? ((e == 4 && P2P_BOX3_HELM_PAIR) ? 4 : 2) : (e == 4 ? 2 : 1);
+}
 struct B3Carve {
     int p, qi, part, nbs, pre, nbd, total;
 };

@@ -525,7 +525,7 @@ void build_host_plan_3d(const p2p_plan_desc &d, HostPlan &hp) {
     hp.src_cap = max27;
     hp.nt = box3d_threads(d.kernel);
     const int e = d.precision == P2P_FP32 ? 4 : 8, comps = d.kernel == P2P_KERNEL_HELMHOLTZ_3D ? 2 : 1;
-    hp.smem_bytes = box3d_smem(hp.src_cap, e, comps, hp.nt, (comps == 2 || e == 4) ? 2 : 1);
+    hp.smem_bytes = box3d_smem(hp.src_cap, e, comps, hp.nt, box3d_parts(comps == 2, e));
     if (hp.smem_bytes > kSmemLimit)
         fail(P2P_ERROR_NOT_SUPPORTED, "3D: a box's 27 neighbours hold " + std::to_string(max27) +
                                           " sources (> shared memory); use a deeper level");
