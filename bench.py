@@ -4,13 +4,16 @@ P2P pair-interactions/s; roofline fraction).
 
 One *step* = one apply of the whole hot path (SURVEY.md §8(a) apply rows:
 [halo weight exchange] -> P2P kernel) over each config of the workload, with
-inputs resident in HBM.  Default workload = BASELINE.json configs[1], the
-density sweep: 1e6 points at 16, 32 and 64 points per box, TILED layout
-(redundant only on the tile ring), fp32 (the headline), Morton plan order;
-the NR and R layouts and fp64 are reported under "extras".
+inputs resident in HBM.  Default workload = BASELINE.json configs[3], the
+configuration the metric is quoted on at 1/2/4/8 B200: the 2e7-point
+surface-like cloud (a 1250 x 1000-box plate at L = 12, 16 points per box),
+TILED layout (redundant only on the tile ring), fp32 (the headline), Morton
+plan order; the same step in fp64 is the "fp64" field, the NR and R layouts
+are reported under "extras".
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-  torchrun --nproc-per-node N bench.py --gpus N ...   (strong scaling, NCCL halo exchange)
+  torchrun --nproc-per-node N bench.py --gpus N ...   (strong scaling: the same global problem
+                                                       Morton-range sharded, NCCL halo exchange)
 
 Timing: W warm-up steps, then K steps timed with CUDA events on the apply
 stream, L2 flushed (256 MiB write) between steps, barrier + synchronize on
@@ -36,9 +39,9 @@ sys.path.insert(0, ROOT)
 from paper_2403_01596_b200 import workloads as W  # noqa: E402
 
 WORKLOADS = {
-    "density_1e6": ["d16_1e6", "d32_1e6", "d64_1e6"],           # configs[1] (headline)
+    "density_1e6": ["d16_1e6", "d32_1e6", "d64_1e6"],           # configs[1]
     "lowdensity_1e7": ["lowd025_1e7", "lowd1_1e7", "lowd2_1e7", "lowd4_1e7"],  # configs[2]
-    "surface_2e7": ["surf_2e7"],                                # configs[3]
+    "surface_2e7": ["surf_2e7"],                                # configs[3] (headline, default)
     "d32_7e7": ["d32_7e7"],                                     # configs[4]
     "tiny": ["tiny"],                                           # configs[0]
     "helmholtz_1e6": ["d16_1e6", "d4_1e6"],                     # NEXT-3: 2D Helmholtz, leaf = lambda/4
@@ -51,8 +54,24 @@ DEFAULT_KERNEL = {"helmholtz_1e6": "helmholtz", "contour_helmholtz": "helmholtz"
                   "cube3d_helmholtz": "helmholtz3d"}
 MUFU_PER_PAIR_3D = {"laplace3d": 1, "helmholtz3d": 3}  # RSQ; RSQ + SIN + COS
 METRIC = "P2P pair-interactions/s"
-MUFU_LG2_PER_CLK_PER_SM = 16       # SFU issue rate (checked by libp2p_peaks)
 SM_COUNT = 148
+PEAKS_JSON = os.path.join(ROOT, "profiles", "r02_peaks.json")  # tools/peaks.py on a B200 (libp2p_peaks.so)
+FP64_DP_OPS_PER_PAIR = 17  # r^2 + guard + accumulate (6) + the table-driven log (11)
+
+
+def _measured_peaks():
+    """MUFU.LG2 and DFMA rates per clock per SM measured by tools/peaks.py (committed JSON); the
+    nominal 16 lg2 / 64 DFMA per clk per SM (B200_PROFILING.md) if the file is absent."""
+    try:
+        d = json.load(open(PEAKS_JSON))
+        return (d["mufu_lg2"]["per_clk_per_sm"], d["dfma"]["per_clk_per_sm"] / 2.0,
+                f"profiles/r02_peaks.json (measured {d['when'][:10]}: {d['mufu_lg2']['per_clk_per_sm']:.2f} "
+                f"lg2/clk/SM, {d['dfma']['per_clk_per_sm'] / 2:.2f} DFMA/clk/SM)")
+    except Exception:
+        return 16.0, 64.0, "nominal 16 lg2 / 64 DFMA per clk per SM (profiles/r02_peaks.json absent)"
+
+
+MUFU_LG2_PER_CLK_PER_SM, DFMA_PER_CLK_PER_SM, PEAK_BASIS = _measured_peaks()
 
 
 def parse():
@@ -61,14 +80,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="density_1e6", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="surface_2e7", choices=sorted(WORKLOADS))
     ap.add_argument("--layout", default="tiled", choices=["nr", "r", "tiled"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--kind", default="iid", choices=["iid", "stratified"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = each config's plate widened N x (same points per box, N x the "
-                         "points, per-GPU work fixed), Morton-range sharded with the halo exchange; "
-                         "strong = the same global problem split N ways")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N > 1: strong = the same global problem Morton-range split N ways (SURVEY §8(d) "
+                         "E_P = T_1 / (P T_P)); weak = each config's plate widened N x (same points per box)")
     ap.add_argument("--no-extras", action="store_true", help="skip the R / fp64 detail lines")
     ap.add_argument("--build", choices=["device", "host"], default="device",
                     help="N = 1 plans: built on the GPU (p2p_plan_create_device) or by the host builder")
@@ -462,18 +480,13 @@ def main():
 
 
 def _owned_user_indices(pl, src, part, rank):
-    """User indices of the sources this rank owns (global plan range part[0, rank]..part[0, rank+1])."""
+    """User indices of the sources this rank owns (global plan range part[0, rank]..part[0, rank+1]):
+    the owned block of the local set (contiguous, plan_builder.cpp)."""
     gidx = pl.export("src_global")
     uidx = pl.export("src_perm")
     lo, hi = part[0, rank], part[0, rank + 1]
-    m = (gidx >= lo) & (gidx < hi)
-    owned = uidx[m]
-    # the local set may miss owned sources outside every tile region: rebuild from a full plan order
-    if len(owned) != hi - lo:
-        from paper_2403_01596_b200 import p2p
-        full = p2p.Plan(src, src[:1], level=pl.info["level"], device=-1)
-        owned = full.export("src_perm")[lo:hi]
-        full.close()
+    owned = uidx[(gidx >= lo) & (gidx < hi)]
+    assert len(owned) == hi - lo
     return owned
 
 

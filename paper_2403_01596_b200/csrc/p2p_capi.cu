@@ -46,7 +46,7 @@ struct p2p_plan_s {
     int device = -1;
     cudaStream_t stream = nullptr;
     // device arrays
-    DevBuf pi_src_xy, pi_tgt_xy, pi_nei_off, pi_nei_idx, pr_records, pr_slot, phi_user, halo_lidx, tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, send_idx;
+    DevBuf pi_src_xy, pi_tgt_xy, pi_nei_off, pi_nei_idx, pr_records, pr_slot, phi_user, paper_q, halo_lidx, tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
     DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uidx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, log_tab, tgt_ruv, tgt_pack_off, tile_tgt_base;
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
@@ -76,7 +76,7 @@ struct p2p_plan_s {
         device_bytes += (int64_t)bytes;
     }
     void release() {
-        DevBuf *all[] = {&pi_src_xy, &pi_tgt_xy, &pi_nei_off, &pi_nei_idx, &pr_records, &pr_slot, &phi_user, &halo_lidx, &tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
+        DevBuf *all[] = {&pi_src_xy, &pi_tgt_xy, &pi_nei_off, &pi_nei_idx, &pr_records, &pr_slot, &phi_user, &paper_q, &halo_lidx, &tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
                          &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uidx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi, &leaf_rng, &leaf_org, &ul_off, &ul_leaf,
@@ -354,11 +354,13 @@ void apply_paper(p2p_plan_s &P, const void *d_q, void *d_out, int order, int acc
     const double *q = (const double *)d_q;
     double *out = (double *)d_out;
     if (order == P2P_ORDER_PLAN) {
+        // scatter into a buffer of its own: d_q may be io_q itself (p2p_apply_host, plan order)
+        if (!P.paper_q.p) P.alloc(P.paper_q, (size_t)std::max<int64_t>(hp.n_src, 1) * sizeof(double));
         if (hp.n_src)
             p2p::dev::scatter_kernel<double><<<grid_for(hp.n_src), 256, 0, s>>>(
-                (const int32_t *)P.src_uidx.p, (const double *)d_q, (double *)P.io_q.p, hp.n_src, 0);
+                (const int32_t *)P.src_uidx.p, (const double *)d_q, (double *)P.paper_q.p, hp.n_src, 0);
         if (!P.phi_user.p) P.alloc(P.phi_user, (size_t)std::max<int64_t>(hp.n_tgt, 1) * sizeof(double));
-        q = (const double *)P.io_q.p;
+        q = (const double *)P.paper_q.p;
         out = (double *)P.phi_user.p;
     }
     const double eps2 = hp.eps * hp.eps;

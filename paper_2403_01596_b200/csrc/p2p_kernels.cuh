@@ -646,8 +646,9 @@ p2p_r_kernel(const P2PArgs<T> a) {
                 else hi = mid;
             }
             const typename V2<T>::type uv = a.tgt_uv[tb + t];
-            tu[t] = uv.x;
-            tv[t] = uv.y;
+            // fp32: the halo frame is the 3x3 block's corner, one box below and left (R17)
+            tu[t] = sizeof(T) == 4 ? uv.x + a.h : uv.x;
+            tv[t] = sizeof(T) == 4 ? uv.y + a.h : uv.y;
             tbx[t] = lo;
         }
         asm volatile(
@@ -1412,7 +1413,11 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
                 if (nb + step < 27 && s_pre[nb + step] <= i) nb += step;
             const int j = s_nbs[nb] + (i - s_pre[nb]);
             const int code = s_nbd[nb];
-            const T sx = (T)((code & 3) - 1), sy = (T)(((code >> 2) & 3) - 1), sz = (T)(((code >> 4) & 3) - 1);
+            // fp32: the frame is shifted by one box (x + 1, y + 1, z + 1): every target then sits
+            // >= 1 from the origin, so two staged coordinates either coincide or differ by
+            // >= 2^-24 > eps S, and the unguarded loop's r^2 = 0 check is the whole guard (R17)
+            constexpr int SH = sizeof(T) == 4 ? 0 : 1;
+            const T sx = (T)((code & 3) - SH), sy = (T)(((code >> 2) & 3) - SH), sz = (T)(((code >> 4) & 3) - SH);
             const int jq = a.src_idx ? a.src_idx[j] : j;
             T q, qi = (T)0;
             if constexpr (HELM) {
@@ -1458,8 +1463,10 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
             const int c0 = (int)((int64_t)total * ch / C), c1 = (int)((int64_t)total * (ch + 1) / C);
             if constexpr (HPAIR) {
                 const int ta = 2 * u, tb = min(2 * u + 1, nt - 1);
-                const float *pa = reinterpret_cast<const float *>(a.tgt_p4) + 4 * (int64_t)(t0 + ta);
-                const float *pb = reinterpret_cast<const float *>(a.tgt_p4) + 4 * (int64_t)(t0 + tb);
+                const float4 pa4 = reinterpret_cast<const float4 *>(a.tgt_p4)[t0 + ta];
+                const float4 pb4 = reinterpret_cast<const float4 *>(a.tgt_p4)[t0 + tb];
+                const float pa[3] = {pa4.x + 1.f, pa4.y + 1.f, pa4.z + 1.f};  // fp32 frame shift (R17)
+                const float pb[3] = {pb4.x + 1.f, pb4.y + 1.f, pb4.z + 1.f};
                 float r0, i0, r1, i1;
                 box3d_pairs2_helm_f32(reinterpret_cast<const float4 *>(s_p), reinterpret_cast<const float *>(s_qi), c0,
                                       c1, pa[0], pa[1], pa[2], pb[0], pb[1], pb[2], (float)a.eps2, (float)a.kh, r0, i0,
@@ -1475,8 +1482,10 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
                 }
             } else if constexpr (PAIR) {
                 const int ta = 2 * u, tb = min(2 * u + 1, nt - 1);
-                const float *pa = reinterpret_cast<const float *>(a.tgt_p4) + 4 * (int64_t)(t0 + ta);
-                const float *pb = reinterpret_cast<const float *>(a.tgt_p4) + 4 * (int64_t)(t0 + tb);
+                const float4 pa4 = reinterpret_cast<const float4 *>(a.tgt_p4)[t0 + ta];
+                const float4 pb4 = reinterpret_cast<const float4 *>(a.tgt_p4)[t0 + tb];
+                const float pa[3] = {pa4.x + 1.f, pa4.y + 1.f, pa4.z + 1.f};  // fp32 frame shift (R17)
+                const float pb[3] = {pb4.x + 1.f, pb4.y + 1.f, pb4.z + 1.f};
                 float r0, r1, dummy;
                 box3d_pairs2_f32(reinterpret_cast<const float4 *>(s_p), c0, c1, pa[0], pa[1], pa[2], pb[0], pb[1],
                                  pb[2], r0, r1);
@@ -1498,7 +1507,9 @@ __global__ void __launch_bounds__(NT) p2p_box3d_kernel(const P2PArgs<T> a) {
                     s_part[2 * it + 1] = (T)r1;
                 }
             } else {
-                const T *tp = a.tgt_p4 + 4 * (int64_t)(t0 + u);
+                const T *tq = a.tgt_p4 + 4 * (int64_t)(t0 + u);
+                constexpr T SH = sizeof(T) == 4 ? (T)1 : (T)0;  // fp32 frame shift (R17)
+                const T tp[3] = {tq[0] + SH, tq[1] + SH, tq[2] + SH};
                 T re = (T)0, im = (T)0;
                 box3d_pairs<T, HELM>(s_p, s_qi, c0, c1, tp[0], tp[1], tp[2], a.eps2, a.kh, re, im);
                 if (C == 1) {

@@ -824,6 +824,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
 
     // ---- partition: contiguous Morton ranges of tiles balanced by pair count.
     const int P = d.part_world, r = d.part_rank;
+    std::vector<int64_t> box_begin((size_t)P + 1);  // first box of each rank's Morton range
     {
         std::vector<int64_t> prefix((size_t)ntiles + 1, 0);
         for (int64_t i = 0; i < ntiles; ++i) prefix[i + 1] = prefix[i] + hp.tile_pairs_g[i];
@@ -839,7 +840,6 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             }
             hp.part_tile[q] = std::max<int64_t>(lo, hp.part_tile[q - 1]);
         }
-        std::vector<int64_t> box_begin((size_t)P + 1);
         for (int q = 0; q <= P; ++q) {
             if (q == 0) box_begin[q] = 0;
             else if (q == P || hp.part_tile[q] >= ntiles) box_begin[q] = hp.B;
@@ -869,7 +869,10 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             }
     };
 
-    // ---- local source set: all sources (P = 1) or those in the regions of the owned tiles.
+    // ---- local source set: all sources (P = 1), or those in the regions of the owned tiles
+    // plus every box of the owned Morton range, so that the owned sources -- the global plan
+    // range [part_src[r], part_src[r+1]) -- are one contiguous block of the local set (local
+    // order = global order) even where an owned box lies outside every owned tile region.
     hp.src_owned_begin = hp.part_src[r];
     hp.n_src_owned = hp.part_src[r + 1] - hp.part_src[r];
     hp.tgt_begin = hp.part_tgt[r];
@@ -887,6 +890,8 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             region_boxes(t, boxes);
             for (uint32_t m : boxes) mark[m] = 1;
         }
+        for (int64_t b = box_begin[r]; b < box_begin[r + 1]; ++b)
+            if (so[b + 1] > so[b]) mark[b] = 1;
         hp.src_off.assign((size_t)hp.B + 1, 0);
         hp.src_gidx.clear();
         for (int64_t b = 0; b < hp.B; ++b) {
@@ -926,6 +931,8 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             }
         }
         hp.n_halo = halo;
+        if (hp.n_src_local - halo != hp.n_src_owned)  // the dist applies copy owned weights as one block
+            fail(P2P_ERROR_LAYOUT_CORRUPT, "owned sources are not one contiguous block of the local set");
     }
     if (P > 1) {
         std::vector<uint32_t> boxes;
@@ -967,8 +974,12 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     }
 
     // ---- a5 R layout: per target box, its E1 sources packed contiguously in
-    // the 3x3 row order (dy outer, dx inner), coordinates relative to the
-    // target box origin, each box padded to an even count, each tile to 4.
+    // the 3x3 row order (dy outer, dx inner), each box padded to an even count,
+    // each tile to 4.  Coordinates are relative to the target box origin (fp64),
+    // or in fp32 to the corner of its 3x3 block, (ix - 1, iy - 1) h: every target
+    // then sits >= h from the frame origin, so two fp32 coordinates either
+    // coincide or differ by >= ulp(h/2) >= 2^-38 > eps, and the fast loop's
+    // r^2 = 0 check is the whole guard (R17).
     if (d.layout == P2P_LAYOUT_REDUNDANT) {
         const int64_t nlt = (int64_t)hp.tiles.size();
         std::vector<uint32_t> len((size_t)hp.B + 1, 0);
@@ -999,6 +1010,10 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
                     uint32_t ix, iy;
                     morton_decode((uint32_t)b, ix, iy);
                     double ox = ix * hp.h, oy = iy * hp.h;
+                    if (f32) {
+                        ox -= hp.h;
+                        oy -= hp.h;
+                    }
                     int64_t ent = hp.halo_off[b];
                     for (int dy = -1; dy <= 1; ++dy)
                         for (int dx = -1; dx <= 1; ++dx) {

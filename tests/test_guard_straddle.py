@@ -1,0 +1,141 @@
+"""The eps guard at its edge, on every kernel family x precision, vs the fp64 oracle.
+
+SPEC.md S:L153, S:L157 (a pair closer than eps = 1e-12 contributes 0) and PAPER.md P:L265
+(every other E1 pair is evaluated once).  Planted on top of a background cloud, next to a
+box corner (= a tile corner and, for the R and 3D layouts before round 2, their frame origin,
+where fp32 coordinates are finest):
+
+* a target exactly on the corner and one 1e-6 from it, each with a source 5e-13 away
+  (0 < r < eps: the oracle skips the pair);
+* fp64: a control source 4e-12 away (r > eps: the oracle counts it, ln(1/r) = 26.2);
+* fp32: a control 3e-5 away (4e-12 is below fp32's resolution of a coordinate >= h: the
+  fp32 path evaluates the operator on coordinates rounded once, R12 / R17).
+
+Gates as tests/test_gpu_parity.py: relative L2 1e-5 (fp32) / 1e-12 (fp64), plus each planted
+target's own value (whose guarded pair alone would add ~28 if counted) element-wise."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2403_01596_b200 import p2p
+from paper_2403_01596_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+TOL = {"fp32": 1e-5, "fp64": 1e-12}
+TOL_EL = {"fp32": 2e-5, "fp64": 1e-12}
+
+
+def planted(dim, prec, corner=0.5):
+    """(targets, sources, weights) to append: two targets at/near a box corner, a guarded
+    source next to each, one control source."""
+    c = np.full(dim, corner)
+    e0 = np.eye(dim)[0]
+    t = np.stack([c, c + 1e-6])
+    guard = np.stack([c + 5e-13 * np.ones(dim) / np.sqrt(dim), c + 1e-6 + 5e-13 * e0])
+    ctl = (c + 1e-6 + np.eye(dim)[1] * (4e-12 if prec == "fp64" else 3e-5))[None]
+    return t, np.concatenate([guard, ctl]), np.array([1.0, -1.0, 0.75])
+
+
+def problem(dim, prec):
+    s, t, q = W.make_problem("tiny3d" if dim == 3 else "tiny")
+    pt, ps, pq = planted(dim, prec)
+    return np.concatenate([s, ps]), np.concatenate([t, pt]), np.concatenate([q, pq]), len(t)
+
+
+def run(pl, q, complex_w=False):
+    dt = pl.torch_dtype
+    out = pl.apply(torch.as_tensor(q, dtype=dt, device="cuda"), order="user")
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    return got.astype(np.complex128) if complex_w else got.astype(np.float64)
+
+
+def gate(got, ref, bound, prec, first_planted):
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= TOL[prec], err
+    d = np.abs(got - ref)
+    assert np.all(d <= TOL_EL[prec] * bound + 1e-300), np.max(d / bound)
+    # the planted targets themselves (a counted guard pair would add ~28)
+    assert np.all(d[first_planted:] <= TOL_EL[prec] * bound[first_planted:]), d[first_planted:]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("layout", ["nr", "r", "tiled", "tiled_sparse"])
+def test_guard_straddle_laplace2d(layout, prec):
+    src, tgt, q, k = problem(2, prec)
+    level = 7 if layout == "tiled_sparse" else 4  # ~0.25 per box: the TILED lean (flattened) path
+    with p2p.Plan(src, tgt, level=level, layout=layout.split("_")[0], precision=prec) as pl:
+        got = run(pl, q)
+    ref, _ = oracle.direct(src, q, tgt, level)
+    bound, _ = oracle.direct(src, np.abs(q), tgt, level)
+    gate(got, ref, bound, prec, k)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_guard_straddle_device_built(prec):
+    src, tgt, q, k = problem(2, prec)
+    with p2p.Plan(torch.as_tensor(src, device="cuda"), torch.as_tensor(tgt, device="cuda"), level=4,
+                  layout="tiled", precision=prec, build="device") as pl:
+        got = run(pl, q)
+    ref, _ = oracle.direct(src, q, tgt, 4)
+    bound, _ = oracle.direct(src, np.abs(q), tgt, 4)
+    gate(got, ref, bound, prec, k)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("layout", ["paper_i", "paper_r"])
+def test_guard_straddle_paper_layouts(layout, prec):
+    if prec == "fp32":
+        pytest.skip("the paper's kernels are fp64 (PAPER.md L98, L112)")
+    src, tgt, q, k = problem(2, prec)
+    with p2p.Plan(src, tgt, level=4, layout=layout, precision=prec) as pl:
+        got = run(pl, q)
+    ref, _ = oracle.direct(src, q, tgt, 4)
+    bound, _ = oracle.direct(src, np.abs(q), tgt, 4)
+    gate(got, ref, bound, prec, k)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_guard_straddle_adaptive(prec):
+    src, tgt, q, k = problem(2, prec)
+    with p2p.Plan(src, tgt, layout="adaptive", ct=12, l_max=8, precision=prec) as pl:
+        got = run(pl, q)
+    ref, _ = oracle.adaptive_direct(src, q, tgt, 12, 8)
+    bound, _ = oracle.adaptive_direct(src, np.abs(q), tgt, 12, 8)
+    gate(got, ref, bound, prec, k)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_guard_straddle_helmholtz2d(prec):
+    src, tgt, q, k = problem(2, prec)
+    qc = np.concatenate([W.weights_complex(len(src) - 3, 1), np.array([1.0 + 0.5j, -1.0, 0.75j])])
+    kappa = 8.0 * 1.5
+    with p2p.Plan(src, tgt, level=4, layout="tiled", precision=prec, kernel="helmholtz", wavenumber=kappa) as pl:
+        got = run(pl, qc, complex_w=True)
+    ref, _ = oracle.direct_helmholtz(src, qc, tgt, 4, kappa)
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= TOL[prec], err
+    # a counted guard pair would add |G(5e-13)| ~ 4 (the Y0 log singularity) to a planted target
+    assert np.all(np.abs(got[k:] - ref[k:]) <= (1e-3 if prec == "fp32" else 1e-10)), got[k:] - ref[k:]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("kernel", ["laplace3d", "helmholtz3d"])
+def test_guard_straddle_3d(kernel, prec):
+    src, tgt, q, k = problem(3, prec)
+    kw = {"kernel": kernel}
+    if kernel == "helmholtz3d":
+        q = q.astype(np.complex128) * (1 - 0.5j)
+        kw["wavenumber"] = 4.0 * np.pi / 2
+    with p2p.Plan(src, tgt, level=3, layout="nr", precision=prec, **kw) as pl:
+        got = run(pl, q, complex_w=kernel == "helmholtz3d")
+    okw = {} if kernel == "laplace3d" else {"kernel": "helmholtz", "kappa": kw["wavenumber"]}
+    ref, _ = oracle.direct_3d(src, q, tgt, 3, **okw)
+    bound, _ = oracle.direct_3d(src, np.abs(q), tgt, 3)  # sum |q| / (4 pi r) bounds |G q| too
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= TOL[prec], err
+    d = np.abs(got - ref)
+    # a counted guard pair would add 1 / (4 pi 5e-13) ~ 1.6e11 to a planted target
+    assert np.all(d[k:] <= 10 * TOL_EL[prec] * bound[k:]), (d[k:], bound[k:])

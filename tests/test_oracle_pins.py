@@ -289,3 +289,38 @@ def test_box_tmax_brute():
         cs = np.bincount(cell(src[:, 1]) * S + cell(src[:, 0]), minlength=S * S)
         ct = np.bincount(cell(tgt[:, 1]) * S + cell(tgt[:, 0]), minlength=S * S)
         assert oracle.box_tmax(src, tgt, L) == max(cs.max(), ct.max())
+
+
+# ---------------------------------------------------------------- plan-indexing oracle
+def test_sort_points_hand_computed():
+    """oracle_sort_points against a permutation and CSR offsets computed by hand
+    (tests/golden/sort_points_hand.json): ties within a box keep the original index order,
+    edge points follow the half-open rule, an exact duplicate stays after its twin."""
+    g = json.load(open(os.path.join(GOLD, "sort_points_hand.json")))
+    pts = np.array(g["points"])
+    for (ix, iy), code in zip(g["cells"], g["codes"]):
+        assert oracle.morton(ix, iy, g["level"]) == code
+    perm, off = oracle.sort_points(pts, g["level"])
+    assert perm.tolist() == g["perm"]
+    assert off.tolist() == g["offsets"]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_sort_points_spec_invariants(seed):
+    """SPEC.md L112 (partition: every index exactly once), L237 (offsets reconstruct the
+    per-box counts), L242 (insertion order inside a box) on random clouds with many ties."""
+    rng = np.random.default_rng(seed)
+    level = 4
+    S = 1 << (level - 1)
+    pts = rng.integers(0, 2 * S + 1, (500, 2)) / (2.0 * S)  # half the points on cell edges, some at 1.0
+    perm, off = oracle.sort_points(pts, level)
+    assert sorted(perm.tolist()) == list(range(len(pts)))
+    assert off[0] == 0 and off[-1] == len(pts) and np.all(np.diff(off) >= 0)
+    cell = np.minimum(np.floor(pts * S), S - 1).astype(int)
+    for b in range(S * S):
+        members = perm[off[b]:off[b + 1]]
+        assert np.all(np.diff(members) > 0)  # insertion (original index) order
+        for m in members:
+            assert oracle.morton(int(cell[m, 0]), int(cell[m, 1]), level) == b
+    counts = np.bincount([oracle.morton(int(x), int(y), level) for x, y in cell], minlength=S * S)
+    assert np.array_equal(np.diff(off), counts)

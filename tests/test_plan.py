@@ -236,6 +236,29 @@ def test_tiled_slots_and_items(level, precision, split, monkeypatch):
         pl.close()
 
 
+@pytest.mark.parametrize("layout", ["nr", "r", "tiled"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_owned_sources_contiguous_disjoint_clouds(layout, world):
+    """Sources and targets from different distributions (uniform sources, targets in the upper
+    right quarter): owned boxes without targets lie outside every owned tile region.  The owned
+    sources must still be one contiguous block of the local set, [owned_local_begin,
+    + n_src_owned), holding exactly the global plan range [part_src[r], part_src[r+1]) in order --
+    the distributed applies copy the owned weights there as one block."""
+    rng = np.random.default_rng(11)
+    src = rng.uniform(0, 1, (20000, 2))
+    tgt = rng.uniform(0.5, 1, (20000, 2))
+    for r in range(world):
+        pl = _plan(src, tgt, level=8, layout=layout, part_world=world, part_rank=r)
+        info = pl.info
+        part = pl.export("partition").reshape(2, world + 1)
+        sg = pl.export("src_global")
+        assert len(sg) == info["n_src_local"] == info["n_src_owned"] + info["n_halo"]
+        lo = np.searchsorted(sg, part[0, r])
+        np.testing.assert_array_equal(sg[lo:lo + info["n_src_owned"]], np.arange(part[0, r], part[0, r + 1]))
+        assert np.all(np.diff(sg) > 0)
+        pl.close()
+
+
 @pytest.mark.parametrize("world", [2, 3, 5])
 @pytest.mark.parametrize("level", [5, 7])
 def test_interior_launches_read_owned_sources_only(world, level):
