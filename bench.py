@@ -404,7 +404,7 @@ def main():
         achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak_mufu / m,
                     "unit": f"Gpair/s ({m} MUFU per pair)", "frac": achieved / (peak_mufu / m), "traffic": traffic,
-                    "peak_basis": f"{MUFU_LG2_PER_CLK_PER_SM} MUFU/clk/SM x {SM_COUNT} SMs x {peak_clk / 1e6:.0f} MHz "
+                    "peak_basis": f"{MUFU_LG2_PER_CLK_PER_SM:.2f} MUFU/clk/SM x {SM_COUNT} SMs x {peak_clk / 1e6:.0f} MHz "
                                   f"/ {m} per pair; DESIGN.md §9e"}
     elif args.kernel == "helmholtz":  # issue-bound: instructions per pair from ncu
         achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
@@ -420,8 +420,8 @@ def main():
         achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak_mufu, "unit": "Gpair/s (1 MUFU.LG2 per pair)",
                     "frac": achieved / peak_mufu, "traffic": traffic,
-                    "peak_basis": f"{MUFU_LG2_PER_CLK_PER_SM} MUFU.LG2/clk/SM x {SM_COUNT} SMs x "
-                                  f"{peak_clk / 1e6:.0f} MHz (sm_max); DESIGN.md §5"}
+                    "peak_basis": f"{MUFU_LG2_PER_CLK_PER_SM:.2f} MUFU.LG2/clk/SM x {SM_COUNT} SMs x "
+                                  f"{peak_clk / 1e6:.0f} MHz (sm_max); {PEAK_BASIS}"}
     else:
         achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s (algorithmic bytes)",
@@ -462,6 +462,8 @@ def main():
         "gpu_launches": args.steps * len(jobs) * (1 if world == 1 else 3),
         "roofline": roofline, "clocks": clocks, "e2e": e2e, "per_config": per_cfg,
     }
+    if world == 1 and args.precision == "fp32" and args.kernel == "laplace" and not args.profile:
+        out["fp64"] = _fp64_line(args, names, stream, dev, flush, peak_clk)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         out["cpu_baseline"] = {k: v for k, v in cpu_baseline(names, args.kind, args.cpu_seconds, kernel=args.kernel,
                                                              kh=args.kh).items()
@@ -477,6 +479,53 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _fp64_line(args, names, stream, dev, flush, peak_clk):
+    """The same step in fp64 (the paper's precision): plans built the same way,
+    K timed steps with the L2 flushed between them; roofline against the FP64 pipe at
+    FP64_DP_OPS_PER_PAIR DP operations per pair and the measured DFMA rate."""
+    import torch
+    from paper_2403_01596_b200 import p2p
+    plans, qs, outs, pairs = [], [], [], 0
+    for name in names:
+        cfg = W.CONFIGS[name]
+        src, tgt, q = W.make_problem(cfg, kind=args.kind)
+        kw = dict(level=cfg.level, layout=args.layout, precision="fp64", tile_log2=args.tile)
+        if args.build == "device" and args.layout in ("nr", "tiled"):
+            pl = p2p.Plan(torch.as_tensor(src, device=dev), torch.as_tensor(tgt, device=dev), device=dev.index,
+                          build="device", **kw)
+        else:
+            pl = p2p.Plan(src, tgt, device=dev.index, **kw)
+        plans.append(pl)
+        qs.append(torch.as_tensor(q[pl.export("src_perm")], dtype=torch.float64, device=dev))
+        outs.append(torch.empty(max(1, pl.info["n_tgt_local"]), dtype=torch.float64, device=dev))
+        pairs += pl.info["pairs"]
+
+    def step():
+        for pl, q, o in zip(plans, qs, outs):
+            p2p.p2p_apply(pl.handle, q.data_ptr(), o.data_ptr(), p2p.P2P_ORDER_PLAN, 0, stream.cuda_stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in ev:
+        flush.zero_()
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    for pl in plans:
+        pl.close()
+    achieved = pairs / (ms * 1e-3) / 1e9
+    peak = DFMA_PER_CLK_PER_SM * SM_COUNT * peak_clk / FP64_DP_OPS_PER_PAIR / 1e9
+    return {"value": pairs / (ms * 1e-3), "unit": "pair-interactions/s", "ms_per_step": ms, "dtype": "f64",
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "frac": achieved / peak,
+                         "unit": f"Gpair/s ({FP64_DP_OPS_PER_PAIR} DP ops per pair on the FP64 pipe)",
+                         "peak_basis": f"{DFMA_PER_CLK_PER_SM:.2f} DFMA/clk/SM x {SM_COUNT} SMs x "
+                                       f"{peak_clk / 1e6:.0f} MHz / {FP64_DP_OPS_PER_PAIR}; {PEAK_BASIS}"}}
 
 
 def _owned_user_indices(pl, src, part, rank):
@@ -542,14 +591,32 @@ def _helm_inst_per_pair(precision):
         return None
 
 
+def src_sha16():
+    """Hash of the operator's sources (csrc/ + include/): ties a committed ncu summary to the code
+    it was captured on."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in (os.path.join(ROOT, "paper_2403_01596_b200", "csrc"), os.path.join(ROOT, "include")):
+        for f in sorted(os.listdir(d)):
+            if f.endswith((".cu", ".cuh", ".cpp", ".h")):
+                h.update(f.encode())
+                h.update(open(os.path.join(d, f), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def _ncu_traffic(args, names):
-    """dram bytes per launch of the P2P kernel from the committed ncu --set full summary, if any."""
+    """dram bytes per launch of the P2P kernel from the committed ncu --set full summary
+    (profiles/ncu_summary.json, tools/ncu_traffic_json.py), only if it was captured on these
+    sources (same src_sha16); else None."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         data = json.load(open(path))
         key = f"{args.layout}_{args.precision}"
-        vals = [data[n][key]["dram_bytes"] for n in names if n in data and key in data[n]]
-        return float(sum(vals)) if len(vals) == len(names) else None
+        sha = src_sha16()
+        ents = [data[n][key] for n in names if n in data and key in data[n]]
+        if len(ents) != len(names) or any(e.get("src_sha16") != sha for e in ents):
+            return None
+        return float(sum(e["dram_bytes"] for e in ents))
     except Exception:
         return None
 

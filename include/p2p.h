@@ -251,6 +251,38 @@ p2p_status p2p_apply_dist_peer(p2p_plan plan, const void *d_q_owned, const void 
  * peers (every shard written before the call's copies run). */
 p2p_status p2p_gather_peer(p2p_plan plan, const void *const *d_peer_out, void *d_global, void *stream);
 
+/* Device-synchronised peer-memory exchange: the halo weight exchange (a6) and the result
+ * allgatherv (a11) as one-sided NVLink reads between the ranks' HBM, ordered by signal words
+ * in device memory -- no host barrier, no collective library; every step is a stream-ordered
+ * kernel, so an apply can be captured in a CUDA graph.  Set-up (once per plan, collective):
+ *   p2p_peer_buffers: allocates (first call) and returns this rank's published send buffer
+ *     (n_send weights), published result buffer (n_tgt_local results) and signal block
+ *     (zero-initialised, device-synchronised before return); export them with p2p_ipc_export.
+ *   p2p_peer_connect: every rank's three pointers as mapped in this process (HOST arrays of
+ *     part_world DEVICE pointers; p2p_ipc_open for the peers, this rank's own for part_rank) and
+ *     displ[o] = the offset of this rank's segment in rank o's send buffer (the sum of rank o's
+ *     halo_counts send entries for ranks < part_rank).  The caller must ensure every rank's
+ *     p2p_peer_buffers returned before any rank's first apply (e.g. the handle all-gather).
+ * p2p_apply_peer_sync: as p2p_apply_dist, with the halo pulled from the owners: publish this
+ *   rank's send buffer once every reader has finished the previous apply, pull the halo on an
+ *   internal stream (waiting for each owner's signal) while the interior tiles run, then the
+ *   boundary tiles.  Every rank must call it the same number of times (epochs are counted on
+ *   the device).  d_q_owned / d_out as p2p_apply_dist.
+ * p2p_gather (allgatherv, a11): d_global (device, n_tgt results, global plan
+ *   order) receives every rank's n_tgt_local results d_local (plan order); collective.
+ * p2p_peer_check: host-synchronous; P2P_ERROR_CUDA if a wait for a peer's signal gave up after
+ *   20 s (a peer that stopped calling), else SUCCESS.
+ * Applies on one plan must be serialised on one stream (the plan's workspace and signal words
+ * are shared).  part_world <= 16; NR, R and TILED 2D plans (Laplace, Helmholtz).
+ * Errors: INVALID_ARGUMENT (NULL pointers, no connect), NOT_SUPPORTED (other layouts), CUDA. */
+p2p_status p2p_peer_buffers(p2p_plan plan, void **d_pub_w, void **d_pub_o, void **d_sig);
+p2p_status p2p_peer_connect(p2p_plan plan, const void *const *peer_pub_w, const void *const *peer_pub_o,
+                            const void *const *peer_sig, const int64_t *displ);
+p2p_status p2p_apply_peer_sync(p2p_plan plan, const void *d_q_owned, void *d_out, int32_t accumulate,
+                               void *stream);
+p2p_status p2p_gather(p2p_plan plan, const void *d_local, void *d_global, void *stream);
+p2p_status p2p_peer_check(p2p_plan plan);
+
 /* CUDA IPC for p2p_apply_dist_peer.  p2p_ipc_export: the 64-byte handle (host buffer) of the
  * allocation holding d_ptr and d_ptr's byte offset in it (pointers from sub-allocating
  * allocators, e.g. torch's, are fine).  p2p_ipc_open: map a peer's handle on `device` and

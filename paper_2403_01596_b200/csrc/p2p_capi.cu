@@ -52,6 +52,14 @@ struct p2p_plan_s {
     DevBuf q_local, phi, io_q, io_out, queue;  // workspace
     DevBuf leaf_rng, leaf_org, ul_off, ul_leaf, src_cell, tgt_cell;  // ADAPTIVE (NEXT-4)
     DevBuf halo_owner, halo_oidx;                // peer-memory halo: owner rank, owner-local index per halo slot
+    struct PeerSync {                            // device-synchronised peer exchange (p2p_apply_peer_sync, p2p_gather)
+        DevBuf pub_w, pub_o, sig, ctr, err, oidx_w, seg_o;
+        void *pub_w_peer[16] = {}, *pub_o_peer[16] = {}, *sig_peer[16] = {};
+        unsigned readers_w = 0, owners_w = 0, all = 0;
+        bool connected = false;
+        cudaStream_t side = nullptr;
+        cudaEvent_t ev_pub = nullptr, ev_pull = nullptr;
+    } peer;
     int grid = 0;                                // persistent CTAs per launch
     int64_t occ_sms = 1;                         // resident CTAs per SM x SMs (grid cap of a launch)
     unsigned long long *trace = nullptr;         // diagnostics: per-tile timeline buffer (device)
@@ -81,7 +89,14 @@ struct p2p_plan_s {
                          &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uidx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
                          &tgt_pack_off, &tile_tgt_base, &q_local, &phi, &leaf_rng, &leaf_org, &ul_off, &ul_leaf,
                          &src_cell, &tgt_cell, &halo_owner, &halo_oidx,
-                         &io_q, &io_out, &queue};
+                         &io_q, &io_out, &queue, &peer.pub_w, &peer.pub_o, &peer.sig, &peer.ctr, &peer.err,
+                         &peer.oidx_w, &peer.seg_o};
+        if (peer.ev_pub) cudaEventDestroy(peer.ev_pub);
+        if (peer.ev_pull) cudaEventDestroy(peer.ev_pull);
+        if (peer.side) cudaStreamDestroy(peer.side);
+        peer.ev_pub = peer.ev_pull = nullptr;
+        peer.side = nullptr;
+        peer.connected = false;
         for (DevBuf *b : all) {
             if (b->p) cudaFree(b->p);
             b->p = nullptr;
@@ -1215,6 +1230,180 @@ p2p_status p2p_gather_peer(p2p_plan P, const void *const *d_peer_out, void *d_gl
                "gather_peer copy");
         }
     });
+}
+
+// ---- device-synchronised peer exchange (include/p2p.h p2p_peer_buffers .. p2p_gather)
+p2p_status p2p_peer_buffers(p2p_plan P, void **d_pub_w, void **d_pub_o, void **d_sig) {
+    if (!P || !d_pub_w || !d_pub_o || !d_sig) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL pointer");
+    if (P->hp.part_world > 16) return set_error(P2P_ERROR_INVALID_ARGUMENT, "part_world > 16");
+    if (P->hp.layout == P2P_LAYOUT_ADAPTIVE || P->hp.layout == P2P_LAYOUT_PAPER_INDEXING ||
+        P->hp.layout == P2P_LAYOUT_PAPER_REPETITION || P->hp.kernel == P2P_KERNEL_LAPLACE_3D ||
+        P->hp.kernel == P2P_KERNEL_HELMHOLTZ_3D)
+        return set_error(P2P_ERROR_NOT_SUPPORTED, "peer exchange: NR, R and TILED 2D plans");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        auto &ps = P->peer;
+        const p2p::HostPlan &hp = P->hp;
+        const size_t el = (size_t)P->elem * P->comps;
+        if (!ps.sig.p) {
+            P->alloc(ps.pub_w, (size_t)std::max<int64_t>(hp.n_send, 1) * el);
+            P->alloc(ps.pub_o, (size_t)std::max<int64_t>(hp.n_tgt_local, 1) * el);
+            P->alloc(ps.sig, p2p::dev::kSigWords * sizeof(unsigned long long));
+            P->alloc(ps.ctr, 4 * sizeof(unsigned));
+            P->alloc(ps.err, sizeof(int));
+            ck(cudaMemset(ps.sig.p, 0, ps.sig.bytes), "peer signal init");
+            ck(cudaMemset(ps.ctr.p, 0, ps.ctr.bytes), "peer counter init");
+            ck(cudaMemset(ps.err.p, 0, ps.err.bytes), "peer error init");
+            ck(cudaDeviceSynchronize(), "peer buffers");  // zeroed before any peer can map them
+        }
+        *d_pub_w = ps.pub_w.p;
+        *d_pub_o = ps.pub_o.p;
+        *d_sig = ps.sig.p;
+    });
+}
+
+p2p_status p2p_peer_connect(p2p_plan P, const void *const *peer_pub_w, const void *const *peer_pub_o,
+                            const void *const *peer_sig, const int64_t *displ) {
+    if (!P || !peer_pub_w || !peer_pub_o || !peer_sig || !displ)
+        return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL pointer");
+    if (!P->peer.sig.p) return set_error(P2P_ERROR_INVALID_ARGUMENT, "p2p_peer_buffers first");
+    return guarded([&] {
+        DeviceGuard g(P->device);
+        auto &ps = P->peer;
+        const p2p::HostPlan &hp = P->hp;
+        const int W = hp.part_world, me = hp.part_rank;
+        ps.readers_w = ps.owners_w = 0;
+        ps.all = W >= 32 ? ~0u : (1u << W) - 1u;
+        std::vector<int64_t> base((size_t)W + 1, 0);
+        for (int r = 0; r < W; ++r) {
+            if (!peer_pub_w[r] || !peer_pub_o[r] || !peer_sig[r])
+                throw p2p::Error(P2P_ERROR_INVALID_ARGUMENT, "NULL peer pointer");
+            ps.pub_w_peer[r] = const_cast<void *>(peer_pub_w[r]);
+            ps.pub_o_peer[r] = const_cast<void *>(peer_pub_o[r]);
+            ps.sig_peer[r] = const_cast<void *>(peer_sig[r]);
+            if (r != me && hp.send_counts[r] > 0) ps.readers_w |= 1u << r;
+            if (r != me && hp.recv_counts[r] > 0) ps.owners_w |= 1u << r;
+            base[r + 1] = base[r] + hp.recv_counts[r];
+        }
+        // per halo slot: its index in the owner's published send buffer (the owner packs, per
+        // reader, that reader's halo in the reader's order -- the all-to-all layout)
+        std::vector<int32_t> oidx((size_t)hp.n_halo);
+        for (int o = 0, h = 0; o < W; ++o)
+            for (int64_t k = 0; k < hp.recv_counts[o]; ++k, ++h) oidx[h] = (int32_t)(displ[o] + k);
+        if (ps.oidx_w.p) cudaFree(ps.oidx_w.p), ps.oidx_w = DevBuf{};
+        if (ps.seg_o.p) cudaFree(ps.seg_o.p), ps.seg_o = DevBuf{};
+        P->upload(ps.oidx_w, oidx);
+        P->upload(ps.seg_o, hp.part_tgt);
+        ck(cudaStreamSynchronize(P->stream), "peer connect upload");
+        if (!ps.side) ck(cudaStreamCreateWithFlags(&ps.side, cudaStreamNonBlocking), "peer side stream");
+        if (!ps.ev_pub) ck(cudaEventCreateWithFlags(&ps.ev_pub, cudaEventDisableTiming), "peer event");
+        if (!ps.ev_pull) ck(cudaEventCreateWithFlags(&ps.ev_pull, cudaEventDisableTiming), "peer event");
+        ps.connected = true;
+    });
+}
+
+extern "C++" {
+namespace {
+template <typename T, typename V>
+void apply_peer_sync_impl(p2p_plan_s &P, const void *d_q_owned, void *d_out, int accumulate, cudaStream_t s) {
+    namespace D = p2p::dev;
+    auto &ps = P.peer;
+    const p2p::HostPlan &hp = P.hp;
+    unsigned *ctr = (unsigned *)ps.ctr.p;
+    unsigned long long *sig = (unsigned long long *)ps.sig.p;
+    D::PeerPtrs<V> pub{};
+    D::SigPtrs sp{};
+    for (int r = 0; r < hp.part_world; ++r) {
+        pub.p[r] = (const V *)ps.pub_w_peer[r];
+        sp.p[r] = (unsigned long long *)ps.sig_peer[r];
+    }
+    // 1. publish this epoch's send buffer (after every reader is done with the previous one)
+    D::peer_publish_kernel<V><<<grid_for(std::max<int64_t>(hp.n_send, 1)), 256, 0, s>>>(
+        (const int32_t *)P.send_idx.p, (const V *)d_q_owned, (V *)ps.pub_w.p, hp.n_send, sig, 0, ps.readers_w, ctr,
+        (int *)ps.err.p);
+    ck(cudaEventRecord(ps.ev_pub, s), "peer event");
+    // 2. side stream: pull the halo straight from the owners' published buffers
+    ck(cudaStreamWaitEvent(ps.side, ps.ev_pub, 0), "peer fork");
+    D::peer_pull_kernel<V><<<grid_for(std::max<int64_t>(hp.n_halo, 1)), 256, 0, ps.side>>>(
+        pub, sp, sig, 0, hp.part_rank, ps.owners_w, (const int32_t *)P.halo_owner.p, (const int32_t *)ps.oidx_w.p,
+        nullptr, 0, (const int32_t *)P.halo_lidx.p, (V *)P.q_local.p, hp.n_halo, ctr + 1, (int *)ps.err.p);
+    ck(cudaEventRecord(ps.ev_pull, ps.side), "peer event");
+    // 3. interior tiles meanwhile; 4. boundary tiles once the halo is in
+    apply_dist_interior_impl<T>(P, d_q_owned, d_out, accumulate, s);
+    ck(cudaStreamWaitEvent(s, ps.ev_pull, 0), "peer join");
+    if (hp.layout == P2P_LAYOUT_TILED)
+        launch_p2p<T>(P, (const T *)P.q_local.p, (T *)d_out, accumulate, s, false, hp.n_interior,
+                      (int64_t)hp.tiles.size());
+    else
+        launch_p2p<T>(P, (const T *)P.q_local.p, (T *)d_out, accumulate, s);
+    ck(cudaGetLastError(), "apply_peer_sync launch");
+}
+
+template <typename V>
+void gather_sync_impl(p2p_plan_s &P, const void *d_local, void *d_global, cudaStream_t s) {
+    namespace D = p2p::dev;
+    auto &ps = P.peer;
+    const p2p::HostPlan &hp = P.hp;
+    unsigned *ctr = (unsigned *)ps.ctr.p;
+    unsigned long long *sig = (unsigned long long *)ps.sig.p;
+    D::PeerPtrs<V> pub{};
+    D::SigPtrs sp{};
+    for (int r = 0; r < hp.part_world; ++r) {
+        pub.p[r] = (const V *)ps.pub_o_peer[r];
+        sp.p[r] = (unsigned long long *)ps.sig_peer[r];
+    }
+    D::peer_publish_kernel<V><<<grid_for(std::max<int64_t>(hp.n_tgt_local, 1)), 256, 0, s>>>(
+        nullptr, (const V *)d_local, (V *)ps.pub_o.p, hp.n_tgt_local, sig, 1, ps.all, ctr + 2, (int *)ps.err.p);
+    D::peer_pull_kernel<V><<<grid_for(std::max<int64_t>(hp.n_tgt, 1)), 256, 0, s>>>(
+        pub, sp, sig, 1, hp.part_rank, ps.all, nullptr, nullptr, (const int64_t *)ps.seg_o.p, hp.part_world, nullptr,
+        (V *)d_global, hp.n_tgt, ctr + 3, (int *)ps.err.p);
+    ck(cudaGetLastError(), "gather launch");
+}
+}  // namespace
+}  // extern "C++"
+
+p2p_status p2p_apply_peer_sync(p2p_plan P, const void *d_q_owned, void *d_out, int32_t accumulate, void *stream) {
+    if (!P || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or output");
+    if (P->hp.n_src_owned && !d_q_owned) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_q_owned");
+    if (!P->peer.connected) return set_error(P2P_ERROR_INVALID_ARGUMENT, "p2p_peer_connect first");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        const int a = accumulate ? 1 : 0;
+        if (P->elem == 4 && P->comps == 1) apply_peer_sync_impl<float, float>(*P, d_q_owned, d_out, a, s);
+        else if (P->elem == 4) apply_peer_sync_impl<float, float2>(*P, d_q_owned, d_out, a, s);
+        else if (P->comps == 1) apply_peer_sync_impl<double, double>(*P, d_q_owned, d_out, a, s);
+        else apply_peer_sync_impl<double, double2>(*P, d_q_owned, d_out, a, s);
+    });
+}
+
+p2p_status p2p_gather(p2p_plan P, const void *d_local, void *d_global, void *stream) {
+    if (!P || !d_global) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or output");
+    if (P->hp.n_tgt_local && !d_local) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_local");
+    if (!P->peer.connected) return set_error(P2P_ERROR_INVALID_ARGUMENT, "p2p_peer_connect first");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        cudaStream_t s = (cudaStream_t)stream;
+        if (P->elem == 4 && P->comps == 1) gather_sync_impl<float>(*P, d_local, d_global, s);
+        else if (P->elem == 4) gather_sync_impl<float2>(*P, d_local, d_global, s);
+        else if (P->comps == 1) gather_sync_impl<double>(*P, d_local, d_global, s);
+        else gather_sync_impl<double2>(*P, d_local, d_global, s);
+    });
+}
+
+p2p_status p2p_peer_check(p2p_plan P) {
+    if (!P) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan");
+    if (!P->peer.err.p) return P2P_SUCCESS;
+    int e = 0;
+    p2p_status st = guarded([&] {
+        DeviceGuard g(P->device);
+        ck(cudaMemcpy(&e, P->peer.err.p, sizeof(int), cudaMemcpyDeviceToHost), "peer error word");
+    });
+    if (st != P2P_SUCCESS) return st;
+    return e ? set_error(P2P_ERROR_CUDA, "peer exchange: a wait for a peer's signal timed out") : P2P_SUCCESS;
 }
 
 p2p_status p2p_ipc_export(const void *d_ptr, void *handle64, int64_t *offset) {

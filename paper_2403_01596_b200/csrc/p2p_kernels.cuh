@@ -646,9 +646,8 @@ p2p_r_kernel(const P2PArgs<T> a) {
                 else hi = mid;
             }
             const typename V2<T>::type uv = a.tgt_uv[tb + t];
-            // fp32: the halo frame is the 3x3 block's corner, one box below and left (R17)
-            tu[t] = sizeof(T) == 4 ? uv.x + a.h : uv.x;
-            tv[t] = sizeof(T) == 4 ? uv.y + a.h : uv.y;
+            tu[t] = uv.x;  // fp32: relative to the 3x3 block's corner, like the halo (R17)
+            tv[t] = uv.y;
             tbx[t] = lo;
         }
         asm volatile(
@@ -1831,6 +1830,102 @@ __global__ void halo_peer_kernel(PeerPtrs<T> peers, const int32_t *__restrict__ 
                                  const int32_t *__restrict__ lidx, T *__restrict__ q_local, int64_t n) {
     for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < n; h += (int64_t)gridDim.x * blockDim.x)
         q_local[lidx[h]] = peers.p[owner[h]][oidx[h]];
+}
+
+// ---- device-synchronised peer exchange (p2p_apply_peer_sync / p2p_gather; include/p2p.h).
+// Every rank owns a signal block in its own HBM, mapped by its peers (CUDA IPC; NVLink on a
+// node): [kSigReady + x] the epoch up to which it has published buffer x (0 = halo weights,
+// 1 = results), [kSigDone + x*16 + s] the epoch up to which reader s has finished reading it,
+// [kSigCount + x] its own epoch counter.  An owner publishes epoch e only after every reader has
+// finished e - 1; a reader reads only after the owner has published e.  Flags are written with
+// st.release.sys after a system-scope fence and polled with ld.acquire.sys; the peers' data is
+// read with ld.global.cv (never a stale L1 line).  No host synchronisation anywhere: the whole
+// exchange is stream-ordered kernels (graph-capturable).  A wait longer than kPeerTimeoutNs
+// sets the error word and gives up (a dead peer cannot hang the device).
+constexpr int kSigReady = 0, kSigCount = 2, kSigDone = 4, kSigWords = 4 + 2 * 16;
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+struct SigPtrs {
+    unsigned long long *p[16];
+};
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void wait_epoch(const unsigned long long *flag, unsigned long long e, int *err) {
+    const unsigned long long t0 = gtimer();
+    while (ld_acquire_sys(flag) < e) {
+        if (gtimer() - t0 > kPeerTimeoutNs) {
+            atomicExch(err, 1);
+            return;
+        }
+        __nanosleep(128);
+    }
+}
+// Publish buffer x for epoch e = counter + 1: wait for the readers in `readers` (bit mask) to be
+// done with e - 1, pub[i] = src[idx ? idx[i] : i], then (last CTA) counter = e and ready = e.
+template <typename V>
+__global__ void peer_publish_kernel(const int32_t *__restrict__ idx, const V *__restrict__ src, V *__restrict__ pub,
+                                    int64_t n, unsigned long long *sig, int x, unsigned readers, unsigned *ctr,
+                                    int *err) {
+    const unsigned long long e = sig[kSigCount + x] + 1;  // stable: only this kernel's last CTA writes it
+    if (threadIdx.x == 0)
+        for (int s = 0; s < 16; ++s)
+            if (readers >> s & 1u) wait_epoch(sig + kSigDone + 16 * x + s, e - 1, err);
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        pub[i] = src[idx ? idx[i] : i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(ctr, 1u) == gridDim.x - 1) {
+            *ctr = 0u;
+            sig[kSigCount + x] = e;
+            __threadfence_system();
+            st_release_sys(sig + kSigReady + x, e);
+        }
+    }
+}
+
+// Read epoch e (= this rank's counter, already advanced by its publish kernel) of the owners in
+// `owners`: dst[didx ? didx[h] : h] = pub[owner(h)][oidx(h)], where owner / oidx come from the
+// arrays or, without them, from `nseg` contiguous segments (seg_begin[r] .. seg_begin[r + 1]
+// read from rank r's buffer at offset h - seg_begin[r]); then (last CTA) done = e at every owner.
+template <typename V>
+__global__ void peer_pull_kernel(PeerPtrs<V> pub, SigPtrs sig, const unsigned long long *own_sig, int x, int me,
+                                 unsigned owners, const int32_t *__restrict__ owner, const int32_t *__restrict__ oidx,
+                                 const int64_t *__restrict__ seg_begin, int nseg, const int32_t *__restrict__ didx,
+                                 V *__restrict__ dst, int64_t n, unsigned *ctr, int *err) {
+    const unsigned long long e = own_sig[kSigCount + x];
+    if (threadIdx.x == 0)
+        for (int o = 0; o < 16; ++o)
+            if (owners >> o & 1u) wait_epoch(sig.p[o] + kSigReady + x, e, err);
+    __syncthreads();
+    for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < n; h += (int64_t)gridDim.x * blockDim.x) {
+        int o;
+        int64_t j;
+        if (owner) {
+            o = owner[h];
+            j = oidx[h];
+        } else {
+            o = 0;
+            while (o + 1 < nseg && seg_begin[o + 1] <= h) ++o;
+            j = h - seg_begin[o];
+        }
+        dst[didx ? didx[h] : h] = __ldcv(pub.p[o] + j);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(ctr, 1u) == gridDim.x - 1) {
+            *ctr = 0u;
+            for (int o = 0; o < 16; ++o)
+                if (owners >> o & 1u) st_release_sys(sig.p[o] + kSigDone + 16 * x + me, e);
+        }
+    }
 }
 
 template <typename T>

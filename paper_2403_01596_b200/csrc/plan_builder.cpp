@@ -954,20 +954,22 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     }
 
     // ---- a5 NR layout: box-local coordinates u = x - ix*h (exact in fp64 by Sterbenz).
-    auto fill_points = [&](auto &vec, const double *xy, const std::vector<int32_t> &uidx) {
+    // (fp32 R targets: relative to the corner of their 3x3 block, (ix - 1) h -- the R halo's frame,
+    // computed in fp64 and rounded once like the halo's sources, so a collocated pair is exactly 0)
+    auto fill_points = [&](auto &vec, const double *xy, const std::vector<int32_t> &uidx, int shift = 0) {
         int64_t n = (int64_t)uidx.size();
         vec.resize((size_t)(2 * n));
         parallel_for(n, [&](int64_t a, int64_t bnd) {
             for (int64_t i = a; i < bnd; ++i) {
                 double x = xy[2 * (int64_t)uidx[i]], y = xy[2 * (int64_t)uidx[i] + 1];
-                vec[2 * i] = (typename std::decay_t<decltype(vec)>::value_type)(x - cell_of(x, S) * hp.h);
-                vec[2 * i + 1] = (typename std::decay_t<decltype(vec)>::value_type)(y - cell_of(y, S) * hp.h);
+                vec[2 * i] = (typename std::decay_t<decltype(vec)>::value_type)(x - ((double)cell_of(x, S) - shift) * hp.h);
+                vec[2 * i + 1] = (typename std::decay_t<decltype(vec)>::value_type)(y - ((double)cell_of(y, S) - shift) * hp.h);
             }
         });
     };
     if (d.precision == P2P_FP32) {
         fill_points(hp.f32.src_uv, d.src_xy, hp.src_uidx);
-        fill_points(hp.f32.tgt_uv, d.tgt_xy, hp.tgt_uidx);
+        fill_points(hp.f32.tgt_uv, d.tgt_xy, hp.tgt_uidx, d.layout == P2P_LAYOUT_REDUNDANT ? 1 : 0);
     } else {
         fill_points(hp.f64.src_uv, d.src_xy, hp.src_uidx);
         fill_points(hp.f64.tgt_uv, d.tgt_xy, hp.tgt_uidx);

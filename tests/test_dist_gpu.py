@@ -1,8 +1,10 @@
-"""DistributedP2P end to end on the GPU (ranks share the box's GPU; gloo, host-staged exchange):
+"""DistributedP2P end to end on the GPU (NCCL when every rank has its own GPU; else the ranks share
+the box's GPU with a gloo, host-staged exchange):
 each rank exchanges halo weights (synchronously, and pipelined through exchange_async on a
 communication stream as bench.py does; and with the peer-memory halo, the owners' buffers read
 through CUDA IPC mappings), applies its partition, and gathers all targets; the gathered result
-must be bit-identical to the single-plan apply (same tiles, same sum order)."""
+must be bit-identical to the single-plan apply (same tiles, same sum order) and match the fp64
+oracle within the north_star gates."""
 import os
 import socket
 
@@ -31,19 +33,25 @@ def _worker(rank, world, port, level, prec, results, kernel="laplace"):
     from paper_2403_01596_b200 import workloads as W
     from paper_2403_01596_b200.dist import DistributedP2P
 
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    # NCCL (device tensors, the bench path) whenever every rank has a GPU of its own; otherwise
+    # the ranks share the box's GPU and the exchange is host-staged over gloo (test mode)
+    nccl = torch.cuda.device_count() >= world
+    dev = rank if nccl else 0
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl" if nccl else "gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world, **({"device_id": torch.device("cuda", dev)} if nccl else {}))
     try:
-        torch.cuda.set_device(0)
         src, tgt, q = W.make_problem(W.widened(W.CONFIGS["tiny"], 4))
         kw = {}
         if kernel == "helmholtz":  # complex weights through the same exchange (re, im pairs)
             q = W.weights_complex(len(src), 1)
             kw = dict(kernel="helmholtz", wavenumber=1.2 * (1 << (level - 1)))
-        dp = DistributedP2P(src, tgt, device=0, host_staged=True, level=level, layout="tiled", precision=prec, **kw)
+        dp = DistributedP2P(src, tgt, device=dev, host_staged=not nccl, level=level, layout="tiled", precision=prec,
+                            **kw)
         dt = dp.plan.torch_dtype
         lo, hi = dp.owned_source_range()
         full = p2p.Plan(src, tgt, level=level, device=-1)
-        q_owned = torch.as_tensor(q[full.export("src_perm")[lo:hi]], dtype=dt, device="cuda")
+        q_owned = torch.as_tensor(q[full.export("src_perm")[lo:hi]], dtype=dt, device=f"cuda:{dev}")
         full.close()
         out_sync = dp.apply(q_owned)
         comm = torch.cuda.Stream()
@@ -90,3 +98,14 @@ def test_distributed_apply_bit_identical(world, level, prec, kernel):
     assert np.array_equal(g_sync, ref)
     assert np.array_equal(g_async, ref)
     assert np.array_equal(g_peer, ref)
+    # and against the fp64 oracle itself (SURVEY §8(c) gates), global plan order
+    import oracle
+    with p2p.Plan(src, tgt, level=level, device=-1) as host:
+        tperm = host.export("tgt_perm")
+    if kernel == "helmholtz":
+        oref = oracle.direct_helmholtz(src, q, tgt, level, kw["wavenumber"])[0][tperm]
+    else:
+        oref = oracle.direct(src, q, tgt, level)[0][tperm]
+    tol = 1e-5 if prec == "fp32" else 1e-12
+    for g in (g_sync, g_async, g_peer):
+        assert np.linalg.norm(g - oref) / np.linalg.norm(oref) <= tol

@@ -29,12 +29,16 @@ TOL_EL = {"fp32": 2e-5, "fp64": 1e-12}
 
 def planted(dim, prec, corner=0.5):
     """(targets, sources, weights) to append: two targets at/near a box corner, a guarded
-    source next to each, one control source."""
+    source next to each, one control source.  3D fp32: the second target 1e-3 from the corner
+    and the control 1e-2 away -- 1/r magnifies the rounding of fp32 coordinates (relative
+    error ~ ulp(h) / r), so closer non-guarded pairs are beyond fp32's 1e-5 gate."""
     c = np.full(dim, corner)
     e0 = np.eye(dim)[0]
-    t = np.stack([c, c + 1e-6])
-    guard = np.stack([c + 5e-13 * np.ones(dim) / np.sqrt(dim), c + 1e-6 + 5e-13 * e0])
-    ctl = (c + 1e-6 + np.eye(dim)[1] * (4e-12 if prec == "fp64" else 3e-5))[None]
+    d_t = 1e-3 if (dim == 3 and prec == "fp32") else 1e-6
+    d_c = 4e-12 if prec == "fp64" else (1e-2 if dim == 3 else 3e-5)
+    t = np.stack([c, c + d_t])
+    guard = np.stack([c + 5e-13 * np.ones(dim) / np.sqrt(dim), c + d_t + 5e-13 * e0])
+    ctl = (c + d_t + np.eye(dim)[1] * d_c)[None]
     return t, np.concatenate([guard, ctl]), np.array([1.0, -1.0, 0.75])
 
 

@@ -12,6 +12,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from bench import src_sha16  # noqa: E402  (run it in the same gpurun call as the capture)
 OUT = os.path.join(ROOT, "profiles", "ncu_summary.json")
 FIELDS = {"dram_bytes_read": "dram__bytes_read.sum", "dram_bytes_write": "dram__bytes_write.sum",
           "duration_us_ncu": "gpu__time_duration.sum",
@@ -42,7 +44,7 @@ def main(argv):
         names = names.split(",")
         assert len(launches) >= len(names), (rep, len(launches), names)
         for name, r in zip(names, launches):
-            ent = {"kernel": r[idx["Kernel Name"]], "report": os.path.basename(rep)}
+            ent = {"kernel": r[idx["Kernel Name"]], "report": os.path.basename(rep), "src_sha16": src_sha16()}
             for f, m in FIELDS.items():
                 if m in idx and r[idx[m]] not in ("", "n/a"):
                     v = float(r[idx[m]].replace(",", ""))
