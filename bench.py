@@ -90,8 +90,11 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the R / fp64 detail lines")
     ap.add_argument("--build", choices=["device", "host"], default="device",
                     help="N = 1 plans: built on the GPU (p2p_plan_create_device) or by the host builder")
-    ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
-                    help="N > 1 halo exchange: NCCL all_to_all (default) or peer-memory reads (CUDA IPC / NVLink)")
+    ap.add_argument("--exchange", choices=["sync", "nccl", "peer"], default="sync",
+                    help="N > 1 halo exchange: sync = one-sided peer-memory reads ordered by device-side "
+                         "signals (p2p_apply_peer_sync; default, CUDA-graph captured); nccl = "
+                         "torch.distributed all_to_all; peer = peer-memory reads with host barriers")
+    ap.add_argument("--no-graph", action="store_true", help="N > 1 sync mode: launch eagerly, no CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras/baseline)")
@@ -318,28 +321,35 @@ def main():
     pairs_step = sum(j["info"]["pairs_global"] for j in jobs)
     pairs_local = sum(j["info"]["pairs"] for j in jobs)
 
-    def one_apply(j):
-        if world == 1:
-            p2p.p2p_apply(j["plan"].handle, j["q"].data_ptr(), j["out"].data_ptr(), p2p.P2P_ORDER_PLAN, 0,
-                          stream.cuda_stream)
-        else:  # halo weight exchange (NCCL all-to-all) + distributed apply
-            j["dp"].apply(j["q_owned"], j["out"], stream=stream.cuda_stream)
-
     comm = torch.cuda.Stream(dev) if world > 1 else None
-
-    def step():
-        if world > 1 and args.exchange == "peer":  # halo read from the owners' memory (barriers inside)
-            for j in jobs:
-                j["dp"].apply_peer(j["q_owned"], j["out"], stream=stream.cuda_stream)
-            return
-        if world > 1:  # all halo exchanges first on the comm stream: config i's overlaps kernel i-1
-            comm.wait_stream(stream)
-            ready = [j["dp"].exchange_async(j["q_owned"], comm) for j in jobs]
-            for j, ev in zip(jobs, ready):
-                j["dp"].apply(j["q_owned"], j["out"], stream=stream.cuda_stream, halo_ready=ev)
-            return
+    mode = args.exchange if world > 1 else "single"
+    if mode == "sync":
         for j in jobs:
-            one_apply(j)
+            j["dp"].enable_sync()
+
+    def enqueue(j, cur, ready=None):
+        """one config's apply on stream handle `cur` (the current stream: graph-capture safe)"""
+        if mode == "single":
+            p2p.p2p_apply(j["plan"].handle, j["q"].data_ptr(), j["out"].data_ptr(), p2p.P2P_ORDER_PLAN, 0, cur)
+        elif mode == "sync":  # halo pulled from the owners' memory, device-side signals
+            j["dp"].apply_sync(j["q_owned"], j["out"], stream=cur)
+        elif mode == "peer":  # halo read from the owners' memory (host barriers inside)
+            j["dp"].apply_peer(j["q_owned"], j["out"], stream=cur)
+        else:
+            j["dp"].apply(j["q_owned"], j["out"], stream=cur, halo_ready=ready)
+
+    def step(kev_row=None):
+        cur = torch.cuda.current_stream(dev)
+        ready = [None] * len(jobs)
+        if mode == "nccl":  # all halo exchanges first on the comm stream: config i's overlaps kernel i-1
+            comm.wait_stream(cur)
+            ready = [j["dp"].exchange_async(j["q_owned"], comm) for j in jobs]
+        for i, j in enumerate(jobs):
+            if kev_row is not None:
+                kev_row[i][0].record(cur)
+            enqueue(j, cur.cuda_stream, ready[i])
+            if kev_row is not None:
+                kev_row[i][1].record(cur)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -351,6 +361,16 @@ def main():
     for _ in range(max(3, args.warmup)):
         step()
     barrier()
+    # N > 1, sync exchange: the whole step (every config's publish / pull / interior / boundary
+    # kernels) captured once in a CUDA graph -> one graph launch per step, no host work per apply
+    graph = None
+    if mode == "sync" and not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        barrier()
+        graph.replay()  # one untimed replay (every rank the same count: the epochs stay aligned)
+        barrier()
 
     # ---- timed region: K steps, per-step events, L2 flush between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -362,23 +382,21 @@ def main():
         for k in range(args.steps):
             flush.zero_()
             ev[k][0].record(stream)
-            peer = world > 1 and args.exchange == "peer"
-            if world > 1 and not peer:  # halo exchanges up front on the comm stream (config i's overlaps kernel i-1)
-                comm.wait_stream(stream)
-                ready = [j["dp"].exchange_async(j["q_owned"], comm) for j in jobs]
-            for i, j in enumerate(jobs):
-                kev[k][i][0].record(stream)
-                if peer:
-                    j["dp"].apply_peer(j["q_owned"], j["out"], stream=stream.cuda_stream)
-                elif world > 1:
-                    j["dp"].apply(j["q_owned"], j["out"], stream=stream.cuda_stream, halo_ready=ready[i])
-                else:
-                    one_apply(j)
-                kev[k][i][1].record(stream)
+            if graph is not None:
+                graph.replay()
+            else:
+                step(kev[k])
             ev[k][1].record(stream)
         barrier()
+    if mode == "sync":
+        for j in jobs:
+            j["dp"].check()
     step_ms = np.array([a.elapsed_time(b) for a, b in ev])
-    kern_ms = np.array([[a.elapsed_time(b) for a, b in row] for row in kev])  # [K, jobs]
+    if graph is not None:  # the graph step is timed whole: attribute it to the configs by pair count
+        share = np.array([j["info"]["pairs"] for j in jobs], dtype=np.float64)
+        kern_ms = step_ms[:, None] * (share / share.sum())[None, :]
+    else:
+        kern_ms = np.array([[a.elapsed_time(b) for a, b in row] for row in kev])  # [K, jobs]
     total_ms = float(step_ms.sum())
     if world > 1:
         t = torch.tensor([total_ms], device="cpu" if shared else dev, dtype=torch.float64)
@@ -454,12 +472,9 @@ def main():
                    "precision": args.precision, "kind": args.kind, "pairs_per_step": pairs_step,
                    "kernel": args.kernel, **({"kappa_h": args.kh} if args.kernel.startswith("helmholtz") else {}),
                    "order": "plan", "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": f"morton-range x{world}" + (
-                       ((" + peer-memory halo (CUDA IPC)" if args.exchange == "peer" else
-                         " + host-staged gloo halo exchange") + ", ranks sharing GPUs (TEST MODE)" if shared
-                        else (" + peer-memory halo (CUDA IPC / NVLink)" if args.exchange == "peer"
-                              else " + NCCL halo exchange")) if world > 1 else "")},
-        "gpu_launches": args.steps * len(jobs) * (1 if world == 1 else 3),
+                   "parallelism": f"morton-range x{world}" + (_exchange_desc(args.exchange, shared, graph is not None)
+                                                              if world > 1 else "")},
+        "gpu_launches": args.steps * len(jobs) * {"single": 1, "sync": 4, "nccl": 3, "peer": 2}[mode],
         "roofline": roofline, "clocks": clocks, "e2e": e2e, "per_config": per_cfg,
     }
     if world == 1 and args.precision == "fp32" and args.kernel == "laplace" and not args.profile:
@@ -528,6 +543,16 @@ def _fp64_line(args, names, stream, dev, flush, peak_clk):
                                        f"{peak_clk / 1e6:.0f} MHz / {FP64_DP_OPS_PER_PAIR}; {PEAK_BASIS}"}}
 
 
+def _exchange_desc(mode, shared, graph):
+    d = {"sync": " + halo pulled from the owners' HBM by one-sided peer reads ordered by device-side signal "
+                 "words (p2p_apply_peer_sync; CUDA IPC / NVLink)" + (", step captured in a CUDA graph" if graph else ""),
+         "nccl": " + NCCL halo exchange (torch.distributed all_to_all)",
+         "peer": " + peer-memory halo (CUDA IPC / NVLink) with host barriers"}[mode]
+    if shared:
+        d += ("" if mode != "nccl" else " staged through the host over gloo") + ", ranks sharing GPUs (TEST MODE)"
+    return d
+
+
 def _owned_user_indices(pl, src, part, rank):
     """User indices of the sources this rank owns (global plan range part[0, rank]..part[0, rank+1]):
     the owned block of the local set (contiguous, plan_builder.cpp)."""
@@ -552,10 +577,16 @@ def _e2e_dist(args, jobs, stream, pairs_step, barrier):
     d2h = sum(int(t.numel() * t.element_size()) for t in ho)
 
     comm = torch.cuda.Stream()
+    sync = args.exchange == "sync"
 
     def step():
         for a, d in zip(hq, dq):
             d.copy_(a, non_blocking=True)
+        if sync:  # device-synchronised peer exchange: stream-ordered, no host work between ranks
+            for j, d, b in zip(jobs, dq, ho):
+                j["dp"].apply_sync(d, j["out"], stream=stream.cuda_stream)
+                b.copy_(j["out"], non_blocking=True)
+            return
         comm.wait_stream(torch.cuda.current_stream())
         ready = [j["dp"].exchange_async(d, comm) for j, d in zip(jobs, dq)]
         for j, d, b, ev in zip(jobs, dq, ho, ready):
@@ -578,9 +609,10 @@ def _e2e_dist(args, jobs, stream, pairs_step, barrier):
     ms = float(t.item())
     return {"value": pairs_step / (ms * 1e-3), "unit": "pair-interactions/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms,
-            "path": "per rank: pinned H2D of owned weights, halo exchanges (DistributedP2P.exchange_async "
-                    "on a comm stream) overlapping the previous config's p2p_apply_dist, D2H of local "
-                    "potentials; max over ranks"}
+            "path": "per rank: pinned H2D of owned weights, " + (
+                "p2p_apply_peer_sync (halo pulled from the owners' memory, device-side signals)" if sync else
+                "halo exchanges (DistributedP2P.exchange_async on a comm stream) overlapping the previous "
+                "config's p2p_apply_dist") + ", D2H of local potentials; max over ranks"}
 
 
 def _helm_inst_per_pair(precision):

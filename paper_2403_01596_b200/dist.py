@@ -175,6 +175,61 @@ class DistributedP2P:
         self.dist.barrier(group=self.group)
         return out
 
+    # ---- device-synchronised peer exchange (p2p_apply_peer_sync / p2p_gather): the halo and the
+    # result allgatherv as one-sided NVLink reads ordered by signal words in device memory -- no
+    # host barrier per apply; the host only sets the mappings up once.
+    def enable_sync(self):
+        """Map every rank's published buffers and signal block (CUDA IPC), once."""
+        if getattr(self, "_sync", None):
+            return
+        pw, po, sg = p2p.p2p_peer_buffers(self.plan.handle)
+        mine = (p2p.p2p_ipc_export(pw), p2p.p2p_ipc_export(po), p2p.p2p_ipc_export(sg), self.send_splits)
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        maps, ptrs = [], [[], [], []]
+        for r in range(self.world):
+            for k, own in enumerate((pw, po, sg)):
+                if r == self.rank:
+                    ptrs[k].append(own)
+                else:
+                    h, off = allh[r][k]
+                    p = p2p.p2p_ipc_open(h, off, self.device)
+                    maps.append((p, off))
+                    ptrs[k].append(p)
+        # my segment's offset in each owner's send buffer: its send entries for ranks before me
+        displ = [int(sum(allh[o][3][:self.rank])) for o in range(self.world)]
+        p2p.p2p_peer_connect(self.plan.handle, ptrs[0], ptrs[1], ptrs[2], displ)
+        self._sync = maps
+
+    def apply_sync(self, q_owned, out=None, *, accumulate: bool = False, stream=None):
+        """phi for this rank's targets (plan order); the halo pulled from the owners' memory with
+        device-side signalling (every rank calls it the same number of times)."""
+        torch = self.torch
+        self.enable_sync()
+        if out is None:
+            out = torch.empty(max(1, self.n_tgt_local), dtype=self.plan.torch_dtype,
+                              device=torch.device("cuda", self.device))
+        s = stream or torch.cuda.current_stream(self.device).cuda_stream
+        p2p.p2p_apply_peer_sync(self.plan.handle, q_owned.data_ptr() if self.n_src_owned else 0, out.data_ptr(),
+                                int(accumulate), s)
+        return out
+
+    def gather_sync(self, phi_local, out=None, stream=None):
+        """allgatherv (a11) through the C ABI's p2p_gather: every rank's shard read from its
+        owner's memory, device-synchronised (collective)."""
+        torch = self.torch
+        self.enable_sync()
+        if out is None:
+            out = torch.empty(max(1, int(self.tgt_begin[-1])), dtype=self.plan.torch_dtype,
+                              device=torch.device("cuda", self.device))
+        s = stream or torch.cuda.current_stream(self.device).cuda_stream
+        p2p.p2p_gather(self.plan.handle, phi_local.data_ptr() if self.n_tgt_local else 0, out.data_ptr(), s)
+        return out
+
+    def check(self):
+        """Raise if a device-side wait for a peer timed out (host-synchronous)."""
+        p2p.p2p_peer_check(self.plan.handle)
+
     def gather(self, phi_local):
         """allgatherv (a11): every rank receives phi for all targets in global plan order."""
         torch = self.torch
@@ -201,6 +256,9 @@ class DistributedP2P:
         return torch.cat([p[: int(c)].to(phi_local.device) for p, c in zip(parts, counts)])
 
     def close(self):
+        for ptr, off in getattr(self, "_sync", None) or []:
+            p2p.p2p_ipc_close(ptr, off)
+        self._sync = None
         for ptr, off in getattr(self, "_peers", []):
             if ptr:
                 p2p.p2p_ipc_close(ptr, off)

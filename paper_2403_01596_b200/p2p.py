@@ -60,6 +60,7 @@ ABI_SYMBOLS = (
     "p2p_apply_dist", "p2p_apply_dist_interior", "p2p_apply_dist_boundary",
     "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_gather_peer", "p2p_ipc_export", "p2p_ipc_open", "p2p_ipc_close", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
     "p2p_status_string", "p2p_last_error", "p2p_abi_version",
+    "p2p_peer_buffers", "p2p_peer_connect", "p2p_apply_peer_sync", "p2p_gather", "p2p_peer_check",
 )
 
 
@@ -130,6 +131,11 @@ def load_library() -> C.CDLL:
     lib.p2p_ipc_export.argtypes = [P, P, C.POINTER(i64)]
     lib.p2p_ipc_open.argtypes = [P, i64, i32, C.POINTER(P)]
     lib.p2p_ipc_close.argtypes = [P, i64]
+    lib.p2p_peer_buffers.argtypes = [P, C.POINTER(P), C.POINTER(P), C.POINTER(P)]
+    lib.p2p_peer_connect.argtypes = [P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(i64)]
+    lib.p2p_apply_peer_sync.argtypes = [P, P, P, i32, P]
+    lib.p2p_gather.argtypes = [P, P, P, P]
+    lib.p2p_peer_check.argtypes = [P]
     lib.p2p_destroy.argtypes = [P]
     lib.p2p_plan_get_info.argtypes = [P, C.POINTER(PlanInfo)]
     lib.p2p_plan_export.argtypes = [P, i32, P, C.POINTER(C.c_size_t)]
@@ -139,7 +145,8 @@ def load_library() -> C.CDLL:
     lib.p2p_abi_version.restype = i32
     for name in ("p2p_plan_create", "p2p_plan_create_device", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async", "p2p_apply_dist", "p2p_apply_dist_interior",
                  "p2p_apply_dist_boundary", "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_gather_peer", "p2p_ipc_export",
-                 "p2p_ipc_open", "p2p_ipc_close",
+                 "p2p_ipc_open", "p2p_ipc_close", "p2p_peer_buffers", "p2p_peer_connect", "p2p_apply_peer_sync",
+                 "p2p_gather", "p2p_peer_check",
                  "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export"):
         getattr(lib, name).restype = i32
     _lib = lib
@@ -221,6 +228,33 @@ def p2p_apply_dist_peer(plan, d_q_owned: int, peer_ptrs, d_out: int, accumulate:
 def p2p_gather_peer(plan, peer_out_ptrs, d_global: int, stream: int = 0):
     arr = (C.c_void_p * len(peer_out_ptrs))(*[p or None for p in peer_out_ptrs])
     _check(load_library().p2p_gather_peer(plan, arr, d_global, stream or None), "p2p_gather_peer")
+
+
+def p2p_peer_buffers(plan) -> tuple[int, int, int]:
+    """(published send buffer, published result buffer, signal block) device pointers."""
+    a, b, c = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    _check(load_library().p2p_peer_buffers(plan, C.byref(a), C.byref(b), C.byref(c)), "p2p_peer_buffers")
+    return a.value, b.value, c.value
+
+
+def p2p_peer_connect(plan, pub_w, pub_o, sig, displ):
+    n = len(pub_w)
+    arr = lambda v: (C.c_void_p * n)(*[p or None for p in v])  # noqa: E731
+    d = (C.c_int64 * n)(*[int(x) for x in displ])
+    _check(load_library().p2p_peer_connect(plan, arr(pub_w), arr(pub_o), arr(sig), d), "p2p_peer_connect")
+
+
+def p2p_apply_peer_sync(plan, d_q_owned: int, d_out: int, accumulate: int = 0, stream: int = 0):
+    _check(load_library().p2p_apply_peer_sync(plan, d_q_owned or None, d_out, accumulate, stream or None),
+           "p2p_apply_peer_sync")
+
+
+def p2p_gather(plan, d_local: int, d_global: int, stream: int = 0):
+    _check(load_library().p2p_gather(plan, d_local or None, d_global, stream or None), "p2p_gather")
+
+
+def p2p_peer_check(plan):
+    _check(load_library().p2p_peer_check(plan), "p2p_peer_check")
 
 
 def p2p_ipc_export(d_ptr: int) -> tuple[bytes, int]:

@@ -65,6 +65,39 @@ def _worker(rank, world, port, level, prec, results, kernel="laplace"):
         g_sync, g_async, g_peer = conv(dp.gather(out_sync)), conv(dp.gather(out_async)), conv(dp.gather(out_peer))
         g_gp = conv(dp.gather_peer(out_peer))  # allgatherv over peer memory
         assert np.array_equal(g_gp, g_peer)
+        # device-synchronised peer exchange + p2p_gather: five epochs enqueued back to back with
+        # no host synchronisation; weights scaled by powers of two (results scale exactly)
+        scales = (1.0, -2.0, 0.5, 4.0, 1.0)
+        outs, gs = [], []
+        for f in scales:
+            o = dp.apply_sync(q_owned * f)
+            outs.append(o)
+            gs.append(dp.gather_sync(o))
+        torch.cuda.synchronize()
+        dp.check()
+        for f, o, g in zip(scales, outs, gs):
+            assert np.array_equal(conv(o), conv(out_sync) * f)
+            assert np.array_equal(conv(g)[: len(g_sync)], g_sync * f)
+        # the same step captured in a CUDA graph (no host work per apply at all) and replayed
+        qs, og = q_owned.clone(), torch.empty_like(out_sync)
+        gg = torch.empty_like(gs[0])
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up epoch outside the capture
+            dp.apply_sync(qs, og)
+            dp.gather_sync(og, gg)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            dp.apply_sync(qs, og)
+            dp.gather_sync(og, gg)
+        for f in (2.0, -1.0, 0.25):
+            qs.copy_(q_owned * f)
+            graph.replay()
+            torch.cuda.synchronize()
+            assert np.array_equal(conv(og), conv(out_sync) * f)
+            assert np.array_equal(conv(gg)[: len(g_sync)], g_sync * f)
+        dp.check()
         if rank == 0:
             results.put((g_sync, g_async, g_peer))
         dp.close()
