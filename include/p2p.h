@@ -283,6 +283,35 @@ p2p_status p2p_apply_peer_sync(p2p_plan plan, const void *d_q_owned, void *d_out
 p2p_status p2p_gather(p2p_plan plan, const void *d_local, void *d_global, void *stream);
 p2p_status p2p_peer_check(p2p_plan plan);
 
+/* Partitioned plans from each rank's OWN points (north_star: "a one-time
+ * exchange distributes halo source points"): no rank ever holds the global point set.
+ *   1. p2p_box_counts: per-box counts of n points (host [n][2] in [0,1]^2) at leaf level `level`
+ *      -> counts[4^(level-1)] (Morton order, overwritten).  Every rank counts the points it
+ *      holds; the caller sums the counts over the ranks (an allreduce): the GLOBAL counts.
+ *   2. p2p_partition_route: from the global counts alone, the partition the global builder
+ *      would make, and for each passed point the bit mask of the ranks that need it (sources:
+ *      the owner of its box and every rank with an owned tile whose region (tile + one-box
+ *      ring) holds the box -- the halo; targets: the owner of its box).  desc: level > 0,
+ *      layout NR / R / TILED, part_world <= 32, part_rank = the caller, n_src / n_tgt /
+ *      src_xy / tgt_xy = the passed points (may be 0 / NULL); *_ids = their global ids
+ *      (distinct int64 per set: they fix the order of points inside a box, as the caller's
+ *      point index does for p2p_plan_create).
+ *   3. the caller sends every point (coordinates + id) to the ranks in its mask (an all-to-all);
+ *   4. p2p_plan_create_local: the partition's plan from what arrived -- every point of every
+ *      box the rank needs, once (else INVALID_ARGUMENT naming the box) -- with the same
+ *      desc fields and global counts.  The plan (tiles, local order, halo, send lists) equals
+ *      p2p_plan_create's with the global point set for this part_rank, so applies are
+ *      bit-identical.  ORDER_USER and the host-buffer applies are NOT_SUPPORTED on it (there is
+ *      no global user order on one rank); p2p_plan_export(SRC_PERM / TGT_PERM) give indices into
+ *      the passed arrays.  Host build only; `device` as p2p_plan_create. */
+p2p_status p2p_box_counts(int32_t level, int64_t n, const double *xy, int32_t *counts);
+p2p_status p2p_partition_route(const p2p_plan_desc *desc, const int64_t *src_ids, const int64_t *tgt_ids,
+                               const int32_t *src_counts, const int32_t *tgt_counts, int64_t n_src_global,
+                               int64_t n_tgt_global, uint32_t *src_mask, uint32_t *tgt_mask);
+p2p_status p2p_plan_create_local(const p2p_plan_desc *desc, const int64_t *src_ids, const int64_t *tgt_ids,
+                                 const int32_t *src_counts, const int32_t *tgt_counts, int64_t n_src_global,
+                                 int64_t n_tgt_global, p2p_plan *out);
+
 /* CUDA IPC for p2p_apply_dist_peer.  p2p_ipc_export: the 64-byte handle (host buffer) of the
  * allocation holding d_ptr and d_ptr's byte offset in it (pointers from sub-allocating
  * allocators, e.g. torch's, are fine).  p2p_ipc_open: map a peer's handle on `device` and

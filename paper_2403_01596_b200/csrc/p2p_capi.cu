@@ -1027,13 +1027,13 @@ void p2p_plan_desc_init(p2p_plan_desc *d) {
     d->part_rank = 0;
 }
 
-p2p_status p2p_plan_create(const p2p_plan_desc *desc, p2p_plan *out) {
+static p2p_status plan_create_common(const p2p_plan_desc *desc, const p2p::LocalInput *li, p2p_plan *out) {
     if (out) *out = nullptr;
     if (!desc || !out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL desc or out");
     std::unique_ptr<p2p_plan_s> P(new (std::nothrow) p2p_plan_s());
     if (!P) return set_error(P2P_ERROR_OUT_OF_MEMORY, "host allocation failed");
     p2p_status st = guarded([&] {
-        p2p::build_host_plan(*desc, P->hp);
+        p2p::build_host_plan(*desc, P->hp, li);
         P->device = desc->device;
         P->elem = desc->precision == P2P_FP32 ? 4 : 8;
         P->comps = (desc->kernel == P2P_KERNEL_HELMHOLTZ_2D || desc->kernel == P2P_KERNEL_HELMHOLTZ_3D) ? 2 : 1;
@@ -1058,6 +1058,47 @@ p2p_status p2p_plan_create(const p2p_plan_desc *desc, p2p_plan *out) {
     });
     if (st == P2P_SUCCESS) *out = P.release();
     return st;
+}
+
+p2p_status p2p_plan_create(const p2p_plan_desc *desc, p2p_plan *out) { return plan_create_common(desc, nullptr, out); }
+
+p2p_status p2p_plan_create_local(const p2p_plan_desc *desc, const int64_t *src_ids, const int64_t *tgt_ids,
+                                 const int32_t *src_counts, const int32_t *tgt_counts, int64_t n_src_global,
+                                 int64_t n_tgt_global, p2p_plan *out) {
+    p2p::LocalInput li;
+    li.src_ids = src_ids;
+    li.tgt_ids = tgt_ids;
+    li.src_counts = src_counts;
+    li.tgt_counts = tgt_counts;
+    li.n_src_global = n_src_global;
+    li.n_tgt_global = n_tgt_global;
+    return plan_create_common(desc, &li, out);
+}
+
+p2p_status p2p_box_counts(int32_t level, int64_t n, const double *xy, int32_t *counts) {
+    if (level < 1 || level > 15) return set_error(P2P_ERROR_INVALID_ARGUMENT, "level outside 1..15");
+    if (n < 0 || (n && !xy) || !counts) return set_error(P2P_ERROR_INVALID_ARGUMENT, "bad arguments");
+    return guarded([&] { p2p::box_counts(level, n, xy, counts); });
+}
+
+p2p_status p2p_partition_route(const p2p_plan_desc *desc, const int64_t *src_ids, const int64_t *tgt_ids,
+                               const int32_t *src_counts, const int32_t *tgt_counts, int64_t n_src_global,
+                               int64_t n_tgt_global, uint32_t *src_mask, uint32_t *tgt_mask) {
+    if (!desc || (desc->n_src && !src_mask) || (desc->n_tgt && !tgt_mask))
+        return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL desc or mask");
+    p2p::LocalInput li;
+    li.src_ids = src_ids;
+    li.tgt_ids = tgt_ids;
+    li.src_counts = src_counts;
+    li.tgt_counts = tgt_counts;
+    li.n_src_global = n_src_global;
+    li.n_tgt_global = n_tgt_global;
+    li.src_mask = src_mask;
+    li.tgt_mask = tgt_mask;
+    return guarded([&] {
+        p2p::HostPlan hp;
+        p2p::build_host_plan(*desc, hp, &li);
+    });
 }
 
 p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src_xy, const double *d_tgt_xy,
@@ -1107,6 +1148,8 @@ p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src
 p2p_status p2p_apply(p2p_plan P, const void *d_q, void *d_out, int32_t order, int32_t accumulate, void *stream) {
     if (!P || !d_q || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or buffer");
     if (order != P2P_ORDER_PLAN && order != P2P_ORDER_USER) return set_error(P2P_ERROR_INVALID_ARGUMENT, "bad order");
+    if (P->hp.local_input && order == P2P_ORDER_USER)
+        return set_error(P2P_ERROR_NOT_SUPPORTED, "local-input plans: plan order only (no global user order here)");
     return guarded([&] {
         require_device(P);
         DeviceGuard g(P->device);
@@ -1120,6 +1163,7 @@ static p2p_status apply_host_common(p2p_plan P, const void *h_q, void *h_out, in
                                     void *stream, bool sync) {
     if (!P || !h_q || !h_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or buffer");
     if (order != P2P_ORDER_PLAN && order != P2P_ORDER_USER) return set_error(P2P_ERROR_INVALID_ARGUMENT, "bad order");
+    if (P->hp.local_input) return set_error(P2P_ERROR_NOT_SUPPORTED, "local-input plans: p2p_apply_dist*");
     return guarded([&] {
         require_device(P);
         DeviceGuard g(P->device);

@@ -295,6 +295,7 @@ struct HostPlan {
     int64_t reg_entries = 0;
     int64_t table_entries = 0;                    // TILED: uint16 entries of the region tables (tiles x stride)
     bool device_built = false;                    // built by the device builder (p2p_plan_create_device)
+    bool local_input = false;                     // built from this rank's points only (p2p_plan_create_local)
 
     Layout<float> f32;
     Layout<double> f64;
@@ -323,7 +324,21 @@ struct TileStats {
 int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const TileStats &st);
 void check_kernel(const p2p_plan_desc &d);  // kernel function + envelope (throws Error)
 
-void build_host_plan(const p2p_plan_desc &desc, HostPlan &hp);
+// Local-input partitioned plans (p2p_plan_create_local / p2p_partition_route): this rank passes
+// only the points it holds (with their global ids) and the GLOBAL per-box point counts; the
+// partition, tile choice and global plan indices follow from the counts alone, so the plan is
+// the one the global-input builder makes for this rank (bit-identical applies).
+struct LocalInput {
+    const int64_t *src_ids = nullptr, *tgt_ids = nullptr;        // global ids of the passed points
+    const int32_t *src_counts = nullptr, *tgt_counts = nullptr;  // [4^(L-1)] global counts, Morton order
+    int64_t n_src_global = 0, n_tgt_global = 0;
+    // route-only mode: stop after the partition and write, per passed point, the bit mask of the
+    // ranks that need it (sources: the owner of its box + every rank with an owned tile whose
+    // region holds the box; targets: the owner of its box)
+    uint32_t *src_mask = nullptr, *tgt_mask = nullptr;
+};
+void build_host_plan(const p2p_plan_desc &desc, HostPlan &hp, const LocalInput *li = nullptr);
+void box_counts(int level, int64_t n, const double *xy, int32_t *counts);  // [4^(L-1)] per-box counts
 void build_host_plan_3d(const p2p_plan_desc &desc, HostPlan &hp);
 void build_host_plan_adaptive(const p2p_plan_desc &desc, HostPlan &hp);
 // ADAPTIVE kernel shared memory: staged sources (x, y, q) relative to the target leaf, the

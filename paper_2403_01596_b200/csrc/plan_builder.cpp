@@ -648,11 +648,59 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     return smem;
 }
 
-void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
+// Local input: global CSR offsets from the global per-box counts, and the passed points sorted
+// by (box, global id) -- the global plan's order restricted to them.
+void local_sort(const double *xy, const int64_t *ids, int64_t n, const HostPlan &hp, std::vector<uint32_t> &code,
+                std::vector<int32_t> &order) {
+    code.resize((size_t)n);
+    parallel_for(n, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i)
+            code[i] = morton_encode(cell_of(xy[2 * i], hp.S), cell_of(xy[2 * i + 1], hp.S));
+    });
+    order.resize((size_t)n);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+        return code[a] != code[b] ? code[a] < code[b] : ids[a] < ids[b];
+    });
+    for (int64_t i = 1; i < n; ++i)
+        if (code[order[i]] == code[order[i - 1]] && ids[order[i]] == ids[order[i - 1]])
+            fail(P2P_ERROR_INVALID_ARGUMENT, "duplicate global id among the passed points");
+}
+
+void box_counts(int level, int64_t n, const double *xy, int32_t *counts) {
+    const int64_t S = int64_t(1) << (level - 1), B = S * S;
+    if (n) validate_points(xy, n, "points");
+    std::fill(counts, counts + B, 0);
+    for (int64_t i = 0; i < n; ++i) counts[morton_encode(cell_of(xy[2 * i], S), cell_of(xy[2 * i + 1], S))] += 1;
+}
+
+std::vector<int32_t> offsets_from_counts(const int32_t *counts, int64_t B, int64_t n_global, const char *what) {
+    std::vector<int32_t> off((size_t)B + 1, 0);
+    int64_t acc = 0;
+    for (int64_t b = 0; b < B; ++b) {
+        if (counts[b] < 0) fail(P2P_ERROR_INVALID_ARGUMENT, std::string("negative ") + what + " box count");
+        acc += counts[b];
+        if (acc > INT32_MAX - 8) fail(P2P_ERROR_NOT_SUPPORTED, "more than 2^31 points per set");
+        off[b + 1] = (int32_t)acc;
+    }
+    if (acc != n_global) fail(P2P_ERROR_INVALID_ARGUMENT, std::string(what) + " box counts do not sum to n_global");
+    return off;
+}
+
+void build_host_plan(const p2p_plan_desc &d, HostPlan &hp, const LocalInput *li) {
     auto t0 = std::chrono::steady_clock::now();
+    if (li) {
+        if (d.level <= 0) fail(P2P_ERROR_NOT_SUPPORTED, "local-input plans need an explicit level");
+        if (d.layout != P2P_LAYOUT_NONREDUNDANT && d.layout != P2P_LAYOUT_REDUNDANT && d.layout != P2P_LAYOUT_TILED)
+            fail(P2P_ERROR_NOT_SUPPORTED, "local-input plans: NR, R and TILED layouts");
+        if (d.part_world > 32) fail(P2P_ERROR_NOT_SUPPORTED, "local-input plans: part_world <= 32");
+        if ((d.n_src && !li->src_ids) || (d.n_tgt && !li->tgt_ids) || !li->src_counts || !li->tgt_counts)
+            fail(P2P_ERROR_INVALID_ARGUMENT, "NULL ids or box counts");
+    }
     if (d.struct_size != sizeof(p2p_plan_desc)) fail(P2P_ERROR_INVALID_ARGUMENT, "desc.struct_size mismatch");
     check_kernel(d);
     if (kernel_dim(d.kernel) == 3) {
+        if (li) fail(P2P_ERROR_NOT_SUPPORTED, "local-input plans: 2D kernels");
         build_host_plan_3d(d, hp);
         return;
     }
@@ -670,8 +718,17 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     if (!(d.epsilon > 0.0) || !std::isfinite(d.epsilon)) fail(P2P_ERROR_INVALID_ARGUMENT, "epsilon must be > 0");
     if (d.part_world < 1 || d.part_rank < 0 || d.part_rank >= d.part_world)
         fail(P2P_ERROR_INVALID_ARGUMENT, "bad part_world / part_rank");
-    validate_points(d.src_xy, d.n_src, "sources");
-    validate_points(d.tgt_xy, d.n_tgt, "targets");
+    if (!li) {
+        validate_points(d.src_xy, d.n_src, "sources");
+        validate_points(d.tgt_xy, d.n_tgt, "targets");
+    } else {  // zero passed points is fine (a rank may hold none); the global sets may not be empty
+        if (d.n_src < 0 || d.n_tgt < 0 || (d.n_src && !d.src_xy) || (d.n_tgt && !d.tgt_xy))
+            fail(P2P_ERROR_INVALID_ARGUMENT, "bad local point arrays");
+        if (d.n_src) validate_points(d.src_xy, d.n_src, "sources");
+        if (d.n_tgt) validate_points(d.tgt_xy, d.n_tgt, "targets");
+        if (li->n_src_global < 1 || li->n_tgt_global < 1)
+            fail(P2P_ERROR_INVALID_ARGUMENT, "n = 0 (SPEC.md L55)");
+    }
     if (d.n_src > INT32_MAX - 8 || d.n_tgt > INT32_MAX - 8)
         fail(P2P_ERROR_NOT_SUPPORTED, "more than 2^31 points per set");
 
@@ -683,8 +740,9 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     hp.kappa = d.kernel == P2P_KERNEL_HELMHOLTZ_2D ? d.wavenumber : 0.0;
     hp.part_world = d.part_world;
     hp.part_rank = d.part_rank;
-    hp.n_src = d.n_src;
-    hp.n_tgt = d.n_tgt;
+    hp.n_src = li ? li->n_src_global : d.n_src;
+    hp.n_tgt = li ? li->n_tgt_global : d.n_tgt;
+    hp.local_input = li != nullptr;
 
     // ---- a1 level
     int L = d.level > 0 ? d.level : ct_loop_level(d);
@@ -697,8 +755,17 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     hp.h = 1.0 / (double)hp.S;
 
     // ---- a2, a3
-    csr_sort(d.src_xy, d.n_src, hp, hp.src_off_g, hp.src_perm_g);
-    csr_sort(d.tgt_xy, d.n_tgt, hp, hp.tgt_off_g, hp.tgt_perm_g);
+    std::vector<uint32_t> lcode_s, lcode_t;  // local input: passed points' box codes ...
+    std::vector<int32_t> lord_s, lord_t;      // ... and their (box, global id) order
+    if (!li) {
+        csr_sort(d.src_xy, d.n_src, hp, hp.src_off_g, hp.src_perm_g);
+        csr_sort(d.tgt_xy, d.n_tgt, hp, hp.tgt_off_g, hp.tgt_perm_g);
+    } else {
+        hp.src_off_g = offsets_from_counts(li->src_counts, hp.B, hp.n_src, "source");
+        hp.tgt_off_g = offsets_from_counts(li->tgt_counts, hp.B, hp.n_tgt, "target");
+        local_sort(d.src_xy, li->src_ids, d.n_src, hp, lcode_s, lord_s);
+        local_sort(d.tgt_xy, li->tgt_ids, d.n_tgt, hp, lcode_t, lord_t);
+    }
     const int32_t *so = hp.src_off_g.data(), *to = hp.tgt_off_g.data();
     auto ns = [&](int64_t b) -> int64_t { return so[b + 1] - so[b]; };
     auto ntg = [&](int64_t b) -> int64_t { return to[b + 1] - to[b]; };
@@ -869,6 +936,35 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
             }
     };
 
+    // ---- local input, route-only (p2p_partition_route): which ranks need each passed point
+    auto owner_of_box = [&](int64_t b) -> int {
+        return (int)(std::upper_bound(box_begin.begin(), box_begin.end(), b) - box_begin.begin()) - 1;
+    };
+    if (li && (li->src_mask || li->tgt_mask)) {
+        const int64_t S2 = hp.S;
+        auto tile_nonempty = [&](int64_t t) { return to[(t + 1) * WW] > to[t * WW]; };
+        if (li->src_mask)
+            parallel_for(d.n_src, [&](int64_t a, int64_t bnd) {
+                for (int64_t i = a; i < bnd; ++i) {
+                    const uint32_t b = lcode_s[i];
+                    uint32_t m = 1u << std::min(owner_of_box(b), 31);
+                    uint32_t ix, iy;
+                    morton_decode(b, ix, iy);
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            const int64_t x = (int64_t)ix + dx, y = (int64_t)iy + dy;
+                            if (x < 0 || y < 0 || x >= S2 || y >= S2) continue;
+                            const int64_t t = (int64_t)morton_encode((uint32_t)x, (uint32_t)y) >> (2 * k);
+                            if (tile_nonempty(t)) m |= 1u << owner_of_box(t * WW);
+                        }
+                    li->src_mask[i] = m;
+                }
+            });
+        if (li->tgt_mask)
+            for (int64_t i = 0; i < d.n_tgt; ++i) li->tgt_mask[i] = 1u << owner_of_box(lcode_t[i]);
+        return;
+    }
+
     // ---- local source set: all sources (P = 1), or those in the regions of the owned tiles
     // plus every box of the owned Morton range, so that the owned sources -- the global plan
     // range [part_src[r], part_src[r+1]) -- are one contiguous block of the local set (local
@@ -877,7 +973,50 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
     hp.n_src_owned = hp.part_src[r + 1] - hp.part_src[r];
     hp.tgt_begin = hp.part_tgt[r];
     hp.n_tgt_local = hp.part_tgt[r + 1] - hp.part_tgt[r];
-    if (P == 1) {
+    if (li) {
+        // the marked boxes: (P = 1) every box; else the regions of the owned tiles and the owned
+        // box range.  Each must arrive whole: all of its sources, in (box, global id) order.
+        std::vector<uint8_t> mark((size_t)hp.B, P == 1 ? 1 : 0);
+        if (P > 1) {
+            std::vector<uint32_t> boxes;
+            for (int32_t t : hp.tiles) {
+                boxes.clear();
+                region_boxes(t, boxes);
+                for (uint32_t m : boxes) mark[m] = 1;
+            }
+            for (int64_t b = box_begin[r]; b < box_begin[r + 1]; ++b) mark[b] = 1;
+        }
+        hp.src_off.assign((size_t)hp.B + 1, 0);
+        hp.src_gidx.clear();
+        hp.src_uidx.clear();
+        const int64_t nl = d.n_src;
+        int64_t p = 0;
+        for (int64_t b = 0; b < hp.B; ++b) {
+            const int64_t lo = p;
+            while (p < nl && lcode_s[lord_s[p]] == (uint32_t)b) ++p;
+            if (mark[b] && ns(b)) {
+                if (p - lo != ns(b))
+                    fail(P2P_ERROR_INVALID_ARGUMENT, "local input: box " + std::to_string(b) + " needs " +
+                                                         std::to_string(ns(b)) + " sources, " +
+                                                         std::to_string(p - lo) + " passed");
+                for (int64_t j = 0; j < ns(b); ++j) {
+                    hp.src_gidx.push_back((int32_t)(so[b] + j));
+                    hp.src_uidx.push_back(lord_s[lo + j]);
+                }
+            }
+            hp.src_off[b + 1] = (int32_t)hp.src_gidx.size();
+        }
+        hp.n_src_local = (int64_t)hp.src_gidx.size();
+        // targets: exactly those of the owned box range
+        if (d.n_tgt != hp.n_tgt_local)
+            fail(P2P_ERROR_INVALID_ARGUMENT, "local input: " + std::to_string(hp.n_tgt_local) + " owned targets, " +
+                                                 std::to_string(d.n_tgt) + " passed");
+        for (int64_t i = 0; i < d.n_tgt; ++i) {
+            const int64_t b = lcode_t[lord_t[i]];
+            if (b < box_begin[r] || b >= box_begin[r + 1])
+                fail(P2P_ERROR_INVALID_ARGUMENT, "local input: a passed target lies outside this rank's boxes");
+        }
+    } else if (P == 1) {
         hp.src_off = hp.src_off_g;
         hp.n_src_local = hp.n_src;
         hp.src_gidx.resize((size_t)hp.n_src);
@@ -901,13 +1040,16 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp) {
         }
         hp.n_src_local = (int64_t)hp.src_gidx.size();
     }
-    hp.src_uidx.resize((size_t)hp.n_src_local);
-    for (int64_t i = 0; i < hp.n_src_local; ++i) hp.src_uidx[i] = hp.src_perm_g[hp.src_gidx[i]];
+    if (!li) {
+        hp.src_uidx.resize((size_t)hp.n_src_local);
+        for (int64_t i = 0; i < hp.n_src_local; ++i) hp.src_uidx[i] = hp.src_perm_g[hp.src_gidx[i]];
+    }
 
     hp.tgt_off.resize((size_t)hp.B + 1);
     for (int64_t b = 0; b <= hp.B; ++b)
         hp.tgt_off[b] = (int32_t)std::min<int64_t>(std::max<int64_t>(to[b] - hp.tgt_begin, 0), hp.n_tgt_local);
-    hp.tgt_uidx.assign(hp.tgt_perm_g.begin() + hp.tgt_begin, hp.tgt_perm_g.begin() + hp.tgt_begin + hp.n_tgt_local);
+    if (li) hp.tgt_uidx.assign(lord_t.begin(), lord_t.end());
+    else hp.tgt_uidx.assign(hp.tgt_perm_g.begin() + hp.tgt_begin, hp.tgt_perm_g.begin() + hp.tgt_begin + hp.n_tgt_local);
 
     // ---- halo bookkeeping for the per-apply weight exchange (P > 1).
     hp.recv_counts.assign((size_t)P, 0);

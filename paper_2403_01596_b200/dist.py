@@ -20,18 +20,19 @@ from . import p2p
 
 
 class DistributedP2P:
-    def __init__(self, src_xy, tgt_xy, *, group=None, device: int | None = None, host_staged: bool = False,
-                 **plan_kwargs):
+    def __init__(self, src_xy=None, tgt_xy=None, *, group=None, device: int | None = None, host_staged: bool = False,
+                 plan=None, **plan_kwargs):
         import torch
         import torch.distributed as dist
         self.dist, self.torch = dist, torch
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.device = torch.cuda.current_device() if device is None else device
+        self.device = (torch.cuda.current_device() if torch.cuda.is_available() else -1) if device is None else device
         self.host_staged = host_staged  # gloo / test mode: exchange through host tensors
-        self.plan = p2p.Plan(src_xy, tgt_xy, device=self.device, part_world=self.world, part_rank=self.rank,
-                             **plan_kwargs)
+        self.plan = plan if plan is not None else p2p.Plan(
+            src_xy, tgt_xy, device=self.device, part_world=self.world, part_rank=self.rank, **plan_kwargs)
+        self.src_ids = self.tgt_ids = None  # from_local: global ids of the received points
         info = self.plan.info
         self.info = info
         part = self.plan.export("partition").reshape(2, self.world + 1)
@@ -39,9 +40,84 @@ class DistributedP2P:
         hc = self.plan.export("halo_counts").reshape(2, self.world)
         self.recv_splits, self.send_splits = hc[0].tolist(), hc[1].tolist()
         dt = self.plan.torch_dtype
-        dev = torch.device("cuda", self.device)
-        self._send = torch.empty(max(1, info["n_send"]), dtype=dt, device=dev)
-        self._halo = torch.empty(max(1, info["n_halo"]), dtype=dt, device=dev)
+        if self.device >= 0:
+            dev = torch.device("cuda", self.device)
+            self._send = torch.empty(max(1, info["n_send"]), dtype=dt, device=dev)
+            self._halo = torch.empty(max(1, info["n_halo"]), dtype=dt, device=dev)
+
+    @classmethod
+    def from_local(cls, src_xy, tgt_xy, src_ids, tgt_ids, *, level: int, group=None, device: int | None = None,
+                   host_staged: bool = False, **plan_kwargs):
+        """Each rank passes only the points it holds (any split of the global sets) with their
+        global ids; no rank ever sees the global point set (north_star: "a one-time exchange
+        distributes halo source points").  Collective:
+          1. per-box counts of the held points (p2p_box_counts), summed over the ranks (allreduce);
+          2. the partition from the global counts, and per held point the ranks that need it
+             (p2p_partition_route: the owner of its box + the ranks whose tile regions hold it);
+          3. one all-to-all of (x, y, id) records -- owned points and the halo sources;
+          4. this rank's plan from what arrived (p2p_plan_create_local), identical to the plan
+             the global builder makes for this rank.
+        Weights then go in per owned source, in the order owned_source_ids() gives."""
+        import torch
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        src_xy = np.ascontiguousarray(src_xy, dtype=np.float64).reshape(-1, 2)
+        tgt_xy = np.ascontiguousarray(tgt_xy, dtype=np.float64).reshape(-1, 2)
+        src_ids = np.ascontiguousarray(src_ids, dtype=np.int64)
+        tgt_ids = np.ascontiguousarray(tgt_ids, dtype=np.int64)
+        if device is None:
+            device = torch.cuda.current_device() if torch.cuda.is_available() else -1
+        on_dev = not host_staged and device >= 0 and dist.get_backend(group) == "nccl"
+        cdev = torch.device("cuda", device) if on_dev else torch.device("cpu")
+        # 1. global per-box counts
+        counts = np.concatenate([p2p.p2p_box_counts(level, src_xy), p2p.p2p_box_counts(level, tgt_xy)])
+        ct = torch.from_numpy(counts).to(cdev)
+        dist.all_reduce(ct, group=group)
+        counts = ct.cpu().numpy()
+        B = len(counts) // 2
+        cs, ctg = counts[:B], counts[B:]
+        # 2. routing
+        kw = dict(plan_kwargs)
+        desc = p2p.make_desc(src_xy, tgt_xy, level=level, part_world=world, part_rank=rank, device=device, **kw)
+        smask, tmask = p2p.p2p_partition_route(desc, src_ids, tgt_ids, cs, ctg)
+
+        # 3. one all-to-all per point set: (x, y, id) records (ids < 2^53 are exact in float64)
+        def route(xy, ids, mask):
+            recs, cnt = [], []
+            for r in range(world):
+                sel = (mask >> np.uint32(r)) & np.uint32(1) == 1
+                recs.append(np.column_stack([xy[sel], ids[sel].astype(np.float64)]))
+                cnt.append(int(sel.sum()))
+            send = torch.from_numpy(np.ascontiguousarray(np.concatenate(recs).reshape(-1))).to(cdev)
+            sc = torch.tensor(cnt, dtype=torch.int64, device=cdev)
+            rc = torch.empty_like(sc)
+            dist.all_to_all_single(rc, sc, group=group)
+            rcn = rc.cpu().tolist()
+            recv = torch.empty(3 * sum(rcn), dtype=torch.float64, device=cdev)
+            dist.all_to_all_single(recv, send, [3 * c for c in rcn], [3 * c for c in cnt], group=group)
+            a = recv.cpu().numpy().reshape(-1, 3)
+            return np.ascontiguousarray(a[:, :2]), a[:, 2].astype(np.int64)
+
+        rs_xy, rs_id = route(src_xy, src_ids, smask)
+        rt_xy, rt_id = route(tgt_xy, tgt_ids, tmask)
+        # 4. this rank's plan
+        plan = p2p.Plan(rs_xy, rt_xy, level=level, part_world=world, part_rank=rank, device=device, build="local",
+                        local=(rs_id, rt_id, cs, ctg), **kw)
+        self = cls(group=group, device=device, host_staged=host_staged, plan=plan)
+        self.src_ids, self.tgt_ids = rs_id, rt_id
+        self.src_xy_local, self.tgt_xy_local = rs_xy, rt_xy  # what arrived (the plan copied it)
+        return self
+
+    def owned_source_ids(self) -> np.ndarray:
+        """from_local plans: global ids of this rank's owned sources, in the order apply() takes
+        their weights (global plan order)."""
+        gidx = self.plan.export("src_global")
+        lo, hi = self.owned_source_range()
+        return self.src_ids[self.plan.export("src_perm")[(gidx >= lo) & (gidx < hi)]]
+
+    def target_ids(self) -> np.ndarray:
+        """from_local plans: global ids of this rank's targets, in the order apply() returns them."""
+        return self.tgt_ids[self.plan.export("tgt_perm")]
 
     @property
     def n_src_owned(self) -> int:

@@ -61,6 +61,7 @@ ABI_SYMBOLS = (
     "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_gather_peer", "p2p_ipc_export", "p2p_ipc_open", "p2p_ipc_close", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
     "p2p_status_string", "p2p_last_error", "p2p_abi_version",
     "p2p_peer_buffers", "p2p_peer_connect", "p2p_apply_peer_sync", "p2p_gather", "p2p_peer_check",
+    "p2p_box_counts", "p2p_partition_route", "p2p_plan_create_local",
 )
 
 
@@ -136,6 +137,9 @@ def load_library() -> C.CDLL:
     lib.p2p_apply_peer_sync.argtypes = [P, P, P, i32, P]
     lib.p2p_gather.argtypes = [P, P, P, P]
     lib.p2p_peer_check.argtypes = [P]
+    lib.p2p_box_counts.argtypes = [i32, i64, P, P]
+    lib.p2p_partition_route.argtypes = [C.POINTER(PlanDesc), P, P, P, P, i64, i64, P, P]
+    lib.p2p_plan_create_local.argtypes = [C.POINTER(PlanDesc), P, P, P, P, i64, i64, C.POINTER(P)]
     lib.p2p_destroy.argtypes = [P]
     lib.p2p_plan_get_info.argtypes = [P, C.POINTER(PlanInfo)]
     lib.p2p_plan_export.argtypes = [P, i32, P, C.POINTER(C.c_size_t)]
@@ -146,7 +150,7 @@ def load_library() -> C.CDLL:
     for name in ("p2p_plan_create", "p2p_plan_create_device", "p2p_apply", "p2p_apply_host", "p2p_apply_host_async", "p2p_apply_dist", "p2p_apply_dist_interior",
                  "p2p_apply_dist_boundary", "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_gather_peer", "p2p_ipc_export",
                  "p2p_ipc_open", "p2p_ipc_close", "p2p_peer_buffers", "p2p_peer_connect", "p2p_apply_peer_sync",
-                 "p2p_gather", "p2p_peer_check",
+                 "p2p_gather", "p2p_peer_check", "p2p_box_counts", "p2p_partition_route", "p2p_plan_create_local",
                  "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export"):
         getattr(lib, name).restype = i32
     _lib = lib
@@ -257,6 +261,39 @@ def p2p_peer_check(plan):
     _check(load_library().p2p_peer_check(plan), "p2p_peer_check")
 
 
+def p2p_box_counts(level: int, xy) -> np.ndarray:
+    """int32 per-box counts [4^(level-1)] (Morton order) of the points xy [n, 2]."""
+    xy = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, 2)
+    out = np.empty(1 << (2 * (level - 1)), dtype=np.int32)
+    _check(load_library().p2p_box_counts(level, len(xy), xy.ctypes.data if len(xy) else None, out.ctypes.data),
+           "p2p_box_counts")
+    return out
+
+
+def _local_args(src_ids, tgt_ids, src_counts, tgt_counts):
+    a = [np.ascontiguousarray(src_ids, dtype=np.int64), np.ascontiguousarray(tgt_ids, dtype=np.int64),
+         np.ascontiguousarray(src_counts, dtype=np.int32), np.ascontiguousarray(tgt_counts, dtype=np.int32)]
+    ptr = [x.ctypes.data if x.size else None for x in a]
+    return a, ptr, int(a[2].sum(dtype=np.int64)), int(a[3].sum(dtype=np.int64))
+
+
+def p2p_partition_route(desc, src_ids, tgt_ids, src_counts, tgt_counts):
+    """(source masks, target masks): per passed point, the bit mask of the ranks that need it."""
+    keep, ptr, ns, nt = _local_args(src_ids, tgt_ids, src_counts, tgt_counts)
+    sm = np.zeros(max(1, desc.n_src), dtype=np.uint32)
+    tm = np.zeros(max(1, desc.n_tgt), dtype=np.uint32)
+    _check(load_library().p2p_partition_route(C.byref(desc), *ptr, ns, nt, sm.ctypes.data, tm.ctypes.data),
+           "p2p_partition_route")
+    return sm[:desc.n_src], tm[:desc.n_tgt]
+
+
+def p2p_plan_create_local(desc, src_ids, tgt_ids, src_counts, tgt_counts):
+    keep, ptr, ns, nt = _local_args(src_ids, tgt_ids, src_counts, tgt_counts)
+    h = C.c_void_p()
+    _check(load_library().p2p_plan_create_local(C.byref(desc), *ptr, ns, nt, C.byref(h)), "p2p_plan_create_local")
+    return h
+
+
 def p2p_ipc_export(d_ptr: int) -> tuple[bytes, int]:
     """(64-byte IPC handle of the allocation holding d_ptr, d_ptr's offset in it)."""
     buf = C.create_string_buffer(64)
@@ -297,6 +334,31 @@ def p2p_plan_export(plan, kind) -> np.ndarray:
 
 
 # ------------------------------------------------------------- convenience
+_LAYOUTS = {"nr": P2P_LAYOUT_NONREDUNDANT, "r": P2P_LAYOUT_REDUNDANT, "tiled": P2P_LAYOUT_TILED,
+            "paper_i": P2P_LAYOUT_PAPER_INDEXING, "paper_r": P2P_LAYOUT_PAPER_REPETITION,
+            "adaptive": P2P_LAYOUT_ADAPTIVE}
+
+
+def make_desc(src_xy, tgt_xy, *, level: int = 0, ct: int = 15, l_start: int = 3, l_max: int = 15,
+              level_delta: int = 0, epsilon: float = 1e-12, layout: str = "nr", precision: str = "fp32",
+              device: int = 0, tile_log2: int = -1, stream: int = 0, part_world: int = 1, part_rank: int = 0,
+              kernel: str = "laplace", wavenumber: float = 0.0) -> PlanDesc:
+    """A p2p_plan_desc over host point arrays (kept alive by the caller while it is used)."""
+    d = p2p_plan_desc_init()
+    d.n_src, d.n_tgt = len(src_xy), len(tgt_xy)
+    d.src_xy = src_xy.ctypes.data if len(src_xy) else None
+    d.tgt_xy = tgt_xy.ctypes.data if len(tgt_xy) else None
+    d.level, d.ct, d.l_start, d.l_max, d.level_delta = level, ct, l_start, l_max, level_delta
+    d.epsilon = epsilon
+    d.layout = _LAYOUTS[layout]
+    d.precision = {"fp32": P2P_FP32, "fp64": P2P_FP64}[precision]
+    d.device, d.tile_log2, d.stream = device, tile_log2, stream or None
+    d.part_world, d.part_rank = part_world, part_rank
+    d.kernel = KERNELS[kernel]
+    d.wavenumber = wavenumber
+    return d
+
+
 class Plan:
     """A P2P plan: ``Plan(src_xy, tgt_xy, level=...)`` then ``plan.apply(q, out)``.
 
@@ -310,16 +372,19 @@ class Plan:
     device: CUDA ordinal, or -1 for a host-only plan (build + export only).
     build: "host" (p2p_plan_create: the C++ builder on the CPU) or "device"
     (p2p_plan_create_device: the same plan built by GPU kernels; src_xy / tgt_xy may then
-    be CUDA float64 [n, 2] tensors, numpy input is copied to the device first).
+    be CUDA float64 [n, 2] tensors, numpy input is copied to the device first), or "local"
+    (p2p_plan_create_local: a partition's plan from the points this rank received; pass
+    ``local=(src_ids, tgt_ids, src_counts, tgt_counts)`` -- their global ids and the global
+    per-box counts; see dist.DistributedP2P.from_local).
     """
 
     def __init__(self, src_xy, tgt_xy=None, *, level: int = 0, ct: int = 15, l_start: int = 3,
                  l_max: int = 15, level_delta: int = 0, epsilon: float = 1e-12, layout: str = "nr",
                  precision: str = "fp32", device: int = 0, tile_log2: int = -1, stream: int = 0,
                  part_world: int = 1, part_rank: int = 0, build: str = "host", kernel: str = "laplace",
-                 wavenumber: float = 0.0):
-        if build not in ("host", "device"):
-            raise ValueError("build must be 'host' or 'device'")
+                 wavenumber: float = 0.0, local=None):
+        if build not in ("host", "device", "local"):
+            raise ValueError("build must be 'host', 'device' or 'local'")
         dim = 3 if kernel.endswith("3d") else 2
         d = p2p_plan_desc_init()
         if build == "device":
@@ -357,6 +422,8 @@ class Plan:
                 d.stream = torch.cuda.current_stream(device).cuda_stream or None
             self._h = p2p_plan_create_device(d, self._src.data_ptr(), self._tgt.data_ptr())
             self._src = self._tgt = None  # read during the call only
+        elif build == "local":
+            self._h = p2p_plan_create_local(d, *local)
         else:
             self._h = p2p_plan_create(d)
         self.info = p2p_plan_get_info(self._h)
