@@ -90,10 +90,11 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the R / fp64 detail lines")
     ap.add_argument("--build", choices=["device", "host"], default="device",
                     help="N = 1 plans: built on the GPU (p2p_plan_create_device) or by the host builder")
-    ap.add_argument("--exchange", choices=["sync", "nccl", "peer"], default="sync",
+    ap.add_argument("--exchange", choices=["auto", "sync", "nccl", "peer"], default="auto",
                     help="N > 1 halo exchange: sync = one-sided peer-memory reads ordered by device-side "
-                         "signals (p2p_apply_peer_sync; default, CUDA-graph captured); nccl = "
-                         "torch.distributed all_to_all; peer = peer-memory reads with host barriers")
+                         "signals (p2p_apply_peer_sync; CUDA-graph captured); nccl = torch.distributed "
+                         "all_to_all; peer = peer-memory reads with host barriers; auto (default) = sync or "
+                         "nccl, whichever ran the faster step (max over ranks)")
     ap.add_argument("--no-graph", action="store_true", help="N > 1 sync mode: launch eagerly, no CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
@@ -297,12 +298,12 @@ def main():
     weak = world > 1 and args.scaling == "weak"
     for name in names:
         cfg = W.widened(W.CONFIGS[name], world) if weak else W.CONFIGS[name]
-        src, tgt, q = W.make_problem(cfg, kind=args.kind)
         name = cfg.name
         kw = dict(level=cfg.level, layout=args.layout, precision=args.precision, tile_log2=args.tile,
                   **_kernel_kw(args, cfg))
-        q = _weights(args, cfg, q)
         if world == 1:
+            src, tgt, q = W.make_problem(cfg, kind=args.kind)
+            q = _weights(args, cfg, q)
             if args.build == "device" and args.layout in ("nr", "tiled"):  # built on the GPU (NEXT-2)
                 pl = p2p.Plan(torch.as_tensor(src, device=dev), torch.as_tensor(tgt, device=dev), device=local,
                               build="device", **kw)
@@ -310,22 +311,24 @@ def main():
                 pl = p2p.Plan(src, tgt, device=local, **kw)
             job = {"name": name, "cfg": cfg, "plan": pl, "info": pl.info, "q_user": q,
                    "q": torch.as_tensor(q[pl.export("src_perm")], dtype=pl.torch_dtype, device=dev)}
-        else:
-            dp = DistributedP2P(src, tgt, device=local, host_staged=shared, **kw)
+        else:  # this rank generates only its share; the plan comes from the ranks' own points
+            s_xy, t_xy, sid, tid = W.problem_share(cfg, rank, world, kind=args.kind)
+            kw.pop("level")
+            dp = DistributedP2P.from_local(s_xy, t_xy, sid, tid, level=cfg.level, device=local, host_staged=shared,
+                                           **kw)
             pl = dp.plan
-            job = {"name": name, "cfg": cfg, "plan": pl, "dp": dp, "info": pl.info, "q_user": q,
-                   "q_owned": torch.as_tensor(q[_owned_user_indices(pl, src, dp.src_begin.reshape(1, -1), rank)],
-                                              dtype=pl.torch_dtype, device=dev)}
+            oid = dp.owned_source_ids()
+            qo = (W.weights_complex(cfg.n, cfg.seed, index=oid) if args.kernel.startswith("helmholtz")
+                  else W.weights(cfg.n, cfg.seed, index=oid))
+            job = {"name": name, "cfg": cfg, "plan": pl, "dp": dp, "info": pl.info,
+                   "q_owned": torch.as_tensor(qo, dtype=pl.torch_dtype, device=dev)}
         job["out"] = torch.empty(max(1, job["info"]["n_tgt_local"]), dtype=pl.torch_dtype, device=dev)
         jobs.append(job)
     pairs_step = sum(j["info"]["pairs_global"] for j in jobs)
     pairs_local = sum(j["info"]["pairs"] for j in jobs)
 
     comm = torch.cuda.Stream(dev) if world > 1 else None
-    mode = args.exchange if world > 1 else "single"
-    if mode == "sync":
-        for j in jobs:
-            j["dp"].enable_sync()
+    mode = "single"
 
     def enqueue(j, cur, ready=None):
         """one config's apply on stream handle `cur` (the current stream: graph-capture safe)"""
@@ -358,20 +361,53 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    for _ in range(max(3, args.warmup)):
-        step()
-    barrier()
-    # N > 1, sync exchange: the whole step (every config's publish / pull / interior / boundary
-    # kernels) captured once in a CUDA graph -> one graph launch per step, no host work per apply
-    graph = None
-    if mode == "sync" and not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cpu" if shared else dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def prepare(m):
+        """warm up exchange mode m; N > 1 sync: capture the whole step (every config's publish /
+        pull / interior / boundary kernels) in a CUDA graph -> one graph launch per step"""
+        nonlocal mode
+        mode = m
+        if m == "sync":
+            for j in jobs:
+                j["dp"].enable_sync()
+        for _ in range(max(3, args.warmup)):
             step()
         barrier()
-        graph.replay()  # one untimed replay (every rank the same count: the epochs stay aligned)
-        barrier()
+        g = None
+        if m == "sync" and not args.no_graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            barrier()
+            g.replay()  # one untimed replay (every rank the same count: the epochs stay aligned)
+            barrier()
+        return g
 
+    # N > 1, --exchange auto: both exchanges, 5 untimed-for-the-record steps each, the faster
+    # (max over ranks, so every rank decides alike) is the one timed below
+    autotune = None
+    if world > 1 and args.exchange == "auto":
+        autotune = {}
+        for m in ("sync", "nccl"):
+            g = prepare(m)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            e0.record(stream)
+            for _ in range(5):
+                g.replay() if g is not None else step()
+            e1.record(stream)
+            barrier()
+            autotune[m] = max_over_ranks(e0.elapsed_time(e1) / 5)
+        chosen = min(autotune, key=autotune.get)
+    else:
+        chosen = args.exchange if world > 1 else "single"
+    graph = prepare(chosen)
     # ---- timed region: K steps, per-step events, L2 flush between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in jobs]
@@ -397,11 +433,7 @@ def main():
         kern_ms = step_ms[:, None] * (share / share.sum())[None, :]
     else:
         kern_ms = np.array([[a.elapsed_time(b) for a, b in row] for row in kev])  # [K, jobs]
-    total_ms = float(step_ms.sum())
-    if world > 1:
-        t = torch.tensor([total_ms], device="cpu" if shared else dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(float(step_ms.sum()))
     ms_per_step = total_ms / args.steps
     value = pairs_step / (ms_per_step * 1e-3)
 
@@ -460,6 +492,7 @@ def main():
                         "t_max": j["info"]["t_max"]})
 
     # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
+    args.exchange_chosen = mode
     e2e = _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier)
 
     out = {
@@ -472,8 +505,9 @@ def main():
                    "precision": args.precision, "kind": args.kind, "pairs_per_step": pairs_step,
                    "kernel": args.kernel, **({"kappa_h": args.kh} if args.kernel.startswith("helmholtz") else {}),
                    "order": "plan", "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": f"morton-range x{world}" + (_exchange_desc(args.exchange, shared, graph is not None)
-                                                              if world > 1 else "")},
+                   "parallelism": f"morton-range x{world}" + (_exchange_desc(mode, shared, graph is not None)
+                                                              if world > 1 else ""),
+                   **({"exchange": mode, "exchange_autotune_ms": autotune} if world > 1 else {})},
         "gpu_launches": args.steps * len(jobs) * {"single": 1, "sync": 4, "nccl": 3, "peer": 2}[mode],
         "roofline": roofline, "clocks": clocks, "e2e": e2e, "per_config": per_cfg,
     }
@@ -553,17 +587,6 @@ def _exchange_desc(mode, shared, graph):
     return d
 
 
-def _owned_user_indices(pl, src, part, rank):
-    """User indices of the sources this rank owns (global plan range part[0, rank]..part[0, rank+1]):
-    the owned block of the local set (contiguous, plan_builder.cpp)."""
-    gidx = pl.export("src_global")
-    uidx = pl.export("src_perm")
-    lo, hi = part[0, rank], part[0, rank + 1]
-    owned = uidx[(gidx >= lo) & (gidx < hi)]
-    assert len(owned) == hi - lo
-    return owned
-
-
 def _e2e_dist(args, jobs, stream, pairs_step, barrier):
     """N > 1: each rank's public-API step from host memory: H2D of its owned weights (pinned),
     halo exchange + distributed apply (DistributedP2P.apply), D2H of its potentials; time = max
@@ -577,7 +600,7 @@ def _e2e_dist(args, jobs, stream, pairs_step, barrier):
     d2h = sum(int(t.numel() * t.element_size()) for t in ho)
 
     comm = torch.cuda.Stream()
-    sync = args.exchange == "sync"
+    sync = getattr(args, "exchange_chosen", args.exchange) == "sync"
 
     def step():
         for a, d in zip(hq, dq):

@@ -191,12 +191,14 @@ def _below(limit: float, x: np.ndarray) -> np.ndarray:
 
 
 def plate_points(cfg: PlateConfig, stream_x: int, stream_y: int, kind: str = "iid",
-                 seed: int | None = None, n: int | None = None) -> np.ndarray:
-    """[n, 2] float64 points on the plate of ``cfg``."""
+                 seed: int | None = None, n: int | None = None, index=None) -> np.ndarray:
+    """[n, 2] float64 points on the plate of ``cfg`` (``index``: only those points of the set,
+    e.g. one rank's share -- the counter-based generator makes any subset directly)."""
     seed = cfg.seed if seed is None else seed
     n = cfg.n if n is None else n
     h = 1.0 / cfg.side
-    idx = np.arange(n, dtype=np.uint64)
+    idx = np.arange(n, dtype=np.uint64) if index is None else np.asarray(index, dtype=np.uint64)
+    n = len(idx)
     ux = uniform01(seed, stream_x, idx)
     uy = uniform01(seed, stream_y, idx)
     xy = np.empty((n, 2), dtype=np.float64)
@@ -206,10 +208,10 @@ def plate_points(cfg: PlateConfig, stream_x: int, stream_y: int, kind: str = "ii
         xy[:, 1] = _below(wy, uy * wy)
     elif kind == "stratified":
         boxes = cfg.sx * cfg.sy
-        if n % boxes:
+        if (cfg.n if index is not None else n) % boxes:
             raise ValueError("stratified generator needs an integer density")
-        d = n // boxes
-        j = np.arange(n, dtype=np.int64) // d
+        d = (cfg.n if index is not None else n) // boxes
+        j = idx.astype(np.int64) // d
         bx = (j % cfg.sx).astype(np.float64)
         by = (j // cfg.sx).astype(np.float64)
         # (b + u) < b + 1 keeps the point inside its cell; scaling by h = 2^-(L-1) is exact.
@@ -220,14 +222,25 @@ def plate_points(cfg: PlateConfig, stream_x: int, stream_y: int, kind: str = "ii
     return xy
 
 
-def weights(n: int, seed: int, stream: int = 4) -> np.ndarray:
-    """q ~ U[-1, 1) as float64."""
-    return 2.0 * uniform01(seed, stream, np.arange(n, dtype=np.uint64)) - 1.0
+def weights(n: int, seed: int, stream: int = 4, index=None) -> np.ndarray:
+    """q ~ U[-1, 1) as float64; ``index``: only those weights."""
+    idx = np.arange(n, dtype=np.uint64) if index is None else np.asarray(index, dtype=np.uint64)
+    return 2.0 * uniform01(seed, stream, idx) - 1.0
 
 
-def weights_complex(n: int, seed: int) -> np.ndarray:
+def weights_complex(n: int, seed: int, index=None) -> np.ndarray:
     """Complex weights for the Helmholtz kernel (NEXT-3): re, im ~ U[-1, 1) (streams 4 and 5)."""
-    return weights(n, seed) + 1j * weights(n, seed, stream=5)
+    return weights(n, seed, index=index) + 1j * weights(n, seed, stream=5, index=index)
+
+
+def problem_share(cfg: PlateConfig | str, rank: int, world: int, kind: str = "iid"):
+    """One rank's interleaved share of a workload (global ids rank, rank + world, ...): (src_xy,
+    tgt_xy, src_ids, tgt_ids) -- what DistributedP2P.from_local takes; the rank never
+    generates the other points."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    ids = np.arange(rank, cfg.n, world, dtype=np.int64)
+    return plate_points(cfg, 2, 3, kind, index=ids), plate_points(cfg, 0, 1, kind, index=ids), ids, ids.copy()
 
 
 def make_problem(cfg: PlateConfig | str, kind: str = "iid", seed: int | None = None,

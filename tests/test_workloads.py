@@ -32,3 +32,18 @@ def test_widened_points_on_plate():
 def test_widened_level_cap():
     with pytest.raises(ValueError):
         W.widened(W.CONFIGS["lowd025_1e7"], 8)
+
+
+@pytest.mark.parametrize("kind", ["iid", "stratified"])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_problem_share_is_a_subset(kind, world):
+    """A rank's share (DistributedP2P.from_local input) is exactly the global points at its ids."""
+    c = W.CONFIGS["tiny"]
+    s, t, q = W.make_problem(c, kind=kind)
+    seen = []
+    for r in range(world):
+        a, b, i, j = W.problem_share(c, r, world, kind)
+        assert np.array_equal(a, s[i]) and np.array_equal(b, t[j])
+        assert np.array_equal(W.weights(c.n, c.seed, index=i), q[i])
+        seen.append(i)
+    assert np.array_equal(np.sort(np.concatenate(seen)), np.arange(c.n))
