@@ -56,7 +56,7 @@ MUFU_PER_PAIR_3D = {"laplace3d": 1, "helmholtz3d": 3}  # RSQ; RSQ + SIN + COS
 METRIC = "P2P pair-interactions/s"
 SM_COUNT = 148
 PEAKS_JSON = os.path.join(ROOT, "profiles", "r02_peaks.json")  # tools/peaks.py on a B200 (libp2p_peaks.so)
-FP64_DP_OPS_PER_PAIR = 17  # r^2 + guard + accumulate (6) + the table-driven log (11)
+FP64_DP_OPS_PER_PAIR = 14  # r^2 + guard + accumulate (6) + the table-driven log (8)
 
 
 def _measured_peaks():

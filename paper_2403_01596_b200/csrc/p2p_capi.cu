@@ -9,6 +9,8 @@
 #include <numeric>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing unless a profiler attaches
+
 #include "p2p.h"
 #include "p2p_kernels.cuh"
 #include "plan.h"
@@ -37,6 +39,13 @@ void ck(cudaError_t e, const char *what) {
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
+};
+
+// NVTX range over one ABI call / phase (nsys and ncu timelines: plan, exchange, interior,
+// boundary, gather)
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
 };
 
 }  // namespace
@@ -340,6 +349,7 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.tile_tgt_base = (const int32_t *)P.tile_tgt_base.p;
         a.ns = hp.ns;
         a.flat = hp.flat ? 1 : 0;
+        a.pairs = hp.duo ? 1 : 0;
         a.nbuf = hp.nbuf;
         a.kappa = (T)hp.kappa;
         void *args[] = {&a};
@@ -846,7 +856,8 @@ void build_device_plan(p2p_plan_s &P, const p2p_plan_desc &d, const double *dsrc
         ck(cudaMemsetAsync(err, 0, sizeof(int), s), "memset");
         P.alloc(P.tile_tgt_base, (size_t)nt * 4);
         if (nt)
-            tiled_table_kernel<<<nblocks(nt, 64), 64, 0, s>>>(tiles_m, nt, k, S, ts, hp.pad, hp.tpi, hp.ns, so, to,
+            tiled_table_kernel<<<nblocks(nt, 64), 64, 0, s>>>(tiles_m, nt, k, S, ts, hp.pad, hp.tpi, hp.ns,
+                                                               hp.duo ? 1 : 0, so, to,
                                                              (uint16_t *)P.reg_table.p, reg_sz, slot_sz, item_sz,
                                                              (int32_t *)P.tile_tgt_base.p, err);
         int herr = 0;
@@ -879,12 +890,12 @@ void build_device_plan(p2p_plan_s &P, const p2p_plan_desc &d, const double *dsrc
             ck(cudaMemsetAsync(P.tgt_oix.p, 0xFF, P.tgt_oix.bytes, s), "memset");
             ck(cudaMemsetAsync(P.tgt_ruv.p, 0, P.tgt_ruv.bytes, s), "memset");
         }
-        const size_t slot_smem = (size_t)3 * WW * 4;
+        const size_t slot_smem = (size_t)4 * WW * 4;
         ck(cudaFuncSetAttribute(tiled_slots_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024),
            "smem attr");
         if (nt)
             tiled_slots_kernel<T><<<nblocks(nt, 1), 128, slot_smem, s>>>(
-                tiles_m, nt, k, hp.h, hp.tpi, hp.tsort ? 1 : 0, to, n9, tperm, (const double2 *)dtgt,
+                tiles_m, nt, k, hp.h, hp.tpi, hp.tsort ? 1 : 0, hp.duo ? 1 : 0, to, n9, tperm, (const double2 *)dtgt,
                 (const uint32_t *)P.tgt_pack_off.p, (uint16_t *)P.tgt_bl.p, (uint16_t *)P.tgt_oix.p, (T *)P.tgt_ruv.p);
         // ---- queue order: longest first when the working set fits L2, else Morton with the tail split
         if (hp.ns == 3) {
@@ -1028,6 +1039,7 @@ void p2p_plan_desc_init(p2p_plan_desc *d) {
 }
 
 static p2p_status plan_create_common(const p2p_plan_desc *desc, const p2p::LocalInput *li, p2p_plan *out) {
+    Nvtx nvtx_("p2p_plan_create");
     if (out) *out = nullptr;
     if (!desc || !out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL desc or out");
     std::unique_ptr<p2p_plan_s> P(new (std::nothrow) p2p_plan_s());
@@ -1103,6 +1115,7 @@ p2p_status p2p_partition_route(const p2p_plan_desc *desc, const int64_t *src_ids
 
 p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src_xy, const double *d_tgt_xy,
                                   p2p_plan *out) {
+    Nvtx nvtx_("p2p_plan_create_device");
     if (out) *out = nullptr;
     if (!desc || !out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL desc or out");
     std::unique_ptr<p2p_plan_s> P(new (std::nothrow) p2p_plan_s());
@@ -1146,6 +1159,7 @@ p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src
 }
 
 p2p_status p2p_apply(p2p_plan P, const void *d_q, void *d_out, int32_t order, int32_t accumulate, void *stream) {
+    Nvtx nvtx_("p2p_apply");
     if (!P || !d_q || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or buffer");
     if (order != P2P_ORDER_PLAN && order != P2P_ORDER_USER) return set_error(P2P_ERROR_INVALID_ARGUMENT, "bad order");
     if (P->hp.local_input && order == P2P_ORDER_USER)
@@ -1198,6 +1212,7 @@ p2p_status p2p_apply_dist(p2p_plan P, const void *d_q_owned, const void *d_q_hal
 
 p2p_status p2p_apply_dist_interior(p2p_plan P, const void *d_q_owned, void *d_out, int32_t accumulate,
                                    void *stream) {
+    Nvtx nvtx_("p2p_apply_dist interior");
     if (!P || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or output");
     if (P->hp.n_src_owned && !d_q_owned) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_q_owned");
     return guarded([&] {
@@ -1211,6 +1226,7 @@ p2p_status p2p_apply_dist_interior(p2p_plan P, const void *d_q_owned, void *d_ou
 
 p2p_status p2p_apply_dist_boundary(p2p_plan P, const void *d_q_halo, void *d_out, int32_t accumulate,
                                    void *stream) {
+    Nvtx nvtx_("p2p_apply_dist boundary");
     if (!P || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or output");
     if (P->hp.n_halo && !d_q_halo) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_q_halo");
     return guarded([&] {
@@ -1363,6 +1379,7 @@ void apply_peer_sync_impl(p2p_plan_s &P, const void *d_q_owned, void *d_out, int
         sp.p[r] = (unsigned long long *)ps.sig_peer[r];
     }
     // 1. publish this epoch's send buffer (after every reader is done with the previous one)
+    Nvtx n1("publish + pull halo (exchange)");
     D::peer_publish_kernel<V><<<grid_for(std::max<int64_t>(hp.n_send, 1)), 256, 0, s>>>(
         (const int32_t *)P.send_idx.p, (const V *)d_q_owned, (V *)ps.pub_w.p, hp.n_send, sig, 0, ps.readers_w, ctr,
         (int *)ps.err.p);
@@ -1374,7 +1391,8 @@ void apply_peer_sync_impl(p2p_plan_s &P, const void *d_q_owned, void *d_out, int
         nullptr, 0, (const int32_t *)P.halo_lidx.p, (V *)P.q_local.p, hp.n_halo, ctr + 1, (int *)ps.err.p);
     ck(cudaEventRecord(ps.ev_pull, ps.side), "peer event");
     // 3. interior tiles meanwhile; 4. boundary tiles once the halo is in
-    apply_dist_interior_impl<T>(P, d_q_owned, d_out, accumulate, s);
+    { Nvtx n2("interior tiles"); apply_dist_interior_impl<T>(P, d_q_owned, d_out, accumulate, s); }
+    Nvtx n3("boundary tiles");
     ck(cudaStreamWaitEvent(s, ps.ev_pull, 0), "peer join");
     if (hp.layout == P2P_LAYOUT_TILED)
         launch_p2p<T>(P, (const T *)P.q_local.p, (T *)d_out, accumulate, s, false, hp.n_interior,
@@ -1408,6 +1426,7 @@ void gather_sync_impl(p2p_plan_s &P, const void *d_local, void *d_global, cudaSt
 }  // extern "C++"
 
 p2p_status p2p_apply_peer_sync(p2p_plan P, const void *d_q_owned, void *d_out, int32_t accumulate, void *stream) {
+    Nvtx nvtx_("p2p_apply_peer_sync");
     if (!P || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or output");
     if (P->hp.n_src_owned && !d_q_owned) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_q_owned");
     if (!P->peer.connected) return set_error(P2P_ERROR_INVALID_ARGUMENT, "p2p_peer_connect first");
@@ -1424,6 +1443,7 @@ p2p_status p2p_apply_peer_sync(p2p_plan P, const void *d_q_owned, void *d_out, i
 }
 
 p2p_status p2p_gather(p2p_plan P, const void *d_local, void *d_global, void *stream) {
+    Nvtx nvtx_("p2p_gather (allgatherv)");
     if (!P || !d_global) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or output");
     if (P->hp.n_tgt_local && !d_local) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL d_local");
     if (!P->peer.connected) return set_error(P2P_ERROR_INVALID_ARGUMENT, "p2p_peer_connect first");
@@ -1490,6 +1510,7 @@ p2p_status p2p_ipc_close(void *d_ptr, int64_t offset) {
 }
 
 p2p_status p2p_halo_pack(p2p_plan P, const void *d_q_owned, void *d_send, void *stream) {
+    Nvtx nvtx_("p2p_halo_pack (exchange)");
     if (!P) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan");
     if (P->hp.n_send && (!d_q_owned || !d_send)) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL buffer");
     return guarded([&] {

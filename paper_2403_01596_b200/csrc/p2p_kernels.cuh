@@ -162,24 +162,23 @@ __device__ __noinline__ float span1_f32_guarded(const float2 *__restrict__ UV, c
     }
     return acc;
 }
-// fp64 log, table-driven (libdevice's log is ~30 DP ops; this is ~11): x = m 2^e, m in [1, 2);
-// k = top 7 mantissa bits; LT[k] = (c_inv, -log c_inv) with c_inv ~ 1 / (1 + (k + 1/2)/128) (host,
-// plan_builder.cpp); t = m c_inv - 1 (one fma, |t| < 2^-8); log1p(t) to degree 6 (truncation
-// < 2e-18); log x = e ln2 + (-log c_inv) + log1p(t).  x must be a positive normal double.
-constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
+// fp64 log, table-driven (libdevice's log is ~30 DP ops; this is 8): x = m 2^e, m in [1, 2);
+// k = top 8 mantissa bits; LT[k] = (c_inv, -log c_inv) with c_inv ~ 1 / (1 + (k + 1/2)/256) (host,
+// plan_builder.cpp); t = m c_inv - 1 (one fma, |t| < 2^-9); log1p(t) to degree 5 (truncation
+// < 1e-17); log x = e ln2 + (-log c_inv + log1p(t)), e ln2 in one fma (|e| <= 80 for r^2 >= eps^2:
+// the rounding of ln2 adds < 2e-15 to a result of that size).  x must be a positive normal double.
+constexpr double kLn2d = 6.93147180559945309417e-01;
 __device__ __forceinline__ double log_tab(double x, const double2 *__restrict__ LT) {
     const long long b = __double_as_longlong(x);
     const int e = (int)(b >> 52) - 1023;
-    const double2 c = LT[(int)(b >> 45) & 127];
+    const double2 c = LT[(int)(b >> 44) & 255];
     const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
     const double t = fma(m, c.x, -1.0);
-    double q = fma(t, -1.0 / 6.0, 0.2);
-    q = fma(t, q, -0.25);
+    double q = fma(t, 0.2, -0.25);
     q = fma(t, q, 1.0 / 3.0);
     q = fma(t, q, -0.5);
     const double p = fma(t * t, q, t);
-    const double de = (double)e;
-    return fma(de, kLn2Hi, c.y) + fma(de, kLn2Lo, p);
+    return fma((double)e, kLn2d, c.y + p);
 }
 
 // fp64, (u, v) per entry, explicit guard.
@@ -218,6 +217,45 @@ __device__ __forceinline__ float span3_f32(const float2 *__restrict__ UV, const 
         acc = fmaf(Q[j], lg2_approx(fmaf(dv, dv, du * du)), acc);
     }
     return acc;
+}
+// Two targets of one box (same runs) per thread: each source loaded and each index computed once
+// for both, the two distances in f32x2 (FADD2 x 2, FMUL2, FFMA2 per source).
+__device__ __forceinline__ void span3x2_f32(const float2 *__restrict__ UV, const float *__restrict__ Q,
+                                            const Runs3 &r, float ua, float va, float ub, float vb, float &acca,
+                                            float &accb) {
+    const f2_t U = f2_pack(ua, ub), V = f2_pack(va, vb);
+    float a0 = 0.f, a1 = 0.f;
+    const int v1 = r.v0 + r.n;
+#pragma unroll 2
+    for (int v = r.v0; v < v1; ++v) {
+        const int j = r.at(v);
+        const float2 s = UV[j];
+        const float q = Q[j];
+        const f2_t du = f2_sub(U, f2_pack(s.x, s.x)), dv = f2_sub(V, f2_pack(s.y, s.y));
+        float x0, x1;
+        f2_unpack(f2_fma(dv, dv, f2_mul(du, du)), x0, x1);
+        a0 = fmaf(q, lg2_approx(x0), a0);
+        a1 = fmaf(q, lg2_approx(x1), a1);
+    }
+    acca = a0;
+    accb = a1;
+}
+__device__ __forceinline__ void span1x2_f32(const float2 *__restrict__ UV, const float *__restrict__ Q, int j0, int j1,
+                                            float ua, float va, float ub, float vb, float &acca, float &accb) {
+    const f2_t U = f2_pack(ua, ub), V = f2_pack(va, vb);
+    float a0 = acca, a1 = accb;
+#pragma unroll 2
+    for (int j = j0; j < j1; ++j) {
+        const float2 s = UV[j];
+        const float q = Q[j];
+        const f2_t du = f2_sub(U, f2_pack(s.x, s.x)), dv = f2_sub(V, f2_pack(s.y, s.y));
+        float x0, x1;
+        f2_unpack(f2_fma(dv, dv, f2_mul(du, du)), x0, x1);
+        a0 = fmaf(q, lg2_approx(x0), a0);
+        a1 = fmaf(q, lg2_approx(x1), a1);
+    }
+    acca = a0;
+    accb = a1;
 }
 __device__ __forceinline__ double span3_f64(const double2 *__restrict__ UV, const double *__restrict__ Q,
                                             const Runs3 &r, double ut, double vt, double eps2,
@@ -302,6 +340,7 @@ struct P2PArgs {
     const int32_t *tile_tgt_base;   // TILED: plan index of each tile's first target
     int ns;                     // TILED: work items per target (1 = whole target, 3 = one per row-run)
     int flat;                   // TILED lean path: sweep the three row-runs as one sequence
+    int pairs;                  // TILED lean fp32: the first table[RR + 2] units are 2-target units
     int nbuf;                   // TILED: 2 = prefetch the next tile's record during this tile
     unsigned long long *trace;  // optional per-tile timeline (diagnostics; nullptr = off)
     T *out;
@@ -331,16 +370,31 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 
 // s_q[i] = q[s_idx[i]] (0 for pads) for i = first, first + stride, ... < n, with
 // up to 8 independent L2 loads in flight per thread.
+// q[j] if j >= 0, else 0: one predicated ld.global.nc (no branch, no load for j < 0)
+__device__ __forceinline__ float ldg_pred(const float *q, int j) {
+    float w;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ge.s32 p, %2, 0;\n\tmov.b32 %0, 0;\n\t"
+                 "@p ld.global.nc.f32 %0, [%1];\n\t}"
+                 : "=f"(w) : "l"(q + (j < 0 ? 0 : j)), "r"(j));
+    return w;
+}
+__device__ __forceinline__ double ldg_pred(const double *q, int j) {
+    double w;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ge.s32 p, %2, 0;\n\tmov.b64 %0, 0;\n\t"
+                 "@p ld.global.nc.f64 %0, [%1];\n\t}"
+                 : "=d"(w) : "l"(q + (j < 0 ? 0 : j)), "r"(j));
+    return w;
+}
 template <typename T>
 __device__ __forceinline__ void gather_weights(const int32_t *__restrict__ s_idx, const T *__restrict__ q,
                                                T *__restrict__ s_q, int n, int first, int stride) {
     for (int base = first; base < n; base += 8 * stride) {
         T v[8];
 #pragma unroll
-        for (int x = 0; x < 8; ++x) {
+        for (int x = 0; x < 8; ++x) {  // predicated loads, no branches: pads (-1) and i >= n give 0
             const int i = base + x * stride;
             const int32_t j = i < n ? s_idx[i] : -1;
-            v[x] = j >= 0 ? __ldg(q + j) : (T)0;
+            v[x] = ldg_pred(q, j);
         }
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
@@ -739,7 +793,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
     extern __shared__ __align__(128) unsigned char smem[];
     // next tile + its first target, double-buffered by iteration parity: thread 0 writes slot
     // (it + 1) & 1 during iteration it while the others may still read slot it & 1
-    __shared__ int s_next[2], s_base_next[2];
+    __shared__ int s_next[2], s_base_next[2], s_part_next[2];
     const int k = a.k, W = 1 << k, R = W + 2, RR = R * R;
     const TCarve c = tiled_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI, NS, a.nbuf);
     const bool db = a.nbuf == 2;
@@ -790,11 +844,16 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         s_next[0] = t0;
         if (t0 < a.ntiles) {
             s_base_next[0] = a.tile_tgt_base[a.tile_slot[t0]];
+            s_part_next[0] = a.tile_part[t0];
             issue(t0, 0);
         }
     }
     __syncthreads();
-    int cur = s_next[0], buf = 0, tb = s_base_next[0], it = 0;
+    int cur = s_next[0], buf = 0, tb = s_base_next[0], pinfo = s_part_next[0], it = 0;
+    // loop-invariant launch options, held in registers
+    const int32_t *const out_idx = a.out_idx;
+    T *const out = a.out;
+    const bool accumulate = a.accumulate != 0;
     uint32_t parity = 0u;  // bit b = phase parity of buffer b's mbarrier
 
     while (cur < a.ntiles) {
@@ -816,6 +875,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             s_next[(it + 1) & 1] = nx;
             if (nx < a.ntiles) {
                 s_base_next[(it + 1) & 1] = a.tile_tgt_base[a.tile_slot[nx]];
+                s_part_next[(it + 1) & 1] = a.tile_part[nx];
                 if (db) issue(nx, buf ^ 1);
             }
         }
@@ -831,10 +891,13 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             parity ^= 1u << buf;
         }
         if (trc) trc[2] = gtimer();
-        const int nent = (int)table[RR], nslot = (int)table[RR + 1], nu = nslot / TPI;
+        const int nent = (int)table[RR], nslot = (int)table[RR + 1];
+        // lean fp32 pairs: units [0, npu) are 2-target units (slots 2u, 2u + 1), then single slots
+        const int npu = (LEAN && sizeof(T) == 4 && a.pairs) ? (int)table[RR + 2] : 0;
+        const int nu = nslot / TPI - npu;
         gather_weights(s_idx, a.q, s_q, nent, tid, NT);  // weights through the per-entry index
         __syncthreads();
-        const int pinfo = a.tile_part[cur], npart = pinfo >> 16, ipart = pinfo & 0xffff;
+        const int npart = pinfo >> 16, ipart = pinfo & 0xffff;
         int ub = 0, ue = nu;
         if (npart > 1) {  // tail tile split into npart unit ranges (nu * npart < 2^31)
             ub = (nu * ipart) / npart;
@@ -891,12 +954,36 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             } else {
                 acc = -0.5 * acc;
             }
-            const int oi = a.out_idx ? a.out_idx[tb + o] : tb + o;
-            a.out[oi] = a.accumulate ? a.out[oi] + acc : acc;
+            const int oi = out_idx ? out_idx[tb + o] : tb + o;
+            out[oi] = accumulate ? out[oi] + acc : acc;
         };
 
         if constexpr (LEAN) {  // one thread per target (boxes by n9): three row-runs, flattened or in turn
-            for (int t = ub + tid; t < ue; t += NT) {
+            for (int u = ub + tid; u < ue; u += NT) {
+                if constexpr (sizeof(T) == 4) {
+                    if (u < npu) {  // two targets of one box
+                        const int t0 = 2 * u, jb = tbl[t0];
+                        float r0 = 0.f, r1 = 0.f;
+                        if (a.flat) {
+                            const Runs3 runs(table[jb], table[jb + 3], table[jb + R], table[jb + R + 3],
+                                             table[jb + 2 * R], table[jb + 2 * R + 3]);
+                            span3x2_f32(reinterpret_cast<const float2 *>(s_uv), reinterpret_cast<const float *>(s_q),
+                                        runs, tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t0 + 2], tuv[2 * t0 + 3], r0, r1);
+                        } else {
+#pragma unroll
+                            for (int row = 0; row < 3; ++row) {
+                                const int j0 = jb + row * R;
+                                span1x2_f32(reinterpret_cast<const float2 *>(s_uv),
+                                            reinterpret_cast<const float *>(s_q), table[j0], table[j0 + 3],
+                                            tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t0 + 2], tuv[2 * t0 + 3], r0, r1);
+                            }
+                        }
+                        finish(t0, r0);
+                        finish(t0 + 1, r1);
+                        continue;
+                    }
+                }
+                const int t = npu + u;  // single slots follow the 2-target units' 2 npu slots
                 const int jb = tbl[t];
                 const T ux = tuv[2 * t], uy = tuv[2 * t + 1];
                 T acc = (T)0;
@@ -959,6 +1046,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         ++it;
         cur = s_next[it & 1];
         tb = s_base_next[it & 1];
+        pinfo = s_part_next[it & 1];
         if (db) buf ^= 1;
         else if (tid == 0 && cur < a.ntiles) issue(cur, 0);
     }
@@ -979,10 +1067,34 @@ __device__ __forceinline__ void bessel_j0y0<float>(float x, float &J, float &Y) 
     J = j0f(x);
     Y = y0f(x);
 }
+// fp64, x > 6 (the series covers x <= 6): the modulus / phase form of H0^(1) = J0 + i Y0
+// (A&S 9.2.17, 9.2.28-30): J0 = M cos(theta), Y0 = M sin(theta), M = sqrt(2 / (pi x)) m(w),
+// theta = x - pi/4 + g(w) / x, w = (6 / x)^2; m and g are degree-15 / 17 polynomials in w fitted
+// to 60-digit mpmath values (tools/gen_hankel_coeffs.py; |error| < 2e-17 on x >= 6), so J0 and
+// Y0 carry the ~1e-16 relative error of the fp64 x itself (CUDA's j0 / y0: 5e-12 absolute).
+__constant__ double kHankM[16] = {-1.009491152938711e-08, 8.57361572380178e-08, -3.3621255599445164e-07,
+    8.119914966752918e-07, -1.3646187307687262e-06, 1.7230350554592675e-06, -1.7496035271524972e-06,
+    1.5517824092842689e-06, -1.3504203538737336e-06, 1.3405018556771033e-06, -1.764884373894713e-06,
+    3.481928813934044e-06, -1.1635076105372948e-05, 7.987316710141125e-05, -0.0017361111111073842, 1.0};
+__constant__ double kHankG[18] = {1.0760822573387157e-07, -1.0085244871057431e-06, 4.380518381796627e-06,
+    -1.1732236951590672e-05, 2.1778454372757905e-05, -2.993602677569589e-05, 3.194496675304352e-05,
+    -2.764766382910038e-05, 2.0464690083447213e-05, -1.3981396693431658e-05, 9.833845375076344e-06,
+    -8.117210709175648e-06, 8.851138042211988e-06, -1.3976003481602903e-05, 3.510941725411511e-05,
+    -0.00016170548761511877, 0.001808449074070366, -0.125};
 template <>
 __device__ __forceinline__ void bessel_j0y0<double>(double x, double &J, double &Y) {
-    J = j0(x);
-    Y = y0(x);
+    const double rx = 1.0 / x, w = 36.0 * rx * rx;
+    double m = kHankM[0], g = kHankG[0];
+#pragma unroll
+    for (int i = 1; i < 16; ++i) m = fma(m, w, kHankM[i]);
+#pragma unroll
+    for (int i = 1; i < 18; ++i) g = fma(g, w, kHankG[i]);
+    const double th = (x - 0.78539816339744830962) + g * rx;
+    double s, c;
+    sincos(th, &s, &c);
+    const double M = m * sqrt(0.63661977236758134308 * rx);  // sqrt(2 / (pi x))
+    J = M * c;
+    Y = M * s;
 }
 
 // Small arguments (z = (kappa r / 2)^2 <= kHelmZmax): J0 and Y0 from their ascending series
