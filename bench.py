@@ -72,6 +72,14 @@ def _measured_peaks():
 
 
 MUFU_LG2_PER_CLK_PER_SM, DFMA_PER_CLK_PER_SM, PEAK_BASIS = _measured_peaks()
+try:  # FP32 FMA lanes per clk per SM (FFMA2 = 2 FMA per lane-instruction; peaks.json counts 4 FLOP)
+    FFMA_PER_CLK_PER_SM = json.load(open(PEAKS_JSON))["ffma2"]["per_clk_per_sm"] / 2.0
+except Exception:
+    FFMA_PER_CLK_PER_SM = 128.0
+# 2D Helmholtz, per pair on the series branch (every pair of the kappa h = pi/2 workload):
+# fp32: r^2 4, z 1, two degree-10 Horner chains 20, ln 1 (+ MUFU), Y 2, complex multiply-add 4
+# fp64: r^2 4, z 1, two degree-18 chains 36, the table log 8, ln 1, Y 2, complex multiply-add 4
+HELM_OPS_PER_PAIR = {"fp32": 32, "fp64": 56}
 
 
 def parse():
@@ -97,6 +105,7 @@ def parse():
                          "nccl, whichever ran the faster step (max over ranks)")
     ap.add_argument("--no-graph", action="store_true", help="N > 1 sync mode: launch eagerly, no CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (quick A/B runs)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras/baseline)")
     ap.add_argument("--configs", default="", help="comma list of config names overriding --workload")
@@ -456,16 +465,16 @@ def main():
                     "unit": f"Gpair/s ({m} MUFU per pair)", "frac": achieved / (peak_mufu / m), "traffic": traffic,
                     "peak_basis": f"{MUFU_LG2_PER_CLK_PER_SM:.2f} MUFU/clk/SM x {SM_COUNT} SMs x {peak_clk / 1e6:.0f} MHz "
                                   f"/ {m} per pair; DESIGN.md §9e"}
-    elif args.kernel == "helmholtz":  # issue-bound: instructions per pair from ncu
+    elif args.kernel == "helmholtz":  # FMA-pipe bound at the algorithm's op count
         achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
-        ipp = _helm_inst_per_pair(args.precision)
-        peak = 128 * SM_COUNT * peak_clk / ipp / 1e9 if ipp else None
+        ops = HELM_OPS_PER_PAIR[args.precision]
+        per_clk = FFMA_PER_CLK_PER_SM if args.precision == "fp32" else DFMA_PER_CLK_PER_SM
+        peak = per_clk * SM_COUNT * peak_clk / ops / 1e9
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak,
-                    "unit": f"Gpair/s (issue slots at {ipp} thread-instructions per pair)" if ipp else "Gpair/s",
-                    "frac": achieved / peak if peak else None, "traffic": traffic,
-                    "peak_basis": f"128 lanes x {SM_COUNT} SMs x {peak_clk / 1e6:.0f} MHz issue / thread-instructions "
-                                  "per pair (ncu smsp__thread_inst_executed.sum / pairs, "
-                                  "profiles/helm_inst_per_pair.json)"}
+                    "unit": f"Gpair/s ({ops} {'FP32' if args.precision == 'fp32' else 'FP64'} FMA-pipe ops per pair)",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "peak_basis": f"{per_clk:.1f} FMA/clk/SM x {SM_COUNT} SMs x {peak_clk / 1e6:.0f} MHz / {ops} ops "
+                                  f"per pair (the series branch's algorithmic count, DESIGN.md §9c); {PEAK_BASIS}"}
     elif t_mufu >= t_hbm:
         achieved = pairs_local / (kernel_ms * 1e-3) / 1e9
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak_mufu, "unit": "Gpair/s (1 MUFU.LG2 per pair)",
@@ -493,7 +502,7 @@ def main():
 
     # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
     args.exchange_chosen = mode
-    e2e = _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier)
+    e2e = None if args.no_e2e else _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier)
 
     out = {
         "metric": METRIC, "value": value, "unit": "pair-interactions/s", "n_gpus": world, "steps": args.steps,
@@ -638,14 +647,6 @@ def _e2e_dist(args, jobs, stream, pairs_step, barrier):
                 "config's p2p_apply_dist") + ", D2H of local potentials; max over ranks"}
 
 
-def _helm_inst_per_pair(precision):
-    """Thread-instructions per pair of the Helmholtz kernel, measured by ncu (tools/helm_ipp.py)."""
-    try:
-        return float(json.load(open(os.path.join(ROOT, "profiles", "helm_inst_per_pair.json")))[precision])
-    except Exception:
-        return None
-
-
 def src_sha16():
     """Hash of the operator's sources (csrc/ + include/): ties a committed ncu summary to the code
     it was captured on."""
@@ -677,44 +678,54 @@ def _ncu_traffic(args, names):
 
 
 def _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier):
-    """Same metric through the C ABI with pinned HOST buffers (p2p_apply_host_async):
-    every step copies q host->device, applies (user order: permutation kernels
-    included), copies phi device->host.  Each config runs on its own stream so
-    one config's PCIe copies overlap another's kernels."""
+    """Same metric through the C ABI with pinned HOST buffers (p2p_apply_host_async): every
+    step copies q host->device, applies (user order: permutation kernels included), copies phi
+    device->host.  Steps are pipelined the way a serving loop runs them: each plan has two
+    workspace slots (p2p_plan_set_workspaces) and consecutive steps alternate between two
+    streams per config, so step k's D2H overlaps step k+1's H2D and kernel (each apply waits on
+    the device for the apply that last used its slot)."""
     import torch
     from paper_2403_01596_b200 import p2p
     if world > 1:
         return _e2e_dist(args, jobs, stream, pairs_step, barrier)
     hq = [torch.as_tensor(j["q_user"], dtype=j["plan"].torch_dtype).pin_memory() for j in jobs]
-    ho = [torch.empty(j["info"]["n_tgt"], dtype=j["plan"].torch_dtype).pin_memory() for j in jobs]
+    ho = [[torch.empty(j["info"]["n_tgt"], dtype=j["plan"].torch_dtype).pin_memory() for _ in range(2)]
+          for j in jobs]
     h2d = sum(int(t.numel() * t.element_size()) for t in hq)
-    d2h = sum(int(t.numel() * t.element_size()) for t in ho)
-    side = [torch.cuda.Stream(dev) for _ in jobs]
+    d2h = sum(int(t[0].numel() * t[0].element_size()) for t in ho)
+    for j in jobs:
+        j["plan"].set_workspaces(2)
+    side = [[torch.cuda.Stream(dev) for _ in range(2)] for _ in jobs]
 
-    def step():
+    def run(steps):
         start = torch.cuda.Event()
         start.record(stream)
-        for j, a, b, st in zip(jobs, hq, ho, side):
-            st.wait_event(start)
-            p2p.p2p_apply_host_async(j["plan"].handle, a.data_ptr(), b.data_ptr(), p2p.P2P_ORDER_USER, 0,
-                                     st.cuda_stream)
-            done = torch.cuda.Event()
-            done.record(st)
-            stream.wait_event(done)
+        for ss in side:
+            for st in ss:
+                st.wait_event(start)
+        for k in range(steps):
+            for j, a, b, ss in zip(jobs, hq, ho, side):
+                st = ss[k % 2]
+                p2p.p2p_apply_host_async(j["plan"].handle, a.data_ptr(), b[k % 2].data_ptr(), p2p.P2P_ORDER_USER, 0,
+                                         st.cuda_stream)
+        for ss in side:
+            for st in ss:
+                done = torch.cuda.Event()
+                done.record(st)
+                stream.wait_event(done)
 
-    for _ in range(3):
-        step()
+    run(3)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        step()
+    run(args.steps)
     e1.record(stream)
     barrier()
     ms = e0.elapsed_time(e1) / args.steps
     return {"value": pairs_step / (ms * 1e-3), "unit": "pair-interactions/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms,
-            "path": "p2p_apply_host_async, pinned host buffers, user order, one stream per config"}
+            "path": "p2p_apply_host_async, pinned host buffers, user order; two workspace slots per plan, "
+                    "consecutive steps on alternating streams (step k's D2H overlaps step k+1's H2D + kernel)"}
 
 
 def _plan_build(args, jobs, dev):

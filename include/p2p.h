@@ -191,6 +191,18 @@ p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src
 p2p_status p2p_apply(p2p_plan plan, const void *d_q, void *d_out, int32_t order,
                      int32_t accumulate, void *stream);
 
+/* Applies in flight: by default a plan has one workspace (gathered weights, partial results,
+ * staging for host buffers, the tile queue), so applies on one plan must be serialised on one
+ * stream (applies on different plans may overlap freely).  p2p_plan_set_workspaces(plan, n)
+ * (1 <= n <= 8) gives the plan n workspace slots, rotated over p2p_apply / p2p_apply_host /
+ * p2p_apply_host_async calls: up to n applies of one plan may then be in flight on different
+ * streams -- e.g. step k's D2H overlapping step k+1's H2D and kernel; each apply waits on the
+ * device (an event) for the apply that last used its slot, so no host synchronisation is
+ * needed.  Calls from several host threads on one plan must still be serialised.  Single-
+ * partition NR / R / TILED / 3D / ADAPTIVE plans (NOT_SUPPORTED for part_world > 1 and the
+ * paper's layouts).  Extra device memory: n - 1 copies of the workspace. */
+p2p_status p2p_plan_set_workspaces(p2p_plan plan, int32_t n);
+
 /* Same operation with HOST buffers (h_q: n_src weights, h_out: n_tgt_local
  * (ORDER_PLAN) or n_tgt (ORDER_USER) results).  Copies h_q to the device,
  * applies, copies the result back and synchronises `stream`.  For full copy

@@ -58,7 +58,16 @@ struct p2p_plan_s {
     DevBuf pi_src_xy, pi_tgt_xy, pi_nei_off, pi_nei_idx, pr_records, pr_slot, phi_user, paper_q, halo_lidx, tiles, src_off, tgt_off, src_uv, tgt_uv, src_gidx, src_uidx, tgt_uidx, send_idx;
     DevBuf halo_off, halo_idx, halo_uv, halo_q;
     DevBuf tile_slot, tile_part, reg_off, reg_idx, reg_uidx, reg_uv, reg_table, tgt_bl, tgt_oix, item_off, items, log_tab, tgt_ruv, tgt_pack_off, tile_tgt_base;
-    DevBuf q_local, phi, io_q, io_out, queue;  // workspace
+    DevBuf q_local, phi, io_q, io_out, queue;  // workspace (the active slot's buffers)
+    // p2p_plan_set_workspaces: n workspace slots rotated over p2p_apply / p2p_apply_host* so up
+    // to n applies of one plan can be in flight on different streams; each apply waits (device
+    // side, an event) for the apply that last used its slot.  Empty = one slot, the fields above.
+    struct Workspace {
+        DevBuf q_local, phi, io_q, io_out, queue;
+        cudaEvent_t done = nullptr;
+    };
+    std::vector<Workspace> ws;
+    size_t ws_next = 0;
     DevBuf leaf_rng, leaf_org, ul_off, ul_leaf, src_cell, tgt_cell;  // ADAPTIVE (NEXT-4)
     DevBuf halo_owner, halo_oidx;                // peer-memory halo: owner rank, owner-local index per halo slot
     struct PeerSync {                            // device-synchronised peer exchange (p2p_apply_peer_sync, p2p_gather)
@@ -93,6 +102,15 @@ struct p2p_plan_s {
         device_bytes += (int64_t)bytes;
     }
     void release() {
+        if (!ws.empty()) {  // the fields alias one slot: free the slots, then forget the aliases
+            for (Workspace &w : ws) {
+                for (DevBuf *b : {&w.q_local, &w.phi, &w.io_q, &w.io_out, &w.queue})
+                    if (b->p) cudaFree(b->p);
+                if (w.done) cudaEventDestroy(w.done);
+            }
+            ws.clear();
+            q_local = phi = io_q = io_out = queue = DevBuf{};
+        }
         DevBuf *all[] = {&pi_src_xy, &pi_tgt_xy, &pi_nei_off, &pi_nei_idx, &pr_records, &pr_slot, &phi_user, &paper_q, &halo_lidx, &tiles, &src_off, &tgt_off, &src_uv, &tgt_uv, &src_gidx, &src_uidx, &tgt_uidx,
                          &send_idx, &halo_off, &halo_idx, &halo_uv, &halo_q,
                          &tile_slot, &tile_part, &reg_off, &reg_idx, &reg_uidx, &reg_uv, &reg_table, &tgt_bl, &tgt_oix, &item_off, &items, &log_tab, &tgt_ruv,
@@ -349,7 +367,6 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.tile_tgt_base = (const int32_t *)P.tile_tgt_base.p;
         a.ns = hp.ns;
         a.flat = hp.flat ? 1 : 0;
-        a.pairs = hp.duo ? 1 : 0;
         a.nbuf = hp.nbuf;
         a.kappa = (T)hp.kappa;
         void *args[] = {&a};
@@ -856,8 +873,7 @@ void build_device_plan(p2p_plan_s &P, const p2p_plan_desc &d, const double *dsrc
         ck(cudaMemsetAsync(err, 0, sizeof(int), s), "memset");
         P.alloc(P.tile_tgt_base, (size_t)nt * 4);
         if (nt)
-            tiled_table_kernel<<<nblocks(nt, 64), 64, 0, s>>>(tiles_m, nt, k, S, ts, hp.pad, hp.tpi, hp.ns,
-                                                               hp.duo ? 1 : 0, so, to,
+            tiled_table_kernel<<<nblocks(nt, 64), 64, 0, s>>>(tiles_m, nt, k, S, ts, hp.pad, hp.tpi, hp.ns, so, to,
                                                              (uint16_t *)P.reg_table.p, reg_sz, slot_sz, item_sz,
                                                              (int32_t *)P.tile_tgt_base.p, err);
         int herr = 0;
@@ -890,12 +906,12 @@ void build_device_plan(p2p_plan_s &P, const p2p_plan_desc &d, const double *dsrc
             ck(cudaMemsetAsync(P.tgt_oix.p, 0xFF, P.tgt_oix.bytes, s), "memset");
             ck(cudaMemsetAsync(P.tgt_ruv.p, 0, P.tgt_ruv.bytes, s), "memset");
         }
-        const size_t slot_smem = (size_t)4 * WW * 4;
+        const size_t slot_smem = (size_t)3 * WW * 4;
         ck(cudaFuncSetAttribute(tiled_slots_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024),
            "smem attr");
         if (nt)
             tiled_slots_kernel<T><<<nblocks(nt, 1), 128, slot_smem, s>>>(
-                tiles_m, nt, k, hp.h, hp.tpi, hp.tsort ? 1 : 0, hp.duo ? 1 : 0, to, n9, tperm, (const double2 *)dtgt,
+                tiles_m, nt, k, hp.h, hp.tpi, hp.tsort ? 1 : 0, to, n9, tperm, (const double2 *)dtgt,
                 (const uint32_t *)P.tgt_pack_off.p, (uint16_t *)P.tgt_bl.p, (uint16_t *)P.tgt_oix.p, (T *)P.tgt_ruv.p);
         // ---- queue order: longest first when the working set fits L2, else Morton with the tail split
         if (hp.ns == 3) {
@@ -1158,6 +1174,69 @@ p2p_status p2p_plan_create_device(const p2p_plan_desc *desc, const double *d_src
     return st;
 }
 
+namespace {
+// Selects the next workspace slot for one apply (stream-ordered wait on its last user) and
+// records the slot's event when the apply's work is enqueued.
+struct WsSlot {
+    p2p_plan_s &P;
+    cudaStream_t s;
+    p2p_plan_s::Workspace *w = nullptr;
+    WsSlot(p2p_plan_s &P_, cudaStream_t s_) : P(P_), s(s_) {
+        if (P.ws.size() < 2) return;
+        w = &P.ws[P.ws_next++ % P.ws.size()];
+        ck(cudaStreamWaitEvent(s, w->done, 0), "workspace wait");
+        P.q_local = w->q_local;
+        P.phi = w->phi;
+        P.io_q = w->io_q;
+        P.io_out = w->io_out;
+        P.queue = w->queue;
+    }
+    ~WsSlot() {
+        if (w) cudaEventRecord(w->done, s);
+    }
+};
+}  // namespace
+
+p2p_status p2p_plan_set_workspaces(p2p_plan P, int32_t n) {
+    if (!P || n < 1 || n > 8) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or n outside 1..8");
+    if (P->hp.part_world > 1) return set_error(P2P_ERROR_NOT_SUPPORTED, "workspace slots: single-partition plans");
+    if (P->hp.layout == P2P_LAYOUT_PAPER_INDEXING || P->hp.layout == P2P_LAYOUT_PAPER_REPETITION)
+        return set_error(P2P_ERROR_NOT_SUPPORTED, "workspace slots: not for the paper's layouts");
+    return guarded([&] {
+        require_device(P);
+        DeviceGuard g(P->device);
+        auto &ws = P->ws;
+        if (ws.empty()) {  // slot 0 = the plan's own buffers
+            ws.resize(1);
+            ws[0].q_local = P->q_local;
+            ws[0].phi = P->phi;
+            ws[0].io_q = P->io_q;
+            ws[0].io_out = P->io_out;
+            ws[0].queue = P->queue;
+            ck(cudaEventCreateWithFlags(&ws[0].done, cudaEventDisableTiming), "workspace event");
+            ck(cudaEventRecord(ws[0].done, P->stream), "workspace event");
+        }
+        while ((int)ws.size() < n) {
+            p2p_plan_s::Workspace w;
+            auto mk = [&](DevBuf &b, size_t bytes) {
+                b.bytes = bytes;
+                ck(cudaMalloc(&b.p, std::max<size_t>(bytes, 16)), "cudaMalloc workspace");
+                P->device_bytes += (int64_t)bytes;
+            };
+            mk(w.q_local, ws[0].q_local.bytes);
+            mk(w.phi, ws[0].phi.bytes);
+            mk(w.io_q, ws[0].io_q.bytes);
+            mk(w.io_out, ws[0].io_out.bytes);
+            mk(w.queue, 16);
+            ck(cudaMemset(w.queue.p, 0, 16), "queue init");  // kernels reset it on exit
+            ck(cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming), "workspace event");
+            ck(cudaEventRecord(w.done, P->stream), "workspace event");
+            ws.push_back(w);
+        }
+        ck(cudaDeviceSynchronize(), "workspace init");
+    });
+}
+
 p2p_status p2p_apply(p2p_plan P, const void *d_q, void *d_out, int32_t order, int32_t accumulate, void *stream) {
     Nvtx nvtx_("p2p_apply");
     if (!P || !d_q || !d_out) return set_error(P2P_ERROR_INVALID_ARGUMENT, "NULL plan or buffer");
@@ -1168,6 +1247,7 @@ p2p_status p2p_apply(p2p_plan P, const void *d_q, void *d_out, int32_t order, in
         require_device(P);
         DeviceGuard g(P->device);
         cudaStream_t s = (cudaStream_t)stream;
+        WsSlot slot(*P, s);
         if (P->elem == 4) apply_impl<float>(*P, d_q, d_out, order, accumulate ? 1 : 0, s);
         else apply_impl<double>(*P, d_q, d_out, order, accumulate ? 1 : 0, s);
     });
@@ -1183,6 +1263,7 @@ static p2p_status apply_host_common(p2p_plan P, const void *h_q, void *h_out, in
         DeviceGuard g(P->device);
         cudaStream_t s = (cudaStream_t)stream;
         const p2p::HostPlan &hp = P->hp;
+        WsSlot slot(*P, s);
         const size_t qb = (size_t)hp.n_src * P->elem * P->comps;
         const size_t ob = (size_t)(order == P2P_ORDER_USER ? hp.n_tgt : hp.n_tgt_local) * P->elem * P->comps;
         ck(cudaMemcpyAsync(P->io_q.p, h_q, qb, cudaMemcpyHostToDevice, s), "H2D q");

@@ -167,18 +167,32 @@ __device__ __noinline__ float span1_f32_guarded(const float2 *__restrict__ UV, c
 // plan_builder.cpp); t = m c_inv - 1 (one fma, |t| < 2^-9); log1p(t) to degree 5 (truncation
 // < 1e-17); log x = e ln2 + (-log c_inv + log1p(t)), e ln2 in one fma (|e| <= 80 for r^2 >= eps^2:
 // the rounding of ln2 adds < 2e-15 to a result of that size).  x must be a positive normal double.
+// (P2P_LOG256 = 0: round 1's 128-entry table, degree 6, ln2 split hi / lo: 11 DP ops.)
 constexpr double kLn2d = 6.93147180559945309417e-01;
+constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
 __device__ __forceinline__ double log_tab(double x, const double2 *__restrict__ LT) {
     const long long b = __double_as_longlong(x);
     const int e = (int)(b >> 52) - 1023;
-    const double2 c = LT[(int)(b >> 44) & 255];
     const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+#if P2P_LOG256
+    const double2 c = LT[(int)(b >> 44) & 255];
     const double t = fma(m, c.x, -1.0);
     double q = fma(t, 0.2, -0.25);
     q = fma(t, q, 1.0 / 3.0);
     q = fma(t, q, -0.5);
     const double p = fma(t * t, q, t);
     return fma((double)e, kLn2d, c.y + p);
+#else
+    const double2 c = LT[(int)(b >> 45) & 127];
+    const double t = fma(m, c.x, -1.0);
+    double q = fma(t, -1.0 / 6.0, 0.2);
+    q = fma(t, q, -0.25);
+    q = fma(t, q, 1.0 / 3.0);
+    q = fma(t, q, -0.5);
+    const double p = fma(t * t, q, t);
+    const double de = (double)e;
+    return fma(de, kLn2Hi, c.y) + fma(de, kLn2Lo, p);
+#endif
 }
 
 // fp64, (u, v) per entry, explicit guard.
@@ -217,45 +231,6 @@ __device__ __forceinline__ float span3_f32(const float2 *__restrict__ UV, const 
         acc = fmaf(Q[j], lg2_approx(fmaf(dv, dv, du * du)), acc);
     }
     return acc;
-}
-// Two targets of one box (same runs) per thread: each source loaded and each index computed once
-// for both, the two distances in f32x2 (FADD2 x 2, FMUL2, FFMA2 per source).
-__device__ __forceinline__ void span3x2_f32(const float2 *__restrict__ UV, const float *__restrict__ Q,
-                                            const Runs3 &r, float ua, float va, float ub, float vb, float &acca,
-                                            float &accb) {
-    const f2_t U = f2_pack(ua, ub), V = f2_pack(va, vb);
-    float a0 = 0.f, a1 = 0.f;
-    const int v1 = r.v0 + r.n;
-#pragma unroll 2
-    for (int v = r.v0; v < v1; ++v) {
-        const int j = r.at(v);
-        const float2 s = UV[j];
-        const float q = Q[j];
-        const f2_t du = f2_sub(U, f2_pack(s.x, s.x)), dv = f2_sub(V, f2_pack(s.y, s.y));
-        float x0, x1;
-        f2_unpack(f2_fma(dv, dv, f2_mul(du, du)), x0, x1);
-        a0 = fmaf(q, lg2_approx(x0), a0);
-        a1 = fmaf(q, lg2_approx(x1), a1);
-    }
-    acca = a0;
-    accb = a1;
-}
-__device__ __forceinline__ void span1x2_f32(const float2 *__restrict__ UV, const float *__restrict__ Q, int j0, int j1,
-                                            float ua, float va, float ub, float vb, float &acca, float &accb) {
-    const f2_t U = f2_pack(ua, ub), V = f2_pack(va, vb);
-    float a0 = acca, a1 = accb;
-#pragma unroll 2
-    for (int j = j0; j < j1; ++j) {
-        const float2 s = UV[j];
-        const float q = Q[j];
-        const f2_t du = f2_sub(U, f2_pack(s.x, s.x)), dv = f2_sub(V, f2_pack(s.y, s.y));
-        float x0, x1;
-        f2_unpack(f2_fma(dv, dv, f2_mul(du, du)), x0, x1);
-        a0 = fmaf(q, lg2_approx(x0), a0);
-        a1 = fmaf(q, lg2_approx(x1), a1);
-    }
-    acca = a0;
-    accb = a1;
 }
 __device__ __forceinline__ double span3_f64(const double2 *__restrict__ UV, const double *__restrict__ Q,
                                             const Runs3 &r, double ut, double vt, double eps2,
@@ -340,7 +315,6 @@ struct P2PArgs {
     const int32_t *tile_tgt_base;   // TILED: plan index of each tile's first target
     int ns;                     // TILED: work items per target (1 = whole target, 3 = one per row-run)
     int flat;                   // TILED lean path: sweep the three row-runs as one sequence
-    int pairs;                  // TILED lean fp32: the first table[RR + 2] units are 2-target units
     int nbuf;                   // TILED: 2 = prefetch the next tile's record during this tile
     unsigned long long *trace;  // optional per-tile timeline (diagnostics; nullptr = off)
     T *out;
@@ -850,10 +824,6 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
     }
     __syncthreads();
     int cur = s_next[0], buf = 0, tb = s_base_next[0], pinfo = s_part_next[0], it = 0;
-    // loop-invariant launch options, held in registers
-    const int32_t *const out_idx = a.out_idx;
-    T *const out = a.out;
-    const bool accumulate = a.accumulate != 0;
     uint32_t parity = 0u;  // bit b = phase parity of buffer b's mbarrier
 
     while (cur < a.ntiles) {
@@ -891,10 +861,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             parity ^= 1u << buf;
         }
         if (trc) trc[2] = gtimer();
-        const int nent = (int)table[RR], nslot = (int)table[RR + 1];
-        // lean fp32 pairs: units [0, npu) are 2-target units (slots 2u, 2u + 1), then single slots
-        const int npu = (LEAN && sizeof(T) == 4 && a.pairs) ? (int)table[RR + 2] : 0;
-        const int nu = nslot / TPI - npu;
+        const int nent = (int)table[RR], nslot = (int)table[RR + 1], nu = nslot / TPI;
         gather_weights(s_idx, a.q, s_q, nent, tid, NT);  // weights through the per-entry index
         __syncthreads();
         const int npart = pinfo >> 16, ipart = pinfo & 0xffff;
@@ -954,36 +921,12 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             } else {
                 acc = -0.5 * acc;
             }
-            const int oi = out_idx ? out_idx[tb + o] : tb + o;
-            out[oi] = accumulate ? out[oi] + acc : acc;
+            const int oi = a.out_idx ? a.out_idx[tb + o] : tb + o;
+            a.out[oi] = a.accumulate ? a.out[oi] + acc : acc;
         };
 
         if constexpr (LEAN) {  // one thread per target (boxes by n9): three row-runs, flattened or in turn
-            for (int u = ub + tid; u < ue; u += NT) {
-                if constexpr (sizeof(T) == 4) {
-                    if (u < npu) {  // two targets of one box
-                        const int t0 = 2 * u, jb = tbl[t0];
-                        float r0 = 0.f, r1 = 0.f;
-                        if (a.flat) {
-                            const Runs3 runs(table[jb], table[jb + 3], table[jb + R], table[jb + R + 3],
-                                             table[jb + 2 * R], table[jb + 2 * R + 3]);
-                            span3x2_f32(reinterpret_cast<const float2 *>(s_uv), reinterpret_cast<const float *>(s_q),
-                                        runs, tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t0 + 2], tuv[2 * t0 + 3], r0, r1);
-                        } else {
-#pragma unroll
-                            for (int row = 0; row < 3; ++row) {
-                                const int j0 = jb + row * R;
-                                span1x2_f32(reinterpret_cast<const float2 *>(s_uv),
-                                            reinterpret_cast<const float *>(s_q), table[j0], table[j0 + 3],
-                                            tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t0 + 2], tuv[2 * t0 + 3], r0, r1);
-                            }
-                        }
-                        finish(t0, r0);
-                        finish(t0 + 1, r1);
-                        continue;
-                    }
-                }
-                const int t = npu + u;  // single slots follow the 2-target units' 2 npu slots
+            for (int t = ub + tid; t < ue; t += NT) {
                 const int jb = tbl[t];
                 const T ux = tuv[2 * t], uy = tuv[2 * t + 1];
                 T acc = (T)0;
@@ -1025,7 +968,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                 for (int x = 0; x < TPI; ++x) finish(TPI * u + x, acc[x]);
             }
         } else {  // (unit, row) items in the plan's order, then the fixed-order reduction of the partials
-            for (int it = 3 * ub + tid; it < 3 * ue; it += NT) {
+            for (int it = 3 * ub + tid; it < 3 * ue; it += NT) {  // the plan's LPT-dealt batches, static
                 const int w = items[it], u = w >> 2, row = w & 3;
                 T res[TPI];
                 unit_row(u, row, res);

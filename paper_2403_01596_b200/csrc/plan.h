@@ -21,7 +21,11 @@ namespace p2p {
 // ---- shared-memory layouts of the P2P kernels (byte offsets), used by the
 // plan builder (sizing), the launcher and the kernels (carving).
 P2P_HD inline int align16(int x) { return (x + 15) & ~15; }
-constexpr int kLogTab = 256;  // fp64 log: table of (1/c_k rounded, -log of it), c_k = 1 + (k + 1/2) / 256
+#ifndef P2P_LOG256
+#define P2P_LOG256 1  // fp64 log: 256-entry table + degree-5 log1p (0: round 1's 128 entries + degree 6)
+#endif
+// fp64 log: table of (1/c_k rounded, -log of it), c_k = 1 + (k + 1/2) / kLogTab
+constexpr int kLogTab = P2P_LOG256 ? 256 : 128;
 
 struct NrCarve {
     int sstart, gstart, cnt, toff, pstart, uj0, ut, tslot, tu, tv, part, src, ltab, total, ucap;
@@ -86,8 +90,7 @@ struct TCarve {
 // (multiple of 8); tpi: slots per unit; ns: items per unit (1, or 3 row-runs).
 P2P_HD inline int tiled_table_stride(int k) {
     const int W = 1 << k, R = W + 2;
-    // uint16: region box starts [R*R + 1], the tile's slot count, its 2-target unit count (lean pairs)
-    return (R * R + 3 + 7) & ~7;
+    return (R * R + 2 + 7) & ~7;  // uint16: region box starts [R*R + 1], then the tile's slot count
 }
 P2P_HD inline int tiled_item_cap(int slot_cap, int tpi, int ns) {
     return ns == 3 ? (3 * (slot_cap / tpi) + 7) & ~7 : 0;
@@ -278,7 +281,6 @@ struct HostPlan {
     bool lean = false;                            // TILED lean kernel path (tpi 1, ns 1, unpadded)
     bool tsort = false;                           // ns 1: target boxes of a tile ordered by n9 (descending)
     bool flat = false;                            // lean path: row-runs swept as one sequence (sparse)
-    bool duo = false;                             // lean fp32: 2-target units for boxes holding >= 2 targets
     std::vector<double> log_tab;                  // fp64: kLogTab x (c_inv, -log c_inv) for the table-driven log
 
     // ---- the paper's layouts (PAPER_INDEXING / PAPER_REPETITION)

@@ -617,10 +617,6 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     // row loops (P2P_FLAT overrides)
     hp.flat = hp.lean && (hp.density_occ < 3.0 || d.precision == P2P_FP64);
     if (const char *v = std::getenv("P2P_FLAT")) hp.flat = hp.lean && std::atoi(v) != 0;
-    // lean fp32 Laplace: two targets of one box per thread share every index computation and
-    // source load (boxes with >= 2 targets; their 2-target units first, then the single slots)
-    hp.duo = hp.lean && d.precision == P2P_FP32 && d.kernel == P2P_KERNEL_LAPLACE_2D;
-    if (const char *v = std::getenv("P2P_PAIRS")) hp.duo = hp.duo && std::atoi(v) != 0;
     if (d.kernel == P2P_KERNEL_HELMHOLTZ_2D) {  // one thread per target, n9-sorted, flattened runs
         hp.tpi = 1;
         hp.pad = false;
@@ -1276,11 +1272,6 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp, const LocalInput *li)
             hp.tile_tgt_base[i] = hp.tgt_off[m0];
             hp.tgt_pack_off[i + 1] = hp.tgt_pack_off[i] + (uint32_t)pad8(n);
             hp.reg_table[i * ts + R * R + 1] = (uint16_t)n;
-            if (hp.duo) {  // 2-target units: floor(c / 2) per box
-                int64_t np2 = 0;
-                for (int64_t bl = 0; bl < WW; ++bl) np2 += (hp.tgt_off[m0 + bl + 1] - hp.tgt_off[m0 + bl]) / 2;
-                hp.reg_table[i * ts + R * R + 2] = (uint16_t)np2;
-            }
         }
         const int64_t np = hp.tgt_pack_off[nlt];
         hp.tgt_bl.assign((size_t)np, 0);
@@ -1301,19 +1292,12 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp, const LocalInput *li)
                 if (hp.tsort)
                     std::stable_sort(order.begin(), order.end(),
                                      [&](int32_t x, int32_t y) { return n9[(size_t)(m0 + x)] > n9[(size_t)(m0 + y)]; });
-                // slot of the x-th target of each box, in `order`: pairs plans put the boxes'
-                // 2-target units first (boxes in order), then the boxes' odd last targets
-                int64_t jpair = hp.tgt_pack_off[i], jsing = jpair;
-                if (hp.duo)
-                    for (int32_t bl : order) jsing += 2 * ((hp.tgt_off[m0 + bl + 1] - hp.tgt_off[m0 + bl]) / 2);
                 int64_t j = hp.tgt_pack_off[i];
                 for (int32_t bl : order) {
                     const int64_t b = m0 + bl, ns_b = box_slots(b);
                     uint32_t bx, by;
                     morton_decode((uint32_t)bl, bx, by);
-                    const int64_t paired = hp.duo ? 2 * (ns_b / 2) : 0;
                     for (int64_t x = 0; x < ns_b; ++x, ++j) {
-                        if (hp.duo) j = x < paired ? jpair++ : jsing++;
                         const int64_t g = std::min<int64_t>(hp.tgt_off[b] + x, hp.tgt_off[b + 1] - 1);
                         const int64_t u = hp.tgt_uidx[g];
                         hp.tgt_bl[j] = (uint16_t)(by * R + bx);

@@ -257,8 +257,7 @@ __global__ void iota_kernel(int32_t *__restrict__ p, int64_t n) {
 // row-major order, then the region size and the slot count), the region's padded size and the
 // tile's slot and item counts.  err[0] |= 1: region > 65535 entries; |= 2: slot limit exceeded.
 __global__ void tiled_table_kernel(const int32_t *__restrict__ tiles, int64_t nt, int k, int64_t S, int ts, int pad,
-                                   int tpi, int ns, int pairs, const int32_t *__restrict__ so,
-                                   const int32_t *__restrict__ to,
+                                   int tpi, int ns, const int32_t *__restrict__ so, const int32_t *__restrict__ to,
                                    uint16_t *__restrict__ table, uint32_t *__restrict__ reg_sz,
                                    uint32_t *__restrict__ slot_sz, uint32_t *__restrict__ item_sz,
                                    int32_t *__restrict__ tgt_base, int *err) {
@@ -280,15 +279,13 @@ __global__ void tiled_table_kernel(const int32_t *__restrict__ tiles, int64_t nt
         tab[R * R] = (uint16_t)run;
         reg_sz[i] = (uint32_t)p4(run);
         const int64_t m0 = t * WW;
-        int64_t n = 0, np2 = 0;
+        int64_t n = 0;
         for (int64_t bl = 0; bl < WW; ++bl) {
             const int64_t c = to[m0 + bl + 1] - to[m0 + bl];
             n += tpi == 2 ? c + (c & 1) : c;
-            np2 += c / 2;
         }
         if (n > (ns == 3 ? 16383 * tpi : 65534)) atomicOr(err, 2);
         tab[R * R + 1] = (uint16_t)n;
-        if (pairs) tab[R * R + 2] = (uint16_t)np2;  // lean pairs: 2-target units
         slot_sz[i] = (uint32_t)p8(n);
         item_sz[i] = ns == 3 ? (uint32_t)p8(3 * (n / tpi)) : 0u;  // NS = 3: (unit, row-run) items
         tgt_base[i] = to[m0];
@@ -337,17 +334,16 @@ __global__ void tiled_region_kernel(const int32_t *__restrict__ tiles, int64_t n
 // descending n9 (stable), each box's targets in plan order; tpi = 2: an odd box ends with a
 // duplicate of its last target (output index 0xFFFF).  Per slot: coordinates relative to the
 // region origin, row-run base j0 = by R + bx, tile-local output index.
-// Dynamic smem: 4 int32 per box of the tile (WW <= 4096).
+// Dynamic smem: 3 int32 per box of the tile (WW <= 4096).
 template <typename T>
 __global__ void tiled_slots_kernel(const int32_t *__restrict__ tiles, int64_t nt, int k, double h, int tpi, int tsort,
-                                   int pairs, const int32_t *__restrict__ to, const int32_t *__restrict__ n9,
+                                   const int32_t *__restrict__ to, const int32_t *__restrict__ n9,
                                    const int32_t *__restrict__ tperm, const double2 *__restrict__ txy,
                                    const uint32_t *__restrict__ pack_off, uint16_t *__restrict__ bl_out,
                                    uint16_t *__restrict__ oix_out, T *__restrict__ ruv) {
     extern __shared__ int32_t sm[];
     const int WW = 1 << (2 * k), W = 1 << k, R = W + 2;
-    // nonempty boxes (Morton order), n9, slot start, (pairs) slot of the odd last target
-    int32_t *box = sm, *key = sm + WW, *start = sm + 2 * WW, *single = sm + 3 * WW;
+    int32_t *box = sm, *key = sm + WW, *start = sm + 2 * WW;  // nonempty boxes (Morton order), n9, slot start
     __shared__ int nbox;
     for (int64_t i = blockIdx.x; i < nt; i += gridDim.x) {
         const int64_t t = tiles[i], m0 = t * WW;
@@ -384,14 +380,8 @@ __global__ void tiled_slots_kernel(const int32_t *__restrict__ tiles, int64_t nt
                 const int64_t b = m0 + box[a];
                 const int c = to[b + 1] - to[b];
                 start[a] = s;
-                s += pairs ? 2 * (c / 2) : tpi == 2 ? c + (c & 1) : c;
+                s += tpi == 2 ? c + (c & 1) : c;
             }
-            if (pairs)  // the odd last targets follow every 2-target unit, boxes in the same order
-                for (int r = 0; r < m; ++r) {
-                    const int a = key[r];
-                    const int64_t b = m0 + box[a];
-                    if ((to[b + 1] - to[b]) & 1) single[a] = s++;
-                }
         }
         __syncthreads();
         const int64_t tx = compact((uint32_t)t), ty = compact((uint32_t)t >> 1);
@@ -403,7 +393,6 @@ __global__ void tiled_slots_kernel(const int32_t *__restrict__ tiles, int64_t nt
             const uint32_t bx = compact((uint32_t)bl), by = compact((uint32_t)bl >> 1);
             int64_t j = (int64_t)pack_off[i] + start[a];
             for (int x = 0; x < nsl; ++x, ++j) {
-                if (pairs && x == 2 * (c / 2)) j = (int64_t)pack_off[i] + single[a];
                 const int64_t g = min((int64_t)to[b] + x, (int64_t)to[b + 1] - 1);
                 const double2 p = txy[tperm[g]];
                 bl_out[j] = (uint16_t)(by * R + bx);

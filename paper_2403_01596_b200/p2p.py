@@ -61,7 +61,7 @@ ABI_SYMBOLS = (
     "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_gather_peer", "p2p_ipc_export", "p2p_ipc_open", "p2p_ipc_close", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export",
     "p2p_status_string", "p2p_last_error", "p2p_abi_version",
     "p2p_peer_buffers", "p2p_peer_connect", "p2p_apply_peer_sync", "p2p_gather", "p2p_peer_check",
-    "p2p_box_counts", "p2p_partition_route", "p2p_plan_create_local",
+    "p2p_box_counts", "p2p_partition_route", "p2p_plan_create_local", "p2p_plan_set_workspaces",
 )
 
 
@@ -115,6 +115,20 @@ def load_library() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
+    if os.environ.get("P2P_LIB"):  # A/B experiments with older builds: skip symbols they lack
+        class _Tolerant:
+            def __init__(self, l):
+                object.__setattr__(self, "_l", l)
+
+            def __getattr__(self, name):
+                try:
+                    return getattr(self._l, name)
+                except AttributeError:
+                    return C.CFUNCTYPE(None)()  # placeholder; calling it is an error
+
+            def __setattr__(self, name, v):
+                setattr(self._l, name, v)
+        lib = _Tolerant(lib)
     P, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
     lib.p2p_plan_desc_init.argtypes = [C.POINTER(PlanDesc)]
     lib.p2p_plan_desc_init.restype = None
@@ -138,6 +152,7 @@ def load_library() -> C.CDLL:
     lib.p2p_gather.argtypes = [P, P, P, P]
     lib.p2p_peer_check.argtypes = [P]
     lib.p2p_box_counts.argtypes = [i32, i64, P, P]
+    lib.p2p_plan_set_workspaces.argtypes = [P, i32]
     lib.p2p_partition_route.argtypes = [C.POINTER(PlanDesc), P, P, P, P, i64, i64, P, P]
     lib.p2p_plan_create_local.argtypes = [C.POINTER(PlanDesc), P, P, P, P, i64, i64, C.POINTER(P)]
     lib.p2p_destroy.argtypes = [P]
@@ -151,7 +166,7 @@ def load_library() -> C.CDLL:
                  "p2p_apply_dist_boundary", "p2p_halo_pack", "p2p_apply_dist_peer", "p2p_gather_peer", "p2p_ipc_export",
                  "p2p_ipc_open", "p2p_ipc_close", "p2p_peer_buffers", "p2p_peer_connect", "p2p_apply_peer_sync",
                  "p2p_gather", "p2p_peer_check", "p2p_box_counts", "p2p_partition_route", "p2p_plan_create_local",
-                 "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export"):
+                 "p2p_plan_set_workspaces", "p2p_destroy", "p2p_plan_get_info", "p2p_plan_export"):
         getattr(lib, name).restype = i32
     _lib = lib
     return lib
@@ -259,6 +274,10 @@ def p2p_gather(plan, d_local: int, d_global: int, stream: int = 0):
 
 def p2p_peer_check(plan):
     _check(load_library().p2p_peer_check(plan), "p2p_peer_check")
+
+
+def p2p_plan_set_workspaces(plan, n: int):
+    _check(load_library().p2p_plan_set_workspaces(plan, n), "p2p_plan_set_workspaces")
 
 
 def p2p_box_counts(level: int, xy) -> np.ndarray:
@@ -448,6 +467,10 @@ class Plan:
 
     def export(self, kind) -> np.ndarray:
         return p2p_plan_export(self._h, kind)
+
+    def set_workspaces(self, n: int):
+        """Up to n applies of this plan in flight on different streams (p2p_plan_set_workspaces)."""
+        p2p_plan_set_workspaces(self._h, n)
 
     def _stream(self, stream):
         if stream is not None:

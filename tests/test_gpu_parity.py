@@ -263,3 +263,31 @@ def test_paper_layouts_parity_sparse_and_ct(layout):
         check(pl, src, tgt, q, c.level - 5)
     with p2p.Plan(src, tgt, level=0, layout=layout, precision="fp64", ct=15) as pl:
         check(pl, src, tgt, q, pl.info["level"])
+
+
+@pytest.mark.parametrize("layout,prec", [("tiled", "fp32"), ("nr", "fp64"), ("r", "fp32")])
+def test_workspace_slots_pipelined(layout, prec):
+    """p2p_plan_set_workspaces: applies of one plan in flight on different streams (host buffers
+    and device buffers), no host synchronisation between them; every result equals the
+    one-slot result for its weights (scaled by powers of two: exact)."""
+    src, tgt, q = W.make_problem("d16_1e6", n=40000)
+    with p2p.Plan(src, tgt, level=8, layout=layout, precision=prec) as pl:
+        qd = torch.as_tensor(q, dtype=pl.torch_dtype, device="cuda")
+        ref = pl.apply(qd, order="user").double().cpu().numpy()
+        pl.set_workspaces(3)
+        streams = [torch.cuda.Stream() for _ in range(3)]
+        scales = [1.0, 2.0, -0.5, 4.0, 0.25, -1.0]
+        hq = [(q * f).astype(pl.np_dtype) for f in scales]
+        hq = [torch.from_numpy(a).pin_memory() for a in hq]
+        ho = [torch.empty(len(tgt), dtype=pl.torch_dtype).pin_memory() for _ in scales]
+        outs = []
+        for k, f in enumerate(scales):
+            st = streams[k % 3]
+            p2p.p2p_apply_host_async(pl.handle, hq[k].data_ptr(), ho[k].data_ptr(), p2p.P2P_ORDER_USER, 0,
+                                     st.cuda_stream)
+            with torch.cuda.stream(st):
+                outs.append(pl.apply(qd * f, order="user", stream=st.cuda_stream))
+        torch.cuda.synchronize()
+        for k, f in enumerate(scales):
+            assert np.array_equal(ho[k].double().numpy(), ref * f)
+            assert np.array_equal(outs[k].double().cpu().numpy(), ref * f)
