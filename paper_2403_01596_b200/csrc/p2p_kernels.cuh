@@ -195,6 +195,57 @@ __device__ __forceinline__ double log_tab(double x, const double2 *__restrict__ 
 #endif
 }
 
+// fp64 log without the shared-memory table (the TILED lean fp64 path, sparse tiles): a 32-entry
+// table held one entry per lane in registers (c_k rounded to float, L_k = -log c_k;
+// plan_builder.cpp build_log_table) and fetched with warp shuffles.  The 256-entry table's random
+// LDS.128 are 2.5x bank-conflicted (69 % of the dense fp64 kernel's shared wavefronts, ncu
+// surf_2e7); without them the sparse fp64 path runs 13 % faster, while the dense path (long
+// runs, 44 instructions per pair with the shuffles and masks) turns issue-bound and keeps
+// log_tab (profiles/r02_ncu_fp64.txt).
+// k = top 5 mantissa bits, t = m c_k - 1 (|t| < 2^-6 + 2^-23), log1p(t) to degree 8 (truncation
+// < 1e-17), log x = fma(e, ln2, L_k + log1p(t)): 11 DP operations.  All 32 lanes of the warp must
+// call it together (converged); x must be a positive normal double.
+__device__ __forceinline__ double log_shfl(double x, float lc, double lL) {
+    const long long b = __double_as_longlong(x);
+    const int e = (int)(b >> 52) - 1023;
+    const int kk = (int)(b >> 47) & 31;
+    const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+    const float c = __shfl_sync(0xffffffffu, lc, kk);
+    const double L = __shfl_sync(0xffffffffu, lL, kk);
+    const double t = fma(m, (double)c, -1.0);
+    double q = fma(t, -0.125, 1.0 / 7.0);
+    q = fma(t, q, -1.0 / 6.0);
+    q = fma(t, q, 0.2);
+    q = fma(t, q, -0.25);
+    q = fma(t, q, 1.0 / 3.0);
+    q = fma(t, q, -0.5);
+    const double p = fma(t * t, q, t);
+    return fma((double)e, kLn2d, L + p);
+}
+
+// fp64, one target's sources j(v), v < n, with the explicit guard, for log_shfl: every lane of the
+// warp runs the warp's longest count (lanes past their own n -- or with no target: n = 0 --
+// evaluate a masked pair), so the shuffles always see the whole warp.
+template <typename J>
+__device__ __forceinline__ double sweep_f64w(const double2 *__restrict__ UV, const double *__restrict__ Q, int n,
+                                             J jof, double ut, double vt, double eps2, float lc, double lL) {
+    const int nmax = __reduce_max_sync(0xffffffffu, n);
+    double acc = 0.0;
+#pragma unroll 2
+    for (int v = 0; v < nmax; ++v) {
+        const bool live = v < n;
+        const int j = live ? jof(v) : 0;
+        const double2 s = UV[j];
+        const double du = ut - s.x, dv = vt - s.y;
+        const double r2 = fma(dv, dv, du * du);
+        const bool use = live && r2 >= eps2;
+        const double lg = log_shfl(use ? r2 : 1.0, lc, lL);
+        const double qj = Q[j];
+        acc = use ? fma(qj, lg, acc) : acc;
+    }
+    return acc;
+}
+
 // fp64, (u, v) per entry, explicit guard.
 __device__ __forceinline__ double span1_f64(const double2 *__restrict__ UV, const double *__restrict__ Q, int j0,
                                             int j1, double ut, double vt, double eps2,
@@ -775,9 +826,16 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
     T *part = reinterpret_cast<T *>(smem + c.part);
     double2 *s_lt = reinterpret_cast<double2 *>(smem + c.ltab);
     uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + c.bar);
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     if constexpr (sizeof(T) == 8)
         for (int i = tid; i < kLogTab; i += NT) s_lt[i] = a.log_tab[i];
+    float lc = 0.f;  // fp64: this lane's entry of the 32-entry shuffle table (log_shfl)
+    double lL = 0.0;
+    if constexpr (sizeof(T) == 8) {
+        const double2 e = a.log_tab[kLogTab + lane];
+        lc = (float)e.x;
+        lL = e.y;
+    }
 
     auto issue = [&](int ti, int b) {  // one elected thread: arm buffer b and bulk-copy tile ti's record
         const int slot = a.tile_slot[ti];
@@ -925,7 +983,20 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             a.out[oi] = a.accumulate ? a.out[oi] + acc : acc;
         };
 
-        if constexpr (LEAN) {  // one thread per target (boxes by n9): three row-runs, flattened or in turn
+        if constexpr (LEAN && sizeof(T) == 8) {  // fp64: flattened runs, whole-warp rounds (log_shfl)
+            for (int base = ub + (tid & ~31); base < ue; base += NT) {
+                const int t = base + lane;
+                const bool has = t < ue;
+                const int jb = has ? tbl[t] : 0;
+                const Runs3 runs(table[jb], table[jb + 3], table[jb + R], table[jb + R + 3], table[jb + 2 * R],
+                                 table[jb + 2 * R + 3]);
+                const double acc = sweep_f64w(
+                    reinterpret_cast<const double2 *>(s_uv), reinterpret_cast<const double *>(s_q), has ? runs.n : 0,
+                    [&](int v) { return runs.at(runs.v0 + v); }, has ? (double)tuv[2 * t] : 0.0,
+                    has ? (double)tuv[2 * t + 1] : 0.0, (double)a.eps2, lc, lL);
+                if (has) finish(t, (T)acc);
+            }
+        } else if constexpr (LEAN) {  // one thread per target (boxes by n9): three row-runs, flattened or in turn
             for (int t = ub + tid; t < ue; t += NT) {
                 const int jb = tbl[t];
                 const T ux = tuv[2 * t], uy = tuv[2 * t + 1];

@@ -26,6 +26,7 @@ P2P_HD inline int align16(int x) { return (x + 15) & ~15; }
 #endif
 // fp64 log: table of (1/c_k rounded, -log of it), c_k = 1 + (k + 1/2) / kLogTab
 constexpr int kLogTab = P2P_LOG256 ? 256 : 128;
+constexpr int kLogTab32 = 32;  // fp64 log, warp-register table (log_shfl): one entry per lane
 
 struct NrCarve {
     int sstart, gstart, cnt, toff, pstart, uj0, ut, tslot, tu, tv, part, src, ltab, total, ucap;

@@ -173,15 +173,23 @@ void balance_batches(const std::vector<int32_t> &ord, const std::vector<int32_t>
 
 }  // namespace
 
-// fp64 log table: (c_inv_k, -log c_inv_k), c_inv_k = 1 / (1 + (k + 1/2) / 128) rounded to double,
-// the log from the 64-bit-mantissa long double logl (the kernels' `log_tab`).
+// fp64 log tables, the log from the 64-bit-mantissa long double logl:
+//   [0, kLogTab): (c_inv_k, -log c_inv_k), c_inv_k = 1 / (1 + (k + 1/2) / kLogTab) rounded to
+//     double -- the shared-memory table of the kernels' `log_tab`;
+//   then kLogTab32 entries (c_k, -log c_k), c_k = 1 / (1 + (k + 1/2) / 32) rounded to FLOAT (held
+//     exactly in the double) -- the warp-register table of `log_shfl` (lane k holds entry k).
 void build_log_table(HostPlan &hp) {
-    hp.log_tab.resize(2 * kLogTab);
+    hp.log_tab.resize(2 * (kLogTab + kLogTab32));
     for (int kk = 0; kk < kLogTab; ++kk) {
         const double c = 1.0 + (kk + 0.5) / kLogTab;
         const double cinv = 1.0 / c;
         hp.log_tab[2 * kk] = cinv;
         hp.log_tab[2 * kk + 1] = (double)(-logl((long double)cinv));
+    }
+    for (int kk = 0; kk < kLogTab32; ++kk) {
+        const float cinv = (float)(1.0 / (1.0 + (kk + 0.5) / kLogTab32));
+        hp.log_tab[2 * (kLogTab + kk)] = (double)cinv;
+        hp.log_tab[2 * (kLogTab + kk) + 1] = (double)(-logl((long double)cinv));
     }
 }
 
