@@ -367,6 +367,7 @@ void launch_p2p(p2p_plan_s &P, const T *q_local, T *out, int accumulate, cudaStr
         a.tile_tgt_base = (const int32_t *)P.tile_tgt_base.p;
         a.ns = hp.ns;
         a.flat = hp.flat ? 1 : 0;
+        a.lt8 = hp.lt8 ? 1 : 0;
         a.nbuf = hp.nbuf;
         a.kappa = (T)hp.kappa;
         void *args[] = {&a};

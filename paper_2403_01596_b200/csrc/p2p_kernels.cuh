@@ -195,6 +195,38 @@ __device__ __forceinline__ double log_tab(double x, const double2 *__restrict__ 
 #endif
 }
 
+// fp64 log for the dense TILED path: a 64-entry table replicated 8 times in shared memory, entry k
+// of copy c at 16-byte slot 8 k + c, and lane l reads copy l & 7 -- the 8 lanes of each quarter-
+// warp phase of an LDS.128 always hit 8 distinct bank groups (no conflicts; the 256-entry table's
+// random lookups cost 2.5x the ideal wavefronts).  k = top 6 mantissa bits, |t| < 2^-7, log1p
+// to degree 7 (truncation < 1e-17): 10 DP operations.
+__device__ __forceinline__ double log_tab8(double x, const double2 *__restrict__ LT8, int l8) {
+    const long long b = __double_as_longlong(x);
+    const int e = (int)(b >> 52) - 1023;
+    const double2 c = LT8[(((int)(b >> 46) & 63) << 3) + l8];
+    const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+    const double t = fma(m, c.x, -1.0);
+    double q = fma(t, 1.0 / 7.0, -1.0 / 6.0);
+    q = fma(t, q, 0.2);
+    q = fma(t, q, -0.25);
+    q = fma(t, q, 1.0 / 3.0);
+    q = fma(t, q, -0.5);
+    const double p = fma(t * t, q, t);
+    return fma((double)e, kLn2d, c.y + p);
+}
+__device__ __forceinline__ double span1_f64r(const double2 *__restrict__ UV, const double *__restrict__ Q, int j0,
+                                             int j1, double ut, double vt, double eps2,
+                                             const double2 *__restrict__ LT8, int l8) {
+    double acc = 0.0;
+    for (int j = j0; j < j1; ++j) {
+        const double2 s = UV[j];
+        const double du = ut - s.x, dv = vt - s.y;
+        const double r2 = fma(dv, dv, du * du);
+        if (r2 >= eps2) acc = fma(Q[j], log_tab8(r2, LT8, l8), acc);
+    }
+    return acc;
+}
+
 // fp64 log without the shared-memory table (the TILED lean fp64 path, sparse tiles): a 32-entry
 // table held one entry per lane in registers (c_k rounded to float, L_k = -log c_k;
 // plan_builder.cpp build_log_table) and fetched with warp shuffles.  The 256-entry table's random
@@ -366,6 +398,7 @@ struct P2PArgs {
     const int32_t *tile_tgt_base;   // TILED: plan index of each tile's first target
     int ns;                     // TILED: work items per target (1 = whole target, 3 = one per row-run)
     int flat;                   // TILED lean path: sweep the three row-runs as one sequence
+    int lt8;                    // TILED dense fp64: log_tab8 (8-fold 64-entry table) instead of log_tab
     int nbuf;                   // TILED: 2 = prefetch the next tile's record during this tile
     unsigned long long *trace;  // optional per-tile timeline (diagnostics; nullptr = off)
     T *out;
@@ -820,15 +853,19 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
     // (it + 1) & 1 during iteration it while the others may still read slot it & 1
     __shared__ int s_next[2], s_base_next[2], s_part_next[2];
     const int k = a.k, W = 1 << k, R = W + 2, RR = R * R;
-    const TCarve c = tiled_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI, NS, a.nbuf);
+    const TCarve c = tiled_carve(k, a.src_cap, a.tgt_cap, (int)sizeof(T), TPI, NS, a.nbuf, a.lt8);
     const bool db = a.nbuf == 2;
     T *s_q = reinterpret_cast<T *>(smem + c.q);
     T *part = reinterpret_cast<T *>(smem + c.part);
     double2 *s_lt = reinterpret_cast<double2 *>(smem + c.ltab);
     uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + c.bar);
     const int tid = threadIdx.x, lane = tid & 31;
-    if constexpr (sizeof(T) == 8)
-        for (int i = tid; i < kLogTab; i += NT) s_lt[i] = a.log_tab[i];
+    if constexpr (sizeof(T) == 8 && NS == 3) {  // dense fp64: the 8-fold table of log_tab8, or log_tab's
+        if (a.lt8)
+            for (int i = tid; i < 8 * kLogTab8; i += NT) s_lt[i] = a.log_tab[kLogTab + kLogTab32 + (i >> 3)];
+        else
+            for (int i = tid; i < kLogTab; i += NT) s_lt[i] = a.log_tab[i];
+    }
     float lc = 0.f;  // fp64: this lane's entry of the 32-entry shuffle table (log_shfl)
     double lL = 0.0;
     if constexpr (sizeof(T) == 8) {
@@ -950,8 +987,12 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                 res[0] = span1_f32(reinterpret_cast<const float2 *>(s_uv), reinterpret_cast<const float *>(s_q), i0,
                                    i1, tuv[2 * t0], tuv[2 * t0 + 1]);
             } else {
-                res[0] = span1_f64(reinterpret_cast<const double2 *>(s_uv), reinterpret_cast<const double *>(s_q), i0,
-                                   i1, tuv[2 * t0], tuv[2 * t0 + 1], a.eps2, s_lt);
+                if (a.lt8)
+                    res[0] = span1_f64r(reinterpret_cast<const double2 *>(s_uv), reinterpret_cast<const double *>(s_q),
+                                        i0, i1, tuv[2 * t0], tuv[2 * t0 + 1], a.eps2, s_lt, lane & 7);
+                else
+                    res[0] = span1_f64(reinterpret_cast<const double2 *>(s_uv), reinterpret_cast<const double *>(s_q),
+                                       i0, i1, tuv[2 * t0], tuv[2 * t0 + 1], a.eps2, s_lt);
             }
         };
         // final value of slot t from its row-ordered sum (fp32: guarded redo if non-finite),

@@ -27,6 +27,7 @@ P2P_HD inline int align16(int x) { return (x + 15) & ~15; }
 // fp64 log: table of (1/c_k rounded, -log of it), c_k = 1 + (k + 1/2) / kLogTab
 constexpr int kLogTab = P2P_LOG256 ? 256 : 128;
 constexpr int kLogTab32 = 32;  // fp64 log, warp-register table (log_shfl): one entry per lane
+constexpr int kLogTab8 = 64;   // fp64 log, dense TILED: 64 entries replicated 8x (log_tab8, no bank conflicts)
 
 struct NrCarve {
     int sstart, gstart, cnt, toff, pstart, uj0, ut, tslot, tu, tv, part, src, ltab, total, ucap;
@@ -96,7 +97,7 @@ P2P_HD inline int tiled_table_stride(int k) {
 P2P_HD inline int tiled_item_cap(int slot_cap, int tpi, int ns) {
     return ns == 3 ? (3 * (slot_cap / tpi) + 7) & ~7 : 0;
 }
-P2P_HD inline TCarve tiled_carve(int k, int src_cap, int slot_cap, int e, int tpi, int ns, int nbuf) {
+P2P_HD inline TCarve tiled_carve(int k, int src_cap, int slot_cap, int e, int tpi, int ns, int nbuf, int lt8 = 0) {
     TCarve c;
     c.tstride = tiled_table_stride(k);
     c.icap = tiled_item_cap(slot_cap, tpi, ns);
@@ -111,8 +112,9 @@ P2P_HD inline TCarve tiled_carve(int k, int src_cap, int slot_cap, int e, int tp
     c.buf0 = 0;
     c.q = nbuf * c.bufsz;
     c.part = align16(c.q + e * src_cap);  // NS = 3: three partial sums per slot
-    c.ltab = align16(c.part + (ns == 3 ? 3 * e * slot_cap : 0));  // fp64: the log table (kLogTab entries)
-    c.bar = align16(c.ltab + (e == 8 ? 16 * kLogTab : 0));
+    // fp64 dense (ns = 3): the log table -- kLogTab entries, or (lt8) 8 x kLogTab8; lean: none (log_shfl)
+    c.ltab = align16(c.part + (ns == 3 ? 3 * e * slot_cap : 0));
+    c.bar = align16(c.ltab + (e == 8 && ns == 3 ? 16 * (lt8 ? 8 * kLogTab8 : kLogTab) : 0));
     c.total = c.bar + 16;
     return c;
 }
@@ -282,6 +284,7 @@ struct HostPlan {
     bool lean = false;                            // TILED lean kernel path (tpi 1, ns 1, unpadded)
     bool tsort = false;                           // ns 1: target boxes of a tile ordered by n9 (descending)
     bool flat = false;                            // lean path: row-runs swept as one sequence (sparse)
+    bool lt8 = false;                             // dense fp64: the 8-fold 64-entry log table (log_tab8)
     std::vector<double> log_tab;                  // fp64: kLogTab x (c_inv, -log c_inv) for the table-driven log
 
     // ---- the paper's layouts (PAPER_INDEXING / PAPER_REPETITION)

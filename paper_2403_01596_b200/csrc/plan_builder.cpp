@@ -177,9 +177,11 @@ void balance_batches(const std::vector<int32_t> &ord, const std::vector<int32_t>
 //   [0, kLogTab): (c_inv_k, -log c_inv_k), c_inv_k = 1 / (1 + (k + 1/2) / kLogTab) rounded to
 //     double -- the shared-memory table of the kernels' `log_tab`;
 //   then kLogTab32 entries (c_k, -log c_k), c_k = 1 / (1 + (k + 1/2) / 32) rounded to FLOAT (held
-//     exactly in the double) -- the warp-register table of `log_shfl` (lane k holds entry k).
+//     exactly in the double) -- the warp-register table of `log_shfl` (lane k holds entry k);
+//   then kLogTab8 entries (c_inv_k, -log c_inv_k), c_inv_k = 1 / (1 + (k + 1/2) / 64) -- staged
+//     8-fold in shared memory by the dense fp64 TILED kernel (`log_tab8`).
 void build_log_table(HostPlan &hp) {
-    hp.log_tab.resize(2 * (kLogTab + kLogTab32));
+    hp.log_tab.resize(2 * (kLogTab + kLogTab32 + kLogTab8));
     for (int kk = 0; kk < kLogTab; ++kk) {
         const double c = 1.0 + (kk + 0.5) / kLogTab;
         const double cinv = 1.0 / c;
@@ -190,6 +192,11 @@ void build_log_table(HostPlan &hp) {
         const float cinv = (float)(1.0 / (1.0 + (kk + 0.5) / kLogTab32));
         hp.log_tab[2 * (kLogTab + kk)] = (double)cinv;
         hp.log_tab[2 * (kLogTab + kk) + 1] = (double)(-logl((long double)cinv));
+    }
+    for (int kk = 0; kk < kLogTab8; ++kk) {  // then kLogTab8 entries (c_inv_k, -log c_inv_k) for log_tab8
+        const double cinv = 1.0 / (1.0 + (kk + 0.5) / kLogTab8);
+        hp.log_tab[2 * (kLogTab + kLogTab32 + kk)] = cinv;
+        hp.log_tab[2 * (kLogTab + kLogTab32 + kk) + 1] = (double)(-logl((long double)cinv));
     }
 }
 
@@ -623,6 +630,11 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     // flattened row-runs pay below ~3 sources per box (more index work per pair,
     // fewer idle lanes) and always in fp64 (the log dwarfs the index work); above,
     // row loops (P2P_FLAT overrides)
+    // dense fp64: the conflict-free replicated log table (one more DP op per pair, no bank
+    // conflicts) pays below ~24 sources per box; denser boxes keep the 256-entry table (measured,
+    // tools/gpu_f64_ab2.sh: surf_2e7 / d16 -3..-4 %, d32 / d64 +5..+10 % with it)
+    hp.lt8 = d.layout == P2P_LAYOUT_TILED && dense64 && hp.density_occ < 24.0;
+    if (const char *v = std::getenv("P2P_LT8")) hp.lt8 = d.layout == P2P_LAYOUT_TILED && dense64 && std::atoi(v) != 0;
     hp.flat = hp.lean && (hp.density_occ < 3.0 || d.precision == P2P_FP64);
     if (const char *v = std::getenv("P2P_FLAT")) hp.flat = hp.lean && std::atoi(v) != 0;
     if (d.kernel == P2P_KERNEL_HELMHOLTZ_2D) {  // one thread per target, n9-sorted, flattened runs
@@ -650,7 +662,7 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     }
     int64_t smem = d.layout == P2P_LAYOUT_NONREDUNDANT ? (int64_t)nr_carve(k, sc, tc, e, hp.tpi).total
                    : d.layout == P2P_LAYOUT_TILED
-                       ? (int64_t)tiled_carve(k, sc, tc, e, hp.tpi, hp.ns, hp.nbuf).total
+                       ? (int64_t)tiled_carve(k, sc, tc, e, hp.tpi, hp.ns, hp.nbuf, hp.lt8).total
                                                        : (int64_t)r_carve(k, sc, tc, e).total;
     hp.smem_bytes = smem;
     return smem;
