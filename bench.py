@@ -680,22 +680,23 @@ def _ncu_traffic(args, names):
 def _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier):
     """Same metric through the C ABI with pinned HOST buffers (p2p_apply_host_async): every
     step copies q host->device, applies (user order: permutation kernels included), copies phi
-    device->host.  Steps are pipelined the way a serving loop runs them: each plan has two
-    workspace slots (p2p_plan_set_workspaces) and consecutive steps alternate between two
-    streams per config, so step k's D2H overlaps step k+1's H2D and kernel (each apply waits on
+    device->host.  Steps are pipelined the way a serving loop runs them: each plan has three
+    workspace slots (p2p_plan_set_workspaces) and consecutive steps rotate over three streams
+    per config, so step k's D2H overlaps step k+1's H2D and kernel (each apply waits on
     the device for the apply that last used its slot)."""
     import torch
     from paper_2403_01596_b200 import p2p
     if world > 1:
         return _e2e_dist(args, jobs, stream, pairs_step, barrier)
     hq = [torch.as_tensor(j["q_user"], dtype=j["plan"].torch_dtype).pin_memory() for j in jobs]
-    ho = [[torch.empty(j["info"]["n_tgt"], dtype=j["plan"].torch_dtype).pin_memory() for _ in range(2)]
+    NS = 3
+    ho = [[torch.empty(j["info"]["n_tgt"], dtype=j["plan"].torch_dtype).pin_memory() for _ in range(NS)]
           for j in jobs]
     h2d = sum(int(t.numel() * t.element_size()) for t in hq)
     d2h = sum(int(t[0].numel() * t[0].element_size()) for t in ho)
     for j in jobs:
-        j["plan"].set_workspaces(2)
-    side = [[torch.cuda.Stream(dev) for _ in range(2)] for _ in jobs]
+        j["plan"].set_workspaces(NS)
+    side = [[torch.cuda.Stream(dev) for _ in range(NS)] for _ in jobs]
 
     def run(steps):
         start = torch.cuda.Event()
@@ -705,8 +706,8 @@ def _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier):
                 st.wait_event(start)
         for k in range(steps):
             for j, a, b, ss in zip(jobs, hq, ho, side):
-                st = ss[k % 2]
-                p2p.p2p_apply_host_async(j["plan"].handle, a.data_ptr(), b[k % 2].data_ptr(), p2p.P2P_ORDER_USER, 0,
+                st = ss[k % NS]
+                p2p.p2p_apply_host_async(j["plan"].handle, a.data_ptr(), b[k % NS].data_ptr(), p2p.P2P_ORDER_USER, 0,
                                          st.cuda_stream)
         for ss in side:
             for st in ss:
@@ -724,8 +725,8 @@ def _e2e(args, jobs, world, rank, stream, dev, pairs_step, barrier):
     ms = e0.elapsed_time(e1) / args.steps
     return {"value": pairs_step / (ms * 1e-3), "unit": "pair-interactions/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms,
-            "path": "p2p_apply_host_async, pinned host buffers, user order; two workspace slots per plan, "
-                    "consecutive steps on alternating streams (step k's D2H overlaps step k+1's H2D + kernel)"}
+            "path": "p2p_apply_host_async, pinned host buffers, user order; three workspace slots per plan, "
+                    "consecutive steps on rotating streams (step k's D2H overlaps step k+1's H2D + kernel)"}
 
 
 def _plan_build(args, jobs, dev):

@@ -838,11 +838,16 @@ p2p_r_kernel(const P2PArgs<T> a) {
 #ifndef P2P_BOX3_HELM_PAIR
 #define P2P_BOX3_HELM_PAIR 1  // 3D Helmholtz fp32: two targets per thread
 #endif
+#ifndef P2P_LEAN_MINB
+#define P2P_LEAN_MINB 0  // > 0: register cap via min resident CTAs for the 64-thread lean instances
+#endif
 #ifndef P2P_DENSE_MINB
 #define P2P_DENSE_MINB 0  // > 0: register cap via min resident CTAs for the TPI = 2 instances (experiments)
 #endif
 template <typename T, int TPI, int NT, bool PAD, int NS>
-__global__ void __launch_bounds__(NT, (TPI == 2 && P2P_DENSE_MINB > 0) ? P2P_DENSE_MINB : 0)
+__global__ void __launch_bounds__(NT, (TPI == 2 && P2P_DENSE_MINB > 0)                          ? P2P_DENSE_MINB
+                                      : (TPI == 1 && !PAD && NS == 1 && NT == 64 && P2P_LEAN_MINB > 0) ? P2P_LEAN_MINB
+                                                                                                  : 0)
 p2p_tiled_kernel(const P2PArgs<T> a) {
     static_assert(TPI == 1 || (TPI == 2 && PAD && sizeof(T) == 4), "TPI = 2 is the padded fp32 path");
     static_assert(!PAD || sizeof(T) == 4, "the padded layout is fp32");

@@ -110,8 +110,11 @@ P2P_HD inline TCarve tiled_carve(int k, int src_cap, int slot_cap, int e, int tp
     c.items = c.oix + 2 * slot_cap;
     c.bufsz = align16(c.items + 2 * c.icap);
     c.buf0 = 0;
-    c.q = nbuf * c.bufsz;
-    c.part = align16(c.q + e * src_cap);  // NS = 3: three partial sums per slot
+    // weights: fp32 single-buffered records gather q in place over the entry indices (each entry's
+    // index is read and its weight written by the same thread; the indices are dead afterwards)
+    const bool q_alias = e == 4 && nbuf == 1;
+    c.q = q_alias ? c.idx : nbuf * c.bufsz;
+    c.part = align16(q_alias ? nbuf * c.bufsz : c.q + e * src_cap);  // NS = 3: three partial sums per slot
     // fp64 dense (ns = 3): the log table -- kLogTab entries, or (lt8) 8 x kLogTab8; lean: none (log_shfl)
     c.ltab = align16(c.part + (ns == 3 ? 3 * e * slot_cap : 0));
     c.bar = align16(c.ltab + (e == 8 && ns == 3 ? 16 * (lt8 ? 8 * kLogTab8 : kLogTab) : 0));
@@ -128,7 +131,7 @@ struct HCarve {
 P2P_HD inline HCarve helm_carve(int k, int src_cap, int slot_cap, int e) {
     HCarve h;
     h.t = tiled_carve(k, src_cap, slot_cap, e, 1, 1, 1);
-    h.q = h.t.q;
+    h.q = h.t.bufsz;  // complex weights (2 e bytes) after the record buffer (not over the indices)
     h.ltab = align16(h.q + 2 * e * src_cap);
     h.bar = align16(h.ltab + (e == 8 ? 16 * kLogTab : 0));
     h.total = h.bar + 16;
