@@ -489,6 +489,12 @@ def main():
                      "hbm_gbs_alg": alg_bytes / (kernel_ms * 1e-3) / 1e9,
                      "mufu_frac": pairs_local / (kernel_ms * 1e-3) / 1e9 / peak_mufu,
                      "floor_frac": max(t_mufu, t_hbm) / (kernel_ms * 1e-3)})
+    # the same bytes without SURVEY §8(d)'s 8 B per box of CSR offsets (the TILED kernel reads its
+    # region tables instead): points only, 12 B per target + 12 B per source (fp32)
+    pts_bytes = sum(3 * (4 if args.precision == "fp32" else 8) * (j["info"]["n_tgt_local"] + j["info"]["n_src_local"])
+                    for j in jobs)
+    roofline.update({"alg_bytes_points_only": pts_bytes,
+                     "hbm_frac_points_only": pts_bytes / (kernel_ms * 1e-3) / 1e9 / peak_hbm})
     per_cfg = []
     for i, j in enumerate(jobs):
         kms = float(np.mean(kern_ms[:, i]))
