@@ -1121,7 +1121,7 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
 // rational / asymptotic approximations on the FMA pipe + one sincos and one log beyond the
 // small-argument branch), 4 FMA for the complex multiply-add.
 template <typename T>
-__device__ __forceinline__ void bessel_j0y0(T x, T &J, T &Y);
+__device__ void bessel_j0y0(T x, T &J, T &Y);
 template <>
 __device__ __forceinline__ void bessel_j0y0<float>(float x, float &J, float &Y) {
     J = j0f(x);
@@ -1142,7 +1142,7 @@ __constant__ double kHankG[18] = {1.0760822573387157e-07, -1.0085244871057431e-0
     -8.117210709175648e-06, 8.851138042211988e-06, -1.3976003481602903e-05, 3.510941725411511e-05,
     -0.00016170548761511877, 0.001808449074070366, -0.125};
 template <>
-__device__ __forceinline__ void bessel_j0y0<double>(double x, double &J, double &Y) {
+__device__ __noinline__ void bessel_j0y0<double>(double x, double &J, double &Y) {  // cold: kappa r > 6 only
     const double rx = 1.0 / x, w = 36.0 * rx * rx;
     double m = kHankM[0], g = kHankG[0];
 #pragma unroll
