@@ -169,6 +169,9 @@ __device__ __noinline__ float span1_f32_guarded(const float2 *__restrict__ UV, c
 // the rounding of ln2 adds < 2e-15 to a result of that size).  x must be a positive normal double.
 // (P2P_LOG256 = 0: round 1's 128-entry table, degree 6, ln2 split hi / lo: 11 DP ops.)
 constexpr double kLn2d = 6.93147180559945309417e-01;
+// the log polynomials' coefficients that are not short immediates, in the constant bank: DFMA
+// reads them as c[][] operands (as immediates each costs a UMOV pair per use)
+__constant__ double kLogK[6] = {1.0 / 7.0, -1.0 / 6.0, 0.2, 1.0 / 3.0, 6.93147180559945309417e-01, -0.125};
 constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
 __device__ __forceinline__ double log_tab(double x, const double2 *__restrict__ LT) {
     const long long b = __double_as_longlong(x);
@@ -177,11 +180,11 @@ __device__ __forceinline__ double log_tab(double x, const double2 *__restrict__ 
 #if P2P_LOG256
     const double2 c = LT[(int)(b >> 44) & 255];
     const double t = fma(m, c.x, -1.0);
-    double q = fma(t, 0.2, -0.25);
-    q = fma(t, q, 1.0 / 3.0);
+    double q = fma(t, kLogK[2], -0.25);
+    q = fma(t, q, kLogK[3]);
     q = fma(t, q, -0.5);
     const double p = fma(t * t, q, t);
-    return fma((double)e, kLn2d, c.y + p);
+    return fma((double)e, kLogK[4], c.y + p);
 #else
     const double2 c = LT[(int)(b >> 45) & 127];
     const double t = fma(m, c.x, -1.0);
@@ -206,23 +209,27 @@ __device__ __forceinline__ double log_tab8(double x, const double2 *__restrict__
     const double2 c = LT8[(((int)(b >> 46) & 63) << 3) + l8];
     const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
     const double t = fma(m, c.x, -1.0);
-    double q = fma(t, 1.0 / 7.0, -1.0 / 6.0);
-    q = fma(t, q, 0.2);
+    double q = fma(t, kLogK[0], kLogK[1]);
+    q = fma(t, q, kLogK[2]);
     q = fma(t, q, -0.25);
-    q = fma(t, q, 1.0 / 3.0);
+    q = fma(t, q, kLogK[3]);
     q = fma(t, q, -0.5);
     const double p = fma(t * t, q, t);
-    return fma((double)e, kLn2d, c.y + p);
+    return fma((double)e, kLogK[4], c.y + p);
 }
 __device__ __forceinline__ double span1_f64r(const double2 *__restrict__ UV, const double *__restrict__ Q, int j0,
                                              int j1, double ut, double vt, double eps2,
                                              const double2 *__restrict__ LT8, int l8) {
     double acc = 0.0;
-    for (int j = j0; j < j1; ++j) {
+#pragma unroll 4
+    for (int j = j0; j < j1; ++j) {  // guard by selection, no branch (a guarded pair's log is of 1.0)
         const double2 s = UV[j];
         const double du = ut - s.x, dv = vt - s.y;
         const double r2 = fma(dv, dv, du * du);
-        if (r2 >= eps2) acc = fma(Q[j], log_tab8(r2, LT8, l8), acc);
+        const bool ok = r2 >= eps2;
+        const double lg = log_tab8(ok ? r2 : 1.0, LT8, l8);
+        const double qj = Q[j];
+        acc = ok ? fma(qj, lg, acc) : acc;
     }
     return acc;
 }
@@ -245,14 +252,14 @@ __device__ __forceinline__ double log_shfl(double x, float lc, double lL) {
     const float c = __shfl_sync(0xffffffffu, lc, kk);
     const double L = __shfl_sync(0xffffffffu, lL, kk);
     const double t = fma(m, (double)c, -1.0);
-    double q = fma(t, -0.125, 1.0 / 7.0);
-    q = fma(t, q, -1.0 / 6.0);
-    q = fma(t, q, 0.2);
+    double q = fma(t, kLogK[5], kLogK[0]);
+    q = fma(t, q, kLogK[1]);
+    q = fma(t, q, kLogK[2]);
     q = fma(t, q, -0.25);
-    q = fma(t, q, 1.0 / 3.0);
+    q = fma(t, q, kLogK[3]);
     q = fma(t, q, -0.5);
     const double p = fma(t * t, q, t);
-    return fma((double)e, kLn2d, L + p);
+    return fma((double)e, kLogK[4], L + p);
 }
 
 // fp64, one target's sources j(v), v < n, with the explicit guard, for log_shfl: every lane of the
