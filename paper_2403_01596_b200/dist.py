@@ -132,7 +132,17 @@ class DistributedP2P:
         return int(self.src_begin[self.rank]), int(self.src_begin[self.rank + 1])
 
     def exchange(self, q_owned, stream=None):
-        """Halo weight exchange (a6): pack what the peers need, all-to-all, return the halo buffer."""
+        """Halo weight exchange (a6): pack what the peers need, all-to-all, return the halo buffer.
+        ``stream`` (a raw cudaStream_t handle): the pack kernel and the collective both run on it
+        (torch collectives use the current stream, so it is made current for the call), so an
+        apply enqueued on the same stream is ordered after the exchange."""
+        torch = self.torch
+        if stream is not None and stream != torch.cuda.current_stream(self.device).cuda_stream:
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=torch.device("cuda", self.device))):
+                return self._exchange(q_owned, stream)
+        return self._exchange(q_owned, stream)
+
+    def _exchange(self, q_owned, stream):
         info = self.info
         n_send, n_halo = int(info["n_send"]), int(info["n_halo"])
         if n_send:

@@ -54,6 +54,11 @@ def _worker(rank, world, port, level, prec, results, kernel="laplace"):
         q_owned = torch.as_tensor(q[full.export("src_perm")[lo:hi]], dtype=dt, device=f"cuda:{dev}")
         full.close()
         out_sync = dp.apply(q_owned)
+        side = torch.cuda.Stream()  # an explicit stream that is not the current one
+        side.wait_stream(torch.cuda.current_stream())
+        out_side = dp.apply(q_owned, stream=side.cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(out_side, out_sync)
         comm = torch.cuda.Stream()
         ev = dp.exchange_async(q_owned, comm)
         out_async = dp.apply(q_owned, halo_ready=ev)
