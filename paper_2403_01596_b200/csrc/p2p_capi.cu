@@ -164,6 +164,7 @@ const void *tiled_fn(int tpi, int nt, bool pad, int ns) {
         if (pad) return ns == 3 ? tiled_fn_nt<float, 1, true, 3>(nt) : tiled_fn_nt<float, 1, true, 1>(nt);
         return ns == 3 ? tiled_fn_nt<float, 1, false, 3>(nt) : tiled_fn_nt<float, 1, false, 1>(nt);
     } else {
+        if (tpi == 2) return tiled_fn_nt<double, 2, false, 3>(nt);  // dense fp64, two targets per unit
         return ns == 3 ? tiled_fn_nt<double, 1, false, 3>(nt) : tiled_fn_nt<double, 1, false, 1>(nt);
     }
 }

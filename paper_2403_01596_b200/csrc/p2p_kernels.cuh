@@ -234,6 +234,30 @@ __device__ __forceinline__ double span1_f64r(const double2 *__restrict__ UV, con
     return acc;
 }
 
+// Dense fp64, two targets (a, b) of one box per source load: the guard by selection, the log
+// from the replicated 64-entry table (lt8) or the 256-entry one.
+__device__ __forceinline__ void span1x2_f64(const double2 *__restrict__ UV, const double *__restrict__ Q, int j0,
+                                            int j1, double ua, double va, double ub, double vb, double eps2,
+                                            const double2 *__restrict__ LT, int l8, int lt8, double &ra,
+                                            double &rb) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll 2
+    for (int j = j0; j < j1; ++j) {
+        const double2 s = UV[j];
+        const double qj = Q[j];
+        const double dua = ua - s.x, dva = va - s.y, dub = ub - s.x, dvb = vb - s.y;
+        const double r2a = fma(dva, dva, dua * dua), r2b = fma(dvb, dvb, dub * dub);
+        const bool oka = r2a >= eps2, okb = r2b >= eps2;
+        const double xa = oka ? r2a : 1.0, xb = okb ? r2b : 1.0;
+        const double la = lt8 ? log_tab8(xa, LT, l8) : log_tab(xa, LT);
+        const double lb = lt8 ? log_tab8(xb, LT, l8) : log_tab(xb, LT);
+        a0 = oka ? fma(qj, la, a0) : a0;
+        a1 = okb ? fma(qj, lb, a1) : a1;
+    }
+    ra = a0;
+    rb = a1;
+}
+
 // fp64 log without the shared-memory table (the TILED lean fp64 path, sparse tiles): a 32-entry
 // table held one entry per lane in registers (c_k rounded to float, L_k = -log c_k;
 // plan_builder.cpp build_log_table) and fetched with warp shuffles.  The 256-entry table's random
@@ -303,6 +327,9 @@ __device__ __forceinline__ double span1_f64(const double2 *__restrict__ UV, cons
 // mapped to j = v + (v >= b1 ? d1 : 0) + (v >= b2 ? d2 : 0): lanes whose targets
 // have equal totals (tsort plans) stay converged across row boundaries.  One
 // accumulator, sources in row order (a fixed order per target).
+#ifndef P2P_SPAN3_UNROLL
+#define P2P_SPAN3_UNROLL 2  // the sparse flattened loop (tools/gpu_ab_variants.sh: 1, 2, 4)
+#endif
 struct Runs3 {
     int v0, n, b1, d1, b2, d2;
     __device__ __forceinline__ Runs3(int s0, int e0, int s1, int e1, int s2, int e2)
@@ -313,7 +340,7 @@ __device__ __forceinline__ float span3_f32(const float2 *__restrict__ UV, const 
                                            float ut, float vt) {
     float acc = 0.f;
     const int v1 = r.v0 + r.n;
-#pragma unroll 2
+    P2P_UNROLL(P2P_SPAN3_UNROLL)
     for (int v = r.v0; v < v1; ++v) {
         const int j = r.at(v);
         const float2 s = UV[j];
@@ -856,7 +883,8 @@ __global__ void __launch_bounds__(NT, (TPI == 2 && P2P_DENSE_MINB > 0)          
                                       : (TPI == 1 && !PAD && NS == 1 && NT == 64 && P2P_LEAN_MINB > 0) ? P2P_LEAN_MINB
                                                                                                   : 0)
 p2p_tiled_kernel(const P2PArgs<T> a) {
-    static_assert(TPI == 1 || (TPI == 2 && PAD && sizeof(T) == 4), "TPI = 2 is the padded fp32 path");
+    static_assert(TPI == 1 || (TPI == 2 && PAD && sizeof(T) == 4) || (TPI == 2 && !PAD && sizeof(T) == 8 && NS == 3),
+                  "TPI = 2: the padded fp32 path, or dense fp64 (unpadded, row items)");
     static_assert(!PAD || sizeof(T) == 4, "the padded layout is fp32");
     static_assert(NS == 1 || NS == 3, "one item per unit, or one per row-run");
     constexpr bool LEAN = NS == 1 && TPI == 1 && !PAD;
@@ -998,6 +1026,10 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
             } else if constexpr (sizeof(T) == 4) {
                 res[0] = span1_f32(reinterpret_cast<const float2 *>(s_uv), reinterpret_cast<const float *>(s_q), i0,
                                    i1, tuv[2 * t0], tuv[2 * t0 + 1]);
+            } else if constexpr (TPI == 2) {  // dense fp64: two targets per source load
+                span1x2_f64(reinterpret_cast<const double2 *>(s_uv), reinterpret_cast<const double *>(s_q), i0, i1,
+                            tuv[2 * t0], tuv[2 * t0 + 1], tuv[2 * t0 + 2], tuv[2 * t0 + 3], a.eps2, s_lt, lane & 7,
+                            a.lt8, res[0], res[1]);
             } else {
                 if (a.lt8)
                     res[0] = span1_f64r(reinterpret_cast<const double2 *>(s_uv), reinterpret_cast<const double *>(s_q),

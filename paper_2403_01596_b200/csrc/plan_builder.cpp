@@ -589,6 +589,11 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     hp.max_tile_halo = st.max_tile_halo;
     hp.src_cap = d.layout == P2P_LAYOUT_REDUNDANT ? hp.max_tile_halo : pad4(hp.max_region);
     hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= 8.0 && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT) ? 2 : 1;
+    // dense fp64 TILED: two targets per unit as well (each source load serves both; P2P_TPI64=0: one)
+    if (d.precision == P2P_FP64 && d.layout == P2P_LAYOUT_TILED && hp.density_occ >= 8.0 && k <= 3) {
+        hp.tpi = 2;
+        if (const char *v = std::getenv("P2P_TPI64")) hp.tpi = std::atoi(v) == 1 ? 1 : 2;
+    }
     // TILED defaults: dense fp32 -> padded pairs, 2 targets per unit, (unit, row) items;
     // sparse or fp64 -> unpadded, one item per target; 128-thread CTAs.
     hp.pad = d.layout == P2P_LAYOUT_TILED ? (hp.tpi == 2) : true;
