@@ -400,10 +400,33 @@ def main():
 
     # N > 1, --exchange auto: both exchanges, 5 untimed-for-the-record steps each, the faster
     # (max over ranks, so every rank decides alike) is the one timed below
+    def all_ok(ok):  # every rank reaches this with its local verdict: a collective decision
+        if world == 1:
+            return ok
+        t = torch.tensor([1 if ok else 0], device="cpu" if shared else dev, dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
+    def sync_ready():
+        """Map the peers' buffers (one object all-gather, then local IPC opens) and agree on the
+        outcome before any further collective, so a rank that cannot map a peer makes every rank
+        fall back to the NCCL exchange instead of diverging."""
+        ok = True
+        try:
+            for j in jobs:
+                j["dp"].enable_sync()
+        except Exception as e:  # noqa: BLE001 -- reported in the JSON line, decided collectively
+            ok = False
+            print(f"sync exchange unavailable on rank {rank}: {e}", file=sys.stderr)
+        return all_ok(ok)
+
     autotune = None
     if world > 1 and args.exchange == "auto":
         autotune = {}
         for m in ("sync", "nccl"):
+            if m == "sync" and not sync_ready():
+                autotune[m] = None
+                continue
             g = prepare(m)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             barrier()
@@ -412,8 +435,16 @@ def main():
                 g.replay() if g is not None else step()
             e1.record(stream)
             barrier()
-            autotune[m] = max_over_ranks(e0.elapsed_time(e1) / 5)
-        chosen = min(autotune, key=autotune.get)
+            ok = True
+            if m == "sync":  # a device-side wait that gave up (20 s) disqualifies the mode everywhere
+                try:
+                    for j in jobs:
+                        j["dp"].check()
+                except Exception:  # noqa: BLE001
+                    ok = False
+            ms_m = max_over_ranks(e0.elapsed_time(e1) / 5)
+            autotune[m] = ms_m if all_ok(ok) else None
+        chosen = min((m for m in autotune if autotune[m] is not None), key=autotune.get)
     else:
         chosen = args.exchange if world > 1 else "single"
     graph = prepare(chosen)
