@@ -455,6 +455,7 @@ def main():
     sampler = ClockSampler(local)
     barrier()
     with sampler:
+        t_host = time.perf_counter()
         for k in range(args.steps):
             flush.zero_()
             ev[k][0].record(stream)
@@ -463,6 +464,7 @@ def main():
             else:
                 step(kev[k])
             ev[k][1].record(stream)
+        host_enqueue_ms = (time.perf_counter() - t_host) * 1e3 / args.steps  # CPU time to enqueue one step
         barrier()
     if mode == "sync":
         for j in jobs:
@@ -555,6 +557,9 @@ def main():
                                                               if world > 1 else ""),
                    **({"exchange": mode, "exchange_autotune_ms": autotune} if world > 1 else {})},
         "gpu_launches": args.steps * len(jobs) * {"single": 1, "sync": 4, "nccl": 3, "peer": 2}[mode],
+        # host-side cost of issuing one step (max over ranks) against the device step time: a step
+        # whose enqueue takes less than its GPU time is not host-bound (N > 1 sync: one graph launch)
+        "host_enqueue_ms_per_step": max_over_ranks(host_enqueue_ms),
         "roofline": roofline, "clocks": clocks, "e2e": e2e, "per_config": per_cfg,
     }
     if world == 1 and args.precision == "fp32" and args.kernel == "laplace" and not args.profile:
