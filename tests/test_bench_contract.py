@@ -29,3 +29,18 @@ def test_reference_arm_json_line():
               "cpu_baseline", "e2e", "config"):
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_defaults_measure_the_headline():
+    """The driver runs bench.py with no flags: the workload must be BASELINE.json configs[3] (the
+    configuration its metric is quoted on at 1/2/4/8 B200), strong scaling for N > 1, and the
+    roofline denominators must come from the committed measurement."""
+    sys.argv = ["bench.py"]
+    a = bench.parse()
+    assert a.workload == "surface_2e7" and bench.WORKLOADS[a.workload] == ["surf_2e7"]
+    assert a.scaling == "strong" and a.exchange == "auto" and a.layout == "tiled" and a.precision == "fp32"
+    peaks = json.load(open(bench.PEAKS_JSON))
+    assert 14.0 < peaks["mufu_lg2"]["per_clk_per_sm"] < 17.0 and 50.0 < peaks["dfma"]["per_clk_per_sm"] / 2 < 70.0
+    assert bench.MUFU_LG2_PER_CLK_PER_SM == peaks["mufu_lg2"]["per_clk_per_sm"]
+    assert "profiles/r02_peaks.json" in bench.PEAK_BASIS
+    assert len(bench.src_sha16()) == 16 and bench.src_sha16() == bench.src_sha16()
