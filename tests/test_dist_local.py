@@ -52,9 +52,15 @@ def _worker(rank, world, port, layout, kind, results):
         else:
             src, tgt, q = W.make_problem("d16_1e6", n=30000)
             level = 7
-        # this rank holds an interleaved share only (the global arrays below are used for checks)
-        sid = np.arange(rank, len(src), world)
-        tid = np.arange(rank, len(tgt), world)
+        # this rank holds an interleaved share only (the global arrays below are used for checks);
+        # "empty": the last rank holds no points at all (it still owns a Morton range)
+        if kind == "empty":
+            holders = world - 1
+            sid = np.arange(rank, len(src), holders) if rank < holders else np.zeros(0, dtype=np.int64)
+            tid = np.arange(rank, len(tgt), holders) if rank < holders else np.zeros(0, dtype=np.int64)
+        else:
+            sid = np.arange(rank, len(src), world)
+            tid = np.arange(rank, len(tgt), world)
         dp = DistributedP2P.from_local(src[sid], tgt[tid], sid, tid, level=level, device=-1, host_staged=True,
                                        layout=layout, precision="fp32")
         ref = p2p.Plan(src, tgt, level=level, layout=layout, precision="fp32", device=-1, part_world=world,
@@ -84,7 +90,7 @@ def _worker(rank, world, port, layout, kind, results):
 
 
 @pytest.mark.parametrize("layout", ["tiled", "nr", "r"])
-@pytest.mark.parametrize("world,kind", [(2, "iid"), (3, "iid"), (3, "disjoint")])
+@pytest.mark.parametrize("world,kind", [(2, "iid"), (3, "iid"), (3, "disjoint"), (3, "empty")])
 def test_plan_from_local_points(layout, world, kind):
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
