@@ -1000,6 +1000,9 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         gather_weights(s_idx, a.q, s_q, nent, tid, NT);  // weights through the per-entry index
         __syncthreads();
         const int npart = pinfo >> 16, ipart = pinfo & 0xffff;
+        // lean, plan order, whole tile: the slots are n9-sorted, so their outputs are scattered; stage
+        // them in shared memory and store the tile's contiguous output range coalesced instead
+        const bool stage = LEAN && a.out_idx == nullptr && npart == 1;
         int ub = 0, ue = nu;
         if (npart > 1) {  // tail tile split into npart unit ranges (nu * npart < 2^31)
             ub = (nu * ipart) / npart;
@@ -1063,6 +1066,10 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                 acc = (-0.5f * kLn2) * acc;
             } else {
                 acc = -0.5 * acc;
+            }
+            if (LEAN && stage) {  // staged in output order, stored coalesced after the tile's barrier
+                part[o] = acc;
+                return;
             }
             const int oi = a.out_idx ? a.out_idx[tb + o] : tb + o;
             a.out[oi] = a.accumulate ? a.out[oi] + acc : acc;
@@ -1142,12 +1149,18 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
         }
         __syncthreads();  // buffer `buf` and the work arrays are free; s_next / s_base_next visible
         if (trc) trc[5] = gtimer();
+        const int tb_done = tb;
         ++it;
         cur = s_next[it & 1];
         tb = s_base_next[it & 1];
         pinfo = s_part_next[it & 1];
         if (db) buf ^= 1;
         else if (tid == 0 && cur < a.ntiles) issue(cur, 0);
+        if (LEAN && stage)  // the staged results (the next writes to `part` follow the next barrier)
+            for (int i = tid; i < nslot; i += NT) {
+                T *o = a.out + tb_done + i;
+                *o = a.accumulate ? *o + part[i] : part[i];
+            }
     }
     if (tid == 0) queue_exit(a.queue);
 }

@@ -115,8 +115,9 @@ P2P_HD inline TCarve tiled_carve(int k, int src_cap, int slot_cap, int e, int tp
     const bool q_alias = e == 4 && nbuf == 1;
     c.q = q_alias ? c.idx : nbuf * c.bufsz;
     c.part = align16(q_alias ? nbuf * c.bufsz : c.q + e * src_cap);  // NS = 3: three partial sums per slot
+    // ns = 1, tpi = 1 (lean): `part` stages the tile's results in output order (coalesced stores)
     // fp64 dense (ns = 3): the log table -- kLogTab entries, or (lt8) 8 x kLogTab8; lean: none (log_shfl)
-    c.ltab = align16(c.part + (ns == 3 ? 3 * e * slot_cap : 0));
+    c.ltab = align16(c.part + (ns == 3 ? 3 * e * slot_cap : tpi == 1 ? e * slot_cap : 0));
     c.bar = align16(c.ltab + (e == 8 && ns == 3 ? 16 * (lt8 ? 8 * kLogTab8 : kLogTab) : 0));
     c.total = c.bar + 16;
     return c;
