@@ -9,9 +9,11 @@ T=${TAG:-r02}
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; tail -2 gpurun_out/${T}_smoke.log
 timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/${T}_gpu_tests.log 2>&1; tail -2 gpurun_out/${T}_gpu_tests.log
 timeout 900 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; tail -c 300 gpurun_out/${T}_bench.json
-for WL in lowdensity_1e7 density_1e6 d32_7e7; do
+for WL in lowdensity_1e7 density_1e6; do
   timeout 900 python bench.py --workload $WL --steps 10 --no-extras > gpurun_out/${T}_bench_$WL.json 2> gpurun_out/${T}_bench_$WL.err
 done
+# configs[4]: "redundant vs non-redundant layout" -- the extras carry NR / R / TILED x fp32 / fp64
+timeout 1800 python bench.py --workload d32_7e7 --steps 10 > gpurun_out/${T}_bench_d32_7e7.json 2> gpurun_out/${T}_bench_d32_7e7.err
 for WL in helmholtz_1e6 cube3d_1e6 cube3d_helmholtz contour_2e5; do
   timeout 600 python bench.py --workload $WL --steps 10 > gpurun_out/${T}_bench_$WL.json 2> gpurun_out/${T}_bench_$WL.err
 done
