@@ -454,18 +454,20 @@ def main():
            for _ in range(args.steps)]
     sampler = ClockSampler(local)
     barrier()
+    host_ms = []
     with sampler:
-        t_host = time.perf_counter()
         for k in range(args.steps):
             flush.zero_()
             ev[k][0].record(stream)
+            t_host = time.perf_counter()
             if graph is not None:
                 graph.replay()
             else:
                 step(kev[k])
+            host_ms.append((time.perf_counter() - t_host) * 1e3)  # CPU time to enqueue the step's work
             ev[k][1].record(stream)
-        host_enqueue_ms = (time.perf_counter() - t_host) * 1e3 / args.steps  # CPU time to enqueue one step
         barrier()
+    host_enqueue_ms = float(np.median(host_ms))
     if mode == "sync":
         for j in jobs:
             j["dp"].check()
@@ -557,8 +559,9 @@ def main():
                                                               if world > 1 else ""),
                    **({"exchange": mode, "exchange_autotune_ms": autotune} if world > 1 else {})},
         "gpu_launches": args.steps * len(jobs) * {"single": 1, "sync": 4, "nccl": 3, "peer": 2}[mode],
-        # host-side cost of issuing one step (max over ranks) against the device step time: a step
-        # whose enqueue takes less than its GPU time is not host-bound (N > 1 sync: one graph launch)
+        # host-side cost of issuing one step's apply work (median over steps, max over ranks) against
+        # the device step time: an enqueue shorter than the GPU step is not host-bound (N > 1 sync:
+        # one graph launch); the L2-flush memset outside it can block on queue backpressure
         "host_enqueue_ms_per_step": max_over_ranks(host_enqueue_ms),
         "roofline": roofline, "clocks": clocks, "e2e": e2e, "per_config": per_cfg,
     }
