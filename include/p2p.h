@@ -28,7 +28,12 @@
  *  - Plan order ("P2P_ORDER_PLAN") is the Morton order of the leaf boxes, and
  *    within a box the original index order (stable sort; "in the
  *    order of the boxes' morton index").  It is the fast path: no permutation.
- *  - One apply may be in flight per plan at a time (the plan owns workspace).
+ *  - One apply may be in flight per plan at a time (the plan owns workspace), unless the plan
+ *    was given more workspace slots (p2p_plan_set_workspaces).
+ *  - Multi-GPU (part_world > 1): plans from the global point set (p2p_plan_create) or from each
+ *    rank's own points (p2p_box_counts / p2p_partition_route / p2p_plan_create_local); the halo
+ *    exchange by the caller's collective (p2p_halo_pack + p2p_apply_dist*) or by the library's
+ *    device-synchronised peer-memory kernels (p2p_peer_* / p2p_apply_peer_sync / p2p_gather).
  *  - There is no CPU fallback: a plan created with device < 0 is host-only
  *    (plan building, introspection and export work; apply returns
  *    P2P_ERROR_NO_DEVICE).
