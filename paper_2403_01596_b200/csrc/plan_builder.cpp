@@ -588,7 +588,12 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     hp.max_region = st.max_region_pad;
     hp.max_tile_halo = st.max_tile_halo;
     hp.src_cap = d.layout == P2P_LAYOUT_REDUNDANT ? hp.max_tile_halo : pad4(hp.max_region);
-    hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= 8.0 && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT) ? 2 : 1;
+    // fp32 two-target units: from 8 points per occupied box (NR), from 3 (TILED: measured against the
+    // lean path on 1e7-point plates, tools/gpu_dense_threshold.sh: D_occ 2.3 lean 191 / dense 207 us,
+    // 3.2 dense 203 / items 219, 4.1 dense 215 / lean 273, 6.0 dense 229 / items 336)
+    const double dense_from = d.layout == P2P_LAYOUT_TILED ? 3.0 : 8.0;
+    hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= dense_from && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT)
+                 ? 2 : 1;
     // dense fp64 TILED: two targets per unit as well (each source load serves both; P2P_TPI64=0: one)
     if (d.precision == P2P_FP64 && d.layout == P2P_LAYOUT_TILED && hp.density_occ >= 8.0 && k <= 3) {
         hp.tpi = 2;
@@ -605,6 +610,9 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     // 256 for dense fp64, 64 (or 32, below) for sparse fp32
     hp.nt = d.layout == P2P_LAYOUT_TILED
                 ? (dense64 ? 256 : hp.tpi > 1 || d.precision == P2P_FP64 ? 128 : 64) : kThreads;
+    // dense fp32 TILED below 5 points per occupied box: 64-thread CTAs (same sweep: D_occ 3.2 64 203 /
+    // 128 227 us, 4.1 215 / 217; 6.0 272 / 229)
+    if (d.layout == P2P_LAYOUT_TILED && d.precision == P2P_FP32 && hp.tpi > 1 && hp.density_occ < 5.0) hp.nt = 64;
     // tuning hooks (experiments only): P2P_TPI, P2P_NS, P2P_NBUF, P2P_PAD, P2P_NT
     if (const char *v = std::getenv("P2P_TPI"))
         if (d.precision == P2P_FP32 && d.layout != P2P_LAYOUT_REDUNDANT) {

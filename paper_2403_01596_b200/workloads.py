@@ -150,6 +150,10 @@ CONFIGS: dict[str, PlateConfig | ContourConfig] = {
         # NEXT-3 (Helmholtz): a 1e6-point plate at 4 points per leaf box (leaf = a quarter
         # wavelength at the helmholtz workload's kappa: ~8 samples per wavelength along x and y)
         PlateConfig("d4_1e6", 500, 500, 10, 1_000_000),
+        # kernel-choice sweeps between the low-density and the density configs (not BASELINE
+        # workloads): 1e7 points at 3 and 6 points per leaf box
+        PlateConfig("lowd3_1e7", 2000, 1667, 12, 10_000_000),
+        PlateConfig("lowd6_1e7", 1291, 1291, 12, 10_000_000),
     ]
 }
 # NEXT-4 curve clouds: Laplace at ~12 points per occupied leaf box (t = 43); Helmholtz with the
