@@ -234,28 +234,34 @@ __device__ __forceinline__ double span1_f64r(const double2 *__restrict__ UV, con
     return acc;
 }
 
-// Dense fp64, two targets (a, b) of one box per source load: the guard by selection, the log
-// from the replicated 64-entry table (lt8) or the 256-entry one.
+// Dense fp64, two targets (a, b) of one box per source load, the log from the replicated 64-entry
+// table (lt8) or the 256-entry one.  The eps guard is off the loop: each target keeps the minimum
+// high word of its r^2 (one integer min per pair; high words of non-negative doubles order like
+// the values), and a target whose minimum does not exceed the high word of eps^2 -- a superset of
+// the targets with a pair closer than eps -- returns NaN, so finish() recomputes it with the
+// explicit guard (same logs, same order: the results equal the guarded loop's).
 __device__ __forceinline__ void span1x2_f64(const double2 *__restrict__ UV, const double *__restrict__ Q, int j0,
                                             int j1, double ua, double va, double ub, double vb, double eps2,
                                             const double2 *__restrict__ LT, int l8, int lt8, double &ra,
                                             double &rb) {
     double a0 = 0.0, a1 = 0.0;
+    int ma = 0x7fffffff, mb = 0x7fffffff;
 #pragma unroll 2
     for (int j = j0; j < j1; ++j) {
         const double2 s = UV[j];
         const double qj = Q[j];
         const double dua = ua - s.x, dva = va - s.y, dub = ub - s.x, dvb = vb - s.y;
         const double r2a = fma(dva, dva, dua * dua), r2b = fma(dvb, dvb, dub * dub);
-        const bool oka = r2a >= eps2, okb = r2b >= eps2;
-        const double xa = oka ? r2a : 1.0, xb = okb ? r2b : 1.0;
-        const double la = lt8 ? log_tab8(xa, LT, l8) : log_tab(xa, LT);
-        const double lb = lt8 ? log_tab8(xb, LT, l8) : log_tab(xb, LT);
-        a0 = oka ? fma(qj, la, a0) : a0;
-        a1 = okb ? fma(qj, lb, a1) : a1;
+        ma = min(ma, __double2hiint(r2a));
+        mb = min(mb, __double2hiint(r2b));
+        const double la = lt8 ? log_tab8(r2a, LT, l8) : log_tab(r2a, LT);
+        const double lb = lt8 ? log_tab8(r2b, LT, l8) : log_tab(r2b, LT);
+        a0 = fma(qj, la, a0);
+        a1 = fma(qj, lb, a1);
     }
-    ra = a0;
-    rb = a1;
+    const int he = __double2hiint(eps2);
+    ra = ma <= he ? __longlong_as_double(0x7ff8000000000000LL) : a0;
+    rb = mb <= he ? __longlong_as_double(0x7ff8000000000000LL) : a1;
 }
 
 // fp64 log without the shared-memory table (the TILED lean fp64 path, sparse tiles): a 32-entry
@@ -1065,6 +1071,19 @@ p2p_tiled_kernel(const P2PArgs<T> a) {
                 }
                 acc = (-0.5f * kLn2) * acc;
             } else {
+                if (TPI == 2 && !isfinite(acc)) {  // dense fp64: a pair flagged closer than eps (span1x2_f64)
+                    const int jb = tbl[t];
+                    acc = 0.0;
+                    for (int row = 0; row < 3; ++row) {
+                        const int j0 = jb + row * R;
+                        const double2 *UV = reinterpret_cast<const double2 *>(s_uv);
+                        const double *Qd = reinterpret_cast<const double *>(s_q);
+                        acc += a.lt8 ? span1_f64r(UV, Qd, table[j0], table[j0 + 3], tuv[2 * t], tuv[2 * t + 1], a.eps2,
+                                                  s_lt, lane & 7)
+                                     : span1_f64(UV, Qd, table[j0], table[j0 + 3], tuv[2 * t], tuv[2 * t + 1], a.eps2,
+                                                 s_lt);
+                    }
+                }
                 acc = -0.5 * acc;
             }
             if (LEAN && stage) {  // staged in output order, stored coalesced after the tile's barrier
