@@ -322,3 +322,20 @@ def test_heavy_tiles_are_split():
         e += np_
     assert n_split > 0
     pl.close()
+
+
+@pytest.mark.parametrize("density,tpi,items,nt", [(2, 1, 1, None), (4, 2, 3, 64), (6, 2, 3, 128), (16, 2, 3, 128)])
+def test_tiled_fp32_kernel_choice(density, tpi, items, nt):
+    """TILED fp32 kernel choice by occupied-box density (measured on 1e7-point
+    plates): the lean one-target path below 3 points per occupied box, the 2-target dense path
+    from 3 (64-thread CTAs below 5 points per box, 128 above)."""
+    cfg = W.PlateConfig("kc", 64, 64, 8, 64 * 64 * density, seed=11)
+    src, tgt, _ = W.make_problem(cfg)
+    pl = _plan(src, tgt, level=cfg.level, layout="tiled", precision="fp32")
+    i = pl.info
+    assert (i["slots_per_unit"], i["items_per_unit"]) == (tpi, items), (density, i["density_occupied"])
+    if nt is not None:
+        assert i["cta_threads"] == nt
+    else:
+        assert i["flags"] & 1 and i["cta_threads"] in (32, 64)  # n9-ordered lean slots
+    pl.close()
