@@ -591,11 +591,14 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     // fp32 two-target units: from 8 points per occupied box (NR), from 3 (TILED: measured against the
     // lean path on 1e7-point plates, tools/gpu_dense_threshold.sh: D_occ 2.3 lean 191 / dense 207 us,
     // 3.2 dense 203 / items 219, 4.1 dense 215 / lean 273, 6.0 dense 229 / items 336)
-    const double dense_from = d.layout == P2P_LAYOUT_TILED ? 3.0 : 8.0;
+    // fp64 TILED two-target units with (unit, row) items from 4 points per occupied box (same plates,
+    // tools/gpu_f64_ab.sh: D_occ 3.2 lean 714 / dense 790 us, 4.1 847 / 769, 6.0 1225 / 920)
+    double dense_from = d.layout == P2P_LAYOUT_TILED ? 3.0 : 8.0, dense64_from = d.layout == P2P_LAYOUT_TILED ? 4.0 : 8.0;
+    if (const char *v = std::getenv("P2P_DENSE_FROM")) dense_from = dense64_from = std::atof(v);  // tuning hook
     hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= dense_from && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT)
                  ? 2 : 1;
     // dense fp64 TILED: two targets per unit as well (each source load serves both; P2P_TPI64=0: one)
-    if (d.precision == P2P_FP64 && d.layout == P2P_LAYOUT_TILED && hp.density_occ >= 8.0 && k <= 3) {
+    if (d.precision == P2P_FP64 && d.layout == P2P_LAYOUT_TILED && hp.density_occ >= dense64_from && k <= 3) {
         hp.tpi = 2;
         if (const char *v = std::getenv("P2P_TPI64")) hp.tpi = std::atoi(v) == 1 ? 1 : 2;
     }
@@ -603,7 +606,7 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     // sparse or fp64 -> unpadded, one item per target; 128-thread CTAs.
     hp.pad = d.layout == P2P_LAYOUT_TILED ? (hp.tpi == 2) : true;
     // fp64 dense boxes: (target, row-run) items too (sorted), 256-thread CTAs (tools/gpu_ab11.sh)
-    const bool dense64 = d.precision == P2P_FP64 && hp.density_occ >= 8.0;
+    const bool dense64 = d.precision == P2P_FP64 && hp.density_occ >= dense64_from;
     hp.ns = hp.tpi > 1 || dense64 ? 3 : 1;
     hp.nbuf = 1;
     // measured best (tools/gpu_ab*.sh): 128 threads for dense fp32 units and sparse fp64,

@@ -339,3 +339,15 @@ def test_tiled_fp32_kernel_choice(density, tpi, items, nt):
     else:
         assert i["flags"] & 1 and i["cta_threads"] in (32, 64)  # n9-ordered lean slots
     pl.close()
+
+
+@pytest.mark.parametrize("density,tpi,items,nt", [(2, 1, 1, 128), (4, 2, 3, 256), (16, 2, 3, 256)])
+def test_tiled_fp64_kernel_choice(density, tpi, items, nt):
+    """TILED fp64: the lean path (flattened runs, register-table log) below 4 points per occupied
+    box, 2-target units with (unit, row) items and 256-thread CTAs from 4."""
+    cfg = W.PlateConfig("kc", 64, 64, 8, 64 * 64 * density, seed=11)
+    src, tgt, _ = W.make_problem(cfg)
+    pl = _plan(src, tgt, level=cfg.level, layout="tiled", precision="fp64")
+    i = pl.info
+    assert (i["slots_per_unit"], i["items_per_unit"], i["cta_threads"]) == (tpi, items, nt), i["density_occupied"]
+    pl.close()
