@@ -66,10 +66,12 @@ def gate(got, ref, bound, prec, first_planted):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
-@pytest.mark.parametrize("layout", ["nr", "r", "tiled", "tiled_sparse"])
+@pytest.mark.parametrize("layout", ["nr", "r", "tiled", "tiled_mid", "tiled_sparse"])
 def test_guard_straddle_laplace2d(layout, prec):
     src, tgt, q, k = problem(2, prec)
-    level = 7 if layout == "tiled_sparse" else 4  # ~0.25 per box: the TILED lean (flattened) path
+    # ~0.25 per box: the TILED lean (flattened) path; ~4 per box: the 2-target dense paths from
+    # 3 (fp32) / 4 (fp64) points per occupied box
+    level = {"tiled_sparse": 7, "tiled_mid": 5}.get(layout, 4)
     with p2p.Plan(src, tgt, level=level, layout=layout.split("_")[0], precision=prec) as pl:
         got = run(pl, q)
     ref, _ = oracle.direct(src, q, tgt, level)
