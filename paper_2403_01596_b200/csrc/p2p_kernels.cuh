@@ -334,7 +334,7 @@ __device__ __forceinline__ double span1_f64(const double2 *__restrict__ UV, cons
 // have equal totals (tsort plans) stay converged across row boundaries.  One
 // accumulator, sources in row order (a fixed order per target).
 #ifndef P2P_SPAN3_UNROLL
-#define P2P_SPAN3_UNROLL 2  // the sparse flattened loop (tools/gpu_ab_variants.sh: 1, 2, 4)
+#define P2P_SPAN3_UNROLL 2  // the sparse flattened loop (tools/gpu/gpu_ab_variants.sh: 1, 2, 4)
 #endif
 struct Runs3 {
     int v0, n, b1, d1, b2, d2;

@@ -147,7 +147,7 @@ struct Error : std::runtime_error {
 constexpr int kMaxLevel = 15;          // full-grid CSR offsets: 4^(L-1) <= 2^28 boxes
 constexpr int kMaxLevel3 = 9;          // 3D: 8^(L-1) <= 2^24 boxes
 // 3D: threads per CTA (one target box per CTA): 64 for Laplace, 128 for Helmholtz (measured,
-// tools/gpu_ab16.sh)
+// tools/gpu/gpu_ab16.sh)
 inline int box3d_threads(int kernel) { return kernel == P2P_KERNEL_HELMHOLTZ_3D ? 128 : 64; }
 P2P_HD inline int kernel_dim(int kernel) { return kernel >= P2P_KERNEL_LAPLACE_3D ? 3 : 2; }
 // 3D box kernel shared memory: staged sources (x, y, z, q_re) and q_im (complex), per-thread

@@ -385,7 +385,7 @@ void build_host_plan_adaptive(const p2p_plan_desc &d, HostPlan &hp) {
     const int e = d.precision == P2P_FP32 ? 4 : 8;
     hp.smem_bytes = adaptive_smem(hp.src_cap, e);
     // fp32 leaves of <= 32 targets: one warp per leaf, 4 warps per CTA (measured: +38 % at CT = 16,
-    // +12 % at CT = 32; slower for larger leaves and for fp64, tools/gpu_ab20.sh); P2P_ADAPTIVE_WARP=0: off
+    // +12 % at CT = 32; slower for larger leaves and for fp64, tools/gpu/gpu_ab20.sh); P2P_ADAPTIVE_WARP=0: off
     hp.warp_leaf = e == 4 && hp.tgt_cap <= 32;
     if (const char *v = std::getenv("P2P_ADAPTIVE_WARP")) hp.warp_leaf = hp.warp_leaf && std::atoi(v) != 0;
     if (hp.warp_leaf) {
@@ -589,10 +589,10 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     hp.max_tile_halo = st.max_tile_halo;
     hp.src_cap = d.layout == P2P_LAYOUT_REDUNDANT ? hp.max_tile_halo : pad4(hp.max_region);
     // fp32 two-target units: from 8 points per occupied box (NR), from 3 (TILED: measured against the
-    // lean path on 1e7-point plates, tools/gpu_dense_threshold.sh: D_occ 2.3 lean 191 / dense 207 us,
+    // lean path on 1e7-point plates, tools/gpu/gpu_dense_threshold.sh: D_occ 2.3 lean 191 / dense 207 us,
     // 3.2 dense 203 / items 219, 4.1 dense 215 / lean 273, 6.0 dense 229 / items 336)
     // fp64 TILED two-target units with (unit, row) items from 4 points per occupied box (same plates,
-    // tools/gpu_f64_ab.sh: D_occ 3.2 lean 714 / dense 790 us, 4.1 847 / 769, 6.0 1225 / 920)
+    // tools/gpu/gpu_f64_ab.sh: D_occ 3.2 lean 714 / dense 790 us, 4.1 847 / 769, 6.0 1225 / 920)
     double dense_from = d.layout == P2P_LAYOUT_TILED ? 3.0 : 8.0, dense64_from = d.layout == P2P_LAYOUT_TILED ? 4.0 : 8.0;
     if (const char *v = std::getenv("P2P_DENSE_FROM")) dense_from = dense64_from = std::atof(v);  // tuning hook
     hp.tpi = (d.precision == P2P_FP32 && hp.density_occ >= dense_from && k <= 3 && d.layout != P2P_LAYOUT_REDUNDANT)
@@ -605,11 +605,11 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     // TILED defaults: dense fp32 -> padded pairs, 2 targets per unit, (unit, row) items;
     // sparse or fp64 -> unpadded, one item per target; 128-thread CTAs.
     hp.pad = d.layout == P2P_LAYOUT_TILED ? (hp.tpi == 2) : true;
-    // fp64 dense boxes: (target, row-run) items too (sorted), 256-thread CTAs (tools/gpu_ab11.sh)
+    // fp64 dense boxes: (target, row-run) items too (sorted), 256-thread CTAs (tools/gpu/gpu_ab11.sh)
     const bool dense64 = d.precision == P2P_FP64 && hp.density_occ >= dense64_from;
     hp.ns = hp.tpi > 1 || dense64 ? 3 : 1;
     hp.nbuf = 1;
-    // measured best (tools/gpu_ab*.sh): 128 threads for dense fp32 units and sparse fp64,
+    // measured best (tools/gpu/gpu_ab*.sh): 128 threads for dense fp32 units and sparse fp64,
     // 256 for dense fp64, 64 (or 32, below) for sparse fp32
     hp.nt = d.layout == P2P_LAYOUT_TILED
                 ? (dense64 ? 256 : hp.tpi > 1 || d.precision == P2P_FP64 ? 128 : 64) : kThreads;
@@ -638,7 +638,7 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     hp.lean = d.layout == P2P_LAYOUT_TILED && hp.tpi == 1 && hp.ns == 1 && !hp.pad;
     hp.tsort = hp.lean;
     if (hp.nt == 32 && !hp.lean) hp.nt = 64;  // one-warp CTAs: lean instances only
-    // lean fp32: ~4 targets per thread measured best (tools/gpu_prof5.sh): one-warp CTAs for small tiles
+    // lean fp32: ~4 targets per thread measured best (tools/gpu/gpu_prof5.sh): one-warp CTAs for small tiles
     if (hp.lean && d.precision == P2P_FP32 && !std::getenv("P2P_NT") &&
         (double)hp.n_tgt / (double)std::max<int64_t>(st.ntiles, 1) < 192.0)
         hp.nt = 32;
@@ -648,7 +648,7 @@ int64_t choose_tile_params(const p2p_plan_desc &d, HostPlan &hp, int k, const Ti
     // row loops (P2P_FLAT overrides)
     // dense fp64: the conflict-free replicated log table (one more DP op per pair, no bank
     // conflicts) pays below ~24 sources per box; denser boxes keep the 256-entry table (measured,
-    // tools/gpu_f64_ab2.sh: surf_2e7 / d16 -3..-4 %, d32 / d64 +5..+10 % with it)
+    // tools/gpu/gpu_f64_ab2.sh: surf_2e7 / d16 -3..-4 %, d32 / d64 +5..+10 % with it)
     hp.lt8 = d.layout == P2P_LAYOUT_TILED && dense64 && hp.density_occ < 24.0;
     if (const char *v = std::getenv("P2P_LT8")) hp.lt8 = d.layout == P2P_LAYOUT_TILED && dense64 && std::atoi(v) != 0;
     hp.flat = hp.lean && (hp.density_occ < 3.0 || d.precision == P2P_FP64);
@@ -1358,7 +1358,7 @@ void build_host_plan(const p2p_plan_desc &d, HostPlan &hp, const LocalInput *li)
     {
         const int64_t ws = (hp.n_src_local + hp.n_tgt_local) * 3 * (int64_t)e + 8 * hp.boxes_in_tiles +
                            (hp.halo_entries + hp.reg_entries) * 3 * (int64_t)e;
-        hp.lpt = ws < (int64_t)100 << 20;  // L2 = 126 MB; measured (tools/gpu_ab12.sh)
+        hp.lpt = ws < (int64_t)100 << 20;  // L2 = 126 MB; measured (tools/gpu/gpu_ab12.sh)
         if (const char *v = std::getenv("P2P_LPT")) hp.lpt = std::atoi(v) != 0;  // tuning hook
         if (hp.lpt) {
             const int64_t base = hp.part_tile[r];

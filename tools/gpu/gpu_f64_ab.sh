@@ -3,7 +3,7 @@
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 TAG=${TAG:-f64ab}
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_guard_straddle.py -m gpu -q -x -k "fp64" > gpurun_out/${TAG}_tests.log 2>&1; tail -1 gpurun_out/${TAG}_tests.log
-VARIANTS="cur ng0" WORKLOADS="lowdensity_1e7" EXTRA="--precision fp64" bash tools/gpu_ab_variants.sh
+VARIANTS="cur ng0" WORKLOADS="lowdensity_1e7" EXTRA="--precision fp64" bash tools/gpu/gpu_ab_variants.sh
 for df in 99 2; do
   P2P_DENSE_FROM=$df timeout 900 python bench.py --workload lowdensity_1e7 --configs lowd2_1e7,lowd3_1e7,lowd4_1e7,lowd6_1e7 \
     --precision fp64 --steps 5 --no-extras --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_df.json 2>/dev/null

@@ -5,6 +5,6 @@
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 T=${TAG:-r02g}
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; tail -1 gpurun_out/${T}_smoke.log
-TAG=$T bash tools/gpu_traffic_r02.sh
+TAG=$T bash tools/gpu/gpu_traffic_r02.sh
 timeout 900 python bench.py --workload lowdensity_1e7 --precision fp64 --steps 5 --no-extras --no-cpu-baseline \
    > gpurun_out/${T}_bench_lowdensity_fp64.json 2>/dev/null; tail -c 300 gpurun_out/${T}_bench_lowdensity_fp64.json
