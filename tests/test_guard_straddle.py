@@ -27,24 +27,24 @@ TOL = {"fp32": 1e-5, "fp64": 1e-12}
 TOL_EL = {"fp32": 2e-5, "fp64": 1e-12}
 
 
-def planted(dim, prec, corner=0.5):
+def planted(dim, prec, corner=0.5, d_ctl=None, d_tgt=None):
     """(targets, sources, weights) to append: two targets at/near a box corner, a guarded
     source next to each, one control source.  3D fp32: the second target 1e-3 from the corner
     and the control 1e-2 away -- 1/r magnifies the rounding of fp32 coordinates (relative
     error ~ ulp(h) / r), so closer non-guarded pairs are beyond fp32's 1e-5 gate."""
     c = np.full(dim, corner)
     e0 = np.eye(dim)[0]
-    d_t = 1e-3 if (dim == 3 and prec == "fp32") else 1e-6
-    d_c = 4e-12 if prec == "fp64" else (1e-2 if dim == 3 else 3e-5)
+    d_t = d_tgt or (1e-3 if (dim == 3 and prec == "fp32") else 1e-6)
+    d_c = d_ctl or (4e-12 if prec == "fp64" else (1e-2 if dim == 3 else 3e-5))
     t = np.stack([c, c + d_t])
     guard = np.stack([c + 5e-13 * np.ones(dim) / np.sqrt(dim), c + d_t + 5e-13 * e0])
     ctl = (c + d_t + np.eye(dim)[1] * d_c)[None]
     return t, np.concatenate([guard, ctl]), np.array([1.0, -1.0, 0.75])
 
 
-def problem(dim, prec):
+def problem(dim, prec, d_ctl=None, d_tgt=None):
     s, t, q = W.make_problem("tiny3d" if dim == 3 else "tiny")
-    pt, ps, pq = planted(dim, prec)
+    pt, ps, pq = planted(dim, prec, d_ctl=d_ctl, d_tgt=d_tgt)
     return np.concatenate([s, ps]), np.concatenate([t, pt]), np.concatenate([q, pq]), len(t)
 
 
@@ -68,10 +68,16 @@ def gate(got, ref, bound, prec, first_planted):
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
 @pytest.mark.parametrize("layout", ["nr", "r", "tiled", "tiled_mid", "tiled_sparse"])
 def test_guard_straddle_laplace2d(layout, prec):
-    src, tgt, q, k = problem(2, prec)
     # ~0.25 per box: the TILED lean (flattened) path; ~4 per box: the 2-target dense paths from
-    # 3 (fp32) / 4 (fp64) points per occupied box
+    # 3 (fp32) / 4 (fp64) points per occupied box.  fp32 at ~4 per box: the second target 1e-4
+    # from the corner and the control 3e-4 away -- the planted targets' element bound (sum |q|
+    # ln(1/r) ~ 60) is a third of level 4's, and the counted pairs 1e-6 apart carry the rounding
+    # of fp32 coordinates >= h (~7e-9) relative to r: 2.7e-5 of that bound, reproduced exactly by
+    # a numpy fp32 replay of the same coordinates (R12 / R17); the guarded pairs stay
+    # 5e-13 apart
     level = {"tiled_sparse": 7, "tiled_mid": 5}.get(layout, 4)
+    mid32 = layout == "tiled_mid" and prec == "fp32"
+    src, tgt, q, k = problem(2, prec, d_ctl=3e-4 if mid32 else None, d_tgt=1e-4 if mid32 else None)
     with p2p.Plan(src, tgt, level=level, layout=layout.split("_")[0], precision=prec) as pl:
         got = run(pl, q)
     ref, _ = oracle.direct(src, q, tgt, level)
